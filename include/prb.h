@@ -1,0 +1,263 @@
+/*
+ * prb.h -- C ABI of the B200-native pod hot path (podracer-b200).
+ *
+ * The reference (ElegantRL-podracer restated as header-only C++20 under
+ * /root/reference/proj/include/podracer) has no C ABI; its "operator API" is
+ * a set of value-semantic C++ functions that throw.  Each
+ * prb_* entry point below replaces one of them; the comment on each names the
+ * reference interface (file:line) it stands in for.  include/podracer_b200/
+ * podracer_b200.hpp re-exposes these with the reference's C++ signatures.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `d_` pointers are device (cuda:N)
+ *     pointers; everything else is host memory.  Device work is issued on
+ *     the context's stream; functions that return host data synchronise it.
+ *   - Every function returns an int status: 0 = PRB_OK, otherwise the
+ *     PRB_ERR_* code of the reference exception class it mirrors
+ *     (common.hpp:19-71).  prb_last_error() gives the message (thread-local).
+ *   - Validation happens before any state changes, as in the reference
+ *     (e.g. adam_step nn.hpp:162-171).
+ *   - Reals on the device are fp32 except the stock portfolio accounting
+ *     (balance, rewards before storage, episode returns), which is fp64 so
+ *     integer share decisions stay bit-exact.
+ */
+#ifndef PRB_H_
+#define PRB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRB_API __attribute__((visibility("default")))
+
+/* Status codes == reference exception classes (common.hpp:19-71). */
+#define PRB_OK 0
+#define PRB_ERR_DIMENSION 1  /* DimensionError  common.hpp:20 */
+#define PRB_ERR_NUMERIC 2    /* NumericError    common.hpp:26 */
+#define PRB_ERR_USAGE 3      /* UsageError      common.hpp:32 */
+#define PRB_ERR_FORMAT 4     /* FormatError     common.hpp:38 */
+#define PRB_ERR_DATA 5       /* DataError       common.hpp:44 */
+#define PRB_ERR_CONFIG 6     /* ConfigError     common.hpp:50 */
+#define PRB_ERR_CORRUPTION 7 /* CorruptionError common.hpp:56 */
+#define PRB_ERR_VERSION 8    /* VersionError    common.hpp:62 */
+#define PRB_ERR_DOMAIN 9     /* DomainError     common.hpp:69 */
+#define PRB_ERR_CUDA 10      /* device / driver failure (no reference analogue) */
+
+PRB_API const char* prb_last_error(void);
+PRB_API int prb_version(void);
+
+/* ---- seeds: common.hpp:79-105 ------------------------------------------ */
+PRB_API uint64_t prb_splitmix64(uint64_t x);                                   /* common.hpp:79 */
+PRB_API uint64_t prb_derive_seed(uint64_t base, const uint64_t* tags, int n);  /* common.hpp:88 */
+
+/* ---- context: one device + one stream (the reference's worker thread) ---- */
+typedef struct prb_ctx_s* prb_ctx;
+PRB_API int prb_ctx_create(int device, prb_ctx* out);
+PRB_API int prb_ctx_destroy(prb_ctx ctx);
+PRB_API int prb_ctx_synchronize(prb_ctx ctx);
+PRB_API void* prb_ctx_stream(prb_ctx ctx); /* cudaStream_t */
+PRB_API int prb_device_alloc(prb_ctx ctx, size_t bytes, void** d_out);
+PRB_API int prb_device_free(prb_ctx ctx, void* d_ptr);
+PRB_API int prb_memcpy_h2d(prb_ctx ctx, void* d_dst, const void* src, size_t bytes); /* synchronous */
+PRB_API int prb_memcpy_d2h(prb_ctx ctx, void* dst, const void* d_src, size_t bytes); /* synchronous */
+PRB_API int prb_memcpy_h2d_async(prb_ctx ctx, void* d_dst, const void* src, size_t bytes);
+PRB_API int prb_memcpy_d2h_async(prb_ctx ctx, void* dst, const void* d_src, size_t bytes);
+
+/* ---- market data (market.hpp) ------------------------------------------ */
+/* Synthetic OHLCV of BASELINE.md §3: mt19937_64(seed); p0 ~ U(10,200);
+ * p_{t+1} = p_t * exp(1e-3 N(0,1)); open=close, high=1.001p, low=0.999p,
+ * volume=1000.  Arrays are [K][T]; any output may be NULL. */
+PRB_API int prb_market_synthetic(uint64_t seed, int K, size_t T, double* open, double* high, double* low,
+                                 double* close, double* volume);
+/* compute_indicators market.hpp:373-392 (MACD, RSI-14, CCI-30, SMA-20);
+ * out[(i*K + k)*T + t].  DataError when T < 35. */
+PRB_API int prb_compute_indicators(const double* high, const double* low, const double* close, size_t T, int K,
+                                   double* out);
+
+typedef struct prb_market_s* prb_market;
+/* MarketData (market.hpp:104-131) after compute_indicators: close [K][T],
+ * indicators [4][K][T] (kIndicatorNames order, market.hpp:101). */
+PRB_API int prb_market_create(prb_ctx ctx, const double* close, const double* indicators, size_t T, int K,
+                              prb_market* out);
+PRB_API int prb_market_destroy(prb_market m);
+
+/* ---- vectorised environments (env.hpp:167-249) ------------------------- */
+typedef struct {
+  double initial_capital;  /* StockConfig stock_env.hpp:15-19 */
+  double max_trade_shares;
+  double cost_rate;
+} prb_stock_config;
+
+typedef struct {
+  size_t state_dim, action_dim, max_episode_steps; /* EnvSpec env.hpp:16-34 */
+  double reward_target;
+  const double* action_low;  /* action_dim entries, owned by the env */
+  const double* action_high;
+} prb_env_spec;
+
+typedef struct prb_vecenv_s* prb_vecenv;
+/* VectorizedEnvironment(factory -> StockTradingEnv(data, cfg, start, end), N)
+ * env.hpp:169 + stock_env.hpp:137-154 (validation: UsageError without
+ * indicators, ConfigError on a bad window, ConfigError on N == 0). */
+PRB_API int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t start, size_t end,
+                                    size_t num_envs, prb_vecenv* out);
+/* VectorizedEnvironment(factory -> PointMass2D, N) env.hpp:111-146. */
+PRB_API int prb_vecenv_create_pointmass(prb_ctx ctx, size_t num_envs, prb_vecenv* out);
+PRB_API int prb_vecenv_destroy(prb_vecenv env);
+PRB_API int prb_vecenv_spec(prb_vecenv env, prb_env_spec* out);   /* spec() env.hpp:181 */
+PRB_API size_t prb_vecenv_num_envs(prb_vecenv env);                /* num_envs() env.hpp:180 */
+PRB_API const float* prb_vecenv_states_device(prb_vecenv env);     /* states() env.hpp:182, [N][S] fp32 */
+/* reset(seed) env.hpp:186-194.  Per-env streams derive_seed(seed, kVecEnv, i)
+ * (mt19937_64, bit-exact with the reference).  d_obs (nullable) receives [N][S]. */
+PRB_API int prb_vecenv_reset(prb_vecenv env, uint64_t seed, float* d_obs);
+/* step(actions) env.hpp:200-236 on device buffers.  d_actions [N][A] fp32
+ * (unclipped; clipped to the spec bounds inside).  Outputs (each nullable):
+ * d_reward [N], d_done [N], and for rows that ended an episode only:
+ * d_terminal_obs [N][S], d_episode_return [N] (fp64), d_episode_length [N].
+ * The new states (post auto-reset) land in prb_vecenv_states_device(). */
+PRB_API int prb_vecenv_step(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done,
+                            float* d_terminal_obs, double* d_episode_return, int32_t* d_episode_length);
+/* Host-buffer forms with the reference's Tensor2 (double) layouts. */
+PRB_API int prb_vecenv_reset_host(prb_vecenv env, uint64_t seed, double* states);
+PRB_API int prb_vecenv_step_host(prb_vecenv env, const double* actions, double* next_states, double* rewards,
+                                 uint8_t* dones, double* terminal_states, double* episode_returns,
+                                 uint64_t* episode_lengths);
+PRB_API int prb_vecenv_states_host(prb_vecenv env, double* states);
+PRB_API int prb_vecenv_step_counts_host(prb_vecenv env, uint64_t* out); /* step_counts() env.hpp:183 */
+
+/* ---- agent: actor (GaussianPolicy) + critic + Adam ---------------------- */
+typedef struct prb_agent_s* prb_agent;
+/* AgentArtifact shape (artifact.hpp:23-86): actor S->hidden...->A (tanh
+ * hidden, linear out, nn.hpp:63-85), log_std[A], critic S->hidden...->1. */
+PRB_API int prb_agent_create(prb_ctx ctx, size_t state_dim, size_t action_dim, const size_t* hidden, int n_hidden,
+                             prb_agent* out);
+PRB_API int prb_agent_destroy(prb_agent a);
+PRB_API size_t prb_agent_param_count(prb_agent a);                  /* param_count() artifact.hpp:30 */
+/* flatten/unflatten_params artifact.hpp:38-72 + AdamState nn.hpp:144-152.
+ * m/v may be NULL (zeros on set, skipped on get). */
+PRB_API int prb_agent_set_host(prb_agent a, const double* flat, const double* m, const double* v, int64_t t,
+                               double lr);
+PRB_API int prb_agent_get_host(prb_agent a, double* flat, double* m, double* v, int64_t* t);
+PRB_API int prb_agent_copy(prb_agent dst, prb_agent src); /* AgentArtifact copy (deep) */
+PRB_API float* prb_agent_params_device(prb_agent a);       /* [P] fp32 flat blob */
+/* artifact_init artifact.hpp:91-105 (host, bit-exact with the reference). */
+PRB_API int prb_artifact_init(size_t state_dim, size_t action_dim, uint64_t seed, const size_t* hidden, int n_hidden,
+                              double* flat_out, size_t* param_count);
+
+/* ---- policy (nn.hpp:229-277) -------------------------------------------- */
+/* policy_sample nn.hpp:250-265 fused with the critic forward of worker_collect
+ * (pod.hpp:112-113).  Noise: Philox4x32-10 keyed by (seed), counter =
+ * (counter, row, d).  d_values / d_eps nullable; d_eps receives the unit
+ * normals used (parity seam).  NumericError on non-finite states. */
+PRB_API int prb_policy_sample(prb_agent a, const float* d_states, size_t n, uint64_t seed, uint64_t counter,
+                              float* d_actions, float* d_log_probs, float* d_values, float* d_eps);
+/* Same with injected unit normals d_eps [n][A] (reference-side seam). */
+PRB_API int prb_policy_sample_eps(prb_agent a, const float* d_states, size_t n, const float* d_eps,
+                                  float* d_actions, float* d_log_probs, float* d_values);
+PRB_API int prb_policy_mean(prb_agent a, const float* d_states, size_t n, float* d_mean);        /* nn.hpp:268 */
+PRB_API int prb_policy_log_prob(prb_agent a, const float* d_states, const float* d_actions, size_t n,
+                                float* d_log_probs);                                              /* nn.hpp:229 */
+PRB_API int prb_critic_value(prb_agent a, const float* d_states, size_t n, float* d_values);      /* nn.hpp:63 */
+
+/* ---- rollout buffer + collection (buffer.hpp, pod.hpp:95-132) ----------- */
+typedef struct prb_rollout_s* prb_rollout;
+/* TransitionBuffer(N*H, S, A) buffer.hpp:39-48, sized for one VecEnv of N
+ * envs collected for H steps.  The stock env's rows are stored compactly
+ * (balance/cap + shares per transition, the 150 shared features by time
+ * index); other envs store full rows. */
+PRB_API int prb_rollout_create(prb_vecenv env, size_t horizon, prb_rollout* out);
+/* As above for an externally supplied buffer (full rows, no env). */
+PRB_API int prb_rollout_create_raw(prb_ctx ctx, size_t num_envs, size_t horizon, size_t state_dim, size_t action_dim,
+                                   prb_rollout* out);
+PRB_API int prb_rollout_destroy(prb_rollout r);
+/* worker_collect pod.hpp:95-132: H steps of policy_sample + critic + step,
+ * then the bootstrap V(s_H) per env.  Noise stream keyed by seed (the
+ * reference's derive_seed(seed, kCollect, w, epoch)). */
+PRB_API int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed);
+/* Host transfer in the REFERENCE index space (chunk e = rows e*H..e*H+H-1,
+ * pod.hpp:89-94): states [N*H][S], actions [N*H][A], log_probs, rewards,
+ * dones, values [N*H], bootstrap [N].  Any pointer may be NULL (download). */
+PRB_API int prb_rollout_download(prb_rollout r, double* states, double* actions, double* log_probs, double* rewards,
+                                 uint8_t* dones, double* values, double* bootstrap);
+PRB_API int prb_rollout_upload(prb_rollout r, const double* states, const double* actions, const double* log_probs,
+                               const double* rewards, const uint8_t* dones, const double* values,
+                               const double* bootstrap);
+
+/* ---- GAE (ppo.hpp:50-71, 212-244) --------------------------------------- */
+/* buffer_advantages: per-env reverse scan + whole-buffer mean/std (std floor
+ * 1e-8).  Results stay on device for prb_ppo_update. */
+PRB_API int prb_gae(prb_rollout r, double gamma, double lambda, int normalize);
+/* Normalised advantages and returns in the reference index space. */
+PRB_API int prb_gae_download(prb_rollout r, double* advantages, double* returns);
+/* compute_gae over raw device arrays in TIME-MAJOR layout [H][N]. */
+PRB_API int prb_compute_gae(prb_ctx ctx, const float* d_rewards, const float* d_values, const uint8_t* d_dones,
+                            const float* d_bootstrap, size_t num_envs, size_t horizon, double gamma, double lambda,
+                            float* d_adv, float* d_ret);
+
+/* ---- PPO (ppo.hpp:18-296) ------------------------------------------------ */
+typedef struct {
+  double gamma, gae_lambda, clip_eps, entropy_coef, value_coef; /* PpoConfig ppo.hpp:18-27 */
+  uint64_t epochs_per_update, minibatch_size, buffer_size;
+  double learning_rate;
+} prb_ppo_config;
+
+typedef struct {
+  double mean_policy_loss, mean_value_loss, mean_entropy; /* PpoUpdateStats ppo.hpp:198-203 */
+  uint64_t minibatches;
+} prb_ppo_stats;
+
+/* ppo_update ppo.hpp:249-296: dst := src, then epochs x full minibatches of
+ * (gather, actor/critic forward, clipped surrogate + value + entropy
+ * gradients, Adam).  GAE is (re)computed from r.  Permutations: if perm is
+ * NULL they are generated on device from seed; else perm holds
+ * epochs*buffer_size indices in the reference index space (e.g. the exact
+ * std::shuffle sequence).  On error dst is unspecified and src untouched. */
+PRB_API int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed,
+                           const uint64_t* perm, prb_agent dst, prb_ppo_stats* stats);
+/* detail::ppo_loss_grads ppo.hpp:116-188 on one minibatch of rollout rows
+ * (reference index space); grads [P] (flat layout) and losses[3] to host.
+ * Requires prb_gae first. */
+PRB_API int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows, size_t n, const prb_ppo_config* cfg,
+                               double* grads, double* losses);
+/* adam_step nn.hpp:164-182 with host gradients (NumericError, state untouched,
+ * on a non-finite gradient). */
+PRB_API int prb_adam_step_host(prb_agent a, const double* grads);
+
+/* ---- learner fusion (pod.hpp:141-172) ----------------------------------- */
+PRB_API int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out);
+
+/* ---- leaderboard (tournament.hpp:44-162) --------------------------------- */
+/* Ranks candidates (score, seq) by (score desc, seq asc) and keeps the top
+ * `capacity` -- identical to sequential leaderboard_update insertion
+ * (tournament.hpp:104-119).  d_order[capacity] receives candidate indices,
+ * d_count the board size.  NumericError on a non-finite score. */
+PRB_API int prb_leaderboard_rank(prb_ctx ctx, const double* d_scores, const uint64_t* d_seqs, size_t n,
+                                 size_t capacity, int32_t* d_order, int32_t* d_count);
+PRB_API int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t* seqs, size_t n,
+                                      size_t capacity, int32_t* order, int32_t* count);
+/* generate_pod_init's mutation (tournament.hpp:149-159): params += N(0, sigma^2)
+ * from a Philox stream keyed by mutation_seed; optimiser t := 0, m/v kept. */
+PRB_API int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma);
+
+/* ---- NCCL over NVLink (tournament C4) --------------------- */
+typedef struct prb_comm_s* prb_comm;
+PRB_API int prb_comm_unique_id(uint8_t id[128]);
+PRB_API int prb_comm_init(prb_ctx ctx, const uint8_t id[128], int nranks, int rank, prb_comm* out);
+PRB_API int prb_comm_destroy(prb_comm c);
+/* All-gather of every rank's n_local (score, seq, pod_id) then the same
+ * ranking on every rank.  Outputs (device): d_all_* [nranks*n_local],
+ * d_order [capacity], d_count. */
+PRB_API int prb_leaderboard_allgather_rank(prb_comm c, const double* d_scores, const uint64_t* d_seqs,
+                                           const int64_t* d_ids, size_t n_local, size_t capacity, double* d_all_scores,
+                                           uint64_t* d_all_seqs, int64_t* d_all_ids, int32_t* d_order,
+                                           int32_t* d_count);
+/* Broadcast an agent's params, m, v and t from `root` (elite broadcast). */
+PRB_API int prb_agent_broadcast(prb_comm c, prb_agent a, int root);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRB_H_ */

@@ -1,0 +1,396 @@
+// agent.cu -- the device AgentArtifact (artifact.hpp:23-86): flat fp32
+// parameter blob in the reference's canonical order, Adam state (nn.hpp:144-182),
+// learner fusion (pod.hpp:141-172), leaderboard ranking (tournament.hpp:104-119)
+// and the generator's mutation (tournament.hpp:149-159).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "prb_internal.h"
+#include "rng.cuh"
+
+using namespace prb;
+
+namespace {
+
+void layout(prb_agent_s* a) {
+  a->adims.clear();
+  a->cdims.clear();
+  a->adims.push_back(a->S);
+  a->cdims.push_back(a->S);
+  for (size_t h : a->hidden) {
+    a->adims.push_back(h);
+    a->cdims.push_back(h);
+  }
+  a->adims.push_back(a->A);
+  a->cdims.push_back(1);
+  size_t off = 0;
+  a->aoff.clear();
+  for (size_t i = 0; i + 1 < a->adims.size(); ++i) {
+    a->aoff.push_back(off);
+    off += a->adims[i] * a->adims[i + 1] + a->adims[i + 1];
+  }
+  a->Pa = off;
+  off += a->A;  // log_std
+  a->coff.clear();
+  for (size_t i = 0; i + 1 < a->cdims.size(); ++i) {
+    a->coff.push_back(off);
+    off += a->cdims[i] * a->cdims[i + 1] + a->cdims[i + 1];
+  }
+  a->P = off;
+  a->Pc = a->P - a->Pa - a->A;
+}
+
+// adam_step nn.hpp:164-182 on device; gate[0] != 0 aborts without touching state.
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, size_t n, const int64_t* __restrict__ t_dev,
+                            const int32_t* __restrict__ gate, float lr, float b1, float b2, float eps) {
+  if (gate && gate[0] != 0) return;
+  const int64_t t = *t_dev;  // already advanced by the producer of g
+  const double bc1 = 1.0 - pow((double)b1, (double)t);
+  const double bc2 = 1.0 - pow((double)b2, (double)t);
+  const float ibc1 = (float)(1.0 / bc1), ibc2 = (float)(1.0 / bc2);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi * ibc1) / (sqrtf(vi * ibc2) + eps);
+  }
+}
+
+__global__ void finite_check_kernel(const float* __restrict__ g, size_t n, int32_t* status, int64_t* t_dev) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  int local = 0;
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) local |= !isfinite(g[i]);
+  if (local) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (bad) {
+      status[0] = PRB_ERR_NUMERIC;
+      status[1] = 1;  // adam_step: non-finite gradient
+    } else {
+      status[0] = 0;
+      *t_dev += 1;
+    }
+  }
+}
+
+__global__ void fuse_kernel(const float* const* __restrict__ src, size_t L, size_t n, float* __restrict__ dst,
+                            float inv) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (size_t a = 0; a < L; ++a) s += src[a][i];
+    dst[i] = s * inv;
+  }
+}
+
+// Rank candidates by (score desc, seq asc); a candidate's rank is the number
+// of candidates that beat it.  Equals sequential leaderboard_update insertion
+// (tournament.hpp:104-119; test_tournament.cpp:95-126).
+__global__ void leaderboard_rank_kernel(const double* __restrict__ score, const uint64_t* __restrict__ seq, int n,
+                                        int capacity, int32_t* __restrict__ order, int32_t* __restrict__ count,
+                                        int32_t* __restrict__ status) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (!isfinite(score[i])) bad = 1;
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) {
+      status[0] = PRB_ERR_NUMERIC;
+      *count = 0;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double si = score[i];
+    const uint64_t qi = seq[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double sj = score[j];
+      rank += (sj > si) || (sj == si && seq[j] < qi);
+    }
+    if (rank < capacity) order[rank] = i;
+  }
+  if (threadIdx.x == 0) {
+    *count = min(n, capacity);
+    status[0] = 0;
+  }
+}
+
+__global__ void mutate_kernel(float* __restrict__ p, size_t n, uint64_t seed, float sigma) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const Philox4 r = philox4x32_10((uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)i, (uint32_t)(i >> 32),
+                                    0x6d757461u /*"muta"*/, 0u);
+    const float2 z = box_muller(r.x, r.y);
+    p[i] += sigma * z.x;
+  }
+}
+
+}  // namespace
+
+void prb_agent_finite_gate_and_adam(prb_agent a, const float* d_grads, cudaStream_t s) {
+  finite_check_kernel<<<1, 1024, 0, s>>>(d_grads, a->P, a->d_status.p, a->d_t.p);
+  const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
+  adam_kernel<<<grid, 256, 0, s>>>(a->d_params.p, d_grads, a->d_m.p, a->d_v.p, a->P, a->d_t.p, a->d_status.p,
+                                   (float)a->lr, (float)a->beta1, (float)a->beta2, (float)a->eps);
+  PRB_CHECK_LAUNCH();
+}
+
+void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s) {
+  const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
+  adam_kernel<<<grid, 256, 0, s>>>(a->d_params.p, d_grads, a->d_m.p, a->d_v.p, a->P, a->d_t.p, gate, (float)a->lr,
+                                   (float)a->beta1, (float)a->beta2, (float)a->eps);
+  PRB_CHECK_LAUNCH();
+}
+
+int prb_agent_status(prb_agent a, std::string* msg);
+
+extern "C" {
+
+int prb_agent_create(prb_ctx ctx, size_t S, size_t A, const size_t* hidden, int nh, prb_agent* out) {
+  return guard([&] {
+    PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_agent_create: NULL argument");
+    PRB_REQUIRE(S > 0 && A > 0, PRB_ERR_USAGE, "mlp_init: need at least input and output dims");
+    PRB_REQUIRE(nh >= 0 && nh <= 6, PRB_ERR_CONFIG, "prb_agent_create: 0..6 hidden layers supported");
+    for (int i = 0; i < nh; ++i)
+      PRB_REQUIRE(hidden[i] > 0 && hidden[i] <= 1024, PRB_ERR_CONFIG, "prb_agent_create: hidden widths 1..1024");
+    PRB_REQUIRE(S <= 4096 && A <= 256, PRB_ERR_CONFIG, "prb_agent_create: state_dim <= 4096, action_dim <= 256");
+    PRB_CUDA(cudaSetDevice(ctx->device));
+    auto* a = new prb_agent_s;
+    a->ctx = ctx;
+    a->S = S;
+    a->A = A;
+    a->hidden.assign(hidden, hidden + nh);
+    layout(a);
+    a->d_params.alloc(a->P);
+    a->d_m.alloc(a->P);
+    a->d_v.alloc(a->P);
+    a->d_grads.alloc(a->P);
+    a->d_t.alloc(1);
+    a->d_status.alloc(4);
+    PRB_CUDA(cudaMemset(a->d_params.p, 0, a->d_params.bytes()));
+    PRB_CUDA(cudaMemset(a->d_m.p, 0, a->d_m.bytes()));
+    PRB_CUDA(cudaMemset(a->d_v.p, 0, a->d_v.bytes()));
+    PRB_CUDA(cudaMemset(a->d_t.p, 0, sizeof(int64_t)));
+    PRB_CUDA(cudaMemset(a->d_status.p, 0, 4 * sizeof(int32_t)));
+    *out = a;
+  });
+}
+
+int prb_agent_destroy(prb_agent a) {
+  return guard([&] {
+    if (a) cudaStreamSynchronize(a->ctx->stream);
+    delete a;
+  });
+}
+
+size_t prb_agent_param_count(prb_agent a) { return a ? a->P : 0; }
+float* prb_agent_params_device(prb_agent a) { return a ? a->d_params.p : nullptr; }
+
+int prb_agent_set_host(prb_agent a, const double* flat, const double* m, const double* v, int64_t t, double lr) {
+  return guard([&] {
+    PRB_REQUIRE(a && flat, PRB_ERR_USAGE, "prb_agent_set_host: NULL argument");
+    std::vector<float> buf(a->P);
+    cudaStream_t s = a->ctx->stream;
+    for (size_t i = 0; i < a->P; ++i) buf[i] = (float)flat[i];
+    PRB_CUDA(cudaMemcpyAsync(a->d_params.p, buf.data(), a->P * sizeof(float), cudaMemcpyHostToDevice, s));
+    a->ctx->sync();
+    if (m) {
+      for (size_t i = 0; i < a->P; ++i) buf[i] = (float)m[i];
+      PRB_CUDA(cudaMemcpyAsync(a->d_m.p, buf.data(), a->P * sizeof(float), cudaMemcpyHostToDevice, s));
+      a->ctx->sync();
+    } else {
+      PRB_CUDA(cudaMemsetAsync(a->d_m.p, 0, a->d_m.bytes(), s));
+    }
+    if (v) {
+      for (size_t i = 0; i < a->P; ++i) buf[i] = (float)v[i];
+      PRB_CUDA(cudaMemcpyAsync(a->d_v.p, buf.data(), a->P * sizeof(float), cudaMemcpyHostToDevice, s));
+      a->ctx->sync();
+    } else {
+      PRB_CUDA(cudaMemsetAsync(a->d_v.p, 0, a->d_v.bytes(), s));
+    }
+    PRB_CUDA(cudaMemcpyAsync(a->d_t.p, &t, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    a->ctx->sync();
+    a->lr = lr;
+  });
+}
+
+int prb_agent_get_host(prb_agent a, double* flat, double* m, double* v, int64_t* t) {
+  return guard([&] {
+    PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_get_host: NULL agent");
+    std::vector<float> buf(a->P);
+    cudaStream_t s = a->ctx->stream;
+    auto pull = [&](const float* d, double* h) {
+      if (!h) return;
+      PRB_CUDA(cudaMemcpyAsync(buf.data(), d, a->P * sizeof(float), cudaMemcpyDeviceToHost, s));
+      a->ctx->sync();
+      for (size_t i = 0; i < a->P; ++i) h[i] = buf[i];
+    };
+    pull(a->d_params.p, flat);
+    pull(a->d_m.p, m);
+    pull(a->d_v.p, v);
+    if (t) {
+      PRB_CUDA(cudaMemcpyAsync(t, a->d_t.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      a->ctx->sync();
+    }
+  });
+}
+
+int prb_agent_copy(prb_agent dst, prb_agent src) {
+  return guard([&] {
+    PRB_REQUIRE(dst && src, PRB_ERR_USAGE, "prb_agent_copy: NULL agent");
+    PRB_REQUIRE(dst->P == src->P && dst->adims == src->adims && dst->cdims == src->cdims, PRB_ERR_USAGE,
+                "prb_agent_copy: incompatible shapes");
+    cudaStream_t s = src->ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(dst->d_params.p, src->d_params.p, src->d_params.bytes(), cudaMemcpyDeviceToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dst->d_m.p, src->d_m.p, src->d_m.bytes(), cudaMemcpyDeviceToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dst->d_v.p, src->d_v.p, src->d_v.bytes(), cudaMemcpyDeviceToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dst->d_t.p, src->d_t.p, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (dst->ctx->stream != s) src->ctx->sync();
+    dst->lr = src->lr;
+  });
+}
+
+int prb_adam_step_host(prb_agent a, const double* grads) {
+  return guard([&] {
+    PRB_REQUIRE(a && grads, PRB_ERR_USAGE, "prb_adam_step_host: NULL argument");
+    for (size_t i = 0; i < a->P; ++i)  // nn.hpp:169-171: reject before touching state
+      PRB_REQUIRE(std::isfinite(grads[i]), PRB_ERR_NUMERIC, "adam_step: non-finite gradient, step aborted");
+    std::vector<float> g(a->P);
+    for (size_t i = 0; i < a->P; ++i) g[i] = (float)grads[i];
+    cudaStream_t s = a->ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(a->d_grads.p, g.data(), a->P * sizeof(float), cudaMemcpyHostToDevice, s));
+    prb_agent_finite_gate_and_adam(a, a->d_grads.p, s);
+    a->ctx->sync();
+  });
+}
+
+int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out) {
+  return guard([&] {
+    PRB_REQUIRE(n > 0 && agents, PRB_ERR_USAGE, "fuse_parameters: empty artifact list");  // pod.hpp:142
+    PRB_REQUIRE(out, PRB_ERR_USAGE, "fuse_parameters: NULL output");
+    for (size_t i = 0; i < n; ++i)
+      PRB_REQUIRE(agents[i] && agents[i]->adims == agents[0]->adims && agents[i]->cdims == agents[0]->cdims &&
+                      agents[i]->A == agents[0]->A,
+                  PRB_ERR_USAGE, "fuse_parameters: artifacts have incompatible shapes");  // pod.hpp:145-148
+    PRB_REQUIRE(out->P == agents[0]->P, PRB_ERR_USAGE, "fuse_parameters: output shape mismatch");
+    prb_ctx_s* ctx = out->ctx;
+    cudaStream_t s = ctx->stream;
+    for (size_t i = 0; i < n; ++i)
+      if (agents[i]->ctx->stream != s) agents[i]->ctx->sync();
+    if (n == 1) {  // a single artifact is returned unchanged (pod.hpp:143)
+      if (agents[0] != out) {
+        int rc = prb_agent_copy(out, agents[0]);
+        if (rc) fail(rc, prb_last_error());
+      }
+      return;
+    }
+    // mean of params, m, v; t = max (pod.hpp:149-171)
+    std::vector<const float*> hp(n), hm(n), hv(n);
+    for (size_t i = 0; i < n; ++i) {
+      hp[i] = agents[i]->d_params.p;
+      hm[i] = agents[i]->d_m.p;
+      hv[i] = agents[i]->d_v.p;
+    }
+    const float** dptr = static_cast<const float**>(ctx->device_scratch(3 * n * sizeof(float*)));
+    std::vector<const float*> all;
+    all.insert(all.end(), hp.begin(), hp.end());
+    all.insert(all.end(), hm.begin(), hm.end());
+    all.insert(all.end(), hv.begin(), hv.end());
+    PRB_CUDA(cudaMemcpyAsync(dptr, all.data(), all.size() * sizeof(float*), cudaMemcpyHostToDevice, s));
+    const float inv = (float)(1.0 / (double)n);
+    const size_t P = out->P;
+    const int grid = (int)std::min<size_t>((P + 255) / 256, 1184);
+    // Aliasing is safe only when out is not an input; stage through grads when it is.
+    bool alias = false;
+    for (size_t i = 0; i < n; ++i) alias |= (agents[i] == out);
+    float* dst_p = alias ? out->d_grads.p : out->d_params.p;
+    fuse_kernel<<<grid, 256, 0, s>>>(dptr, n, P, dst_p, inv);
+    if (alias) {
+      PRB_CUDA(cudaStreamSynchronize(s));
+      PRB_CUDA(cudaMemcpyAsync(out->d_params.p, dst_p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      fuse_kernel<<<grid, 256, 0, s>>>(dptr + n, n, P, out->d_grads.p, inv);
+      PRB_CUDA(cudaMemcpyAsync(out->d_m.p, out->d_grads.p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      fuse_kernel<<<grid, 256, 0, s>>>(dptr + 2 * n, n, P, out->d_grads.p, inv);
+      PRB_CUDA(cudaMemcpyAsync(out->d_v.p, out->d_grads.p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    } else {
+      fuse_kernel<<<grid, 256, 0, s>>>(dptr + n, n, P, out->d_m.p, inv);
+      fuse_kernel<<<grid, 256, 0, s>>>(dptr + 2 * n, n, P, out->d_v.p, inv);
+    }
+    PRB_CHECK_LAUNCH();
+    int64_t tmax = 0;
+    for (size_t i = 0; i < n; ++i) {
+      int64_t ti = 0;
+      PRB_CUDA(cudaMemcpyAsync(&ti, agents[i]->d_t.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      ctx->sync();
+      tmax = std::max(tmax, ti);
+    }
+    PRB_CUDA(cudaMemcpyAsync(out->d_t.p, &tmax, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    out->lr = agents[0]->lr;
+    ctx->sync();
+  });
+}
+
+int prb_leaderboard_rank(prb_ctx ctx, const double* d_scores, const uint64_t* d_seqs, size_t n, size_t capacity,
+                         int32_t* d_order, int32_t* d_count) {
+  return guard([&] {
+    PRB_REQUIRE(ctx, PRB_ERR_USAGE, "prb_leaderboard_rank: NULL ctx");
+    PRB_REQUIRE(capacity > 0, PRB_ERR_CONFIG, "Leaderboard: capacity must be > 0");  // tournament.hpp:47
+    PRB_REQUIRE(n < (1u << 20), PRB_ERR_CONFIG, "prb_leaderboard_rank: too many candidates");
+    int32_t* status = static_cast<int32_t*>(ctx->device_scratch(16));
+    leaderboard_rank_kernel<<<1, 256, 0, ctx->stream>>>(d_scores, d_seqs, (int)n, (int)capacity, d_order, d_count,
+                                                        status);
+    PRB_CHECK_LAUNCH();
+    int32_t st = 0;
+    PRB_CUDA(cudaMemcpyAsync(&st, status, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    PRB_REQUIRE(st == 0, PRB_ERR_NUMERIC, "leaderboard_update: candidate score is not finite");
+  });
+}
+
+int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t* seqs, size_t n, size_t capacity,
+                              int32_t* order, int32_t* count) {
+  return guard([&] {
+    PRB_REQUIRE(ctx, PRB_ERR_USAGE, "prb_leaderboard_rank_host: NULL ctx");
+    DevBuf<double> ds;
+    DevBuf<uint64_t> dq;
+    DevBuf<int32_t> dout;
+    ds.alloc(std::max<size_t>(n, 1));
+    dq.alloc(std::max<size_t>(n, 1));
+    dout.alloc(capacity + 1);
+    cudaStream_t s = ctx->stream;
+    if (n) {
+      PRB_CUDA(cudaMemcpyAsync(ds.p, scores, n * sizeof(double), cudaMemcpyHostToDevice, s));
+      PRB_CUDA(cudaMemcpyAsync(dq.p, seqs, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    }
+    int rc = prb_leaderboard_rank(ctx, ds.p, dq.p, n, capacity, dout.p, dout.p + capacity);
+    if (rc) fail(rc, prb_last_error());
+    std::vector<int32_t> h(capacity + 1);
+    PRB_CUDA(cudaMemcpyAsync(h.data(), dout.p, (capacity + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    ctx->sync();
+    *count = h[capacity];
+    for (int i = 0; i < *count; ++i) order[i] = h[i];
+  });
+}
+
+int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma) {
+  return guard([&] {
+    PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_mutate: NULL agent");
+    cudaStream_t s = a->ctx->stream;
+    if (sigma > 0.0) {
+      const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
+      mutate_kernel<<<grid, 256, 0, s>>>(a->d_params.p, a->P, mutation_seed, (float)sigma);
+      PRB_CHECK_LAUNCH();
+    }
+    PRB_CUDA(cudaMemsetAsync(a->d_t.p, 0, sizeof(int64_t), s));  // optimizer.t = 0 (tournament.hpp:160)
+    a->ctx->sync();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,605 @@
+// env.cu -- vectorised environments on device (VectorizedEnvironment,
+// env.hpp:167-249) with the stock-trading env (stock_env.hpp:55-184) and the
+// PointMass2D analytic control env (env.hpp:84-146).
+//
+// Layout (HBM, SoA so every per-env field is read/written coalesced):
+//   stock:  balance f64 [N], shares i32 [K][N], episode_return f64 [N];
+//           price table f64 [T][K] and the window's shared obs features
+//           f32 [T][5K] are read-only and L2-resident.  All envs of one
+//           VecEnv run in lock-step (same t, same done; stock_env.hpp:161,
+//           env.hpp:221), so t / step_count are scalars owned by the host.
+//   pointmass: state f64 [6][N], steps i32 [N], episode_return f64 [N],
+//           per-env mt19937_64 reset stream u64 [312][N] + idx i32 [N].
+//   obs (VectorizedEnvironment::states_): f32 [N][S] row-major.
+//
+// Arithmetic: the portfolio accounting is fp64 with explicit round-to-nearest
+// intrinsics (no FMA contraction), in the reference's operation order, so
+// balances, share counts, rewards and dones are bit-identical with the
+// -ffp-contract=off reference build.  Obs and rewards are stored as fp32.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "prb_internal.h"
+#include "rng.cuh"
+
+using namespace prb;
+
+namespace {
+
+constexpr int kEnvBlock = 128;
+
+// std::clamp / std::min / std::max semantics (NaN-propagating exactly as libstdc++).
+__device__ __forceinline__ double clamp_ref(double v, double lo, double hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
+__device__ __forceinline__ double min_ref(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double max_ref(double a, double b) { return (a < b) ? b : a; }
+
+struct StockStepArgs {
+  int N, K, S;
+  int t;       // portfolio time before the step
+  int t_obs;   // time index of the returned (post-reset) observation
+  int done;    // uniform episode end
+  int ep_len;  // episode length reported on done
+  const double* __restrict__ close_tk;  // [T][K]
+  const float* __restrict__ feat;       // [T][5K]
+  double cap, max_trade, cost;
+  const float* __restrict__ actions;  // [N][K]
+  double* __restrict__ balance;
+  int32_t* __restrict__ shares;  // [K][N]
+  double* __restrict__ ep_return;
+  float* __restrict__ obs;  // [N][S]
+  float* __restrict__ reward;
+  uint8_t* __restrict__ done_out;
+  float* __restrict__ term_obs;
+  double* __restrict__ term_ret;
+  int32_t* __restrict__ term_len;
+};
+
+// Coalesced write of a CTA's block of obs rows: row r = [priv[r][0..P), shared[0..S-P)].
+__device__ __forceinline__ void write_obs_rows(float* __restrict__ dst, int nrows, int S, int P,
+                                               const float* __restrict__ s_priv, int Pp,
+                                               const float* __restrict__ s_shared) {
+  const int total = nrows * S;
+  int r = threadIdx.x / S, c = threadIdx.x - (threadIdx.x / S) * S;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    dst[i] = (c < P) ? s_priv[r * Pp + c] : s_shared[c - P];
+    c += blockDim.x;
+    while (c >= S) {
+      c -= S;
+      ++r;
+    }
+  }
+}
+
+// One VecEnv step of N stock envs (env.hpp:200-236 -> StockTradingEnv::step
+// stock_env.hpp:165-170 -> stock_env_step :55-103 -> stock_observation :115-131).
+__global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, Kp = K + 1, F = 5 * K;
+  double* s_p0 = reinterpret_cast<double*>(smem_raw);      // [K] close[t]
+  double* s_p1 = s_p0 + K;                                  // [K] close[t+1]
+  float* s_act = reinterpret_cast<float*>(s_p1 + K);        // [128][Kp]
+  int32_t* s_sh = reinterpret_cast<int32_t*>(s_act + kEnvBlock * Kp);  // [K][128]
+  float* s_priv = reinterpret_cast<float*>(s_sh + K * kEnvBlock);      // [128][Kp]
+  float* s_feat_obs = s_priv + kEnvBlock * Kp;                         // [5K]
+  float* s_feat_term = s_feat_obs + F;                                 // [5K]
+
+  const int tid = threadIdx.x;
+  const size_t e0 = (size_t)blockIdx.x * kEnvBlock;
+  const int nloc = min(kEnvBlock, a.N - (int)e0);
+
+  for (int k = tid; k < K; k += blockDim.x) {
+    s_p0[k] = a.close_tk[(size_t)a.t * K + k];
+    s_p1[k] = a.close_tk[(size_t)(a.t + 1) * K + k];
+  }
+  for (int j = tid; j < F; j += blockDim.x) {
+    s_feat_obs[j] = a.feat[(size_t)a.t_obs * F + j];
+    if (a.done) s_feat_term[j] = a.feat[(size_t)(a.t + 1) * F + j];
+  }
+  {  // actions [nloc][K] are one contiguous span: coalesced load into padded rows
+    const float* src = a.actions + e0 * K;
+    const int total = nloc * K;
+    int r = tid / K, c = tid - (tid / K) * K;
+    for (int i = tid; i < total; i += blockDim.x) {
+      s_act[r * Kp + c] = src[i];
+      c += blockDim.x;
+      while (c >= K) {
+        c -= K;
+        ++r;
+      }
+    }
+  }
+  if (tid < nloc)
+    for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = a.shares[(size_t)k * a.N + e0 + tid];
+  __syncthreads();
+
+  if (tid < nloc) {
+    const size_t e = e0 + tid;
+    double bal = a.balance[e];
+    // value_before (PortfolioState::account_value stock_env.hpp:27-31)
+    double vb = bal;
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p0[k]));
+    // desired = trunc(clamp(a) * max_trade_shares)  (:83-87; the VecEnv clip env.hpp:213-215 is idempotent)
+    const float* act = s_act + tid * Kp;
+    // sells first (:88-90)
+    for (int k = 0; k < K; ++k) {
+      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
+      if (d < 0.0) {
+        const int32_t held = s_sh[k * kEnvBlock + tid];
+        const double q = -min_ref(-d, (double)held);
+        const double price = s_p0[k];
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+        s_sh[k * kEnvBlock + tid] = held + (int32_t)q;
+      }
+    }
+    // then buys, each clipped to the affordable balance incl. cost (:91-97)
+    const double cost_factor = __dadd_rn(1.0, a.cost);
+    for (int k = 0; k < K; ++k) {
+      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
+      if (d > 0.0) {
+        const double price = s_p0[k];
+        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
+        const double q = min_ref(d, max_ref(affordable, 0.0));
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+        s_sh[k * kEnvBlock + tid] += (int32_t)q;
+      }
+    }
+    // t+1, reward = value_after - value_before (:99-100)
+    double va = bal;
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p1[k]));
+    const double r = __dsub_rn(va, vb);
+    const double ret = __dadd_rn(a.ep_return[e], r);  // env.hpp:218
+    if (a.reward) a.reward[e] = (float)r;
+    if (a.done_out) a.done_out[e] = (uint8_t)a.done;
+    float* priv = s_priv + tid * Kp;
+    priv[0] = (float)__ddiv_rn(bal, a.cap);
+    for (int k = 0; k < K; ++k) priv[1 + k] = (float)s_sh[k * kEnvBlock + tid];
+    if (a.done) {  // env.hpp:221-229: report the terminal episode, auto-reset (stock_env.hpp:158-163)
+      if (a.term_ret) a.term_ret[e] = ret;
+      if (a.term_len) a.term_len[e] = a.ep_len;
+      a.balance[e] = a.cap;
+      a.ep_return[e] = 0.0;
+    } else {
+      a.balance[e] = bal;
+      a.ep_return[e] = ret;
+    }
+  }
+  __syncthreads();
+  const int S = a.S;
+  if (a.done) {
+    if (a.term_obs) write_obs_rows(a.term_obs + e0 * S, nloc, S, K + 1, s_priv, Kp, s_feat_term);
+    __syncthreads();
+    for (int i = tid; i < nloc * Kp; i += blockDim.x) s_priv[i] = ((i % Kp) == 0) ? (float)(a.cap / a.cap) : 0.0f;
+    if (tid < nloc)
+      for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = 0;
+    __syncthreads();
+  }
+  if (tid < nloc)
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e0 + tid] = s_sh[k * kEnvBlock + tid];
+  write_obs_rows(a.obs + e0 * S, nloc, S, K + 1, s_priv, Kp, s_feat_obs);
+}
+
+// reset (env.hpp:186-194 -> StockTradingEnv::reset stock_env.hpp:158-163)
+__global__ void stock_reset_kernel(int N, int K, int S, double cap, const float* __restrict__ feat_row,
+                                   double* balance, int32_t* shares, double* ep_return, float* obs) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (size_t)N) {
+    balance[e] = cap;
+    ep_return[e] = 0.0;
+    for (int k = 0; k < K; ++k) shares[(size_t)k * N + e] = 0;
+  }
+  const size_t total = (size_t)N * S;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % S);
+    obs[i] = (c == 0) ? (float)(cap / cap) : (c <= K ? 0.0f : feat_row[c - 1 - K]);
+  }
+}
+
+// ---- PointMass2D -----------------------------------------------------------
+
+struct PmStepArgs {
+  int N;
+  const float* __restrict__ actions;  // [N][2]
+  double* __restrict__ st;            // [6][N]
+  int32_t* __restrict__ steps;
+  double* __restrict__ ep_return;
+  uint64_t* __restrict__ mt;  // [312][N]
+  int32_t* __restrict__ mt_idx;
+  float* __restrict__ obs;  // [N][6]
+  float* __restrict__ reward;
+  uint8_t* __restrict__ done_out;
+  float* __restrict__ term_obs;
+  double* __restrict__ term_ret;
+  int32_t* __restrict__ term_len;
+};
+
+__device__ __forceinline__ void pm_reset_draws(uint64_t* mt, size_t N, int32_t& idx, double* s) {
+  // PointMass2D::reset env.hpp:124-133: pos_x, pos_y, goal_x, goal_y ~ U(-0.4, 0.4), vel = 0
+  s[0] = mt64_uniform(mt, N, idx, -0.4, 0.4);
+  s[1] = mt64_uniform(mt, N, idx, -0.4, 0.4);
+  s[2] = 0.0;
+  s[3] = 0.0;
+  s[4] = mt64_uniform(mt, N, idx, -0.4, 0.4);
+  s[5] = mt64_uniform(mt, N, idx, -0.4, 0.4);
+}
+
+__global__ void __launch_bounds__(256) pm_step_kernel(PmStepArgs a) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)a.N) return;
+  const size_t N = a.N;
+  double s[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) s[j] = a.st[j * N + e];
+  const float2 af = reinterpret_cast<const float2*>(a.actions)[e];
+  const double a0 = clamp_ref((double)af.x, -1.0, 1.0), a1 = clamp_ref((double)af.y, -1.0, 1.0);
+  const int32_t steps = a.steps[e];
+  // pointmass_step env.hpp:84-109
+  double n[6];
+  const double v0 = __dadd_rn(__dmul_rn(0.9, s[2]), __dmul_rn(0.1, a0));
+  const double v1 = __dadd_rn(__dmul_rn(0.9, s[3]), __dmul_rn(0.1, a1));
+  n[2] = v0;
+  n[3] = v1;
+  n[0] = __dadd_rn(s[0], __dmul_rn(0.1, v0));
+  n[1] = __dadd_rn(s[1], __dmul_rn(0.1, v1));
+  n[4] = s[4];
+  n[5] = s[5];
+  const double action_sq = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
+  const double dx = __dsub_rn(n[0], n[4]);
+  const double dy = __dsub_rn(n[1], n[5]);
+  const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+  double r = __dsub_rn(-dist, __dmul_rn(0.01, action_sq));
+  const bool reached = dist < 0.05;
+  if (reached) r = __dadd_rn(r, 10.0);
+  const bool done = reached || (steps + 1 >= 200);
+  const double ret = __dadd_rn(a.ep_return[e], r);
+  if (a.reward) a.reward[e] = (float)r;
+  if (a.done_out) a.done_out[e] = done ? 1 : 0;
+  if (done) {
+    if (a.term_obs)
+      for (int j = 0; j < 6; ++j) a.term_obs[e * 6 + j] = (float)n[j];
+    if (a.term_ret) a.term_ret[e] = ret;
+    if (a.term_len) a.term_len[e] = steps + 1;
+    int32_t idx = a.mt_idx[e];
+    pm_reset_draws(a.mt + e, N, idx, n);
+    a.mt_idx[e] = idx;
+    a.steps[e] = 0;
+    a.ep_return[e] = 0.0;
+  } else {
+    a.steps[e] = steps + 1;
+    a.ep_return[e] = ret;
+  }
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    a.st[j * N + e] = n[j];
+    a.obs[e * 6 + j] = (float)n[j];
+  }
+}
+
+__global__ void pm_reset_kernel(int N, uint64_t seed, double* st, int32_t* steps, double* ep_return, uint64_t* mt,
+                                int32_t* mt_idx, float* obs) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N) return;
+  // rngs_[i].seed(derive_seed(seed, kVecEnv, i)) env.hpp:188
+  mt64_seed(mt + e, N, derive_seed2(seed, 1, e));
+  int32_t idx = kMtN;
+  double s[6];
+  pm_reset_draws(mt + e, N, idx, s);
+  mt_idx[e] = idx;
+  steps[e] = 0;
+  ep_return[e] = 0.0;
+  for (int j = 0; j < 6; ++j) {
+    st[j * (size_t)N + e] = s[j];
+    obs[e * 6 + j] = (float)s[j];
+  }
+}
+
+size_t stock_smem_bytes(int K) {
+  const int Kp = K + 1;
+  return 2 * K * sizeof(double) + (size_t)kEnvBlock * Kp * sizeof(float) * 2 + (size_t)K * kEnvBlock * sizeof(int32_t) +
+         (size_t)10 * K * sizeof(float);
+}
+
+void check_env(prb_vecenv env) { PRB_REQUIRE(env, PRB_ERR_USAGE, "vecenv handle is NULL"); }
+
+}  // namespace
+
+// Launch one stock VecEnv step on device buffers (shared with rollout.cu).
+void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
+                           double* d_term_ret, int32_t* d_term_len) {
+  prb_market_s* m = env->market;
+  PRB_REQUIRE(env->t + 1 < m->T, PRB_ERR_USAGE, "stock_env_step: no next timestamp at t=" + std::to_string(env->t));
+  StockStepArgs a;
+  a.N = (int)env->N;
+  a.K = m->K;
+  a.S = (int)env->S;
+  a.t = (int)env->t;
+  const size_t t1 = env->t + 1;
+  const bool done = (t1 + 1 >= m->T) || (t1 >= env->end);  // stock_env.hpp:101,168
+  a.done = done ? 1 : 0;
+  a.t_obs = done ? (int)env->start : (int)t1;
+  a.ep_len = (int)(env->step_count + 1);
+  a.close_tk = m->d_close_tk.p;
+  a.feat = env->d_feat.p;
+  a.cap = env->cfg.initial_capital;
+  a.max_trade = env->cfg.max_trade_shares;
+  a.cost = env->cfg.cost_rate;
+  a.actions = d_actions;
+  a.balance = env->d_balance.p;
+  a.shares = env->d_shares.p;
+  a.ep_return = env->d_ep_return.p;
+  a.obs = env->d_obs.p;
+  a.reward = d_reward;
+  a.done_out = d_done;
+  a.term_obs = d_term_obs;
+  a.term_ret = d_term_ret;
+  a.term_len = d_term_len;
+  const size_t smem = stock_smem_bytes(m->K);
+  static bool attr_set = false;
+  if (!attr_set) {
+    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
+  stock_step_kernel<<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+  PRB_CHECK_LAUNCH();
+  env->t = done ? env->start : t1;
+  env->step_count = done ? 0 : env->step_count + 1;
+}
+
+void prb_pm_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
+                        double* d_term_ret, int32_t* d_term_len) {
+  PmStepArgs a;
+  a.N = (int)env->N;
+  a.actions = d_actions;
+  a.st = env->d_pm_state.p;
+  a.steps = env->d_pm_steps.p;
+  a.ep_return = env->d_ep_return.p;
+  a.mt = env->d_mt.p;
+  a.mt_idx = env->d_mt_idx.p;
+  a.obs = env->d_obs.p;
+  a.reward = d_reward;
+  a.done_out = d_done;
+  a.term_obs = d_term_obs;
+  a.term_ret = d_term_ret;
+  a.term_len = d_term_len;
+  const int grid = (int)((env->N + 255) / 256);
+  pm_step_kernel<<<grid, 256, 0, env->ctx->stream>>>(a);
+  PRB_CHECK_LAUNCH();
+}
+
+void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
+                         double* d_term_ret, int32_t* d_term_len) {
+  PRB_REQUIRE(env->was_reset, PRB_ERR_DIMENSION, "vec_step: sub-environments have no state (call reset first)");
+  if (env->kind == PRB_KIND_STOCK)
+    prb_stock_step_launch(env, d_actions, d_reward, d_done, d_term_obs, d_term_ret, d_term_len);
+  else
+    prb_pm_step_launch(env, d_actions, d_reward, d_done, d_term_obs, d_term_ret, d_term_len);
+}
+
+extern "C" {
+
+int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t start, size_t end, size_t N,
+                            prb_vecenv* out) {
+  return guard([&] {
+    PRB_REQUIRE(m && cfg && out, PRB_ERR_USAGE, "prb_vecenv_create_stock: NULL argument");
+    PRB_REQUIRE(N > 0, PRB_ERR_CONFIG, "VectorizedEnvironment: num_envs must be > 0");           // env.hpp:170
+    PRB_REQUIRE(!m->indicators.empty(), PRB_ERR_USAGE,
+                "StockTradingEnv: market data lacks indicators; run compute_indicators");         // stock_env.hpp:140
+    PRB_REQUIRE(!(end >= m->T || start + 1 >= end + 1 || end <= start), PRB_ERR_CONFIG,
+                "StockTradingEnv: bad window [" + std::to_string(start) + ", " + std::to_string(end) + "] for " +
+                    std::to_string(m->T) + " rows");                                              // stock_env.hpp:143
+    PRB_REQUIRE(cfg->max_trade_shares * (double)(end - start) < 2.0e9, PRB_ERR_CONFIG,
+                "prb: max_trade_shares * episode length must stay below 2e9 (int32 share counts on device)");
+    PRB_REQUIRE(N < (size_t)1 << 31, PRB_ERR_CONFIG, "prb: num_envs must be < 2^31");
+    prb_ctx_s* ctx = m->ctx;
+    PRB_CUDA(cudaSetDevice(ctx->device));
+    auto* env = new prb_vecenv_s;
+    env->ctx = ctx;
+    env->kind = PRB_KIND_STOCK;
+    env->N = N;
+    const int K = m->K;
+    env->S = 1 + 6 * (size_t)K;
+    env->A = K;
+    env->action_low.assign(K, -1.0);
+    env->action_high.assign(K, 1.0);
+    env->max_episode_steps = end - start;
+    env->reward_target = 0.0;
+    env->market = m;
+    env->cfg = *cfg;
+    env->start = start;
+    env->end = end;
+    env->t = start;
+    // shared features per time index: close_k[t]/close_k[start] then indicator_i,k[t] (stock_env.hpp:122-129)
+    const size_t T = m->T, F = 5 * (size_t)K;
+    std::vector<float> feat(T * F);
+    for (size_t t = 0; t < T; ++t) {
+      for (int k = 0; k < K; ++k)
+        feat[t * F + k] = (float)(m->close[(size_t)k * T + t] / m->close[(size_t)k * T + start]);
+      for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < K; ++k) feat[t * F + K + (size_t)i * K + k] = (float)m->indicators[((size_t)i * K + k) * T + t];
+    }
+    env->d_feat.alloc(feat.size());
+    PRB_CUDA(cudaMemcpy(env->d_feat.p, feat.data(), feat.size() * sizeof(float), cudaMemcpyHostToDevice));
+    env->d_balance.alloc(N);
+    env->d_shares.alloc(N * K);
+    env->d_ep_return.alloc(N);
+    env->d_obs.alloc(N * env->S);
+    PRB_CUDA(cudaMemset(env->d_obs.p, 0, env->d_obs.bytes()));
+    *out = env;
+  });
+}
+
+int prb_vecenv_create_pointmass(prb_ctx ctx, size_t N, prb_vecenv* out) {
+  return guard([&] {
+    PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_vecenv_create_pointmass: NULL argument");
+    PRB_REQUIRE(N > 0, PRB_ERR_CONFIG, "VectorizedEnvironment: num_envs must be > 0");
+    PRB_REQUIRE(N < (size_t)1 << 31, PRB_ERR_CONFIG, "prb: num_envs must be < 2^31");
+    PRB_CUDA(cudaSetDevice(ctx->device));
+    auto* env = new prb_vecenv_s;
+    env->ctx = ctx;
+    env->kind = PRB_KIND_POINTMASS;
+    env->N = N;
+    env->S = 6;
+    env->A = 2;
+    env->action_low.assign(2, -1.0);
+    env->action_high.assign(2, 1.0);
+    env->max_episode_steps = 200;
+    env->reward_target = 5.0;
+    env->d_pm_state.alloc(6 * N);
+    env->d_pm_steps.alloc(N);
+    env->d_ep_return.alloc(N);
+    env->d_mt.alloc((size_t)kMtN * N);
+    env->d_mt_idx.alloc(N);
+    env->d_obs.alloc(N * 6);
+    PRB_CUDA(cudaMemset(env->d_obs.p, 0, env->d_obs.bytes()));
+    *out = env;
+  });
+}
+
+int prb_vecenv_destroy(prb_vecenv env) {
+  return guard([&] {
+    if (env) cudaStreamSynchronize(env->ctx->stream);
+    delete env;
+  });
+}
+
+int prb_vecenv_spec(prb_vecenv env, prb_env_spec* out) {
+  return guard([&] {
+    check_env(env);
+    out->state_dim = env->S;
+    out->action_dim = env->A;
+    out->max_episode_steps = env->max_episode_steps;
+    out->reward_target = env->reward_target;
+    out->action_low = env->action_low.data();
+    out->action_high = env->action_high.data();
+  });
+}
+
+size_t prb_vecenv_num_envs(prb_vecenv env) { return env ? env->N : 0; }
+const float* prb_vecenv_states_device(prb_vecenv env) { return env ? env->d_obs.p : nullptr; }
+
+int prb_vecenv_reset(prb_vecenv env, uint64_t seed, float* d_obs) {
+  return guard([&] {
+    check_env(env);
+    cudaStream_t s = env->ctx->stream;
+    const int N = (int)env->N;
+    if (env->kind == PRB_KIND_STOCK) {
+      env->t = env->start;
+      env->step_count = 0;
+      const int K = env->market->K;
+      const int grid = std::min<int>((N + 255) / 256, 4 * env->ctx->num_sms * 8);
+      stock_reset_kernel<<<std::max(grid, 1), 256, 0, s>>>(N, K, (int)env->S, env->cfg.initial_capital,
+                                                           env->d_feat.p + env->start * 5 * (size_t)K,
+                                                           env->d_balance.p, env->d_shares.p, env->d_ep_return.p,
+                                                           env->d_obs.p);
+    } else {
+      pm_reset_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, seed, env->d_pm_state.p, env->d_pm_steps.p,
+                                                      env->d_ep_return.p, env->d_mt.p, env->d_mt_idx.p, env->d_obs.p);
+    }
+    PRB_CHECK_LAUNCH();
+    env->was_reset = true;
+    if (d_obs && d_obs != env->d_obs.p)
+      PRB_CUDA(cudaMemcpyAsync(d_obs, env->d_obs.p, env->d_obs.bytes(), cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int prb_vecenv_step(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_terminal_obs,
+                    double* d_episode_return, int32_t* d_episode_length) {
+  return guard([&] {
+    check_env(env);
+    PRB_REQUIRE(d_actions, PRB_ERR_USAGE, "vec_step: actions is NULL");
+    prb_env_step_launch(env, d_actions, d_reward, d_done, d_terminal_obs, d_episode_return, d_episode_length);
+  });
+}
+
+int prb_vecenv_reset_host(prb_vecenv env, uint64_t seed, double* states) {
+  int rc = prb_vecenv_reset(env, seed, nullptr);
+  if (rc) return rc;
+  return prb_vecenv_states_host(env, states);
+}
+
+int prb_vecenv_states_host(prb_vecenv env, double* states) {
+  return guard([&] {
+    check_env(env);
+    const size_t n = env->N * env->S;
+    float* h = static_cast<float*>(env->ctx->pinned_staging(n * sizeof(float)));
+    PRB_CUDA(cudaMemcpyAsync(h, env->d_obs.p, n * sizeof(float), cudaMemcpyDeviceToHost, env->ctx->stream));
+    env->ctx->sync();
+    for (size_t i = 0; i < n; ++i) states[i] = h[i];
+  });
+}
+
+int prb_vecenv_step_host(prb_vecenv env, const double* actions, double* next_states, double* rewards, uint8_t* dones,
+                         double* terminal_states, double* episode_returns, uint64_t* episode_lengths) {
+  return guard([&] {
+    check_env(env);
+    PRB_REQUIRE(actions, PRB_ERR_USAGE, "vec_step: actions is NULL");
+    const size_t N = env->N, S = env->S, A = env->A;
+    cudaStream_t s = env->ctx->stream;
+    if (env->d_act_scratch.n < N * A) env->d_act_scratch.alloc(N * A);
+    if (env->d_rew_scratch.n < N) env->d_rew_scratch.alloc(N);
+    if (env->d_done_scratch.n < N) env->d_done_scratch.alloc(N);
+    if (env->d_term_scratch.n < N * S) env->d_term_scratch.alloc(N * S);
+    if (env->d_tret_scratch.n < N) env->d_tret_scratch.alloc(N);
+    if (env->d_tlen_scratch.n < N) env->d_tlen_scratch.alloc(N);
+    const size_t stage = std::max(N * A, N * S) * sizeof(float) + N * (sizeof(float) + 1 + 8 + 4) + 64;
+    char* h = static_cast<char*>(env->ctx->pinned_staging(stage));
+    float* hf = reinterpret_cast<float*>(h);
+    for (size_t i = 0; i < N * A; ++i) hf[i] = (float)actions[i];
+    PRB_CUDA(cudaMemcpyAsync(env->d_act_scratch.p, hf, N * A * sizeof(float), cudaMemcpyHostToDevice, s));
+    prb_env_step_launch(env, env->d_act_scratch.p, env->d_rew_scratch.p, env->d_done_scratch.p, env->d_term_scratch.p,
+                        env->d_tret_scratch.p, env->d_tlen_scratch.p);
+    // small outputs first
+    float* h_rew = reinterpret_cast<float*>(h + std::max(N * A, N * S) * sizeof(float));
+    uint8_t* h_done = reinterpret_cast<uint8_t*>(h_rew + N);
+    PRB_CUDA(cudaMemcpyAsync(h_rew, env->d_rew_scratch.p, N * sizeof(float), cudaMemcpyDeviceToHost, s));
+    PRB_CUDA(cudaMemcpyAsync(h_done, env->d_done_scratch.p, N, cudaMemcpyDeviceToHost, s));
+    env->ctx->sync();
+    bool any_done = false;
+    for (size_t i = 0; i < N; ++i) {
+      if (rewards) rewards[i] = h_rew[i];
+      if (dones) dones[i] = h_done[i];
+      any_done |= h_done[i] != 0;
+    }
+    if (any_done && (terminal_states || episode_returns || episode_lengths)) {
+      std::vector<float> term(N * S);
+      std::vector<double> tret(N);
+      std::vector<int32_t> tlen(N);
+      PRB_CUDA(cudaMemcpyAsync(term.data(), env->d_term_scratch.p, N * S * sizeof(float), cudaMemcpyDeviceToHost, s));
+      PRB_CUDA(cudaMemcpyAsync(tret.data(), env->d_tret_scratch.p, N * sizeof(double), cudaMemcpyDeviceToHost, s));
+      PRB_CUDA(cudaMemcpyAsync(tlen.data(), env->d_tlen_scratch.p, N * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      env->ctx->sync();
+      for (size_t i = 0; i < N; ++i) {
+        if (!h_done[i]) continue;
+        if (terminal_states)
+          for (size_t j = 0; j < S; ++j) terminal_states[i * S + j] = term[i * S + j];
+        if (episode_returns) episode_returns[i] = tret[i];
+        if (episode_lengths) episode_lengths[i] = (uint64_t)tlen[i];
+      }
+    }
+    if (next_states) {
+      PRB_CUDA(cudaMemcpyAsync(hf, env->d_obs.p, N * S * sizeof(float), cudaMemcpyDeviceToHost, s));
+      env->ctx->sync();
+      for (size_t i = 0; i < N * S; ++i) next_states[i] = hf[i];
+    }
+  });
+}
+
+int prb_vecenv_step_counts_host(prb_vecenv env, uint64_t* out) {
+  return guard([&] {
+    check_env(env);
+    if (env->kind == PRB_KIND_STOCK) {
+      for (size_t i = 0; i < env->N; ++i) out[i] = env->step_count;
+    } else {
+      std::vector<int32_t> st(env->N);
+      PRB_CUDA(cudaMemcpyAsync(st.data(), env->d_pm_steps.p, env->N * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                               env->ctx->stream));
+      env->ctx->sync();
+      for (size_t i = 0; i < env->N; ++i) out[i] = (uint64_t)st[i];
+    }
+  });
+}
+
+}  // extern "C"

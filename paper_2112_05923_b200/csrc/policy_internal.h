@@ -1,0 +1,48 @@
+// policy_internal.h -- launch descriptors shared by policy.cu / rollout.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "mlp_simt.cuh"
+#include "prb_internal.h"
+
+enum PolicyMode : int {
+  kPolicySample = 0,     // Philox noise
+  kPolicyEpsIn = 1,      // injected unit normals
+  kPolicyMean = 2,       // policy_mean
+  kPolicyLogProb = 3,    // gaussian_log_prob of given actions
+  kPolicyValueOnly = 4,  // critic only
+};
+
+struct PolicyArgs {
+  const float* params;
+  prb::MlpDesc actor, critic;
+  int log_std_off;
+  int A;
+  int ldw;
+  int rows_per_cta;
+  int mode;
+  const float* states;  // [n][S]
+  size_t n;
+  uint64_t seed, counter;
+  const float* eps_in;
+  const float* actions_in;
+  float* actions;
+  float* log_probs;
+  float* values;
+  float* eps_out;
+  float* mean_out;
+  float* obs_store;  // optional: first store_cols of every state row
+  int store_cols;
+  int32_t* status;
+};
+
+PolicyArgs prb_policy_args(prb_agent a, const float* d_states, size_t n);
+size_t prb_policy_smem(const PolicyArgs& p);
+void prb_policy_launch(const PolicyArgs& p, cudaStream_t s);
+void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
+                         double* d_term_ret, int32_t* d_term_len);
+void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s);
+void prb_agent_finite_gate_and_adam(prb_agent a, const float* d_grads, cudaStream_t s);

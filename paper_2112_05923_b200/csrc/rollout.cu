@@ -1,0 +1,226 @@
+// rollout.cu -- the device TransitionBuffer (buffer.hpp:27-135) and
+// worker_collect (pod.hpp:95-132).
+//
+// Storage is time-major: transition (env e, step h) at h*N + e, so every step
+// of the collection loop writes one contiguous slab.  For the stock env the
+// 181-float observation is stored compactly: its per-env part (balance/cap,
+// shares: 1+K floats) per transition, and the 5K shared features once per
+// step as a time index into the env's read-only feature table (all envs of a
+// VecEnv share t, stock_env.hpp:161) -- 124 B instead of 724 B per transition.
+#include <algorithm>
+#include <cstring>
+
+#include "policy_internal.h"
+#include "prb_internal.h"
+
+using namespace prb;
+
+namespace {
+
+void alloc_rollout(prb_rollout_s* r) {
+  const size_t cap = r->N * r->H;
+  r->d_obs.alloc(cap * r->Sp);
+  r->d_row.alloc(r->H);
+  r->d_act.alloc(cap * r->A);
+  r->d_logp.alloc(cap);
+  r->d_rew.alloc(cap);
+  r->d_val.alloc(cap);
+  r->d_adv.alloc(cap);
+  r->d_ret.alloc(cap);
+  r->d_done.alloc(cap);
+  r->d_boot.alloc(r->N);
+  r->d_advstat.alloc(2);
+}
+
+}  // namespace
+
+void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8_t* done, const float* boot, size_t N,
+                    size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize);
+
+extern "C" {
+
+int prb_rollout_create(prb_vecenv env, size_t horizon, prb_rollout* out) {
+  return guard([&] {
+    PRB_REQUIRE(env && out, PRB_ERR_USAGE, "prb_rollout_create: NULL argument");
+    PRB_REQUIRE(horizon > 0, PRB_ERR_CONFIG, "pod.rollout_horizon must be > 0");
+    PRB_REQUIRE(env->N * horizon < ((size_t)1 << 32), PRB_ERR_CONFIG, "prb_rollout_create: N*H must be < 2^32");
+    auto* r = new prb_rollout_s;
+    r->ctx = env->ctx;
+    r->N = env->N;
+    r->H = horizon;
+    r->S = env->S;
+    r->A = env->A;
+    if (env->kind == PRB_KIND_STOCK) {
+      r->obs_mode = 1;
+      r->K = env->market->K;
+      r->Sp = 1 + (size_t)r->K;
+      r->d_feat = env->d_feat.p;
+    } else {
+      r->obs_mode = 0;
+      r->Sp = env->S;
+    }
+    alloc_rollout(r);
+    *out = r;
+  });
+}
+
+int prb_rollout_create_raw(prb_ctx ctx, size_t N, size_t H, size_t S, size_t A, prb_rollout* out) {
+  return guard([&] {
+    PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_rollout_create_raw: NULL argument");
+    PRB_REQUIRE(N > 0 && H > 0 && S > 0 && A > 0, PRB_ERR_CONFIG, "prb_rollout_create_raw: zero dimension");
+    PRB_REQUIRE(N * H < ((size_t)1 << 32), PRB_ERR_CONFIG, "prb_rollout_create_raw: N*H must be < 2^32");
+    auto* r = new prb_rollout_s;
+    r->ctx = ctx;
+    r->N = N;
+    r->H = H;
+    r->S = S;
+    r->A = A;
+    r->obs_mode = 0;
+    r->Sp = S;
+    alloc_rollout(r);
+    *out = r;
+  });
+}
+
+int prb_rollout_destroy(prb_rollout r) {
+  return guard([&] {
+    if (r) cudaStreamSynchronize(r->ctx->stream);
+    delete r;
+  });
+}
+
+int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed) {
+  return guard([&] {
+    PRB_REQUIRE(r && a && env, PRB_ERR_USAGE, "worker_collect: NULL argument");
+    PRB_REQUIRE(env->N == r->N && env->S == r->S && env->A == r->A && a->S == env->S && a->A == env->A,
+                PRB_ERR_USAGE, "worker_collect: rollout/agent/env shapes disagree");
+    PRB_REQUIRE(env->was_reset, PRB_ERR_DIMENSION, "vec_step: sub-environments have no state (call reset first)");
+    const bool compact = env->kind == PRB_KIND_STOCK;
+    if (compact) {
+      if (r->obs_mode != 1) {  // an upload switched the buffer to full rows; switch back
+        r->obs_mode = 1;
+        r->K = env->market->K;
+        r->Sp = 1 + (size_t)r->K;
+        r->d_obs.alloc(r->N * r->H * r->Sp);
+      }
+      r->d_feat = env->d_feat.p;
+    }
+    cudaStream_t s = r->ctx->stream;
+    const size_t N = r->N, H = r->H, A = r->A;
+    std::vector<int32_t> rows(H);
+    for (size_t h = 0; h < H; ++h) {
+      if (compact) rows[h] = (int32_t)env->t;
+      PolicyArgs p = prb_policy_args(a, env->d_obs.p, N);
+      p.mode = kPolicySample;
+      p.seed = seed;
+      p.counter = h;
+      p.actions = r->d_act.p + h * N * A;
+      p.log_probs = r->d_logp.p + h * N;
+      p.values = r->d_val.p + h * N;
+      p.obs_store = r->d_obs.p + h * N * r->Sp;
+      p.store_cols = (int)r->Sp;
+      p.status = nullptr;
+      prb_policy_launch(p, s);
+      prb_env_step_launch(env, p.actions, r->d_rew.p + h * N, r->d_done.p + h * N, nullptr, nullptr, nullptr);
+    }
+    // bootstrap V(s_H) (pod.hpp:127-131)
+    PolicyArgs p = prb_policy_args(a, env->d_obs.p, N);
+    p.mode = kPolicyValueOnly;
+    p.values = r->d_boot.p;
+    p.status = nullptr;
+    prb_policy_launch(p, s);
+    if (compact) PRB_CUDA(cudaMemcpyAsync(r->d_row.p, rows.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    r->ctx->sync();  // rows[] lives on this stack frame
+    r->full = true;
+    r->gae_valid = false;
+  });
+}
+
+int prb_rollout_download(prb_rollout r, double* states, double* actions, double* log_probs, double* rewards,
+                         uint8_t* dones, double* values, double* bootstrap) {
+  return guard([&] {
+    PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_download: NULL rollout");
+    const size_t N = r->N, H = r->H, n = N * H, S = r->S, A = r->A, Sp = r->Sp;
+    cudaStream_t s = r->ctx->stream;
+    auto pull = [&](const auto* d, size_t count, auto& h) {
+      h.resize(count);
+      PRB_CUDA(cudaMemcpyAsync(h.data(), d, count * sizeof(*d), cudaMemcpyDeviceToHost, s));
+    };
+    std::vector<float> obs, act, lp, rw, vl, bt, feat;
+    std::vector<uint8_t> dn;
+    std::vector<int32_t> rows;
+    if (states) pull(r->d_obs.p, n * Sp, obs);
+    if (states && r->obs_mode == 1) {
+      pull(r->d_row.p, H, rows);
+      r->ctx->sync();
+      int32_t tmax = 0;
+      for (int32_t t : rows) tmax = std::max(tmax, t);
+      pull(r->d_feat, (size_t)(tmax + 1) * 5 * r->K, feat);
+    }
+    if (actions) pull(r->d_act.p, n * A, act);
+    if (log_probs) pull(r->d_logp.p, n, lp);
+    if (rewards) pull(r->d_rew.p, n, rw);
+    if (values) pull(r->d_val.p, n, vl);
+    if (dones) pull(r->d_done.p, n, dn);
+    if (bootstrap) pull(r->d_boot.p, N, bt);
+    r->ctx->sync();
+    const size_t F = 5 * (size_t)r->K;
+    for (size_t e = 0; e < N; ++e)
+      for (size_t h = 0; h < H; ++h) {
+        const size_t j = h * N + e, i = e * H + h;  // device time-major -> reference env-major
+        if (states) {
+          for (size_t c = 0; c < Sp; ++c) states[i * S + c] = obs[j * Sp + c];
+          if (r->obs_mode == 1)
+            for (size_t c = 0; c < F; ++c) states[i * S + Sp + c] = feat[(size_t)rows[h] * F + c];
+        }
+        if (actions)
+          for (size_t c = 0; c < A; ++c) actions[i * A + c] = act[j * A + c];
+        if (log_probs) log_probs[i] = lp[j];
+        if (rewards) rewards[i] = rw[j];
+        if (values) values[i] = vl[j];
+        if (dones) dones[i] = dn[j];
+      }
+    if (bootstrap)
+      for (size_t e = 0; e < N; ++e) bootstrap[e] = bt[e];
+  });
+}
+
+int prb_rollout_upload(prb_rollout r, const double* states, const double* actions, const double* log_probs,
+                       const double* rewards, const uint8_t* dones, const double* values, const double* bootstrap) {
+  return guard([&] {
+    PRB_REQUIRE(r && states && actions && log_probs && rewards && dones && values && bootstrap, PRB_ERR_USAGE,
+                "prb_rollout_upload: NULL argument");
+    const size_t N = r->N, H = r->H, n = N * H, S = r->S, A = r->A;
+    if (r->obs_mode != 0) {
+      r->obs_mode = 0;
+      r->Sp = S;
+      r->d_obs.alloc(n * S);
+    }
+    std::vector<float> obs(n * S), act(n * A), lp(n), rw(n), vl(n), bt(N);
+    std::vector<uint8_t> dn(n);
+    for (size_t e = 0; e < N; ++e)
+      for (size_t h = 0; h < H; ++h) {
+        const size_t j = h * N + e, i = e * H + h;
+        for (size_t c = 0; c < S; ++c) obs[j * S + c] = (float)states[i * S + c];
+        for (size_t c = 0; c < A; ++c) act[j * A + c] = (float)actions[i * A + c];
+        lp[j] = (float)log_probs[i];
+        rw[j] = (float)rewards[i];
+        vl[j] = (float)values[i];
+        dn[j] = dones[i] ? 1 : 0;
+      }
+    for (size_t e = 0; e < N; ++e) bt[e] = (float)bootstrap[e];
+    cudaStream_t s = r->ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(r->d_obs.p, obs.data(), obs.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_act.p, act.data(), act.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_logp.p, lp.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_rew.p, rw.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_val.p, vl.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_done.p, dn.data(), n, cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_boot.p, bt.data(), N * sizeof(float), cudaMemcpyHostToDevice, s));
+    r->ctx->sync();
+    r->full = true;
+    r->gae_valid = false;
+  });
+}
+
+}  // extern "C"
