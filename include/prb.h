@@ -192,6 +192,9 @@ PRB_API int prb_rollout_upload(prb_rollout r, const double* states, const double
 PRB_API int prb_gae(prb_rollout r, double gamma, double lambda, int normalize);
 /* Normalised advantages and returns in the reference index space. */
 PRB_API int prb_gae_download(prb_rollout r, double* advantages, double* returns);
+/* Seam: set the (already normalised) advantages and returns directly, in the
+ * reference index space -- the inputs gather_minibatch (ppo.hpp:83-103) reads. */
+PRB_API int prb_rollout_set_advantages(prb_rollout r, const double* advantages, const double* returns);
 /* compute_gae over raw device arrays in TIME-MAJOR layout [H][N]. */
 PRB_API int prb_compute_gae(prb_ctx ctx, const float* d_rewards, const float* d_values, const uint8_t* d_dones,
                             const float* d_bootstrap, size_t num_envs, size_t horizon, double gamma, double lambda,

@@ -150,6 +150,7 @@ SIGNATURES = {
     "prb_rollout_upload": (I, [P, pD, pD, pD, pD, pU8, pD, pD]),
     "prb_gae": (I, [P, D, D, I]),
     "prb_gae_download": (I, [P, pD, pD]),
+    "prb_rollout_set_advantages": (I, [P, pD, pD]),
     "prb_compute_gae": (I, [P, P, P, P, P, SZ, SZ, D, D, P, P]),
     "prb_ppo_update": (I, [P, P, C.POINTER(PpoConfig), U64, pU64, P, C.POINTER(PpoStats)]),
     "prb_ppo_loss_grads": (I, [P, P, pU64, SZ, C.POINTER(PpoConfig), pD, pD]),

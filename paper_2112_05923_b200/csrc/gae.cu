@@ -167,4 +167,24 @@ int prb_gae_download(prb_rollout r, double* advantages, double* returns) {
   });
 }
 
+int prb_rollout_set_advantages(prb_rollout r, const double* advantages, const double* returns) {
+  return guard([&] {
+    PRB_REQUIRE(r && advantages && returns, PRB_ERR_USAGE, "prb_rollout_set_advantages: NULL argument");
+    const size_t N = r->N, H = r->H, n = N * H;
+    std::vector<float> a(n), t(n);
+    for (size_t e = 0; e < N; ++e)
+      for (size_t h = 0; h < H; ++h) {
+        a[h * N + e] = (float)advantages[e * H + h];
+        t[h * N + e] = (float)returns[e * H + h];
+      }
+    const double st[2] = {0.0, 1.0};
+    cudaStream_t s = r->ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(r->d_adv.p, a.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_ret.p, t.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_advstat.p, st, sizeof(st), cudaMemcpyHostToDevice, s));
+    r->ctx->sync();
+    r->gae_valid = true;
+  });
+}
+
 }  // extern "C"

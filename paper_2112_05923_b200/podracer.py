@@ -465,6 +465,12 @@ class Rollout:
         self.ctx.lib.prb_gae_download(self.h, _p(adv, C.c_double), _p(ret, C.c_double))
         return adv, ret
 
+    def set_advantages(self, advantages, returns):
+        """Seam: gather_minibatch inputs (already-normalised advantages, returns)."""
+        a = np.ascontiguousarray(advantages, dtype=np.float64)
+        r = np.ascontiguousarray(returns, dtype=np.float64)
+        self.ctx.lib.prb_rollout_set_advantages(self.h, _p(a, C.c_double), _p(r, C.c_double))
+
     def ppo_loss_grads(self, agent: Agent, rows, cfg: PpoConfig):
         rows = np.ascontiguousarray(rows, dtype=np.uint64)
         g = np.zeros(agent.param_count)
