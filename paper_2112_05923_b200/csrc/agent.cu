@@ -44,16 +44,18 @@ void layout(prb_agent_s* a) {
 // adam_step nn.hpp:164-182 on device; gate[0] != 0 aborts without touching state.
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, size_t n, const int64_t* __restrict__ t_dev,
-                            const int32_t* __restrict__ gate, float lr, float b1, float b2, float eps) {
+                            const int32_t* __restrict__ gate, float lr, double b1d, double b2d, float eps) {
   if (gate && gate[0] != 0) return;
   const int64_t t = *t_dev;  // already advanced by the producer of g
-  const double bc1 = 1.0 - pow((double)b1, (double)t);
-  const double bc2 = 1.0 - pow((double)b2, (double)t);
+  const double bc1 = 1.0 - pow(b1d, (double)t);
+  const double bc2 = 1.0 - pow(b2d, (double)t);
   const float ibc1 = (float)(1.0 / bc1), ibc2 = (float)(1.0 / bc2);
+  // constants rounded once from fp64 (1 - beta2 in fp32 arithmetic would be off by 1e-5 relative)
+  const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
-    const float mi = b1 * m[i] + (1.0f - b1) * gi;
-    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    const float mi = b1 * m[i] + omb1 * gi;
+    const float vi = b2 * v[i] + omb2 * gi * gi;
     m[i] = mi;
     v[i] = vi;
     p[i] -= lr * (mi * ibc1) / (sqrtf(vi * ibc2) + eps);
@@ -138,14 +140,14 @@ void prb_agent_finite_gate_and_adam(prb_agent a, const float* d_grads, cudaStrea
   finite_check_kernel<<<1, 1024, 0, s>>>(d_grads, a->P, a->d_status.p, a->d_t.p);
   const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
   adam_kernel<<<grid, 256, 0, s>>>(a->d_params.p, d_grads, a->d_m.p, a->d_v.p, a->P, a->d_t.p, a->d_status.p,
-                                   (float)a->lr, (float)a->beta1, (float)a->beta2, (float)a->eps);
+                                   (float)a->lr, a->beta1, a->beta2, (float)a->eps);
   PRB_CHECK_LAUNCH();
 }
 
 void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s) {
   const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
   adam_kernel<<<grid, 256, 0, s>>>(a->d_params.p, d_grads, a->d_m.p, a->d_v.p, a->P, a->d_t.p, gate, (float)a->lr,
-                                   (float)a->beta1, (float)a->beta2, (float)a->eps);
+                                   a->beta1, a->beta2, (float)a->eps);
   PRB_CHECK_LAUNCH();
 }
 
