@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark: env transitions/s of the stock-trading pod rollout on B200.
+
+Contract (see the task statement): ``python bench.py --gpus N --steps K
+--warmup W`` (torchrun for N > 1, one rank per GPU) prints ONE JSON line on
+rank 0.  A step is one rollout collection (worker_collect, pod.hpp:95-132) of
+BASELINE.json configs[1]: 30-asset stock-trading VecEnv x 65,536 envs per GPU,
+horizon 256 (16.8M transitions/GPU/step): actor+critic forward, Philox
+sampling, env step, rollout-buffer writes and the bootstrap values.  The same
+run also measures the env-step kernel alone, one full PPO update on the
+collected buffer (GAE + 4 epochs x 1,024-row minibatches + Adam), the
+end-to-end public-API path with host buffers, and the reference CPU path
+(oracle/_ref, the unmodified reference headers) on the host cores.
+
+``--impl reference`` times only the reference CPU implementation (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env transitions/sec (1/2/4/8 B200, device-timed) vs host-CPU ref; % HBM roofline"
+UNIT = "transitions/s"
+K_ASSETS, T_ROWS, MARKET_SEED = 30, 2048, 2112
+S_DIM = 1 + 6 * K_ASSETS
+# algorithmic work per transition
+ENV_BYTES = 36 * K_ASSETS + 41  # action 4K + balance 16 + shares 8K + ep_return 16 + obs 4(1+6K) + reward 4 + done 1
+MLP_FLOPS = 2 * (181 * 64 + 64 * 64 + 64 * 30) + 2 * (181 * 64 + 64 * 64 + 64 * 1)  # 66,688
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.torch:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.torch:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.torch:
+            self.dist.destroy_process_group()
+
+
+def market_arrays():
+    from paper_2112_05923_b200 import podracer as pr
+    m = pr.synthetic_market(K_ASSETS, T_ROWS, MARKET_SEED)
+    ind = pr.compute_indicators(m["high"], m["low"], m["close"])
+    return m, ind
+
+
+def cpu_reference_rate(m, ind, seconds: float, envs_per_worker: int = 64, horizon: int = 32):
+    """The reference's own worker_collect (pod.hpp:408-433: one VecEnv per
+    thread, disjoint buffer segments) on this box's host cores, built from the
+    unmodified headers (oracle/_ref/libpodracer_ref_bench.so)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import REF_BENCH_SO, load_ref, ptr, SZ
+    ref = load_ref(REF_BENCH_SO)
+    if ref is None:
+        return None
+    from paper_2112_05923_b200 import podracer as pr
+    cores = os.cpu_count() or 1
+    W = 1 << (cores.bit_length() - 1)  # largest power of two <= cores
+    flat = pr.artifact_init(S_DIM, K_ASSETS, 7)
+    hid = np.array([64, 64], dtype=np.uint64)
+    close = np.ascontiguousarray(m["close"]); indc = np.ascontiguousarray(ind)
+    total_s, total_tr, reps = 0.0, 0, 0
+    while total_s < seconds or reps < 1:
+        dt = ref.ref_bench_collect(ptr(close), ptr(indc), T_ROWS, K_ASSETS, 0, T_ROWS - 1, W, envs_per_worker,
+                                   horizon, ptr(flat), ptr(hid, SZ), 2, 2112 + reps)
+        total_s += dt
+        total_tr += W * envs_per_worker * horizon
+        reps += 1
+    return {"value": total_tr / total_s, "unit": UNIT, "cores": W, "kind": "reference",
+            "sample": f"worker_collect x{reps}: {W} threads x {envs_per_worker} stock envs x horizon {horizon} "
+                      f"({total_tr} transitions, {total_s:.1f} s), 64x64 actor/critic, f64, -O3 -march=x86-64-v3"}
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    m, ind = market_arrays()
+    # each step = one bounded sample of the configs[1] workload on the host cores
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_rate(m, ind, seconds=0.0)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"}))
+            return
+        if i >= args.warmup:
+            rates.append(r)
+    value = float(np.mean([r["value"] for r in rates]))
+    cb = dict(rates[-1])
+    cb["value"] = value
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_dict(args), "cpu_baseline": cb,
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def config_dict(args):
+    return {"workload": f"configs[1]: single-pod PPO rollout, stock-trading VecEnv {K_ASSETS} assets x "
+                        f"{args.envs} envs/GPU, horizon {args.horizon}",
+            "assets": K_ASSETS, "envs_per_gpu": args.envs, "horizon": args.horizon, "market_rows": T_ROWS,
+            "actor_critic": "181-64-64-30 / 181-64-64-1 tanh", "parallelism": f"replicas x{args.gpus} (one pod per GPU)",
+            "l2": "no flush: each step writes a %.1f GB rollout buffer >> 126 MB L2" % (
+                args.envs * args.horizon * (4 * (1 + K_ASSETS) + 4 * K_ASSETS + 13) / 1e9)}
+
+
+def run_ours(args, d: Dist):
+    from paper_2112_05923_b200 import podracer as pr
+    lib = pr._lib.lib()
+    hbm, bf16, bf16_sus, peak_src = load_peaks()
+    ctx = pr.Context(d.local)
+    m, ind = market_arrays()
+    market = pr.MarketData(ctx, m["close"], ind)
+    cfg = pr.StockConfig()
+    N, H = args.envs, args.horizon
+    env = pr.VectorizedEnvironment.stock(ctx, market, cfg, 0, T_ROWS - 1, N)
+    env.reset(2112 + d.rank)
+    agent = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=7 + d.rank)
+    ro = pr.Rollout.for_env(env, H)
+
+    # ---- warm-up ----
+    for i in range(args.warmup):
+        ro.collect(agent, env, seed=1000 + i)
+    ctx.synchronize()
+
+    # ---- timed region: K rollout collections, device events on the launching stream ----
+    lib.prb_ctx_profile(ctx.h, 1)
+    clocks = ClockSampler(d.local)
+    d.barrier()
+    ctx.synchronize()
+    clocks.start()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        ro.collect(agent, env, seed=2000 + i)
+    ctx.synchronize()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    prof = {}
+    for name, kind in (("policy_fwd_sample", 0), ("env_stock_step", 1)):
+        ms, n = C.c_double(), C.c_uint64()
+        lib.prb_ctx_profile_read(ctx.h, kind, C.byref(ms), C.byref(n))
+        prof[name] = (ms.value, n.value)
+    lib.prb_ctx_profile(ctx.h, 0)
+    # device time of the region = sum of the stream's kernel intervals is a lower bound; the
+    # stream is serial, so the region's device duration is measured by events around it:
+    dev_ms = time_region(lib, ctx, lambda: [ro.collect(agent, env, seed=3000 + i) for i in range(args.steps)])
+    d.barrier()
+    dev_ms = d.max(dev_ms)
+    transitions = d.world * args.steps * N * H
+    value = transitions / (dev_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (per-launch work / average launch time) ----
+    kernels = {}
+    pol_ms, pol_n = prof["policy_fwd_sample"]
+    env_ms, env_n = prof["env_stock_step"]
+    kernels["policy_fwd_sample"] = {"ms_total": pol_ms, "launches": pol_n, "share": pol_ms / (wall * 1e3),
+                                    "bound": "tensor", "unit": "TFLOP/s",
+                                    "achieved": (N * MLP_FLOPS) / (pol_ms / max(pol_n, 1) / 1e3) / 1e12,
+                                    "peak": bf16_sus}
+    kernels["env_stock_step"] = {"ms_total": env_ms, "launches": env_n, "share": env_ms / (wall * 1e3),
+                                 "bound": "hbm", "unit": "GB/s",
+                                 "achieved": (N * ENV_BYTES) / (env_ms / max(env_n, 1) / 1e3) / 1e9, "peak": hbm}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
+    kd = kernels[dom]
+    roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
+                "unit": kd["unit"], "frac": kd["achieved"] / kd["peak"], "traffic": None,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json {'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
+    for k in kernels.values():
+        k["frac"] = k["achieved"] / k["peak"]
+
+    # ---- env step alone (the VecEnv boundary), device actions resident ----
+    d_act = C.c_void_p()
+    lib.prb_rollout_device_fields(ro.h, None, C.byref(d_act), None, None, None, None, None)
+    d_rew, d_done = ctx.alloc((N,)), ctx.alloc((N,), np.uint8)
+    env.reset(5)
+    n_env_steps = 200
+    env_ms_total = time_region(lib, ctx, lambda: [env.step_device(d_act.value + (i % H) * N * K_ASSETS * 4,
+                                                                  d_rew.ptr, d_done.ptr)
+                                                  for i in range(n_env_steps)])
+    env_rate = N * n_env_steps / (env_ms_total / 1e3)
+    env_step = {"value": d.world * env_rate if d.world > 1 else env_rate, "unit": UNIT,
+                "achieved_gbs": env_rate * ENV_BYTES / 1e9, "frac_hbm": env_rate * ENV_BYTES / 1e9 / hbm,
+                "bytes_per_transition": ENV_BYTES, "steps": n_env_steps}
+
+    # ---- one full PPO update on the collected buffer (GAE + epochs x minibatches + Adam) ----
+    ppo = None
+    if not args.skip_ppo:
+        pcfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=args.ppo_epochs, buffer_size=N * H)
+        out_agent = pr.Agent(ctx, S_DIM, K_ASSETS)
+        res = {}
+
+        def upd():
+            res["stats"] = pr.ppo_update(agent, ro, pcfg, seed=9, out=out_agent)[1]
+        ppo_ms = time_region(lib, ctx, upd)
+        coll_ms = dev_ms / args.steps
+        st = res["stats"]
+        ppo = {"update_ms": ppo_ms, "minibatches": st.minibatches, "ms_per_minibatch": ppo_ms / max(st.minibatches, 1),
+               "epochs": args.ppo_epochs, "minibatch_size": 1024,
+               "iteration_transitions_per_s": N * H / ((coll_ms + ppo_ms) / 1e3),
+               "mean_policy_loss": st.mean_policy_loss, "mean_value_loss": st.mean_value_loss}
+
+    # ---- end to end through the public API with host buffers ----
+    P = agent.param_count
+    host_params = np.ascontiguousarray(agent.flatten_params().astype(np.float32))
+    host_rew = np.zeros(N * H, dtype=np.float32)
+    d_params = lib.prb_agent_params_device(agent.h)
+    d_rw = C.c_void_p()
+    lib.prb_rollout_device_fields(ro.h, None, None, None, C.byref(d_rw), None, None, None)
+    pin = pinned(host_params.nbytes + host_rew.nbytes)
+    hp = np.frombuffer(pin, dtype=np.float32, count=P)
+    hr = np.frombuffer(pin, dtype=np.float32, count=N * H, offset=host_params.nbytes)
+    hp[:] = host_params
+
+    def e2e_steps():
+        for i in range(args.steps):
+            lib.prb_memcpy_h2d_async(ctx.h, d_params, hp.ctypes.data, hp.nbytes)
+            lib.prb_rollout_collect(ro.h, agent.h, env.h, 4000 + i)
+            lib.prb_memcpy_d2h_async(ctx.h, hr.ctypes.data, d_rw.value, hr.nbytes)
+        ctx.synchronize()
+    d.barrier()
+    t0 = time.perf_counter()
+    e2e_steps()
+    e2e_s = d.max(time.perf_counter() - t0)
+    e2e = {"value": transitions / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hp.nbytes),
+           "d2h_bytes_per_step": int(hr.nbytes), "note": "host wall clock incl. pinned h2d params + d2h rewards"}
+
+    # ---- CPU baseline: the reference path on this box's host cores (rank 0, N=1 only) ----
+    cpu = None
+    if d.rank == 0 and d.world == 1 and not args.skip_cpu:
+        cpu = cpu_reference_rate(m, ind, seconds=args.cpu_seconds)
+
+    launches = args.steps * (2 * H + 1)
+    if d.rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32 (MLP, obs) + f64 (portfolio accounting)",
+               "data": "synthetic (BASELINE.md §3 market, random-init artifact_init weights)",
+               "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
+               "ppo_update": ppo, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+               "wall_s_profiled_region": wall}
+        print(json.dumps(out))
+    d.close()
+
+
+def time_region(lib, ctx, fn) -> float:
+    """Device milliseconds of everything fn() enqueues on ctx's stream (CUDA events, sync both sides)."""
+    cudart = _cudart()
+    stream = C.c_void_p(ctx.stream)
+    a, b = C.c_void_p(), C.c_void_p()
+    cudart.cudaEventCreate(C.byref(a))
+    cudart.cudaEventCreate(C.byref(b))
+    ctx.synchronize()
+    cudart.cudaEventRecord(a, stream)
+    fn()
+    cudart.cudaEventRecord(b, stream)
+    cudart.cudaEventSynchronize(b)
+    ms = C.c_float()
+    cudart.cudaEventElapsedTime(C.byref(ms), a, b)
+    cudart.cudaEventDestroy(a)
+    cudart.cudaEventDestroy(b)
+    return float(ms.value)
+
+
+_CUDART = None
+
+
+def _cudart():
+    global _CUDART
+    if _CUDART is None:
+        for name in ("libcudart.so.12", "libcudart.so", "/usr/local/cuda/lib64/libcudart.so.12"):
+            try:
+                _CUDART = C.CDLL(name)
+                break
+            except OSError:
+                continue
+        if _CUDART is None:
+            raise RuntimeError("libcudart not found")
+        _CUDART.cudaEventRecord.argtypes = [C.c_void_p, C.c_void_p]
+        _CUDART.cudaEventSynchronize.argtypes = [C.c_void_p]
+        _CUDART.cudaEventElapsedTime.argtypes = [C.POINTER(C.c_float), C.c_void_p, C.c_void_p]
+        _CUDART.cudaEventDestroy.argtypes = [C.c_void_p]
+        _CUDART.cudaHostAlloc.argtypes = [C.POINTER(C.c_void_p), C.c_size_t, C.c_uint]
+    return _CUDART
+
+
+def pinned(nbytes: int):
+    p = C.c_void_p()
+    rc = _cudart().cudaHostAlloc(C.byref(p), nbytes, 0)
+    if rc != 0:
+        raise RuntimeError(f"cudaHostAlloc failed ({rc})")
+    return (C.c_char * nbytes).from_address(p.value)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--envs", type=int, default=65536)
+    ap.add_argument("--horizon", type=int, default=256)
+    ap.add_argument("--ppo-epochs", type=int, default=4)
+    ap.add_argument("--skip-ppo", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    d = Dist()
+    if args.impl == "reference":
+        run_reference(args, d)
+        d.close()
+        return
+    run_ours(args, d)
+
+
+if __name__ == "__main__":
+    main()

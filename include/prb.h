@@ -65,6 +65,20 @@ PRB_API int prb_memcpy_h2d(prb_ctx ctx, void* d_dst, const void* src, size_t byt
 PRB_API int prb_memcpy_d2h(prb_ctx ctx, void* dst, const void* d_src, size_t bytes); /* synchronous */
 PRB_API int prb_memcpy_h2d_async(prb_ctx ctx, void* d_dst, const void* src, size_t bytes);
 PRB_API int prb_memcpy_d2h_async(prb_ctx ctx, void* dst, const void* d_src, size_t bytes);
+/* Per-kernel CUDA-event timing on the context's stream (no reference
+ * analogue; the reference has no tracing).  enable resets the
+ * counters; read returns the summed device milliseconds and launch count of
+ * one kernel class. */
+#define PRB_PROF_POLICY 0
+#define PRB_PROF_ENV_STOCK 1
+#define PRB_PROF_ENV_POINTMASS 2
+#define PRB_PROF_GAE 3
+#define PRB_PROF_PPO_FWDBWD 4
+#define PRB_PROF_PPO_REDUCE 5
+#define PRB_PROF_ADAM 6
+#define PRB_PROF_ROLLOUT 7
+PRB_API int prb_ctx_profile(prb_ctx ctx, int enable);
+PRB_API int prb_ctx_profile_read(prb_ctx ctx, int kind, double* total_ms, uint64_t* launches);
 
 /* ---- market data (market.hpp) ------------------------------------------ */
 /* Synthetic OHLCV of BASELINE.md §3: mt19937_64(seed); p0 ~ U(10,200);
@@ -177,6 +191,10 @@ PRB_API int prb_rollout_destroy(prb_rollout r);
  * then the bootstrap V(s_H) per env.  Noise stream keyed by seed (the
  * reference's derive_seed(seed, kCollect, w, epoch)). */
 PRB_API int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed);
+/* Device views of the time-major buffer fields ([H][N] rows; obs rows hold
+ * the stored obs floats per transition). Any out pointer may be NULL. */
+PRB_API int prb_rollout_device_fields(prb_rollout r, float** d_obs, float** d_actions, float** d_log_probs,
+                                      float** d_rewards, float** d_values, uint8_t** d_dones, float** d_bootstrap);
 /* Host transfer in the REFERENCE index space (chunk e = rows e*H..e*H+H-1,
  * pod.hpp:89-94): states [N*H][S], actions [N*H][A], log_probs, rewards,
  * dones, values [N*H], bootstrap [N].  Any pointer may be NULL (download). */

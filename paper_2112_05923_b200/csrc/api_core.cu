@@ -53,6 +53,17 @@ void* prb_ctx_s::device_scratch(size_t bytes) {
 
 void prb_ctx_s::sync() { PRB_CUDA(cudaStreamSynchronize(stream)); }
 
+cudaEvent_t prb_ctx_s::take_event() {
+  if (ev_pool.empty()) {
+    cudaEvent_t e;
+    PRB_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = ev_pool.back();
+  ev_pool.pop_back();
+  return e;
+}
+
 extern "C" {
 
 const char* prb_last_error(void) { return g_last_error.c_str(); }
@@ -93,6 +104,41 @@ int prb_ctx_destroy(prb_ctx c) {
 }
 
 int prb_ctx_synchronize(prb_ctx c) { return guard([&] { c->sync(); }); }
+
+int prb_ctx_profile(prb_ctx c, int enable) {
+  return guard([&] {
+    PRB_REQUIRE(c, PRB_ERR_USAGE, "prb_ctx_profile: NULL ctx");
+    c->sync();
+    for (auto& e : c->ev_live) {
+      c->ev_pool.push_back(e.a);
+      c->ev_pool.push_back(e.b);
+    }
+    c->ev_live.clear();
+    for (int i = 0; i < 16; ++i) {
+      c->prof_ms[i] = 0.0;
+      c->prof_n[i] = 0;
+    }
+    c->profiling = enable != 0;
+  });
+}
+
+int prb_ctx_profile_read(prb_ctx c, int kind, double* total_ms, uint64_t* launches) {
+  return guard([&] {
+    PRB_REQUIRE(c && kind >= 0 && kind < 16, PRB_ERR_USAGE, "prb_ctx_profile_read: bad argument");
+    c->sync();
+    for (auto& e : c->ev_live) {
+      float ms = 0.f;
+      PRB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      c->prof_ms[e.kind] += ms;
+      c->prof_n[e.kind] += 1;
+      c->ev_pool.push_back(e.a);
+      c->ev_pool.push_back(e.b);
+    }
+    c->ev_live.clear();
+    if (total_ms) *total_ms = c->prof_ms[kind];
+    if (launches) *launches = c->prof_n[kind];
+  });
+}
 void* prb_ctx_stream(prb_ctx c) { return c ? (void*)c->stream : nullptr; }
 
 int prb_device_alloc(prb_ctx c, size_t bytes, void** out) {

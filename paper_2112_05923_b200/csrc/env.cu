@@ -342,7 +342,10 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
     attr_set = true;
   }
   const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
-  stock_step_kernel<<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+  {
+    ProfScope prof(env->ctx, kProfEnvStock);
+    stock_step_kernel<<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+  }
   PRB_CHECK_LAUNCH();
   env->t = done ? env->start : t1;
   env->step_count = done ? 0 : env->step_count + 1;
@@ -365,7 +368,10 @@ void prb_pm_step_launch(prb_vecenv env, const float* d_actions, float* d_reward,
   a.term_ret = d_term_ret;
   a.term_len = d_term_len;
   const int grid = (int)((env->N + 255) / 256);
-  pm_step_kernel<<<grid, 256, 0, env->ctx->stream>>>(a);
+  {
+    ProfScope prof(env->ctx, kProfEnvPm);
+    pm_step_kernel<<<grid, 256, 0, env->ctx->stream>>>(a);
+  }
   PRB_CHECK_LAUNCH();
 }
 

@@ -114,7 +114,10 @@ void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8
                     size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize) {
   const int grid = (int)((N + 255) / 256);
   double* partials = stat ? static_cast<double*>(ctx->device_scratch((size_t)grid * 3 * sizeof(double))) : nullptr;
-  gae_kernel<<<grid, 256, 0, ctx->stream>>>(rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials);
+  {
+    ProfScope prof(ctx, kProfGae);
+    gae_kernel<<<grid, 256, 0, ctx->stream>>>(rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials);
+  }
   PRB_CHECK_LAUNCH();
   if (stat) {
     gae_stats_kernel<<<1, 256, 0, ctx->stream>>>(partials, grid, normalize, stat);

@@ -160,7 +160,9 @@ size_t prb_policy_smem(const PolicyArgs& p) {
   return (size_t)R * (ldx + 2 * p.ldw + ldA) * sizeof(float);
 }
 
-void prb_policy_launch(const PolicyArgs& p, cudaStream_t s) {
+void prb_policy_launch(const PolicyArgs& p, prb_ctx_s* ctx) {
+  cudaStream_t s = ctx->stream;
+  ProfScope prof(ctx, kProfPolicy);
   if (p.n == 0) return;
   const size_t smem = prb_policy_smem(p);
   PRB_REQUIRE(smem <= 220 * 1024, PRB_ERR_CONFIG, "policy: tile does not fit in shared memory");
@@ -199,7 +201,7 @@ int prb_policy_sample(prb_agent a, const float* d_states, size_t n, uint64_t see
     p.log_probs = d_log_probs;
     p.values = d_values;
     p.eps_out = d_eps;
-    prb_policy_launch(p, a->ctx->stream);
+    prb_policy_launch(p, a->ctx);
     finish_checked(a, "policy_sample states");  // nn.hpp:252
   });
 }
@@ -214,7 +216,7 @@ int prb_policy_sample_eps(prb_agent a, const float* d_states, size_t n, const fl
     p.actions = d_actions;
     p.log_probs = d_log_probs;
     p.values = d_values;
-    prb_policy_launch(p, a->ctx->stream);
+    prb_policy_launch(p, a->ctx);
     finish_checked(a, "policy_sample states");
   });
 }
@@ -226,7 +228,7 @@ int prb_policy_mean(prb_agent a, const float* d_states, size_t n, float* d_mean)
     p.mode = kPolicyMean;
     p.mean_out = d_mean;
     p.status = nullptr;
-    prb_policy_launch(p, a->ctx->stream);
+    prb_policy_launch(p, a->ctx);
     a->ctx->sync();
   });
 }
@@ -239,7 +241,7 @@ int prb_policy_log_prob(prb_agent a, const float* d_states, const float* d_actio
     p.actions_in = d_actions;
     p.log_probs = d_lp;
     p.status = nullptr;
-    prb_policy_launch(p, a->ctx->stream);
+    prb_policy_launch(p, a->ctx);
     a->ctx->sync();
   });
 }
@@ -251,7 +253,7 @@ int prb_critic_value(prb_agent a, const float* d_states, size_t n, float* d_valu
     p.mode = kPolicyValueOnly;
     p.values = d_values;
     p.status = nullptr;
-    prb_policy_launch(p, a->ctx->stream);
+    prb_policy_launch(p, a->ctx);
     a->ctx->sync();
   });
 }

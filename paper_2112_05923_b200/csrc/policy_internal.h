@@ -41,7 +41,7 @@ struct PolicyArgs {
 
 PolicyArgs prb_policy_args(prb_agent a, const float* d_states, size_t n);
 size_t prb_policy_smem(const PolicyArgs& p);
-void prb_policy_launch(const PolicyArgs& p, cudaStream_t s);
+void prb_policy_launch(const PolicyArgs& p, prb_ctx_s* ctx);
 void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
                          double* d_term_ret, int32_t* d_term_len);
 void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s);

@@ -429,7 +429,7 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
 void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
   const int grid = (p.mb + p.R - 1) / p.R;
   const size_t smem = carve(p, nullptr, nullptr);
-  ppo_fwd_bwd_kernel<<<grid, kPpoThreads, smem, s>>>(p);
+  ppo_fwd_bwd_kernel<<<grid, kPpoThreads, smem, s>>>(p);  // steps run inside CUDA graphs: no event scopes
   ReduceArgs r;
   r.partial = ws.partial.p;
   r.nparts = grid;

@@ -99,6 +99,41 @@ struct prb_ctx_s {
   void* pinned_staging(size_t bytes);
   void* device_scratch(size_t bytes);
   void sync();
+  // Per-kernel CUDA-event timing on this stream (prb_ctx_profile_*).
+  bool profiling = false;
+  struct Ev {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> ev_live;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[16] = {0};
+  uint64_t prof_n[16] = {0};
+  cudaEvent_t take_event();
+};
+
+// Kernel classes reported by prb_ctx_profile_read (index == PRB_PROF_* in prb.h).
+enum { kProfPolicy = 0, kProfEnvStock = 1, kProfEnvPm = 2, kProfGae = 3, kProfPpoFwdBwd = 4, kProfPpoReduce = 5,
+       kProfAdam = 6, kProfRollout = 7, kProfCount = 8 };
+
+// RAII event pair around one launch when the context is profiling.
+struct ProfScope {
+  prb_ctx_s* c;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(prb_ctx_s* ctx, int k) : c(ctx), kind(k) {
+    if (c && c->profiling) {
+      a = c->take_event();
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = c->take_event();
+      cudaEventRecord(b, c->stream);
+      c->ev_live.push_back({kind, a, b});
+    }
+  }
 };
 
 struct prb_market_s {

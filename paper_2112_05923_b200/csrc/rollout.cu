@@ -120,7 +120,7 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
       p.obs_store = r->d_obs.p + h * N * r->Sp;
       p.store_cols = (int)r->Sp;
       p.status = nullptr;
-      prb_policy_launch(p, s);
+      prb_policy_launch(p, r->ctx);
       prb_env_step_launch(env, p.actions, r->d_rew.p + h * N, r->d_done.p + h * N, nullptr, nullptr, nullptr);
     }
     // bootstrap V(s_H) (pod.hpp:127-131)
@@ -128,11 +128,25 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     p.mode = kPolicyValueOnly;
     p.values = r->d_boot.p;
     p.status = nullptr;
-    prb_policy_launch(p, s);
+    prb_policy_launch(p, r->ctx);
     if (compact) PRB_CUDA(cudaMemcpyAsync(r->d_row.p, rows.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     r->ctx->sync();  // rows[] lives on this stack frame
     r->full = true;
     r->gae_valid = false;
+  });
+}
+
+int prb_rollout_device_fields(prb_rollout r, float** d_obs, float** d_actions, float** d_log_probs, float** d_rewards,
+                              float** d_values, uint8_t** d_dones, float** d_bootstrap) {
+  return guard([&] {
+    PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_device_fields: NULL rollout");
+    if (d_obs) *d_obs = r->d_obs.p;
+    if (d_actions) *d_actions = r->d_act.p;
+    if (d_log_probs) *d_log_probs = r->d_logp.p;
+    if (d_rewards) *d_rewards = r->d_rew.p;
+    if (d_values) *d_values = r->d_val.p;
+    if (d_dones) *d_dones = r->d_done.p;
+    if (d_bootstrap) *d_bootstrap = r->d_boot.p;
   });
 }
 
