@@ -37,6 +37,7 @@ K_ASSETS, T_ROWS, MARKET_SEED = 30, 2048, 2112
 S_DIM = 1 + 6 * K_ASSETS
 # algorithmic work per transition
 ENV_BYTES = 36 * K_ASSETS + 41  # action 4K + balance 16 + shares 8K + ep_return 16 + obs 4(1+6K) + reward 4 + done 1
+BUF_BYTES = 4 * (1 + K_ASSETS) + 4 * K_ASSETS + 4 * 3 + 1  # compact rollout row: obs 124 + act 120 + logp/val/rew 12 + done 1
 MLP_FLOPS = 2 * (181 * 64 + 64 * 64 + 64 * 30) + 2 * (181 * 64 + 64 * 64 + 64 * 1)  # 66,688
 
 
@@ -210,64 +211,54 @@ def run_ours(args, d: Dist):
         ro.collect(agent, env, seed=1000 + i)
     ctx.synchronize()
 
-    # ---- timed region: K rollout collections, device events on the launching stream ----
-    lib.prb_ctx_profile(ctx.h, 1)
+    # ---- timed region: K rollout collections, CUDA events on the launching stream ----
+    lib.prb_ctx_profile(ctx.h, 1)  # per-kernel event pairs inside the region (kernel shares / roofline)
     clocks = ClockSampler(d.local)
     d.barrier()
     ctx.synchronize()
     clocks.start()
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        ro.collect(agent, env, seed=2000 + i)
-    ctx.synchronize()
-    wall = time.perf_counter() - t0
+    dev_ms = time_region(lib, ctx, lambda: [ro.collect(agent, env, seed=2000 + i) for i in range(args.steps)])
     clk = clocks.stop()
     prof = {}
-    for name, kind in (("policy_fwd_sample", 0), ("env_stock_step", 1)):
+    for name, kind in (("policy_fwd_sample", 0), ("env_stock_step", 1), ("stock_rollout_fused", 7)):
         ms, n = C.c_double(), C.c_uint64()
         lib.prb_ctx_profile_read(ctx.h, kind, C.byref(ms), C.byref(n))
         prof[name] = (ms.value, n.value)
     lib.prb_ctx_profile(ctx.h, 0)
-    # device time of the region = sum of the stream's kernel intervals is a lower bound; the
-    # stream is serial, so the region's device duration is measured by events around it:
-    dev_ms = time_region(lib, ctx, lambda: [ro.collect(agent, env, seed=3000 + i) for i in range(args.steps)])
     d.barrier()
     dev_ms = d.max(dev_ms)
     transitions = d.world * args.steps * N * H
     value = transitions / (dev_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (per-launch work / average launch time) ----
+    # ---- roofline of the dominant kernel (algorithmic work per launch / average launch time) ----
     kernels = {}
-    pol_ms, pol_n = prof["policy_fwd_sample"]
-    env_ms, env_n = prof["env_stock_step"]
-    kernels["policy_fwd_sample"] = {"ms_total": pol_ms, "launches": pol_n, "share": pol_ms / (wall * 1e3),
-                                    "bound": "tensor", "unit": "TFLOP/s",
-                                    "achieved": (N * MLP_FLOPS) / (pol_ms / max(pol_n, 1) / 1e3) / 1e12,
-                                    "peak": bf16_sus}
-    kernels["env_stock_step"] = {"ms_total": env_ms, "launches": env_n, "share": env_ms / (wall * 1e3),
-                                 "bound": "hbm", "unit": "GB/s",
-                                 "achieved": (N * ENV_BYTES) / (env_ms / max(env_n, 1) / 1e3) / 1e9, "peak": hbm}
+    region_ms = dev_ms
+    for name, (ms, n) in prof.items():
+        if n == 0:
+            continue
+        avg_s = ms / n / 1e3
+        if name == "policy_fwd_sample":
+            k = {"bound": "tensor", "unit": "TFLOP/s", "achieved": N * MLP_FLOPS / avg_s / 1e12, "peak": bf16_sus,
+                 "work_per_launch": f"{N} rows x {MLP_FLOPS} FLOP"}
+        elif name == "env_stock_step":
+            k = {"bound": "hbm", "unit": "GB/s", "achieved": N * ENV_BYTES / avg_s / 1e9, "peak": hbm,
+                 "work_per_launch": f"{N} envs x {ENV_BYTES} B"}
+        else:
+            k = {"bound": "tensor", "unit": "TFLOP/s", "achieved": N * H * MLP_FLOPS / avg_s / 1e12, "peak": bf16_sus,
+                 "work_per_launch": f"{N}x{H} transitions x {MLP_FLOPS} FLOP (actor+critic fwd)",
+                 "hbm_gbs": N * H * BUF_BYTES / avg_s / 1e9, "hbm_frac": N * H * BUF_BYTES / avg_s / 1e9 / hbm,
+                 "hbm_bytes_per_transition": BUF_BYTES}
+        k.update({"ms_total": ms, "launches": n, "share": ms / region_ms, "frac": k["achieved"] / k["peak"]})
+        kernels[name] = k
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
     kd = kernels[dom]
     roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
-                "unit": kd["unit"], "frac": kd["achieved"] / kd["peak"], "traffic": None,
-                "peak_source": f"{peak_src} (MEASURED_PEAKS.json {'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
-    for k in kernels.values():
-        k["frac"] = k["achieved"] / k["peak"]
+                "unit": kd["unit"], "frac": kd["frac"], "traffic": None,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json "
+                               f"{'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
 
-    # ---- env step alone (the VecEnv boundary), device actions resident ----
-    d_act = C.c_void_p()
-    lib.prb_rollout_device_fields(ro.h, None, C.byref(d_act), None, None, None, None, None)
-    d_rew, d_done = ctx.alloc((N,)), ctx.alloc((N,), np.uint8)
-    env.reset(5)
-    n_env_steps = 200
-    env_ms_total = time_region(lib, ctx, lambda: [env.step_device(d_act.value + (i % H) * N * K_ASSETS * 4,
-                                                                  d_rew.ptr, d_done.ptr)
-                                                  for i in range(n_env_steps)])
-    env_rate = N * n_env_steps / (env_ms_total / 1e3)
-    env_step = {"value": d.world * env_rate if d.world > 1 else env_rate, "unit": UNIT,
-                "achieved_gbs": env_rate * ENV_BYTES / 1e9, "frac_hbm": env_rate * ENV_BYTES / 1e9 / hbm,
-                "bytes_per_transition": ENV_BYTES, "steps": n_env_steps}
+    # ---- env step alone (the VecEnv boundary) at configs[4] scale: 1M envs/GPU, > L2 ----
+    env_step = env_leg(pr, lib, ctx, market, cfg, args.env_envs, hbm, d)
 
     # ---- one full PPO update on the collected buffer (GAE + epochs x minibatches + Adam) ----
     ppo = None
@@ -316,17 +307,43 @@ def run_ours(args, d: Dist):
     if d.rank == 0 and d.world == 1 and not args.skip_cpu:
         cpu = cpu_reference_rate(m, ind, seconds=args.cpu_seconds)
 
-    launches = args.steps * (2 * H + 1)
+    # kernel launches in the timed region: fused collect = shared-layer kernel + fused kernel
+    launches = int(prof["policy_fwd_sample"][1] + prof["env_stock_step"][1] + 2 * prof["stock_rollout_fused"][1])
     if d.rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (MLP, obs) + f64 (portfolio accounting)",
                "data": "synthetic (BASELINE.md §3 market, random-init artifact_init weights)",
                "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
-               "ppo_update": ppo, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-               "wall_s_profiled_region": wall}
+               "ppo_update": ppo, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk}
         print(json.dumps(out))
     d.close()
+
+
+def env_leg(pr, lib, ctx, market, cfg, n_envs, hbm, d, steps=50):
+    """prb_vecenv_step on device buffers: n_envs stock envs, U(-1.2,1.2) fp32 actions resident in HBM."""
+    env = pr.VectorizedEnvironment.stock(ctx, market, cfg, 0, T_ROWS - 1, n_envs)
+    env.reset(5)
+    rng = np.random.default_rng(0)
+    acts = [pr.DeviceArray.from_numpy(ctx, rng.uniform(-1.2, 1.2, (n_envs, K_ASSETS)).astype(np.float32))
+            for _ in range(2)]
+    d_rew, d_done = ctx.alloc((n_envs,)), ctx.alloc((n_envs,), np.uint8)
+    for i in range(3):
+        env.step_device(acts[i % 2].ptr, d_rew.ptr, d_done.ptr)
+    lib.prb_ctx_profile(ctx.h, 1)
+    region = time_region(lib, ctx, lambda: [env.step_device(acts[i % 2].ptr, d_rew.ptr, d_done.ptr)
+                                            for i in range(steps)])
+    ms, n = C.c_double(), C.c_uint64()
+    lib.prb_ctx_profile_read(ctx.h, 1, C.byref(ms), C.byref(n))
+    lib.prb_ctx_profile(ctx.h, 0)
+    region = d.max(region)
+    kern_rate = n_envs * n.value / (ms.value / 1e3)
+    rate = n_envs * steps / (region / 1e3)
+    return {"value": d.world * rate, "unit": UNIT, "envs_per_gpu": n_envs, "steps": steps,
+            "kernel_avg_us": ms.value / max(n.value, 1) * 1e3,
+            "achieved_gbs": kern_rate * ENV_BYTES / 1e9, "frac_hbm": kern_rate * ENV_BYTES / 1e9 / hbm,
+            "bytes_per_transition": ENV_BYTES,
+            "note": "obs [N][181] fp32 written every step (VecStepResult.next_states); state/actions > L2"}
 
 
 def time_region(lib, ctx, fn) -> float:
@@ -387,6 +404,7 @@ def main():
     ap.add_argument("--envs", type=int, default=65536)
     ap.add_argument("--horizon", type=int, default=256)
     ap.add_argument("--ppo-epochs", type=int, default=4)
+    ap.add_argument("--env-envs", type=int, default=1 << 20)
     ap.add_argument("--skip-ppo", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

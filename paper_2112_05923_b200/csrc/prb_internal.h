@@ -214,4 +214,5 @@ struct prb_rollout_s {
   bool gae_valid = false;
   bool normalized = true;
   bool full = false;
+  bool fused = true;  // prb_rollout_set_mode: fused persistent collect kernel when supported
 };

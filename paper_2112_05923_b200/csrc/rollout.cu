@@ -34,6 +34,9 @@ void alloc_rollout(prb_rollout_s* r) {
 
 }  // namespace
 
+bool prb_fused_rollout_supported(prb_rollout r, prb_agent a, prb_vecenv env);
+void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed, std::vector<int32_t>& rows);
+
 void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8_t* done, const float* boot, size_t N,
                     size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize);
 
@@ -108,6 +111,14 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     cudaStream_t s = r->ctx->stream;
     const size_t N = r->N, H = r->H, A = r->A;
     std::vector<int32_t> rows(H);
+    if (r->fused && prb_fused_rollout_supported(r, a, env)) {
+      prb_fused_rollout_launch(r, a, env, seed, rows);
+      PRB_CUDA(cudaMemcpyAsync(r->d_row.p, rows.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      r->ctx->sync();
+      r->full = true;
+      r->gae_valid = false;
+      return;
+    }
     for (size_t h = 0; h < H; ++h) {
       if (compact) rows[h] = (int32_t)env->t;
       PolicyArgs p = prb_policy_args(a, env->d_obs.p, N);
@@ -133,6 +144,13 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     r->ctx->sync();  // rows[] lives on this stack frame
     r->full = true;
     r->gae_valid = false;
+  });
+}
+
+int prb_rollout_set_mode(prb_rollout r, int mode) {
+  return guard([&] {
+    PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_set_mode: NULL rollout");
+    r->fused = mode != 0;
   });
 }
 

@@ -437,6 +437,10 @@ class Rollout:
     def capacity(self) -> int:
         return self.N * self.H
 
+    def set_mode(self, fused: bool):
+        """True (default): one fused persistent kernel per collect when supported."""
+        self.ctx.lib.prb_rollout_set_mode(self.h, 1 if fused else 0)
+
     def collect(self, agent: Agent, env: VectorizedEnvironment, seed: int):
         """worker_collect pod.hpp:95-132."""
         self.ctx.lib.prb_rollout_collect(self.h, agent.h, env.h, seed)

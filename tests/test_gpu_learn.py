@@ -369,7 +369,8 @@ def _replay_stock(orc, close, ind, cfg, start, end, N, H, acts, K):
     return states.reshape(N * H, S), rewards.ravel(), dones.ravel(), obs
 
 
-def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc):
+@pytest.mark.parametrize("fused", [False, True])
+def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
     K, T, N, H = 30, 200, 96, 48
     m = pr.synthetic_market(K, T, seed=2112)
     ind = pr.compute_indicators(m["high"], m["low"], m["close"])
@@ -381,6 +382,7 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc):
     S = 1 + 6 * K
     agent = pr.Agent.init(ctx, S, K, seed=7)
     ro = pr.Rollout.for_env(env, H)
+    ro.set_mode(fused)
     ro.collect(agent, env, seed=99)
     b = ro.download()
     acts = b["actions"].reshape(N, H, K)
@@ -389,10 +391,25 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc):
     assert np.array_equal(b["states"], f32(st))  # compact rows + shared features == full obs
     assert np.array_equal(b["rewards"], f32(rw)) and np.array_equal(b["dones"], dn)
     assert dn.reshape(N, H)[:, 29].all()
-    assert np.array_equal(agent.log_prob(b["states"], b["actions"]), b["log_probs"].astype(np.float32))
-    assert np.array_equal(agent.value(b["states"]), b["values"].astype(np.float32))
-    assert np.array_equal(agent.value(env.states()), b["bootstrap"].astype(np.float32))
     assert np.array_equal(env.states(), f32(final))
+    lp, val, boot = (agent.log_prob(b["states"], b["actions"]), agent.value(b["states"]),
+                     agent.value(env.states()))
+    if not fused:  # the per-step path runs exactly the standalone policy kernel
+        assert np.array_equal(lp, b["log_probs"].astype(np.float32))
+        assert np.array_equal(val, b["values"].astype(np.float32))
+        assert np.array_equal(boot, b["bootstrap"].astype(np.float32))
+    else:  # fused kernel: same function, shared-feature term summed separately (fp32 order)
+        assert np.max(np.abs(lp - b["log_probs"])) <= 2e-4
+        assert np.all(np.abs(val - b["values"]) <= 1e-5 * (1 + np.abs(val)))
+        assert np.all(np.abs(boot - b["bootstrap"]) <= 1e-5 * (1 + np.abs(boot)))
+        # noise stream identical to the standalone sampler: eps recovered from the actions
+        mean = agent.policy_mean(b["states"])
+        flat = agent.flatten_params()
+        ls = flat[S * 64 + 64 + 64 * 64 + 64 + 64 * K + K:][:K]
+        eps = (b["actions"] - mean) / np.exp(ls)
+        s0 = np.ascontiguousarray(b["states"].reshape(N, H, S)[:, 0])  # step 0 of every env
+        ref_eps = agent.policy_sample(s0, seed=99, counter=0)["eps"]
+        assert np.allclose(eps.reshape(N, H, K)[:, 0], ref_eps, atol=1e-3)
 
 
 def test_collect_pointmass_rollout(pr, ctx, orc):
