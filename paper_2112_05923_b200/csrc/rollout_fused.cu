@@ -67,11 +67,11 @@ struct Smem {
   float W3c[kH2];           // critic head
   float b1[128], b2[128], b3[32], ls[32], sig[32];
   float b3c;
-  float x[kRows][kXW];
-  float h1[kRows][128];
-  float h2[kRows][128];
-  float head[kRows][32];    // mean 0..A-1, value at 31
-  float act[kRows][32];
+  alignas(16) float x[kRows][kXW];  // float4-read operands must stay 16-byte aligned
+  alignas(16) float h1[kRows][128];
+  alignas(16) float h2[kRows][128];
+  alignas(16) float head[kRows][32];    // mean 0..A-1, value at 31
+  alignas(16) float act[kRows][32];
   double bal[kRows], ret[kRows];
   double p0[kXW], p1[kXW];
   int32_t sh[kXW][kRows];
