@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Small deterministic drivers for ncu captures (one kernel family each).
+
+  python profiles/drive.py collect  [N] [H]   # fused stock rollout (or --unfused)
+  python profiles/drive.py env      [N]       # prb_vecenv_step on device buffers
+  python profiles/drive.py ppo      [N] [H]   # a few PPO minibatch steps
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2112_05923_b200 import podracer as pr  # noqa: E402
+
+
+def setup(N):
+    ctx = pr.Context(0)
+    m = pr.synthetic_market(30, 2048, 2112)
+    ind = pr.compute_indicators(m["high"], m["low"], m["close"])
+    market = pr.MarketData(ctx, m["close"], ind)
+    env = pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(), 0, 2047, N)
+    env.reset(1)
+    return ctx, market, env
+
+
+def main():
+    what = sys.argv[1]
+    fused = "--unfused" not in sys.argv
+    args = [a for a in sys.argv[2:] if not a.startswith("--")]
+    if what == "collect":
+        N = int(args[0]) if args else 65536
+        H = int(args[1]) if len(args) > 1 else 32
+        ctx, market, env = setup(N)
+        agent = pr.Agent.init(ctx, 181, 30, seed=7)
+        ro = pr.Rollout.for_env(env, H)
+        ro.set_mode(fused)
+        for i in range(3):
+            ro.collect(agent, env, seed=i)
+        ctx.synchronize()
+    elif what == "env":
+        N = int(args[0]) if args else 1 << 20
+        ctx, market, env = setup(N)
+        a = pr.DeviceArray.from_numpy(ctx, np.random.default_rng(0).uniform(-1.2, 1.2, (N, 30)).astype(np.float32))
+        r, d = ctx.alloc((N,)), ctx.alloc((N,), np.uint8)
+        for _ in range(6):
+            env.step_device(a.ptr, r.ptr, d.ptr)
+        ctx.synchronize()
+    elif what == "ppo":
+        N = int(args[0]) if args else 4096
+        H = int(args[1]) if len(args) > 1 else 64
+        ctx, market, env = setup(N)
+        agent = pr.Agent.init(ctx, 181, 30, seed=7)
+        ro = pr.Rollout.for_env(env, H)
+        ro.collect(agent, env, seed=1)
+        cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=1, buffer_size=N * H)
+        pr.ppo_update(agent, ro, cfg, seed=3)
+        ctx.synchronize()
+    print("ok", what)
+
+
+if __name__ == "__main__":
+    main()
