@@ -283,6 +283,11 @@ PRB_API int prb_leaderboard_allgather_rank(prb_comm c, const double* d_scores, c
 /* Broadcast an agent's params, m, v and t from `root` (elite broadcast). */
 PRB_API int prb_agent_broadcast(prb_comm c, prb_agent a, int root);
 
+/* ---- self-test of the tcgen05 building block (tests only) --------------- */
+/* D[128][N] = bf16(A[128][K]) . bf16(B[N][K])^T with fp32 accumulation in
+ * TMEM, one CTA, K % 16 == 0 (<= 256), N % 16 == 0 (<= 256). */
+PRB_API int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

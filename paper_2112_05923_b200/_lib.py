@@ -168,6 +168,7 @@ SIGNATURES = {
     "prb_comm_destroy": (I, [P]),
     "prb_leaderboard_allgather_rank": (I, [P, P, P, P, SZ, SZ, P, P, P, P, P]),
     "prb_agent_broadcast": (I, [P, P, I]),
+    "prb_debug_tc_gemm": (I, [P, I, I, pF, pF, pF]),
 }
 
 UNCHECKED = {"prb_last_error", "prb_version", "prb_splitmix64", "prb_derive_seed", "prb_ctx_stream",

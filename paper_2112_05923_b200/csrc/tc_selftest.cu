@@ -1,0 +1,78 @@
+// tc_selftest.cu -- validates the tcgen05 descriptor / TMEM conventions of tc.cuh
+// with one M=128 x N x K bf16 GEMM (D = A . B^T, A [128][K], B [N][K]).
+#include <vector>
+
+#include "prb_internal.h"
+#include <cuda_bf16.h>
+
+#include "tc.cuh"
+
+using namespace prb;
+
+namespace {
+
+__global__ void __launch_bounds__(128) tc_gemm_selftest_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                               float* __restrict__ D, int K, int N) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sA = smem;                 // 128*K*2 bytes
+  unsigned char* sB = smem + 128 * K * 2;   // N*K*2 bytes
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 128 * K; i += blockDim.x) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sA + tc::kmajor_offset(r, k, K)) = __float2bfloat16_rn(A[i]);
+  }
+  for (int i = tid; i < N * K; i += blockDim.x) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sB + tc::kmajor_offset(r, k, K)) = __float2bfloat16_rn(B[i]);
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
+  if (tid == 0) tc::mbar_init(&mbar, 1);
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_bf16(128, N);
+    for (int j = 0; j < K / 16; ++j) {
+      const uint64_t ad = tc::smem_desc(tc::smem_u32(sA) + j * 256, 128, K * 16);
+      const uint64_t bd = tc::smem_desc(tc::smem_u32(sB) + j * 256, 128, K * 16);
+      tc::mma_bf16(tbase, ad, bd, idesc, j > 0);
+    }
+    tc::mma_commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after_sync();
+  for (int c = 0; c < N; c += 16) {
+    float v[16];
+    tc::tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
+    for (int i = 0; i < 16; ++i) D[tid * N + c + i] = v[i];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, 256);
+}
+
+}  // namespace
+
+extern "C" int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* hA, const float* hB, float* hD) {
+  return guard([&] {
+    PRB_REQUIRE(ctx && hA && hB && hD, PRB_ERR_USAGE, "prb_debug_tc_gemm: NULL argument");
+    PRB_REQUIRE(K % 16 == 0 && K <= 256 && N % 16 == 0 && N <= 256, PRB_ERR_CONFIG, "prb_debug_tc_gemm: bad shape");
+    DevBuf<float> dA, dB, dD;
+    dA.alloc(128 * K);
+    dB.alloc((size_t)N * K);
+    dD.alloc(128 * (size_t)N);
+    cudaStream_t s = ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(dA.p, hA, dA.bytes(), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dB.p, hB, dB.bytes(), cudaMemcpyHostToDevice, s));
+    const size_t smem = (size_t)(128 + N) * K * 2;
+    PRB_CUDA(cudaFuncSetAttribute(tc_gemm_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    tc_gemm_selftest_kernel<<<1, 128, smem, s>>>(dA.p, dB.p, dD.p, K, N);
+    PRB_CHECK_LAUNCH();
+    PRB_CUDA(cudaMemcpyAsync(hD, dD.p, dD.bytes(), cudaMemcpyDeviceToHost, s));
+    ctx->sync();
+  });
+}
