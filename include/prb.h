@@ -191,10 +191,12 @@ PRB_API int prb_rollout_destroy(prb_rollout r);
  * then the bootstrap V(s_H) per env.  Noise stream keyed by seed (the
  * reference's derive_seed(seed, kCollect, w, epoch)). */
 PRB_API int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed);
-/* Collection mode: 1 (default) = one fused persistent kernel per rollout when
- * the shapes allow it (stock env, 64x64 nets); 0 = one policy launch + one
- * VecEnv step launch per time step (the same kernels prb_policy_sample /
- * prb_vecenv_step run). */
+/* Collection mode.  When the shapes allow it (stock env, 64x64 nets):
+ * 2 (default) = one fused persistent kernel per rollout, actor/critic layers
+ * on tcgen05 tensor cores (bf16 operands, fp32 TMEM accumulators);
+ * 1 = the same fused kernel with fp32 SIMT layers (reference-precision path).
+ * 0 = one policy launch + one VecEnv step launch per time step (the kernels
+ * prb_policy_sample / prb_vecenv_step run).  Other shapes always use 0. */
 PRB_API int prb_rollout_set_mode(prb_rollout r, int mode);
 /* Device views of the time-major buffer fields ([H][N] rows; obs rows hold
  * the stored obs floats per transition). Any out pointer may be NULL. */

@@ -214,5 +214,5 @@ struct prb_rollout_s {
   bool gae_valid = false;
   bool normalized = true;
   bool full = false;
-  bool fused = true;  // prb_rollout_set_mode: fused persistent collect kernel when supported
+  int mode = 2;  // prb_rollout_set_mode: 0 per-step kernels, 1 fused fp32 SIMT, 2 fused tcgen05 (default)
 };

@@ -111,7 +111,7 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     cudaStream_t s = r->ctx->stream;
     const size_t N = r->N, H = r->H, A = r->A;
     std::vector<int32_t> rows(H);
-    if (r->fused && prb_fused_rollout_supported(r, a, env)) {
+    if (r->mode != 0 && prb_fused_rollout_supported(r, a, env)) {
       prb_fused_rollout_launch(r, a, env, seed, rows);
       PRB_CUDA(cudaMemcpyAsync(r->d_row.p, rows.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));
       r->ctx->sync();
@@ -150,7 +150,8 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
 int prb_rollout_set_mode(prb_rollout r, int mode) {
   return guard([&] {
     PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_set_mode: NULL rollout");
-    r->fused = mode != 0;
+    PRB_REQUIRE(mode >= 0 && mode <= 2, PRB_ERR_CONFIG, "prb_rollout_set_mode: mode must be 0, 1 or 2");
+    r->mode = mode;
   });
 }
 

@@ -20,6 +20,7 @@
 #include "policy_internal.h"
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "rollout_tc.h"
 
 using namespace prb;
 
@@ -430,15 +431,32 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
     f.b_rew = r->d_rew.p;
     f.b_done = r->d_done.p;
     f.b_boot = r->d_boot.p;
-    static bool attr = false;
-    if (!attr) {
-      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sizeof(Smem)));
-      attr = true;
+    if (r->mode == 2) {  // tcgen05 bf16 MLP (rollout_tc.cu)
+      TcRolloutArgs ta{};
+      ta.params = f.params;
+      ta.a_w1 = f.a_w1; ta.a_w2 = f.a_w2; ta.a_w3 = f.a_w3;
+      ta.c_w1 = f.c_w1; ta.c_w2 = f.c_w2; ta.c_w3 = f.c_w3;
+      ta.log_std = f.log_std;
+      ta.S = f.S; ta.K = f.K;
+      ta.shared_l1 = f.shared_l1; ta.t_seq = f.t_seq; ta.done_seq = f.done_seq;
+      ta.close_tk = f.close_tk; ta.feat = f.feat;
+      ta.cap = f.cap; ta.max_trade = f.max_trade; ta.cost = f.cost;
+      ta.N = f.N; ta.H = f.H; ta.seed = f.seed;
+      ta.balance = f.balance; ta.shares = f.shares; ta.ep_return = f.ep_return; ta.obs_out = f.obs_out;
+      ta.b_obs = f.b_obs; ta.b_act = f.b_act; ta.b_logp = f.b_logp; ta.b_val = f.b_val; ta.b_rew = f.b_rew;
+      ta.b_done = f.b_done; ta.b_boot = f.b_boot;
+      launch_stock_rollout_tc(ta, s);
+    } else {  // fp32 SIMT MLP
+      static bool attr = false;
+      if (!attr) {
+        PRB_CUDA(cudaFuncSetAttribute(stock_rollout_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(Smem)));
+        attr = true;
+      }
+      const unsigned grid = (unsigned)((N + kRows - 1) / kRows);
+      stock_rollout_fused_kernel<<<grid, kThreads, sizeof(Smem), s>>>(f);
+      PRB_CHECK_LAUNCH();
     }
-    const unsigned grid = (unsigned)((N + kRows - 1) / kRows);
-    stock_rollout_fused_kernel<<<grid, kThreads, sizeof(Smem), s>>>(f);
-    PRB_CHECK_LAUNCH();
   }
   env->t = t;
   env->step_count = sc;

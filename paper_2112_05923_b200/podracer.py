@@ -437,9 +437,10 @@ class Rollout:
     def capacity(self) -> int:
         return self.N * self.H
 
-    def set_mode(self, fused: bool):
-        """True (default): one fused persistent kernel per collect when supported."""
-        self.ctx.lib.prb_rollout_set_mode(self.h, 1 if fused else 0)
+    def set_mode(self, mode):
+        """2 (default): fused kernel with tcgen05 layers; 1: fused fp32 SIMT; 0: per-step kernels.
+        (bools map True -> 1, False -> 0)."""
+        self.ctx.lib.prb_rollout_set_mode(self.h, int(mode))
 
     def collect(self, agent: Agent, env: VectorizedEnvironment, seed: int):
         """worker_collect pod.hpp:95-132."""

@@ -369,7 +369,7 @@ def _replay_stock(orc, close, ind, cfg, start, end, N, H, acts, K):
     return states.reshape(N * H, S), rewards.ravel(), dones.ravel(), obs
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
     K, T, N, H = 30, 200, 96, 48
     m = pr.synthetic_market(K, T, seed=2112)
@@ -398,10 +398,13 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
         assert np.array_equal(lp, b["log_probs"].astype(np.float32))
         assert np.array_equal(val, b["values"].astype(np.float32))
         assert np.array_equal(boot, b["bootstrap"].astype(np.float32))
-    else:  # fused kernel: same function, shared-feature term summed separately (fp32 order)
-        assert np.max(np.abs(lp - b["log_probs"])) <= 2e-4
-        assert np.all(np.abs(val - b["values"]) <= 1e-5 * (1 + np.abs(val)))
-        assert np.all(np.abs(boot - b["bootstrap"]) <= 1e-5 * (1 + np.abs(boot)))
+    else:
+        # mode 1: fused fp32 kernel, shared-feature term summed separately (fp32 order only)
+        # mode 2: tcgen05 layers, bf16 operands + tanh.approx: the stated bf16 tolerance
+        tl, tv = (2e-4, 1e-5) if fused == 1 else (0.15, 2e-2)
+        assert np.max(np.abs(lp - b["log_probs"])) <= tl, np.max(np.abs(lp - b["log_probs"]))
+        assert np.all(np.abs(val - b["values"]) <= tv * (1 + np.abs(val))), np.max(np.abs(val - b["values"]))
+        assert np.all(np.abs(boot - b["bootstrap"]) <= tv * (1 + np.abs(boot)))
         # noise stream identical to the standalone sampler: eps recovered from the actions
         mean = agent.policy_mean(b["states"])
         flat = agent.flatten_params()
@@ -409,7 +412,7 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
         eps = (b["actions"] - mean) / np.exp(ls)
         s0 = np.ascontiguousarray(b["states"].reshape(N, H, S)[:, 0])  # step 0 of every env
         ref_eps = agent.policy_sample(s0, seed=99, counter=0)["eps"]
-        assert np.allclose(eps.reshape(N, H, K)[:, 0], ref_eps, atol=1e-3)
+        assert np.allclose(eps.reshape(N, H, K)[:, 0], ref_eps, atol=1e-3 if fused == 1 else 5e-2)
 
 
 def test_collect_pointmass_rollout(pr, ctx, orc):
