@@ -401,8 +401,8 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
     else:
         # mode 1: fused fp32 kernel, shared-feature term summed separately (fp32 order only)
         # mode 2: tcgen05 layers, bf16 operands + tanh.approx: the stated bf16 tolerance
-        tl, tv = (2e-4, 1e-5) if fused == 1 else (0.15, 2e-2)
-        assert np.max(np.abs(lp - b["log_probs"])) <= tl, np.max(np.abs(lp - b["log_probs"]))
+        tl, tv = (2e-4, 1e-5) if fused == 1 else (1e-2, 5e-2)
+        assert np.all(np.abs(lp - b["log_probs"]) <= tl * (1 + np.abs(lp))), np.max(np.abs(lp - b["log_probs"]))
         assert np.all(np.abs(val - b["values"]) <= tv * (1 + np.abs(val))), np.max(np.abs(val - b["values"]))
         assert np.all(np.abs(boot - b["bootstrap"]) <= tv * (1 + np.abs(boot)))
         # noise stream identical to the standalone sampler: eps recovered from the actions
