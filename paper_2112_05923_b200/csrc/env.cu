@@ -73,6 +73,7 @@ __device__ __forceinline__ void write_obs_rows(float* __restrict__ dst, int nrow
 
 // One VecEnv step of N stock envs (env.hpp:200-236 -> StockTradingEnv::step
 // stock_env.hpp:165-170 -> stock_env_step :55-103 -> stock_observation :115-131).
+template <int KMAX>
 __global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, Kp = K + 1, F = 5 * K;
@@ -96,26 +97,51 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) 
     s_feat_obs[j] = a.feat[(size_t)a.t_obs * F + j];
     if (a.done) s_feat_term[j] = a.feat[(size_t)(a.t + 1) * F + j];
   }
-  {  // actions [nloc][K] are one contiguous span: coalesced load into padded rows
-    const float* src = a.actions + e0 * K;
-    const int total = nloc * K;
-    int r = tid / K, c = tid - (tid / K) * K;
-    for (int i = tid; i < total; i += blockDim.x) {
-      s_act[r * Kp + c] = src[i];
-      c += blockDim.x;
-      while (c >= K) {
-        c -= K;
-        ++r;
+  // Issue every global load of this CTA before consuming any (memory-level
+  // parallelism is what an HBM-bound step needs): the [nloc][K] action block
+  // as 16-byte vectors, the env's shares (SoA, coalesced), balance, return.
+  const int total = nloc * K;
+  const float* src = a.actions + e0 * K;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  const int total4 = vec_ok ? total / 4 : 0;
+  constexpr int kVec = (kEnvBlock * KMAX / 4 + kEnvBlock - 1) / kEnvBlock;  // float4 per thread (K <= KMAX)
+  float4 av[kVec];
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const int idx = tid + j * kEnvBlock;
+    if (idx < total4) av[j] = __ldg(reinterpret_cast<const float4*>(src) + idx);
+  }
+  int32_t shv[KMAX];
+  const bool live = tid < nloc;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    if (k < K && live) shv[k] = __ldg(a.shares + (size_t)k * a.N + e0 + tid);
+  const double bal_in = live ? a.balance[e0 + tid] : 0.0;
+  const double ret_in = live ? a.ep_return[e0 + tid] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const int idx = tid + j * kEnvBlock;
+    if (idx < total4) {
+      const float v4[4] = {av[j].x, av[j].y, av[j].z, av[j].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int f = idx * 4 + c, r = f / K;
+        s_act[r * Kp + (f - r * K)] = v4[c];
       }
     }
   }
-  if (tid < nloc)
-    for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = a.shares[(size_t)k * a.N + e0 + tid];
+  for (int f = total4 * 4 + tid; f < total; f += kEnvBlock) {  // tail / unaligned fallback
+    const int r = f / K;
+    s_act[r * Kp + (f - r * K)] = src[f];
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    if (k < K && live) s_sh[k * kEnvBlock + tid] = shv[k];
   __syncthreads();
 
   if (tid < nloc) {
     const size_t e = e0 + tid;
-    double bal = a.balance[e];
+    double bal = bal_in;
     // value_before (PortfolioState::account_value stock_env.hpp:27-31)
     double vb = bal;
     for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p0[k]));
@@ -150,7 +176,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) 
     double va = bal;
     for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p1[k]));
     const double r = __dsub_rn(va, vb);
-    const double ret = __dadd_rn(a.ep_return[e], r);  // env.hpp:218
+    const double ret = __dadd_rn(ret_in, r);  // env.hpp:218
     if (a.reward) a.reward[e] = (float)r;
     if (a.done_out) a.done_out[e] = (uint8_t)a.done;
     float* priv = s_priv + tid * Kp;
@@ -338,13 +364,17 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
   const size_t smem = stock_smem_bytes(m->K);
   static bool attr_set = false;
   if (!attr_set) {
-    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
   const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
   {
     ProfScope prof(env->ctx, kProfEnvStock);
-    stock_step_kernel<<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+    if (m->K <= 32)
+      stock_step_kernel<32><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+    else
+      stock_step_kernel<64><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
   }
   PRB_CHECK_LAUNCH();
   env->t = done ? env->start : t1;
@@ -399,6 +429,7 @@ int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t st
     PRB_REQUIRE(cfg->max_trade_shares * (double)(end - start) < 2.0e9, PRB_ERR_CONFIG,
                 "prb: max_trade_shares * episode length must stay below 2e9 (int32 share counts on device)");
     PRB_REQUIRE(N < (size_t)1 << 31, PRB_ERR_CONFIG, "prb: num_envs must be < 2^31");
+    PRB_REQUIRE(m->K <= 64, PRB_ERR_CONFIG, "prb: the device stock env supports up to 64 tickers");
     prb_ctx_s* ctx = m->ctx;
     PRB_CUDA(cudaSetDevice(ctx->device));
     auto* env = new prb_vecenv_s;
