@@ -27,7 +27,7 @@ using namespace prb;
 
 namespace {
 
-constexpr int kEnvBlock = 128;
+constexpr int kEnvBlock = 64;
 
 // std::clamp / std::min / std::max semantics (NaN-propagating exactly as libstdc++).
 __device__ __forceinline__ double clamp_ref(double v, double lo, double hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
