@@ -56,10 +56,42 @@ struct StockStepArgs {
 };
 
 // Coalesced write of a CTA's block of obs rows: row r = [priv[r][0..P), shared[0..S-P)].
+// The block is one contiguous span; when it is 16-byte aligned it is written
+// as float4 (4x fewer store instructions), tracking (row, col) incrementally.
 __device__ __forceinline__ void write_obs_rows(float* __restrict__ dst, int nrows, int S, int P,
                                                const float* __restrict__ s_priv, int Pp,
                                                const float* __restrict__ s_shared) {
   const int total = nrows * S;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const int total4 = total >> 2;
+    const int step = 4 * (int)blockDim.x;
+    int f = 4 * threadIdx.x;
+    int r = f / S, c = f - r * S;
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int q = threadIdx.x; q < total4; q += blockDim.x) {
+      float v[4];
+      int rr = r, cc = c;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] = (cc < P) ? s_priv[rr * Pp + cc] : s_shared[cc - P];
+        if (++cc == S) {
+          cc = 0;
+          ++rr;
+        }
+      }
+      d4[q] = make_float4(v[0], v[1], v[2], v[3]);
+      c += step;
+      while (c >= S) {
+        c -= S;
+        ++r;
+      }
+    }
+    for (int i = total4 * 4 + threadIdx.x; i < total; i += blockDim.x) {
+      const int rr = i / S, cc = i - rr * S;
+      dst[i] = (cc < P) ? s_priv[rr * Pp + cc] : s_shared[cc - P];
+    }
+    return;
+  }
   int r = threadIdx.x / S, c = threadIdx.x - (threadIdx.x / S) * S;
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     dst[i] = (c < P) ? s_priv[r * Pp + c] : s_shared[c - P];
