@@ -239,6 +239,179 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) 
   write_obs_rows(a.obs + e0 * S, nloc, S, K + 1, s_priv, Kp, s_feat_obs);
 }
 
+// ---- v2: asynchronous staging (cp.async) and no private-obs copy -----------
+// Every load of the CTA is an LDGSTS issued up front (no registers held, all
+// bytes in flight at once); the obs writer reads the portfolio straight from
+// the share table, so shared memory is ~280 B/env and 10+ CTAs fit per SM.
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+struct ObsSrc {  // obs row r = [x0[r], shares[0..K)[r], shared[0..5K)]
+  const float* x0;
+  const int32_t* sh;  // [K][kEnvBlock]
+  const float* shared;
+  int K;
+  __device__ __forceinline__ float at(int r, int c) const {
+    return c == 0 ? x0[r] : (c <= K ? (float)sh[(c - 1) * kEnvBlock + r] : shared[c - 1 - K]);
+  }
+};
+
+__device__ __forceinline__ void write_obs_v2(float* __restrict__ dst, int nrows, int S, const ObsSrc& src) {
+  const int total = nrows * S;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const int total4 = total >> 2;
+    const int step = 4 * (int)blockDim.x;
+    int f = 4 * threadIdx.x;
+    int r = f / S, c = f - r * S;
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int q = threadIdx.x; q < total4; q += blockDim.x) {
+      float v[4];
+      int rr = r, cc = c;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] = src.at(rr, cc);
+        if (++cc == S) {
+          cc = 0;
+          ++rr;
+        }
+      }
+      d4[q] = make_float4(v[0], v[1], v[2], v[3]);
+      c += step;
+      while (c >= S) {
+        c -= S;
+        ++r;
+      }
+    }
+    for (int i = total4 * 4 + threadIdx.x; i < total; i += blockDim.x) {
+      const int rr = i / S;
+      dst[i] = src.at(rr, i - rr * S);
+    }
+  } else {
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int rr = i / S;
+      dst[i] = src.at(rr, i - rr * S);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, F = 5 * K;
+  double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
+  double* s_p1 = s_p0 + K;                                      // [K]
+  double* s_bal = s_p1 + K;                                     // [kEnvBlock]
+  double* s_ret = s_bal + kEnvBlock;                            // [kEnvBlock]
+  float* s_act = reinterpret_cast<float*>(s_ret + kEnvBlock);   // [kEnvBlock*K] (+ 4 pad)
+  int32_t* s_sh = reinterpret_cast<int32_t*>(s_act + ((kEnvBlock * K + 7) & ~3));  // [K][kEnvBlock]
+  float* s_x0 = reinterpret_cast<float*>(s_sh + K * kEnvBlock);                  // [kEnvBlock]
+  float* s_feat_obs = s_x0 + kEnvBlock;                                          // [5K]
+  float* s_feat_term = s_feat_obs + F;                                           // [5K]
+  const int tid = threadIdx.x;
+  const size_t e0 = (size_t)blockIdx.x * kEnvBlock;
+  const int nloc = min(kEnvBlock, a.N - (int)e0);
+  const bool live = tid < nloc;
+  // ---- every load in flight at once ----
+  const float* src = a.actions + e0 * K;
+  const int total = nloc * K;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  const int total4 = vec_ok ? total / 4 : 0;
+  for (int q = tid; q < total4; q += kEnvBlock) cp_async16(s_act + 4 * q, src + 4 * q);
+  for (int f = total4 * 4 + tid; f < total; f += kEnvBlock) cp_async4(s_act + f, src + f);
+  if (live) {
+    for (int k = 0; k < K; ++k) cp_async4(s_sh + k * kEnvBlock + tid, a.shares + (size_t)k * a.N + e0 + tid);
+    cp_async8(s_bal + tid, a.balance + e0 + tid);
+    cp_async8(s_ret + tid, a.ep_return + e0 + tid);
+  }
+  for (int k = tid; k < K; k += kEnvBlock) {
+    cp_async8(s_p0 + k, a.close_tk + (size_t)a.t * K + k);
+    cp_async8(s_p1 + k, a.close_tk + (size_t)(a.t + 1) * K + k);
+  }
+  for (int j = tid; j < F; j += kEnvBlock) {
+    cp_async4(s_feat_obs + j, a.feat + (size_t)a.t_obs * F + j);
+    if (a.done) cp_async4(s_feat_term + j, a.feat + (size_t)(a.t + 1) * F + j);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- accounting (stock_env_step stock_env.hpp:55-103), fp64, reference order ----
+  if (live) {
+    const size_t e = e0 + tid;
+    double bal = s_bal[tid];
+    int32_t* sh = s_sh + tid;
+    const float* act = s_act + tid * K;
+    double vb = bal;
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k * kEnvBlock], s_p0[k]));
+    for (int k = 0; k < K; ++k) {
+      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
+      if (d < 0.0) {
+        const int32_t held = sh[k * kEnvBlock];
+        const double q = -min_ref(-d, (double)held);
+        const double price = s_p0[k];
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+        sh[k * kEnvBlock] = held + (int32_t)q;
+      }
+    }
+    const double cost_factor = __dadd_rn(1.0, a.cost);
+    for (int k = 0; k < K; ++k) {
+      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
+      if (d > 0.0) {
+        const double price = s_p0[k];
+        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
+        const double q = min_ref(d, max_ref(affordable, 0.0));
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+        sh[k * kEnvBlock] += (int32_t)q;
+      }
+    }
+    double va = bal;
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k * kEnvBlock], s_p1[k]));
+    const double r = __dsub_rn(va, vb);
+    const double ret = __dadd_rn(s_ret[tid], r);
+    if (a.reward) a.reward[e] = (float)r;
+    if (a.done_out) a.done_out[e] = (uint8_t)a.done;
+    s_x0[tid] = (float)__ddiv_rn(bal, a.cap);
+    if (a.done) {
+      if (a.term_ret) a.term_ret[e] = ret;
+      if (a.term_len) a.term_len[e] = a.ep_len;
+      a.balance[e] = a.cap;
+      a.ep_return[e] = 0.0;
+    } else {
+      a.balance[e] = bal;
+      a.ep_return[e] = ret;
+    }
+  }
+  __syncthreads();
+  const int S = a.S;
+  if (a.done) {  // terminal obs, then auto-reset the portfolios (env.hpp:221-229)
+    if (a.term_obs) write_obs_v2(a.term_obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_term, K});
+    __syncthreads();
+    s_x0[tid] = (float)(a.cap / a.cap);
+    for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = 0;
+    __syncthreads();
+  }
+  if (live)
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e0 + tid] = s_sh[k * kEnvBlock + tid];
+  write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K});
+}
+
+size_t stock_v2_smem_bytes(int K) {
+  return (2 * (size_t)K + 2 * kEnvBlock) * sizeof(double) + (((size_t)kEnvBlock * K + 7) & ~size_t(3)) * 4 +
+         (size_t)K * kEnvBlock * 4 + kEnvBlock * 4 + 10 * (size_t)K * 4;
+}
+
 // reset (env.hpp:186-194 -> StockTradingEnv::reset stock_env.hpp:158-163)
 __global__ void stock_reset_kernel(int N, int K, int S, double cap, const float* __restrict__ feat_row,
                                    double* balance, int32_t* shares, double* ep_return, float* obs) {
@@ -393,20 +566,25 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
   a.term_obs = d_term_obs;
   a.term_ret = d_term_ret;
   a.term_len = d_term_len;
-  const size_t smem = stock_smem_bytes(m->K);
   static bool attr_set = false;
   if (!attr_set) {
     PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PRB_CUDA(cudaFuncSetAttribute(stock_step_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
   const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
   {
     ProfScope prof(env->ctx, kProfEnvStock);
-    if (m->K <= 32)
-      stock_step_kernel<32><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
-    else
-      stock_step_kernel<64><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+    if (env->step_kernel == 2) {
+      stock_step_v2_kernel<<<grid, kEnvBlock, stock_v2_smem_bytes(m->K), env->ctx->stream>>>(a);
+    } else {
+      const size_t smem = stock_smem_bytes(m->K);
+      if (m->K <= 32)
+        stock_step_kernel<32><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+      else
+        stock_step_kernel<64><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+    }
   }
   PRB_CHECK_LAUNCH();
   env->t = done ? env->start : t1;

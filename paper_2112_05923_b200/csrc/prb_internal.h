@@ -160,6 +160,7 @@ struct prb_vecenv_s {
   prb_market_s* market = nullptr;
   prb_stock_config cfg{};
   size_t start = 0, end = 0;
+  int step_kernel = 2;     // 2: cp.async staging (default), 1: register staging (kept for A/B)
   size_t t = 0;            // uniform portfolio time index (stock_env.hpp:161)
   uint64_t step_count = 0; // uniform VecEnv step counter (env.hpp:217)
   prb::DevBuf<float> d_feat;       // [T][5K] shared obs features for this window
