@@ -261,11 +261,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 struct ObsSrc {  // obs row r = [x0[r], shares[0..K)[r], shared[0..5K)]
   const float* x0;
-  const int32_t* sh;  // [K][kEnvBlock]
+  const int32_t* sh;  // [kEnvBlock][Kp] env-major, odd stride: conflict-free both ways
   const float* shared;
-  int K;
+  int K, Kp;
   __device__ __forceinline__ float at(int r, int c) const {
-    return c == 0 ? x0[r] : (c <= K ? (float)sh[(c - 1) * kEnvBlock + r] : shared[c - 1 - K]);
+    return c == 0 ? x0[r] : (c <= K ? (float)sh[r * Kp + c - 1] : shared[c - 1 - K]);
   }
 };
 
@@ -309,14 +309,14 @@ __device__ __forceinline__ void write_obs_v2(float* __restrict__ dst, int nrows,
 
 __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K, F = 5 * K;
+  const int K = a.K, F = 5 * K, Kp = (K & 1) ? K + 2 : K + 1;
   double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
   double* s_p1 = s_p0 + K;                                      // [K]
   double* s_bal = s_p1 + K;                                     // [kEnvBlock]
   double* s_ret = s_bal + kEnvBlock;                            // [kEnvBlock]
   float* s_act = reinterpret_cast<float*>(s_ret + kEnvBlock);   // [kEnvBlock*K] (+ 4 pad)
-  int32_t* s_sh = reinterpret_cast<int32_t*>(s_act + ((kEnvBlock * K + 7) & ~3));  // [K][kEnvBlock]
-  float* s_x0 = reinterpret_cast<float*>(s_sh + K * kEnvBlock);                  // [kEnvBlock]
+  int32_t* s_sh = reinterpret_cast<int32_t*>(s_act + ((kEnvBlock * K + 7) & ~3));  // [kEnvBlock][Kp]
+  float* s_x0 = reinterpret_cast<float*>(s_sh + Kp * kEnvBlock);                  // [kEnvBlock]
   float* s_feat_obs = s_x0 + kEnvBlock;                                          // [5K]
   float* s_feat_term = s_feat_obs + F;                                           // [5K]
   const int tid = threadIdx.x;
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
   for (int q = tid; q < total4; q += kEnvBlock) cp_async16(s_act + 4 * q, src + 4 * q);
   for (int f = total4 * 4 + tid; f < total; f += kEnvBlock) cp_async4(s_act + f, src + f);
   if (live) {
-    for (int k = 0; k < K; ++k) cp_async4(s_sh + k * kEnvBlock + tid, a.shares + (size_t)k * a.N + e0 + tid);
+    for (int k = 0; k < K; ++k) cp_async4(s_sh + tid * Kp + k, a.shares + (size_t)k * a.N + e0 + tid);
     cp_async8(s_bal + tid, a.balance + e0 + tid);
     cp_async8(s_ret + tid, a.ep_return + e0 + tid);
   }
@@ -349,19 +349,19 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
   if (live) {
     const size_t e = e0 + tid;
     double bal = s_bal[tid];
-    int32_t* sh = s_sh + tid;
+    int32_t* sh = s_sh + tid * Kp;
     const float* act = s_act + tid * K;
     double vb = bal;
-    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k * kEnvBlock], s_p0[k]));
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], s_p0[k]));
     for (int k = 0; k < K; ++k) {
       const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
       if (d < 0.0) {
-        const int32_t held = sh[k * kEnvBlock];
+        const int32_t held = sh[k];
         const double q = -min_ref(-d, (double)held);
         const double price = s_p0[k];
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
-        sh[k * kEnvBlock] = held + (int32_t)q;
+        sh[k] = held + (int32_t)q;
       }
     }
     const double cost_factor = __dadd_rn(1.0, a.cost);
@@ -373,11 +373,11 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
         const double q = min_ref(d, max_ref(affordable, 0.0));
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
-        sh[k * kEnvBlock] += (int32_t)q;
+        sh[k] += (int32_t)q;
       }
     }
     double va = bal;
-    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k * kEnvBlock], s_p1[k]));
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s_p1[k]));
     const double r = __dsub_rn(va, vb);
     const double ret = __dadd_rn(s_ret[tid], r);
     if (a.reward) a.reward[e] = (float)r;
@@ -396,20 +396,20 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
   __syncthreads();
   const int S = a.S;
   if (a.done) {  // terminal obs, then auto-reset the portfolios (env.hpp:221-229)
-    if (a.term_obs) write_obs_v2(a.term_obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_term, K});
+    if (a.term_obs) write_obs_v2(a.term_obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_term, K, Kp});
     __syncthreads();
     s_x0[tid] = (float)(a.cap / a.cap);
-    for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = 0;
+    for (int k = 0; k < K; ++k) s_sh[tid * Kp + k] = 0;
     __syncthreads();
   }
   if (live)
-    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e0 + tid] = s_sh[k * kEnvBlock + tid];
-  write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K});
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e0 + tid] = s_sh[tid * Kp + k];
+  write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K, Kp});
 }
 
 size_t stock_v2_smem_bytes(int K) {
   return (2 * (size_t)K + 2 * kEnvBlock) * sizeof(double) + (((size_t)kEnvBlock * K + 7) & ~size_t(3)) * 4 +
-         (size_t)K * kEnvBlock * 4 + kEnvBlock * 4 + 10 * (size_t)K * 4;
+         (size_t)(K + 2) * kEnvBlock * 4 + kEnvBlock * 4 + 10 * (size_t)K * 4;
 }
 
 // reset (env.hpp:186-194 -> StockTradingEnv::reset stock_env.hpp:158-163)
