@@ -271,6 +271,24 @@ struct ObsSrc {  // obs row r = [x0[r], shares[0..K)[r], shared[0..5K)]
 
 __device__ __forceinline__ void write_obs_v2(float* __restrict__ dst, int nrows, int S, const ObsSrc& src) {
   const int total = nrows * S;
+  if (src.K <= 31) {
+    // Warp per row: lanes 0..K write the private part (one coalesced store),
+    // then the 5K shared features -- identical for every row, so each lane
+    // keeps its <= 5 feature values in registers for the whole block.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int P = src.K + 1, F = 5 * src.K;
+    float fv[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) fv[j] = (lane + 32 * j < F) ? src.shared[lane + 32 * j] : 0.f;
+    for (int r = warp; r < nrows; r += nw) {
+      float* row = dst + (size_t)r * S;
+      if (lane < P) row[lane] = (lane == 0) ? src.x0[r] : (float)src.sh[r * src.Kp + lane - 1];
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (lane + 32 * j < F) row[P + lane + 32 * j] = fv[j];
+    }
+    return;
+  }
   if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     const int total4 = total >> 2;
     const int step = 4 * (int)blockDim.x;
