@@ -425,6 +425,116 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
   write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K, Kp});
 }
 
+// ---- v3 (K <= 32, K even): actions straight into registers -----------------
+// Each thread's 4K action bytes are issued as float2 loads before anything
+// else and consumed from registers; the share table stays in shared memory for
+// the obs writer.  ~170 B of shared memory per env -> ~2x the resident warps
+// of v2, which is what keeps HBM busy while other CTAs run the fp64 chain.
+template <int KMAX>
+__global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, F = 5 * K, Kp = K + 1;  // K even -> odd stride
+  double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
+  double* s_p1 = s_p0 + K;                                      // [K]
+  int32_t* s_sh = reinterpret_cast<int32_t*>(s_p1 + K);         // [kEnvBlock][Kp]
+  float* s_x0 = reinterpret_cast<float*>(s_sh + Kp * kEnvBlock);  // [kEnvBlock]
+  float* s_feat_obs = s_x0 + kEnvBlock;                            // [5K]
+  float* s_feat_term = s_feat_obs + F;                             // [5K]
+  const int tid = threadIdx.x;
+  const size_t e0 = (size_t)blockIdx.x * kEnvBlock;
+  const int nloc = min(kEnvBlock, a.N - (int)e0);
+  const bool live = tid < nloc;
+  const size_t e = e0 + tid;
+  float2 act2[KMAX / 2];
+  const float2* arow = reinterpret_cast<const float2*>(a.actions + (live ? e : e0) * K);
+#pragma unroll
+  for (int j = 0; j < KMAX / 2; ++j)
+    if (2 * j < K) act2[j] = __ldg(arow + j);
+  const double bal_in = live ? a.balance[e] : 0.0;
+  const double ret_in = live ? a.ep_return[e] : 0.0;
+  if (live)
+    for (int k = 0; k < K; ++k) cp_async4(s_sh + tid * Kp + k, a.shares + (size_t)k * a.N + e);
+  for (int k = tid; k < K; k += kEnvBlock) {
+    cp_async8(s_p0 + k, a.close_tk + (size_t)a.t * K + k);
+    cp_async8(s_p1 + k, a.close_tk + (size_t)(a.t + 1) * K + k);
+  }
+  for (int j = tid; j < F; j += kEnvBlock) {
+    cp_async4(s_feat_obs + j, a.feat + (size_t)a.t_obs * F + j);
+    if (a.done) cp_async4(s_feat_term + j, a.feat + (size_t)(a.t + 1) * F + j);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (live) {
+    double bal = bal_in;
+    int32_t* sh = s_sh + tid * Kp;
+    double vb = bal;
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], s_p0[k]));
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {  // sells first (stock_env.hpp:88-90)
+      if (k < K) {
+        const float ak = (k & 1) ? act2[k >> 1].y : act2[k >> 1].x;
+        const double d = trunc(__dmul_rn(clamp_ref((double)ak, -1.0, 1.0), a.max_trade));
+        if (d < 0.0) {
+          const int32_t held = sh[k];
+          const double q = -min_ref(-d, (double)held);
+          const double price = s_p0[k];
+          const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+          sh[k] = held + (int32_t)q;
+        }
+      }
+    }
+    const double cost_factor = __dadd_rn(1.0, a.cost);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {  // then buys (:91-97)
+      if (k < K) {
+        const float ak = (k & 1) ? act2[k >> 1].y : act2[k >> 1].x;
+        const double d = trunc(__dmul_rn(clamp_ref((double)ak, -1.0, 1.0), a.max_trade));
+        if (d > 0.0) {
+          const double price = s_p0[k];
+          const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
+          const double q = min_ref(d, max_ref(affordable, 0.0));
+          const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
+          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
+          sh[k] += (int32_t)q;
+        }
+      }
+    }
+    double va = bal;
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s_p1[k]));
+    const double r = __dsub_rn(va, vb);
+    const double ret = __dadd_rn(ret_in, r);
+    if (a.reward) a.reward[e] = (float)r;
+    if (a.done_out) a.done_out[e] = (uint8_t)a.done;
+    s_x0[tid] = (float)__ddiv_rn(bal, a.cap);
+    if (a.done) {
+      if (a.term_ret) a.term_ret[e] = ret;
+      if (a.term_len) a.term_len[e] = a.ep_len;
+      a.balance[e] = a.cap;
+      a.ep_return[e] = 0.0;
+    } else {
+      a.balance[e] = bal;
+      a.ep_return[e] = ret;
+    }
+  }
+  __syncthreads();
+  const int S = a.S;
+  if (a.done) {
+    if (a.term_obs) write_obs_v2(a.term_obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_term, K, Kp});
+    __syncthreads();
+    s_x0[tid] = (float)(a.cap / a.cap);
+    for (int k = 0; k < K; ++k) s_sh[tid * Kp + k] = 0;
+    __syncthreads();
+  }
+  if (live)
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e] = s_sh[tid * Kp + k];
+  write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K, Kp});
+}
+
+size_t stock_v3_smem_bytes(int K) {
+  return 2 * (size_t)K * sizeof(double) + (size_t)(K + 1) * kEnvBlock * 4 + kEnvBlock * 4 + 10 * (size_t)K * 4;
+}
+
 size_t stock_v2_smem_bytes(int K) {
   return (2 * (size_t)K + 2 * kEnvBlock) * sizeof(double) + (((size_t)kEnvBlock * K + 7) & ~size_t(3)) * 4 +
          (size_t)(K + 2) * kEnvBlock * 4 + kEnvBlock * 4 + 10 * (size_t)K * 4;
@@ -594,7 +704,9 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
   const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
   {
     ProfScope prof(env->ctx, kProfEnvStock);
-    if (env->step_kernel == 2) {
+    if (env->step_kernel == 2 && m->K <= 32 && (m->K & 1) == 0) {
+      stock_step_v3_kernel<32><<<grid, kEnvBlock, stock_v3_smem_bytes(m->K), env->ctx->stream>>>(a);
+    } else if (env->step_kernel == 2) {
       stock_step_v2_kernel<<<grid, kEnvBlock, stock_v2_smem_bytes(m->K), env->ctx->stream>>>(a);
     } else {
       const size_t smem = stock_smem_bytes(m->K);
