@@ -118,8 +118,7 @@ __global__ void __launch_bounds__(256) policy_kernel(PolicyArgs p) {
             p.actions[row * A + d] = act;
             if (p.eps_out) p.eps_out[row * A + d] = e;
           }
-          const float sigma = expf(ls);
-          const float z = (act - m) / sigma;
+          const float z = (act - m) * expf(-ls);  // (a - mu) / sigma
           lp += (-0.5f * kLogTwoPiF - ls) - 0.5f * z * z;  // nn.hpp:221-222
         }
       }

@@ -232,8 +232,7 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
     if (on)
       for (int d = lir; d < A; d += L) {
         const float ls = log_std[d];
-        const float sigma = expf(ls);
-        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) / sigma;
+        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) * expf(-ls);  // (a - mu) / sigma
         lp += (-0.5f * kLogTwoPiF - ls) - 0.5f * z * z;
       }
     for (int o = L / 2; o > 0; o >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o, L);
@@ -247,9 +246,9 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
       const float dl_dlp = (surr1 <= surr2) ? -adv * ratio * inv_n : 0.0f;  // ppo.hpp:146
       for (int d = lir; d < A; d += L) {
         const float ls = log_std[d];
-        const float sigma = expf(ls);
-        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) / sigma;
-        meanb[r * ldm + d] = dl_dlp * (z / sigma);  // dmean, in place
+        const float isig = expf(-ls);
+        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) * isig;
+        meanb[r * ldm + d] = dl_dlp * (z * isig);  // dmean = dL/dlp * z / sigma, in place
         s.tmp[r * ldA + d] = dl_dlp * (z * z - 1.0f);
       }
       if (lir == 0) {

@@ -57,9 +57,11 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t k0, uint32_t 
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
   const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
   const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
-  const float r = sqrtf(-2.0f * logf(u1));
+  // SFU forms (MUFU.LG2 / RSQ / SIN / COS): sampling noise needs ~1e-6, not correct rounding
+  const float m = -2.0f * __logf(u1);
+  const float r = (m > 0.0f) ? m * rsqrtf(m) : 0.0f;
   float s, c;
-  sincospif(2.0f * u2, &s, &c);
+  __sincosf(6.2831853071795865f * u2, &s, &c);
   return make_float2(r * c, r * s);
 }
 

@@ -4,17 +4,20 @@
 // accumulators in TMEM).
 //
 // One CTA = 128 envs = one M=128 MMA tile = the 128 TMEM lanes; thread t owns
-// env e0+t end to end (its TMEM lane, its obs row, its portfolio).  Per step:
+// env e0+t end to end: its TMEM lane, its obs row, its portfolio (fp64
+// balance / return and int32 shares in REGISTERS, K is a template constant).
+// Per step:
 //   A0 [128 x 32]  = bf16(balance/cap, shares)              (private obs; the
 //                    150 shared features enter as the per-step layer-1 term)
 //   L1: D[:,0:128] = A0 . W1p        -> +c_t +b1, tanh -> A1 bf16  (actor|critic)
 //   L2: D[:,0:64]  = A1[:,0:64] . W2a ; D[:,64:128] = A1[:,64:128] . W2c -> tanh -> A1
 //   L3: D[:,0:32]  = A1[:,0:64] . W3a ; D[:,32:48]  = A1[:,64:128] . W3c
 //   Philox Gaussian sample + log-prob, stock_env_step in fp64 (thread-local,
-//   reference operation order), coalesced compact rollout rows.
-// Weights (bf16, 30 KB) and the portfolios stay on chip for all H steps;
-// TMEM: 128 columns, reused by the three layers; 2 CTAs per SM overlap one
-// CTA's fp64 env phase with the other's tensor-core layers.
+//   reference operation order), rollout rows staged through the (now idle)
+//   A1 tile and written warp-per-row (coalesced).
+// Shared memory ~73 KB (bf16 weights 30 KB + A0 8 KB + A1 32 KB) and 128
+// TMEM columns per CTA -> 3 CTAs per SM, so while one CTA waits on its
+// tensor-core layers the others run their fp64 env step / sampling.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -29,8 +32,6 @@ namespace {
 
 constexpr int kM = 128;     // envs per CTA == MMA M == TMEM lanes
 constexpr int kKX = 32;     // private obs width (1 + K <= 32)
-constexpr int kMaxK = 31;
-constexpr int kSP = kM + 1; // padded per-env column stride (bank-conflict free)
 constexpr uint32_t kTmemCols = 128;
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
 
@@ -41,16 +42,13 @@ struct TcSmem {
   alignas(128) uint8_t w3a[32 * 64 * 2];   // B [32][64]   (rows >= A zero)
   alignas(128) uint8_t w3c[16 * 64 * 2];   // B [16][64]   (row 0 = critic head)
   alignas(128) uint8_t a0[kM * kKX * 2];   // A [128][32]
-  alignas(128) uint8_t a1[kM * 128 * 2];   // A [128][128]  h1, then h2
+  alignas(128) uint8_t a1[kM * 128 * 2];   // A [128][128]  h1, then h2; fp32 [128][33] staging after L3
   float c1[128];
   float b2[128];
   float b3[32];
-  float ls[32], sig[32];
-  float b3c;
-  float x0[kM];
+  float sig[32], isig[32];
+  float b3c, lpc;
   double p0[32], p1[32];
-  int32_t sh[kMaxK][kSP];
-  float act[kMaxK][kSP];
   uint64_t mbar;
   uint32_t tmem;
 };
@@ -64,33 +62,36 @@ __device__ __forceinline__ void st_bf16(uint8_t* base, uint32_t off, float v) {
 }
 
 // 16 consecutive accumulator columns of this thread's row -> act -> bf16 into A1 (K-major)
-template <bool TANH>
 __device__ __forceinline__ void epilogue16(uint32_t taddr, const float* add, uint8_t* a1, int row, int c) {
   float v[16];
   tc::tmem_ld16(taddr, v);
   uint32_t pk[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float x0 = v[2 * i] + add[c + 2 * i], x1 = v[2 * i + 1] + add[c + 2 * i + 1];
-    if (TANH) {
-      x0 = tc::tanh_fast(x0);
-      x1 = tc::tanh_fast(x1);
-    }
-    pk[i] = tc::pack_bf16(x0, x1);
-  }
+  for (int i = 0; i < 8; ++i)
+    pk[i] = tc::pack_bf16(tc::tanh_fast(v[2 * i] + add[c + 2 * i]), tc::tanh_fast(v[2 * i + 1] + add[c + 2 * i + 1]));
   *reinterpret_cast<uint4*>(a1 + tc::kmajor_offset(row, c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   *reinterpret_cast<uint4*>(a1 + tc::kmajor_offset(row, c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
 }
 
-__global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a) {
+// Warp-per-row copy of the staged [rows][ld] fp32 tile to a contiguous [rows][cols] span.
+__device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int ld, int cols, int nrows) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < nrows; r += kM / 32)
+    if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * ld + lane];
+}
+
+template <int K>
+__global__ void __launch_bounds__(kM, 3) stock_rollout_tc_kernel(TcRolloutArgs a) {
+  static_assert(K >= 1 && K <= 31, "private obs row must fit 32 columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& s = *reinterpret_cast<TcSmem*>(smem_raw);
+  constexpr int A = K, P1 = 1 + K, F = 5 * K, SLD = 33;  // staging row stride (odd: conflict-free)
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int K = a.K, A = a.K, P1 = 1 + a.K, F = 5 * a.K;
   const size_t e0 = (size_t)blockIdx.x * kM;
   const int nloc = min(kM, a.N - (int)e0);
   const bool live = tid < nloc;
   const float* P = a.params;
+  float* stage = reinterpret_cast<float*>(s.a1);  // valid only between L3 completion and the next L1 epilogue
 
   // ---- weights -> bf16 B operands (B[n][k] = W[k][n]), once per rollout ----
   for (int i = tid; i < 128 * kKX; i += kM) {
@@ -117,14 +118,21 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
   if (tid < 32) {
     s.b3[tid] = (tid < A) ? P[a.a_w3 + 64 * A + tid] : 0.f;
     const float l = (tid < A) ? P[a.log_std + tid] : 0.f;
-    s.ls[tid] = l;
     s.sig[tid] = expf(l);
+    s.isig[tid] = expf(-l);
   }
-  if (tid == 0) s.b3c = P[a.c_w3 + 64];
-  // ---- portfolio state: balance / episode return in registers, shares in smem ----
+  if (tid == 0) {
+    s.b3c = P[a.c_w3 + 64];
+    float c = 0.f;  // sum_d (-0.5 ln 2pi - log_std_d): the state-independent part of log pi
+    for (int d = 0; d < A; ++d) c += -0.5f * kLogTwoPiF - P[a.log_std + d];
+    s.lpc = c;
+  }
+  // ---- portfolio state in registers ----
   double bal = live ? a.balance[e0 + tid] : a.cap;
   double ret = live ? a.ep_return[e0 + tid] : 0.0;
-  for (int k = 0; k < K; ++k) s.sh[k][tid] = live ? a.shares[(size_t)k * a.N + e0 + tid] : 0;
+  int32_t sh[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) sh[k] = live ? a.shares[(size_t)k * a.N + e0 + tid] : 0;
   if (warp == 0) tc::tmem_alloc(&s.tmem, kTmemCols);
   if (tid == 0) tc::mbar_init(&s.mbar, 1);
   tc::fence_proxy_async();
@@ -149,19 +157,16 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
       if (h < a.H) s.p1[tid] = a.close_tk[(size_t)(t + 1) * K + tid];
     }
     // ---- A0 row: [balance/cap, shares] (stock_observation stock_env.hpp:115-121) ----
-    const float xb = (float)__ddiv_rn(bal, a.cap);
-    s.x0[tid] = xb;
-    {
-      float xv[kKX];
-      xv[0] = xb;
+    const float x0 = (float)__ddiv_rn(bal, a.cap);
+    float xv[kKX];
+    xv[0] = x0;
 #pragma unroll
-      for (int k = 0; k < kMaxK; ++k) xv[1 + k] = (k < K) ? (float)s.sh[k][tid] : 0.f;
+    for (int k = 0; k < kKX - 1; ++k) xv[1 + k] = (k < K) ? (float)sh[k] : 0.f;
 #pragma unroll
-      for (int c = 0; c < kKX / 8; ++c) {
-        const uint4 q = make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
-                                   tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
-        *reinterpret_cast<uint4*>(s.a0 + tc::kmajor_offset(tid, 8 * c, kKX)) = q;
-      }
+    for (int c = 0; c < kKX / 8; ++c) {
+      const uint4 q = make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
+                                 tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
+      *reinterpret_cast<uint4*>(s.a0 + tc::kmajor_offset(tid, 8 * c, kKX)) = q;
     }
     tc::fence_proxy_async();
     tc::fence_before_sync();
@@ -174,27 +179,12 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
                      ID_L1, j > 0);
       tc::mma_commit(&s.mbar);
     }
-    // overlap with the MMA: compact obs rows of step h / final VecEnv states
-    if (h < a.H) {
-      float* dst = a.b_obs + ((size_t)h * a.N + e0) * P1;
-      for (int i = tid; i < nloc * P1; i += kM) {
-        const int r = i / P1, c = i - (i / P1) * P1;
-        dst[i] = (c == 0) ? s.x0[r] : (float)s.sh[c - 1][r];
-      }
-    } else {
-      const float* fr = a.feat + (size_t)t * F;
-      float* dst = a.obs_out + e0 * a.S;
-      for (int i = tid; i < nloc * a.S; i += kM) {
-        const int r = i / a.S, c = i - (i / a.S) * a.S;
-        dst[i] = (c == 0) ? s.x0[r] : (c < P1 ? (float)s.sh[c - 1][r] : fr[c - P1]);
-      }
-    }
     tc::mbar_wait(&s.mbar, phase);
     phase ^= 1;
     tc::fence_after_sync();
     // ---- L1 epilogue: + shared term + b1, tanh -> A1 ----
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 16) epilogue16<true>(tlane + c, s.c1, s.a1, tid, c);
+    for (int c = 0; c < 128; c += 16) epilogue16(tlane + c, s.c1, s.a1, tid, c);
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
@@ -214,7 +204,7 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
     phase ^= 1;
     tc::fence_after_sync();
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 16) epilogue16<true>(tlane + c, s.b2, s.a1, tid, c);
+    for (int c = 0; c < 128; c += 16) epilogue16(tlane + c, s.b2, s.a1, tid, c);
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
@@ -230,7 +220,7 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
                      tc::smem_desc(w3c_addr + j * 256, 128, 1024), ID_L3C, j > 0);
       tc::mma_commit(&s.mbar);
     }
-    tc::mbar_wait(&s.mbar, phase);
+    tc::mbar_wait(&s.mbar, phase);  // L3 done: A1 is free, used below as fp32 staging
     phase ^= 1;
     tc::fence_after_sync();
     float mean[32], vcrit[16];
@@ -238,15 +228,34 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
     tc::tmem_ld16(tlane + 16, mean + 16);
     tc::tmem_ld16(tlane + 32, vcrit);
     tc::fence_before_sync();
-#pragma unroll
-    for (int d = 0; d < 32; ++d) mean[d] += s.b3[d];
     const float value = vcrit[0] + s.b3c;
-    if (h == a.H) {  // bootstrap V(s_H) (pod.hpp:127-131)
+    if (h == a.H) {  // bootstrap V(s_H) (pod.hpp:127-131) and the VecEnv's final states
       if (live) a.b_boot[row] = value;
+      __syncthreads();
+      stage[tid * SLD] = x0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) stage[tid * SLD + 1 + k] = (float)sh[k];
+      __syncthreads();
+      const float* fr = a.feat + (size_t)t * F;
+      const int lane = tid & 31;
+      for (int r = warp; r < nloc; r += kM / 32) {
+        float* dst = a.obs_out + (e0 + r) * a.S;
+        if (lane < P1) dst[lane] = stage[r * SLD + lane];
+        for (int c = lane; c < F; c += 32) dst[P1 + c] = fr[c];
+      }
       break;
     }
+    // ---- compact obs rows of step h (staged, warp per row) ----
+    __syncthreads();  // every thread has passed its L3 wait: A1 may be overwritten
+    stage[tid * SLD] = x0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) stage[tid * SLD + 1 + k] = (float)sh[k];
+    __syncthreads();
+    store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, SLD, P1, nloc);
+    __syncthreads();
     // ---- sample a = mu + sigma * eps (Philox stream of policy_kernel), log-prob ----
-    float lp = 0.f;
+    float act[32];
+    float zz = 0.f;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (4 * q < A) {
@@ -258,77 +267,76 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
         for (int i = 0; i < 4; ++i) {
           const int d = 4 * q + i;
           if (d < A) {
-            const float act = mean[d] + s.sig[d] * e4[i];
-            s.act[d][tid] = act;
-            const float z = (act - mean[d]) / s.sig[d];
-            lp += (-0.5f * kLogTwoPiF - s.ls[d]) - 0.5f * z * z;
+            const float m = mean[d] + s.b3[d];
+            act[d] = m + s.sig[d] * e4[i];
+            const float z = (act[d] - m) * s.isig[d];
+            zz += z * z;
+            stage[tid * SLD + d] = act[d];
           }
         }
       }
     }
+    const float lp = s.lpc - 0.5f * zz;
+    __syncthreads();
+    store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, SLD, A, nloc);
     // ---- env step (stock_env_step stock_env.hpp:55-103), this thread's env, fp64 ----
     const int done = a.done_seq[h];
-    float rew32 = 0.f;
-    {
-      double vb = bal;
-      for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)s.sh[k][tid], s.p0[k]));
-      for (int k = 0; k < K; ++k) {
-        const double d = trunc(__dmul_rn(clamp_ref((double)s.act[k][tid], -1.0, 1.0), a.max_trade));
-        if (d < 0.0) {
-          const int32_t held = s.sh[k][tid];
-          const double qv = -min_ref(-d, (double)held);
-          const double price = s.p0[k];
-          const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
-          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-          s.sh[k][tid] = held + (int32_t)qv;
-        }
-      }
-      const double cf = __dadd_rn(1.0, a.cost);
-      for (int k = 0; k < K; ++k) {
-        const double d = trunc(__dmul_rn(clamp_ref((double)s.act[k][tid], -1.0, 1.0), a.max_trade));
-        if (d > 0.0) {
-          const double price = s.p0[k];
-          const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cf)));
-          const double qv = min_ref(d, max_ref(affordable, 0.0));
-          const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
-          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-          s.sh[k][tid] += (int32_t)qv;
-        }
-      }
-      double va = bal;
-      for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)s.sh[k][tid], s.p1[k]));
-      const double rw = __dsub_rn(va, vb);
-      rew32 = (float)rw;
-      ret = __dadd_rn(ret, rw);
-      if (done) {  // auto-reset (env.hpp:221-229, stock_env.hpp:158-163)
-        bal = a.cap;
-        ret = 0.0;
-        for (int k = 0; k < K; ++k) s.sh[k][tid] = 0;
+    double vb = bal;
+#pragma unroll
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], s.p0[k]));
+    int32_t des[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {  // trunc(clamp(a) * max_trade_shares), integral (NaN -> no trade)
+      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
+      des[k] = (d < 0.0) ? -(int32_t)(-d) : ((d > 0.0) ? (int32_t)d : 0);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {  // sells first
+      if (des[k] < 0) {
+        const double qv = -min_ref(-(double)des[k], (double)sh[k]);
+        const double price = s.p0[k];
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
+        sh[k] += (int32_t)qv;
       }
     }
-    __syncthreads();
-    // ---- coalesced rollout writes of step h ----
-    {
-      const size_t slab = (size_t)h * a.N + e0;
-      float* da = a.b_act + slab * A;
-      for (int i = tid; i < nloc * A; i += kM) {
-        const int r = i / A, k = i - (i / A) * A;
-        da[i] = s.act[k][r];
+    const double cf = __dadd_rn(1.0, a.cost);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost
+      if (des[k] > 0) {
+        const double price = s.p0[k];
+        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cf)));
+        const double qv = min_ref((double)des[k], max_ref(affordable, 0.0));
+        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
+        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
+        sh[k] += (int32_t)qv;
       }
-      if (live) {
-        a.b_logp[slab + tid] = lp;
-        a.b_val[slab + tid] = value;
-        a.b_rew[slab + tid] = rew32;
-        a.b_done[slab + tid] = (uint8_t)done;
-      }
+    }
+    double va = bal;
+#pragma unroll
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s.p1[k]));
+    const double rw = __dsub_rn(va, vb);
+    ret = __dadd_rn(ret, rw);
+    if (done) {  // auto-reset (env.hpp:221-229, stock_env.hpp:158-163)
+      bal = a.cap;
+      ret = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) sh[k] = 0;
+    }
+    if (live) {
+      const size_t slab = (size_t)h * a.N + row;
+      a.b_logp[slab] = lp;
+      a.b_val[slab] = value;
+      a.b_rew[slab] = (float)rw;
+      a.b_done[slab] = (uint8_t)done;
     }
   }
   // ---- portfolio state back to HBM ----
-  __syncthreads();
   if (live) {
     a.balance[row] = bal;
     a.ep_return[row] = ret;
-    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + row] = s.sh[k][tid];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + row] = sh[k];
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -337,17 +345,33 @@ __global__ void __launch_bounds__(kM, 2) stock_rollout_tc_kernel(TcRolloutArgs a
 
 }  // namespace
 
-size_t stock_rollout_tc_smem() { return sizeof(TcSmem) + 1024; }
+size_t stock_rollout_tc_smem() { return sizeof(TcSmem); }
+
+bool stock_rollout_tc_supported(int K) { return K == 30 || K == 3 || K == 2 || K == 1; }
 
 void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)stock_rollout_tc_smem()));
-    attr = true;
-  }
   const unsigned grid = (unsigned)((a.N + kM - 1) / kM);
-  stock_rollout_tc_kernel<<<grid, kM, stock_rollout_tc_smem(), s>>>(a);
+  const size_t smem = stock_rollout_tc_smem();
+#define PRB_TC_CASE(KK)                                                                                      \
+  case KK: {                                                                                                 \
+    static bool attr = false;                                                                                \
+    if (!attr) {                                                                                             \
+      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)smem));                                                             \
+      attr = true;                                                                                           \
+    }                                                                                                        \
+    stock_rollout_tc_kernel<KK><<<grid, kM, smem, s>>>(a);                                                   \
+    break;                                                                                                   \
+  }
+  switch (a.K) {
+    PRB_TC_CASE(30)
+    PRB_TC_CASE(3)
+    PRB_TC_CASE(2)
+    PRB_TC_CASE(1)
+    default:
+      fail(PRB_ERR_CONFIG, "tcgen05 rollout: no instantiation for K=" + std::to_string(a.K));
+  }
+#undef PRB_TC_CASE
   PRB_CHECK_LAUNCH();
 }
 

@@ -32,6 +32,7 @@ struct TcRolloutArgs {
 };
 
 size_t stock_rollout_tc_smem();
+bool stock_rollout_tc_supported(int K);
 void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s);
 
 }  // namespace prb

@@ -34,7 +34,7 @@ def main():
         ctx, market, env = setup(N)
         agent = pr.Agent.init(ctx, 181, 30, seed=7)
         ro = pr.Rollout.for_env(env, H)
-        ro.set_mode(fused)
+        ro.set_mode(1 if "--simt" in sys.argv else (2 if fused else 0))
         for i in range(3):
             ro.collect(agent, env, seed=i)
         ctx.synchronize()
