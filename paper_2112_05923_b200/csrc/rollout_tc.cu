@@ -6,18 +6,21 @@
 // One CTA = 128 envs = one M=128 MMA tile = the 128 TMEM lanes; thread t owns
 // env e0+t end to end: its TMEM lane, its obs row, its portfolio (fp64
 // balance / return and int32 shares in REGISTERS, K is a template constant).
-// Per step:
-//   A0 [128 x 32]  = bf16(balance/cap, shares)              (private obs; the
-//                    150 shared features enter as the per-step layer-1 term)
-//   L1: D[:,0:128] = A0 . W1p        -> +c_t +b1, tanh -> A1 bf16  (actor|critic)
-//   L2: D[:,0:64]  = A1[:,0:64] . W2a ; D[:,64:128] = A1[:,64:128] . W2c -> tanh -> A1
-//   L3: D[:,0:32]  = A1[:,0:64] . W3a ; D[:,32:48]  = A1[:,64:128] . W3c
+// Per step (D = the CTA's 128 TMEM columns, X = one 16 KB bf16 operand tile):
+//   X  <- bf16(balance/cap, shares)               [128 x 32]  private obs
+//   L1 : D[0:128]  = X . W1p          (actor | critic; the 150 shared
+//                                      features enter as the per-step term c_t)
+//   X  <- tanh(D[0:64] + c_t)          actor h1      L2a: D[0:64]   = X . W2a
+//   X  <- tanh(D[64:128] + c_t)        critic h1     L2c: D[64:128] = X . W2c
+//   X  <- tanh(D[0:64] + b2)           actor h2      L3a: D[0:32]   = X . W3a
+//   X  <- tanh(D[64:128] + b2)         critic h2     L3c: D[32:48]  = X . W3c
 //   Philox Gaussian sample + log-prob, stock_env_step in fp64 (thread-local,
-//   reference operation order), rollout rows staged through the (now idle)
-//   A1 tile and written warp-per-row (coalesced).
-// Shared memory ~73 KB (bf16 weights 30 KB + A0 8 KB + A1 32 KB) and 128
-// TMEM columns per CTA -> 3 CTAs per SM, so while one CTA waits on its
-// tensor-core layers the others run their fp64 env step / sampling.
+//   reference operation order), rollout rows staged through X and written
+//   warp-per-row (coalesced).
+// One operand tile reused five times keeps shared memory at ~49 KB/CTA and
+// TMEM at 128 columns/CTA, so 4 CTAs (512 envs) are resident per SM: the
+// 65,536-env configs[1] VecEnv (512 tiles) runs as a single wave, and while one
+// CTA waits on its tensor-core layer the others run epilogues / env steps.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -34,6 +37,7 @@ constexpr int kM = 128;     // envs per CTA == MMA M == TMEM lanes
 constexpr int kKX = 32;     // private obs width (1 + K <= 32)
 constexpr uint32_t kTmemCols = 128;
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
+constexpr int kSLD = 31;    // fp32 staging row stride (odd: conflict-free both ways)
 
 struct TcSmem {
   alignas(128) uint8_t w1[128 * kKX * 2];  // B [n=128][k=32]  W1 private rows, actor | critic
@@ -41,8 +45,7 @@ struct TcSmem {
   alignas(128) uint8_t w2c[64 * 64 * 2];
   alignas(128) uint8_t w3a[32 * 64 * 2];   // B [32][64]   (rows >= A zero)
   alignas(128) uint8_t w3c[16 * 64 * 2];   // B [16][64]   (row 0 = critic head)
-  alignas(128) uint8_t a0[kM * kKX * 2];   // A [128][32]
-  alignas(128) uint8_t a1[kM * 128 * 2];   // A [128][128]  h1, then h2; fp32 [128][33] staging after L3
+  alignas(128) uint8_t x[kM * 64 * 2];     // A tile: [128][32] obs, [128][64] h, fp32 [128][31] staging
   float c1[128];
   float b2[128];
   float b3[32];
@@ -61,37 +64,64 @@ __device__ __forceinline__ void st_bf16(uint8_t* base, uint32_t off, float v) {
   *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(v);
 }
 
-// 16 consecutive accumulator columns of this thread's row -> act -> bf16 into A1 (K-major)
-__device__ __forceinline__ void epilogue16(uint32_t taddr, const float* add, uint8_t* a1, int row, int c) {
-  float v[16];
-  tc::tmem_ld16(taddr, v);
-  uint32_t pk[8];
+// 64 accumulator columns [col, col+64) of this thread's row -> tanh(. + add) -> bf16 X [128][64]
+__device__ __forceinline__ void epilogue64(uint32_t tlane, int col, const float* add, uint8_t* x, int row) {
+#pragma unroll 1
+  for (int c = 0; c < 64; c += 16) {
+    float v[16];
+    tc::tmem_ld16(tlane + col + c, v);
+    uint32_t pk[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    pk[i] = tc::pack_bf16(tc::tanh_fast(v[2 * i] + add[c + 2 * i]), tc::tanh_fast(v[2 * i + 1] + add[c + 2 * i + 1]));
-  *reinterpret_cast<uint4*>(a1 + tc::kmajor_offset(row, c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-  *reinterpret_cast<uint4*>(a1 + tc::kmajor_offset(row, c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    for (int i = 0; i < 8; ++i)
+      pk[i] = tc::pack_bf16(tc::tanh_fast(v[2 * i] + add[col + c + 2 * i]),
+                            tc::tanh_fast(v[2 * i + 1] + add[col + c + 2 * i + 1]));
+    *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c, 64)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c + 8, 64)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  }
 }
 
-// Warp-per-row copy of the staged [rows][ld] fp32 tile to a contiguous [rows][cols] span.
-__device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int ld, int cols, int nrows) {
+// X written by the threads -> visible to the tensor core; all TMEM reads done.
+__device__ __forceinline__ void publish_operand() {
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+}
+
+// thread 0: D[d_col..] (+)= X[128 x 16*ksteps] . B ; commit; everyone waits.
+__device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32_t x_addr, uint32_t x_sbo,
+                                          uint32_t b_addr, uint32_t b_sbo, int ksteps, uint32_t idesc,
+                                          uint64_t* mbar, uint32_t& phase) {
+  if (threadIdx.x == 0) {
+    tc::fence_after_sync();
+    for (int j = 0; j < ksteps; ++j)
+      tc::mma_bf16(tbase + d_col, tc::smem_desc(x_addr + j * 256, 128, x_sbo), tc::smem_desc(b_addr + j * 256, 128, b_sbo),
+                   idesc, j > 0);
+    tc::mma_commit(mbar);
+  }
+  tc::mbar_wait(mbar, phase);
+  phase ^= 1;
+  tc::fence_after_sync();
+}
+
+// Warp-per-row copy of the staged [rows][kSLD] fp32 tile to a contiguous [rows][cols] span.
+__device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int cols, int nrows) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = warp; r < nrows; r += kM / 32)
-    if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * ld + lane];
+    if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * kSLD + lane];
 }
 
 template <int K>
-__global__ void __launch_bounds__(kM, 3) stock_rollout_tc_kernel(TcRolloutArgs a) {
-  static_assert(K >= 1 && K <= 31, "private obs row must fit 32 columns");
+__global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a) {
+  static_assert(K >= 1 && K <= 30, "private obs row and staging must fit 31 columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& s = *reinterpret_cast<TcSmem*>(smem_raw);
-  constexpr int A = K, P1 = 1 + K, F = 5 * K, SLD = 33;  // staging row stride (odd: conflict-free)
+  constexpr int A = K, P1 = 1 + K, F = 5 * K;
   const int tid = threadIdx.x, warp = tid >> 5;
   const size_t e0 = (size_t)blockIdx.x * kM;
   const int nloc = min(kM, a.N - (int)e0);
   const bool live = tid < nloc;
   const float* P = a.params;
-  float* stage = reinterpret_cast<float*>(s.a1);  // valid only between L3 completion and the next L1 epilogue
+  float* stage = reinterpret_cast<float*>(s.x);
 
   // ---- weights -> bf16 B operands (B[n][k] = W[k][n]), once per rollout ----
   for (int i = tid; i < 128 * kKX; i += kM) {
@@ -135,13 +165,12 @@ __global__ void __launch_bounds__(kM, 3) stock_rollout_tc_kernel(TcRolloutArgs a
   for (int k = 0; k < K; ++k) sh[k] = live ? a.shares[(size_t)k * a.N + e0 + tid] : 0;
   if (warp == 0) tc::tmem_alloc(&s.tmem, kTmemCols);
   if (tid == 0) tc::mbar_init(&s.mbar, 1);
-  tc::fence_proxy_async();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = s.tmem;
   const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
-  const uint32_t a0_addr = tc::smem_u32(s.a0), a1_addr = tc::smem_u32(s.a1);
+  const uint32_t x_addr = tc::smem_u32(s.x);
   const uint32_t w1_addr = tc::smem_u32(s.w1), w2a_addr = tc::smem_u32(s.w2a), w2c_addr = tc::smem_u32(s.w2c);
   const uint32_t w3a_addr = tc::smem_u32(s.w3a), w3c_addr = tc::smem_u32(s.w3c);
   constexpr uint32_t ID_L1 = tc::idesc_bf16(128, 128), ID_L2 = tc::idesc_bf16(128, 64);
@@ -151,149 +180,111 @@ __global__ void __launch_bounds__(kM, 3) stock_rollout_tc_kernel(TcRolloutArgs a
 
   for (int h = 0; h <= a.H; ++h) {
     const int t = a.t_seq[h];
+    __syncthreads();  // previous step's staging reads of X are done
     s.c1[tid] = a.shared_l1[(size_t)h * 128 + tid] + b1_mine;
     if (tid < K) {
       s.p0[tid] = a.close_tk[(size_t)t * K + tid];
       if (h < a.H) s.p1[tid] = a.close_tk[(size_t)(t + 1) * K + tid];
     }
-    // ---- A0 row: [balance/cap, shares] (stock_observation stock_env.hpp:115-121) ----
+    // ---- X <- [balance/cap, shares] (stock_observation stock_env.hpp:115-121) ----
     const float x0 = (float)__ddiv_rn(bal, a.cap);
-    float xv[kKX];
-    xv[0] = x0;
+    {
+      float xv[kKX];
+      xv[0] = x0;
 #pragma unroll
-    for (int k = 0; k < kKX - 1; ++k) xv[1 + k] = (k < K) ? (float)sh[k] : 0.f;
+      for (int k = 0; k < kKX - 1; ++k) xv[1 + k] = (k < K) ? (float)sh[k] : 0.f;
 #pragma unroll
-    for (int c = 0; c < kKX / 8; ++c) {
-      const uint4 q = make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
-                                 tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
-      *reinterpret_cast<uint4*>(s.a0 + tc::kmajor_offset(tid, 8 * c, kKX)) = q;
+      for (int c = 0; c < kKX / 8; ++c)
+        *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(tid, 8 * c, kKX)) =
+            make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
+                       tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
     }
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (tid == 0) {  // ---- L1: [128x32] . [32x128] ----
-      tc::fence_after_sync();
-#pragma unroll
-      for (int j = 0; j < kKX / 16; ++j)
-        tc::mma_bf16(tbase, tc::smem_desc(a0_addr + j * 256, 128, kKX * 16), tc::smem_desc(w1_addr + j * 256, 128, kKX * 16),
-                     ID_L1, j > 0);
-      tc::mma_commit(&s.mbar);
-    }
-    tc::mbar_wait(&s.mbar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-    // ---- L1 epilogue: + shared term + b1, tanh -> A1 ----
-#pragma unroll 1
-    for (int c = 0; c < 128; c += 16) epilogue16(tlane + c, s.c1, s.a1, tid, c);
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (tid == 0) {  // ---- L2: actor / critic [128x64] . [64x64] ----
-      tc::fence_after_sync();
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        tc::mma_bf16(tbase, tc::smem_desc(a1_addr + j * 256, 128, 2048), tc::smem_desc(w2a_addr + j * 256, 128, 1024),
-                     ID_L2, j > 0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        tc::mma_bf16(tbase + 64, tc::smem_desc(a1_addr + 1024 + j * 256, 128, 2048),
-                     tc::smem_desc(w2c_addr + j * 256, 128, 1024), ID_L2, j > 0);
-      tc::mma_commit(&s.mbar);
-    }
-    tc::mbar_wait(&s.mbar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-#pragma unroll 1
-    for (int c = 0; c < 128; c += 16) epilogue16(tlane + c, s.b2, s.a1, tid, c);
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (tid == 0) {  // ---- L3: actor head [128x64].[64x32], critic head [128x64].[64x16] ----
-      tc::fence_after_sync();
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        tc::mma_bf16(tbase, tc::smem_desc(a1_addr + j * 256, 128, 2048), tc::smem_desc(w3a_addr + j * 256, 128, 1024),
-                     ID_L3A, j > 0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        tc::mma_bf16(tbase + 32, tc::smem_desc(a1_addr + 1024 + j * 256, 128, 2048),
-                     tc::smem_desc(w3c_addr + j * 256, 128, 1024), ID_L3C, j > 0);
-      tc::mma_commit(&s.mbar);
-    }
-    tc::mbar_wait(&s.mbar, phase);  // L3 done: A1 is free, used below as fp32 staging
-    phase ^= 1;
-    tc::fence_after_sync();
-    float mean[32], vcrit[16];
-    tc::tmem_ld16(tlane + 0, mean);
-    tc::tmem_ld16(tlane + 16, mean + 16);
+    publish_operand();
+    mma_layer(tbase, 0, x_addr, kKX * 16, w1_addr, kKX * 16, kKX / 16, ID_L1, &s.mbar, phase);   // L1
+    epilogue64(tlane, 0, s.c1, s.x, tid);                                                          // actor h1
+    publish_operand();
+    mma_layer(tbase, 0, x_addr, 1024, w2a_addr, 1024, 4, ID_L2, &s.mbar, phase);                    // L2a
+    epilogue64(tlane, 64, s.c1, s.x, tid);                                                         // critic h1
+    publish_operand();
+    mma_layer(tbase, 64, x_addr, 1024, w2c_addr, 1024, 4, ID_L2, &s.mbar, phase);                   // L2c
+    epilogue64(tlane, 0, s.b2, s.x, tid);                                                          // actor h2
+    publish_operand();
+    mma_layer(tbase, 0, x_addr, 1024, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase);                   // L3a
+    epilogue64(tlane, 64, s.b2, s.x, tid);                                                         // critic h2
+    publish_operand();
+    mma_layer(tbase, 32, x_addr, 1024, w3c_addr, 1024, 4, ID_L3C, &s.mbar, phase);                  // L3c
+    float vcrit[16];
     tc::tmem_ld16(tlane + 32, vcrit);
-    tc::fence_before_sync();
     const float value = vcrit[0] + s.b3c;
+    __syncthreads();  // every thread is past its L3c wait: X is free for fp32 staging
     if (h == a.H) {  // bootstrap V(s_H) (pod.hpp:127-131) and the VecEnv's final states
+      tc::fence_before_sync();
       if (live) a.b_boot[row] = value;
-      __syncthreads();
-      stage[tid * SLD] = x0;
+      stage[tid * kSLD] = x0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) stage[tid * SLD + 1 + k] = (float)sh[k];
+      for (int k = 0; k < K; ++k) stage[tid * kSLD + 1 + k] = (float)sh[k];
       __syncthreads();
       const float* fr = a.feat + (size_t)t * F;
       const int lane = tid & 31;
       for (int r = warp; r < nloc; r += kM / 32) {
         float* dst = a.obs_out + (e0 + r) * a.S;
-        if (lane < P1) dst[lane] = stage[r * SLD + lane];
+        if (lane < P1) dst[lane] = stage[r * kSLD + lane];
         for (int c = lane; c < F; c += 32) dst[P1 + c] = fr[c];
       }
       break;
     }
-    // ---- compact obs rows of step h (staged, warp per row) ----
-    __syncthreads();  // every thread has passed its L3 wait: A1 may be overwritten
-    stage[tid * SLD] = x0;
+    // ---- compact obs rows of step h ----
+    stage[tid * kSLD] = x0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) stage[tid * SLD + 1 + k] = (float)sh[k];
+    for (int k = 0; k < K; ++k) stage[tid * kSLD + 1 + k] = (float)sh[k];
     __syncthreads();
-    store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, SLD, P1, nloc);
+    store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, P1, nloc);
     __syncthreads();
-    // ---- sample a = mu + sigma * eps (Philox stream of policy_kernel), log-prob ----
-    float act[32];
+    // ---- a = mu + sigma * eps (Philox stream of policy_kernel), log-prob; actions staged ----
     float zz = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (4 * q < A) {
-        const Philox4 rr = philox4x32_10((uint32_t)a.seed, (uint32_t)(a.seed >> 32), (uint32_t)q, (uint32_t)row,
-                                         (uint32_t)h, 0u);
-        const float2 z0 = box_muller(rr.x, rr.y), z1 = box_muller(rr.z, rr.w);
-        const float e4[4] = {z0.x, z0.y, z1.x, z1.y};
+    for (int half = 0; half < 2; ++half) {
+      if (16 * half < A) {
+        float mean[16];
+        tc::tmem_ld16(tlane + 16 * half, mean);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int d = 4 * q + i;
-          if (d < A) {
-            const float m = mean[d] + s.b3[d];
-            act[d] = m + s.sig[d] * e4[i];
-            const float z = (act[d] - m) * s.isig[d];
-            zz += z * z;
-            stage[tid * SLD + d] = act[d];
+        for (int qq = 0; qq < 4; ++qq) {
+          const int q = 4 * half + qq;
+          if (4 * q < A) {
+            const Philox4 rr = philox4x32_10((uint32_t)a.seed, (uint32_t)(a.seed >> 32), (uint32_t)q, (uint32_t)row,
+                                             (uint32_t)h, 0u);
+            const float2 z0 = box_muller(rr.x, rr.y), z1 = box_muller(rr.z, rr.w);
+            const float e4[4] = {z0.x, z0.y, z1.x, z1.y};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int d = 4 * q + i;
+              if (d < A) {
+                const float m = mean[4 * qq + i] + s.b3[d];
+                const float act = m + s.sig[d] * e4[i];
+                const float z = (act - m) * s.isig[d];
+                zz += z * z;
+                stage[tid * kSLD + d] = act;
+              }
+            }
           }
         }
       }
     }
+    tc::fence_before_sync();
     const float lp = s.lpc - 0.5f * zz;
     __syncthreads();
-    store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, SLD, A, nloc);
+    store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, A, nloc);
     // ---- env step (stock_env_step stock_env.hpp:55-103), this thread's env, fp64 ----
+    const float* my = stage + tid * kSLD;
     const int done = a.done_seq[h];
     double vb = bal;
 #pragma unroll
     for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], s.p0[k]));
-    int32_t des[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {  // trunc(clamp(a) * max_trade_shares), integral (NaN -> no trade)
-      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
-      des[k] = (d < 0.0) ? -(int32_t)(-d) : ((d > 0.0) ? (int32_t)d : 0);
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {  // sells first
-      if (des[k] < 0) {
-        const double qv = -min_ref(-(double)des[k], (double)sh[k]);
+    for (int k = 0; k < K; ++k) {  // sells first (:88-90)
+      const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
+      if (d < 0.0) {
+        const double qv = -min_ref(-d, (double)sh[k]);
         const double price = s.p0[k];
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
@@ -302,11 +293,12 @@ __global__ void __launch_bounds__(kM, 3) stock_rollout_tc_kernel(TcRolloutArgs a
     }
     const double cf = __dadd_rn(1.0, a.cost);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost
-      if (des[k] > 0) {
+    for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
+      const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
+      if (d > 0.0) {
         const double price = s.p0[k];
         const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cf)));
-        const double qv = min_ref((double)des[k], max_ref(affordable, 0.0));
+        const double qv = min_ref(d, max_ref(affordable, 0.0));
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
         sh[k] += (int32_t)qv;
