@@ -1,0 +1,375 @@
+// podracer_b200.hpp -- header-only C++ drop-in for the reference's pod hot-path
+// API (ElegantRL-podracer, /root/reference/proj/include/podracer), implemented
+// over the prb_* C ABI (include/prb.h, libprb.so).
+//
+// Names, argument meaning, value semantics and exceptions follow the reference:
+//   VectorizedEnvironment::reset/step/states/step_counts   env.hpp:167-249
+//   policy_sample / policy_mean / gaussian_log_prob         nn.hpp:229-270
+//   adam_step                                               nn.hpp:164-182
+//   worker_collect + TransitionBuffer                       pod.hpp:95-132, buffer.hpp:27-135
+//   buffer_advantages                                       ppo.hpp:212-244
+//   ppo_update                                              ppo.hpp:249-296
+//   fuse_parameters                                         pod.hpp:141-172
+//   leaderboard ranking                                     tournament.hpp:104-119
+// Each status code returned by the C ABI is rethrown as the matching
+// exception class of common.hpp:19-71.  Host tensors are row-major double,
+// exactly the reference's Tensor2 layout; the device keeps fp32 / fp64 copies.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../prb.h"
+
+namespace podracer_b200 {
+
+// ---- exceptions (common.hpp:19-71) -------------------------------------------
+struct DimensionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumericError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct UsageError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct FormatError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DataError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CorruptionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct VersionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DomainError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+inline void check(int rc) {
+  if (rc == PRB_OK) return;
+  const std::string m = prb_last_error();
+  switch (rc) {
+    case PRB_ERR_DIMENSION: throw DimensionError(m);
+    case PRB_ERR_NUMERIC: throw NumericError(m);
+    case PRB_ERR_USAGE: throw UsageError(m);
+    case PRB_ERR_FORMAT: throw FormatError(m);
+    case PRB_ERR_DATA: throw DataError(m);
+    case PRB_ERR_CONFIG: throw ConfigError(m);
+    case PRB_ERR_CORRUPTION: throw CorruptionError(m);
+    case PRB_ERR_VERSION: throw VersionError(m);
+    case PRB_ERR_DOMAIN: throw DomainError(m);
+    default: throw DeviceError(m);
+  }
+}
+
+// ---- value types mirroring the reference ----------------------------------------
+struct Tensor2 {  // tensor.hpp:13-32
+  std::size_t rows = 0, cols = 0;
+  std::vector<double> data;
+  Tensor2() = default;
+  Tensor2(std::size_t r, std::size_t c, double fill = 0.0) : rows(r), cols(c), data(r * c, fill) {}
+  double& at(std::size_t r, std::size_t c) { return data[r * cols + c]; }
+  double at(std::size_t r, std::size_t c) const { return data[r * cols + c]; }
+  std::string shape_str() const { return "[" + std::to_string(rows) + "x" + std::to_string(cols) + "]"; }
+};
+
+struct StockConfig {  // stock_env.hpp:15-19
+  double initial_capital = 1'000'000.0;
+  double max_trade_shares = 100.0;
+  double cost_rate = 0.002;
+};
+
+struct VecStepInfo {  // env.hpp:153-158
+  bool episode_end = false;
+  std::vector<double> terminal_state;
+  double episode_return = 0.0;
+  std::size_t episode_length = 0;
+};
+
+struct VecStepResult {  // env.hpp:160-165
+  Tensor2 next_states;
+  std::vector<double> rewards;
+  std::vector<std::uint8_t> dones;
+  std::vector<VecStepInfo> infos;
+};
+
+struct PpoConfig {  // ppo.hpp:18-27
+  double gamma = 0.99, gae_lambda = 0.95, clip_eps = 0.2, entropy_coef = 0.01, value_coef = 0.5;
+  std::size_t epochs_per_update = 4, minibatch_size = 1024, buffer_size = 4096;
+  double learning_rate = 1e-3;
+  prb_ppo_config c() const {
+    return prb_ppo_config{gamma, gae_lambda, clip_eps, entropy_coef, value_coef, epochs_per_update, minibatch_size,
+                          buffer_size, learning_rate};
+  }
+};
+
+struct PpoUpdateStats {  // ppo.hpp:198-203
+  double mean_policy_loss = 0.0, mean_value_loss = 0.0, mean_entropy = 0.0;
+  std::size_t minibatches = 0;
+};
+
+struct PolicySample {  // nn.hpp:245-248
+  Tensor2 actions;
+  std::vector<double> log_probs;
+};
+
+// ---- device handles ------------------------------------------------------------
+class Context {
+ public:
+  explicit Context(int device = 0) { check(prb_ctx_create(device, &h_)); }
+  ~Context() { prb_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  prb_ctx get() const { return h_; }
+  void synchronize() const { check(prb_ctx_synchronize(h_)); }
+
+ private:
+  prb_ctx h_ = nullptr;
+};
+
+// Device-side MarketData (market.hpp:104-131): close [K][T], indicators [4][K][T].
+class MarketData {
+ public:
+  MarketData(Context& ctx, const std::vector<double>& close, const std::vector<double>* indicators, std::size_t T,
+             int K) {
+    check(prb_market_create(ctx.get(), close.data(), indicators ? indicators->data() : nullptr, T, K, &h_));
+  }
+  ~MarketData() { prb_market_destroy(h_); }
+  MarketData(const MarketData&) = delete;
+  MarketData& operator=(const MarketData&) = delete;
+  prb_market get() const { return h_; }
+
+ private:
+  prb_market h_ = nullptr;
+};
+
+class VectorizedEnvironment {  // env.hpp:167-249
+ public:
+  static std::unique_ptr<VectorizedEnvironment> stock(const MarketData& m, const StockConfig& cfg, std::size_t start,
+                                                      std::size_t end, std::size_t num_envs) {
+    prb_stock_config c{cfg.initial_capital, cfg.max_trade_shares, cfg.cost_rate};
+    prb_vecenv h = nullptr;
+    check(prb_vecenv_create_stock(m.get(), &c, start, end, num_envs, &h));
+    return std::unique_ptr<VectorizedEnvironment>(new VectorizedEnvironment(h));
+  }
+  static std::unique_ptr<VectorizedEnvironment> pointmass(Context& ctx, std::size_t num_envs) {
+    prb_vecenv h = nullptr;
+    check(prb_vecenv_create_pointmass(ctx.get(), num_envs, &h));
+    return std::unique_ptr<VectorizedEnvironment>(new VectorizedEnvironment(h));
+  }
+  ~VectorizedEnvironment() { prb_vecenv_destroy(h_); }
+  VectorizedEnvironment(const VectorizedEnvironment&) = delete;
+  VectorizedEnvironment& operator=(const VectorizedEnvironment&) = delete;
+
+  std::size_t num_envs() const { return prb_vecenv_num_envs(h_); }
+  const prb_env_spec& spec() const { return spec_; }
+  prb_vecenv get() const { return h_; }
+
+  Tensor2 reset(std::uint64_t seed) {
+    Tensor2 s(num_envs(), spec_.state_dim);
+    check(prb_vecenv_reset_host(h_, seed, s.data.data()));
+    return s;
+  }
+  Tensor2 states() const {
+    Tensor2 s(num_envs(), spec_.state_dim);
+    check(prb_vecenv_states_host(h_, s.data.data()));
+    return s;
+  }
+  std::vector<std::size_t> step_counts() const {
+    std::vector<std::uint64_t> c(num_envs());
+    check(prb_vecenv_step_counts_host(h_, c.data()));
+    return std::vector<std::size_t>(c.begin(), c.end());
+  }
+  VecStepResult step(const Tensor2& actions) {
+    const std::size_t N = num_envs(), S = spec_.state_dim, A = spec_.action_dim;
+    if (actions.rows != N || actions.cols != A)  // env.hpp:201-205
+      throw DimensionError("vec_step: actions " + actions.shape_str() + " vs expected [" + std::to_string(N) + "x" +
+                           std::to_string(A) + "]");
+    VecStepResult out;
+    out.next_states = Tensor2(N, S);
+    out.rewards.resize(N);
+    out.dones.resize(N);
+    std::vector<double> term(N * S), tret(N);
+    std::vector<std::uint64_t> tlen(N);
+    check(prb_vecenv_step_host(h_, actions.data.data(), out.next_states.data.data(), out.rewards.data(),
+                               out.dones.data(), term.data(), tret.data(), tlen.data()));
+    out.infos.resize(N);
+    for (std::size_t i = 0; i < N; ++i) {
+      if (!out.dones[i]) continue;
+      out.infos[i].episode_end = true;
+      out.infos[i].terminal_state.assign(term.begin() + i * S, term.begin() + (i + 1) * S);
+      out.infos[i].episode_return = tret[i];
+      out.infos[i].episode_length = tlen[i];
+    }
+    return out;
+  }
+
+ private:
+  explicit VectorizedEnvironment(prb_vecenv h) : h_(h) { check(prb_vecenv_spec(h_, &spec_)); }
+  prb_vecenv h_ = nullptr;
+  prb_env_spec spec_{};
+};
+
+// Device AgentArtifact: actor (GaussianPolicy) + critic + Adam state in the
+// canonical flat layout (artifact.hpp:35-51).
+class Agent {
+ public:
+  Agent(Context& ctx, std::size_t state_dim, std::size_t action_dim, std::vector<std::size_t> hidden = {64, 64})
+      : ctx_(&ctx), S_(state_dim), A_(action_dim), hidden_(std::move(hidden)) {
+    check(prb_agent_create(ctx.get(), S_, A_, hidden_.data(), (int)hidden_.size(), &h_));
+  }
+  ~Agent() { prb_agent_destroy(h_); }
+  Agent(const Agent&) = delete;
+  Agent& operator=(const Agent&) = delete;
+
+  // artifact_init artifact.hpp:91-105 (bit-exact draws)
+  static std::unique_ptr<Agent> init(Context& ctx, std::size_t S, std::size_t A, std::uint64_t seed, double lr,
+                                     std::vector<std::size_t> hidden = {64, 64}) {
+    auto a = std::make_unique<Agent>(ctx, S, A, hidden);
+    std::size_t n = 0;
+    check(prb_artifact_init(S, A, seed, hidden.data(), (int)hidden.size(), nullptr, &n));
+    std::vector<double> flat(n);
+    check(prb_artifact_init(S, A, seed, hidden.data(), (int)hidden.size(), flat.data(), nullptr));
+    a->set(flat, nullptr, nullptr, 0, lr);
+    return a;
+  }
+  std::unique_ptr<Agent> clone() const {
+    auto b = std::make_unique<Agent>(*ctx_, S_, A_, hidden_);
+    check(prb_agent_copy(b->h_, h_));
+    return b;
+  }
+  std::size_t param_count() const { return prb_agent_param_count(h_); }
+  void set(const std::vector<double>& flat, const std::vector<double>* m, const std::vector<double>* v, std::int64_t t,
+           double lr) {
+    if (flat.size() != param_count())  // unflatten_params artifact.hpp:53-58
+      throw DimensionError("unflatten_params: " + std::to_string(flat.size()) + " values vs " +
+                           std::to_string(param_count()) + " params");
+    check(prb_agent_set_host(h_, flat.data(), m ? m->data() : nullptr, v ? v->data() : nullptr, t, lr));
+  }
+  std::vector<double> flatten_params() const {
+    std::vector<double> f(param_count());
+    check(prb_agent_get_host(h_, f.data(), nullptr, nullptr, nullptr));
+    return f;
+  }
+  std::int64_t optimizer_t() const {
+    std::int64_t t = 0;
+    check(prb_agent_get_host(h_, nullptr, nullptr, nullptr, &t));
+    return t;
+  }
+  void adam_step(const std::vector<double>& grads) {  // nn.hpp:164-182
+    if (grads.size() != param_count())
+      throw DimensionError("adam_step: params " + std::to_string(param_count()) + ", grads " +
+                           std::to_string(grads.size()));
+    check(prb_adam_step_host(h_, grads.data()));
+  }
+  prb_agent get() const { return h_; }
+  Context& context() const { return *ctx_; }
+  std::size_t state_dim() const { return S_; }
+  std::size_t action_dim() const { return A_; }
+  const std::vector<std::size_t>& hidden() const { return hidden_; }
+
+ private:
+  Context* ctx_;
+  std::size_t S_, A_;
+  std::vector<std::size_t> hidden_;
+  prb_agent h_ = nullptr;
+};
+
+namespace detail {
+struct DeviceBuffer {
+  prb_ctx ctx;
+  void* p = nullptr;
+  DeviceBuffer(prb_ctx c, std::size_t bytes) : ctx(c) { check(prb_device_alloc(c, bytes, &p)); }
+  ~DeviceBuffer() { prb_device_free(ctx, p); }
+};
+inline std::vector<float> to_f32(const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); }
+}  // namespace detail
+
+// policy_sample nn.hpp:250-265 (noise: Philox stream keyed by seed/counter)
+inline PolicySample policy_sample(const Agent& a, const Tensor2& states, std::uint64_t seed, std::uint64_t counter = 0) {
+  if (states.cols != a.state_dim())
+    throw DimensionError("mlp_forward: input " + states.shape_str() + " vs weights [" + std::to_string(a.state_dim()) +
+                         "x..]");
+  prb_ctx c = a.context().get();
+  const std::size_t n = states.rows, A = a.action_dim();
+  detail::DeviceBuffer ds(c, n * states.cols * 4 + 4), da(c, n * A * 4 + 4), dl(c, n * 4 + 4);
+  const std::vector<float> s32 = detail::to_f32(states.data);
+  check(prb_memcpy_h2d(c, ds.p, s32.data(), s32.size() * 4));
+  check(prb_policy_sample(a.get(), static_cast<const float*>(ds.p), n, seed, counter, static_cast<float*>(da.p),
+                          static_cast<float*>(dl.p), nullptr, nullptr));
+  std::vector<float> act(n * A), lp(n);
+  check(prb_memcpy_d2h(c, act.data(), da.p, act.size() * 4));
+  check(prb_memcpy_d2h(c, lp.data(), dl.p, lp.size() * 4));
+  PolicySample out;
+  out.actions = Tensor2(n, A);
+  out.actions.data.assign(act.begin(), act.end());
+  out.log_probs.assign(lp.begin(), lp.end());
+  return out;
+}
+
+// Device TransitionBuffer sized for one VecEnv x horizon (buffer.hpp:39-48).
+class TransitionBuffer {
+ public:
+  TransitionBuffer(const VectorizedEnvironment& env, std::size_t horizon) {
+    check(prb_rollout_create(env.get(), horizon, &h_));
+    N_ = env.num_envs();
+    H_ = horizon;
+  }
+  ~TransitionBuffer() { prb_rollout_destroy(h_); }
+  TransitionBuffer(const TransitionBuffer&) = delete;
+  TransitionBuffer& operator=(const TransitionBuffer&) = delete;
+  std::size_t capacity() const { return N_ * H_; }
+  prb_rollout get() const { return h_; }
+  // rewards in the reference index space (env e, step t at e*H + t, pod.hpp:89-94)
+  std::vector<double> rewards() const {
+    std::vector<double> r(capacity());
+    check(prb_rollout_download(h_, nullptr, nullptr, nullptr, r.data(), nullptr, nullptr, nullptr));
+    return r;
+  }
+
+ private:
+  prb_rollout h_ = nullptr;
+  std::size_t N_ = 0, H_ = 0;
+};
+
+// worker_collect pod.hpp:95-132
+inline void worker_collect(const Agent& a, VectorizedEnvironment& env, TransitionBuffer& buf, std::uint64_t seed) {
+  check(prb_rollout_collect(buf.get(), a.get(), env.get(), seed));
+}
+
+// buffer_advantages ppo.hpp:212-244 -> (advantages, returns), reference index space
+inline std::pair<std::vector<double>, std::vector<double>> buffer_advantages(TransitionBuffer& buf,
+                                                                             const PpoConfig& cfg,
+                                                                             bool normalize = true) {
+  check(prb_gae(buf.get(), cfg.gamma, cfg.gae_lambda, normalize ? 1 : 0));
+  std::vector<double> adv(buf.capacity()), ret(buf.capacity());
+  check(prb_gae_download(buf.get(), adv.data(), ret.data()));
+  return {std::move(adv), std::move(ret)};
+}
+
+// ppo_update ppo.hpp:249-296: returns a trained copy; the input is untouched.
+inline std::pair<std::unique_ptr<Agent>, PpoUpdateStats> ppo_update(const Agent& a, TransitionBuffer& buf,
+                                                                    const PpoConfig& cfg, std::uint64_t seed,
+                                                                    const std::vector<std::uint64_t>* perm = nullptr) {
+  auto out = std::make_unique<Agent>(a.context(), a.state_dim(), a.action_dim(), a.hidden());
+  const prb_ppo_config c = cfg.c();
+  prb_ppo_stats st{};
+  check(prb_ppo_update(a.get(), buf.get(), &c, seed, perm ? perm->data() : nullptr, out->get(), &st));
+  return {std::move(out), PpoUpdateStats{st.mean_policy_loss, st.mean_value_loss, st.mean_entropy, st.minibatches}};
+}
+
+// fuse_parameters pod.hpp:141-172
+inline std::unique_ptr<Agent> fuse_parameters(const std::vector<const Agent*>& agents) {
+  if (agents.empty()) throw UsageError("fuse_parameters: empty artifact list");
+  const Agent& a0 = *agents.front();
+  auto out = std::make_unique<Agent>(a0.context(), a0.state_dim(), a0.action_dim(), a0.hidden());
+  std::vector<prb_agent> hs;
+  for (const Agent* a : agents) hs.push_back(a->get());
+  check(prb_fuse_parameters(hs.data(), hs.size(), out->get()));
+  return out;
+}
+
+// Leaderboard order after inserting candidates in seq order (tournament.hpp:104-119)
+inline std::vector<int> leaderboard_rank(Context& ctx, const std::vector<double>& scores,
+                                         const std::vector<std::uint64_t>& seqs, std::size_t capacity) {
+  std::vector<std::int32_t> order(capacity);
+  std::int32_t n = 0;
+  check(prb_leaderboard_rank_host(ctx.get(), scores.data(), seqs.data(), scores.size(), capacity, order.data(), &n));
+  return std::vector<int>(order.begin(), order.begin() + n);
+}
+
+}  // namespace podracer_b200

@@ -1,0 +1,149 @@
+// test_dropin.cpp -- the C++ drop-in API (include/podracer_b200/podracer_b200.hpp)
+// driven the way the reference's pod_train drives its own API (pod.hpp:353-485),
+// checked against the C oracle (oracle/podracer_oracle.c, linked as test code).
+// Run on a GPU box by tests/test_gpu_cpp.py; prints "DROPIN OK" on success.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "podracer_b200/podracer_b200.hpp"
+
+extern "C" {
+typedef struct {
+  double initial_capital, max_trade_shares, cost_rate;
+} orc_stock_cfg;
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} orc_mt64;
+void orc_stock_vec_reset(size_t, int, const orc_stock_cfg*, size_t, double*, double*, size_t*, size_t*, double*);
+int orc_stock_vec_step(size_t, int, const orc_stock_cfg*, size_t, size_t, const double*, const double*, size_t,
+                       double*, double*, size_t*, size_t*, double*, const double*, double*, double*, uint8_t*, double*,
+                       double*, uint64_t*);
+void orc_pm_vec_reset(size_t, uint64_t, orc_mt64*, double*, uint64_t*, double*);
+}
+
+namespace pb = podracer_b200;
+
+static int failures = 0;
+#define EXPECT(cond)                                                   \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                      \
+    }                                                                  \
+  } while (0)
+
+int main() {
+  pb::Context ctx(0);
+  const int K = 30;
+  const size_t T = 160, N = 37, S = 1 + 6 * K;
+  std::vector<double> open(K * T), high(K * T), low(K * T), close(K * T), vol(K * T), ind(4 * K * T);
+  pb::check(prb_market_synthetic(2112, K, T, open.data(), high.data(), low.data(), close.data(), vol.data()));
+  pb::check(prb_compute_indicators(high.data(), low.data(), close.data(), T, K, ind.data()));
+  pb::MarketData market(ctx, close, &ind, T, K);
+  pb::StockConfig cfg;
+  cfg.initial_capital = 1e5;
+  const size_t start = 10, end = 70;
+  auto env = pb::VectorizedEnvironment::stock(market, cfg, start, end, N);
+  EXPECT(env->spec().state_dim == S && env->spec().action_dim == (size_t)K);
+
+  // ---- VecEnv parity against the oracle over two auto-resets ----
+  orc_stock_cfg oc{cfg.initial_capital, cfg.max_trade_shares, cfg.cost_rate};
+  std::vector<double> bal(N), sh(N * K), ret(N);
+  std::vector<size_t> t(N), sc(N);
+  orc_stock_vec_reset(N, K, &oc, start, bal.data(), sh.data(), t.data(), sc.data(), ret.data());
+  pb::Tensor2 s0 = env->reset(3);
+  EXPECT(s0.rows == N && s0.cols == S);
+  std::mt19937_64 rng(9);
+  std::uniform_real_distribution<double> u(-1.2, 1.2);
+  size_t dones = 0;
+  for (int step = 0; step < 130; ++step) {
+    pb::Tensor2 a(N, K);
+    for (auto& x : a.data) x = (double)(float)u(rng);  // the device consumes fp32 actions
+    pb::VecStepResult r = env->step(a);
+    std::vector<double> nx(N * S), rw(N), term(N * S), tr(N);
+    std::vector<uint8_t> d(N);
+    std::vector<uint64_t> tl(N);
+    EXPECT(orc_stock_vec_step(N, K, &oc, start, end, close.data(), ind.data(), T, bal.data(), sh.data(), t.data(),
+                              sc.data(), ret.data(), a.data.data(), nx.data(), rw.data(), d.data(), term.data(),
+                              tr.data(), tl.data()) == 0);
+    for (size_t i = 0; i < N; ++i) {
+      EXPECT(r.dones[i] == d[i]);
+      EXPECT((float)r.rewards[i] == (float)rw[i]);
+      for (size_t j = 0; j < S; ++j) EXPECT((float)r.next_states.at(i, j) == (float)nx[i * S + j]);
+      if (d[i]) {
+        ++dones;
+        EXPECT(r.infos[i].episode_end && r.infos[i].episode_length == tl[i] && r.infos[i].episode_return == tr[i]);
+      }
+    }
+  }
+  EXPECT(dones == 2 * N);
+  bool threw = false;
+  try {
+    env->step(pb::Tensor2(N - 1, K));
+  } catch (const pb::DimensionError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+
+  // ---- PointMass resets are the reference's own per-env streams ----
+  auto pm = pb::VectorizedEnvironment::pointmass(ctx, 16);
+  pb::Tensor2 p0 = pm->reset(77);
+  std::vector<orc_mt64> gens(16);
+  std::vector<double> st(16 * 6), er(16);
+  std::vector<uint64_t> psc(16);
+  orc_pm_vec_reset(16, 77, gens.data(), st.data(), psc.data(), er.data());
+  for (size_t i = 0; i < st.size(); ++i) EXPECT((float)p0.data[i] == (float)st[i]);
+
+  // ---- one pod iteration: collect, GAE, PPO update, fusion of two learners ----
+  auto actor = pb::Agent::init(ctx, S, K, 7, 1e-3);
+  EXPECT(actor->param_count() == 33661);
+  pb::PolicySample ps = pb::policy_sample(*actor, s0, 5);
+  EXPECT(ps.actions.rows == N && ps.log_probs.size() == N);
+  env->reset(4);
+  const size_t H = 32;
+  pb::TransitionBuffer buf(*env, H);
+  pb::worker_collect(*actor, *env, buf, 11);
+  auto [adv, ret2] = pb::buffer_advantages(buf, pb::PpoConfig{});
+  double m = 0, v = 0;
+  for (double x : adv) m += x;
+  m /= adv.size();
+  for (double x : adv) v += (x - m) * (x - m);
+  v /= adv.size();
+  EXPECT(std::fabs(m) < 1e-5 && std::fabs(v - 1.0) < 1e-3);
+  pb::PpoConfig pc;
+  pc.buffer_size = N * H;
+  pc.minibatch_size = 128;
+  pc.epochs_per_update = 2;
+  auto l0 = pb::ppo_update(*actor, buf, pc, 1);
+  auto l1 = pb::ppo_update(*actor, buf, pc, 2);
+  EXPECT(l0.second.minibatches == 2 * (N * H / 128));
+  EXPECT(l0.first->optimizer_t() == (int64_t)l0.second.minibatches);
+  auto fused = pb::fuse_parameters({l0.first.get(), l1.first.get()});
+  const auto f0 = l0.first->flatten_params(), f1 = l1.first->flatten_params(), ff = fused->flatten_params();
+  for (size_t i = 0; i < ff.size(); ++i) EXPECT(std::fabs(ff[i] - 0.5 * (f0[i] + f1[i])) <= 1e-6 * (1 + std::fabs(ff[i])));
+  const auto fa = actor->flatten_params();
+  bool changed = false;
+  for (size_t i = 0; i < fa.size(); ++i) changed |= fa[i] != f0[i];
+  EXPECT(changed);  // trained copy differs; the input artifact is untouched (checked in the Python suite)
+  threw = false;
+  try {
+    pb::PpoConfig bad = pc;
+    bad.minibatch_size = pc.buffer_size * 2;
+    pb::ppo_update(*actor, buf, bad, 1);
+  } catch (const pb::ConfigError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  const std::vector<int> order = pb::leaderboard_rank(ctx, {1.0, 3.0, 3.0, 2.0}, {0, 1, 2, 3}, 3);
+  EXPECT(order.size() == 3 && order[0] == 1 && order[1] == 2 && order[2] == 3);
+
+  if (failures) {
+    std::fprintf(stderr, "%d failures\n", failures);
+    return 1;
+  }
+  std::printf("DROPIN OK\n");
+  return 0;
+}
