@@ -7,8 +7,10 @@
 //   1. ppo_fwd_bwd: each CTA gathers R rows of the minibatch (permutation
 //      computed on the fly: a keyed Feistel bijection of the buffer, or the
 //      injected reference permutation), rebuilds the observation (compact stock
-//      rows + shared feature row), runs actor+critic forward with activations
-//      cached in shared memory, forms the clipped-surrogate / value / entropy
+//      rows + shared feature row), stages the whole actor+critic weight set in
+//      shared memory (row stride out+1: conflict-free for the forward's
+//      column walk and the backward's row walk), runs the forward with cached
+//      activations, forms the clipped-surrogate / value / entropy head
 //      gradients (subgradient ties as ppo.hpp:146), backpropagates, and writes
 //      its partial dW/db/dlog_std and loss sums to a [CTA][P] slab.
 //   2. ppo_reduce: deterministic fixed-order sum of the partials, entropy term,
@@ -32,6 +34,7 @@ namespace {
 
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
 constexpr int kPpoThreads = 256;
+constexpr size_t kSmemBudget = 220 * 1024;
 
 struct PpoArgs {
   const float* params;
@@ -56,6 +59,7 @@ struct PpoArgs {
   int bits;           // Feistel domain bits (even)
   int mb;             // minibatch rows
   int R;              // rows per CTA
+  int stage;          // 1: weights staged in shared memory (ld = out + 1)
   const int64_t* step;  // device minibatch counter (epoch = step / nmb)
   double clip, ent, vf;
   float* partial;  // [grid][Pext]
@@ -88,7 +92,16 @@ __device__ __forceinline__ uint32_t mb_row(const PpoArgs& a, int64_t step, uint3
   return feistel_perm(pos, a.n, a.bits, derive_seed2(a.seed, 0x50504fULL /*"PPO"*/, epoch));
 }
 
+// floats of the staged weight set: every layer of both nets at row stride out+1
+__host__ __device__ inline size_t staged_floats(const PpoArgs& a) {
+  size_t n = 0;
+  for (int l = 0; l < a.actor.nl; ++l) n += (size_t)a.actor.dims[l] * (a.actor.dims[l + 1] + 1);
+  for (int l = 0; l < a.critic.nl; ++l) n += (size_t)a.critic.dims[l] * (a.critic.dims[l + 1] + 1);
+  return (n + 3) & ~size_t(3);
+}
+
 struct Smem {
+  float* w;  // staged weights (nullptr when not staged)
   float* x;
   float* aa[kMaxLayers];
   int lda[kMaxLayers];
@@ -112,6 +125,8 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) 
     o += (n + 3) & ~size_t(3);
     return p;
   };
+  float* w = a.stage ? take(staged_floats(a)) : nullptr;
+  if (s) s->w = w;
   float* x = take((size_t)R8 * ldx);
   if (s) s->x = x;
   for (int l = 0; l < a.actor.nl; ++l) {
@@ -148,35 +163,76 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) 
   return o * sizeof(float);
 }
 
-// partial[gW] = sum_r in[r][k] * d[r][j], partial[gb] = sum_r d[r][j]
-__device__ __forceinline__ void grad_w_tile(const float* s_in, int ldi, int in, const float* s_d, int ldd, int out,
-                                            int nrows, float* __restrict__ gW) {
-  const int total = in * out;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int k = idx / out, j = idx - (idx / out) * out;
-    float acc = 0.0f;
-    for (int r = 0; r < nrows; ++r) acc = fmaf(s_in[r * ldi + k], s_d[r * ldd + j], acc);
-    gW[idx] = acc;
+// Weight locations for one net: staged copy (stride out+1) or the HBM blob (stride out).
+__device__ __forceinline__ LayerPtrs layer_ptrs(const PpoArgs& a, const MlpDesc& d, float* staged_base) {
+  LayerPtrs lp;
+  float* cur = staged_base;
+  for (int l = 0; l < d.nl; ++l) {
+    const float* Wg = a.params + d.off[l];
+    lp.B[l] = Wg + (size_t)d.dims[l] * d.dims[l + 1];
+    if (staged_base) {
+      lp.W[l] = cur;
+      lp.ldw[l] = d.dims[l + 1] + 1;
+      cur += (size_t)d.dims[l] * (d.dims[l + 1] + 1);
+    } else {
+      lp.W[l] = Wg;
+      lp.ldw[l] = d.dims[l + 1];
+    }
   }
-  for (int j = threadIdx.x; j < out; j += blockDim.x) {
-    float acc = 0.0f;
-    for (int r = 0; r < nrows; ++r) acc += s_d[r * ldd + j];
-    gW[total + j] = acc;
+  return lp;
+}
+
+__device__ __forceinline__ void stage_weights(const PpoArgs& a, const MlpDesc& d, float* dst) {
+  for (int l = 0; l < d.nl; ++l) {
+    const int in = d.dims[l], out = d.dims[l + 1], ld = out + 1;
+    const float* src = a.params + d.off[l];
+    // row k of W -> dst[k*ld ...]: lanes walk a row (coalesced reads, conflict-free writes)
+    const int OJ = out < 32 ? out : 32;
+    const int KT = kPpoThreads / 32;
+    const int lane = threadIdx.x & 31, kt = threadIdx.x >> 5;
+    if (lane < OJ)
+      for (int k = kt; k < in; k += KT)
+        for (int j = lane; j < out; j += OJ) dst[k * ld + j] = __ldg(src + (size_t)k * out + j);
+    dst += (size_t)in * ld;
   }
 }
 
-// d_prev[r][k] = (sum_j d[r][j] W[k][j]) * (1 - a[r][k]^2)
-__device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int out, const float* __restrict__ W,
-                                                int in, const float* s_a, int lda, float* s_dp, int ldp, int nrows) {
-  const int total = nrows * in;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx / in, k = idx - (idx / in) * in;
-    const float* wr = W + (size_t)k * out;
+// gW[k][j] = sum_r in[r][k] d[r][j]; gb[j] = sum_r d[r][j]   (matmul_tn + column_sums, tensor.hpp:85-183)
+__device__ __forceinline__ void grad_w_tile(const float* s_in, int ldi, int in, const float* s_d, int ldd, int out,
+                                            int nrows, float* __restrict__ gW) {
+  const int TJ = out > 32 ? 64 : 32;
+  const int KT = blockDim.x / TJ;
+  const int jt = threadIdx.x % TJ, kt = threadIdx.x / TJ;
+  for (int j = jt; j < out; j += TJ) {
+    for (int k = kt; k < in; k += KT) {
+      float acc = 0.0f;
+      for (int r = 0; r < nrows; ++r) acc = fmaf(s_in[r * ldi + k], s_d[r * ldd + j], acc);
+      gW[(size_t)k * out + j] = acc;
+    }
+    if (kt == 0) {
+      float acc = 0.0f;
+      for (int r = 0; r < nrows; ++r) acc += s_d[r * ldd + j];
+      gW[(size_t)in * out + j] = acc;
+    }
+  }
+}
+
+// d_prev[r][k] = (sum_j d[r][j] W[k][j]) * (1 - a[r][k]^2)   (matmul_nt, nn.hpp:125-130)
+__device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int out, const float* W, int ldw, int in,
+                                                const float* s_a, int lda, float* s_dp, int ldp, int nrows) {
+  int KT = 32;
+  while (KT < in && KT < (int)blockDim.x) KT <<= 1;
+  const int NRG = blockDim.x / KT;
+  const int kk = threadIdx.x % KT, rg = threadIdx.x / KT;
+  for (int r = rg; r < nrows; r += NRG) {
     const float* dr = s_d + r * ldd;
-    float acc = 0.0f;
-    for (int j = 0; j < out; ++j) acc = fmaf(dr[j], __ldg(wr + j), acc);
-    const float av = s_a[r * lda + k];
-    s_dp[r * ldp + k] = acc * (1.0f - av * av);
+    for (int k = kk; k < in; k += KT) {
+      const float* wr = W + (size_t)k * ldw;
+      float acc = 0.0f;
+      for (int j = 0; j < out; ++j) acc = fmaf(dr[j], wr[j], acc);
+      const float av = s_a[r * lda + k];
+      s_dp[r * ldp + k] = acc * (1.0f - av * av);
+    }
   }
 }
 
@@ -192,6 +248,17 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
   const int q0 = blockIdx.x * R;
   const int nrows = min(R, a.mb - q0);
   const double mean = a.advstat[0], denom = a.advstat[1];
+  float* wa = nullptr;
+  float* wc = nullptr;
+  if (a.stage) {
+    wa = s.w;
+    size_t na = 0;
+    for (int l = 0; l < a.actor.nl; ++l) na += (size_t)a.actor.dims[l] * (a.actor.dims[l + 1] + 1);
+    wc = s.w + na;
+    stage_weights(a, a.actor, wa);
+    stage_weights(a, a.critic, wc);
+  }
+  const LayerPtrs lpa = layer_ptrs(a, a.actor, wa), lpc = layer_ptrs(a, a.critic, wc);
   // ---- gather (gather_minibatch ppo.hpp:83-103) ----
   for (int r = threadIdx.x / 32; r < nrows; r += blockDim.x / 32) {
     const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
@@ -213,8 +280,8 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
   }
   __syncthreads();
   // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
-  mlp_forward_tile(a.params, a.actor, s.x, ldx, s.aa, s.lda, nrows);
-  mlp_forward_tile(a.params, a.critic, s.x, ldx, s.ca, s.ldc, nrows);
+  mlp_forward_tile_p(a.actor, lpa, s.x, ldx, s.aa, s.lda, nrows);
+  mlp_forward_tile_p(a.critic, lpc, s.x, ldx, s.ca, s.ldc, nrows);
   // ---- per-row losses and head gradients (ppo.hpp:128-167) ----
   const float inv_n = 1.0f / (float)a.mb;
   const float* log_std = a.params + a.log_std_off;
@@ -262,9 +329,11 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
   }
   __syncthreads();
   float* part = a.partial + (size_t)blockIdx.x * a.Pext;
+  const int ldp = a.ldw > ldA ? a.ldw : ldA;
   // ---- backward (mlp_backward_accumulate nn.hpp:105-132) ----
   for (int net = 0; net < 2; ++net) {
     const MlpDesc& d = net ? a.critic : a.actor;
+    const LayerPtrs& lp = net ? lpc : lpa;
     float* const* acts = net ? s.ca : s.aa;
     const int* lds = net ? s.ldc : s.lda;
     const float* delta = acts[d.nl - 1];
@@ -276,8 +345,7 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
       grad_w_tile(lin, ldi, in, delta, ldd, out, nrows, part + d.off[l]);
       if (l > 0) {
         float* dp = (delta == s.d0) ? s.d1 : s.d0;
-        const int ldp = a.ldw > ldA ? a.ldw : ldA;
-        delta_prev_tile(delta, ldd, out, a.params + d.off[l], in, lin, ldi, dp, ldp, nrows);
+        delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, lin, ldi, dp, ldp, nrows);
         __syncthreads();
         delta = dp;
         ldd = ldp;
@@ -316,8 +384,17 @@ __global__ void __launch_bounds__(256) ppo_reduce_kernel(ReduceArgs r) {
   if (r.status[0] != 0) return;
   int bad = 0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < r.P; p += gridDim.x * blockDim.x) {
-    float acc = 0.0f;
-    for (int b = 0; b < r.nparts; ++b) acc += r.partial[(size_t)b * r.Pext + p];
+    // fixed-order sum in 4 interleaved lanes (loads in flight together), then combined
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int b = 0;
+    for (; b + 4 <= r.nparts; b += 4) {
+      s0 += r.partial[(size_t)(b + 0) * r.Pext + p];
+      s1 += r.partial[(size_t)(b + 1) * r.Pext + p];
+      s2 += r.partial[(size_t)(b + 2) * r.Pext + p];
+      s3 += r.partial[(size_t)(b + 3) * r.Pext + p];
+    }
+    for (; b < r.nparts; ++b) s0 += r.partial[(size_t)b * r.Pext + p];
+    float acc = (s0 + s1) + (s2 + s3);
     if (p >= r.log_std_off && p < r.log_std_off + r.A) acc -= (float)r.ent;  // ppo.hpp:157
     r.grads[p] = acc;
     bad |= !isfinite(acc);
@@ -413,8 +490,10 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   // rows per CTA: as many CTAs as possible while every CTA keeps >= 8 rows
   p.R = 8;
   while (p.R < 64 && (size_t)(mb / (p.R * 2)) >= (size_t)a->ctx->num_sms) p.R *= 2;
-  while (p.R > 8 && carve(p, nullptr, nullptr) > 200 * 1024) p.R /= 2;
-  PRB_REQUIRE(carve(p, nullptr, nullptr) <= 220 * 1024, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
+  p.stage = 1;
+  if (carve(p, nullptr, nullptr) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
+  while (p.R > 8 && carve(p, nullptr, nullptr) > kSmemBudget) p.R /= 2;
+  PRB_REQUIRE(carve(p, nullptr, nullptr) <= kSmemBudget, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
   const int grid = (mb + p.R - 1) / p.R;
   if (ws.partial.n < (size_t)grid * p.Pext) ws.partial.alloc((size_t)grid * p.Pext);
   if (!ws.scratch.p) ws.scratch.alloc(4);
@@ -445,7 +524,7 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   r.step = ws.step.p;
   r.stats = ws.stats.p;
   r.apply = apply;
-  const int rgrid = (int)std::min<size_t>((p.P + 255) / 256, 592);
+  const int rgrid = (int)std::min<size_t>((p.P + 255) / 256, 1184);
   ppo_reduce_kernel<<<rgrid, 256, 0, s>>>(r);
   if (apply) prb_adam_launch(a, a->d_grads.p, a->d_status.p, s);
 }
@@ -473,7 +552,7 @@ void check_status(prb_agent a) {
 void set_smem_attr() {
   static bool done = false;
   if (!done) {
-    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     done = true;
   }
 }
