@@ -190,11 +190,20 @@ __device__ __forceinline__ void stage_weights(const PpoArgs& a, const MlpDesc& d
     const int OJ = out < 32 ? out : 32;
     const int KT = kPpoThreads / 32;
     const int lane = threadIdx.x & 31, kt = threadIdx.x >> 5;
+    // LDGSTS: every element in flight at once, no register round trip (waited in stage_wait())
     if (lane < OJ)
       for (int k = kt; k < in; k += KT)
-        for (int j = lane; j < out; j += OJ) dst[k * ld + j] = __ldg(src + (size_t)k * out + j);
+        for (int j = lane; j < out; j += OJ)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(dst + k * ld + j)),
+                       "l"(src + (size_t)k * out + j)
+                       : "memory");
     dst += (size_t)in * ld;
   }
+}
+
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
 // gW[k][j] = sum_r in[r][k] d[r][j]; gb[j] = sum_r d[r][j]   (matmul_tn + column_sums, tensor.hpp:85-183)
@@ -258,6 +267,7 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
     stage_weights(a, a.actor, wa);
     stage_weights(a, a.critic, wc);
   }
+  // the gather below overlaps with the weight copies in flight; waited before the forward
   const LayerPtrs lpa = layer_ptrs(a, a.actor, wa), lpc = layer_ptrs(a, a.critic, wc);
   // ---- gather (gather_minibatch ppo.hpp:83-103) ----
   for (int r = threadIdx.x / 32; r < nrows; r += blockDim.x / 32) {
@@ -278,6 +288,7 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
       s.misc[r * 4 + 2] = a.ret[i];
     }
   }
+  if (a.stage) stage_wait();
   __syncthreads();
   // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
   mlp_forward_tile_p(a.actor, lpa, s.x, ldx, s.aa, s.lda, nrows);
@@ -380,24 +391,38 @@ struct ReduceArgs {
   int apply;          // 0 = grads only (prb_ppo_loss_grads)
 };
 
-__global__ void __launch_bounds__(256) ppo_reduce_kernel(ReduceArgs r) {
+// Block = 32 parameters x 8 slices of the CTA partials; slice s sums partials
+// s, s+8, ... with 4 independent accumulators, then the 8 slices are combined
+// in a fixed order through shared memory: deterministic, and ~1,000 blocks of
+// independent loads instead of one 128-long dependent chain per parameter.
+constexpr int kRedCols = 32, kRedSlices = 8;
+
+__global__ void __launch_bounds__(kRedCols * kRedSlices) ppo_reduce_kernel(ReduceArgs r) {
   if (r.status[0] != 0) return;
-  int bad = 0;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < r.P; p += gridDim.x * blockDim.x) {
-    // fixed-order sum in 4 interleaved lanes (loads in flight together), then combined
+  __shared__ float part_sum[kRedSlices][kRedCols];
+  const int col = threadIdx.x % kRedCols, slice = threadIdx.x / kRedCols;
+  const int p = blockIdx.x * kRedCols + col;
+  if (p < r.P) {
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int b = 0;
-    for (; b + 4 <= r.nparts; b += 4) {
-      s0 += r.partial[(size_t)(b + 0) * r.Pext + p];
-      s1 += r.partial[(size_t)(b + 1) * r.Pext + p];
-      s2 += r.partial[(size_t)(b + 2) * r.Pext + p];
-      s3 += r.partial[(size_t)(b + 3) * r.Pext + p];
+    int b = slice;
+    for (; b + 3 * kRedSlices < r.nparts; b += 4 * kRedSlices) {
+      s0 += r.partial[(size_t)(b + 0 * kRedSlices) * r.Pext + p];
+      s1 += r.partial[(size_t)(b + 1 * kRedSlices) * r.Pext + p];
+      s2 += r.partial[(size_t)(b + 2 * kRedSlices) * r.Pext + p];
+      s3 += r.partial[(size_t)(b + 3 * kRedSlices) * r.Pext + p];
     }
-    for (; b < r.nparts; ++b) s0 += r.partial[(size_t)b * r.Pext + p];
-    float acc = (s0 + s1) + (s2 + s3);
+    for (; b < r.nparts; b += kRedSlices) s0 += r.partial[(size_t)b * r.Pext + p];
+    part_sum[slice][col] = (s0 + s1) + (s2 + s3);
+  }
+  __syncthreads();
+  int bad = 0;
+  if (slice == 0 && p < r.P) {
+    float acc = part_sum[0][col];
+#pragma unroll
+    for (int sl = 1; sl < kRedSlices; ++sl) acc += part_sum[sl][col];
     if (p >= r.log_std_off && p < r.log_std_off + r.A) acc -= (float)r.ent;  // ppo.hpp:157
     r.grads[p] = acc;
-    bad |= !isfinite(acc);
+    bad = !isfinite(acc);
   }
   if (bad) atomicOr(&r.scratch[1], 1);
   __threadfence();
@@ -524,8 +549,8 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   r.step = ws.step.p;
   r.stats = ws.stats.p;
   r.apply = apply;
-  const int rgrid = (int)std::min<size_t>((p.P + 255) / 256, 1184);
-  ppo_reduce_kernel<<<rgrid, 256, 0, s>>>(r);
+  const int rgrid = (p.P + kRedCols - 1) / kRedCols;
+  ppo_reduce_kernel<<<rgrid, kRedCols * kRedSlices, 0, s>>>(r);
   if (apply) prb_adam_launch(a, a->d_grads.p, a->d_status.p, s);
 }
 
