@@ -30,6 +30,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 METRIC = "env transitions/sec (1/2/4/8 B200, device-timed) vs host-CPU ref; % HBM roofline"
 UNIT = "transitions/s"
