@@ -278,6 +278,13 @@ def run_ours(args, d: Dist):
                "iteration_transitions_per_s": N * H / ((coll_ms + ppo_ms) / 1e3),
                "mean_policy_loss": st.mean_policy_loss, "mean_value_loss": st.mean_value_loss}
 
+    # ---- the other BASELINE configs, measured in the same run (not the headline) ----
+    other = {}
+    if not args.skip_configs:
+        other["configs[2]_pointmass"] = leg_pointmass(pr, lib, ctx, args.pm_envs, args.pm_horizon, d)
+        other["configs[4]_stock_1M"] = leg_stock_large(pr, lib, ctx, market, cfg, args.c5_envs, H, d)
+    other["configs[3]_tournament"] = leg_tournament(pr, ctx, d, args.pods_per_gpu)
+
     # ---- end to end through the public API with host buffers ----
     P = agent.param_count
     host_params = np.ascontiguousarray(agent.flatten_params().astype(np.float32))
@@ -316,9 +323,73 @@ def run_ours(args, d: Dist):
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (MLP, obs) + f64 (portfolio accounting)",
                "data": "synthetic (BASELINE.md §3 market, random-init artifact_init weights)",
                "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
-               "ppo_update": ppo, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk}
+               "ppo_update": ppo, "other_configs": other, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+               "clocks": clk}
         print(json.dumps(out))
     d.close()
+
+
+def leg_pointmass(pr, lib, ctx, n_envs, horizon, d):
+    """configs[2]: PointMass2D (SPEC.md analytic control env) x 262,144 envs, actor/critic 3x256."""
+    env = pr.VectorizedEnvironment.pointmass(ctx, n_envs)
+    env.reset(7)
+    agent = pr.Agent.init(ctx, 6, 2, seed=7, hidden=(256, 256, 256))
+    ro = pr.Rollout.for_env(env, horizon)
+    ro.collect(agent, env, seed=1)
+    ms = d.max(time_region(lib, ctx, lambda: ro.collect(agent, env, seed=2)))
+    flops = 2 * (6 * 256 + 256 * 256 * 2 + 256 * 2) + 2 * (6 * 256 + 256 * 256 * 2 + 256)
+    rate = n_envs * horizon / (ms / 1e3)
+    return {"value": d.world * rate, "unit": UNIT, "envs_per_gpu": n_envs, "horizon": horizon, "ms_per_collect": ms,
+            "mlp_tflops": rate * flops / 1e12, "path": "per-step policy (fp32 SIMT) + pointmass step kernels",
+            "note": "3x256 tcgen05 path not built yet (weights exceed one SM's smem; DESIGN.md §10)"}
+
+
+def leg_stock_large(pr, lib, ctx, market, cfg, n_envs, horizon, d):
+    """configs[4] per-GPU scale: 1,048,576 stock envs x 256 steps (compact rollout rows, 69 GB)."""
+    env = pr.VectorizedEnvironment.stock(ctx, market, cfg, 0, T_ROWS - 1, n_envs)
+    env.reset(11)
+    agent = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=7)
+    ro = pr.Rollout.for_env(env, horizon)
+    ro.collect(agent, env, seed=1)
+    ms = d.max(time_region(lib, ctx, lambda: ro.collect(agent, env, seed=2)))
+    rate = n_envs * horizon / (ms / 1e3)
+    del ro
+    return {"value": d.world * rate, "unit": UNIT, "envs_per_gpu": n_envs, "horizon": horizon, "ms_per_collect": ms,
+            "rollout_gb_per_gpu": n_envs * horizon * BUF_BYTES / 1e9}
+
+
+def leg_tournament(pr, ctx, d, pods):
+    """configs[3]: per generation, NCCL all-gather of every rank's pods' (score, seq, id), identical
+    ranking on every rank, and top-3 elite weight broadcasts from their owner ranks."""
+    from paper_2112_05923_b200 import tournament as tn
+    if d.world > 1:
+        def share(b):
+            obj = [b]
+            d.dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+    else:
+        def share(b):
+            return b
+    comm = tn.Communicator(ctx, d.rank, d.world, share)
+    elite = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=5)
+    gens, times = 5, []
+    for g in range(gens + 2):
+        rng = np.random.default_rng(g * 131 + d.rank)
+        scores = rng.normal(size=pods)
+        ids = [tn.global_pod_id(d.rank, i, pods) for i in range(pods)]
+        seqs = [tn.arrival_seq(g, p, d.world * pods) for p in ids]
+        d.barrier()
+        t0 = time.perf_counter()
+        board, _ = tn.allgather_rank(comm, scores, seqs, ids, 10)
+        for b in board[:3]:
+            tn.broadcast_agent(comm, elite, tn.owner_rank(b.pod_id, pods))
+        ctx.synchronize()
+        if g >= 2:
+            times.append(d.max(time.perf_counter() - t0))
+    comm.close()
+    return {"pods_per_gpu": pods, "pods_total": pods * d.world, "ms_per_generation": 1e3 * float(np.median(times)),
+            "elite_bytes": 3 * 3 * elite.param_count * 4,
+            "what": "all-gather (score,seq,pod_id) + device ranking + 3 elite broadcasts (params,m,v,t); host-timed"}
 
 
 def env_leg(pr, lib, ctx, market, cfg, n_envs, hbm, d, steps=50):
@@ -406,6 +477,11 @@ def main():
     ap.add_argument("--horizon", type=int, default=256)
     ap.add_argument("--ppo-epochs", type=int, default=4)
     ap.add_argument("--env-envs", type=int, default=1 << 20)
+    ap.add_argument("--skip-configs", action="store_true")
+    ap.add_argument("--pm-envs", type=int, default=262144)
+    ap.add_argument("--pm-horizon", type=int, default=16)
+    ap.add_argument("--c5-envs", type=int, default=1 << 20)
+    ap.add_argument("--pods-per-gpu", type=int, default=8)
     ap.add_argument("--skip-ppo", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
