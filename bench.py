@@ -30,7 +30,16 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+os.environ["NCCL_DEBUG"] = "WARN"
+# Exactly one line on stdout: native libraries (NCCL banners, ...) write to fd 1,
+# so fd 1 is pointed at stderr and the JSON line goes to a saved copy of it.
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    _JSON_OUT.write(json.dumps(obj) + "\n")
+    _JSON_OUT.flush()
 
 METRIC = "env transitions/sec (1/2/4/8 B200, device-timed) vs host-CPU ref; % HBM roofline"
 UNIT = "transitions/s"
@@ -169,7 +178,7 @@ def run_reference(args, d: Dist):
     for i in range(args.warmup + args.steps):
         r = cpu_reference_rate(m, ind, seconds=0.0)
         if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"}))
+            emit(({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"}))
             return
         if i >= args.warmup:
             rates.append(r)
@@ -181,7 +190,7 @@ def run_reference(args, d: Dist):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_dict(args), "cpu_baseline": cb,
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    emit((out))
 
 
 def config_dict(args):
@@ -325,7 +334,7 @@ def run_ours(args, d: Dist):
                "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
                "ppo_update": ppo, "other_configs": other, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
                "clocks": clk}
-        print(json.dumps(out))
+        emit((out))
     d.close()
 
 
