@@ -348,9 +348,12 @@ def leg_pointmass(pr, lib, ctx, n_envs, horizon, d):
     ms = d.max(time_region(lib, ctx, lambda: ro.collect(agent, env, seed=2)))
     flops = 2 * (6 * 256 + 256 * 256 * 2 + 256 * 2) + 2 * (6 * 256 + 256 * 256 * 2 + 256)
     rate = n_envs * horizon / (ms / 1e3)
+    tflops = rate * flops / 1e12
     return {"value": d.world * rate, "unit": UNIT, "envs_per_gpu": n_envs, "horizon": horizon, "ms_per_collect": ms,
-            "mlp_tflops": rate * flops / 1e12, "path": "per-step policy (fp32 SIMT) + pointmass step kernels",
-            "note": "3x256 tcgen05 path not built yet (weights exceed one SM's smem; DESIGN.md §10)"}
+            "mlp_tflops": tflops, "tensor_frac": tflops / load_peaks()[2],
+            "flop_per_transition": flops,
+            "path": "rollout_pm_tc.cu: persistent tcgen05 3x256 actor/critic, bf16 weights streamed from L2 "
+                    "through a 5-slot bulk-copy ring, fp64 PointMass step + mt19937_64 resets in the same kernel"}
 
 
 def leg_stock_large(pr, lib, ctx, market, cfg, n_envs, horizon, d):
@@ -488,7 +491,7 @@ def main():
     ap.add_argument("--env-envs", type=int, default=1 << 20)
     ap.add_argument("--skip-configs", action="store_true")
     ap.add_argument("--pm-envs", type=int, default=262144)
-    ap.add_argument("--pm-horizon", type=int, default=16)
+    ap.add_argument("--pm-horizon", type=int, default=256)
     ap.add_argument("--c5-envs", type=int, default=1 << 20)
     ap.add_argument("--pods-per-gpu", type=int, default=8)
     ap.add_argument("--skip-ppo", action="store_true")

@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "prb_internal.h"
+#include "pm_env.cuh"
 #include "rng.cuh"
 
 using namespace prb;
@@ -574,16 +575,6 @@ struct PmStepArgs {
   int32_t* __restrict__ term_len;
 };
 
-__device__ __forceinline__ void pm_reset_draws(uint64_t* mt, size_t N, int32_t& idx, double* s) {
-  // PointMass2D::reset env.hpp:124-133: pos_x, pos_y, goal_x, goal_y ~ U(-0.4, 0.4), vel = 0
-  s[0] = mt64_uniform(mt, N, idx, -0.4, 0.4);
-  s[1] = mt64_uniform(mt, N, idx, -0.4, 0.4);
-  s[2] = 0.0;
-  s[3] = 0.0;
-  s[4] = mt64_uniform(mt, N, idx, -0.4, 0.4);
-  s[5] = mt64_uniform(mt, N, idx, -0.4, 0.4);
-}
-
 __global__ void __launch_bounds__(256) pm_step_kernel(PmStepArgs a) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (size_t)a.N) return;
@@ -594,24 +585,10 @@ __global__ void __launch_bounds__(256) pm_step_kernel(PmStepArgs a) {
   const float2 af = reinterpret_cast<const float2*>(a.actions)[e];
   const double a0 = clamp_ref((double)af.x, -1.0, 1.0), a1 = clamp_ref((double)af.y, -1.0, 1.0);
   const int32_t steps = a.steps[e];
-  // pointmass_step env.hpp:84-109
-  double n[6];
-  const double v0 = __dadd_rn(__dmul_rn(0.9, s[2]), __dmul_rn(0.1, a0));
-  const double v1 = __dadd_rn(__dmul_rn(0.9, s[3]), __dmul_rn(0.1, a1));
-  n[2] = v0;
-  n[3] = v1;
-  n[0] = __dadd_rn(s[0], __dmul_rn(0.1, v0));
-  n[1] = __dadd_rn(s[1], __dmul_rn(0.1, v1));
-  n[4] = s[4];
-  n[5] = s[5];
-  const double action_sq = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
-  const double dx = __dsub_rn(n[0], n[4]);
-  const double dy = __dsub_rn(n[1], n[5]);
-  const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-  double r = __dsub_rn(-dist, __dmul_rn(0.01, action_sq));
-  const bool reached = dist < 0.05;
-  if (reached) r = __dadd_rn(r, 10.0);
-  const bool done = reached || (steps + 1 >= 200);
+  // pointmass_step env.hpp:84-109 (pm_env.cuh)
+  double n[6], r;
+  bool done;
+  pm::step(s, a0, a1, steps, n, r, done);
   const double ret = __dadd_rn(a.ep_return[e], r);
   if (a.reward) a.reward[e] = (float)r;
   if (a.done_out) a.done_out[e] = done ? 1 : 0;
@@ -621,7 +598,7 @@ __global__ void __launch_bounds__(256) pm_step_kernel(PmStepArgs a) {
     if (a.term_ret) a.term_ret[e] = ret;
     if (a.term_len) a.term_len[e] = steps + 1;
     int32_t idx = a.mt_idx[e];
-    pm_reset_draws(a.mt + e, N, idx, n);
+    pm::reset_draws(a.mt + e, N, idx, n);
     a.mt_idx[e] = idx;
     a.steps[e] = 0;
     a.ep_return[e] = 0.0;
@@ -644,7 +621,7 @@ __global__ void pm_reset_kernel(int N, uint64_t seed, double* st, int32_t* steps
   mt64_seed(mt + e, N, derive_seed2(seed, 1, e));
   int32_t idx = kMtN;
   double s[6];
-  pm_reset_draws(mt + e, N, idx, s);
+  pm::reset_draws(mt + e, N, idx, s);
   mt_idx[e] = idx;
   steps[e] = 0;
   ep_return[e] = 0.0;

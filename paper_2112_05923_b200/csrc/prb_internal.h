@@ -211,6 +211,7 @@ struct prb_rollout_s {
   prb::DevBuf<float> d_logp, d_rew, d_val, d_adv, d_ret;  // [cap]
   prb::DevBuf<uint8_t> d_done;     // [cap]
   prb::DevBuf<float> d_boot;       // [N] bootstrap V(s_H)
+  prb::DevBuf<uint8_t> d_pack;     // bf16 weight chunks of the PointMass 3x256 tcgen05 rollout
   prb::DevBuf<double> d_advstat;   // mean, denom of the advantages (ppo.hpp:234-242)
   bool gae_valid = false;
   bool normalized = true;

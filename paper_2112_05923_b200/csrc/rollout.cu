@@ -12,6 +12,7 @@
 
 #include "policy_internal.h"
 #include "prb_internal.h"
+#include "rollout_pm_tc.h"
 
 using namespace prb;
 
@@ -35,6 +36,48 @@ void alloc_rollout(prb_rollout_s* r) {
 }  // namespace
 
 bool prb_fused_rollout_supported(prb_rollout r, prb_agent a, prb_vecenv env);
+
+// configs[2]: PointMass2D with the 3x256 actor/critic -> rollout_pm_tc.cu
+static bool pm_tc_supported(prb_rollout r, prb_agent a, prb_vecenv env) {
+  return r->mode == 2 && env->kind == PRB_KIND_POINTMASS && a->S == 6 && a->A == 2 && a->hidden.size() == 3 &&
+         a->hidden[0] == 256 && a->hidden[1] == 256 && a->hidden[2] == 256 && r->obs_mode == 0 && r->Sp == 6;
+}
+
+static void pm_tc_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed) {
+  cudaStream_t s = r->ctx->stream;
+  PmPackOffsets o{};
+  o.S = (int)a->S;
+  o.A = (int)a->A;
+  for (int i = 0; i < 4; ++i) {
+    o.a_w[i] = (int)a->aoff[i];
+    o.c_w[i] = (int)a->coff[i];
+  }
+  o.log_std = (int)a->Pa;
+  if (r->d_pack.n != kPmPackBytes) r->d_pack.alloc(kPmPackBytes);
+  ProfScope prof(r->ctx, kProfRollout);
+  launch_pm_pack(a->d_params.p, o, r->d_pack.p, s);
+  PmTcArgs t{};
+  t.pack = r->d_pack.p;
+  t.params = a->d_params.p;
+  t.o = o;
+  t.N = (int)r->N;
+  t.H = (int)r->H;
+  t.seed = seed;
+  t.st = env->d_pm_state.p;
+  t.steps = env->d_pm_steps.p;
+  t.ep_return = env->d_ep_return.p;
+  t.mt = env->d_mt.p;
+  t.mt_idx = env->d_mt_idx.p;
+  t.obs_out = env->d_obs.p;
+  t.b_obs = r->d_obs.p;
+  t.b_act = r->d_act.p;
+  t.b_logp = r->d_logp.p;
+  t.b_val = r->d_val.p;
+  t.b_rew = r->d_rew.p;
+  t.b_done = r->d_done.p;
+  t.b_boot = r->d_boot.p;
+  launch_pm_rollout_tc(t, r->ctx->num_sms, s);
+}
 void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed, std::vector<int32_t>& rows);
 
 void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8_t* done, const float* boot, size_t N,
@@ -111,6 +154,13 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     cudaStream_t s = r->ctx->stream;
     const size_t N = r->N, H = r->H, A = r->A;
     std::vector<int32_t> rows(H);
+    if (pm_tc_supported(r, a, env)) {
+      pm_tc_collect(r, a, env, seed);
+      r->ctx->sync();
+      r->full = true;
+      r->gae_valid = false;
+      return;
+    }
     if (r->mode != 0 && prb_fused_rollout_supported(r, a, env)) {
       prb_fused_rollout_launch(r, a, env, seed, rows);
       PRB_CUDA(cudaMemcpyAsync(r->d_row.p, rows.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));

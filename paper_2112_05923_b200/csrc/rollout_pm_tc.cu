@@ -1,0 +1,364 @@
+// rollout_pm_tc.cu -- worker_collect (pod.hpp:95-132) for the PointMass2D
+// VecEnv (env.hpp:84-146) with the configs[2] 3x256 actor/critic
+// (6-256-256-256-2 / 6-256-256-256-1, tanh) on the 5th-gen tensor cores.
+//
+// The 3x256 weights (557 KB as bf16) do not fit one SM, so they are STREAMED:
+// a one-off pack kernel lays them out in HBM as bf16 chunks already in the
+// UMMA K-major operand layout, in exactly the order the MMAs consume them, and
+// a producer warp streams the chunks (L2-resident after the first tile) into a
+// 5-slot shared-memory ring with 1-D bulk async copies (TMA engine, mbarrier
+// transaction counts).  One persistent CTA per SM, 320 threads, warp roles:
+//   warps 0-3  actor group : obs tile, actor epilogues (TMEM -> +b, tanh ->
+//                            bf16 operand), Philox sample + log-prob,
+//                            PointMass step in fp64, rollout writes
+//   warps 4-7  critic group: critic epilogues, value / bootstrap writes
+//   warp  8    MMA issuer  : tcgen05.mma M=128, fp32 accumulators in TMEM
+//                            (actor D = cols 0-255, critic D = cols 256-511)
+//   warp  9    producer    : weight chunks -> ring
+// Actor and critic are independent chains sharing only the obs tile, so the
+// tensor core runs one net's layer while the other group runs its epilogue.
+// Per-step chunk order (36 chunks): W1a W1c | W2a x8 | W2c x8 | W3a x8 | W3c x8 | W4a W4c.
+#include <cuda_bf16.h>
+
+#include "pm_env.cuh"
+#include "prb_internal.h"
+#include "rng.cuh"
+#include "rollout_pm_tc.h"
+#include "tc.cuh"
+
+namespace prb {
+namespace {
+
+constexpr int kM = 128;      // envs per tile == MMA M == TMEM lanes
+constexpr int kHid = 256;    // hidden width
+constexpr int kX = 16;       // obs tile width (6 used)
+constexpr int kStages = 5;   // weight ring slots
+constexpr int kSlot = 16384; // bytes per slot
+constexpr int kChunks = 36;  // weight chunks per step
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kLogTwoPiF = 1.8378770664093454836f;
+
+__host__ __device__ constexpr uint32_t chunk_bytes(int c) { return (c < 2 || c >= 34) ? 8192u : 16384u; }
+__host__ __device__ constexpr uint32_t chunk_off(int c) {
+  return c < 2 ? (uint32_t)c * 8192u : (c < 34 ? 16384u + (uint32_t)(c - 2) * 16384u : 540672u + (uint32_t)(c - 34) * 8192u);
+}
+static_assert(chunk_off(35) + chunk_bytes(35) == kPmPackBytes, "pack size");
+
+// bf16 pack of the flat fp32 params in consumption order (B[n][k] = W[k][n]).
+__global__ void pm_pack_kernel(const float* __restrict__ P, PmPackOffsets o, uint8_t* __restrict__ pack) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float v;
+  uint32_t off;
+  if (i < 2 * 4096) {  // W1 [S x 256] -> [256][16]
+    const int net = i / 4096, j = i % 4096, n = j / kX, k = j % kX;
+    const int w = net ? o.c_w[0] : o.a_w[0];
+    v = (k < o.S) ? P[w + k * kHid + n] : 0.f;
+    off = chunk_off(net) + tc::kmajor_offset(n, k, kX);
+  } else if (i < 2 * 4096 + 4 * 65536) {  // W2/W3 [256 x 256] -> 8 chunks of [256][32]
+    const int j = i - 2 * 4096, L = j / 65536, jj = j % 65536, n = jj / kHid, k = jj % kHid;
+    const int w = (L == 0) ? o.a_w[1] : (L == 1) ? o.c_w[1] : (L == 2) ? o.a_w[2] : o.c_w[2];
+    v = P[w + k * kHid + n];
+    off = chunk_off(2 + 8 * L + k / 32) + tc::kmajor_offset(n, k % 32, 32);
+  } else if (i < 2 * 4096 + 4 * 65536 + 2 * 4096) {  // W4 [256 x out] -> [16][256]
+    const int j = i - 2 * 4096 - 4 * 65536, net = j / 4096, jj = j % 4096, n = jj / kHid, k = jj % kHid;
+    const int out = net ? 1 : o.A;
+    const int w = net ? o.c_w[3] : o.a_w[3];
+    v = (n < out) ? P[w + k * out + n] : 0.f;
+    off = chunk_off(34 + net) + tc::kmajor_offset(n, k, kHid);
+  } else {
+    return;
+  }
+  *reinterpret_cast<__nv_bfloat16*>(pack + off) = __float2bfloat16_rn(v);
+}
+
+struct PmSmem {
+  alignas(1024) uint8_t ring[kStages][kSlot];
+  alignas(1024) uint8_t h[2][kM * kHid * 2];  // bf16 A operands [128][256]: actor, critic
+  alignas(1024) uint8_t x[kM * kX * 2];       // bf16 obs tile [128][16]
+  float bias[2][3][kHid];                     // hidden-layer biases [net][layer]
+  float b4a[2], b4c, sig[2], isig[2], lpc;
+  uint64_t full[kStages], empty[kStages];
+  uint64_t dfull[2];  // MMA -> group: layer result in TMEM
+  uint64_t ready[2];  // group -> MMA: operand written / accumulator free (4 warp arrivals)
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ void group_signal(uint64_t* bar) {
+  tc::fence_proxy_async();  // this thread's operand stores -> async proxy
+  tc::fence_before_sync();  // this thread's TMEM loads are complete
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
+}
+
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t& ph) {
+  tc::mbar_wait(bar, ph);
+  ph ^= 1;
+  tc::fence_after_sync();
+}
+
+// this thread's row of a 256-column accumulator -> tanh(. + b) -> bf16 operand row
+__device__ __forceinline__ void epi_hidden(uint32_t trow, const float* bias, uint8_t* hb, int row) {
+#pragma unroll 1
+  for (int c = 0; c < kHid; c += 32) {
+    uint32_t v[32];
+    tc::tmem_ld32(trow + c, v);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      pk[i] = tc::pack_bf16(tc::tanh_fast(__uint_as_float(v[2 * i]) + bias[c + 2 * i]),
+                            tc::tanh_fast(__uint_as_float(v[2 * i + 1]) + bias[c + 2 * i + 1]));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(hb + tc::kmajor_offset(row, c + 8 * q, kHid)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  PmSmem& s = *reinterpret_cast<PmSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = (a.N + kM - 1) / kM;
+  const float* P = a.params;
+
+  for (int i = tid; i < 2 * 3 * kHid; i += kThreads) {
+    const int net = i / (3 * kHid), L = (i / kHid) % 3, n = i % kHid;
+    const int w = net ? a.o.c_w[L] : a.o.a_w[L];
+    const int in = (L == 0) ? a.o.S : kHid;
+    s.bias[net][L][n] = P[w + in * kHid + n];
+  }
+  if (tid < 2) {
+    s.b4a[tid] = P[a.o.a_w[3] + kHid * 2 + tid];
+    const float l = P[a.o.log_std + tid];
+    s.sig[tid] = expf(l);
+    s.isig[tid] = expf(-l);
+  }
+  if (tid == 0) {
+    s.b4c = P[a.o.c_w[3] + kHid];
+    s.lpc = -kLogTwoPiF - P[a.o.log_std] - P[a.o.log_std + 1];
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.full[i], 1);
+      tc::mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.dfull[i], 1);
+      tc::mbar_init(&s.ready[i], 4);
+    }
+  }
+  if (warp == 8) tc::tmem_alloc(&s.tmem, kTmemCols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = s.tmem;
+
+  if (warp == 9) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int h = 0; h <= a.H; ++h)
+#pragma unroll 1
+          for (int c = 0; c < kChunks; ++c, ++it) {
+            const uint32_t slot = it % kStages, use = it / kStages;
+            if (use) tc::mbar_wait(&s.empty[slot], (use - 1) & 1);
+            tc::mbar_arrive_expect_tx(&s.full[slot], chunk_bytes(c));
+            tc::bulk_g2s(s.ring[slot], a.pack + chunk_off(c), chunk_bytes(c), &s.full[slot]);
+          }
+    }
+  } else if (warp == 8) {  // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t ID_256 = tc::idesc_bf16(kM, kHid), ID_16 = tc::idesc_bf16(kM, 16);
+      const uint32_t x_addr = tc::smem_u32(s.x), ring0 = tc::smem_u32(s.ring[0]);
+      const uint32_t h_addr[2] = {tc::smem_u32(s.h[0]), tc::smem_u32(s.h[1])};
+      uint32_t it = 0, rph[2] = {0, 0};
+      auto take = [&]() -> uint32_t {  // next weight chunk: wait until it has landed
+        const uint32_t slot = it % kStages;
+        tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
+        return slot;
+      };
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int h = 0; h <= a.H; ++h)
+#pragma unroll 1
+          for (int L = 0; L < 4; ++L)
+#pragma unroll 1
+            for (int net = 0; net < 2; ++net) {
+              tc::mbar_wait(&s.ready[net], rph[net]);
+              rph[net] ^= 1;
+              tc::fence_after_sync();
+              const uint32_t d = tbase + (uint32_t)net * kHid;
+              if (L == 0) {  // [128 x 16] obs . [16 x 256]
+                const uint32_t slot = take();
+                tc::mma_bf16(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(ring0 + slot * kSlot, 128, kX * 16),
+                             ID_256, 0);
+                tc::mma_commit(&s.empty[slot]);
+                ++it;
+              } else if (L < 3) {  // [128 x 256] h . [256 x 256], 8 chunks of K=32
+#pragma unroll 1
+                for (int q = 0; q < 8; ++q) {
+                  const uint32_t slot = take();
+                  const uint32_t b = ring0 + slot * kSlot;
+#pragma unroll
+                  for (int j = 0; j < 2; ++j)
+                    tc::mma_bf16(d, tc::smem_desc(h_addr[net] + (2 * q + j) * 256, 128, kHid * 16),
+                                 tc::smem_desc(b + j * 256, 128, 32 * 16), ID_256, (q | j) != 0);
+                  tc::mma_commit(&s.empty[slot]);
+                  ++it;
+                }
+              } else {  // head: [128 x 256] h . [256 x 16]
+                const uint32_t slot = take();
+                const uint32_t b = ring0 + slot * kSlot;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  tc::mma_bf16(d, tc::smem_desc(h_addr[net] + j * 256, 128, kHid * 16),
+                               tc::smem_desc(b + j * 256, 128, kHid * 16), ID_16, j != 0);
+                tc::mma_commit(&s.empty[slot]);
+                ++it;
+              }
+              tc::mma_commit(&s.dfull[net]);
+            }
+    }
+  } else if (warp < 4) {  // ---------------- actor group ----------------
+    const int row = tid;
+    const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);
+    uint32_t dph = 0;
+    const size_t N = a.N;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const size_t e = (size_t)tile * kM + row;
+      const bool live = e < N;
+      double st[6];
+      int32_t steps = 0, idx = 0;
+      double ret = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) st[j] = live ? a.st[j * N + e] : 0.0;
+      if (live) {
+        steps = a.steps[e];
+        ret = a.ep_return[e];
+        idx = a.mt_idx[e];
+      }
+      for (int h = 0; h <= a.H; ++h) {
+        float o[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) o[j] = (float)st[j];
+        {  // obs row -> X (bf16, cols 6..15 zero)
+          uint8_t* xr = s.x;
+          *reinterpret_cast<uint4*>(xr + tc::kmajor_offset(row, 0, kX)) =
+              make_uint4(tc::pack_bf16(o[0], o[1]), tc::pack_bf16(o[2], o[3]), tc::pack_bf16(o[4], o[5]), 0u);
+          *reinterpret_cast<uint4*>(xr + tc::kmajor_offset(row, 8, kX)) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        group_signal(&s.ready[0]);
+#pragma unroll 1
+        for (int L = 0; L < 3; ++L) {
+          group_wait(&s.dfull[0], dph);
+          epi_hidden(trow, s.bias[0][L], s.h[0], row);
+          group_signal(&s.ready[0]);
+        }
+        group_wait(&s.dfull[0], dph);
+        float mv[16];
+        tc::tmem_ld16(trow, mv);
+        if (h == a.H) {  // the VecEnv's states after the rollout
+          if (live)
+#pragma unroll
+            for (int j = 0; j < 6; ++j) a.obs_out[e * 6 + j] = o[j];
+          break;
+        }
+        // a = mu + sigma * eps (Philox stream of policy_kernel), log-prob (nn.hpp:215-224,250-265)
+        const Philox4 rr = philox4x32_10((uint32_t)a.seed, (uint32_t)(a.seed >> 32), 0u, (uint32_t)e, (uint32_t)h, 0u);
+        const float2 z = box_muller(rr.x, rr.y);
+        const float m0 = mv[0] + s.b4a[0], m1 = mv[1] + s.b4a[1];
+        const float act0 = m0 + s.sig[0] * z.x, act1 = m1 + s.sig[1] * z.y;
+        const float z0 = (act0 - m0) * s.isig[0], z1 = (act1 - m1) * s.isig[1];
+        const float lp = s.lpc - 0.5f * (z0 * z0 + z1 * z1);
+        // VecEnv step: clamp to the spec bounds (env.hpp:213-215), pointmass_step, auto-reset
+        double n[6], r;
+        bool done;
+        pm::step(st, pm::clamp_ref((double)act0, -1.0, 1.0), pm::clamp_ref((double)act1, -1.0, 1.0), steps, n, r,
+                 done);
+        ret = __dadd_rn(ret, r);
+        if (done) {
+          if (live) pm::reset_draws(a.mt + e, N, idx, n);
+          steps = 0;
+          ret = 0.0;
+        } else {
+          ++steps;
+        }
+        if (live) {
+          const size_t slab = (size_t)h * N + e;
+          float2* ob = reinterpret_cast<float2*>(a.b_obs + slab * 6);
+          ob[0] = make_float2(o[0], o[1]);
+          ob[1] = make_float2(o[2], o[3]);
+          ob[2] = make_float2(o[4], o[5]);
+          reinterpret_cast<float2*>(a.b_act)[slab] = make_float2(act0, act1);
+          a.b_logp[slab] = lp;
+          a.b_rew[slab] = (float)r;
+          a.b_done[slab] = done ? 1 : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 6; ++j) st[j] = n[j];
+      }
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) a.st[j * N + e] = st[j];
+        a.steps[e] = steps;
+        a.ep_return[e] = ret;
+        a.mt_idx[e] = idx;
+      }
+    }
+  } else {  // ---------------- critic group (warps 4-7) ----------------
+    const int row = tid - kM;
+    const uint32_t trow = tbase + ((uint32_t)((warp - 4) * 32) << 16) + kHid;
+    uint32_t dph = 0;
+    const size_t N = a.N;
+    group_signal(&s.ready[1]);  // critic accumulator free
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const size_t e = (size_t)tile * kM + row;
+      const bool live = e < N;
+      for (int h = 0; h <= a.H; ++h) {
+#pragma unroll 1
+        for (int L = 0; L < 3; ++L) {
+          group_wait(&s.dfull[1], dph);
+          epi_hidden(trow, s.bias[1][L], s.h[1], row);
+          group_signal(&s.ready[1]);
+        }
+        group_wait(&s.dfull[1], dph);
+        float vv[16];
+        tc::tmem_ld16(trow, vv);
+        group_signal(&s.ready[1]);  // accumulator read: the next step's L1 may overwrite it
+        const float value = vv[0] + s.b4c;
+        if (live) {
+          if (h == a.H)
+            a.b_boot[e] = value;  // bootstrap V(s_H) (pod.hpp:127-131)
+          else
+            a.b_val[(size_t)h * N + e] = value;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 8) tc::tmem_dealloc(tbase, kTmemCols);
+}
+
+}  // namespace
+
+size_t pm_rollout_tc_smem() { return sizeof(PmSmem); }
+
+void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, cudaStream_t s) {
+  const int total = 2 * 4096 + 4 * 65536 + 2 * 4096;
+  pm_pack_kernel<<<(total + 255) / 256, 256, 0, s>>>(params, o, pack);
+  PRB_CHECK_LAUNCH();
+}
+
+void launch_pm_rollout_tc(const PmTcArgs& a, int num_sms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(PmSmem)));
+    attr = true;
+  }
+  const int ntiles = (a.N + kM - 1) / kM;
+  const int grid = ntiles < num_sms ? ntiles : num_sms;
+  pm_rollout_tc_kernel<<<grid, kThreads, sizeof(PmSmem), s>>>(a);
+  PRB_CHECK_LAUNCH();
+}
+
+}  // namespace prb

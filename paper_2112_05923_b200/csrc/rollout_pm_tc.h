@@ -1,0 +1,42 @@
+// rollout_pm_tc.h -- launch descriptor of the tcgen05 PointMass 3x256 rollout.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace prb {
+
+constexpr uint32_t kPmPackBytes = 4 * 8192 + 32 * 16384;  // bf16 weight chunks of both nets
+
+struct PmPackOffsets {
+  int S, A;                // 6, 2
+  int a_w[4], c_w[4];      // flat W offsets of the 4 layers (bias follows each W)
+  int log_std;
+};
+
+struct PmTcArgs {
+  const uint8_t* pack;  // kPmPackBytes, from launch_pm_pack
+  const float* params;
+  PmPackOffsets o;
+  int N, H;
+  uint64_t seed;
+  double* st;        // [6][N]
+  int32_t* steps;    // [N]
+  double* ep_return; // [N]
+  uint64_t* mt;      // [312][N]
+  int32_t* mt_idx;   // [N]
+  float* obs_out;    // [N][6]
+  float* b_obs;      // [H][N][6]
+  float* b_act;      // [H][N][2]
+  float* b_logp;
+  float* b_val;
+  float* b_rew;
+  uint8_t* b_done;
+  float* b_boot;
+};
+
+size_t pm_rollout_tc_smem();
+void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, cudaStream_t s);
+void launch_pm_rollout_tc(const PmTcArgs& a, int num_sms, cudaStream_t s);
+
+}  // namespace prb

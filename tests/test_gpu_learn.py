@@ -415,8 +415,12 @@ def test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, fused):
         assert np.allclose(eps.reshape(N, H, K)[:, 0], ref_eps, atol=1e-3 if fused == 1 else 5e-2)
 
 
-def test_collect_pointmass_rollout(pr, ctx, orc):
-    N, H = 64, 250
+@pytest.mark.parametrize("mode,N,H", [(0, 64, 250), (2, 64, 250), (2, 1000, 40), (2, 40000, 6)])
+def test_collect_pointmass_rollout(pr, ctx, orc, mode, N, H):
+    """PointMass2D worker_collect: the env transitions replay bit-exactly on the
+    oracle from the recorded actions; mode 2 (tcgen05 3x256, bf16 operands)
+    log-probs / values agree with the fp32 policy on the recorded states within
+    the bf16 tolerance.  N=40000 spans more tiles than SMs (persistent loop)."""
     env = pr.VectorizedEnvironment.pointmass(ctx, N)
     env.reset(3)
     oracle_g = (MT64 * N)()
@@ -424,6 +428,7 @@ def test_collect_pointmass_rollout(pr, ctx, orc):
     orc.orc_pm_vec_reset(N, 3, oracle_g, ptr(st), ptr(sc, U64), ptr(er))
     agent = pr.Agent.init(ctx, 6, 2, seed=4, hidden=(256, 256, 256))
     ro = pr.Rollout.for_env(env, H)
+    ro.set_mode(mode)
     ro.collect(agent, env, seed=8)
     b = ro.download()
     states = b["states"].reshape(N, H, 6); acts = b["actions"].reshape(N, H, 2)
@@ -434,4 +439,30 @@ def test_collect_pointmass_rollout(pr, ctx, orc):
                             ptr(d, U8), ptr(np.zeros((N, 6))), ptr(np.zeros(N)), ptr(np.zeros(N, np.uint64), U64))
         assert np.array_equal(b["rewards"].reshape(N, H)[:, h], f32(r))
         assert np.array_equal(b["dones"].reshape(N, H)[:, h], d)
-    assert b["dones"].sum() >= N
+    assert np.array_equal(env.states(), f32(st))
+    assert np.array_equal(env.step_counts(), sc)
+    if H >= 200:
+        assert b["dones"].sum() >= N
+    lp, val, boot = (agent.log_prob(b["states"], b["actions"]), agent.value(b["states"]),
+                     agent.value(env.states()))
+    if mode == 0:
+        assert np.array_equal(lp, b["log_probs"].astype(np.float32))
+        assert np.array_equal(val, b["values"].astype(np.float32))
+    else:  # bf16 operands + tanh.approx through 3 hidden layers of 256
+        tl, tv = 1e-2, 2e-2
+        assert np.all(np.abs(lp - b["log_probs"]) <= tl * (1 + np.abs(lp))), np.max(np.abs(lp - b["log_probs"]))
+        assert np.all(np.abs(val - b["values"]) <= tv * (1 + np.abs(val))), np.max(np.abs(val - b["values"]))
+        assert np.all(np.abs(boot - b["bootstrap"]) <= tv * (1 + np.abs(boot)))
+        mean = agent.policy_mean(b["states"])
+        # noise stream identical to the standalone sampler: eps recovered from the actions
+        ls = _pm_log_std(agent)
+        eps = (b["actions"] - mean) / np.exp(ls)
+        s0 = np.ascontiguousarray(states[:, 0])
+        ref_eps = agent.policy_sample(s0, seed=8, counter=0)["eps"]
+        assert np.allclose(eps.reshape(N, H, 2)[:, 0], ref_eps, atol=5e-2)
+
+
+def _pm_log_std(agent):
+    flat = agent.flatten_params()
+    pa = 6 * 256 + 256 + 2 * (256 * 256 + 256) + 256 * 2 + 2
+    return flat[pa:pa + 2]
