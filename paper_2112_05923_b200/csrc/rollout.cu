@@ -8,6 +8,8 @@
 // step as a time index into the env's read-only feature table (all envs of a
 // VecEnv share t, stock_env.hpp:161) -- 124 B instead of 724 B per transition.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "policy_internal.h"
@@ -76,7 +78,23 @@ static void pm_tc_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t s
   t.b_rew = r->d_rew.p;
   t.b_done = r->d_done.p;
   t.b_boot = r->d_boot.p;
+  const char* trace_path = getenv("PRB_PM_TRACE");  // debug: clock64 phase trace of CTA 0
+  prb::DevBuf<unsigned long long> d_trace;
+  if (trace_path) {
+    d_trace.alloc(4 * kPmTraceLen);
+    PRB_CUDA(cudaMemsetAsync(d_trace.p, 0, d_trace.bytes(), s));
+    t.trace = d_trace.p;
+  }
   launch_pm_rollout_tc(t, r->ctx->num_sms, s);
+  if (trace_path) {
+    std::vector<unsigned long long> h(4 * kPmTraceLen);
+    PRB_CUDA(cudaMemcpyAsync(h.data(), d_trace.p, d_trace.bytes(), cudaMemcpyDeviceToHost, s));
+    PRB_CUDA(cudaStreamSynchronize(s));
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+  }
 }
 void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed, std::vector<int32_t>& rows);
 

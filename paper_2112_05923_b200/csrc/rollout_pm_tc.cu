@@ -3,21 +3,21 @@
 // (6-256-256-256-2 / 6-256-256-256-1, tanh) on the 5th-gen tensor cores.
 //
 // The 3x256 weights (557 KB as bf16) do not fit one SM, so they are STREAMED:
-// a one-off pack kernel lays them out in HBM as bf16 chunks already in the
-// UMMA K-major operand layout, in exactly the order the MMAs consume them, and
-// a producer warp streams the chunks (L2-resident after the first tile) into a
-// 5-slot shared-memory ring with 1-D bulk async copies (TMA engine, mbarrier
-// transaction counts).  One persistent CTA per SM, 320 threads, warp roles:
-//   warps 0-3  actor group : obs tile, actor epilogues (TMEM -> +b, tanh ->
-//                            bf16 operand), Philox sample + log-prob,
-//                            PointMass step in fp64, rollout writes
-//   warps 4-7  critic group: critic epilogues, value / bootstrap writes
-//   warp  8    MMA issuer  : tcgen05.mma M=128, fp32 accumulators in TMEM
-//                            (actor D = cols 0-255, critic D = cols 256-511)
-//   warp  9    producer    : weight chunks -> ring
-// Actor and critic are independent chains sharing only the obs tile, so the
-// tensor core runs one net's layer while the other group runs its epilogue.
-// Per-step chunk order (36 chunks): W1a W1c | W2a x8 | W2c x8 | W3a x8 | W3c x8 | W4a W4c.
+// a one-off pack kernel lays them out in HBM as bf16 chunks ([256 N][32 K],
+// 16 KB) already in the UMMA K-major operand layout, and producer warps stream
+// them (L2-resident after the first tile) through a 5-slot shared-memory ring
+// with 1-D bulk async copies (TMA engine, mbarrier transaction counts), in the
+// exact order the single MMA issuer consumes them.  One persistent CTA per SM,
+// 384 threads.  The actor and the critic are two chains that share only the obs
+// tile; the critic runs one epilogue behind the actor so that one net's
+// epilogue overlaps the other net's MMAs:
+//   warps 0-3   actor epilogues (TMEM -> +b, tanh -> bf16 operand), obs tile,
+//               Philox sample + log-prob, PointMass step in fp64, rollout rows
+//   warps 4-7   critic epilogues, value / bootstrap writes
+//   warp  8     MMA issuer: tcgen05.mma M=128 N=256 K=16 in a fixed global
+//               order, fp32 accumulators in TMEM (actor cols 0-255, critic 256-511)
+//   warps 9+    producers (kProducers) of the weight ring
+// Per net and step: 18 chunks = W1 [256x16] | W2 8 x [256x32] | W3 8 x [256x32] | W4 [16x256].
 #include <cuda_bf16.h>
 
 #include "pm_env.cuh"
@@ -32,56 +32,77 @@ namespace {
 constexpr int kM = 128;      // envs per tile == MMA M == TMEM lanes
 constexpr int kHid = 256;    // hidden width
 constexpr int kX = 16;       // obs tile width (6 used)
-constexpr int kStages = 5;   // weight ring slots
-constexpr int kSlot = 16384; // bytes per slot
-constexpr int kChunks = 36;  // weight chunks per step
-constexpr int kThreads = 320;
+constexpr int kKC = kPmChunkK;         // K per weight chunk of the hidden layers
+constexpr int kCPL = kHid / kKC;        // chunks per hidden layer
+constexpr int kSlot = kHid * kKC * 2;   // bytes per chunk / ring slot ([256 N][kKC K] bf16)
+constexpr int kStages = kKC == 16 ? 10 : 5;  // ring slots shared by both nets (smem: kStages x kSlot)
+constexpr int kChunks = 2 + 2 * kCPL;   // chunks per net per step: W1 | W2 | W3 | W4
+constexpr uint32_t kNetPack = kChunks * kSlot;
+// W1 [256][16] and W4 [16][256] are 8 KB; the hidden-layer chunks are kSlot
+__host__ __device__ constexpr uint32_t chunk_bytes(int c) { return (c == 0 || c == kChunks - 1) ? 8192u : (uint32_t)kSlot; }
+__device__ __forceinline__ int op_nchunks(int layer) { return (layer == 1 || layer == 2) ? kCPL : 1; }
+__device__ __forceinline__ int op_chunk(int layer, int q) {
+  return layer == 0 ? 0 : (layer == 3 ? kChunks - 1 : 1 + kCPL * (layer - 1) + q);
+}
+constexpr int kProducers = 3;  // producer warps: one warp keeps ~one bulk copy in flight
+constexpr int kThreads = 32 * (9 + kProducers);
+// op k of a step: (net, layer) in issue order, see the kernel
+__device__ constexpr int kOpNet[8] = {0, 1, 1, 0, 1, 0, 1, 0};
+__device__ constexpr int kOpLayer[8] = {0, 3, 0, 1, 1, 2, 2, 3};
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
-
-__host__ __device__ constexpr uint32_t chunk_bytes(int c) { return (c < 2 || c >= 34) ? 8192u : 16384u; }
-__host__ __device__ constexpr uint32_t chunk_off(int c) {
-  return c < 2 ? (uint32_t)c * 8192u : (c < 34 ? 16384u + (uint32_t)(c - 2) * 16384u : 540672u + (uint32_t)(c - 34) * 8192u);
-}
-static_assert(chunk_off(35) + chunk_bytes(35) == kPmPackBytes, "pack size");
+static_assert(2 * kNetPack == kPmPackBytes, "pack size");
 
 // bf16 pack of the flat fp32 params in consumption order (B[n][k] = W[k][n]).
+// Per net, 34 chunks of 8 KB: W1 [256][16], W2/W3 as 16 K-steps [256][16], W4 [16][256].
 __global__ void pm_pack_kernel(const float* __restrict__ P, PmPackOffsets o, uint8_t* __restrict__ pack) {
+  constexpr int kPerNet = 4096 + 2 * 65536 + 4096;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * kPerNet) return;
+  const int net = i / kPerNet, j = i % kPerNet;
+  const int* w = net ? o.c_w : o.a_w;
+  uint8_t* base = pack + (size_t)net * kNetPack;
   float v;
   uint32_t off;
-  if (i < 2 * 4096) {  // W1 [S x 256] -> [256][16]
-    const int net = i / 4096, j = i % 4096, n = j / kX, k = j % kX;
-    const int w = net ? o.c_w[0] : o.a_w[0];
-    v = (k < o.S) ? P[w + k * kHid + n] : 0.f;
-    off = chunk_off(net) + tc::kmajor_offset(n, k, kX);
-  } else if (i < 2 * 4096 + 4 * 65536) {  // W2/W3 [256 x 256] -> 8 chunks of [256][32]
-    const int j = i - 2 * 4096, L = j / 65536, jj = j % 65536, n = jj / kHid, k = jj % kHid;
-    const int w = (L == 0) ? o.a_w[1] : (L == 1) ? o.c_w[1] : (L == 2) ? o.a_w[2] : o.c_w[2];
-    v = P[w + k * kHid + n];
-    off = chunk_off(2 + 8 * L + k / 32) + tc::kmajor_offset(n, k % 32, 32);
-  } else if (i < 2 * 4096 + 4 * 65536 + 2 * 4096) {  // W4 [256 x out] -> [16][256]
-    const int j = i - 2 * 4096 - 4 * 65536, net = j / 4096, jj = j % 4096, n = jj / kHid, k = jj % kHid;
+  if (j < 4096) {  // W1 [S x 256]
+    const int n = j / kX, k = j % kX;
+    v = (k < o.S) ? P[w[0] + k * kHid + n] : 0.f;
+    off = tc::kmajor_offset(n, k, kX);
+  } else if (j < 4096 + 2 * 65536) {  // W2 / W3 [256 x 256]
+    const int jj = j - 4096, L = jj / 65536, r = jj % 65536, n = r / kHid, k = r % kHid;
+    v = P[w[1 + L] + k * kHid + n];
+    off = (uint32_t)(1 + kCPL * L + k / kKC) * kSlot + tc::kmajor_offset(n, k % kKC, kKC);
+  } else {  // W4 [256 x out] -> [16][256]
+    const int jj = j - 4096 - 2 * 65536, n = jj / kHid, k = jj % kHid;
     const int out = net ? 1 : o.A;
-    const int w = net ? o.c_w[3] : o.a_w[3];
-    v = (n < out) ? P[w + k * out + n] : 0.f;
-    off = chunk_off(34 + net) + tc::kmajor_offset(n, k, kHid);
-  } else {
-    return;
+    v = (n < out) ? P[w[3] + k * out + n] : 0.f;
+    off = (uint32_t)(kChunks - 1) * kSlot + tc::kmajor_offset(n, k, kHid);
   }
-  *reinterpret_cast<__nv_bfloat16*>(pack + off) = __float2bfloat16_rn(v);
+  *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(v);
 }
 
 struct PmSmem {
-  alignas(1024) uint8_t ring[kStages][kSlot];
-  alignas(1024) uint8_t h[2][kM * kHid * 2];  // bf16 A operands [128][256]: actor, critic
-  alignas(1024) uint8_t x[kM * kX * 2];       // bf16 obs tile [128][16]
-  float bias[2][3][kHid];                     // hidden-layer biases [net][layer]
+  alignas(1024) uint8_t ring[kStages][kSlot];     // weight ring (both nets, global op order)
+  alignas(1024) uint8_t h[2][kM * kHid * 2];      // bf16 A operands [128][256]: actor, critic
+  alignas(1024) uint8_t x[kM * kX * 2];           // bf16 obs tile [128][16]
+  float bias[2][3][kHid];                         // hidden-layer biases [net][layer]
   float b4a[2], b4c, sig[2], isig[2], lpc;
   uint64_t full[kStages], empty[kStages];
   uint64_t dfull[2];  // MMA -> group: layer result in TMEM
   uint64_t ready[2];  // group -> MMA: operand written / accumulator free (4 warp arrivals)
+  uint64_t xready;    // actor group -> both MMA warps: obs tile written (4 warp arrivals)
+  uint64_t xfree;     // critic MMA -> actor group: the critic's L1 has consumed the obs tile
+  uint64_t aepi1;     // actor group -> critic MMA: actor layer-1 epilogue done (phase offset)
   uint32_t tmem;
+};
+
+// clock64 event trace of CTA 0 (debug; a.trace == nullptr in production)
+struct Tracer {
+  unsigned long long* p = nullptr;
+  int n = 0;
+  __device__ __forceinline__ void mark() {
+    if (p && n < kPmTraceLen) p[n++] = clock64();
+  }
 };
 
 __device__ __forceinline__ void group_signal(uint64_t* bar) {
@@ -141,10 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
       tc::mbar_init(&s.full[i], 1);
       tc::mbar_init(&s.empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&s.dfull[i], 1);
-      tc::mbar_init(&s.ready[i], 4);
+    for (int n = 0; n < 2; ++n) {
+      tc::mbar_init(&s.dfull[n], 1);
+      tc::mbar_init(&s.ready[n], 4);
     }
+    tc::mbar_init(&s.xready, 4);
+    tc::mbar_init(&s.xfree, 1);
+    tc::mbar_init(&s.aepi1, 4);
   }
   if (warp == 8) tc::tmem_alloc(&s.tmem, kTmemCols);
   tc::fence_before_sync();
@@ -152,75 +176,114 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
   tc::fence_after_sync();
   const uint32_t tbase = s.tmem;
 
-  if (warp == 9) {  // ---------------- producer ----------------
+  // Global MMA order, identical for the producers and the issuer.  Per step g:
+  //   A1(g), C4(g-1), C1(g), A2(g), C2(g), A3(g), C3(g), A4(g)      and a final C4.
+  // The critic runs about one epilogue behind the actor (C1 waits for the actor's
+  // layer-1 epilogue), so this order is also the order in which the operands
+  // become ready: one ring serves both nets without head-of-line blocking.
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int G = my_tiles * (a.H + 1);  // steps this CTA runs
+  if (warp >= 9) {  // ---------------- producers ----------------
+    // Bulk copies issued by one warp complete roughly one at a time
+    // (profiles/mb/mb_l2smem.cu); chunk `it` goes to producer it % kProducers.
+    const int pr = warp - 9;
     if (lane == 0) {
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int h = 0; h <= a.H; ++h)
+      for (int g = 0; g <= G; ++g)
 #pragma unroll 1
-          for (int c = 0; c < kChunks; ++c, ++it) {
+        for (int k = 0; k < 8; ++k) {
+          if ((g == G && k != 1) || (g == 0 && k == 1)) continue;
+          const int net = kOpNet[k], layer = kOpLayer[k], nq = op_nchunks(layer);
+#pragma unroll 1
+          for (int q = 0; q < nq; ++q, ++it) {
+            if ((int)(it % kProducers) != pr) continue;
             const uint32_t slot = it % kStages, use = it / kStages;
+            const int c = op_chunk(layer, q);
             if (use) tc::mbar_wait(&s.empty[slot], (use - 1) & 1);
             tc::mbar_arrive_expect_tx(&s.full[slot], chunk_bytes(c));
-            tc::bulk_g2s(s.ring[slot], a.pack + chunk_off(c), chunk_bytes(c), &s.full[slot]);
+            tc::bulk_g2s(s.ring[slot], a.pack + (size_t)net * kNetPack + (size_t)c * kSlot, chunk_bytes(c),
+                         &s.full[slot]);
           }
+        }
     }
   } else if (warp == 8) {  // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t ID_256 = tc::idesc_bf16(kM, kHid), ID_16 = tc::idesc_bf16(kM, 16);
       const uint32_t x_addr = tc::smem_u32(s.x), ring0 = tc::smem_u32(s.ring[0]);
-      const uint32_t h_addr[2] = {tc::smem_u32(s.h[0]), tc::smem_u32(s.h[1])};
-      uint32_t it = 0, rph[2] = {0, 0};
+      uint32_t it = 0, rph[2] = {0, 0}, xph = 0, eph = 0;
+      Tracer tr;
+      if (a.trace && blockIdx.x == 0) tr.p = a.trace + 2 * kPmTraceLen;
+      unsigned long long waited = 0;  // trace: clocks spent waiting for weight chunks
       auto take = [&]() -> uint32_t {  // next weight chunk: wait until it has landed
         const uint32_t slot = it % kStages;
-        tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
-        return slot;
+        if (tr.p) {
+          const unsigned long long t0 = clock64();
+          tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
+          waited += clock64() - t0;
+        } else {
+          tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
+        }
+        return ring0 + slot * kSlot;
       };
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int h = 0; h <= a.H; ++h)
+      auto release = [&]() {  // the chunk's MMAs done -> slot reusable
+        tc::mma_commit(&s.empty[it % kStages]);
+        ++it;
+      };
+      for (int g = 0; g <= G; ++g)
 #pragma unroll 1
-          for (int L = 0; L < 4; ++L)
-#pragma unroll 1
-            for (int net = 0; net < 2; ++net) {
-              tc::mbar_wait(&s.ready[net], rph[net]);
-              rph[net] ^= 1;
-              tc::fence_after_sync();
-              const uint32_t d = tbase + (uint32_t)net * kHid;
-              if (L == 0) {  // [128 x 16] obs . [16 x 256]
-                const uint32_t slot = take();
-                tc::mma_bf16(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(ring0 + slot * kSlot, 128, kX * 16),
-                             ID_256, 0);
-                tc::mma_commit(&s.empty[slot]);
-                ++it;
-              } else if (L < 3) {  // [128 x 256] h . [256 x 256], 8 chunks of K=32
-#pragma unroll 1
-                for (int q = 0; q < 8; ++q) {
-                  const uint32_t slot = take();
-                  const uint32_t b = ring0 + slot * kSlot;
-#pragma unroll
-                  for (int j = 0; j < 2; ++j)
-                    tc::mma_bf16(d, tc::smem_desc(h_addr[net] + (2 * q + j) * 256, 128, kHid * 16),
-                                 tc::smem_desc(b + j * 256, 128, 32 * 16), ID_256, (q | j) != 0);
-                  tc::mma_commit(&s.empty[slot]);
-                  ++it;
-                }
-              } else {  // head: [128 x 256] h . [256 x 16]
-                const uint32_t slot = take();
-                const uint32_t b = ring0 + slot * kSlot;
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  tc::mma_bf16(d, tc::smem_desc(h_addr[net] + j * 256, 128, kHid * 16),
-                               tc::smem_desc(b + j * 256, 128, kHid * 16), ID_16, j != 0);
-                tc::mma_commit(&s.empty[slot]);
-                ++it;
-              }
-              tc::mma_commit(&s.dfull[net]);
+        for (int k = 0; k < 8; ++k) {
+          if ((g == G && k != 1) || (g == 0 && k == 1)) continue;
+          const int net = kOpNet[k], layer = kOpLayer[k];
+          if (net == 0 && layer == 0) {
+            tc::mbar_wait(&s.xready, xph);  // obs tile written
+            xph ^= 1;
+          } else {
+            tc::mbar_wait(&s.ready[net], rph[net]);  // operand written / accumulator read
+            rph[net] ^= 1;
+            if (net == 1 && layer == 0) {  // the actor's layer-1 epilogue is done (phase offset)
+              tc::mbar_wait(&s.aepi1, eph);
+              eph ^= 1;
             }
+          }
+          tc::fence_after_sync();
+          tr.mark();
+          const uint32_t d = tbase + (uint32_t)net * kHid;
+          const uint32_t h_addr = tc::smem_u32(s.h[net]);
+          if (layer == 0) {  // [128 x 16] obs . [16 x 256]
+            const uint32_t b = take();
+            tc::mma_bf16(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(b, 128, kX * 16), ID_256, 0);
+            release();
+            if (net == 1) tc::mma_commit(&s.xfree);
+          } else if (layer < 3) {  // [128 x 256] h . [256 x 256], kCPL chunks of kKC/16 K-steps
+#pragma unroll 1
+            for (int q = 0; q < kCPL; ++q) {
+              const uint32_t b = take();
+#pragma unroll
+              for (int j = 0; j < kKC / 16; ++j)
+                tc::mma_bf16(d, tc::smem_desc(h_addr + (q * (kKC / 16) + j) * 256, 128, kHid * 16),
+                             tc::smem_desc(b + j * 256, 128, kKC * 16), ID_256, (q | j) != 0);
+              release();
+            }
+          } else {  // head: [128 x 256] h . [256 x 16]
+            const uint32_t b = take();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              tc::mma_bf16(d, tc::smem_desc(h_addr + j * 256, 128, kHid * 16),
+                           tc::smem_desc(b + j * 256, 128, kHid * 16), ID_16, j != 0);
+            release();
+          }
+          tc::mma_commit(&s.dfull[net]);
+          tr.mark();
+          if (tr.p && g < 8 && k == 7) a.trace[3 * kPmTraceLen + g] = waited;
+        }
     }
   } else if (warp < 4) {  // ---------------- actor group ----------------
     const int row = tid;
     const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);
-    uint32_t dph = 0;
+    uint32_t dph = 0, fph = 0;
+    bool first = true;
+    Tracer tr;
+    if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
     const size_t N = a.N;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const size_t e = (size_t)tile * kM + row;
@@ -239,20 +302,29 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
         float o[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) o[j] = (float)st[j];
-        {  // obs row -> X (bf16, cols 6..15 zero)
-          uint8_t* xr = s.x;
-          *reinterpret_cast<uint4*>(xr + tc::kmajor_offset(row, 0, kX)) =
-              make_uint4(tc::pack_bf16(o[0], o[1]), tc::pack_bf16(o[2], o[3]), tc::pack_bf16(o[4], o[5]), 0u);
-          *reinterpret_cast<uint4*>(xr + tc::kmajor_offset(row, 8, kX)) = make_uint4(0u, 0u, 0u, 0u);
+        if (!first) {  // the critic's L1 of the previous step has consumed X
+          tc::mbar_wait(&s.xfree, fph);
+          fph ^= 1;
         }
-        group_signal(&s.ready[0]);
+        first = false;
+        {  // obs row -> X (bf16, cols 6..15 zero)
+          *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(row, 0, kX)) =
+              make_uint4(tc::pack_bf16(o[0], o[1]), tc::pack_bf16(o[2], o[3]), tc::pack_bf16(o[4], o[5]), 0u);
+          *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(row, 8, kX)) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        group_signal(&s.xready);
+        tr.mark();
 #pragma unroll 1
         for (int L = 0; L < 3; ++L) {
           group_wait(&s.dfull[0], dph);
+          tr.mark();
           epi_hidden(trow, s.bias[0][L], s.h[0], row);
           group_signal(&s.ready[0]);
+          if (L == 0 && (threadIdx.x & 31) == 0) tc::mbar_arrive(&s.aepi1);
+          tr.mark();
         }
         group_wait(&s.dfull[0], dph);
+        tr.mark();
         float mv[16];
         tc::tmem_ld16(trow, mv);
         if (h == a.H) {  // the VecEnv's states after the rollout
@@ -294,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
         }
 #pragma unroll
         for (int j = 0; j < 6; ++j) st[j] = n[j];
+        tr.mark();
       }
       if (live) {
 #pragma unroll
@@ -307,6 +380,8 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
     const int row = tid - kM;
     const uint32_t trow = tbase + ((uint32_t)((warp - 4) * 32) << 16) + kHid;
     uint32_t dph = 0;
+    Tracer tr;
+    if (a.trace && blockIdx.x == 0 && tid == kM) tr.p = a.trace + kPmTraceLen;
     const size_t N = a.N;
     group_signal(&s.ready[1]);  // critic accumulator free
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -316,14 +391,18 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
 #pragma unroll 1
         for (int L = 0; L < 3; ++L) {
           group_wait(&s.dfull[1], dph);
+          tr.mark();
           epi_hidden(trow, s.bias[1][L], s.h[1], row);
           group_signal(&s.ready[1]);
+          tr.mark();
         }
         group_wait(&s.dfull[1], dph);
+        tr.mark();
         float vv[16];
         tc::tmem_ld16(trow, vv);
         group_signal(&s.ready[1]);  // accumulator read: the next step's L1 may overwrite it
         const float value = vv[0] + s.b4c;
+        tr.mark();
         if (live) {
           if (h == a.H)
             a.b_boot[e] = value;  // bootstrap V(s_H) (pod.hpp:127-131)
@@ -343,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
 size_t pm_rollout_tc_smem() { return sizeof(PmSmem); }
 
 void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, cudaStream_t s) {
-  const int total = 2 * 4096 + 4 * 65536 + 2 * 4096;
+  const int total = 2 * (4096 + 2 * 65536 + 4096);
   pm_pack_kernel<<<(total + 255) / 256, 256, 0, s>>>(params, o, pack);
   PRB_CHECK_LAUNCH();
 }

@@ -6,7 +6,9 @@
 
 namespace prb {
 
-constexpr uint32_t kPmPackBytes = 4 * 8192 + 32 * 16384;  // bf16 weight chunks of both nets
+constexpr int kPmChunkK = 32;  // K per streamed weight chunk of the 256x256 layers (16 or 32)
+// bf16 weight chunks of both nets: per net W1 | 256/kPmChunkK chunks each of W2, W3 | W4
+constexpr uint32_t kPmPackBytes = 2u * (2 + 2 * (256 / kPmChunkK)) * (256u * kPmChunkK * 2);
 
 struct PmPackOffsets {
   int S, A;                // 6, 2
@@ -33,7 +35,9 @@ struct PmTcArgs {
   float* b_rew;
   uint8_t* b_done;
   float* b_boot;
+  unsigned long long* trace;  // optional [4][kPmTraceLen] clock64 events of CTA 0 (PRB_PM_TRACE), else null
 };
+constexpr int kPmTraceLen = 512;
 
 size_t pm_rollout_tc_smem();
 void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, cudaStream_t s);

@@ -4,6 +4,7 @@
   python profiles/drive.py collect  [N] [H]   # fused stock rollout (or --unfused)
   python profiles/drive.py env      [N]       # prb_vecenv_step on device buffers
   python profiles/drive.py ppo      [N] [H]   # a few PPO minibatch steps
+  python profiles/drive.py pm       [N] [H]   # PointMass 3x256 tcgen05 rollout (configs[2])
 """
 import os
 import sys
@@ -55,6 +56,17 @@ def main():
         ro.collect(agent, env, seed=1)
         cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=1, buffer_size=N * H)
         pr.ppo_update(agent, ro, cfg, seed=3)
+        ctx.synchronize()
+    elif what == "pm":
+        N = int(args[0]) if args else 262144
+        H = int(args[1]) if len(args) > 1 else 16
+        ctx = pr.Context(0)
+        env = pr.VectorizedEnvironment.pointmass(ctx, N)
+        env.reset(7)
+        agent = pr.Agent.init(ctx, 6, 2, seed=7, hidden=(256, 256, 256))
+        ro = pr.Rollout.for_env(env, H)
+        for i in range(2):
+            ro.collect(agent, env, seed=i)
         ctx.synchronize()
     print("ok", what)
 
