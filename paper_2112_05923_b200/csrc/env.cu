@@ -23,6 +23,7 @@
 #include "prb_internal.h"
 #include "pm_env.cuh"
 #include "rng.cuh"
+#include "stock_env.cuh"
 
 using namespace prb;
 
@@ -198,8 +199,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) 
       const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
       if (d > 0.0) {
         const double price = s_p0[k];
-        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
-        const double q = min_ref(d, max_ref(affordable, 0.0));
+        const double q = stock::buy_qty(d, bal, __dmul_rn(price, cost_factor));
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
         s_sh[k * kEnvBlock + tid] += (int32_t)q;
@@ -388,8 +388,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
       const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
       if (d > 0.0) {
         const double price = s_p0[k];
-        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
-        const double q = min_ref(d, max_ref(affordable, 0.0));
+        const double q = stock::buy_qty(d, bal, __dmul_rn(price, cost_factor));
         const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
         bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
         sh[k] += (int32_t)q;
@@ -493,8 +492,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
         const double d = trunc(__dmul_rn(clamp_ref((double)ak, -1.0, 1.0), a.max_trade));
         if (d > 0.0) {
           const double price = s_p0[k];
-          const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cost_factor)));
-          const double q = min_ref(d, max_ref(affordable, 0.0));
+          const double q = stock::buy_qty(d, bal, __dmul_rn(price, cost_factor));
           const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
           bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
           sh[k] += (int32_t)q;

@@ -15,11 +15,14 @@
 // (shared_layer1_kernel) and the per-env first layer is a 31-wide product.
 // The result is the same function; only fp32 summation order differs.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "policy_internal.h"
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "stock_env.cuh"
 #include "rollout_tc.h"
 
 using namespace prb;
@@ -287,8 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) stock_rollout_fused_kernel(FusedA
         const double d = trunc(__dmul_rn(clamp_ref((double)s.act[r][k], -1.0, 1.0), a.max_trade));
         if (d > 0.0) {
           const double price = s.p0[k];
-          const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cf)));
-          const double qv = min_ref(d, max_ref(affordable, 0.0));
+          const double qv = stock::buy_qty(d, bal, __dmul_rn(price, cf));
           const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
           bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
           s.sh[k][r] += (int32_t)qv;
@@ -445,7 +447,23 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
       ta.balance = f.balance; ta.shares = f.shares; ta.ep_return = f.ep_return; ta.obs_out = f.obs_out;
       ta.b_obs = f.b_obs; ta.b_act = f.b_act; ta.b_logp = f.b_logp; ta.b_val = f.b_val; ta.b_rew = f.b_rew;
       ta.b_done = f.b_done; ta.b_boot = f.b_boot;
+      const char* trace_path = getenv("PRB_TC_TRACE");  // debug: clock64 phase trace of CTA 0
+      DevBuf<unsigned long long> d_trace;
+      if (trace_path) {
+        d_trace.alloc(kTcTraceLen);
+        PRB_CUDA(cudaMemsetAsync(d_trace.p, 0, d_trace.bytes(), s));
+        ta.trace = d_trace.p;
+      }
       launch_stock_rollout_tc(ta, s);
+      if (trace_path) {
+        std::vector<unsigned long long> hbuf(kTcTraceLen);
+        PRB_CUDA(cudaMemcpyAsync(hbuf.data(), d_trace.p, d_trace.bytes(), cudaMemcpyDeviceToHost, s));
+        PRB_CUDA(cudaStreamSynchronize(s));
+        if (FILE* f = fopen(trace_path, "wb")) {
+          fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
+          fclose(f);
+        }
+      }
     } else {  // fp32 SIMT MLP
       static bool attr = false;
       if (!attr) {

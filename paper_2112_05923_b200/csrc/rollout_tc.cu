@@ -27,6 +27,7 @@
 
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "stock_env.cuh"
 #include "rollout_tc.h"
 #include "tc.cuh"
 
@@ -177,10 +178,13 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   constexpr uint32_t ID_L3A = tc::idesc_bf16(128, 32), ID_L3C = tc::idesc_bf16(128, 16);
   uint32_t phase = 0;
   const size_t row = e0 + tid;
+  tc::Tracer<kTcTraceLen> tr;
+  if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
 
   for (int h = 0; h <= a.H; ++h) {
     const int t = a.t_seq[h];
     __syncthreads();  // previous step's staging reads of X are done
+    tr.mark();
     s.c1[tid] = a.shared_l1[(size_t)h * 128 + tid] + b1_mine;
     if (tid < K) {
       s.p0[tid] = a.close_tk[(size_t)t * K + tid];
@@ -199,20 +203,30 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
             make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
                        tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
     }
+    tr.mark();
     publish_operand();
     mma_layer(tbase, 0, x_addr, kKX * 16, w1_addr, kKX * 16, kKX / 16, ID_L1, &s.mbar, phase);   // L1
+    tr.mark();
     epilogue64(tlane, 0, s.c1, s.x, tid);                                                          // actor h1
+    tr.mark();
     publish_operand();
     mma_layer(tbase, 0, x_addr, 1024, w2a_addr, 1024, 4, ID_L2, &s.mbar, phase);                    // L2a
+    tr.mark();
     epilogue64(tlane, 64, s.c1, s.x, tid);                                                         // critic h1
+    tr.mark();
     publish_operand();
     mma_layer(tbase, 64, x_addr, 1024, w2c_addr, 1024, 4, ID_L2, &s.mbar, phase);                   // L2c
+    tr.mark();
     epilogue64(tlane, 0, s.b2, s.x, tid);                                                          // actor h2
+    tr.mark();
     publish_operand();
     mma_layer(tbase, 0, x_addr, 1024, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase);                   // L3a
+    tr.mark();
     epilogue64(tlane, 64, s.b2, s.x, tid);                                                         // critic h2
+    tr.mark();
     publish_operand();
     mma_layer(tbase, 32, x_addr, 1024, w3c_addr, 1024, 4, ID_L3C, &s.mbar, phase);                  // L3c
+    tr.mark();
     float vcrit[16];
     tc::tmem_ld16(tlane + 32, vcrit);
     const float value = vcrit[0] + s.b3c;
@@ -240,6 +254,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     __syncthreads();
     store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, P1, nloc);
     __syncthreads();
+    tr.mark();
     // ---- a = mu + sigma * eps (Philox stream of policy_kernel), log-prob; actions staged ----
     float zz = 0.f;
 #pragma unroll
@@ -273,9 +288,15 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     tc::fence_before_sync();
     const float lp = s.lpc - 0.5f * zz;
     __syncthreads();
+    tr.mark();
     store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, A, nloc);
+    tr.mark();
     // ---- env step (stock_env_step stock_env.hpp:55-103), this thread's env, fp64 ----
-    const float* my = stage + tid * kSLD;
+    // `my` is re-read in each loop (volatile): the desired quantities are cheap to
+    // recompute, and keeping 30 of them live as doubles next to the 30 share
+    // counts would spill the shares to local memory.  Both loops are branch-free
+    // (a zero-quantity trade leaves balance and shares bit-identical).
+    const volatile float* my = stage + tid * kSLD;
     const int done = a.done_seq[h];
     double vb = bal;
 #pragma unroll
@@ -283,32 +304,28 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // sells first (:88-90)
       const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
-      if (d < 0.0) {
-        const double qv = -min_ref(-d, (double)sh[k]);
-        const double price = s.p0[k];
-        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
-        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-        sh[k] += (int32_t)qv;
-      }
+      const double qv = (d < 0.0) ? -min_ref(-d, (double)sh[k]) : 0.0;
+      const double price = s.p0[k];
+      const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
+      bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
+      sh[k] += (int32_t)qv;
     }
     const double cf = __dadd_rn(1.0, a.cost);
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
       const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
-      if (d > 0.0) {
-        const double price = s.p0[k];
-        const double affordable = floor(__ddiv_rn(bal, __dmul_rn(price, cf)));
-        const double qv = min_ref(d, max_ref(affordable, 0.0));
-        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
-        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-        sh[k] += (int32_t)qv;
-      }
+      const double price = s.p0[k];
+      const double qv = (d > 0.0) ? stock::buy_qty(d, bal, __dmul_rn(price, cf)) : 0.0;
+      const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
+      bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
+      sh[k] += (int32_t)qv;
     }
     double va = bal;
 #pragma unroll
     for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s.p1[k]));
     const double rw = __dsub_rn(va, vb);
     ret = __dadd_rn(ret, rw);
+    tr.mark();
     if (done) {  // auto-reset (env.hpp:221-229, stock_env.hpp:158-163)
       bal = a.cap;
       ret = 0.0;
@@ -322,6 +339,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
       a.b_rew[slab] = (float)rw;
       a.b_done[slab] = (uint8_t)done;
     }
+    tr.mark();
   }
   // ---- portfolio state back to HBM ----
   if (live) {

@@ -29,7 +29,9 @@ struct TcRolloutArgs {
   float* b_rew;
   uint8_t* b_done;
   float* b_boot;
+  unsigned long long* trace;  // optional clock64 phase trace of CTA 0 thread 0 (PRB_TC_TRACE), else null
 };
+constexpr int kTcTraceLen = 512;
 
 size_t stock_rollout_tc_smem();
 bool stock_rollout_tc_supported(int K);

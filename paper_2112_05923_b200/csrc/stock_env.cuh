@@ -1,0 +1,22 @@
+// stock_env.cuh -- shared device pieces of stock_env_step (stock_env.hpp:55-103).
+#pragma once
+
+namespace prb {
+namespace stock {
+
+// Buy quantity  min(desired, max(floor(balance / (price * (1 + cost))), 0))
+// (stock_env.hpp:91-97), bit-identical to the reference, with the fp64
+// division skipped when it cannot matter: if the EXACT product desired * pc
+// is <= balance (its sign is that of the single-rounding FMA residual), the
+// exact quotient is >= desired, so is its rounding (desired is a double), and
+// floor() of it; the result is then `desired` itself.  Only cash-limited buys
+// pay for __ddiv_rn, which is the long pole of the per-env dependency chain.
+__device__ __forceinline__ double buy_qty(double desired, double balance, double pc) {
+  if (__fma_rn(desired, pc, -balance) <= 0.0) return desired;
+  const double affordable = floor(__ddiv_rn(balance, pc));
+  const double floor0 = (affordable < 0.0) ? 0.0 : affordable;  // std::max(affordable, 0.0)
+  return (floor0 < desired) ? floor0 : desired;                  // std::min(desired, .)
+}
+
+}  // namespace stock
+}  // namespace prb

@@ -138,6 +138,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// clock64 event trace (debug builds of a launch pass a buffer; null in production)
+template <int LEN>
+struct Tracer {
+  unsigned long long* p = nullptr;
+  int n = 0;
+  __device__ __forceinline__ void mark() {
+    if (p && n < LEN) p[n++] = clock64();
+  }
+};
+
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
