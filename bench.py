@@ -49,6 +49,9 @@ S_DIM = 1 + 6 * K_ASSETS
 ENV_BYTES = 36 * K_ASSETS + 41  # action 4K + balance 16 + shares 8K + ep_return 16 + obs 4(1+6K) + reward 4 + done 1
 BUF_BYTES = 4 * (1 + K_ASSETS) + 4 * K_ASSETS + 4 * 3 + 1  # compact rollout row: obs 124 + act 120 + logp/val/rew 12 + done 1
 MLP_FLOPS = 2 * (181 * 64 + 64 * 64 + 64 * 30) + 2 * (181 * 64 + 64 * 64 + 64 * 1)  # 66,688
+# dram__bytes_read.sum + dram__bytes_write.sum of stock_rollout_tc_kernel<30> from one `ncu --set full`
+# capture (profiles/r1_tc_r3_full.txt: 65,536 envs x 32 steps), per transition; scaled to the launch below.
+TC_DRAM_BYTES_PER_TRANSITION = (9149952 + 538574592) / (65536 * 32)
 
 
 def load_peaks():
@@ -263,7 +266,9 @@ def run_ours(args, d: Dist):
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
     kd = kernels[dom]
     roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
-                "unit": kd["unit"], "frac": kd["frac"], "traffic": None,
+                "unit": kd["unit"], "frac": kd["frac"],
+                "traffic": (N * H * TC_DRAM_BYTES_PER_TRANSITION if dom == "stock_rollout_fused" else None),
+                "traffic_source": "ncu dram bytes/transition, profiles/r1_tc_r3_full.txt, x transitions per launch",
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json "
                                f"{'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
 

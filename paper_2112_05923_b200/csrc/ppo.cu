@@ -4,18 +4,22 @@
 //
 // One minibatch step = three stream-ordered kernels, all parameters and the
 // whole rollout staying in HBM/L2:
-//   1. ppo_fwd_bwd: each CTA gathers R rows of the minibatch (permutation
-//      computed on the fly: a keyed Feistel bijection of the buffer, or the
-//      injected reference permutation), rebuilds the observation (compact stock
-//      rows + shared feature row), stages the whole actor+critic weight set in
-//      shared memory (row stride out+1: conflict-free for the forward's
-//      column walk and the backward's row walk), runs the forward with cached
-//      activations, forms the clipped-surrogate / value / entropy head
-//      gradients (subgradient ties as ppo.hpp:146), backpropagates, and writes
-//      its partial dW/db/dlog_std and loss sums to a [CTA][P] slab.
-//   2. ppo_reduce: deterministic fixed-order sum of the partials, entropy term,
-//      finiteness gate (losses first, then gradients -- reference order), and
-//      the last CTA advances t / the minibatch counter.
+//   1. ppo_fwd_delta (row-parallel): each CTA gathers R rows of the minibatch
+//      (permutation computed on the fly: a keyed Feistel bijection of the
+//      buffer, or the injected reference permutation), rebuilds the
+//      observation (compact stock rows + shared feature row), stages the whole
+//      actor+critic weight set in shared memory (row stride out+1), runs the
+//      forward with cached activations, forms the clipped-surrogate / value /
+//      entropy head gradients (subgradient ties as ppo.hpp:146) and
+//      back-propagates the deltas; it writes every layer's input rows and
+//      delta rows (plus the per-row log_std terms and losses) to a [mb x ...]
+//      slab (a few MB, L2-resident).
+//   2. ppo_grad (output-parallel): dW_l = H_{l-1}^T . delta_l with the bias as
+//      an extra ones-column (the flat layout stores b_l right after W_l), in
+//      64x64 output tiles x row splits; 4x4 register blocking, fixed-order
+//      sums; the last split of a tile sums the split partials in order
+//      (deterministic), and the last tile evaluates the step's gate: losses
+//      first, then gradients (reference order), advancing t / the counter.
 //   3. adam (agent.cu), skipped by the gate so a non-finite step leaves the
 //      state untouched (nn.hpp:169-171).
 // The minibatch counter lives on device, so a run of steps is one CUDA graph.
@@ -62,9 +66,13 @@ struct PpoArgs {
   int stage;          // 1: weights staged in shared memory (ld = out + 1)
   const int64_t* step;  // device minibatch counter (epoch = step / nmb)
   double clip, ent, vf;
-  float* partial;  // [grid][Pext]
   int32_t* status;
   int ldw;  // max hidden width rounded to 4
+  // per-row slab written by ppo_fwd_delta: layer inputs and deltas, row-major [mb][width]
+  float* slab;
+  int hin_off[2][kMaxLayers];  // H_{l-1} rows ([mb][dims[l]]); l = 0 is the observation (shared)
+  int del_off[2][kMaxLayers];  // delta_l rows ([mb][dims[l+1]])
+  int ls_off, loss_off;        // [mb][A] log_std terms, [mb][2] policy / value loss terms
 };
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n).
@@ -206,23 +214,12 @@ __device__ __forceinline__ void stage_wait() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-// gW[k][j] = sum_r in[r][k] d[r][j]; gb[j] = sum_r d[r][j]   (matmul_tn + column_sums, tensor.hpp:85-183)
-__device__ __forceinline__ void grad_w_tile(const float* s_in, int ldi, int in, const float* s_d, int ldd, int out,
-                                            int nrows, float* __restrict__ gW) {
-  const int TJ = out > 32 ? 64 : 32;
-  const int KT = blockDim.x / TJ;
-  const int jt = threadIdx.x % TJ, kt = threadIdx.x / TJ;
-  for (int j = jt; j < out; j += TJ) {
-    for (int k = kt; k < in; k += KT) {
-      float acc = 0.0f;
-      for (int r = 0; r < nrows; ++r) acc = fmaf(s_in[r * ldi + k], s_d[r * ldd + j], acc);
-      gW[(size_t)k * out + j] = acc;
-    }
-    if (kt == 0) {
-      float acc = 0.0f;
-      for (int r = 0; r < nrows; ++r) acc += s_d[r * ldd + j];
-      gW[(size_t)in * out + j] = acc;
-    }
+// rows [q0, q0+nrows) of a [mb][w] slab array <- smem tile s (row stride lds)
+__device__ __forceinline__ void store_rows_g(float* __restrict__ g, int w, const float* s, int lds, int nrows, int q0) {
+  const int n = nrows * w;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = i / w, c = i - r * w;
+    g[(size_t)(q0 + r) * w + c] = s[r * lds + c];
   }
 }
 
@@ -245,7 +242,7 @@ __device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int o
   }
 }
 
-__global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
+__global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   if (a.status[0] != 0) return;
   extern __shared__ __align__(16) float smem[];
   Smem s;
@@ -293,6 +290,12 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
   // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
   mlp_forward_tile_p(a.actor, lpa, s.x, ldx, s.aa, s.lda, nrows);
   mlp_forward_tile_p(a.critic, lpc, s.x, ldx, s.ca, s.ldc, nrows);
+  // layer inputs for the gradient GEMMs: the observation and every hidden activation
+  store_rows_g(a.slab + a.hin_off[0][0], a.S, s.x, ldx, nrows, q0);
+  for (int l = 1; l < a.actor.nl; ++l)
+    store_rows_g(a.slab + a.hin_off[0][l], a.actor.dims[l], s.aa[l - 1], s.lda[l - 1], nrows, q0);
+  for (int l = 1; l < a.critic.nl; ++l)
+    store_rows_g(a.slab + a.hin_off[1][l], a.critic.dims[l], s.ca[l - 1], s.ldc[l - 1], nrows, q0);
   // ---- per-row losses and head gradients (ppo.hpp:128-167) ----
   const float inv_n = 1.0f / (float)a.mb;
   const float* log_std = a.params + a.log_std_off;
@@ -339,9 +342,13 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
     }
   }
   __syncthreads();
-  float* part = a.partial + (size_t)blockIdx.x * a.Pext;
+  // head deltas, log_std terms and per-row losses
+  store_rows_g(a.slab + a.del_off[0][a.actor.nl - 1], A, meanb, ldm, nrows, q0);
+  store_rows_g(a.slab + a.del_off[1][a.critic.nl - 1], 1, s.ca[a.critic.nl - 1], s.ldc[a.critic.nl - 1], nrows, q0);
+  store_rows_g(a.slab + a.ls_off, A, s.tmp, ldA, nrows, q0);
+  store_rows_g(a.slab + a.loss_off, 2, s.loss, 2, nrows, q0);
   const int ldp = a.ldw > ldA ? a.ldw : ldA;
-  // ---- backward (mlp_backward_accumulate nn.hpp:105-132) ----
+  // ---- backward deltas (mlp_backward_accumulate nn.hpp:105-132, the matmul_nt half) ----
   for (int net = 0; net < 2; ++net) {
     const MlpDesc& d = net ? a.critic : a.actor;
     const LayerPtrs& lp = net ? lpc : lpa;
@@ -349,123 +356,205 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_bwd_kernel(PpoArgs a) {
     const int* lds = net ? s.ldc : s.lda;
     const float* delta = acts[d.nl - 1];
     int ldd = lds[d.nl - 1];
-    for (int l = d.nl - 1; l >= 0; --l) {
+    for (int l = d.nl - 1; l >= 1; --l) {
       const int in = d.dims[l], out = d.dims[l + 1];
-      const float* lin = (l == 0) ? s.x : acts[l - 1];
-      const int ldi = (l == 0) ? ldx : lds[l - 1];
-      grad_w_tile(lin, ldi, in, delta, ldd, out, nrows, part + d.off[l]);
-      if (l > 0) {
-        float* dp = (delta == s.d0) ? s.d1 : s.d0;
-        delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, lin, ldi, dp, ldp, nrows);
-        __syncthreads();
-        delta = dp;
-        ldd = ldp;
-      }
+      float* dp = (delta == s.d0) ? s.d1 : s.d0;
+      delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, acts[l - 1], lds[l - 1], dp, ldp, nrows);
+      __syncthreads();
+      store_rows_g(a.slab + a.del_off[net][l - 1], in, dp, ldp, nrows, q0);
+      delta = dp;
+      ldd = ldp;
     }
     __syncthreads();
   }
-  // log_std partial (entropy term added once in the reduce) and loss sums
-  for (int dd = threadIdx.x; dd < A; dd += blockDim.x) {
-    float acc = 0.0f;
-    for (int r = 0; r < nrows; ++r) acc += s.tmp[r * ldA + dd];
-    part[a.log_std_off + dd] = acc;
-  }
-  if (threadIdx.x < 2) {
-    float acc = 0.0f;
-    for (int r = 0; r < nrows; ++r) acc += s.loss[r * 2 + threadIdx.x];
-    part[a.P + threadIdx.x] = acc;
-  }
 }
 
-struct ReduceArgs {
-  const float* partial;
-  int nparts, P, Pext, log_std_off, A;
+// ---- ppo_grad: output-parallel dW / db / dlog_std, fixed-order sums, step gate ----
+constexpr int kGT = 64;        // output tile (k rows x j cols of [W; b])
+constexpr int kGChunk = 128;   // rows per split
+constexpr int kGLd = kGT + 4;  // smem row stride (float4-aligned)
+constexpr int kMaxSplits = 8;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
+
+struct GradArgs {
+  const float* slab;
+  int hin_off[2][kMaxLayers], del_off[2][kMaxLayers], ls_off, loss_off;
+  MlpDesc net[2];
+  int mb, RS, P, Pext, log_std_off, A;
+  const int4* tiles;  // {net, layer (-1: log_std + losses), k0, j0}
+  int ntiles;
+  float* partial;     // [RS][Pext]
+  float* grads;
+  int32_t* tickets;   // [ntiles] + [ntiles] = completed-tile counter, [ntiles+1] = gradient non-finite flag
   double ent;
   const float* params;
-  float* grads;
-  int32_t* status;    // [0] code, [1] detail
-  int32_t* scratch;   // [0] ticket, [1] grad-nonfinite flag
-  int64_t* t;         // Adam t (advanced when the step is accepted)
-  int64_t* step;      // minibatch counter
-  double* stats;      // sums: policy, value, entropy, count
-  int apply;          // 0 = grads only (prb_ppo_loss_grads)
+  int32_t* status;
+  int64_t* t;
+  int64_t* step;
+  double* stats;
+  int apply;
 };
 
-// Block = 32 parameters x 8 slices of the CTA partials; slice s sums partials
-// s, s+8, ... with 4 independent accumulators, then the 8 slices are combined
-// in a fixed order through shared memory: deterministic, and ~1,000 blocks of
-// independent loads instead of one 128-long dependent chain per parameter.
-constexpr int kRedCols = 32, kRedSlices = 8;
-
-__global__ void __launch_bounds__(kRedCols * kRedSlices) ppo_reduce_kernel(ReduceArgs r) {
-  if (r.status[0] != 0) return;
-  __shared__ float part_sum[kRedSlices][kRedCols];
-  const int col = threadIdx.x % kRedCols, slice = threadIdx.x / kRedCols;
-  const int p = blockIdx.x * kRedCols + col;
-  if (p < r.P) {
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int b = slice;
-    for (; b + 3 * kRedSlices < r.nparts; b += 4 * kRedSlices) {
-      s0 += r.partial[(size_t)(b + 0 * kRedSlices) * r.Pext + p];
-      s1 += r.partial[(size_t)(b + 1 * kRedSlices) * r.Pext + p];
-      s2 += r.partial[(size_t)(b + 2 * kRedSlices) * r.Pext + p];
-      s3 += r.partial[(size_t)(b + 3 * kRedSlices) * r.Pext + p];
-    }
-    for (; b < r.nparts; b += kRedSlices) s0 += r.partial[(size_t)b * r.Pext + p];
-    part_sum[slice][col] = (s0 + s1) + (s2 + s3);
-  }
-  __syncthreads();
-  int bad = 0;
-  if (slice == 0 && p < r.P) {
-    float acc = part_sum[0][col];
+__global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
+  if (g.status[0] != 0) return;
+  extern __shared__ __align__(16) float gsm[];
+  float* As = gsm;
+  float* Bs = gsm + kGChunk * kGLd;
+  const int tile = blockIdx.x / g.RS, split = blockIdx.x % g.RS;
+  const int4 td = g.tiles[tile];
+  const int per = (g.mb + g.RS - 1) / g.RS;  // rows of this split, processed in kGChunk sub-chunks
+  const int rbeg = split * per, rend = min(g.mb, rbeg + per);
+  const int tid = threadIdx.x;
+  float* part = g.partial + (size_t)split * g.Pext;
+  if (td.y >= 0) {
+    const MlpDesc& d = g.net[td.x];
+    const int l = td.y, in = d.dims[l], out = d.dims[l + 1], k0 = td.z, j0 = td.w;
+    const float* H = g.slab + g.hin_off[td.x][l];
+    const float* D = g.slab + g.del_off[td.x][l];
+    const int tk = tid >> 4, tj = tid & 15;
+    float acc[4][4];
 #pragma unroll
-    for (int sl = 1; sl < kRedSlices; ++sl) acc += part_sum[sl][col];
-    if (p >= r.log_std_off && p < r.log_std_off + r.A) acc -= (float)r.ent;  // ppo.hpp:157
-    r.grads[p] = acc;
-    bad = !isfinite(acc);
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int r0 = rbeg; r0 < rend; r0 += kGChunk) {
+      const int nr = min(kGChunk, rend - r0);
+      __syncthreads();  // previous sub-chunk consumed
+      for (int i = tid; i < nr * kGT; i += 256) {
+        const int r = i / kGT, c = i % kGT, k = k0 + c, j = j0 + c;
+        const size_t row = (size_t)(r0 + r);
+        As[r * kGLd + c] = (k < in) ? H[row * in + k] : (k == in ? 1.0f : 0.0f);  // bias row = ones column
+        Bs[r * kGLd + c] = (j < out) ? D[row * out + j] : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int r = 0; r < nr; ++r) {
+        const float4 av = *reinterpret_cast<const float4*>(As + r * kGLd + 4 * tk);
+        const float4 bv = *reinterpret_cast<const float4*>(Bs + r * kGLd + 4 * tj);
+        const float ak[4] = {av.x, av.y, av.z, av.w}, bj[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ak[i], bj[j], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = k0 + 4 * tk + i;
+      if (k > in) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int jj = j0 + 4 * tj + j;
+        if (jj < out) part[d.off[l] + k * out + jj] = acc[i][j];
+      }
+    }
+  } else {  // log_std terms and the two loss sums over this split's rows
+    const float* LS = g.slab + g.ls_off;
+    const float* LO = g.slab + g.loss_off;
+    for (int c = tid; c < g.A + 2; c += 256) {
+      float acc = 0.0f;
+      if (c < g.A)
+        for (int r = rbeg; r < rend; ++r) acc += LS[(size_t)r * g.A + c];
+      else
+        for (int r = rbeg; r < rend; ++r) acc += LO[(size_t)r * 2 + (c - g.A)];
+      part[c < g.A ? g.log_std_off + c : g.P + (c - g.A)] = acc;
+    }
   }
-  if (bad) atomicOr(&r.scratch[1], 1);
+  // ---- the last split of this tile sums the split partials in split order ----
   __threadfence();
-  __shared__ int last;
-  if (threadIdx.x == 0) last = (atomicAdd(&r.scratch[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&g.tickets[tile], 1) == g.RS - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  int bad = 0;
+  if (td.y >= 0) {
+    const MlpDesc& d = g.net[td.x];
+    const int l = td.y, in = d.dims[l], out = d.dims[l + 1], k0 = td.z, j0 = td.w;
+    // 16 outputs per thread in two batches of 8, all split loads of a batch in flight (RS <= 8)
+#pragma unroll 1
+    for (int b0 = 0; b0 < kGT * kGT; b0 += 8 * 256) {
+      float v[8][kMaxSplits];
+      size_t idx[8];
+      bool ok[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int i = b0 + o * 256 + tid, k = k0 + i / kGT, j = j0 + i % kGT;
+        ok[o] = k <= in && j < out;
+        idx[o] = ok[o] ? (size_t)d.off[l] + (size_t)k * out + j : 0;
+#pragma unroll
+        for (int sp = 0; sp < kMaxSplits; ++sp)
+          v[o][sp] = (ok[o] && sp < g.RS) ? g.partial[(size_t)sp * g.Pext + idx[o]] : 0.0f;
+      }
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        if (!ok[o]) continue;
+        float sum = 0.0f;
+#pragma unroll
+        for (int sp = 0; sp < kMaxSplits; ++sp)
+          if (sp < g.RS) sum += v[o][sp];
+        g.grads[idx[o]] = sum;
+        bad |= !isfinite(sum);
+      }
+    }
+  } else {
+    for (int c = tid; c < g.A; c += 256) {
+      const size_t idx = (size_t)g.log_std_off + c;
+      float sum = 0.0f;
+      for (int sp = 0; sp < g.RS; ++sp) sum += g.partial[(size_t)sp * g.Pext + idx];
+      sum -= (float)g.ent;  // ppo.hpp:157
+      g.grads[idx] = sum;
+      bad |= !isfinite(sum);
+    }
+  }
+  if (bad) atomicOr(&g.tickets[g.ntiles + 1], 1);
+  if (tid == 0) g.tickets[tile] = 0;
+  // ---- the last tile evaluates the step (reference order: losses, then gradients) ----
+  __threadfence();
+  __syncthreads();
+  __shared__ int lastall;
+  if (tid == 0) lastall = (atomicAdd(&g.tickets[g.ntiles], 1) == g.ntiles - 1);
+  __syncthreads();
+  if (!lastall || tid != 0) return;
   __threadfence();
   double pl = 0.0, vl = 0.0;
-  for (int b = 0; b < r.nparts; ++b) {
-    pl += r.partial[(size_t)b * r.Pext + r.P];
-    vl += r.partial[(size_t)b * r.Pext + r.P + 1];
+  for (int sp = 0; sp < g.RS; ++sp) {
+    pl += g.partial[(size_t)sp * g.Pext + g.P];
+    vl += g.partial[(size_t)sp * g.Pext + g.P + 1];
   }
   double ent = 0.0;  // policy_entropy nn.hpp:273-277
-  for (int d = 0; d < r.A; ++d) ent += 0.5 * (1.8378770664093454836 + 1.0) + (double)r.params[r.log_std_off + d];
-  const int gbad = atomicAdd(&r.scratch[1], 0);
-  r.scratch[0] = 0;
-  r.scratch[1] = 0;
+  for (int dd = 0; dd < g.A; ++dd) ent += 0.5 * (1.8378770664093454836 + 1.0) + (double)g.params[g.log_std_off + dd];
+  const int gbad = atomicAdd(&g.tickets[g.ntiles + 1], 0);
+  g.tickets[g.ntiles] = 0;
+  g.tickets[g.ntiles + 1] = 0;
   if (!isfinite(pl)) {
-    r.status[0] = PRB_ERR_NUMERIC;
-    r.status[1] = 10;
+    g.status[0] = PRB_ERR_NUMERIC;
+    g.status[1] = 10;
   } else if (!isfinite(vl)) {
-    r.status[0] = PRB_ERR_NUMERIC;
-    r.status[1] = 11;
+    g.status[0] = PRB_ERR_NUMERIC;
+    g.status[1] = 11;
   } else if (!isfinite(ent)) {
-    r.status[0] = PRB_ERR_NUMERIC;
-    r.status[1] = 12;
-  } else if (gbad && r.apply) {
-    r.status[0] = PRB_ERR_NUMERIC;
-    r.status[1] = 1;
+    g.status[0] = PRB_ERR_NUMERIC;
+    g.status[1] = 12;
+  } else if (gbad && g.apply) {
+    g.status[0] = PRB_ERR_NUMERIC;
+    g.status[1] = 1;
   } else {
-    r.stats[0] += pl;
-    r.stats[1] += vl;
-    r.stats[2] += ent;
-    r.stats[3] += 1.0;
-    if (r.apply) *r.t += 1;
+    g.stats[0] += pl;
+    g.stats[1] += vl;
+    g.stats[2] += ent;
+    g.stats[3] += 1.0;
+    if (g.apply) *g.t += 1;
   }
-  *r.step += 1;
+  *g.step += 1;
 }
 
 struct PpoWorkspace {
-  DevBuf<float> partial;
-  DevBuf<int32_t> scratch;
+  DevBuf<float> partial;   // [RS][Pext] split partials of the gradient GEMMs
+  DevBuf<float> slab;      // per-row layer inputs / deltas of one minibatch
+  DevBuf<int4> tiles;      // ppo_grad tile list
+  DevBuf<int32_t> tickets; // [ntiles] split tickets, completed-tile counter, gradient flag
+  int ntiles = 0, RS = 1;
   DevBuf<int64_t> step;
   DevBuf<double> stats;
   DevBuf<uint32_t> perm;
@@ -519,12 +608,42 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   if (carve(p, nullptr, nullptr) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
   while (p.R > 8 && carve(p, nullptr, nullptr) > kSmemBudget) p.R /= 2;
   PRB_REQUIRE(carve(p, nullptr, nullptr) <= kSmemBudget, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
-  const int grid = (mb + p.R - 1) / p.R;
-  if (ws.partial.n < (size_t)grid * p.Pext) ws.partial.alloc((size_t)grid * p.Pext);
-  if (!ws.scratch.p) ws.scratch.alloc(4);
+  // per-row slab: observation, hidden activations (layer inputs) and deltas of both nets
+  size_t off = 0;
+  auto take = [&](size_t w) {
+    const size_t o = off;
+    off += ((size_t)mb * w + 3) & ~size_t(3);
+    PRB_REQUIRE(off < ((size_t)1 << 31), PRB_ERR_CONFIG, "ppo: minibatch slab too large");
+    return (int)o;
+  };
+  p.hin_off[0][0] = p.hin_off[1][0] = take((size_t)p.S);
+  for (int net = 0; net < 2; ++net) {
+    const MlpDesc& d = net ? p.critic : p.actor;
+    for (int l = 1; l < d.nl; ++l) p.hin_off[net][l] = take((size_t)d.dims[l]);
+    for (int l = 0; l < d.nl; ++l) p.del_off[net][l] = take((size_t)d.dims[l + 1]);
+  }
+  p.ls_off = take((size_t)p.A);
+  p.loss_off = take(2);
+  if (ws.slab.n < off) ws.slab.alloc(off);
+  p.slab = ws.slab.p;
+  // gradient tiles: every [W_l; b_l] of both nets in 64x64 output tiles, plus log_std + losses
+  std::vector<int4> tiles;
+  for (int net = 0; net < 2; ++net) {
+    const MlpDesc& d = net ? p.critic : p.actor;
+    for (int l = 0; l < d.nl; ++l)
+      for (int k0 = 0; k0 <= d.dims[l]; k0 += kGT)
+        for (int j0 = 0; j0 < d.dims[l + 1]; j0 += kGT) tiles.push_back(make_int4(net, l, k0, j0));
+  }
+  tiles.push_back(make_int4(0, -1, 0, 0));
+  ws.ntiles = (int)tiles.size();
+  ws.RS = std::min(kMaxSplits, (mb + kGChunk - 1) / kGChunk);
+  ws.tiles.alloc(tiles.size());
+  PRB_CUDA(cudaMemcpy(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  ws.tickets.alloc((size_t)ws.ntiles + 2);
+  PRB_CUDA(cudaMemset(ws.tickets.p, 0, ws.tickets.bytes()));
+  if (ws.partial.n < (size_t)ws.RS * p.Pext) ws.partial.alloc((size_t)ws.RS * p.Pext);
   if (!ws.step.p) ws.step.alloc(1);
   if (!ws.stats.p) ws.stats.alloc(4);
-  p.partial = ws.partial.p;
   p.step = ws.step.p;
   return p;
 }
@@ -532,25 +651,34 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
 void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
   const int grid = (p.mb + p.R - 1) / p.R;
   const size_t smem = carve(p, nullptr, nullptr);
-  ppo_fwd_bwd_kernel<<<grid, kPpoThreads, smem, s>>>(p);  // steps run inside CUDA graphs: no event scopes
-  ReduceArgs r;
-  r.partial = ws.partial.p;
-  r.nparts = grid;
-  r.P = p.P;
-  r.Pext = p.Pext;
-  r.log_std_off = p.log_std_off;
-  r.A = p.A;
-  r.ent = ent;
-  r.params = p.params;
-  r.grads = a->d_grads.p;
-  r.status = a->d_status.p;
-  r.scratch = ws.scratch.p;
-  r.t = a->d_t.p;
-  r.step = ws.step.p;
-  r.stats = ws.stats.p;
-  r.apply = apply;
-  const int rgrid = (p.P + kRedCols - 1) / kRedCols;
-  ppo_reduce_kernel<<<rgrid, kRedCols * kRedSlices, 0, s>>>(r);
+  ppo_fwd_delta_kernel<<<grid, kPpoThreads, smem, s>>>(p);  // steps run inside CUDA graphs: no event scopes
+  GradArgs g;
+  g.slab = p.slab;
+  std::memcpy(g.hin_off, p.hin_off, sizeof(g.hin_off));
+  std::memcpy(g.del_off, p.del_off, sizeof(g.del_off));
+  g.ls_off = p.ls_off;
+  g.loss_off = p.loss_off;
+  g.net[0] = p.actor;
+  g.net[1] = p.critic;
+  g.mb = p.mb;
+  g.RS = ws.RS;
+  g.P = p.P;
+  g.Pext = p.Pext;
+  g.log_std_off = p.log_std_off;
+  g.A = p.A;
+  g.tiles = ws.tiles.p;
+  g.ntiles = ws.ntiles;
+  g.partial = ws.partial.p;
+  g.grads = a->d_grads.p;
+  g.tickets = ws.tickets.p;
+  g.ent = ent;
+  g.params = p.params;
+  g.status = a->d_status.p;
+  g.t = a->d_t.p;
+  g.step = ws.step.p;
+  g.stats = ws.stats.p;
+  g.apply = apply;
+  ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
   if (apply) prb_adam_launch(a, a->d_grads.p, a->d_status.p, s);
 }
 
@@ -577,7 +705,9 @@ void check_status(prb_agent a) {
 void set_smem_attr() {
   static bool done = false;
   if (!done) {
-    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(2 * kGChunk * kGLd * sizeof(float))));
     done = true;
   }
 }
@@ -642,7 +772,6 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
       p.perm = ws.perm.p;
       dst->ctx->sync();
     }
-    PRB_CUDA(cudaMemsetAsync(ws.scratch.p, 0, 4 * sizeof(int32_t), s));
     PRB_CUDA(cudaMemsetAsync(ws.step.p, 0, sizeof(int64_t), s));
     PRB_CUDA(cudaMemsetAsync(ws.stats.p, 0, 4 * sizeof(double), s));
     // Minibatch steps are identical launches (the counter is on device):
@@ -694,7 +823,6 @@ int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows, size_t 
     p.perm = ws.perm.p;
     p.n = (uint32_t)n;  // one "epoch" whose permutation is exactly `rows`
     p.nmb = 1;
-    PRB_CUDA(cudaMemsetAsync(ws.scratch.p, 0, 4 * sizeof(int32_t), s));
     PRB_CUDA(cudaMemsetAsync(ws.step.p, 0, sizeof(int64_t), s));
     PRB_CUDA(cudaMemsetAsync(ws.stats.p, 0, 4 * sizeof(double), s));
     PRB_CUDA(cudaMemsetAsync(a->d_status.p, 0, 4 * sizeof(int32_t), s));
