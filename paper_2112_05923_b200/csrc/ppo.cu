@@ -2,7 +2,7 @@
 // detail::ppo_loss_grads ppo.hpp:116-188, mlp_backward_accumulate
 // nn.hpp:105-132, adam_step nn.hpp:164-182).
 //
-// One minibatch step = three stream-ordered kernels, all parameters and the
+// One minibatch step = four stream-ordered kernels, all parameters and the
 // whole rollout staying in HBM/L2:
 //   1. ppo_fwd_delta (row-parallel): each CTA gathers R rows of the minibatch
 //      (permutation computed on the fly: a keyed Feistel bijection of the
@@ -14,17 +14,20 @@
 //      back-propagates the deltas; it writes every layer's input rows and
 //      delta rows (plus the per-row log_std terms and losses) to a [mb x ...]
 //      slab (a few MB, L2-resident).
-//   2. ppo_grad (output-parallel): dW_l = H_{l-1}^T . delta_l with the bias as
-//      an extra ones-column (the flat layout stores b_l right after W_l), in
-//      64x64 output tiles x row splits; 4x4 register blocking, fixed-order
-//      sums; the last split of a tile sums the split partials in order
-//      (deterministic), and the last tile evaluates the step's gate: losses
+//   2. ppo_grad (output-parallel): dW_l = H_{l-1}^T . delta_l (and db_l =
+//      colsum(delta_l) in the k0 = 0 tiles; the flat layout stores b_l right
+//      after W_l) in 64x64 output tiles x row splits; 4x4 register blocking,
+//      fixed-order sums into a [splits x P] partial slab.
+//   3. ppo_sum: one thread per parameter sums the split partials in split
+//      order (deterministic); the last CTA evaluates the step's gate: losses
 //      first, then gradients (reference order), advancing t / the counter.
-//   3. adam (agent.cu), skipped by the gate so a non-finite step leaves the
+//   4. adam (agent.cu), skipped by the gate so a non-finite step leaves the
 //      state untouched (nn.hpp:169-171).
 // The minibatch counter lives on device, so a run of steps is one CUDA graph.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "mlp_simt.cuh"
@@ -39,6 +42,7 @@ namespace {
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
 constexpr int kPpoThreads = 256;
 constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int kGatherUnroll = 8;  // observation columns per lane loaded before any store (S <= 256 in one pass)
 
 struct PpoArgs {
   const float* params;
@@ -266,23 +270,44 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   }
   // the gather below overlaps with the weight copies in flight; waited before the forward
   const LayerPtrs lpa = layer_ptrs(a, a.actor, wa), lpc = layer_ptrs(a, a.critic, wc);
-  // ---- gather (gather_minibatch ppo.hpp:83-103) ----
+  // ---- gather (gather_minibatch ppo.hpp:83-103): a warp per row, every load of a row in flight ----
   for (int r = threadIdx.x / 32; r < nrows; r += blockDim.x / 32) {
     const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
     const int lane = threadIdx.x & 31;
-    if (a.obs_mode == 1) {
-      const uint32_t h = i / a.N;
-      const float* fr = a.feat + (size_t)a.row[h] * (a.S - a.Sp);
-      for (int c = lane; c < a.S; c += 32)
-        s.x[r * ldx + c] = (c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp];
-    } else {
-      for (int c = lane; c < a.S; c += 32) s.x[r * ldx + c] = a.obs[(size_t)i * a.S + c];
+    const float* fr = nullptr;
+    if (a.obs_mode == 1) fr = a.feat + (size_t)a.row[i / a.N] * (a.S - a.Sp);
+    float xv[kGatherUnroll];
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const int c = lane + 32 * u;
+      float v = 0.0f;
+      if (c < a.S) {
+        if (a.obs_mode == 1)
+          v = (c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp];
+        else
+          v = a.obs[(size_t)i * a.S + c];
+      }
+      xv[u] = v;
     }
-    for (int c = lane; c < A; c += 32) s.actn[r * ldA + c] = a.act[(size_t)i * A + c];
+    for (int c = lane + 32 * kGatherUnroll; c < a.S; c += 32)  // wide observations
+      s.x[r * ldx + c] = (a.obs_mode == 1) ? ((c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp])
+                                           : a.obs[(size_t)i * a.S + c];
+    const float act = (lane < A) ? a.act[(size_t)i * A + lane] : 0.0f;
+    float lp0 = 0.f, advv = 0.f, retv = 0.f;
     if (lane == 0) {
-      s.misc[r * 4 + 0] = a.logp[i];
-      s.misc[r * 4 + 1] = (float)(((double)a.adv[i] - mean) / denom);
-      s.misc[r * 4 + 2] = a.ret[i];
+      lp0 = a.logp[i];
+      advv = a.adv[i];
+      retv = a.ret[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u)
+      if (lane + 32 * u < a.S) s.x[r * ldx + lane + 32 * u] = xv[u];
+    if (lane < A) s.actn[r * ldA + lane] = act;
+    for (int c = lane + 32; c < A; c += 32) s.actn[r * ldA + c] = a.act[(size_t)i * A + c];
+    if (lane == 0) {
+      s.misc[r * 4 + 0] = lp0;
+      s.misc[r * 4 + 1] = (float)(((double)advv - mean) / denom);
+      s.misc[r * 4 + 2] = retv;
     }
   }
   if (a.stage) stage_wait();
@@ -373,7 +398,8 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
 constexpr int kGT = 64;        // output tile (k rows x j cols of [W; b])
 constexpr int kGChunk = 128;   // rows per split
 constexpr int kGLd = kGT + 4;  // smem row stride (float4-aligned)
-constexpr int kMaxSplits = 8;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
+constexpr int kMaxSplits = 16;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
+constexpr int kGRows = 64;      // target rows per split
 
 struct GradArgs {
   const float* slab;
@@ -384,7 +410,7 @@ struct GradArgs {
   int ntiles;
   float* partial;     // [RS][Pext]
   float* grads;
-  int32_t* tickets;   // [ntiles] + [ntiles] = completed-tile counter, [ntiles+1] = gradient non-finite flag
+  int32_t* tickets;   // [0] ppo_sum completed-CTA counter, [1] gradient non-finite flag
   double ent;
   const float* params;
   int32_t* status;
@@ -392,9 +418,18 @@ struct GradArgs {
   int64_t* step;
   double* stats;
   int apply;
+  unsigned long long* trace;  // debug (PRB_PPO_TRACE): [grid][8] globaltimer marks, else null
 };
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
+  unsigned long long* tr = (g.trace && threadIdx.x == 0) ? g.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (tr) tr[0] = gtime();
   if (g.status[0] != 0) return;
   extern __shared__ __align__(16) float gsm[];
   float* As = gsm;
@@ -410,8 +445,11 @@ __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
     const int l = td.y, in = d.dims[l], out = d.dims[l + 1], k0 = td.z, j0 = td.w;
     const float* H = g.slab + g.hin_off[td.x][l];
     const float* D = g.slab + g.del_off[td.x][l];
-    const int tk = tid >> 4, tj = tid & 15;
-    float acc[4][4];
+    // thread = 4 k x 4 j outputs; warp w owns columns j0 + 8w .. 8w+7, so warps past `out` skip the math
+    const int tk = tid & 15, tj = tid >> 4;
+    const bool active = j0 + 8 * (tid >> 5) < out;
+    const bool with_bias = (k0 == 0);  // the k0 = 0 tile also sums delta's columns (the bias row)
+    float acc[4][4], bsum[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -419,114 +457,130 @@ __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
     for (int r0 = rbeg; r0 < rend; r0 += kGChunk) {
       const int nr = min(kGChunk, rend - r0);
       __syncthreads();  // previous sub-chunk consumed
-      for (int i = tid; i < nr * kGT; i += 256) {
-        const int r = i / kGT, c = i % kGT, k = k0 + c, j = j0 + c;
-        const size_t row = (size_t)(r0 + r);
-        As[r * kGLd + c] = (k < in) ? H[row * in + k] : (k == in ? 1.0f : 0.0f);  // bias row = ones column
-        Bs[r * kGLd + c] = (j < out) ? D[row * out + j] : 0.0f;
+      // 8 rows per thread per pass, all 16 loads in flight before the stores
+      const int c = tid % kGT, k = k0 + c, j = j0 + c;
+      for (int rb = tid / kGT; rb < nr; rb += 8 * (256 / kGT)) {
+        float av[8], bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = rb + u * (256 / kGT);
+          const size_t row = (size_t)(r0 + r);
+          av[u] = (r < nr && k < in) ? H[row * in + k] : 0.0f;
+          bv[u] = (r < nr && j < out) ? D[row * out + j] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = rb + u * (256 / kGT);
+          if (r < nr) {
+            As[r * kGLd + c] = av[u];
+            Bs[r * kGLd + c] = bv[u];
+          }
+        }
       }
       __syncthreads();
+      if (active) {
 #pragma unroll 4
-      for (int r = 0; r < nr; ++r) {
-        const float4 av = *reinterpret_cast<const float4*>(As + r * kGLd + 4 * tk);
-        const float4 bv = *reinterpret_cast<const float4*>(Bs + r * kGLd + 4 * tj);
-        const float ak[4] = {av.x, av.y, av.z, av.w}, bj[4] = {bv.x, bv.y, bv.z, bv.w};
+        for (int r = 0; r < nr; ++r) {
+          const float4 av = *reinterpret_cast<const float4*>(As + r * kGLd + 4 * tk);
+          const float4 bv = *reinterpret_cast<const float4*>(Bs + r * kGLd + 4 * tj);
+          const float ak[4] = {av.x, av.y, av.z, av.w}, bj[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ak[i], bj[j], acc[i][j]);
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ak[i], bj[j], acc[i][j]);
+          if (with_bias) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bsum[j] += bj[j];
+          }
+        }
       }
     }
+    if (active) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int k = k0 + 4 * tk + i;
-      if (k > in) continue;
+      for (int i = 0; i < 4; ++i) {
+        const int k = k0 + 4 * tk + i;
+        if (k >= in) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int jj = j0 + 4 * tj + j;
-        if (jj < out) part[d.off[l] + k * out + jj] = acc[i][j];
+        for (int j = 0; j < 4; ++j) {
+          const int jj = j0 + 4 * tj + j;
+          if (jj < out) part[d.off[l] + k * out + jj] = acc[i][j];
+        }
       }
+      if (with_bias && tk == 0)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int jj = j0 + 4 * tj + j;
+          if (jj < out) part[d.off[l] + in * out + jj] = bsum[j];
+        }
     }
   } else {  // log_std terms and the two loss sums over this split's rows
     const float* LS = g.slab + g.ls_off;
     const float* LO = g.slab + g.loss_off;
     for (int c = tid; c < g.A + 2; c += 256) {
+      const float* src = (c < g.A) ? LS + c : LO + (c - g.A);
+      const int ld = (c < g.A) ? g.A : 2;
       float acc = 0.0f;
-      if (c < g.A)
-        for (int r = rbeg; r < rend; ++r) acc += LS[(size_t)r * g.A + c];
-      else
-        for (int r = rbeg; r < rend; ++r) acc += LO[(size_t)r * 2 + (c - g.A)];
+      for (int r = rbeg; r < rend; r += 16) {  // 16 loads in flight, summed in row order
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (r + u < rend) ? src[(size_t)(r + u) * ld] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (r + u < rend) acc += v[u];
+      }
       part[c < g.A ? g.log_std_off + c : g.P + (c - g.A)] = acc;
     }
   }
-  // ---- the last split of this tile sums the split partials in split order ----
-  __threadfence();
-  __syncthreads();
-  __shared__ int last;
-  if (tid == 0) last = (atomicAdd(&g.tickets[tile], 1) == g.RS - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+  if (tr) tr[1] = gtime();
+}
+
+// ---- ppo_sum: grads[p] = sum of the split partials in split order (+ entropy term for
+// log_std), non-finite flag; the last CTA evaluates the step's gate (losses first, then
+// gradients: the reference order) and advances t / the minibatch counter ----
+__global__ void __launch_bounds__(256) ppo_sum_kernel(GradArgs g) {
+  if (g.status[0] != 0) return;
+  const int tid = threadIdx.x;
+  const int p = blockIdx.x * 256 + tid;
   int bad = 0;
-  if (td.y >= 0) {
-    const MlpDesc& d = g.net[td.x];
-    const int l = td.y, in = d.dims[l], out = d.dims[l + 1], k0 = td.z, j0 = td.w;
-    // 16 outputs per thread in two batches of 8, all split loads of a batch in flight (RS <= 8)
-#pragma unroll 1
-    for (int b0 = 0; b0 < kGT * kGT; b0 += 8 * 256) {
-      float v[8][kMaxSplits];
-      size_t idx[8];
-      bool ok[8];
+  if (p < g.P) {
+    float v[kMaxSplits];
 #pragma unroll
-      for (int o = 0; o < 8; ++o) {
-        const int i = b0 + o * 256 + tid, k = k0 + i / kGT, j = j0 + i % kGT;
-        ok[o] = k <= in && j < out;
-        idx[o] = ok[o] ? (size_t)d.off[l] + (size_t)k * out + j : 0;
+    for (int sp = 0; sp < kMaxSplits; ++sp) v[sp] = (sp < g.RS) ? g.partial[(size_t)sp * g.Pext + p] : 0.0f;
+    float sum = 0.0f;
 #pragma unroll
-        for (int sp = 0; sp < kMaxSplits; ++sp)
-          v[o][sp] = (ok[o] && sp < g.RS) ? g.partial[(size_t)sp * g.Pext + idx[o]] : 0.0f;
-      }
-#pragma unroll
-      for (int o = 0; o < 8; ++o) {
-        if (!ok[o]) continue;
-        float sum = 0.0f;
-#pragma unroll
-        for (int sp = 0; sp < kMaxSplits; ++sp)
-          if (sp < g.RS) sum += v[o][sp];
-        g.grads[idx[o]] = sum;
-        bad |= !isfinite(sum);
-      }
-    }
-  } else {
-    for (int c = tid; c < g.A; c += 256) {
-      const size_t idx = (size_t)g.log_std_off + c;
-      float sum = 0.0f;
-      for (int sp = 0; sp < g.RS; ++sp) sum += g.partial[(size_t)sp * g.Pext + idx];
-      sum -= (float)g.ent;  // ppo.hpp:157
-      g.grads[idx] = sum;
-      bad |= !isfinite(sum);
-    }
+    for (int sp = 0; sp < kMaxSplits; ++sp)
+      if (sp < g.RS) sum += v[sp];
+    if (p >= g.log_std_off && p < g.log_std_off + g.A) sum -= (float)g.ent;  // ppo.hpp:157
+    g.grads[p] = sum;
+    bad = !isfinite(sum);
   }
-  if (bad) atomicOr(&g.tickets[g.ntiles + 1], 1);
-  if (tid == 0) g.tickets[tile] = 0;
-  // ---- the last tile evaluates the step (reference order: losses, then gradients) ----
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(&g.tickets[1], 1);
   __threadfence();
-  __syncthreads();
   __shared__ int lastall;
-  if (tid == 0) lastall = (atomicAdd(&g.tickets[g.ntiles], 1) == g.ntiles - 1);
+  if (tid == 0) lastall = (atomicAdd(&g.tickets[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
-  if (!lastall || tid != 0) return;
+  if (!lastall) return;
   __threadfence();
+  // split loss sums and log_std values loaded by the block, summed by one thread in order
+  __shared__ double red[2 * kMaxSplits + 256];
+  if (tid < g.RS) {
+    red[tid] = g.partial[(size_t)tid * g.Pext + g.P];
+    red[kMaxSplits + tid] = g.partial[(size_t)tid * g.Pext + g.P + 1];
+  }
+  for (int dd = tid; dd < g.A && dd < 256; dd += 256) red[2 * kMaxSplits + dd] = (double)g.params[g.log_std_off + dd];
+  __syncthreads();
+  if (tid != 0) return;
   double pl = 0.0, vl = 0.0;
   for (int sp = 0; sp < g.RS; ++sp) {
-    pl += g.partial[(size_t)sp * g.Pext + g.P];
-    vl += g.partial[(size_t)sp * g.Pext + g.P + 1];
+    pl += red[sp];
+    vl += red[kMaxSplits + sp];
   }
   double ent = 0.0;  // policy_entropy nn.hpp:273-277
-  for (int dd = 0; dd < g.A; ++dd) ent += 0.5 * (1.8378770664093454836 + 1.0) + (double)g.params[g.log_std_off + dd];
-  const int gbad = atomicAdd(&g.tickets[g.ntiles + 1], 0);
-  g.tickets[g.ntiles] = 0;
-  g.tickets[g.ntiles + 1] = 0;
+  for (int dd = 0; dd < g.A; ++dd)
+    ent += 0.5 * (1.8378770664093454836 + 1.0) + (dd < 256 ? red[2 * kMaxSplits + dd] : (double)g.params[g.log_std_off + dd]);
+  const int gbad = atomicAdd(&g.tickets[1], 0);
+  g.tickets[0] = 0;
+  g.tickets[1] = 0;
   if (!isfinite(pl)) {
     g.status[0] = PRB_ERR_NUMERIC;
     g.status[1] = 10;
@@ -558,6 +612,7 @@ struct PpoWorkspace {
   DevBuf<int64_t> step;
   DevBuf<double> stats;
   DevBuf<uint32_t> perm;
+  DevBuf<unsigned long long> trace;  // PRB_PPO_TRACE
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -631,15 +686,19 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   for (int net = 0; net < 2; ++net) {
     const MlpDesc& d = net ? p.critic : p.actor;
     for (int l = 0; l < d.nl; ++l)
-      for (int k0 = 0; k0 <= d.dims[l]; k0 += kGT)
+      for (int k0 = 0; k0 < d.dims[l]; k0 += kGT)
         for (int j0 = 0; j0 < d.dims[l + 1]; j0 += kGT) tiles.push_back(make_int4(net, l, k0, j0));
   }
   tiles.push_back(make_int4(0, -1, 0, 0));
   ws.ntiles = (int)tiles.size();
-  ws.RS = std::min(kMaxSplits, (mb + kGChunk - 1) / kGChunk);
+  ws.RS = std::min(kMaxSplits, (mb + kGRows - 1) / kGRows);
   ws.tiles.alloc(tiles.size());
   PRB_CUDA(cudaMemcpy(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  ws.tickets.alloc((size_t)ws.ntiles + 2);
+  ws.tickets.alloc(2);  // [0] completed-CTA counter of ppo_sum, [1] gradient non-finite flag
+  if (getenv("PRB_PPO_TRACE")) {
+    ws.trace.alloc((size_t)ws.ntiles * ws.RS * 8);
+    PRB_CUDA(cudaMemset(ws.trace.p, 0, ws.trace.bytes()));
+  }
   PRB_CUDA(cudaMemset(ws.tickets.p, 0, ws.tickets.bytes()));
   if (ws.partial.n < (size_t)ws.RS * p.Pext) ws.partial.alloc((size_t)ws.RS * p.Pext);
   if (!ws.step.p) ws.step.alloc(1);
@@ -678,7 +737,9 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   g.step = ws.step.p;
   g.stats = ws.stats.p;
   g.apply = apply;
+  g.trace = ws.trace.p;
   ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
+  ppo_sum_kernel<<<(p.P + 255) / 256, 256, 0, s>>>(g);
   if (apply) prb_adam_launch(a, a->d_grads.p, a->d_status.p, s);
 }
 
@@ -793,6 +854,14 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
       for (size_t i = 0; i < steps; ++i) launch_step(p, dst, ws, cfg->entropy_coef, 1, s);
     }
     PRB_CHECK_LAUNCH();
+    if (const char* tp = getenv("PRB_PPO_TRACE")) {  // debug: globaltimer marks of the last step's ppo_grad CTAs
+      std::vector<unsigned long long> h(ws.trace.n);
+      PRB_CUDA(cudaMemcpy(h.data(), ws.trace.p, ws.trace.bytes(), cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen(tp, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
     check_status(dst);
     double st[4];
     PRB_CUDA(cudaMemcpyAsync(st, ws.stats.p, sizeof(st), cudaMemcpyDeviceToHost, s));
