@@ -104,30 +104,29 @@ __device__ __forceinline__ uint32_t mb_row(const PpoArgs& a, int64_t step, uint3
   return feistel_perm(pos, a.n, a.bits, derive_seed2(a.seed, 0x50504fULL /*"PPO"*/, epoch));
 }
 
-// floats of the staged weight set: every layer of both nets at row stride out+1
-__host__ __device__ inline size_t staged_floats(const PpoArgs& a) {
+// floats of one net's staged weight set: every layer at row stride out+1
+__host__ __device__ inline size_t staged_floats(const MlpDesc& d) {
   size_t n = 0;
-  for (int l = 0; l < a.actor.nl; ++l) n += (size_t)a.actor.dims[l] * (a.actor.dims[l + 1] + 1);
-  for (int l = 0; l < a.critic.nl; ++l) n += (size_t)a.critic.dims[l] * (a.critic.dims[l + 1] + 1);
+  for (int l = 0; l < d.nl; ++l) n += (size_t)d.dims[l] * (d.dims[l + 1] + 1);
   return (n + 3) & ~size_t(3);
 }
 
 struct Smem {
-  float* w;  // staged weights (nullptr when not staged)
+  float* w;  // staged weights of this CTA's net (nullptr when not staged)
   float* x;
-  float* aa[kMaxLayers];
-  int lda[kMaxLayers];
-  float* ca[kMaxLayers];
-  int ldc[kMaxLayers];
+  float* h[kMaxLayers];  // post-activation outputs of each layer
+  int ldh[kMaxLayers];
   float* d0;
   float* d1;
   float* actn;
   float* misc;  // [R8][4]: old_lp, adv_norm, ret, -
   float* tmp;   // [R8][ldA]
-  float* loss;  // [R8][2]
+  float* loss;  // [R8]
 };
 
-__host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) {
+// shared-memory carve-up of one CTA working on net `net` (0 actor, 1 critic)
+__host__ __device__ inline size_t carve(const PpoArgs& a, int net, float* base, Smem* s) {
+  const MlpDesc& d = net ? a.critic : a.actor;
   const int R8 = (a.R + 7) & ~7;
   const int ldx = (a.S + 3) & ~3;
   const int ldA = (a.A + 3) & ~3;
@@ -137,24 +136,16 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) 
     o += (n + 3) & ~size_t(3);
     return p;
   };
-  float* w = a.stage ? take(staged_floats(a)) : nullptr;
+  float* w = a.stage ? take(staged_floats(d)) : nullptr;
   if (s) s->w = w;
   float* x = take((size_t)R8 * ldx);
   if (s) s->x = x;
-  for (int l = 0; l < a.actor.nl; ++l) {
-    const int ld = (a.actor.dims[l + 1] + 3) & ~3;
+  for (int l = 0; l < d.nl; ++l) {
+    const int ld = (d.dims[l + 1] + 3) & ~3;
     float* p = take((size_t)R8 * ld);
     if (s) {
-      s->aa[l] = p;
-      s->lda[l] = ld;
-    }
-  }
-  for (int l = 0; l < a.critic.nl; ++l) {
-    const int ld = (a.critic.dims[l + 1] + 3) & ~3;
-    float* p = take((size_t)R8 * ld);
-    if (s) {
-      s->ca[l] = p;
-      s->ldc[l] = ld;
+      s->h[l] = p;
+      s->ldh[l] = ld;
     }
   }
   const int ldd = a.ldw > ldA ? a.ldw : ldA;
@@ -163,7 +154,7 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) 
   float* actn = take((size_t)R8 * ldA);
   float* misc = take((size_t)R8 * 4);
   float* tmp = take((size_t)R8 * ldA);
-  float* loss = take((size_t)R8 * 2);
+  float* loss = take((size_t)R8);
   if (s) {
     s->d0 = d0;
     s->d1 = d1;
@@ -174,6 +165,8 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, float* base, Smem* s) 
   }
   return o * sizeof(float);
 }
+
+inline size_t carve_max(const PpoArgs& a) { return std::max(carve(a, 0, nullptr, nullptr), carve(a, 1, nullptr, nullptr)); }
 
 // Weight locations for one net: staged copy (stride out+1) or the HBM blob (stride out).
 __device__ __forceinline__ LayerPtrs layer_ptrs(const PpoArgs& a, const MlpDesc& d, float* staged_base) {
@@ -246,11 +239,15 @@ __device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int o
   }
 }
 
+// blockIdx.y = net: the actor and the critic are independent through the forward,
+// their heads and the backward, so each CTA carries one net (half the weights to stage).
 __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   if (a.status[0] != 0) return;
   extern __shared__ __align__(16) float smem[];
+  const int net = blockIdx.y;
+  const MlpDesc& d = net ? a.critic : a.actor;
   Smem s;
-  carve(a, smem, &s);
+  carve(a, net, smem, &s);
   const int64_t step = *a.step;
   const int R = a.R;
   const int ldx = (a.S + 3) & ~3;
@@ -258,18 +255,9 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   const int q0 = blockIdx.x * R;
   const int nrows = min(R, a.mb - q0);
   const double mean = a.advstat[0], denom = a.advstat[1];
-  float* wa = nullptr;
-  float* wc = nullptr;
-  if (a.stage) {
-    wa = s.w;
-    size_t na = 0;
-    for (int l = 0; l < a.actor.nl; ++l) na += (size_t)a.actor.dims[l] * (a.actor.dims[l + 1] + 1);
-    wc = s.w + na;
-    stage_weights(a, a.actor, wa);
-    stage_weights(a, a.critic, wc);
-  }
+  if (a.stage) stage_weights(a, d, s.w);
   // the gather below overlaps with the weight copies in flight; waited before the forward
-  const LayerPtrs lpa = layer_ptrs(a, a.actor, wa), lpc = layer_ptrs(a, a.critic, wc);
+  const LayerPtrs lp = layer_ptrs(a, d, s.w);
   // ---- gather (gather_minibatch ppo.hpp:83-103): a warp per row, every load of a row in flight ----
   for (int r = threadIdx.x / 32; r < nrows; r += blockDim.x / 32) {
     const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
@@ -292,18 +280,23 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
     for (int c = lane + 32 * kGatherUnroll; c < a.S; c += 32)  // wide observations
       s.x[r * ldx + c] = (a.obs_mode == 1) ? ((c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp])
                                            : a.obs[(size_t)i * a.S + c];
-    const float act = (lane < A) ? a.act[(size_t)i * A + lane] : 0.0f;
-    float lp0 = 0.f, advv = 0.f, retv = 0.f;
-    if (lane == 0) {
-      lp0 = a.logp[i];
-      advv = a.adv[i];
+    float act = 0.f, lp0 = 0.f, advv = 0.f, retv = 0.f;
+    if (net == 0) {
+      act = (lane < A) ? a.act[(size_t)i * A + lane] : 0.0f;
+      if (lane == 0) {
+        lp0 = a.logp[i];
+        advv = a.adv[i];
+      }
+    } else if (lane == 0) {
       retv = a.ret[i];
     }
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u)
       if (lane + 32 * u < a.S) s.x[r * ldx + lane + 32 * u] = xv[u];
-    if (lane < A) s.actn[r * ldA + lane] = act;
-    for (int c = lane + 32; c < A; c += 32) s.actn[r * ldA + c] = a.act[(size_t)i * A + c];
+    if (net == 0) {
+      if (lane < A) s.actn[r * ldA + lane] = act;
+      for (int c = lane + 32; c < A; c += 32) s.actn[r * ldA + c] = a.act[(size_t)i * A + c];
+    }
     if (lane == 0) {
       s.misc[r * 4 + 0] = lp0;
       s.misc[r * 4 + 1] = (float)(((double)advv - mean) / denom);
@@ -313,84 +306,74 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   if (a.stage) stage_wait();
   __syncthreads();
   // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
-  mlp_forward_tile_p(a.actor, lpa, s.x, ldx, s.aa, s.lda, nrows);
-  mlp_forward_tile_p(a.critic, lpc, s.x, ldx, s.ca, s.ldc, nrows);
-  // layer inputs for the gradient GEMMs: the observation and every hidden activation
-  store_rows_g(a.slab + a.hin_off[0][0], a.S, s.x, ldx, nrows, q0);
-  for (int l = 1; l < a.actor.nl; ++l)
-    store_rows_g(a.slab + a.hin_off[0][l], a.actor.dims[l], s.aa[l - 1], s.lda[l - 1], nrows, q0);
-  for (int l = 1; l < a.critic.nl; ++l)
-    store_rows_g(a.slab + a.hin_off[1][l], a.critic.dims[l], s.ca[l - 1], s.ldc[l - 1], nrows, q0);
+  mlp_forward_tile_p(d, lp, s.x, ldx, s.h, s.ldh, nrows);
+  // layer inputs for the gradient GEMMs: the observation (actor CTAs) and every hidden activation
+  if (net == 0) store_rows_g(a.slab + a.hin_off[0][0], a.S, s.x, ldx, nrows, q0);
+  for (int l = 1; l < d.nl; ++l) store_rows_g(a.slab + a.hin_off[net][l], d.dims[l], s.h[l - 1], s.ldh[l - 1], nrows, q0);
   // ---- per-row losses and head gradients (ppo.hpp:128-167) ----
   const float inv_n = 1.0f / (float)a.mb;
-  const float* log_std = a.params + a.log_std_off;
-  float* meanb = s.aa[a.actor.nl - 1];
-  const int ldm = s.lda[a.actor.nl - 1];
-  const int Q = (A + 3) / 4;
-  int L = 1;
-  while (L < Q && L < 32) L <<= 1;
-  const int rpp = blockDim.x / L;
-  const int lir = threadIdx.x % L;
-  const int rmax = ((nrows + rpp - 1) / rpp) * rpp;
-  for (int r = threadIdx.x / L; r < rmax; r += rpp) {
-    const bool on = r < nrows;
-    float lp = 0.0f;
-    if (on)
-      for (int d = lir; d < A; d += L) {
-        const float ls = log_std[d];
-        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) * expf(-ls);  // (a - mu) / sigma
-        lp += (-0.5f * kLogTwoPiF - ls) - 0.5f * z * z;
+  float* head = s.h[d.nl - 1];
+  const int ldm = s.ldh[d.nl - 1];
+  if (net == 0) {
+    const float* log_std = a.params + a.log_std_off;
+    const int Q = (A + 3) / 4;
+    int L = 1;
+    while (L < Q && L < 32) L <<= 1;
+    const int rpp = blockDim.x / L;
+    const int lir = threadIdx.x % L;
+    const int rmax = ((nrows + rpp - 1) / rpp) * rpp;
+    for (int r = threadIdx.x / L; r < rmax; r += rpp) {
+      const bool on = r < nrows;
+      float lpv = 0.0f;
+      if (on)
+        for (int dd = lir; dd < A; dd += L) {
+          const float ls = log_std[dd];
+          const float z = (s.actn[r * ldA + dd] - head[r * ldm + dd]) * expf(-ls);  // (a - mu) / sigma
+          lpv += (-0.5f * kLogTwoPiF - ls) - 0.5f * z * z;
+        }
+      for (int o = L / 2; o > 0; o >>= 1) lpv += __shfl_xor_sync(0xffffffffu, lpv, o, L);
+      if (on) {
+        const float ratio = expf(lpv - s.misc[r * 4 + 0]);
+        const float adv = s.misc[r * 4 + 1];
+        const float surr1 = ratio * adv;
+        const float lo = (float)(1.0 - a.clip), hi = (float)(1.0 + a.clip);
+        const float clipped = (ratio < lo) ? lo : ((hi < ratio) ? hi : ratio);  // std::clamp
+        const float surr2 = clipped * adv;
+        const float dl_dlp = (surr1 <= surr2) ? -adv * ratio * inv_n : 0.0f;  // ppo.hpp:146
+        for (int dd = lir; dd < A; dd += L) {
+          const float ls = log_std[dd];
+          const float isig = expf(-ls);
+          const float z = (s.actn[r * ldA + dd] - head[r * ldm + dd]) * isig;
+          head[r * ldm + dd] = dl_dlp * (z * isig);  // dmean = dL/dlp * z / sigma, in place
+          s.tmp[r * ldA + dd] = dl_dlp * (z * z - 1.0f);
+        }
+        if (lir == 0) s.loss[r] = -((surr2 < surr1) ? surr2 : surr1) * inv_n;  // std::min (NaN-propagating)
       }
-    for (int o = L / 2; o > 0; o >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o, L);
-    if (on) {
-      const float ratio = expf(lp - s.misc[r * 4 + 0]);
-      const float adv = s.misc[r * 4 + 1];
-      const float surr1 = ratio * adv;
-      const float lo = (float)(1.0 - a.clip), hi = (float)(1.0 + a.clip);
-      const float clipped = (ratio < lo) ? lo : ((hi < ratio) ? hi : ratio);  // std::clamp
-      const float surr2 = clipped * adv;
-      const float dl_dlp = (surr1 <= surr2) ? -adv * ratio * inv_n : 0.0f;  // ppo.hpp:146
-      for (int d = lir; d < A; d += L) {
-        const float ls = log_std[d];
-        const float isig = expf(-ls);
-        const float z = (s.actn[r * ldA + d] - meanb[r * ldm + d]) * isig;
-        meanb[r * ldm + d] = dl_dlp * (z * isig);  // dmean = dL/dlp * z / sigma, in place
-        s.tmp[r * ldA + d] = dl_dlp * (z * z - 1.0f);
-      }
-      if (lir == 0) {
-        s.loss[r * 2 + 0] = -((surr2 < surr1) ? surr2 : surr1) * inv_n;  // std::min (NaN-propagating)
-        float* vb = s.ca[a.critic.nl - 1];
-        const float err = vb[r * s.ldc[a.critic.nl - 1]] - s.misc[r * 4 + 2];
-        s.loss[r * 2 + 1] = err * err * inv_n;
-        vb[r * s.ldc[a.critic.nl - 1]] = (float)a.vf * 2.0f * err * inv_n;  // dV, in place
-      }
+    }
+  } else {
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+      const float err = head[r * ldm] - s.misc[r * 4 + 2];
+      s.loss[r] = err * err * inv_n;
+      head[r * ldm] = (float)a.vf * 2.0f * err * inv_n;  // dV, in place
     }
   }
   __syncthreads();
-  // head deltas, log_std terms and per-row losses
-  store_rows_g(a.slab + a.del_off[0][a.actor.nl - 1], A, meanb, ldm, nrows, q0);
-  store_rows_g(a.slab + a.del_off[1][a.critic.nl - 1], 1, s.ca[a.critic.nl - 1], s.ldc[a.critic.nl - 1], nrows, q0);
-  store_rows_g(a.slab + a.ls_off, A, s.tmp, ldA, nrows, q0);
-  store_rows_g(a.slab + a.loss_off, 2, s.loss, 2, nrows, q0);
+  // head delta, log_std terms (actor) and this net's per-row loss column
+  store_rows_g(a.slab + a.del_off[net][d.nl - 1], d.dims[d.nl], head, ldm, nrows, q0);
+  if (net == 0) store_rows_g(a.slab + a.ls_off, A, s.tmp, ldA, nrows, q0);
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) a.slab[a.loss_off + (size_t)(q0 + r) * 2 + net] = s.loss[r];
   const int ldp = a.ldw > ldA ? a.ldw : ldA;
   // ---- backward deltas (mlp_backward_accumulate nn.hpp:105-132, the matmul_nt half) ----
-  for (int net = 0; net < 2; ++net) {
-    const MlpDesc& d = net ? a.critic : a.actor;
-    const LayerPtrs& lp = net ? lpc : lpa;
-    float* const* acts = net ? s.ca : s.aa;
-    const int* lds = net ? s.ldc : s.lda;
-    const float* delta = acts[d.nl - 1];
-    int ldd = lds[d.nl - 1];
-    for (int l = d.nl - 1; l >= 1; --l) {
-      const int in = d.dims[l], out = d.dims[l + 1];
-      float* dp = (delta == s.d0) ? s.d1 : s.d0;
-      delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, acts[l - 1], lds[l - 1], dp, ldp, nrows);
-      __syncthreads();
-      store_rows_g(a.slab + a.del_off[net][l - 1], in, dp, ldp, nrows, q0);
-      delta = dp;
-      ldd = ldp;
-    }
+  const float* delta = head;
+  int ldd = ldm;
+  for (int l = d.nl - 1; l >= 1; --l) {
+    const int in = d.dims[l], out = d.dims[l + 1];
+    float* dp = (delta == s.d0) ? s.d1 : s.d0;
+    delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, s.h[l - 1], s.ldh[l - 1], dp, ldp, nrows);
     __syncthreads();
+    store_rows_g(a.slab + a.del_off[net][l - 1], in, dp, ldp, nrows, q0);
+    delta = dp;
+    ldd = ldp;
   }
 }
 
@@ -660,9 +643,9 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   p.R = 8;
   while (p.R < 64 && (size_t)(mb / (p.R * 2)) >= (size_t)a->ctx->num_sms) p.R *= 2;
   p.stage = 1;
-  if (carve(p, nullptr, nullptr) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
-  while (p.R > 8 && carve(p, nullptr, nullptr) > kSmemBudget) p.R /= 2;
-  PRB_REQUIRE(carve(p, nullptr, nullptr) <= kSmemBudget, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
+  if (carve_max(p) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
+  while (p.R > 8 && carve_max(p) > kSmemBudget) p.R /= 2;
+  PRB_REQUIRE(carve_max(p) <= kSmemBudget, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
   // per-row slab: observation, hidden activations (layer inputs) and deltas of both nets
   size_t off = 0;
   auto take = [&](size_t w) {
@@ -708,8 +691,8 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
 }
 
 void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
-  const int grid = (p.mb + p.R - 1) / p.R;
-  const size_t smem = carve(p, nullptr, nullptr);
+  const dim3 grid((p.mb + p.R - 1) / p.R, 2);
+  const size_t smem = carve_max(p);
   ppo_fwd_delta_kernel<<<grid, kPpoThreads, smem, s>>>(p);  // steps run inside CUDA graphs: no event scopes
   GradArgs g;
   g.slab = p.slab;
