@@ -352,6 +352,26 @@ inline std::pair<std::unique_ptr<Agent>, PpoUpdateStats> ppo_update(const Agent&
   return {std::move(out), PpoUpdateStats{st.mean_policy_loss, st.mean_value_loss, st.mean_entropy, st.minibatches}};
 }
 
+// EvaluationRecord pod.hpp:30-36 and evaluate pod.hpp:43-83: one episode per env of
+// `env` (reset with derive_seed(seed, kEpisode, i); its state is consumed).
+struct EvaluationRecord {
+  double wall_seconds = 0.0;
+  std::int64_t env_steps = 0;
+  std::vector<double> episodic_rewards;
+  double mean = 0.0;
+  double std_dev = 0.0;
+  std::uint64_t eval_steps = 0;
+};
+
+inline EvaluationRecord evaluate(const Agent& actor, VectorizedEnvironment& env, std::uint64_t seed,
+                                 bool sample_actions = false) {
+  EvaluationRecord rec;
+  rec.episodic_rewards.resize(env.num_envs());
+  check(prb_evaluate(actor.get(), env.get(), seed, sample_actions ? 1 : 0, rec.episodic_rewards.data(), &rec.mean,
+                     &rec.std_dev, &rec.eval_steps));
+  return rec;
+}
+
 // fuse_parameters pod.hpp:141-172
 inline std::unique_ptr<Agent> fuse_parameters(const std::vector<const Agent*>& agents) {
   if (agents.empty()) throw UsageError("fuse_parameters: empty artifact list");

@@ -254,6 +254,19 @@ PRB_API int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows,
  * on a non-finite gradient). */
 PRB_API int prb_adam_step_host(prb_agent a, const double* grads);
 
+/* ---- evaluator (evaluate pod.hpp:43-83, PodEvaluator::process :313-316) --
+ * `episodes` = env's num_envs evaluation episodes of the agent's policy:
+ * the VecEnv is reset with the per-episode streams derive_seed(seed,
+ * kEpisode, i) (its state is consumed) and stepped with the policy mean
+ * clipped to the spec bounds (sample_actions != 0: Gaussian samples with
+ * Philox noise in place of the reference's mt19937_64 normals).  Outputs the
+ * fp64 total reward of each episode (its first done), their mean and
+ * population standard deviation (EvaluationRecord), and the evaluation env
+ * steps taken.  UsageError if an episode does not end within the env's step
+ * bound. */
+PRB_API int prb_evaluate(prb_agent a, prb_vecenv env, uint64_t seed, int sample_actions, double* episodic_rewards,
+                         double* mean, double* std_dev, uint64_t* eval_steps);
+
 /* ---- learner fusion (pod.hpp:141-172) ----------------------------------- */
 PRB_API int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out);
 

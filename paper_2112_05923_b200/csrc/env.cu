@@ -611,12 +611,12 @@ __global__ void __launch_bounds__(256) pm_step_kernel(PmStepArgs a) {
   }
 }
 
-__global__ void pm_reset_kernel(int N, uint64_t seed, double* st, int32_t* steps, double* ep_return, uint64_t* mt,
-                                int32_t* mt_idx, float* obs) {
+__global__ void pm_reset_kernel(int N, uint64_t seed, uint64_t tag, double* st, int32_t* steps, double* ep_return,
+                                uint64_t* mt, int32_t* mt_idx, float* obs) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (size_t)N) return;
-  // rngs_[i].seed(derive_seed(seed, kVecEnv, i)) env.hpp:188
-  mt64_seed(mt + e, N, derive_seed2(seed, 1, e));
+  // rngs_[i].seed(derive_seed(seed, kVecEnv, i)) env.hpp:188; the evaluator passes kEpisode (pod.hpp:52)
+  mt64_seed(mt + e, N, derive_seed2(seed, tag, e));
   int32_t idx = kMtN;
   double s[6];
   pm::reset_draws(mt + e, N, idx, s);
@@ -832,26 +832,33 @@ int prb_vecenv_spec(prb_vecenv env, prb_env_spec* out) {
 size_t prb_vecenv_num_envs(prb_vecenv env) { return env ? env->N : 0; }
 const float* prb_vecenv_states_device(prb_vecenv env) { return env ? env->d_obs.p : nullptr; }
 
+// reset(seed) with the per-env streams derive_seed(seed, tag, i): tag 1 = kVecEnv
+// (VectorizedEnvironment::reset env.hpp:186-194), 8 = kEpisode (evaluate pod.hpp:52).
+void prb_vecenv_reset_tagged(prb_vecenv env, uint64_t seed, uint64_t tag) {
+  check_env(env);
+  cudaStream_t s = env->ctx->stream;
+  const int N = (int)env->N;
+  if (env->kind == PRB_KIND_STOCK) {  // deterministic reset: the stream is unused (stock_env.hpp:158-163)
+    env->t = env->start;
+    env->step_count = 0;
+    const int K = env->market->K;
+    const int grid = std::min<int>((N + 255) / 256, 4 * env->ctx->num_sms * 8);
+    stock_reset_kernel<<<std::max(grid, 1), 256, 0, s>>>(N, K, (int)env->S, env->cfg.initial_capital,
+                                                         env->d_feat.p + env->start * 5 * (size_t)K, env->d_balance.p,
+                                                         env->d_shares.p, env->d_ep_return.p, env->d_obs.p);
+  } else {
+    pm_reset_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, seed, tag, env->d_pm_state.p, env->d_pm_steps.p,
+                                                    env->d_ep_return.p, env->d_mt.p, env->d_mt_idx.p, env->d_obs.p);
+  }
+  PRB_CHECK_LAUNCH();
+  env->was_reset = true;
+}
+
 int prb_vecenv_reset(prb_vecenv env, uint64_t seed, float* d_obs) {
   return guard([&] {
     check_env(env);
     cudaStream_t s = env->ctx->stream;
-    const int N = (int)env->N;
-    if (env->kind == PRB_KIND_STOCK) {
-      env->t = env->start;
-      env->step_count = 0;
-      const int K = env->market->K;
-      const int grid = std::min<int>((N + 255) / 256, 4 * env->ctx->num_sms * 8);
-      stock_reset_kernel<<<std::max(grid, 1), 256, 0, s>>>(N, K, (int)env->S, env->cfg.initial_capital,
-                                                           env->d_feat.p + env->start * 5 * (size_t)K,
-                                                           env->d_balance.p, env->d_shares.p, env->d_ep_return.p,
-                                                           env->d_obs.p);
-    } else {
-      pm_reset_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, seed, env->d_pm_state.p, env->d_pm_steps.p,
-                                                      env->d_ep_return.p, env->d_mt.p, env->d_mt_idx.p, env->d_obs.p);
-    }
-    PRB_CHECK_LAUNCH();
-    env->was_reset = true;
+    prb_vecenv_reset_tagged(env, seed, 1);
     if (d_obs && d_obs != env->d_obs.p)
       PRB_CUDA(cudaMemcpyAsync(d_obs, env->d_obs.p, env->d_obs.bytes(), cudaMemcpyDeviceToDevice, s));
   });

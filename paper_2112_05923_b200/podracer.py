@@ -521,6 +521,26 @@ def fuse_parameters(agents: Sequence[Agent], out: Optional[Agent] = None) -> Age
     return dst
 
 
+@dataclass
+class EvaluationRecord:
+    """EvaluationRecord pod.hpp:30-36 (wall_seconds / env_steps are the caller's)."""
+    episodic_rewards: np.ndarray
+    mean: float
+    std_dev: float
+    eval_steps: int
+
+
+def evaluate(agent: Agent, env: "VectorizedEnvironment", seed: int, sample_actions: bool = False) -> EvaluationRecord:
+    """evaluate pod.hpp:43-83: one evaluation episode per env of `env` (which is
+    reset with derive_seed(seed, kEpisode, i) and consumed)."""
+    n = env.num_envs()
+    r = np.zeros(n, dtype=np.float64)
+    m, sd, st = C.c_double(), C.c_double(), C.c_uint64()
+    agent.ctx.lib.prb_evaluate(agent.h, env.h, seed, 1 if sample_actions else 0, _p(r, C.c_double), C.byref(m),
+                               C.byref(sd), C.byref(st))
+    return EvaluationRecord(r, m.value, sd.value, st.value)
+
+
 def leaderboard_rank(ctx: Context, scores, seqs, capacity: int) -> np.ndarray:
     """Board order after inserting (score, seq) candidates (tournament.hpp:104-119)."""
     s = np.ascontiguousarray(scores, dtype=np.float64)

@@ -77,6 +77,7 @@ def load_oracle():
     lib.orc_stock_vec_step.argtypes = [C.c_size_t, C.c_int, C.POINTER(StockCfg), C.c_size_t, C.c_size_t, D, D,
                                        C.c_size_t, D, D, SZ, SZ, D, D, D, D, U8, D, D, U64]
     lib.orc_pointmass_step.argtypes = [D, D, C.c_uint64, D, D, I32]
+    lib.orc_pointmass_reset.argtypes = [C.POINTER(MT64), D]
     lib.orc_pm_vec_reset.argtypes = [C.c_size_t, C.c_uint64, C.POINTER(MT64), D, U64, D]
     lib.orc_pm_vec_step.argtypes = [C.c_size_t, C.POINTER(MT64), D, U64, D, D, D, U8, D, D, U64]
     lib.orc_mlp_param_count.restype = C.c_size_t
