@@ -64,19 +64,44 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML
+    (nvidia_ml_py) polled every 2 ms from a background thread, so even a 30 ms region gets
+    samples; nvidia-smi -lms as the fallback when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.proc, self.nvml, self.stop_evt = device, [], None, None, threading.Event()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop_evt.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, mx, rs))
+                    except Exception:
+                        pass
+                    self.stop_evt.wait(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
+        try:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -84,29 +109,38 @@ class ClockSampler:
             self.proc = None
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 6 and p[0].replace(".", "").isdigit():
+                rs = {n for n, v in zip(names, p[2:6]) if v.lower().startswith("active")}
+                self.rows.append((float(p[0]), float(p[1]) if p[1].replace(".", "").isdigit() else None, rs))
 
     def stop(self):
+        self.stop_evt.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        elif self.nvml is not None:
+            self.thread.join(timeout=1)
         return self.summary()
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [float(r[0]) for r in self.rows]
+        mx = [float(r[1]) for r in self.rows if r[1]]
+        reasons = set()
+        for r in self.rows:
+            if isinstance(r[2], set):
+                reasons |= r[2]
+            else:
+                reasons |= {n for bit, n in self.REASONS.items() if r[2] & bit}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 class Dist:
@@ -179,7 +213,7 @@ def run_reference(args, d: Dist):
     # each step = one bounded sample of the configs[1] workload on the host cores
     rates = []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_rate(m, ind, seconds=0.0)
+        r = cpu_reference_rate(m, ind, seconds=2.0)  # ~2 s of host work per step
         if r is None:
             emit(({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"}))
             return
@@ -189,7 +223,9 @@ def run_reference(args, d: Dist):
     cb = dict(rates[-1])
     cb["value"] = value
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": args.envs * args.horizon / value * 1e3,  # one full configs[1] collect at the sampled rate
+           "ms_per_step_note": "projected: envs x horizon / sampled rate", "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_dict(args), "cpu_baseline": cb,
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
