@@ -77,6 +77,7 @@ struct PpoArgs {
   int hin_off[2][kMaxLayers];  // H_{l-1} rows ([mb][dims[l]]); l = 0 is the observation (shared)
   int del_off[2][kMaxLayers];  // delta_l rows ([mb][dims[l+1]])
   int ls_off, loss_off;        // [mb][A] log_std terms, [mb][2] policy / value loss terms
+  unsigned long long* trace;   // debug (PRB_PPO_TRACE): clock64 phase marks of CTA (0, net), else null
 };
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n).
@@ -114,8 +115,7 @@ __host__ __device__ inline size_t staged_floats(const MlpDesc& d) {
 struct Smem {
   float* w;  // staged weights of this CTA's net (nullptr when not staged)
   float* x;
-  float* h[kMaxLayers];  // post-activation outputs of each layer
-  int ldh[kMaxLayers];
+  float* h0;  // post-activation outputs of layer 0; layer l follows at R8 * round4(dims[i+1]) per layer i < l
   float* d0;
   float* d1;
   float* actn;
@@ -141,12 +141,8 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, int net, float* base, 
   float* x = take((size_t)R8 * ldx);
   if (s) s->x = x;
   for (int l = 0; l < d.nl; ++l) {
-    const int ld = (d.dims[l + 1] + 3) & ~3;
-    float* p = take((size_t)R8 * ld);
-    if (s) {
-      s->h[l] = p;
-      s->ldh[l] = ld;
-    }
+    float* p = take((size_t)R8 * ((d.dims[l + 1] + 3) & ~3));
+    if (s && l == 0) s->h0 = p;
   }
   const int ldd = a.ldw > ldA ? a.ldw : ldA;
   float* d0 = take((size_t)R8 * ldd);
@@ -241,11 +237,20 @@ __device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int o
 
 // blockIdx.y = net: the actor and the critic are independent through the forward,
 // their heads and the backward, so each CTA carries one net (half the weights to stage).
+// STAGED: the net's weights are copied to shared memory (every W access is an LDS);
+// otherwise (nets too wide for the tile) they are read from L2.
+template <bool STAGED>
 __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   if (a.status[0] != 0) return;
   extern __shared__ __align__(16) float smem[];
   const int net = blockIdx.y;
   const MlpDesc& d = net ? a.critic : a.actor;
+  unsigned long long* tr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
+  int ntr = 0;
+  auto mark = [&]() {
+    if (tr && ntr < 16) tr[ntr++] = clock64();
+  };
+  mark();
   Smem s;
   carve(a, net, smem, &s);
   const int64_t step = *a.step;
@@ -255,9 +260,27 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   const int q0 = blockIdx.x * R;
   const int nrows = min(R, a.mb - q0);
   const double mean = a.advstat[0], denom = a.advstat[1];
-  if (a.stage) stage_weights(a, d, s.w);
+  if (STAGED) stage_weights(a, d, s.w);
+  mark();
   // the gather below overlaps with the weight copies in flight; waited before the forward
-  const LayerPtrs lp = layer_ptrs(a, d, s.w);
+  // Per-layer pointers are recomputed from the shared-memory base instead of being kept in
+  // runtime-indexed arrays: an array of pointers lands in local memory and every access
+  // through it becomes a generic (LD/ST) instead of a shared (LDS/STS) access.
+  const int R8 = (R + 7) & ~7;
+  auto h_of = [&](int l) -> float* {
+    float* p = s.h0;
+    for (int i = 0; i < l; ++i) p += (size_t)R8 * ((d.dims[i + 1] + 3) & ~3);
+    return p;
+  };
+  auto ldh_of = [&](int l) { return (d.dims[l + 1] + 3) & ~3; };
+  auto w_of = [&](int l) -> const float* {
+    if (!STAGED) return a.params + d.off[l];
+    float* p = s.w;
+    for (int i = 0; i < l; ++i) p += (size_t)d.dims[i] * (d.dims[i + 1] + 1);
+    return p;
+  };
+  auto ldw_of = [&](int l) { return STAGED ? d.dims[l + 1] + 1 : d.dims[l + 1]; };
+  auto b_of = [&](int l) { return a.params + d.off[l] + (size_t)d.dims[l] * d.dims[l + 1]; };
   // ---- gather (gather_minibatch ppo.hpp:83-103): a warp per row, every load of a row in flight ----
   for (int r = threadIdx.x / 32; r < nrows; r += blockDim.x / 32) {
     const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
@@ -303,17 +326,39 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
       s.misc[r * 4 + 2] = retv;
     }
   }
-  if (a.stage) stage_wait();
+  mark();
+  if (STAGED) stage_wait();
   __syncthreads();
+  mark();
   // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
-  mlp_forward_tile_p(d, lp, s.x, ldx, s.h, s.ldh, nrows);
+  {  // one compact instantiation (RB = 2 rows per thread per pass): the generic dispatcher's
+     // four RB variants x2 activations overflow the instruction cache in this kernel
+    const float* in = s.x;
+    int ldi = ldx;
+#pragma unroll 1
+    for (int l = 0; l < d.nl; ++l) {
+      const int out = d.dims[l + 1];
+      int TJ = 32;
+      while (TJ < out && TJ < (int)blockDim.x) TJ <<= 1;
+      if (l + 1 < d.nl)
+        linear_tile_rb<true, 2>(w_of(l), ldw_of(l), b_of(l), d.dims[l], out, in, ldi, h_of(l), ldh_of(l), nrows, TJ);
+      else
+        linear_tile_rb<false, 2>(w_of(l), ldw_of(l), b_of(l), d.dims[l], out, in, ldi, h_of(l), ldh_of(l), nrows, TJ);
+      mark();
+      __syncthreads();
+      in = h_of(l);
+      ldi = ldh_of(l);
+    }
+  }
+  mark();
   // layer inputs for the gradient GEMMs: the observation (actor CTAs) and every hidden activation
   if (net == 0) store_rows_g(a.slab + a.hin_off[0][0], a.S, s.x, ldx, nrows, q0);
-  for (int l = 1; l < d.nl; ++l) store_rows_g(a.slab + a.hin_off[net][l], d.dims[l], s.h[l - 1], s.ldh[l - 1], nrows, q0);
+  for (int l = 1; l < d.nl; ++l) store_rows_g(a.slab + a.hin_off[net][l], d.dims[l], h_of(l - 1), ldh_of(l - 1), nrows, q0);
+  mark();
   // ---- per-row losses and head gradients (ppo.hpp:128-167) ----
   const float inv_n = 1.0f / (float)a.mb;
-  float* head = s.h[d.nl - 1];
-  const int ldm = s.ldh[d.nl - 1];
+  float* head = h_of(d.nl - 1);
+  const int ldm = ldh_of(d.nl - 1);
   if (net == 0) {
     const float* log_std = a.params + a.log_std_off;
     const int Q = (A + 3) / 4;
@@ -358,22 +403,26 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
     }
   }
   __syncthreads();
+  mark();
   // head delta, log_std terms (actor) and this net's per-row loss column
   store_rows_g(a.slab + a.del_off[net][d.nl - 1], d.dims[d.nl], head, ldm, nrows, q0);
   if (net == 0) store_rows_g(a.slab + a.ls_off, A, s.tmp, ldA, nrows, q0);
   for (int r = threadIdx.x; r < nrows; r += blockDim.x) a.slab[a.loss_off + (size_t)(q0 + r) * 2 + net] = s.loss[r];
   const int ldp = a.ldw > ldA ? a.ldw : ldA;
+  mark();
   // ---- backward deltas (mlp_backward_accumulate nn.hpp:105-132, the matmul_nt half) ----
   const float* delta = head;
   int ldd = ldm;
   for (int l = d.nl - 1; l >= 1; --l) {
     const int in = d.dims[l], out = d.dims[l + 1];
     float* dp = (delta == s.d0) ? s.d1 : s.d0;
-    delta_prev_tile(delta, ldd, out, lp.W[l], lp.ldw[l], in, s.h[l - 1], s.ldh[l - 1], dp, ldp, nrows);
+    delta_prev_tile(delta, ldd, out, w_of(l), ldw_of(l), in, h_of(l - 1), ldh_of(l - 1), dp, ldp, nrows);
     __syncthreads();
+    mark();
     store_rows_g(a.slab + a.del_off[net][l - 1], in, dp, ldp, nrows, q0);
     delta = dp;
     ldd = ldp;
+    mark();
   }
 }
 
@@ -679,7 +728,7 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   PRB_CUDA(cudaMemcpy(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
   ws.tickets.alloc(2);  // [0] completed-CTA counter of ppo_sum, [1] gradient non-finite flag
   if (getenv("PRB_PPO_TRACE")) {
-    ws.trace.alloc((size_t)ws.ntiles * ws.RS * 8);
+    ws.trace.alloc((size_t)ws.ntiles * ws.RS * 8 + 32);
     PRB_CUDA(cudaMemset(ws.trace.p, 0, ws.trace.bytes()));
   }
   PRB_CUDA(cudaMemset(ws.tickets.p, 0, ws.tickets.bytes()));
@@ -692,8 +741,13 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
 
 void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
   const dim3 grid((p.mb + p.R - 1) / p.R, 2);
+  PpoArgs pt = p;
+  pt.trace = ws.trace.p ? ws.trace.p + (size_t)ws.ntiles * ws.RS * 8 : nullptr;
   const size_t smem = carve_max(p);
-  ppo_fwd_delta_kernel<<<grid, kPpoThreads, smem, s>>>(p);  // steps run inside CUDA graphs: no event scopes
+  if (p.stage)
+    ppo_fwd_delta_kernel<true><<<grid, kPpoThreads, smem, s>>>(pt);
+  else
+    ppo_fwd_delta_kernel<false><<<grid, kPpoThreads, smem, s>>>(pt);  // steps run inside CUDA graphs: no event scopes
   GradArgs g;
   g.slab = p.slab;
   std::memcpy(g.hin_off, p.hin_off, sizeof(g.hin_off));
@@ -749,7 +803,10 @@ void check_status(prb_agent a) {
 void set_smem_attr() {
   static bool done = false;
   if (!done) {
-    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBudget));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBudget));
     PRB_CUDA(cudaFuncSetAttribute(ppo_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(2 * kGChunk * kGLd * sizeof(float))));
     done = true;

@@ -11,11 +11,17 @@ namespace stock {
 // exact quotient is >= desired, so is its rounding (desired is a double), and
 // floor() of it; the result is then `desired` itself.  Only cash-limited buys
 // pay for __ddiv_rn, which is the long pole of the per-env dependency chain.
-__device__ __forceinline__ double buy_qty(double desired, double balance, double pc) {
-  if (__fma_rn(desired, pc, -balance) <= 0.0) return desired;
+// The cash-limited slow path is out of line: inlining __ddiv_rn's sequence once
+// per asset of an unrolled K-loop bloats the kernels past the instruction cache.
+static __device__ __noinline__ double buy_qty_limited(double desired, double balance, double pc) {
   const double affordable = floor(__ddiv_rn(balance, pc));
   const double floor0 = (affordable < 0.0) ? 0.0 : affordable;  // std::max(affordable, 0.0)
   return (floor0 < desired) ? floor0 : desired;                  // std::min(desired, .)
+}
+
+__device__ __forceinline__ double buy_qty(double desired, double balance, double pc) {
+  if (__fma_rn(desired, pc, -balance) <= 0.0) return desired;
+  return buy_qty_limited(desired, balance, pc);
 }
 
 }  // namespace stock
