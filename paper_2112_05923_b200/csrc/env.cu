@@ -326,6 +326,28 @@ __device__ __forceinline__ void write_obs_v2(float* __restrict__ dst, int nrows,
   }
 }
 
+// Warp-per-row obs writer from a float table whose row r holds the shares in
+// columns 0..K-1 and balance/cap in column K (odd stride Kp = K+1); lanes 0..K
+// write the private part with one shared-memory load each (no conversion or
+// select on the value), then the 5K shared features -- identical for every row,
+// so each lane keeps its <= 5 feature values in registers for the whole block.
+__device__ __forceinline__ void write_obs_tab(float* __restrict__ dst, int nrows, int S, const float* table, int K,
+                                              int Kp, const float* shared) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P = K + 1, F = 5 * K;
+  const int col = (lane == 0) ? K : lane - 1;
+  float fv[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) fv[j] = (lane + 32 * j < F) ? shared[lane + 32 * j] : 0.f;
+  for (int r = warp; r < nrows; r += nw) {
+    float* row = dst + (size_t)r * S;
+    if (lane < P) row[lane] = table[r * Kp + col];
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      if (lane + 32 * j < F) row[P + lane + 32 * j] = fv[j];
+  }
+}
+
 __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, F = 5 * K, Kp = (K & 1) ? K + 2 : K + 1;
@@ -431,7 +453,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
 // the obs writer.  ~170 B of shared memory per env -> ~2x the resident warps
 // of v2, which is what keeps HBM busy while other CTAs run the fp64 chain.
 template <int KMAX>
-__global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs a) {
+__global__ void __launch_bounds__(kEnvBlock, 16) stock_step_v3_kernel(StockStepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, F = 5 * K, Kp = K + 1;  // K even -> odd stride
   double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
@@ -464,6 +486,15 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
   }
   cp_async_wait_all();
   __syncthreads();
+  // desired_k = trunc(clamp(a_k, -1, 1) * max_trade) (stock_env.hpp:83-87), once per asset, kept
+  // in the action registers as floats (integer-valued, exact below 2^24: the launcher checks
+  // max_trade_shares) for both the sell and the buy pass
+#pragma unroll
+  for (int j = 0; j < KMAX / 2; ++j)
+    if (2 * j < K) {
+      act2[j].x = (float)trunc(__dmul_rn(clamp_ref((double)act2[j].x, -1.0, 1.0), a.max_trade));
+      act2[j].y = (float)trunc(__dmul_rn(clamp_ref((double)act2[j].y, -1.0, 1.0), a.max_trade));
+    }
   if (live) {
     double bal = bal_in;
     int32_t* sh = s_sh + tid * Kp;
@@ -472,8 +503,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {  // sells first (stock_env.hpp:88-90)
       if (k < K) {
-        const float ak = (k & 1) ? act2[k >> 1].y : act2[k >> 1].x;
-        const double d = trunc(__dmul_rn(clamp_ref((double)ak, -1.0, 1.0), a.max_trade));
+        const double d = (double)((k & 1) ? act2[k >> 1].y : act2[k >> 1].x);
         if (d < 0.0) {
           const int32_t held = sh[k];
           const double q = -min_ref(-d, (double)held);
@@ -488,8 +518,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {  // then buys (:91-97)
       if (k < K) {
-        const float ak = (k & 1) ? act2[k >> 1].y : act2[k >> 1].x;
-        const double d = trunc(__dmul_rn(clamp_ref((double)ak, -1.0, 1.0), a.max_trade));
+        const double d = (double)((k & 1) ? act2[k >> 1].y : act2[k >> 1].x);
         if (d > 0.0) {
           const double price = s_p0[k];
           const double q = stock::buy_qty(d, bal, __dmul_rn(price, cost_factor));
@@ -505,7 +534,7 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
     const double ret = __dadd_rn(ret_in, r);
     if (a.reward) a.reward[e] = (float)r;
     if (a.done_out) a.done_out[e] = (uint8_t)a.done;
-    s_x0[tid] = (float)__ddiv_rn(bal, a.cap);
+    const float x0 = (float)__ddiv_rn(bal, a.cap);
     if (a.done) {
       if (a.term_ret) a.term_ret[e] = ret;
       if (a.term_len) a.term_len[e] = a.ep_len;
@@ -515,19 +544,25 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v3_kernel(StockStepArgs 
       a.balance[e] = bal;
       a.ep_return[e] = ret;
     }
+    // shares back to HBM (zero after the auto-reset), then this thread's table row becomes
+    // the private obs part as floats: shares in columns 0..K-1, balance/cap in the spare column K
+    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e] = a.done ? 0 : sh[k];
+    float* rowf = reinterpret_cast<float*>(sh);
+    for (int k = 0; k < K; ++k) rowf[k] = (float)sh[k];
+    rowf[K] = x0;
   }
   __syncthreads();
   const int S = a.S;
+  const float* table = reinterpret_cast<const float*>(s_sh);
   if (a.done) {
-    if (a.term_obs) write_obs_v2(a.term_obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_term, K, Kp});
+    if (a.term_obs) write_obs_tab(a.term_obs + e0 * S, nloc, S, table, K, Kp, s_feat_term);
     __syncthreads();
-    s_x0[tid] = (float)(a.cap / a.cap);
-    for (int k = 0; k < K; ++k) s_sh[tid * Kp + k] = 0;
+    float* rowf = reinterpret_cast<float*>(s_sh + tid * Kp);
+    for (int k = 0; k < K; ++k) rowf[k] = 0.0f;
+    rowf[K] = (float)(a.cap / a.cap);  // StockTradingEnv::reset stock_env.hpp:158-163
     __syncthreads();
   }
-  if (live)
-    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e] = s_sh[tid * Kp + k];
-  write_obs_v2(a.obs + e0 * S, nloc, S, ObsSrc{s_x0, s_sh, s_feat_obs, K, Kp});
+  write_obs_tab(a.obs + e0 * S, nloc, S, table, K, Kp, s_feat_obs);
 }
 
 size_t stock_v3_smem_bytes(int K) {
@@ -679,7 +714,7 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
   const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
   {
     ProfScope prof(env->ctx, kProfEnvStock);
-    if (env->step_kernel == 2 && m->K <= 32 && (m->K & 1) == 0) {
+    if (env->step_kernel == 2 && m->K <= 32 && (m->K & 1) == 0 && env->cfg.max_trade_shares < 16777216.0) {
       stock_step_v3_kernel<32><<<grid, kEnvBlock, stock_v3_smem_bytes(m->K), env->ctx->stream>>>(a);
     } else if (env->step_kernel == 2) {
       stock_step_v2_kernel<<<grid, kEnvBlock, stock_v2_smem_bytes(m->K), env->ctx->stream>>>(a);
