@@ -334,6 +334,9 @@ def run_ours(args, d: Dist):
         other["configs[2]_pointmass"] = leg_pointmass(pr, lib, ctx, args.pm_envs, args.pm_horizon, d)
         other["configs[4]_stock_1M"] = leg_stock_large(pr, lib, ctx, market, cfg, args.c5_envs, H, d)
     other["configs[3]_tournament"] = leg_tournament(pr, ctx, d, args.pods_per_gpu)
+    if not args.skip_configs:
+        other["configs[0]_iteration"] = leg_c1_iteration(pr, lib, ctx, market, cfg, m, ind, d,
+                                                         with_cpu=(d.rank == 0 and d.world == 1 and not args.skip_cpu))
 
     # ---- end to end through the public API with host buffers ----
     # Every step: pinned h2d of the params, worker_collect, d2h of the step's 16.8M rewards.
@@ -415,6 +418,49 @@ def leg_pointmass(pr, lib, ctx, n_envs, horizon, d):
             "flop_per_transition": flops,
             "path": "rollout_pm_tc.cu: persistent tcgen05 3x256 actor/critic, bf16 weights streamed from L2 "
                     "through a 5-slot bulk-copy ring, fp64 PointMass step + mt19937_64 resets in the same kernel"}
+
+
+def leg_c1_iteration(pr, lib, ctx, market, cfg, m, ind, d, with_cpu: bool):
+    """configs[0] (the reference's CPU-runnable case): one full PPO iteration of a pod --
+    collect 1,024 stock envs x 256 steps, GAE, 4 epochs x 256 minibatches of 1,024 with Adam
+    (pod.hpp:408-461) -- on the GPU, next to the reference on the host cores: its threaded
+    worker_collect timed in full and its ppo_update timed on 32 minibatches and scaled."""
+    N1, H1, EP, MB = 1024, 256, 4, 1024
+    env = pr.VectorizedEnvironment.stock(ctx, market, cfg, 0, T_ROWS - 1, N1)
+    env.reset(3)
+    agent = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=7)
+    ro = pr.Rollout.for_env(env, H1)
+    pcfg = pr.PpoConfig(minibatch_size=MB, epochs_per_update=EP, buffer_size=N1 * H1)
+
+    def iteration(i):
+        ro.collect(agent, env, seed=100 + i)
+        pr.ppo_update(agent, ro, pcfg, seed=200 + i, out=agent)
+    iteration(0)
+    ms = d.max(time_region(lib, ctx, lambda: [iteration(i) for i in (1, 2, 3)])) / 3
+    out = {"workload": "configs[0]: 30 assets x 1,024 envs, horizon 256, 4 epochs x 256 minibatches of 1,024",
+           "gpu_ms_per_iteration": ms, "gpu_transitions_per_s": N1 * H1 / (ms / 1e3)}
+    if with_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_bind import REF_BENCH_SO, load_ref, ptr, SZ
+        ref = load_ref(REF_BENCH_SO)
+        if ref is not None:
+            cores = os.cpu_count() or 1
+            W = 1 << (cores.bit_length() - 1)
+            flat = pr.artifact_init(S_DIM, K_ASSETS, 7)
+            hid = np.array([64, 64], dtype=np.uint64)
+            close = np.ascontiguousarray(m["close"]); indc = np.ascontiguousarray(ind)
+            col_s = ref.ref_bench_collect(ptr(close), ptr(indc), T_ROWS, K_ASSETS, 0, T_ROWS - 1, W, N1 // W, H1,
+                                          ptr(flat), ptr(hid, SZ), 2, 2112)
+            nmb = 32
+            ppo_s = ref.ref_bench_ppo(ptr(flat), S_DIM, K_ASSETS, ptr(hid, SZ), 2, nmb * MB, H1, MB, 1, 7)
+            cpu_ms = (col_s + ppo_s / nmb * EP * (N1 * H1 // MB)) * 1e3
+            out.update({"cpu_ms_per_iteration": cpu_ms, "cpu_cores": W,
+                        "cpu_sample": f"worker_collect {W} threads x {N1 // W} envs x {H1} measured ({col_s:.2f} s); "
+                                      f"ppo_update 1 epoch x {nmb} minibatches measured ({ppo_s:.2f} s) and scaled to "
+                                      f"{EP * N1 * H1 // MB} (single-threaded, as one learner)",
+                        "speedup_gpu_vs_cpu": cpu_ms / ms})
+    del ro
+    return out
 
 
 def leg_stock_large(pr, lib, ctx, market, cfg, n_envs, horizon, d):

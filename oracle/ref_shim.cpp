@@ -440,6 +440,39 @@ REF_API int ref_leaderboard_sequence(const double* scores, const int64_t* ids, s
   })
 }
 
+// ppo_update ppo.hpp:249 timing on a synthetic buffer of n transitions (chunks of
+// `horizon`; states/actions/log-probs/values/rewards from mt19937_64(seed)),
+// `epochs` x (n / minibatch) sequential Adam steps.  Returns wall seconds.
+REF_API double ref_bench_ppo(const double* flat, size_t S, size_t A, const size_t* hidden, int nh, size_t n,
+                             size_t horizon, size_t minibatch, size_t epochs, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  std::vector<double> st(n * S), ac(n * A), lp(n), rw(n), vl(n);
+  std::vector<uint8_t> dn(n, 0);
+  for (auto& x : st) x = nd(rng);
+  for (auto& x : ac) x = nd(rng);
+  for (size_t i = 0; i < n; ++i) {
+    lp[i] = -0.5 * (double)A + 0.1 * nd(rng);
+    rw[i] = nd(rng);
+    vl[i] = nd(rng);
+  }
+  const size_t nch = n / horizon;
+  std::vector<size_t> off(nch), len(nch, horizon);
+  std::vector<double> boot(nch, 0.0);
+  for (size_t c = 0; c < nch; ++c) off[c] = c * horizon;
+  TransitionBuffer buf = make_buffer(st.data(), ac.data(), lp.data(), rw.data(), dn.data(), vl.data(), n, S, A,
+                                     off.data(), len.data(), boot.data(), nch);
+  AgentArtifact a = artifact_from(flat, nullptr, nullptr, 0, S, A, hidden, nh, 1e-3);
+  PpoConfig cfg;
+  cfg.epochs_per_update = epochs;
+  cfg.minibatch_size = minibatch;
+  cfg.buffer_size = n;
+  auto t0 = std::chrono::steady_clock::now();
+  PpoUpdateResult r = ppo_update(a, buf, cfg, seed);
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return r.stats.minibatches > 0 ? s : -1.0;
+}
+
 // ---- CPU baseline timing (bench.py --impl reference / cpu_baseline) --------
 // pod_train's collect phase (pod.hpp:408-433): `workers` threads, each owning
 // a VectorizedEnvironment of envs_per_worker stock envs, running worker_collect

@@ -156,6 +156,9 @@ def load_ref(path: str = REF_EXACT_SO):
                              SZ, C.c_int, D, D, D, I64]
     lib.ref_leaderboard_sequence.restype = C.c_int
     lib.ref_leaderboard_sequence.argtypes = [D, I64, C.c_size_t, C.c_size_t, I64, D, SZ, I64]
+    lib.ref_bench_ppo.restype = C.c_double
+    lib.ref_bench_ppo.argtypes = [D, C.c_size_t, C.c_size_t, SZ, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
+                                  C.c_size_t, C.c_uint64]
     lib.ref_bench_collect.restype = C.c_double
     lib.ref_bench_collect.argtypes = [D, D, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
                                       C.c_size_t, D, SZ, C.c_int, C.c_uint64]
