@@ -451,6 +451,12 @@ struct GradArgs {
   double* stats;
   int apply;
   unsigned long long* trace;  // debug (PRB_PPO_TRACE): [grid][8] globaltimer marks, else null
+  // Adam (adam_step nn.hpp:164-182), applied by ppo_sum_adam once the gate is known
+  float* p_rw;
+  float* m;
+  float* v;
+  float lr, eps;
+  double b1, b2;
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -569,12 +575,17 @@ __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
 // ---- ppo_sum: grads[p] = sum of the split partials in split order (+ entropy term for
 // log_std), non-finite flag; the last CTA evaluates the step's gate (losses first, then
 // gradients: the reference order) and advances t / the minibatch counter ----
-__global__ void __launch_bounds__(256) ppo_sum_kernel(GradArgs g) {
+// ---- ppo_sum_adam: grads[p] = sum of the split partials in split order (+ entropy term
+// for log_std) and the non-finite flag; the last CTA to finish evaluates the step's gate
+// (losses first, then gradients: the reference order), advances t / the minibatch counter
+// and releases the others, which then apply Adam to their parameter range (skipped when
+// the gate failed, so a rejected step leaves params/m/v/t untouched, nn.hpp:169-171).
+// Launched cooperatively (every CTA resident), grid-stride over the parameters.
+__global__ void __launch_bounds__(256) ppo_sum_adam_kernel(GradArgs g) {
   if (g.status[0] != 0) return;
   const int tid = threadIdx.x;
-  const int p = blockIdx.x * 256 + tid;
   int bad = 0;
-  if (p < g.P) {
+  for (int p = blockIdx.x * 256 + tid; p < g.P; p += gridDim.x * 256) {
     float v[kMaxSplits];
 #pragma unroll
     for (int sp = 0; sp < kMaxSplits; ++sp) v[sp] = (sp < g.RS) ? g.partial[(size_t)sp * g.Pext + p] : 0.0f;
@@ -584,55 +595,83 @@ __global__ void __launch_bounds__(256) ppo_sum_kernel(GradArgs g) {
       if (sp < g.RS) sum += v[sp];
     if (p >= g.log_std_off && p < g.log_std_off + g.A) sum -= (float)g.ent;  // ppo.hpp:157
     g.grads[p] = sum;
-    bad = !isfinite(sum);
+    bad |= !isfinite(sum);
   }
   if (__syncthreads_or(bad) && tid == 0) atomicOr(&g.tickets[1], 1);
   __threadfence();
   __shared__ int lastall;
   if (tid == 0) lastall = (atomicAdd(&g.tickets[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
-  if (!lastall) return;
-  __threadfence();
-  // split loss sums and log_std values loaded by the block, summed by one thread in order
-  __shared__ double red[2 * kMaxSplits + 256];
-  if (tid < g.RS) {
-    red[tid] = g.partial[(size_t)tid * g.Pext + g.P];
-    red[kMaxSplits + tid] = g.partial[(size_t)tid * g.Pext + g.P + 1];
+  if (lastall) {
+    __threadfence();
+    // split loss sums and log_std values loaded by the block, summed by one thread in order
+    __shared__ double red[2 * kMaxSplits + 256];
+    if (tid < g.RS) {
+      red[tid] = g.partial[(size_t)tid * g.Pext + g.P];
+      red[kMaxSplits + tid] = g.partial[(size_t)tid * g.Pext + g.P + 1];
+    }
+    for (int dd = tid; dd < g.A && dd < 256; dd += 256) red[2 * kMaxSplits + dd] = (double)g.params[g.log_std_off + dd];
+    __syncthreads();
+    if (tid == 0) {
+      double pl = 0.0, vl = 0.0;
+      for (int sp = 0; sp < g.RS; ++sp) {
+        pl += red[sp];
+        vl += red[kMaxSplits + sp];
+      }
+      double ent = 0.0;  // policy_entropy nn.hpp:273-277
+      for (int dd = 0; dd < g.A; ++dd)
+        ent += 0.5 * (1.8378770664093454836 + 1.0) +
+               (dd < 256 ? red[2 * kMaxSplits + dd] : (double)g.params[g.log_std_off + dd]);
+      const int gbad = atomicAdd(&g.tickets[1], 0);
+      g.tickets[1] = 0;
+      if (!isfinite(pl)) {
+        g.status[0] = PRB_ERR_NUMERIC;
+        g.status[1] = 10;
+      } else if (!isfinite(vl)) {
+        g.status[0] = PRB_ERR_NUMERIC;
+        g.status[1] = 11;
+      } else if (!isfinite(ent)) {
+        g.status[0] = PRB_ERR_NUMERIC;
+        g.status[1] = 12;
+      } else if (gbad && g.apply) {
+        g.status[0] = PRB_ERR_NUMERIC;
+        g.status[1] = 1;
+      } else {
+        g.stats[0] += pl;
+        g.stats[1] += vl;
+        g.stats[2] += ent;
+        g.stats[3] += 1.0;
+        if (g.apply) *g.t += 1;
+      }
+      *g.step += 1;
+      __threadfence();
+      atomicExch(&g.tickets[0], 0);  // release the waiting CTAs
+    }
+  } else if (tid == 0) {
+    while (atomicAdd(&g.tickets[0], 0) != 0) {
+    }
   }
-  for (int dd = tid; dd < g.A && dd < 256; dd += 256) red[2 * kMaxSplits + dd] = (double)g.params[g.log_std_off + dd];
   __syncthreads();
-  if (tid != 0) return;
-  double pl = 0.0, vl = 0.0;
-  for (int sp = 0; sp < g.RS; ++sp) {
-    pl += red[sp];
-    vl += red[kMaxSplits + sp];
+  __threadfence();
+  if (!g.apply || *(volatile int32_t*)g.status != 0) return;
+  // ---- Adam on this CTA's parameters (adam_kernel's arithmetic, agent.cu) ----
+  __shared__ float sb[2];
+  if (tid == 0) {
+    const int64_t t = *(volatile int64_t*)g.t;
+    sb[0] = (float)(1.0 / (1.0 - pow(g.b1, (double)t)));
+    sb[1] = (float)(1.0 / (1.0 - pow(g.b2, (double)t)));
   }
-  double ent = 0.0;  // policy_entropy nn.hpp:273-277
-  for (int dd = 0; dd < g.A; ++dd)
-    ent += 0.5 * (1.8378770664093454836 + 1.0) + (dd < 256 ? red[2 * kMaxSplits + dd] : (double)g.params[g.log_std_off + dd]);
-  const int gbad = atomicAdd(&g.tickets[1], 0);
-  g.tickets[0] = 0;
-  g.tickets[1] = 0;
-  if (!isfinite(pl)) {
-    g.status[0] = PRB_ERR_NUMERIC;
-    g.status[1] = 10;
-  } else if (!isfinite(vl)) {
-    g.status[0] = PRB_ERR_NUMERIC;
-    g.status[1] = 11;
-  } else if (!isfinite(ent)) {
-    g.status[0] = PRB_ERR_NUMERIC;
-    g.status[1] = 12;
-  } else if (gbad && g.apply) {
-    g.status[0] = PRB_ERR_NUMERIC;
-    g.status[1] = 1;
-  } else {
-    g.stats[0] += pl;
-    g.stats[1] += vl;
-    g.stats[2] += ent;
-    g.stats[3] += 1.0;
-    if (g.apply) *g.t += 1;
+  __syncthreads();
+  const float ibc1 = sb[0], ibc2 = sb[1];
+  const float b1 = (float)g.b1, b2 = (float)g.b2, omb1 = (float)(1.0 - g.b1), omb2 = (float)(1.0 - g.b2);
+  for (int p = blockIdx.x * 256 + tid; p < g.P; p += gridDim.x * 256) {
+    const float gi = g.grads[p];
+    const float mi = b1 * g.m[p] + omb1 * gi;
+    const float vi = b2 * g.v[p] + omb2 * gi * gi;
+    g.m[p] = mi;
+    g.v[p] = vi;
+    g.p_rw[p] -= g.lr * (mi * ibc1) / (sqrtf(vi * ibc2) + g.eps);
   }
-  *g.step += 1;
 }
 
 struct PpoWorkspace {
@@ -776,8 +815,31 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   g.apply = apply;
   g.trace = ws.trace.p;
   ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
-  ppo_sum_kernel<<<(p.P + 255) / 256, 256, 0, s>>>(g);
-  if (apply) prb_adam_launch(a, a->d_grads.p, a->d_status.p, s);
+  g.p_rw = a->d_params.p;
+  g.m = a->d_m.p;
+  g.v = a->d_v.p;
+  g.lr = (float)a->lr;
+  g.eps = (float)a->eps;
+  g.b1 = a->beta1;
+  g.b2 = a->beta2;
+  static int occ = 0;
+  if (!occ) {
+    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_sum_adam_kernel, 256, 0));
+    occ = std::max(occ, 1);
+  }
+  const int sgrid = std::min((p.P + 255) / 256, a->ctx->num_sms * occ);
+  // cooperative: every CTA resident (the CTAs wait for the last one's gate)
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(sgrid);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  PRB_CUDA(cudaLaunchKernelEx(&lc, ppo_sum_adam_kernel, g));
 }
 
 std::string status_message(int detail) {
