@@ -239,13 +239,11 @@ __device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int o
 // their heads and the backward, so each CTA carries one net (half the weights to stage).
 // STAGED: the net's weights are copied to shared memory (every W access is an LDS);
 // otherwise (nets too wide for the tile) they are read from L2.
+// (bx, net) is the virtual CTA: blockIdx of ppo_fwd_delta_kernel, or a slot of the persistent kernel.
 template <bool STAGED>
-__global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
-  if (a.status[0] != 0) return;
-  extern __shared__ __align__(16) float smem[];
-  const int net = blockIdx.y;
+__device__ __forceinline__ void fwd_delta_block(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
   const MlpDesc& d = net ? a.critic : a.actor;
-  unsigned long long* tr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
+  unsigned long long* tr = (a.trace && bx == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
   int ntr = 0;
   auto mark = [&]() {
     if (tr && ntr < 16) tr[ntr++] = clock64();
@@ -253,11 +251,10 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   mark();
   Smem s;
   carve(a, net, smem, &s);
-  const int64_t step = *a.step;
   const int R = a.R;
   const int ldx = (a.S + 3) & ~3;
   const int A = a.A, ldA = (A + 3) & ~3;
-  const int q0 = blockIdx.x * R;
+  const int q0 = bx * R;
   const int nrows = min(R, a.mb - q0);
   const double mean = a.advstat[0], denom = a.advstat[1];
   if (STAGED) stage_weights(a, d, s.w);
@@ -426,6 +423,13 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   }
 }
 
+template <bool STAGED>
+__global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
+  if (a.status[0] != 0) return;
+  extern __shared__ __align__(16) float smem[];
+  fwd_delta_block<STAGED>(a, blockIdx.x, blockIdx.y, *a.step, smem);
+}
+
 // ---- ppo_grad: output-parallel dW / db / dlog_std, fixed-order sums, step gate ----
 constexpr int kGT = 64;        // output tile (k rows x j cols of [W; b])
 constexpr int kGChunk = 128;   // rows per split
@@ -465,14 +469,11 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-__global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
-  unsigned long long* tr = (g.trace && threadIdx.x == 0) ? g.trace + (size_t)blockIdx.x * 8 : nullptr;
-  if (tr) tr[0] = gtime();
-  if (g.status[0] != 0) return;
-  extern __shared__ __align__(16) float gsm[];
+// virtual CTA vb = tile * RS + split (blockIdx.x of ppo_grad_kernel, or a persistent slot)
+__device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm) {
   float* As = gsm;
   float* Bs = gsm + kGChunk * kGLd;
-  const int tile = blockIdx.x / g.RS, split = blockIdx.x % g.RS;
+  const int tile = vb / g.RS, split = vb % g.RS;
   const int4 td = g.tiles[tile];
   const int per = (g.mb + g.RS - 1) / g.RS;  // rows of this split, processed in kGChunk sub-chunks
   const int rbeg = split * per, rend = min(g.mb, rbeg + per);
@@ -569,6 +570,14 @@ __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
       part[c < g.A ? g.log_std_off + c : g.P + (c - g.A)] = acc;
     }
   }
+}
+
+__global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
+  unsigned long long* tr = (g.trace && threadIdx.x == 0) ? g.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (tr) tr[0] = gtime();
+  if (g.status[0] != 0) return;
+  extern __shared__ __align__(16) float gsm[];
+  grad_block(g, blockIdx.x, gsm);
   if (tr) tr[1] = gtime();
 }
 
@@ -674,6 +683,149 @@ __global__ void __launch_bounds__(256) ppo_sum_adam_kernel(GradArgs g) {
   }
 }
 
+// ---- persistent update: every minibatch step of a ppo_update in ONE cooperative launch ----
+// The four phases of a step are separated by grid-wide barriers instead of kernel
+// boundaries (a graph of 3 launches per minibatch spent most of its time filling and
+// draining the GPU between dependent kernels).  Per step:
+//   A  fwd_delta_block over the (mb/R) x 2 row blocks          | barrier
+//   B  grad_block over the ntiles x RS output tiles            | barrier
+//   C1 split sums -> grads (+ entropy term), non-finite flag; the CTA snapshots log_std and t
+//                                                              | barrier
+//   C2 every CTA evaluates the same gate from the same inputs (losses first, then gradients:
+//      the reference order); CTA 0 alone publishes status / stats / t; Adam on the CTA's
+//      parameter range (skipped, and the loop left by every CTA, when the gate fails)
+//                                                              | barrier
+// The arithmetic of every phase is the per-kernel path's (same device functions, same
+// reduction orders), so both paths give bit-identical parameters.
+// Monotonic arrival counter: barrier i of the launch completes when the counter reaches
+// (i+1) * nblocks.  Arrival is a release reduction, the wait an acquire load, so the
+// writes of every CTA before the barrier are visible to every CTA after it (the
+// __syncthreads on both sides extend this to the whole CTA).  No reset, no generation
+// word: the last arrival's single reduction releases everyone.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int& target, unsigned int nblocks) {
+  target += nblocks;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs a, GradArgs g, int64_t steps,
+                                                                     unsigned int* bar, int32_t* flags,
+                                                                     unsigned long long* trace) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ float s_ls[256];
+  __shared__ int64_t s_t;
+  __shared__ int s_gate;
+  __shared__ float s_bc[2];
+  const int tid = threadIdx.x;
+  const unsigned int nb = gridDim.x;
+  unsigned int bt = 0;  // barrier target
+  const int nA = (a.mb + a.R - 1) / a.R;
+  const int nB = g.ntiles * g.RS;
+  const float b1 = (float)g.b1, b2 = (float)g.b2, omb1 = (float)(1.0 - g.b1), omb2 = (float)(1.0 - g.b2);
+  // PRB_PPO_TRACE: globaltimer stamps of step 4 per CTA (phase ends and barrier exits)
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 10 : nullptr;
+  for (int64_t st = 0; st < steps; ++st) {
+    const bool mk = tr && st == (steps > 4 ? 4 : 0);
+    if (mk) tr[0] = gtime();
+    // ---- A: forward + head gradients + backward deltas, row-parallel ----
+    for (int vb = blockIdx.x; vb < 2 * nA; vb += nb) {
+      fwd_delta_block<STAGED>(a, vb % nA, vb / nA, st, smem);
+      __syncthreads();
+    }
+    if (mk) tr[1] = gtime();
+    grid_barrier(bar, bt, nb);
+    if (mk) tr[2] = gtime();
+    // ---- B: dW / db / log_std / loss split partials, output-parallel ----
+    for (int vb = blockIdx.x; vb < nB; vb += nb) {
+      grad_block(g, vb, smem);
+      __syncthreads();
+    }
+    if (mk) tr[3] = gtime();
+    grid_barrier(bar, bt, nb);
+    if (mk) tr[4] = gtime();
+    // ---- C1: split sums in split order (ppo_sum_adam_kernel's arithmetic) ----
+    int bad = 0;
+    for (int p = blockIdx.x * 256 + tid; p < g.P; p += nb * 256) {
+      float v[kMaxSplits];
+#pragma unroll
+      for (int sp = 0; sp < kMaxSplits; ++sp) v[sp] = (sp < g.RS) ? g.partial[(size_t)sp * g.Pext + p] : 0.0f;
+      float sum = 0.0f;
+#pragma unroll
+      for (int sp = 0; sp < kMaxSplits; ++sp)
+        if (sp < g.RS) sum += v[sp];
+      if (p >= g.log_std_off && p < g.log_std_off + g.A) sum -= (float)g.ent;  // ppo.hpp:157
+      g.grads[p] = sum;
+      bad |= !isfinite(sum);
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&flags[st & 1], 1);
+    for (int dd = tid; dd < g.A; dd += 256) s_ls[dd] = g.params[g.log_std_off + dd];  // before any Adam write
+    if (tid == 0) s_t = *g.t;
+    if (mk) tr[5] = gtime();
+    grid_barrier(bar, bt, nb);
+    if (mk) tr[6] = gtime();
+    // ---- C2: the step's gate, then Adam ----
+    if (tid == 0) {
+      double pl = 0.0, vl = 0.0;
+      for (int sp = 0; sp < g.RS; ++sp) {
+        pl += (double)g.partial[(size_t)sp * g.Pext + g.P];
+        vl += (double)g.partial[(size_t)sp * g.Pext + g.P + 1];
+      }
+      double ent = 0.0;  // policy_entropy nn.hpp:273-277
+      for (int dd = 0; dd < g.A; ++dd) ent += 0.5 * (1.8378770664093454836 + 1.0) + (double)s_ls[dd];
+      const int gbad = *(volatile int32_t*)&flags[st & 1];
+      int code = 0;
+      if (!isfinite(pl))
+        code = 10;
+      else if (!isfinite(vl))
+        code = 11;
+      else if (!isfinite(ent))
+        code = 12;
+      else if (gbad)
+        code = 1;
+      s_gate = code;
+      const int64_t t = s_t + 1;
+      s_bc[0] = (float)(1.0 / (1.0 - pow(g.b1, (double)t)));
+      s_bc[1] = (float)(1.0 / (1.0 - pow(g.b2, (double)t)));
+      if (blockIdx.x == 0) {
+        if (code) {
+          g.status[0] = PRB_ERR_NUMERIC;
+          g.status[1] = code;
+        } else {
+          g.stats[0] += pl;
+          g.stats[1] += vl;
+          g.stats[2] += ent;
+          g.stats[3] += 1.0;
+          *g.t = t;
+        }
+        *g.step += 1;
+        flags[(st + 1) & 1] = 0;  // next step's flag: last read before the previous barrier
+      }
+    }
+    __syncthreads();
+    if (s_gate) break;  // identical decision in every CTA
+    const float ibc1 = s_bc[0], ibc2 = s_bc[1];
+    for (int p = blockIdx.x * 256 + tid; p < g.P; p += nb * 256) {
+      const float gi = g.grads[p];
+      const float mi = b1 * g.m[p] + omb1 * gi;
+      const float vi = b2 * g.v[p] + omb2 * gi * gi;
+      g.m[p] = mi;
+      g.v[p] = vi;
+      g.p_rw[p] -= g.lr * (mi * ibc1) / (sqrtf(vi * ibc2) + g.eps);
+    }
+    if (mk) tr[7] = gtime();
+    grid_barrier(bar, bt, nb);
+    if (mk) tr[8] = gtime();
+  }
+}
+
 struct PpoWorkspace {
   DevBuf<float> partial;   // [RS][Pext] split partials of the gradient GEMMs
   DevBuf<float> slab;      // per-row layer inputs / deltas of one minibatch
@@ -684,6 +836,8 @@ struct PpoWorkspace {
   DevBuf<double> stats;
   DevBuf<uint32_t> perm;
   DevBuf<unsigned long long> trace;  // PRB_PPO_TRACE
+  DevBuf<int32_t> bar;               // persistent update: grid barrier + non-finite flags
+  DevBuf<unsigned long long> ptrace; // PRB_PPO_TRACE of the persistent update: [grid][10]
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -730,6 +884,7 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   // rows per CTA: as many CTAs as possible while every CTA keeps >= 8 rows
   p.R = 8;
   while (p.R < 64 && (size_t)(mb / (p.R * 2)) >= (size_t)a->ctx->num_sms) p.R *= 2;
+  if (const char* rv = getenv("PRB_PPO_R")) p.R = std::max(8, std::min(64, atoi(rv)));  // A/B knob
   p.stage = 1;
   if (carve_max(p) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
   while (p.R > 8 && carve_max(p) > kSmemBudget) p.R /= 2;
@@ -778,15 +933,7 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   return p;
 }
 
-void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
-  const dim3 grid((p.mb + p.R - 1) / p.R, 2);
-  PpoArgs pt = p;
-  pt.trace = ws.trace.p ? ws.trace.p + (size_t)ws.ntiles * ws.RS * 8 : nullptr;
-  const size_t smem = carve_max(p);
-  if (p.stage)
-    ppo_fwd_delta_kernel<true><<<grid, kPpoThreads, smem, s>>>(pt);
-  else
-    ppo_fwd_delta_kernel<false><<<grid, kPpoThreads, smem, s>>>(pt);  // steps run inside CUDA graphs: no event scopes
+GradArgs make_grad_args(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply) {
   GradArgs g;
   g.slab = p.slab;
   std::memcpy(g.hin_off, p.hin_off, sizeof(g.hin_off));
@@ -814,7 +961,6 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   g.stats = ws.stats.p;
   g.apply = apply;
   g.trace = ws.trace.p;
-  ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
   g.p_rw = a->d_params.p;
   g.m = a->d_m.p;
   g.v = a->d_v.p;
@@ -822,6 +968,24 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   g.eps = (float)a->eps;
   g.b1 = a->beta1;
   g.b2 = a->beta2;
+  return g;
+}
+
+void launch_coop(const void* fn, int grid, size_t smem, cudaStream_t s, void** args) {
+  PRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, smem, s));
+}
+
+void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int apply, cudaStream_t s) {
+  const dim3 grid((p.mb + p.R - 1) / p.R, 2);
+  PpoArgs pt = p;
+  pt.trace = ws.trace.p ? ws.trace.p + (size_t)ws.ntiles * ws.RS * 8 : nullptr;
+  const size_t smem = carve_max(p);
+  if (p.stage)
+    ppo_fwd_delta_kernel<true><<<grid, kPpoThreads, smem, s>>>(pt);
+  else
+    ppo_fwd_delta_kernel<false><<<grid, kPpoThreads, smem, s>>>(pt);  // steps run inside CUDA graphs: no event scopes
+  GradArgs g = make_grad_args(p, a, ws, ent, apply);
+  ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
   static int occ = 0;
   if (!occ) {
     PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_sum_adam_kernel, 256, 0));
@@ -829,17 +993,51 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   }
   const int sgrid = std::min((p.P + 255) / 256, a->ctx->num_sms * occ);
   // cooperative: every CTA resident (the CTAs wait for the last one's gate)
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(sgrid);
-  lc.blockDim = dim3(256);
-  lc.dynamicSmemBytes = 0;
-  lc.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  PRB_CUDA(cudaLaunchKernelEx(&lc, ppo_sum_adam_kernel, g));
+  void* args[] = {&g};
+  launch_coop((const void*)ppo_sum_adam_kernel, sgrid, 0, s, args);
+}
+
+size_t persistent_smem(const PpoArgs& p) {
+  return std::max(carve_max(p), (size_t)(2 * kGChunk * kGLd * sizeof(float)));
+}
+
+// Grid of the persistent update (0: not launchable -> per-kernel path).
+int persistent_grid(const PpoArgs& p, prb_agent a, const PpoWorkspace& ws) {
+  if (p.A > 256 || getenv("PRB_PPO_GRAPH")) return 0;  // PRB_PPO_GRAPH: force the per-kernel path (A/B)
+  const size_t smem = persistent_smem(p);
+  int occ = 0;
+  if (p.stage)
+    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_persistent_kernel<true>, kPpoThreads, smem));
+  else
+    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_persistent_kernel<false>, kPpoThreads, smem));
+  if (occ < 1) return 0;
+  const int work = std::max(2 * ((p.mb + p.R - 1) / p.R), ws.ntiles * ws.RS);
+  return std::min(work, a->ctx->num_sms * occ);
+}
+
+void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, int64_t steps, int grid,
+                       cudaStream_t s) {
+  PpoArgs pa = p;
+  pa.trace = nullptr;
+  GradArgs g = make_grad_args(p, a, ws, ent, 1);
+  g.trace = nullptr;
+  ws.bar.alloc(4);  // [0] barrier arrivals, [1] unused, [2..3] per-step non-finite flags
+  PRB_CUDA(cudaMemsetAsync(ws.bar.p, 0, ws.bar.bytes(), s));
+  unsigned int* bar = reinterpret_cast<unsigned int*>(ws.bar.p);
+  int32_t* flags = ws.bar.p + 2;
+  unsigned long long* trace = nullptr;
+  if (getenv("PRB_PPO_TRACE")) {  // [grid][10] phase stamps, then fwd_delta_block's 2 x 16 clock64 marks
+    ws.ptrace.alloc((size_t)grid * 10 + 32);
+    PRB_CUDA(cudaMemsetAsync(ws.ptrace.p, 0, ws.ptrace.bytes(), s));
+    trace = ws.ptrace.p;
+    pa.trace = ws.ptrace.p + (size_t)grid * 10;
+  }
+  void* args[] = {&pa, &g, &steps, &bar, &flags, &trace};
+  const size_t smem = persistent_smem(p);
+  if (p.stage)
+    launch_coop((const void*)ppo_persistent_kernel<true>, grid, smem, s, args);
+  else
+    launch_coop((const void*)ppo_persistent_kernel<false>, grid, smem, s, args);
 }
 
 std::string status_message(int detail) {
@@ -871,6 +1069,10 @@ void set_smem_attr() {
                                   (int)kSmemBudget));
     PRB_CUDA(cudaFuncSetAttribute(ppo_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(2 * kGChunk * kGLd * sizeof(float))));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBudget));
+    PRB_CUDA(cudaFuncSetAttribute(ppo_persistent_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBudget));
     done = true;
   }
 }
@@ -940,7 +1142,11 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     // Minibatch steps are identical launches (the counter is on device):
     // capture a block of them once as a CUDA graph and replay it.
     const size_t kGraphSteps = 32;
-    if (steps >= kGraphSteps) {
+    const int pgrid = persistent_grid(p, dst, ws);
+    if (pgrid > 0 && steps > 0) {
+      launch_persistent(p, dst, ws, cfg->entropy_coef, (int64_t)steps, pgrid, s);
+      PRB_CUDA(cudaStreamSynchronize(s));
+    } else if (steps >= kGraphSteps) {
       cudaGraph_t graph;
       cudaGraphExec_t exec;
       PRB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -957,8 +1163,9 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     }
     PRB_CHECK_LAUNCH();
     if (const char* tp = getenv("PRB_PPO_TRACE")) {  // debug: globaltimer marks of the last step's ppo_grad CTAs
-      std::vector<unsigned long long> h(ws.trace.n);
-      PRB_CUDA(cudaMemcpy(h.data(), ws.trace.p, ws.trace.bytes(), cudaMemcpyDeviceToHost));
+      DevBuf<unsigned long long>& tb = ws.ptrace.p ? ws.ptrace : ws.trace;  // persistent: [grid][10] stamps
+      std::vector<unsigned long long> h(tb.n);
+      PRB_CUDA(cudaMemcpy(h.data(), tb.p, tb.bytes(), cudaMemcpyDeviceToHost));
       if (FILE* f = fopen(tp, "wb")) {
         fwrite(h.data(), 8, h.size(), f);
         fclose(f);

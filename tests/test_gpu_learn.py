@@ -306,6 +306,49 @@ def test_ppo_update_properties(pr, ctx):
         pr.ppo_update(agent, pr.Rollout.raw(ctx, N, H, S, A), cfg, 1)  # buffer must be full (:281-289)
 
 
+@pytest.mark.parametrize("S,A,hid,N,H,mb,epochs", [(181, 30, (64, 64), 64, 64, 1024, 2),
+                                                    (6, 2, (256, 256, 256), 16, 32, 256, 1),
+                                                    (11, 3, (8, 8), 9, 13, 37, 3)])
+def test_ppo_update_persistent_equals_per_kernel_path(pr, ctx, S, A, hid, N, H, mb, epochs, monkeypatch):
+    """The persistent cooperative update (one launch, grid barriers between phases) runs the
+    per-kernel path's device functions in the same reduction orders: bit-identical results."""
+    rng = np.random.default_rng(S + mb)
+    agent = pr.Agent.init(ctx, S, A, seed=3, hidden=hid)
+    ro, _ = _upload_random_buffer(pr, ctx, rng, N, H, S, A)
+    cfg = pr.PpoConfig(epochs_per_update=epochs, minibatch_size=mb, buffer_size=N * H)
+    a1, s1 = pr.ppo_update(agent, ro, cfg, 21)
+    monkeypatch.setenv("PRB_PPO_GRAPH", "1")
+    a2, s2 = pr.ppo_update(agent, ro, cfg, 21)
+    monkeypatch.delenv("PRB_PPO_GRAPH")
+    p1, m1, v1, t1 = a1.get()
+    p2, m2, v2, t2 = a2.get()
+    assert t1 == t2 == epochs * ((N * H) // mb) and s1.minibatches == s2.minibatches == t1
+    assert np.array_equal(p1, p2) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    assert s1.mean_policy_loss == s2.mean_policy_loss and s1.mean_value_loss == s2.mean_value_loss
+    assert s1.mean_entropy == s2.mean_entropy
+
+
+def test_ppo_update_nonfinite_gate_leaves_state(pr, ctx):
+    """A non-finite loss aborts the update at the first step in both paths and names the
+    component (ppo.hpp:169-171); the returned error leaves the source agent untouched."""
+    S, A, hid, N, H = 6, 2, (8, 8), 8, 16
+    rng = np.random.default_rng(4)
+    agent = pr.Agent.init(ctx, S, A, seed=5, hidden=hid)
+    ro, buf = _upload_random_buffer(pr, ctx, rng, N, H, S, A)
+    bad = buf["rewards"].copy(); bad[5] = np.inf
+    ro.upload(buf["states"], buf["actions"], buf["log_probs"], bad, buf["dones"], buf["values"], buf["bootstrap"])
+    cfg = pr.PpoConfig(epochs_per_update=2, minibatch_size=32, buffer_size=N * H)
+    before = agent.flatten_params().copy()
+    with pytest.raises(pr.NumericError):
+        pr.ppo_update(agent, ro, cfg, 3)
+    assert np.array_equal(agent.flatten_params(), before)
+    # the agent and the context stay usable afterwards
+    ro.upload(buf["states"], buf["actions"], buf["log_probs"], buf["rewards"], buf["dones"], buf["values"],
+              buf["bootstrap"])
+    new, st = pr.ppo_update(agent, ro, cfg, 3)
+    assert st.minibatches == 2 * (N * H // 32) and np.all(np.isfinite(new.flatten_params()))
+
+
 def test_fuse_parity(pr, ctx, orc):
     S, A, hid = 5, 2, (4,)
     rng = np.random.default_rng(12)
