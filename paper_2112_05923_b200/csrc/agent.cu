@@ -176,11 +176,15 @@ int prb_agent_create(prb_ctx ctx, size_t S, size_t A, const size_t* hidden, int 
     a->d_grads.alloc(a->P);
     a->d_t.alloc(1);
     a->d_status.alloc(4);
-    PRB_CUDA(cudaMemset(a->d_params.p, 0, a->d_params.bytes()));
-    PRB_CUDA(cudaMemset(a->d_m.p, 0, a->d_m.bytes()));
-    PRB_CUDA(cudaMemset(a->d_v.p, 0, a->d_v.bytes()));
-    PRB_CUDA(cudaMemset(a->d_t.p, 0, sizeof(int64_t)));
-    PRB_CUDA(cudaMemset(a->d_status.p, 0, 4 * sizeof(int32_t)));
+    // on the agent's (non-blocking) stream, then waited: a legacy-stream cudaMemset would not be
+    // ordered with work the caller enqueues on any context stream afterwards
+    cudaStream_t s = a->ctx->stream;
+    PRB_CUDA(cudaMemsetAsync(a->d_params.p, 0, a->d_params.bytes(), s));
+    PRB_CUDA(cudaMemsetAsync(a->d_m.p, 0, a->d_m.bytes(), s));
+    PRB_CUDA(cudaMemsetAsync(a->d_v.p, 0, a->d_v.bytes(), s));
+    PRB_CUDA(cudaMemsetAsync(a->d_t.p, 0, sizeof(int64_t), s));
+    PRB_CUDA(cudaMemsetAsync(a->d_status.p, 0, 4 * sizeof(int32_t), s));
+    PRB_CUDA(cudaStreamSynchronize(s));
     *out = a;
   });
 }

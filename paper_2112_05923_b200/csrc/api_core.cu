@@ -289,7 +289,9 @@ int prb_market_create(prb_ctx ctx, const double* close, const double* indicators
     for (int k = 0; k < K; ++k)
       for (size_t t = 0; t < T; ++t) tk[t * K + k] = close[(size_t)k * T + t];
     m->d_close_tk.alloc(tk.size());
-    PRB_CUDA(cudaMemcpy(m->d_close_tk.p, tk.data(), tk.size() * sizeof(double), cudaMemcpyHostToDevice));
+    PRB_CUDA(cudaMemcpyAsync(m->d_close_tk.p, tk.data(), tk.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             m->ctx->stream));
+    PRB_CUDA(cudaStreamSynchronize(m->ctx->stream));  // creation-time: visible to every stream
     *out = m;
   });
 }

@@ -808,12 +808,14 @@ int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t st
         for (int k = 0; k < K; ++k) feat[t * F + K + (size_t)i * K + k] = (float)m->indicators[((size_t)i * K + k) * T + t];
     }
     env->d_feat.alloc(feat.size());
-    PRB_CUDA(cudaMemcpy(env->d_feat.p, feat.data(), feat.size() * sizeof(float), cudaMemcpyHostToDevice));
+    PRB_CUDA(cudaMemcpyAsync(env->d_feat.p, feat.data(), feat.size() * sizeof(float), cudaMemcpyHostToDevice,
+                             env->ctx->stream));
     env->d_balance.alloc(N);
     env->d_shares.alloc(N * K);
     env->d_ep_return.alloc(N);
     env->d_obs.alloc(N * env->S);
-    PRB_CUDA(cudaMemset(env->d_obs.p, 0, env->d_obs.bytes()));
+    PRB_CUDA(cudaMemsetAsync(env->d_obs.p, 0, env->d_obs.bytes(), env->ctx->stream));
+    PRB_CUDA(cudaStreamSynchronize(env->ctx->stream));  // creation-time: visible to every stream
     *out = env;
   });
 }
@@ -840,7 +842,8 @@ int prb_vecenv_create_pointmass(prb_ctx ctx, size_t N, prb_vecenv* out) {
     env->d_mt.alloc((size_t)kMtN * N);
     env->d_mt_idx.alloc(N);
     env->d_obs.alloc(N * 6);
-    PRB_CUDA(cudaMemset(env->d_obs.p, 0, env->d_obs.bytes()));
+    PRB_CUDA(cudaMemsetAsync(env->d_obs.p, 0, env->d_obs.bytes(), env->ctx->stream));
+    PRB_CUDA(cudaStreamSynchronize(env->ctx->stream));  // creation-time: visible to every stream
     *out = env;
   });
 }

@@ -207,12 +207,13 @@ __device__ __forceinline__ void stage_wait() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-// rows [q0, q0+nrows) of a [mb][w] slab array <- smem tile s (row stride lds)
+// rows [q0, q0+nrows) of a [mb][round4(w)] slab array <- smem tile s (row stride lds); the
+// padding columns are never written (zero since allocation)
 __device__ __forceinline__ void store_rows_g(float* __restrict__ g, int w, const float* s, int lds, int nrows, int q0) {
-  const int n = nrows * w;
+  const int n = nrows * w, gld = (w + 3) & ~3;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int r = i / w, c = i - r * w;
-    g[(size_t)(q0 + r) * w + c] = s[r * lds + c];
+    g[(size_t)(q0 + r) * gld + c] = s[r * lds + c];
   }
 }
 
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
 
 // ---- ppo_grad: output-parallel dW / db / dlog_std, fixed-order sums, step gate ----
 constexpr int kGT = 64;        // output tile (k rows x j cols of [W; b])
-constexpr int kGChunk = 128;   // rows per split
+constexpr int kGChunk = 64;    // rows per sub-chunk of a split (one float4 load round)
 constexpr int kGLd = kGT + 4;  // smem row stride (float4-aligned)
 constexpr int kMaxSplits = 16;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
 constexpr int kGRows = 64;      // target rows per split
@@ -496,24 +497,26 @@ __device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm
     for (int r0 = rbeg; r0 < rend; r0 += kGChunk) {
       const int nr = min(kGChunk, rend - r0);
       __syncthreads();  // previous sub-chunk consumed
-      // 8 rows per thread per pass, all 16 loads in flight before the stores
-      const int c = tid % kGT, k = k0 + c, j = j0 + c;
-      for (int rb = tid / kGT; rb < nr; rb += 8 * (256 / kGT)) {
-        float av[8], bv[8];
+      // float4 columns (slab rows are padded to a multiple of 4 floats, the padding zero):
+      // 16 float4 per 64-wide tile row, 16 rows per pass, every load of the sub-chunk in
+      // flight before the first store
+      const int c4 = tid & 15, rr = tid >> 4;
+      const int k = k0 + 4 * c4, j = j0 + 4 * c4;
+      const int ldh = (in + 3) & ~3, ldd = (out + 3) & ~3;
+      float4 av[kGChunk / 16], bv[kGChunk / 16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int r = rb + u * (256 / kGT);
-          const size_t row = (size_t)(r0 + r);
-          av[u] = (r < nr && k < in) ? H[row * in + k] : 0.0f;
-          bv[u] = (r < nr && j < out) ? D[row * out + j] : 0.0f;
-        }
+      for (int u = 0; u < kGChunk / 16; ++u) {
+        const int r = rr + 16 * u;
+        const size_t row = (size_t)(r0 + r);
+        av[u] = (r < nr && k < in) ? *reinterpret_cast<const float4*>(H + row * ldh + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[u] = (r < nr && j < out) ? *reinterpret_cast<const float4*>(D + row * ldd + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int r = rb + u * (256 / kGT);
-          if (r < nr) {
-            As[r * kGLd + c] = av[u];
-            Bs[r * kGLd + c] = bv[u];
-          }
+      for (int u = 0; u < kGChunk / 16; ++u) {
+        const int r = rr + 16 * u;
+        if (r < nr) {
+          *reinterpret_cast<float4*>(As + r * kGLd + 4 * c4) = av[u];
+          *reinterpret_cast<float4*>(Bs + r * kGLd + 4 * c4) = bv[u];
         }
       }
       __syncthreads();
@@ -557,7 +560,7 @@ __device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm
     const float* LO = g.slab + g.loss_off;
     for (int c = tid; c < g.A + 2; c += 256) {
       const float* src = (c < g.A) ? LS + c : LO + (c - g.A);
-      const int ld = (c < g.A) ? g.A : 2;
+      const int ld = (c < g.A) ? ((g.A + 3) & ~3) : 2;  // log_std rows padded like every slab array
       float acc = 0.0f;
       for (int r = rbeg; r < rend; r += 16) {  // 16 loads in flight, summed in row order
         float v[16];
@@ -718,20 +721,31 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int& 
 template <bool STAGED>
 __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs a, GradArgs g, int64_t steps,
                                                                      unsigned int* bar, int32_t* flags,
-                                                                     unsigned long long* trace) {
+                                                                     float2* bias_tab, unsigned long long* trace) {
   extern __shared__ __align__(16) float smem[];
   __shared__ float s_ls[256];
-  __shared__ int64_t s_t;
-  __shared__ int s_gate;
-  __shared__ float s_bc[2];
+  __shared__ double s_lsum[2 * kMaxSplits];
+  __shared__ int s_lcode;
+  __shared__ double s_loss[3];
   const int tid = threadIdx.x;
   const unsigned int nb = gridDim.x;
   unsigned int bt = 0;  // barrier target
   const int nA = (a.mb + a.R - 1) / a.R;
   const int nB = g.ntiles * g.RS;
   const float b1 = (float)g.b1, b2 = (float)g.b2, omb1 = (float)(1.0 - g.b1), omb2 = (float)(1.0 - g.b2);
+  // Adam bias corrections of every step, computed once up front (adam_kernel's fp64 pow):
+  // step st runs with t = t0 + st + 1 (a failed gate ends the update, so t never skips)
+  {
+    const int64_t t0 = *g.t;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + tid; i < steps; i += (int64_t)nb * 256) {
+      const double t = (double)(t0 + i + 1);
+      bias_tab[i] = make_float2((float)(1.0 / (1.0 - pow(g.b1, t))), (float)(1.0 / (1.0 - pow(g.b2, t))));
+    }
+  }
+  grid_barrier(bar, bt, nb);
   // PRB_PPO_TRACE: globaltimer stamps of step 4 per CTA (phase ends and barrier exits)
   unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 10 : nullptr;
+  const int p0 = blockIdx.x * 256 + tid;  // this thread's first parameter (its Adam update is kept in registers)
   for (int64_t st = 0; st < steps; ++st) {
     const bool mk = tr && st == (steps > 4 ? 4 : 0);
     if (mk) tr[0] = gtime();
@@ -751,9 +765,23 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
     if (mk) tr[3] = gtime();
     grid_barrier(bar, bt, nb);
     if (mk) tr[4] = gtime();
-    // ---- C1: split sums in split order (ppo_sum_adam_kernel's arithmetic) ----
+    // ---- C1: split sums in split order (ppo_sum_adam_kernel's arithmetic), the loss half of
+    // the gate, and this thread's first Adam update computed speculatively ----
+    const float2 bc = bias_tab[st];
+    float np0 = 0.f, nm0 = 0.f, nv0 = 0.f;
+    float m0 = 0.f, v0 = 0.f, w0 = 0.f;
+    if (p0 < g.P) {  // issued with the partial loads below
+      m0 = g.m[p0];
+      v0 = g.v[p0];
+      w0 = g.p_rw[p0];
+    }
+    if (tid >= 32 && tid < 32 + g.RS) {  // loss split sums (gate inputs)
+      s_lsum[tid - 32] = (double)g.partial[(size_t)(tid - 32) * g.Pext + g.P];
+      s_lsum[kMaxSplits + tid - 32] = (double)g.partial[(size_t)(tid - 32) * g.Pext + g.P + 1];
+    }
+    for (int dd = tid; dd < g.A; dd += 256) s_ls[dd] = g.params[g.log_std_off + dd];  // before any Adam write
     int bad = 0;
-    for (int p = blockIdx.x * 256 + tid; p < g.P; p += nb * 256) {
+    for (int p = p0; p < g.P; p += nb * 256) {
       float v[kMaxSplits];
 #pragma unroll
       for (int sp = 0; sp < kMaxSplits; ++sp) v[sp] = (sp < g.RS) ? g.partial[(size_t)sp * g.Pext + p] : 0.0f;
@@ -762,63 +790,62 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       for (int sp = 0; sp < kMaxSplits; ++sp)
         if (sp < g.RS) sum += v[sp];
       if (p >= g.log_std_off && p < g.log_std_off + g.A) sum -= (float)g.ent;  // ppo.hpp:157
-      g.grads[p] = sum;
       bad |= !isfinite(sum);
+      if (p == p0) {
+        nm0 = b1 * m0 + omb1 * sum;
+        nv0 = b2 * v0 + omb2 * sum * sum;
+        np0 = w0 - g.lr * (nm0 * bc.x) / (sqrtf(nv0 * bc.y) + g.eps);
+      } else {
+        g.grads[p] = sum;
+      }
     }
     if (__syncthreads_or(bad) && tid == 0) atomicOr(&flags[st & 1], 1);
-    for (int dd = tid; dd < g.A; dd += 256) s_ls[dd] = g.params[g.log_std_off + dd];  // before any Adam write
-    if (tid == 0) s_t = *g.t;
-    if (mk) tr[5] = gtime();
-    grid_barrier(bar, bt, nb);
-    if (mk) tr[6] = gtime();
-    // ---- C2: the step's gate, then Adam ----
-    if (tid == 0) {
+    if (tid == 0) {  // losses first (the reference order); gradients after the barrier
       double pl = 0.0, vl = 0.0;
       for (int sp = 0; sp < g.RS; ++sp) {
-        pl += (double)g.partial[(size_t)sp * g.Pext + g.P];
-        vl += (double)g.partial[(size_t)sp * g.Pext + g.P + 1];
+        pl += s_lsum[sp];
+        vl += s_lsum[kMaxSplits + sp];
       }
       double ent = 0.0;  // policy_entropy nn.hpp:273-277
       for (int dd = 0; dd < g.A; ++dd) ent += 0.5 * (1.8378770664093454836 + 1.0) + (double)s_ls[dd];
-      const int gbad = *(volatile int32_t*)&flags[st & 1];
-      int code = 0;
-      if (!isfinite(pl))
-        code = 10;
-      else if (!isfinite(vl))
-        code = 11;
-      else if (!isfinite(ent))
-        code = 12;
-      else if (gbad)
-        code = 1;
-      s_gate = code;
-      const int64_t t = s_t + 1;
-      s_bc[0] = (float)(1.0 / (1.0 - pow(g.b1, (double)t)));
-      s_bc[1] = (float)(1.0 / (1.0 - pow(g.b2, (double)t)));
-      if (blockIdx.x == 0) {
-        if (code) {
-          g.status[0] = PRB_ERR_NUMERIC;
-          g.status[1] = code;
-        } else {
-          g.stats[0] += pl;
-          g.stats[1] += vl;
-          g.stats[2] += ent;
-          g.stats[3] += 1.0;
-          *g.t = t;
-        }
-        *g.step += 1;
-        flags[(st + 1) & 1] = 0;  // next step's flag: last read before the previous barrier
-      }
+      s_lcode = !isfinite(pl) ? 10 : (!isfinite(vl) ? 11 : (!isfinite(ent) ? 12 : 0));
+      s_loss[0] = pl;
+      s_loss[1] = vl;
+      s_loss[2] = ent;
     }
-    __syncthreads();
-    if (s_gate) break;  // identical decision in every CTA
-    const float ibc1 = s_bc[0], ibc2 = s_bc[1];
-    for (int p = blockIdx.x * 256 + tid; p < g.P; p += nb * 256) {
+    if (mk) tr[5] = gtime();
+    grid_barrier(bar, bt, nb);
+    if (mk) tr[6] = gtime();
+    // ---- C2: the gate (identical in every CTA), then Adam: the first parameter from
+    // registers, any further ones (wide nets) recomputed from grads ----
+    const int code = s_lcode ? s_lcode : (*(volatile int32_t*)&flags[st & 1] ? 1 : 0);
+    if (blockIdx.x == 0 && tid == 0) {
+      if (code) {
+        g.status[0] = PRB_ERR_NUMERIC;
+        g.status[1] = code;
+      } else {
+        g.stats[0] += s_loss[0];
+        g.stats[1] += s_loss[1];
+        g.stats[2] += s_loss[2];
+        g.stats[3] += 1.0;
+        *g.t += 1;
+      }
+      *g.step += 1;
+      flags[(st + 1) & 1] = 0;  // next step's flag: last read before the previous barrier
+    }
+    if (code) break;  // identical decision in every CTA
+    if (p0 < g.P) {
+      g.m[p0] = nm0;
+      g.v[p0] = nv0;
+      g.p_rw[p0] = np0;
+    }
+    for (int p = p0 + nb * 256; p < g.P; p += nb * 256) {
       const float gi = g.grads[p];
       const float mi = b1 * g.m[p] + omb1 * gi;
       const float vi = b2 * g.v[p] + omb2 * gi * gi;
       g.m[p] = mi;
       g.v[p] = vi;
-      g.p_rw[p] -= g.lr * (mi * ibc1) / (sqrtf(vi * ibc2) + g.eps);
+      g.p_rw[p] -= g.lr * (mi * bc.x) / (sqrtf(vi * bc.y) + g.eps);
     }
     if (mk) tr[7] = gtime();
     grid_barrier(bar, bt, nb);
@@ -837,6 +864,7 @@ struct PpoWorkspace {
   DevBuf<uint32_t> perm;
   DevBuf<unsigned long long> trace;  // PRB_PPO_TRACE
   DevBuf<int32_t> bar;               // persistent update: grid barrier + non-finite flags
+  DevBuf<float2> bias;               // persistent update: Adam bias corrections per step
   DevBuf<unsigned long long> ptrace; // PRB_PPO_TRACE of the persistent update: [grid][10]
 };
 
@@ -897,15 +925,17 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
     PRB_REQUIRE(off < ((size_t)1 << 31), PRB_ERR_CONFIG, "ppo: minibatch slab too large");
     return (int)o;
   };
-  p.hin_off[0][0] = p.hin_off[1][0] = take((size_t)p.S);
+  auto r4 = [](size_t w) { return (w + 3) & ~size_t(3); };  // float4-aligned rows for ppo_grad's loads
+  p.hin_off[0][0] = p.hin_off[1][0] = take(r4((size_t)p.S));
   for (int net = 0; net < 2; ++net) {
     const MlpDesc& d = net ? p.critic : p.actor;
-    for (int l = 1; l < d.nl; ++l) p.hin_off[net][l] = take((size_t)d.dims[l]);
-    for (int l = 0; l < d.nl; ++l) p.del_off[net][l] = take((size_t)d.dims[l + 1]);
+    for (int l = 1; l < d.nl; ++l) p.hin_off[net][l] = take(r4((size_t)d.dims[l]));
+    for (int l = 0; l < d.nl; ++l) p.del_off[net][l] = take(r4((size_t)d.dims[l + 1]));
   }
-  p.ls_off = take((size_t)p.A);
-  p.loss_off = take(2);
-  if (ws.slab.n < off) ws.slab.alloc(off);
+  p.ls_off = take(r4((size_t)p.A));
+  p.loss_off = take(r4(2));
+  ws.slab.ensure(off);
+  PRB_CUDA(cudaMemsetAsync(ws.slab.p, 0, ws.slab.bytes(), a->ctx->stream));  // row padding stays zero
   p.slab = ws.slab.p;
   // gradient tiles: every [W_l; b_l] of both nets in 64x64 output tiles, plus log_std + losses
   std::vector<int4> tiles;
@@ -918,15 +948,18 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   tiles.push_back(make_int4(0, -1, 0, 0));
   ws.ntiles = (int)tiles.size();
   ws.RS = std::min(kMaxSplits, (mb + kGRows - 1) / kGRows);
-  ws.tiles.alloc(tiles.size());
-  PRB_CUDA(cudaMemcpy(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  ws.tickets.alloc(2);  // [0] completed-CTA counter of ppo_sum, [1] gradient non-finite flag
+  ws.tiles.ensure(tiles.size());
+  // every setup copy/memset on the stream the kernels run on (the context stream is
+  // non-blocking: legacy-stream cudaMemset/cudaMemcpy would not be ordered with them)
+  PRB_CUDA(cudaMemcpyAsync(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                           a->ctx->stream));
+  ws.tickets.ensure(2);  // [0] completed-CTA counter of ppo_sum, [1] gradient non-finite flag
   if (getenv("PRB_PPO_TRACE")) {
     ws.trace.alloc((size_t)ws.ntiles * ws.RS * 8 + 32);
-    PRB_CUDA(cudaMemset(ws.trace.p, 0, ws.trace.bytes()));
+    PRB_CUDA(cudaMemsetAsync(ws.trace.p, 0, ws.trace.bytes(), a->ctx->stream));
   }
-  PRB_CUDA(cudaMemset(ws.tickets.p, 0, ws.tickets.bytes()));
-  if (ws.partial.n < (size_t)ws.RS * p.Pext) ws.partial.alloc((size_t)ws.RS * p.Pext);
+  PRB_CUDA(cudaMemsetAsync(ws.tickets.p, 0, ws.tickets.bytes(), a->ctx->stream));
+  ws.partial.ensure((size_t)ws.RS * p.Pext);
   if (!ws.step.p) ws.step.alloc(1);
   if (!ws.stats.p) ws.stats.alloc(4);
   p.step = ws.step.p;
@@ -1021,7 +1054,7 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   pa.trace = nullptr;
   GradArgs g = make_grad_args(p, a, ws, ent, 1);
   g.trace = nullptr;
-  ws.bar.alloc(4);  // [0] barrier arrivals, [1] unused, [2..3] per-step non-finite flags
+  ws.bar.ensure(4);  // [0] barrier arrivals, [1] unused, [2..3] per-step non-finite flags
   PRB_CUDA(cudaMemsetAsync(ws.bar.p, 0, ws.bar.bytes(), s));
   unsigned int* bar = reinterpret_cast<unsigned int*>(ws.bar.p);
   int32_t* flags = ws.bar.p + 2;
@@ -1032,7 +1065,9 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
     trace = ws.ptrace.p;
     pa.trace = ws.ptrace.p + (size_t)grid * 10;
   }
-  void* args[] = {&pa, &g, &steps, &bar, &flags, &trace};
+  ws.bias.ensure((size_t)steps);
+  float2* bias_tab = ws.bias.p;
+  void* args[] = {&pa, &g, &steps, &bar, &flags, &bias_tab, &trace};
   const size_t smem = persistent_smem(p);
   if (p.stage)
     launch_coop((const void*)ppo_persistent_kernel<true>, grid, smem, s, args);
@@ -1126,13 +1161,15 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     if (r->ctx->stream != s) r->ctx->sync();
     r->gae_valid = true;
     r->normalized = true;
-    PpoWorkspace ws;
+    if (!dst->ppo_ws)  // device workspace kept with the agent: no cudaMalloc/cudaFree per update
+      dst->ppo_ws = std::shared_ptr<void>(new PpoWorkspace, [](void* w) { delete static_cast<PpoWorkspace*>(w); });
+    PpoWorkspace& ws = *static_cast<PpoWorkspace*>(dst->ppo_ws.get());
     const int mb = (int)cfg->minibatch_size;
     PpoArgs p = make_args(dst, r, cfg, seed, ws, mb);
     const size_t steps = (size_t)cfg->epochs_per_update * p.nmb;
     if (perm) {
       std::vector<uint32_t> dev = ref_rows_to_device(r, perm, (size_t)cfg->epochs_per_update * n);
-      ws.perm.alloc(dev.size());
+      ws.perm.ensure(dev.size());
       PRB_CUDA(cudaMemcpyAsync(ws.perm.p, dev.data(), dev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
       p.perm = ws.perm.p;
       dst->ctx->sync();
@@ -1217,7 +1254,8 @@ int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows, size_t 
       losses[2] = sums[2];
     }
     if (st[0] != 0) {
-      PRB_CUDA(cudaMemset(a->d_status.p, 0, 4 * sizeof(int32_t)));
+      PRB_CUDA(cudaMemsetAsync(a->d_status.p, 0, 4 * sizeof(int32_t), a->ctx->stream));
+      a->ctx->sync();
       fail(st[0], status_message(st[1]));
     }
     if (grads) {

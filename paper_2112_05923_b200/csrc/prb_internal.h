@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/prb.h"
@@ -76,6 +77,9 @@ struct DevBuf {
     n = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
+  void ensure(size_t count) {  // grow-only (keeps the allocation across calls)
+    if (n < count) alloc(count);
+  }
 };
 
 uint64_t splitmix64(uint64_t x);
@@ -193,6 +197,7 @@ struct prb_agent_s {
   prb::DevBuf<float> d_params, d_m, d_v, d_grads;
   prb::DevBuf<int64_t> d_t;          // Adam step counter (device-resident)
   prb::DevBuf<int32_t> d_status;     // [0]=error code raised on device, [1]=detail
+  std::shared_ptr<void> ppo_ws;      // ppo.cu workspace, kept across prb_ppo_update calls
 };
 
 // Device TransitionBuffer (buffer.hpp:27-135), TIME-MAJOR: transition
