@@ -68,6 +68,7 @@ struct PpoArgs {
   int mb;             // minibatch rows
   int R;              // rows per CTA
   int stage;          // 1: weights staged in shared memory (ld = out + 1)
+  int r8;             // 1: the rows-of-8 path (fwd_delta_r8): staged [W;b], warp-split reductions
   const int64_t* step;  // device minibatch counter (epoch = step / nmb)
   double clip, ent, vf;
   int32_t* status;
@@ -106,11 +107,22 @@ __device__ __forceinline__ uint32_t mb_row(const PpoArgs& a, int64_t step, uint3
 }
 
 // floats of one net's staged weight set: every layer at row stride out+1
-__host__ __device__ inline size_t staged_floats(const MlpDesc& d) {
+// rows-of-8 staged row stride: out+4 when out is a multiple of 4 keeps rows 16-byte aligned
+// (16-byte async copies; the backward reads 4 consecutive weights of a row as one LDS.128, and
+// the 8 rows of a quarter-warp phase then sit 16*(out/4+1) bytes apart: distinct 16-byte bank
+// groups as long as out/4+1 is odd, i.e. out = 0 mod 8); otherwise out+1 (scalar reads).
+// Layer blocks are rounded up to 4 floats so every block starts 16-byte aligned.
+__host__ __device__ inline int r8_ld(int out) { return (out & 3) ? out + 1 : out + 4; }
+__host__ __device__ inline int r8_block(int in, int out) { return ((in + 1) * r8_ld(out) + 3) & ~3; }
+
+__host__ __device__ inline size_t staged_floats(const MlpDesc& d, int r8 = 0) {
   size_t n = 0;
-  for (int l = 0; l < d.nl; ++l) n += (size_t)d.dims[l] * (d.dims[l + 1] + 1);
+  for (int l = 0; l < d.nl; ++l)
+    n += r8 ? (size_t)r8_block(d.dims[l], d.dims[l + 1]) : (size_t)d.dims[l] * (d.dims[l + 1] + 1);
   return (n + 3) & ~size_t(3);
 }
+
+constexpr int kR8Scratch = 8 * 8 * 64;  // rows-of-8 path: [warp][row][col] partial sums
 
 struct Smem {
   float* w;  // staged weights of this CTA's net (nullptr when not staged)
@@ -122,6 +134,8 @@ struct Smem {
   float* misc;  // [R8][4]: old_lp, adv_norm, ret, -
   float* tmp;   // [R8][ldA]
   float* loss;  // [R8]
+  float* scratch;  // r8: [8 warps][8 rows][64 cols]
+  float* ls;       // r8: [ldA] log_std of the step (actor)
 };
 
 // shared-memory carve-up of one CTA working on net `net` (0 actor, 1 critic)
@@ -136,7 +150,7 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, int net, float* base, 
     o += (n + 3) & ~size_t(3);
     return p;
   };
-  float* w = a.stage ? take(staged_floats(d)) : nullptr;
+  float* w = a.stage ? take(staged_floats(d, a.r8)) : nullptr;
   if (s) s->w = w;
   float* x = take((size_t)R8 * ldx);
   if (s) s->x = x;
@@ -151,7 +165,11 @@ __host__ __device__ inline size_t carve(const PpoArgs& a, int net, float* base, 
   float* misc = take((size_t)R8 * 4);
   float* tmp = take((size_t)R8 * ldA);
   float* loss = take((size_t)R8);
+  float* scratch = a.r8 ? take((size_t)kR8Scratch) : nullptr;
+  float* ls = a.r8 ? take((size_t)ldA) : nullptr;
   if (s) {
+    s->scratch = scratch;
+    s->ls = ls;
     s->d0 = d0;
     s->d1 = d1;
     s->actn = actn;
@@ -240,6 +258,300 @@ __device__ __forceinline__ void delta_prev_tile(const float* s_d, int ldd, int o
 // their heads and the backward, so each CTA carries one net (half the weights to stage).
 // STAGED: the net's weights are copied to shared memory (every W access is an LDS);
 // otherwise (nets too wide for the tile) they are read from L2.
+
+// ============================================================================================
+// Rows-of-8 path (R <= 8, every layer width <= 64, A <= 32; the stock 64x64 nets).  The
+// per-kernel tile functions above keep one or two rows per thread, so every staged weight is
+// re-read from shared memory for each row pair and the k-chains are as long as the layer input;
+// here each warp owns a slice of the reduction dimension for ALL 8 rows and up to 64 columns
+// (8 x 2 register accumulators, x read as float4 broadcasts), and the 8 warp partials are
+// summed in fixed warp order (deterministic).  [W; b] are staged together ((in+1) rows at
+// stride out+1, conflict-free for both the row walk of the forward and the column walk of
+// the backward) with 16-byte global loads.
+// ============================================================================================
+
+// [W_l; b_l] of every layer -> dst rows of stride r8_ld(out) (bias = row `in`), asynchronously:
+// 16-byte cp.async when the rows allow it, 4-byte otherwise; waited with stage_wait()
+__device__ __forceinline__ void stage_weights_r8(const PpoArgs& a, const MlpDesc& d, float* dst) {
+  for (int l = 0; l < d.nl; ++l) {
+    const int in = d.dims[l], out = d.dims[l + 1], ld = r8_ld(out);
+    const float* src = a.params + d.off[l];
+    if ((out & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const int c4 = out >> 2, n4 = (in + 1) * c4;
+      for (int q = threadIdx.x; q < n4; q += blockDim.x) {
+        const int k = q / c4, j = (q - k * c4) << 2;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst + k * ld + j)),
+                     "l"(src + (size_t)k * out + j)
+                     : "memory");
+      }
+    } else {
+      const int n = (in + 1) * out;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int k = i / out, j = i - k * out;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst + k * ld + j)),
+                     "l"(src + i)
+                     : "memory");
+      }
+    }
+    dst += r8_block(in, out);
+  }
+}
+
+// scratch[w][r][c] = sum over this warp's slice of i of in[r][i] * Wt(i, c), r < 8, c < ncols <= 64,
+// Wt(i, c) = W[i * ldw + c] (forward, TRANS = false) or W[c * ldw + i] (backward, TRANS = true).
+// Warp w takes the groups of 4 i in [w*ng/8, (w+1)*ng/8); warp 7 also the nred % 4 tail.
+template <bool TRANS>
+__device__ __forceinline__ void r8_partials(const float* W, int ldw, const float* s_in, int ldi, int nred, int ncols,
+                                            float* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = lane, c1 = lane + 32;
+  const bool on0 = c0 < ncols, on1 = c1 < ncols;
+  float acc0[8], acc1[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc0[r] = acc1[r] = 0.0f;
+  const int ng = nred >> 2;
+  const int g0 = (w * ng) >> 3, g1 = ((w + 1) * ng) >> 3;
+  for (int g = g0; g < g1; ++g) {
+    const int i = 4 * g;
+    float w0[4], w1[4];
+    if (TRANS && (ldw & 3) == 0) {  // 16-byte row segments: one LDS.128 per column
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 a4 = on0 ? *reinterpret_cast<const float4*>(W + c0 * ldw + i) : z4;
+      const float4 b4 = on1 ? *reinterpret_cast<const float4*>(W + c1 * ldw + i) : z4;
+      w0[0] = a4.x, w0[1] = a4.y, w0[2] = a4.z, w0[3] = a4.w;
+      w1[0] = b4.x, w1[1] = b4.y, w1[2] = b4.z, w1[3] = b4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w0[u] = on0 ? (TRANS ? W[c0 * ldw + i + u] : W[(i + u) * ldw + c0]) : 0.0f;
+        w1[u] = on1 ? (TRANS ? W[c1 * ldw + i + u] : W[(i + u) * ldw + c1]) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float4 x = *reinterpret_cast<const float4*>(s_in + r * ldi + i);
+      acc0[r] = fmaf(x.x, w0[0], acc0[r]);
+      acc0[r] = fmaf(x.y, w0[1], acc0[r]);
+      acc0[r] = fmaf(x.z, w0[2], acc0[r]);
+      acc0[r] = fmaf(x.w, w0[3], acc0[r]);
+      acc1[r] = fmaf(x.x, w1[0], acc1[r]);
+      acc1[r] = fmaf(x.y, w1[1], acc1[r]);
+      acc1[r] = fmaf(x.z, w1[2], acc1[r]);
+      acc1[r] = fmaf(x.w, w1[3], acc1[r]);
+    }
+  }
+  if (w == 7)
+    for (int i = 4 * ng; i < nred; ++i) {
+      const float wa = on0 ? (TRANS ? W[c0 * ldw + i] : W[i * ldw + c0]) : 0.0f;
+      const float wb = on1 ? (TRANS ? W[c1 * ldw + i] : W[i * ldw + c1]) : 0.0f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float x = s_in[r * ldi + i];
+        acc0[r] = fmaf(x, wa, acc0[r]);
+        acc1[r] = fmaf(x, wb, acc1[r]);
+      }
+    }
+  float* sc = scratch + w * 512;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    sc[r * 64 + c0] = acc0[r];
+    sc[r * 64 + c1] = acc1[r];
+  }
+}
+
+// sum of the 8 warp partials of output (r, c), in warp order
+__device__ __forceinline__ float r8_sum(const float* scratch, int r, int c) {
+  float v = 0.0f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) v += scratch[w * 512 + r * 64 + c];
+  return v;
+}
+
+// rows [q0, q0+nrows) of a [mb][round4(w)] slab array <- smem rows (warp per row, no division)
+__device__ __forceinline__ void store_rows_r8(float* __restrict__ g, int w, const float* s, int lds, int nrows, int q0) {
+  const int lane = threadIdx.x & 31, gld = (w + 3) & ~3;
+  for (int r = threadIdx.x >> 5; r < nrows; r += blockDim.x >> 5) {
+    float* dst = g + (size_t)(q0 + r) * gld;
+    const float* src = s + r * lds;
+    for (int c = lane; c < w; c += 32) dst[c] = src[c];
+  }
+}
+
+__device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
+  const MlpDesc& d = net ? a.critic : a.actor;
+  unsigned long long* tr = (a.trace && bx == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
+  int ntr = 0;
+  auto mark = [&]() {
+    if (tr && ntr < 16) tr[ntr++] = clock64();
+  };
+  mark();
+  Smem s;
+  carve(a, net, smem, &s);
+  const int ldx = (a.S + 3) & ~3;
+  const int A = a.A, ldA = (A + 3) & ~3;
+  const int q0 = bx * 8;
+  const int nrows = min(8, a.mb - q0);
+  const double mean = a.advstat[0], denom = a.advstat[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto h_of = [&](int l) -> float* {
+    float* p = s.h0;
+    for (int i = 0; i < l; ++i) p += 8 * ((d.dims[i + 1] + 3) & ~3);
+    return p;
+  };
+  auto ldh_of = [&](int l) { return (d.dims[l + 1] + 3) & ~3; };
+  auto w_of = [&](int l) -> const float* {
+    float* p = s.w;
+    for (int i = 0; i < l; ++i) p += r8_block(d.dims[i], d.dims[i + 1]);
+    return p;
+  };
+  // weight copies first (asynchronous), then the gather's loads
+  stage_weights_r8(a, d, s.w);
+  mark();
+  // ---- gather (gather_minibatch ppo.hpp:83-103): warp r gathers row r, loads issued first ----
+  float xv[kGatherUnroll];
+  float act = 0.f, lp0 = 0.f, advv = 0.f, retv = 0.f;
+  const int r = warp;
+  if (r < nrows) {
+    const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
+    const float* fr = nullptr;
+    if (a.obs_mode == 1) fr = a.feat + (size_t)a.row[i / a.N] * (a.S - a.Sp);
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const int c = lane + 32 * u;
+      float v = 0.0f;
+      if (c < a.S) {
+        if (a.obs_mode == 1)
+          v = (c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp];
+        else
+          v = a.obs[(size_t)i * a.S + c];
+      }
+      xv[u] = v;
+    }
+    for (int c = lane + 32 * kGatherUnroll; c < a.S; c += 32)  // wide observations
+      s.x[r * ldx + c] = (a.obs_mode == 1) ? ((c < a.Sp) ? a.obs[(size_t)i * a.Sp + c] : fr[c - a.Sp])
+                                           : a.obs[(size_t)i * a.S + c];
+    if (net == 0) {
+      act = (lane < A) ? a.act[(size_t)i * A + lane] : 0.0f;
+      if (lane == 0) {
+        lp0 = a.logp[i];
+        advv = a.adv[i];
+      }
+    } else if (lane == 0) {
+      retv = a.ret[i];
+    }
+  }
+  if (net == 0)
+    for (int dd = threadIdx.x; dd < A; dd += blockDim.x) s.ls[dd] = a.params[a.log_std_off + dd];
+  if (r < nrows) {
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u)
+      if (lane + 32 * u < a.S) s.x[r * ldx + lane + 32 * u] = xv[u];
+    if (net == 0 && lane < A) s.actn[r * ldA + lane] = act;
+    if (lane == 0) {
+      s.misc[r * 4 + 0] = lp0;
+      s.misc[r * 4 + 1] = (float)(((double)advv - mean) / denom);
+      s.misc[r * 4 + 2] = retv;
+    }
+  }
+  mark();
+  stage_wait();
+  mark();
+  __syncthreads();
+  mark();
+  // ---- forward with caches (mlp_forward nn.hpp:63-85) ----
+  {
+    const float* in = s.x;
+    int ldi = ldx;
+#pragma unroll 1
+    for (int l = 0; l < d.nl; ++l) {
+      const int din = d.dims[l], out = d.dims[l + 1];
+      const float* W = w_of(l);
+      r8_partials<false>(W, r8_ld(out), in, ldi, din, out, s.scratch);
+      __syncthreads();
+      float* o = h_of(l);
+      const int ldo = ldh_of(l);
+      const float* b = W + din * r8_ld(out);
+      for (int e = threadIdx.x; e < 8 * out; e += blockDim.x) {
+        const int rr = e / out, c = e - rr * out;
+        const float z = r8_sum(s.scratch, rr, c) + b[c];
+        o[rr * ldo + c] = (l + 1 < d.nl) ? tanhf(z) : z;
+      }
+      __syncthreads();
+      in = o;
+      ldi = ldo;
+      mark();
+    }
+  }
+  // layer inputs for the gradient GEMMs: the observation (actor CTAs) and every hidden activation
+  if (net == 0) store_rows_r8(a.slab + a.hin_off[0][0], a.S, s.x, ldx, nrows, q0);
+  for (int l = 1; l < d.nl; ++l) store_rows_r8(a.slab + a.hin_off[net][l], d.dims[l], h_of(l - 1), ldh_of(l - 1), nrows, q0);
+  mark();
+  // ---- per-row losses and head gradients (ppo.hpp:128-167): warp r = row r ----
+  const float inv_n = 1.0f / (float)a.mb;
+  float* head = h_of(d.nl - 1);
+  const int ldm = ldh_of(d.nl - 1);
+  if (net == 0) {
+    if (r < nrows) {
+      const bool on = lane < A;
+      const float ls = on ? s.ls[lane] : 0.0f;
+      const float isig = expf(-ls);
+      const float z = on ? (s.actn[r * ldA + lane] - head[r * ldm + lane]) * isig : 0.0f;  // (a - mu) / sigma
+      float lpv = on ? (-0.5f * kLogTwoPiF - ls) - 0.5f * z * z : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lpv += __shfl_xor_sync(0xffffffffu, lpv, o);
+      const float ratio = expf(lpv - s.misc[r * 4 + 0]);
+      const float adv = s.misc[r * 4 + 1];
+      const float surr1 = ratio * adv;
+      const float lo = (float)(1.0 - a.clip), hi = (float)(1.0 + a.clip);
+      const float clipped = (ratio < lo) ? lo : ((hi < ratio) ? hi : ratio);  // std::clamp
+      const float surr2 = clipped * adv;
+      const float dl_dlp = (surr1 <= surr2) ? -adv * ratio * inv_n : 0.0f;  // ppo.hpp:146
+      if (on) {
+        head[r * ldm + lane] = dl_dlp * (z * isig);  // dmean = dL/dlp * z / sigma, in place
+        s.tmp[r * ldA + lane] = dl_dlp * (z * z - 1.0f);
+      }
+      if (lane == 0) s.loss[r] = -((surr2 < surr1) ? surr2 : surr1) * inv_n;  // std::min (NaN-propagating)
+    }
+  } else {
+    for (int rr = threadIdx.x; rr < nrows; rr += blockDim.x) {
+      const float err = head[rr * ldm] - s.misc[rr * 4 + 2];
+      s.loss[rr] = err * err * inv_n;
+      head[rr * ldm] = (float)a.vf * 2.0f * err * inv_n;  // dV, in place
+    }
+  }
+  __syncthreads();
+  mark();
+  store_rows_r8(a.slab + a.del_off[net][d.nl - 1], d.dims[d.nl], head, ldm, nrows, q0);
+  if (net == 0) store_rows_r8(a.slab + a.ls_off, A, s.tmp, ldA, nrows, q0);
+  for (int rr = threadIdx.x; rr < nrows; rr += blockDim.x) a.slab[a.loss_off + (size_t)(q0 + rr) * 2 + net] = s.loss[rr];
+  mark();
+  // ---- backward deltas (mlp_backward_accumulate nn.hpp:105-132, the matmul_nt half) ----
+  const int ldp = a.ldw > ldA ? a.ldw : ldA;
+  const float* delta = head;
+  int ldd = ldm;
+  for (int l = d.nl - 1; l >= 1; --l) {
+    const int in = d.dims[l], out = d.dims[l + 1];
+    float* dp = (delta == s.d0) ? s.d1 : s.d0;
+    r8_partials<true>(w_of(l), r8_ld(out), delta, ldd, out, in, s.scratch);
+    __syncthreads();
+    const float* act_in = h_of(l - 1);
+    const int lda = ldh_of(l - 1);
+    for (int e = threadIdx.x; e < 8 * in; e += blockDim.x) {
+      const int rr = e / in, k = e - rr * in;
+      const float av = act_in[rr * lda + k];
+      dp[rr * ldp + k] = r8_sum(s.scratch, rr, k) * (1.0f - av * av);
+    }
+    __syncthreads();
+    mark();
+    store_rows_r8(a.slab + a.del_off[net][l - 1], in, dp, ldp, nrows, q0);
+    delta = dp;
+    ldd = ldp;
+    mark();
+  }
+}
+
 // (bx, net) is the virtual CTA: blockIdx of ppo_fwd_delta_kernel, or a slot of the persistent kernel.
 template <bool STAGED>
 __device__ __forceinline__ void fwd_delta_block(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
@@ -424,19 +736,28 @@ __device__ __forceinline__ void fwd_delta_block(const PpoArgs& a, int bx, int ne
   }
 }
 
-template <bool STAGED>
+// MODE: 0 weights read from L2, 1 staged (fwd_delta_block), 2 rows-of-8 path (fwd_delta_r8)
+template <int MODE>
+__device__ __forceinline__ void fwd_delta_any(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
+  if (MODE == 2)
+    fwd_delta_r8(a, bx, net, step, smem);
+  else
+    fwd_delta_block<MODE == 1>(a, bx, net, step, smem);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kPpoThreads) ppo_fwd_delta_kernel(PpoArgs a) {
   if (a.status[0] != 0) return;
   extern __shared__ __align__(16) float smem[];
-  fwd_delta_block<STAGED>(a, blockIdx.x, blockIdx.y, *a.step, smem);
+  fwd_delta_any<MODE>(a, blockIdx.x, blockIdx.y, *a.step, smem);
 }
 
 // ---- ppo_grad: output-parallel dW / db / dlog_std, fixed-order sums, step gate ----
 constexpr int kGT = 64;        // output tile (k rows x j cols of [W; b])
 constexpr int kGChunk = 64;    // rows per sub-chunk of a split (one float4 load round)
 constexpr int kGLd = kGT + 4;  // smem row stride (float4-aligned)
-constexpr int kMaxSplits = 16;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
-constexpr int kGRows = 64;      // target rows per split
+constexpr int kMaxSplits = 32;  // row splits per tile (each split loops over kGChunk-row sub-chunks)
+constexpr int kGRows = 16;      // minimum rows per split
 
 struct GradArgs {
   const float* slab;
@@ -471,7 +792,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 // virtual CTA vb = tile * RS + split (blockIdx.x of ppo_grad_kernel, or a persistent slot)
-__device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm) {
+__device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm, unsigned long long* btr = nullptr) {
   float* As = gsm;
   float* Bs = gsm + kGChunk * kGLd;
   const int tile = vb / g.RS, split = vb % g.RS;
@@ -520,6 +841,7 @@ __device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm
         }
       }
       __syncthreads();
+      if (btr) btr[0] = gtime();
       if (active) {
 #pragma unroll 4
         for (int r = 0; r < nr; ++r) {
@@ -537,24 +859,27 @@ __device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm
         }
       }
     }
+    if (btr) btr[1] = gtime();
+    // the tile through shared memory, then row segments stored by whole warps (coalesced: a
+    // thread's 4x4 block spans 4 rows, so direct stores would touch 16 rows per instruction)
+    __syncthreads();  // As/Bs free
     if (active) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = k0 + 4 * tk + i;
-        if (k >= in) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int jj = j0 + 4 * tj + j;
-          if (jj < out) part[d.off[l] + k * out + jj] = acc[i][j];
-        }
-      }
-      if (with_bias && tk == 0)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int jj = j0 + 4 * tj + j;
-          if (jj < out) part[d.off[l] + in * out + jj] = bsum[j];
-        }
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<float4*>(As + (4 * tk + i) * kGLd + 4 * tj) =
+            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      if (with_bias && tk == 0) *reinterpret_cast<float4*>(Bs + 4 * tj) = make_float4(bsum[0], bsum[1], bsum[2], bsum[3]);
     }
+    __syncthreads();
+    const int nk = min(kGT, in - k0), nj = min(kGT, out - j0);
+    const int lane = tid & 31;
+    float* pw = part + d.off[l] + j0;
+    for (int kr = tid >> 5; kr < nk; kr += 8) {
+      float* rowp = pw + (size_t)(k0 + kr) * out;
+      if (lane < nj) rowp[lane] = As[kr * kGLd + lane];
+      if (lane + 32 < nj) rowp[lane + 32] = As[kr * kGLd + lane + 32];
+    }
+    if (with_bias && tid < 64 && tid < nj) pw[(size_t)in * out + tid] = Bs[tid];
   } else {  // log_std terms and the two loss sums over this split's rows
     const float* LS = g.slab + g.ls_off;
     const float* LO = g.slab + g.loss_off;
@@ -718,7 +1043,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int& 
   __syncthreads();
 }
 
-template <bool STAGED>
+template <int MODE>
 __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs a, GradArgs g, int64_t steps,
                                                                      unsigned int* bar, int32_t* flags,
                                                                      float2* bias_tab, unsigned long long* trace) {
@@ -744,14 +1069,14 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
   }
   grid_barrier(bar, bt, nb);
   // PRB_PPO_TRACE: globaltimer stamps of step 4 per CTA (phase ends and barrier exits)
-  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 10 : nullptr;
+  unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 16 : nullptr;
   const int p0 = blockIdx.x * 256 + tid;  // this thread's first parameter (its Adam update is kept in registers)
   for (int64_t st = 0; st < steps; ++st) {
     const bool mk = tr && st == (steps > 4 ? 4 : 0);
     if (mk) tr[0] = gtime();
     // ---- A: forward + head gradients + backward deltas, row-parallel ----
     for (int vb = blockIdx.x; vb < 2 * nA; vb += nb) {
-      fwd_delta_block<STAGED>(a, vb % nA, vb / nA, st, smem);
+      fwd_delta_any<MODE>(a, vb % nA, vb / nA, st, smem);
       __syncthreads();
     }
     if (mk) tr[1] = gtime();
@@ -759,7 +1084,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
     if (mk) tr[2] = gtime();
     // ---- B: dW / db / log_std / loss split partials, output-parallel ----
     for (int vb = blockIdx.x; vb < nB; vb += nb) {
-      grad_block(g, vb, smem);
+      grad_block(g, vb, smem, (mk && vb == (int)blockIdx.x) ? tr + 10 : nullptr);
       __syncthreads();
     }
     if (mk) tr[3] = gtime();
@@ -914,6 +1239,16 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   while (p.R < 64 && (size_t)(mb / (p.R * 2)) >= (size_t)a->ctx->num_sms) p.R *= 2;
   if (const char* rv = getenv("PRB_PPO_R")) p.R = std::max(8, std::min(64, atoi(rv)));  // A/B knob
   p.stage = 1;
+  p.r8 = 0;
+  {  // rows-of-8 path: 8-row blocks, every layer output <= 64 wide, A <= 32
+    bool ok = (p.R == 8) && p.A <= 32 && !(getenv("PRB_PPO_R8") && atoi(getenv("PRB_PPO_R8")) == 0);
+    for (int l = 0; l < p.actor.nl; ++l) ok = ok && p.actor.dims[l + 1] <= 64;
+    for (int l = 0; l < p.critic.nl; ++l) ok = ok && p.critic.dims[l + 1] <= 64;
+    if (ok) {
+      p.r8 = 1;
+      if (carve_max(p) > kSmemBudget) p.r8 = 0;
+    }
+  }
   if (carve_max(p) > kSmemBudget) p.stage = 0;  // wide nets: weights stay in L2
   while (p.R > 8 && carve_max(p) > kSmemBudget) p.R /= 2;
   PRB_REQUIRE(carve_max(p) <= kSmemBudget, PRB_ERR_CONFIG, "ppo: network too wide for the SIMT tile");
@@ -947,7 +1282,9 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   }
   tiles.push_back(make_int4(0, -1, 0, 0));
   ws.ntiles = (int)tiles.size();
-  ws.RS = std::min(kMaxSplits, (mb + kGRows - 1) / kGRows);
+  // splits: enough (tile, split) items to give every SM two of them (one wave of the persistent
+  // grid), each split keeping >= kGRows rows
+  ws.RS = std::max(1, std::min({kMaxSplits, (mb + kGRows - 1) / kGRows, 2 * a->ctx->num_sms / ws.ntiles}));
   ws.tiles.ensure(tiles.size());
   // every setup copy/memset on the stream the kernels run on (the context stream is
   // non-blocking: legacy-stream cudaMemset/cudaMemcpy would not be ordered with them)
@@ -1013,10 +1350,13 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
   PpoArgs pt = p;
   pt.trace = ws.trace.p ? ws.trace.p + (size_t)ws.ntiles * ws.RS * 8 : nullptr;
   const size_t smem = carve_max(p);
-  if (p.stage)
-    ppo_fwd_delta_kernel<true><<<grid, kPpoThreads, smem, s>>>(pt);
+  // steps run inside CUDA graphs: no event scopes
+  if (p.r8)
+    ppo_fwd_delta_kernel<2><<<grid, kPpoThreads, smem, s>>>(pt);
+  else if (p.stage)
+    ppo_fwd_delta_kernel<1><<<grid, kPpoThreads, smem, s>>>(pt);
   else
-    ppo_fwd_delta_kernel<false><<<grid, kPpoThreads, smem, s>>>(pt);  // steps run inside CUDA graphs: no event scopes
+    ppo_fwd_delta_kernel<0><<<grid, kPpoThreads, smem, s>>>(pt);
   GradArgs g = make_grad_args(p, a, ws, ent, apply);
   ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
   static int occ = 0;
@@ -1039,10 +1379,9 @@ int persistent_grid(const PpoArgs& p, prb_agent a, const PpoWorkspace& ws) {
   if (p.A > 256 || getenv("PRB_PPO_GRAPH")) return 0;  // PRB_PPO_GRAPH: force the per-kernel path (A/B)
   const size_t smem = persistent_smem(p);
   int occ = 0;
-  if (p.stage)
-    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_persistent_kernel<true>, kPpoThreads, smem));
-  else
-    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_persistent_kernel<false>, kPpoThreads, smem));
+  const void* fn = p.r8 ? (const void*)ppo_persistent_kernel<2>
+                        : (p.stage ? (const void*)ppo_persistent_kernel<1> : (const void*)ppo_persistent_kernel<0>);
+  PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPpoThreads, smem));
   if (occ < 1) return 0;
   const int work = std::max(2 * ((p.mb + p.R - 1) / p.R), ws.ntiles * ws.RS);
   return std::min(work, a->ctx->num_sms * occ);
@@ -1060,19 +1399,18 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   int32_t* flags = ws.bar.p + 2;
   unsigned long long* trace = nullptr;
   if (getenv("PRB_PPO_TRACE")) {  // [grid][10] phase stamps, then fwd_delta_block's 2 x 16 clock64 marks
-    ws.ptrace.alloc((size_t)grid * 10 + 32);
+    ws.ptrace.alloc((size_t)grid * 16 + 32);
     PRB_CUDA(cudaMemsetAsync(ws.ptrace.p, 0, ws.ptrace.bytes(), s));
     trace = ws.ptrace.p;
-    pa.trace = ws.ptrace.p + (size_t)grid * 10;
+    pa.trace = ws.ptrace.p + (size_t)grid * 16;
   }
   ws.bias.ensure((size_t)steps);
   float2* bias_tab = ws.bias.p;
   void* args[] = {&pa, &g, &steps, &bar, &flags, &bias_tab, &trace};
   const size_t smem = persistent_smem(p);
-  if (p.stage)
-    launch_coop((const void*)ppo_persistent_kernel<true>, grid, smem, s, args);
-  else
-    launch_coop((const void*)ppo_persistent_kernel<false>, grid, smem, s, args);
+  launch_coop(p.r8 ? (const void*)ppo_persistent_kernel<2>
+                   : (p.stage ? (const void*)ppo_persistent_kernel<1> : (const void*)ppo_persistent_kernel<0>),
+              grid, smem, s, args);
 }
 
 std::string status_message(int detail) {
@@ -1098,16 +1436,13 @@ void check_status(prb_agent a) {
 void set_smem_attr() {
   static bool done = false;
   if (!done) {
-    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBudget));
-    PRB_CUDA(cudaFuncSetAttribute(ppo_fwd_delta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBudget));
+    const void* fns[] = {(const void*)ppo_fwd_delta_kernel<0>, (const void*)ppo_fwd_delta_kernel<1>,
+                         (const void*)ppo_fwd_delta_kernel<2>, (const void*)ppo_persistent_kernel<0>,
+                         (const void*)ppo_persistent_kernel<1>, (const void*)ppo_persistent_kernel<2>};
+    for (const void* f : fns)
+      PRB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     PRB_CUDA(cudaFuncSetAttribute(ppo_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(2 * kGChunk * kGLd * sizeof(float))));
-    PRB_CUDA(cudaFuncSetAttribute(ppo_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBudget));
-    PRB_CUDA(cudaFuncSetAttribute(ppo_persistent_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBudget));
     done = true;
   }
 }

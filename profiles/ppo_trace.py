@@ -31,7 +31,7 @@ pr.ppo_update(agent, ro, cfg, seed=3)
 del os.environ["PRB_PPO_TRACE"]
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 marks = raw[-32:].reshape(2, 16)
-t = raw[:-32].reshape(-1, 10)
+t = raw[:-32].reshape(-1, 16)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 names = ["step start", "A done", "barrier 1 exit", "B done", "barrier 2 exit", "C1 done", "barrier 3 exit",
@@ -40,11 +40,24 @@ print(f"{len(t)} CTAs; times in us from the earliest step start (min / median / 
 for i, nm in enumerate(names):
     c = (t[:, i] - t0) / 1e3
     print(f"  {nm:22s} {c.min():8.2f} {np.median(c):8.2f} {c.max():8.2f}")
-mk_names = ["stage issued", "gather done", "weights landed", "layer 0", "layer 1", "layer 2", "forward done",
-            "layer inputs stored", "head grads", "head delta stored", "bwd layer 2->1", "stored", "bwd layer 1->0",
-            "stored"]
+mk_names = ["weights issued", "gather landed", "weights landed", "sync", "layer 0", "layer 1", "layer 2", "inputs stored", "head grads", "head stored",
+            "bwd 2->1", "stored", "bwd 1->0", "stored"]  # fwd_delta_r8's marks (3-layer nets)
 for net in (0, 1):
     mk = marks[net]
     mk = mk[mk > 0]
     print(["actor", "critic"][net], "row block 0 (SM cycles from block start):",
           ", ".join(f"{n} {int(c - mk[0])}" for n, c in zip(mk_names, mk[1:])))
+# phase B per gradient tile (virtual CTA vb = blockIdx.x = tile * RS + split when the grid covers it)
+RS = int(os.environ.get("TRACE_RS", "26"))
+bdur = (t[:, 3] - t[:, 2]) / 1e3
+ntile = (len(bdur) + RS - 1) // RS
+bl = (t[:, 10] - t[:, 2]) / 1e3
+bc = (t[:, 11] - t[:, 10]) / 1e3
+bs = (t[:, 3] - t[:, 11]) / 1e3
+ok = t[:, 10] > 0
+print("phase B split (us, median/max over CTAs): loads %.2f/%.2f compute %.2f/%.2f stores %.2f/%.2f" % (
+    np.median(bl[ok]), bl[ok].max(), np.median(bc[ok]), bc[ok].max(), np.median(bs[ok]), bs[ok].max()))
+print("phase B duration per tile (max over its splits, us):",
+      " ".join(f"{i}:{bdur[i * RS:(i + 1) * RS].max():.1f}" for i in range(min(ntile, 12))))
+adur = (t[:, 1] - t[:, 0]) / 1e3
+print("phase A duration: actor CTAs max %.1f us, critic CTAs max %.1f us" % (adur[:128].max(), adur[128:256].max()))
