@@ -311,6 +311,11 @@ def run_ours(args, d: Dist):
     # ---- env step alone (the VecEnv boundary) at configs[4] scale: 1M envs/GPU, > L2 ----
     env_step = env_leg(pr, lib, ctx, market, cfg, args.env_envs, hbm, d)
 
+    # ---- the GAE reverse scan alone on the collected configs[1] buffer (HBM-bound) ----
+    gae = gae_leg(lib, ctx, ro, N, H, hbm, d)
+    # ---- Adam alone on an agent larger than L2 (HBM-bound) ----
+    adam = adam_leg(pr, lib, ctx, hbm, d)
+
     # ---- one full PPO update on the collected buffer (GAE + epochs x minibatches + Adam) ----
     ppo = None
     if not args.skip_ppo:
@@ -396,7 +401,7 @@ def run_ours(args, d: Dist):
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (MLP, obs) + f64 (portfolio accounting)",
                "data": "synthetic (BASELINE.md §3 market, random-init artifact_init weights)",
                "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
-               "ppo_update": ppo, "other_configs": other, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+               "gae": gae, "adam": adam, "ppo_update": ppo, "other_configs": other, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
                "clocks": clk}
         emit((out))
     d.close()
@@ -509,6 +514,49 @@ def leg_tournament(pr, ctx, d, pods):
     return {"pods_per_gpu": pods, "pods_total": pods * d.world, "ms_per_generation": 1e3 * float(np.median(times)),
             "elite_bytes": 3 * 3 * elite.param_count * 4,
             "what": "all-gather (score,seq,pod_id) + device ranking + 3 elite broadcasts (params,m,v,t); host-timed"}
+
+
+GAE_BYTES = 4 + 4 + 1 + 4 + 4  # read reward, value, done; write advantage, return (stats fused in the pass)
+
+
+def gae_leg(lib, ctx, ro, N, H, hbm, d, reps=10):
+    """buffer_advantages (ppo.hpp:212-244) on the collected N x H buffer: the reverse GAE scan,
+    one thread per env walking its time-major column, fp64 recursion, normalisation stats fused."""
+    lib.prb_gae(ro.h, 0.99, 0.95, 1)
+    lib.prb_ctx_profile(ctx.h, 1)
+    region = d.max(time_region(lib, ctx, lambda: [lib.prb_gae(ro.h, 0.99, 0.95, 1) for _ in range(reps)]))
+    ms, n = C.c_double(), C.c_uint64()
+    lib.prb_ctx_profile_read(ctx.h, 3, C.byref(ms), C.byref(n))  # PRB_PROF_GAE
+    lib.prb_ctx_profile(ctx.h, 0)
+    avg_s = ms.value / max(n.value, 1) / 1e3
+    gbs = N * H * GAE_BYTES / avg_s / 1e9
+    return {"transitions_per_s": d.world * N * H / avg_s, "kernel_avg_us": avg_s * 1e6, "achieved_gbs": gbs,
+            "frac_hbm": gbs / hbm, "bytes_per_transition": GAE_BYTES, "region_ms_per_call": region / reps,
+            "buffer": f"{N} envs x {H} steps ({N * H * GAE_BYTES / 1e6:.0f} MB > L2)"}
+
+
+def adam_leg(pr, lib, ctx, hbm, d, reps=20):
+    """adam_step (nn.hpp:164-182) through prb_adam_step_device on an agent whose
+    params + m + v + grads (16 B/param) exceed L2: grid-wide finite gate, then the update."""
+    agent = pr.Agent.init(ctx, 4096, 2, seed=1, hidden=(1024, 1024))  # 10.5M params, 168 MB of state
+    P = agent.param_count
+    g = pr.DeviceArray.from_numpy(ctx, np.random.default_rng(0).normal(size=P).astype(np.float32) * 1e-3)
+    agent.adam_step_device(g.ptr)
+    lib.prb_ctx_profile(ctx.h, 1)
+    region = d.max(time_region(lib, ctx, lambda: [lib.prb_adam_step_device(agent.h, C.c_void_p(g.ptr))
+                                                  for _ in range(reps)]))
+    ms, n = C.c_double(), C.c_uint64()
+    lib.prb_ctx_profile_read(ctx.h, 6, C.byref(ms), C.byref(n))  # PRB_PROF_ADAM
+    lib.prb_ctx_profile(ctx.h, 0)
+    out = {"params": P, "bytes_per_param": 28, "region_ms_per_step": region / reps,
+           "note": "28 B/param = read p, g, m, v + write p, m, v (fp32); the finite check re-reads g (L2)"}
+    if n.value:
+        avg_s = ms.value / n.value / 1e3
+        out.update({"kernel_avg_us": avg_s * 1e6, "achieved_gbs": P * 28 / avg_s / 1e9,
+                    "frac_hbm": P * 28 / avg_s / 1e9 / hbm})
+    step_s = region / reps / 1e3
+    out.update({"step_gbs": P * 28 / step_s / 1e9, "step_frac_hbm": P * 28 / step_s / 1e9 / hbm})
+    return out
 
 
 def env_leg(pr, lib, ctx, market, cfg, n_envs, hbm, d, steps=50):

@@ -253,6 +253,10 @@ PRB_API int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows,
 /* adam_step nn.hpp:164-182 with host gradients (NumericError, state untouched,
  * on a non-finite gradient). */
 PRB_API int prb_adam_step_host(prb_agent a, const double* grads);
+/* adam_step nn.hpp:164-182 with DEVICE fp32 gradients [P] (flat layout): a grid-wide
+ * finite check first (NumericError, state untouched, on a non-finite gradient), then
+ * the update; t advances by one on success. */
+PRB_API int prb_adam_step_device(prb_agent a, const float* d_grads);
 
 /* ---- evaluator (evaluate pod.hpp:43-83, PodEvaluator::process :313-316) --
  * `episodes` = env's num_envs evaluation episodes of the agent's policy:

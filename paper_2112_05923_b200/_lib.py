@@ -159,6 +159,7 @@ SIGNATURES = {
     "prb_ppo_update": (I, [P, P, C.POINTER(PpoConfig), U64, pU64, P, C.POINTER(PpoStats)]),
     "prb_ppo_loss_grads": (I, [P, P, pU64, SZ, C.POINTER(PpoConfig), pD, pD]),
     "prb_adam_step_host": (I, [P, pD]),
+    "prb_adam_step_device": (I, [P, P]),
     "prb_evaluate": (I, [P, P, U64, I, pD, pD, pD, pU64]),
     "prb_fuse_parameters": (I, [C.POINTER(P), SZ, P]),
     "prb_leaderboard_rank": (I, [P, P, P, SZ, SZ, P, P]),

@@ -52,31 +52,62 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
   const float ibc1 = (float)(1.0 / bc1), ibc2 = (float)(1.0 / bc2);
   // constants rounded once from fp64 (1 - beta2 in fp32 arithmetic would be off by 1e-5 relative)
   const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
-    const float mi = b1 * m[i] + omb1 * gi;
-    const float vi = b2 * v[i] + omb2 * gi * gi;
+  auto upd = [&](float gi, float& mi, float& vi, float& pi) {
+    mi = b1 * mi + omb1 * gi;
+    vi = b2 * vi + omb2 * gi * gi;
+    pi -= lr * (mi * ibc1) / (sqrtf(vi * ibc2) + eps);
+  };
+  const size_t tid0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  size_t n4 = 0;
+  if (((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
+        reinterpret_cast<uintptr_t>(v)) & 15) == 0) {  // 16-byte streams (same arithmetic per element)
+    n4 = n / 4;
+    float4* p4 = reinterpret_cast<float4*>(p);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4* m4 = reinterpret_cast<float4*>(m);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    for (size_t i = tid0; i < n4; i += stride) {
+      const float4 gg = g4[i];
+      float4 mm = m4[i], vv = v4[i], pp = p4[i];
+      upd(gg.x, mm.x, vv.x, pp.x);
+      upd(gg.y, mm.y, vv.y, pp.y);
+      upd(gg.z, mm.z, vv.z, pp.z);
+      upd(gg.w, mm.w, vv.w, pp.w);
+      m4[i] = mm;
+      v4[i] = vv;
+      p4[i] = pp;
+    }
+  }
+  for (size_t i = 4 * n4 + tid0; i < n; i += stride) {
+    float mi = m[i], vi = v[i], pi = p[i];
+    upd(g[i], mi, vi, pi);
     m[i] = mi;
     v[i] = vi;
-    p[i] -= lr * (mi * ibc1) / (sqrtf(vi * ibc2) + eps);
+    p[i] = pi;
   }
 }
 
+// Grid-wide finite check of the gradients (nn.hpp:169-171: reject before touching state).
+// status[2] counts finished CTAs, status[3] collects the non-finite flag; the last CTA
+// publishes the verdict (status[0..1]) and advances t on success, then re-arms [2] and [3].
 __global__ void finite_check_kernel(const float* __restrict__ g, size_t n, int32_t* status, int64_t* t_dev) {
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
   int local = 0;
-  for (size_t i = threadIdx.x; i < n; i += blockDim.x) local |= !isfinite(g[i]);
-  if (local) bad = 1;
-  __syncthreads();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    local |= !isfinite(g[i]);
+  if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(&status[3], 1);
   if (threadIdx.x == 0) {
-    if (bad) {
-      status[0] = PRB_ERR_NUMERIC;
-      status[1] = 1;  // adam_step: non-finite gradient
-    } else {
-      status[0] = 0;
-      *t_dev += 1;
+    __threadfence();
+    if (atomicAdd(&status[2], 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      const int bad = atomicExch(&status[3], 0);
+      status[2] = 0;
+      if (bad) {
+        status[0] = PRB_ERR_NUMERIC;
+        status[1] = 1;  // adam_step: non-finite gradient
+      } else {
+        status[0] = 0;
+        *t_dev += 1;
+      }
     }
   }
 }
@@ -137,8 +168,10 @@ __global__ void mutate_kernel(float* __restrict__ p, size_t n, uint64_t seed, fl
 }  // namespace
 
 void prb_agent_finite_gate_and_adam(prb_agent a, const float* d_grads, cudaStream_t s) {
-  finite_check_kernel<<<1, 1024, 0, s>>>(d_grads, a->P, a->d_status.p, a->d_t.p);
-  const int grid = (int)std::min<size_t>((a->P + 255) / 256, 1184);
+  const int cgrid = (int)std::min<size_t>((a->P + 255) / 256, (size_t)a->ctx->num_sms * 8);
+  finite_check_kernel<<<cgrid, 256, 0, s>>>(d_grads, a->P, a->d_status.p, a->d_t.p);
+  const int grid = (int)std::min<size_t>((a->P + 255) / 256, (size_t)a->ctx->num_sms * 8);
+  ProfScope prof(a->ctx, kProfAdam);
   adam_kernel<<<grid, 256, 0, s>>>(a->d_params.p, d_grads, a->d_m.p, a->d_v.p, a->P, a->d_t.p, a->d_status.p,
                                    (float)a->lr, a->beta1, a->beta2, (float)a->eps);
   PRB_CHECK_LAUNCH();
@@ -274,6 +307,22 @@ int prb_adam_step_host(prb_agent a, const double* grads) {
     PRB_CUDA(cudaMemcpyAsync(a->d_grads.p, g.data(), a->P * sizeof(float), cudaMemcpyHostToDevice, s));
     prb_agent_finite_gate_and_adam(a, a->d_grads.p, s);
     a->ctx->sync();
+  });
+}
+
+int prb_adam_step_device(prb_agent a, const float* d_grads) {
+  return guard([&] {
+    PRB_REQUIRE(a && d_grads, PRB_ERR_USAGE, "prb_adam_step_device: NULL argument");
+    cudaStream_t s = a->ctx->stream;
+    prb_agent_finite_gate_and_adam(a, d_grads, s);
+    int32_t st[2];
+    PRB_CUDA(cudaMemcpyAsync(st, a->d_status.p, sizeof(st), cudaMemcpyDeviceToHost, s));
+    a->ctx->sync();
+    if (st[0] != 0) {
+      PRB_CUDA(cudaMemsetAsync(a->d_status.p, 0, 2 * sizeof(int32_t), s));
+      a->ctx->sync();
+      fail(st[0], "adam_step: non-finite gradient, step aborted");
+    }
   });
 }
 

@@ -7,7 +7,8 @@
 // intrinsics in the reference's operation order, so on identical fp32 inputs
 // it reproduces the reference's fp64 result before the final fp32 store.
 // The whole-buffer normalisation statistics (mean, population std floored at
-// 1e-8) are reduced in the same pass with Chan/Welford merges in fp64; the
+// 1e-8) are reduced in the same pass: per-thread fp64 sums of x and x^2, then
+// Chan merges of (n, mean, M2) across threads and blocks in fp64; the
 // PPO gather applies (adv - mean) / denom on the fly, so the normalised
 // advantages never make an extra HBM round trip.
 #include <algorithm>
@@ -18,6 +19,8 @@
 using namespace prb;
 
 namespace {
+
+constexpr int kGaeU = 16;  // recursion steps per pipelined load block
 
 struct Welford {
   double n, mean, m2;
@@ -35,7 +38,7 @@ __device__ __forceinline__ Welford merge(Welford a, Welford b) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
+__global__ void __launch_bounds__(128) gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
                                                   const uint8_t* __restrict__ done, const float* __restrict__ boot,
                                                   int N, int H, double gamma, double lambda, float* __restrict__ adv,
                                                   float* __restrict__ ret, double* __restrict__ partials) {
@@ -45,25 +48,56 @@ __global__ void __launch_bounds__(256) gae_kernel(const float* __restrict__ rew,
     const double gl = __dmul_rn(gamma, lambda);
     double gae = 0.0;
     double next_v = (double)boot[e];
-    for (int h = H - 1; h >= 0; --h) {
-      const size_t j = (size_t)h * N + e;
-      const double r = (double)rew[j];
-      const double v = (double)val[j];
-      const double nonterminal = done[j] ? 0.0 : 1.0;
-      // delta = r + gamma * next_value * nonterminal - v ; gae = delta + gamma*lambda*nonterminal*gae
-      const double delta = __dsub_rn(__dadd_rn(r, __dmul_rn(__dmul_rn(gamma, next_v), nonterminal)), v);
-      gae = __dadd_rn(delta, __dmul_rn(__dmul_rn(gl, nonterminal), gae));
-      const float a32 = (float)gae;
-      adv[j] = a32;
-      ret[j] = (float)__dadd_rn(gae, v);
-      next_v = v;
-      // Welford on the stored value
-      w.n += 1.0;
-      const double x = (double)a32;
-      const double d = x - w.mean;
-      w.mean += d / w.n;
-      w.m2 += d * (x - w.mean);
+    double s1 = 0.0, s2 = 0.0;  // sum and sum of squares of the stored advantages (fp64)
+    // Software pipeline over blocks of kGaeU steps: the loads of the next block (they do not
+    // depend on the recursion) are in flight while the current block's recursion runs.
+    float rA[kGaeU], vA[kGaeU], rB[kGaeU], vB[kGaeU];
+    uint8_t dA[kGaeU], dB[kGaeU];
+    auto load = [&](int h0, float (&rr)[kGaeU], float (&vv)[kGaeU], uint8_t (&dd)[kGaeU]) {
+#pragma unroll
+      for (int u = 0; u < kGaeU; ++u) {
+        const int h = h0 - u;
+        if (h >= 0) {
+          const size_t j = (size_t)h * N + e;
+          rr[u] = rew[j];
+          vv[u] = val[j];
+          dd[u] = done[j];
+        }
+      }
+    };
+    auto run = [&](int h0, const float (&rr)[kGaeU], const float (&vv)[kGaeU], const uint8_t (&dd)[kGaeU]) {
+#pragma unroll
+      for (int u = 0; u < kGaeU; ++u) {
+        const int h = h0 - u;
+        if (h >= 0) {
+          const size_t j = (size_t)h * N + e;
+          const double r = (double)rr[u];
+          const double v = (double)vv[u];
+          const double nonterminal = dd[u] ? 0.0 : 1.0;
+          // delta = r + gamma * next_value * nonterminal - v ; gae = delta + gamma*lambda*nonterminal*gae
+          const double delta = __dsub_rn(__dadd_rn(r, __dmul_rn(__dmul_rn(gamma, next_v), nonterminal)), v);
+          gae = __dadd_rn(delta, __dmul_rn(__dmul_rn(gl, nonterminal), gae));
+          const float a32 = (float)gae;
+          adv[j] = a32;
+          ret[j] = (float)__dadd_rn(gae, v);
+          next_v = v;
+          const double x = (double)a32;
+          s1 += x;
+          s2 = fma(x, x, s2);
+        }
+      }
+    };
+    load(H - 1, rA, vA, dA);
+    for (int h0 = H - 1; h0 >= 0; h0 -= 2 * kGaeU) {
+      load(h0 - kGaeU, rB, vB, dB);
+      run(h0, rA, vA, dA);
+      load(h0 - 2 * kGaeU, rA, vA, dA);
+      run(h0 - kGaeU, rB, vB, dB);
     }
+    // this thread's (n, mean, M2) for the Chan merges below
+    w.n = (double)H;
+    w.mean = s1 / w.n;
+    w.m2 = fmax(s2 - s1 * w.mean, 0.0);
   }
   if (!partials) return;
   // block merge: warp shuffles then smem
@@ -74,7 +108,7 @@ __global__ void __launch_bounds__(256) gae_kernel(const float* __restrict__ rew,
     b.m2 = __shfl_xor_sync(0xffffffffu, w.m2, o);
     w = merge(w, b);
   }
-  __shared__ Welford sw[8];
+  __shared__ Welford sw[4];
   if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = w;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -112,11 +146,11 @@ __global__ void gae_stats_kernel(const double* __restrict__ partials, int nblock
 
 void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8_t* done, const float* boot, size_t N,
                     size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize) {
-  const int grid = (int)((N + 255) / 256);
+  const int grid = (int)((N + 127) / 128);  // 128-thread CTAs: more even spread over the SMs
   double* partials = stat ? static_cast<double*>(ctx->device_scratch((size_t)grid * 3 * sizeof(double))) : nullptr;
   {
     ProfScope prof(ctx, kProfGae);
-    gae_kernel<<<grid, 256, 0, ctx->stream>>>(rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials);
+    gae_kernel<<<grid, 128, 0, ctx->stream>>>(rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials);
   }
   PRB_CHECK_LAUNCH();
   if (stat) {

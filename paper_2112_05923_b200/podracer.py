@@ -331,6 +331,10 @@ class Agent:
             raise DimensionError(f"adam_step: params {self.param_count}, grads {g.size}")
         self.ctx.lib.prb_adam_step_host(self.h, _p(g, C.c_double))
 
+    def adam_step_device(self, d_grads: int):
+        """adam_step (nn.hpp:164-182) with device fp32 gradients at address d_grads."""
+        self.ctx.lib.prb_adam_step_device(self.h, C.c_void_p(d_grads))
+
     def mutate(self, mutation_seed: int, sigma: float):
         self.ctx.lib.prb_agent_mutate(self.h, mutation_seed, sigma)
 

@@ -243,6 +243,34 @@ def test_adam_parity_and_known_answers(pr, ctx, orc):
         assert np.allclose(a1.flatten_params(), -1e-3 * np.sign(gval), atol=1e-9)
 
 
+@pytest.mark.parametrize("S,A,hid", [(5, 2, (4,)), (6, 2, (1024, 1024))])  # P = 63 and 1.06M (multi-CTA gate)
+def test_adam_step_device(pr, ctx, S, A, hid):
+    """prb_adam_step_device (grid-wide finite gate + Adam) == the host-gradient path, and a
+    non-finite gradient anywhere leaves params/m/v/t untouched (nn.hpp:169-171)."""
+    rng = np.random.default_rng(1)
+    a1 = pr.Agent.init(ctx, S, A, seed=2, hidden=hid)
+    a2 = a1.clone()
+    for step in range(3):
+        g = rng.normal(size=a1.param_count).astype(np.float32)
+        a1.adam_step(g.astype(np.float64))
+        dg = pr.DeviceArray.from_numpy(ctx, g)  # kept alive until the step has run
+        a2.adam_step_device(dg.ptr)
+    p1, m1, v1, t1 = a1.get()
+    p2, m2, v2, t2 = a2.get()
+    assert t1 == t2 == 3
+    assert np.array_equal(p1, p2) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    g[-1] = np.nan  # the last element: only the last CTA of the check sees it
+    dg = pr.DeviceArray.from_numpy(ctx, g)
+    with pytest.raises(pr.NumericError):
+        a2.adam_step_device(dg.ptr)
+    p3, m3, v3, t3 = a2.get()
+    assert t3 == 3 and np.array_equal(p3, p2) and np.array_equal(m3, m2) and np.array_equal(v3, v2)
+    g[-1] = 0.5
+    dg = pr.DeviceArray.from_numpy(ctx, g)
+    a2.adam_step_device(dg.ptr)  # usable after the rejected step
+    assert a2.get()[3] == 4
+
+
 def test_ppo_update_matches_reference_permutation(pr, ctx, orc, ref):
     from oracle_bind import load_ref  # noqa: F401  (ref fixture provides the std::shuffle sequence)
     S, A, hid = 6, 2, (8, 8)
