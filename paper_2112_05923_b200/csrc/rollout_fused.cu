@@ -433,7 +433,7 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
     f.b_rew = r->d_rew.p;
     f.b_done = r->d_done.p;
     f.b_boot = r->d_boot.p;
-    if (r->mode == 2 && stock_rollout_tc_supported(K)) {  // tcgen05 bf16 MLP (rollout_tc.cu)
+    if (r->mode == 2 && stock_rollout_tc_supported(K) && env->cfg.max_trade_shares < 2147483648.0) {  // tcgen05 bf16 MLP (rollout_tc.cu)
       TcRolloutArgs ta{};
       ta.params = f.params;
       ta.a_w1 = f.a_w1; ta.a_w2 = f.a_w2; ta.a_w3 = f.a_w3;

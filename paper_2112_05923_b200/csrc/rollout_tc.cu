@@ -180,6 +180,13 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   const size_t row = e0 + tid;
   tc::Tracer<kTcTraceLen> tr;
   if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
+  // value_before of the first step (stock_env.hpp:68); later steps carry value_after
+  double vb = bal;
+  {
+    const int t0 = a.t_seq[0];
+#pragma unroll
+    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], a.close_tk[(size_t)t0 * K + k]));
+  }
 
   for (int h = 0; h <= a.H; ++h) {
     const int t = a.t_seq[h];
@@ -296,35 +303,52 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     // recompute, and keeping 30 of them live as doubles next to the 30 share
     // counts would spill the shares to local memory.  Both loops are branch-free
     // (a zero-quantity trade leaves balance and shares bit-identical).
-    const volatile float* my = stage + tid * kSLD;
+    // desired_k = trunc(clamp(a_k, -1, 1) * max_trade) (stock_env.hpp:83-87) ONCE per step, as
+    // int32 in this thread's staged row (the action rows were stored above; the launcher checks
+    // max_trade < 2^31).  Sells then run in integers except the cash arithmetic, buys convert d
+    // once, and no share count is converted back from a double on the fast paths: the fp64
+    // conversions are what keeps the XU pipe busy in this phase.
+    __syncthreads();  // every warp's act-row copy has read the staged actions
+    volatile float* my = stage + tid * kSLD;  // int32 bit patterns after this loop
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      my[k] = __int_as_float((int32_t)trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade)));
     const int done = a.done_seq[h];
-    double vb = bal;
 #pragma unroll
-    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)sh[k], s.p0[k]));
-#pragma unroll
-    for (int k = 0; k < K; ++k) {  // sells first (:88-90)
-      const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
-      const double qv = (d < 0.0) ? -min_ref(-d, (double)sh[k]) : 0.0;
+    for (int k = 0; k < K; ++k) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
+      const int32_t di = __float_as_int(my[k]);
+      const int32_t qi = (di < 0) ? -min(-di, sh[k]) : 0;
+      const double qv = (double)qi;
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-      sh[k] += (int32_t)qv;
+      sh[k] += qi;
     }
     const double cf = __dadd_rn(1.0, a.cost);
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
-      const double d = trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade));
+      const int32_t di = __float_as_int(my[k]);
+      const double d = (double)di;
       const double price = s.p0[k];
-      const double qv = (d > 0.0) ? stock::buy_qty(d, bal, __dmul_rn(price, cf)) : 0.0;
+      const double pc = __dmul_rn(price, cf);
+      // stock::buy_qty: `d` itself when the exact residual d*pc - bal <= 0 (no conversion back)
+      const bool fast = __fma_rn(d, pc, -bal) <= 0.0;
+      const bool none = stock::cannot_afford_one(bal, pc);  // affordable == 0 without the division
+      const double qv = (di > 0 && !none) ? (fast ? d : stock::buy_qty_limited(d, bal, pc)) : 0.0;
+      const int32_t qi = (di > 0 && !none) ? (fast ? di : (int32_t)qv) : 0;
       const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
-      sh[k] += (int32_t)qv;
+      sh[k] += qi;
     }
     double va = bal;
 #pragma unroll
     for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s.p1[k]));
     const double rw = __dsub_rn(va, vb);
     ret = __dadd_rn(ret, rw);
+    // next step's value_before: the same shares at close[t+1] plus the same balance is exactly
+    // this step's value_after (same operands, same order); after an auto-reset it is
+    // cap + sum(0 * close) = cap
+    vb = done ? a.cap : va;
     tr.mark();
     if (done) {  // auto-reset (env.hpp:221-229, stock_env.hpp:158-163)
       bal = a.cap;

@@ -19,8 +19,19 @@ static __device__ __noinline__ double buy_qty_limited(double desired, double bal
   return (floor0 < desired) ? floor0 : desired;                  // std::min(desired, .)
 }
 
+// Largest double below 1.  If pc * kBelowOne >= balance (exact sign of the single-rounding
+// FMA residual), the exact quotient balance/pc is <= kBelowOne, so its rounding is < 1 and
+// floor() gives 0: the cash-limited buy of an env that cannot afford one share, decided
+// without the fp64 division (the common case once a portfolio's cash is spent).
+constexpr double kBelowOne = 0.99999999999999988898;  // 1 - 2^-53
+
+__device__ __forceinline__ bool cannot_afford_one(double balance, double pc) {
+  return __fma_rn(pc, kBelowOne, -balance) >= 0.0;
+}
+
 __device__ __forceinline__ double buy_qty(double desired, double balance, double pc) {
   if (__fma_rn(desired, pc, -balance) <= 0.0) return desired;
+  if (cannot_afford_one(balance, pc)) return 0.0;
   return buy_qty_limited(desired, balance, pc);
 }
 
