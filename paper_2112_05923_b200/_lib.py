@@ -171,6 +171,7 @@ SIGNATURES = {
     "prb_leaderboard_allgather_rank": (I, [P, P, P, P, SZ, SZ, P, P, P, P, P]),
     "prb_agent_broadcast": (I, [P, P, I]),
     "prb_debug_tc_gemm": (I, [P, I, I, pF, pF, pF]),
+    "prb_debug_trade_math": (I, [P, SZ, pF, D, pD, pD, D, pI32, pD, pI32]),
 }
 
 UNCHECKED = {"prb_last_error", "prb_version", "prb_splitmix64", "prb_derive_seed", "prb_ctx_stream",

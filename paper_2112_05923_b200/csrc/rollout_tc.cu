@@ -53,6 +53,7 @@ struct TcSmem {
   float sig[32], isig[32];
   float b3c, lpc;
   double p0[32], p1[32];
+  stock::BuyPrice bp[32];
   uint64_t mbar;
   uint32_t tmem;
 };
@@ -104,19 +105,37 @@ __device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32
   tc::fence_after_sync();
 }
 
-// Warp-per-row copy of the staged [rows][kSLD] fp32 tile to a contiguous [rows][cols] span.
-__device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int cols, int nrows) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < nrows; r += kM / 32)
-    if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * kSLD + lane];
+// Copy of a staged tile that is already the contiguous [rows][cols] image of its HBM span (this
+// CTA's rows are consecutive): 16-byte streaming stores (the rollout buffer is not re-read
+// before the PPO update), scalar tail.  dst must be 16-byte aligned.
+__device__ __forceinline__ void store_tile(float* __restrict__ dst, const float* stage, int nfl) {
+  const int n4 = nfl >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(stage);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int i = threadIdx.x; i < n4; i += kM) __stcs(d4 + i, s4[i]);
+  for (int i = (n4 << 2) + threadIdx.x; i < nfl; i += kM) __stcs(dst + i, stage[i]);
 }
 
-template <int K>
+// Warp-per-row copy of the staged [rows][kSLD] fp32 tile to a contiguous [rows][cols] span.
+__device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int cols, int nrows,
+                                           int sld = kSLD) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < nrows; r += kM / 32)
+    if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * sld + lane];
+}
+
+template <int K, bool kTrace>
 __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a) {
   static_assert(K >= 1 && K <= 30, "private obs row and staging must fit 31 columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& s = *reinterpret_cast<TcSmem*>(smem_raw);
   constexpr int A = K, P1 = 1 + K, F = 5 * K;
+  // Staging strides: obs rows at kSLD (= P1 when K = 30: the staged tile is the contiguous image
+  // of the CTA's obs rows), action rows at A when K = 30 (contiguous too; the 2-way bank
+  // conflicts of stride 30 cost less than a row-by-row copy), else kSLD.
+  constexpr int SA = (K == 30) ? A : kSLD;
+  constexpr bool kTileObs = (P1 == kSLD), kTileAct = (SA == A);
+  const bool vec_ok = (a.N & 3) == 0;  // 16-byte aligned spans of both tiles
   const int tid = threadIdx.x, warp = tid >> 5;
   const size_t e0 = (size_t)blockIdx.x * kM;
   const int nloc = min(kM, a.N - (int)e0);
@@ -178,7 +197,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   constexpr uint32_t ID_L3A = tc::idesc_bf16(128, 32), ID_L3C = tc::idesc_bf16(128, 16);
   uint32_t phase = 0;
   const size_t row = e0 + tid;
-  tc::Tracer<kTcTraceLen> tr;
+  tc::Tracer<kTcTraceLen, kTrace> tr;
   if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
   // value_before of the first step (stock_env.hpp:68); later steps carry value_after
   double vb = bal;
@@ -194,7 +213,9 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     tr.mark();
     s.c1[tid] = a.shared_l1[(size_t)h * 128 + tid] + b1_mine;
     if (tid < K) {
-      s.p0[tid] = a.close_tk[(size_t)t * K + tid];
+      const double p0 = a.close_tk[(size_t)t * K + tid];
+      s.p0[tid] = p0;
+      s.bp[tid] = stock::buy_price(p0, a.cost);
       if (h < a.H) s.p1[tid] = a.close_tk[(size_t)(t + 1) * K + tid];
     }
     // ---- X <- [balance/cap, shares] (stock_observation stock_env.hpp:115-121) ----
@@ -259,7 +280,10 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
 #pragma unroll
     for (int k = 0; k < K; ++k) stage[tid * kSLD + 1 + k] = (float)sh[k];
     __syncthreads();
-    store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, P1, nloc);
+    if (kTileObs && vec_ok)
+      store_tile(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, nloc * P1);
+    else
+      store_rows(a.b_obs + ((size_t)h * a.N + e0) * P1, stage, P1, nloc);
     __syncthreads();
     tr.mark();
     // ---- a = mu + sigma * eps (Philox stream of policy_kernel), log-prob; actions staged ----
@@ -285,7 +309,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
                 const float act = m + s.sig[d] * e4[i];
                 const float z = (act - m) * s.isig[d];
                 zz += z * z;
-                stage[tid * kSLD + d] = act;
+                stage[tid * SA + d] = act;
               }
             }
           }
@@ -296,53 +320,58 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     const float lp = s.lpc - 0.5f * zz;
     __syncthreads();
     tr.mark();
-    store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, A, nloc);
+    if (kTileAct && vec_ok)
+      store_tile(a.b_act + ((size_t)h * a.N + e0) * A, stage, nloc * A);
+    else
+      store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, A, nloc, SA);
     tr.mark();
     // ---- env step (stock_env_step stock_env.hpp:55-103), this thread's env, fp64 ----
-    // `my` is re-read in each loop (volatile): the desired quantities are cheap to
-    // recompute, and keeping 30 of them live as doubles next to the 30 share
-    // counts would spill the shares to local memory.  Both loops are branch-free
-    // (a zero-quantity trade leaves balance and shares bit-identical).
     // desired_k = trunc(clamp(a_k, -1, 1) * max_trade) (stock_env.hpp:83-87) ONCE per step, as
-    // int32 in this thread's staged row (the action rows were stored above; the launcher checks
-    // max_trade < 2^31).  Sells then run in integers except the cash arithmetic, buys convert d
-    // once, and no share count is converted back from a double on the fast paths: the fp64
-    // conversions are what keeps the XU pipe busy in this phase.
+    // int32 bit patterns written over this thread's staged action row (the action rows were
+    // stored above; `my` is volatile so the 30 values are re-read from shared memory instead of
+    // being kept live next to the 30 share counts).  Sells run in integers except the cash
+    // arithmetic; buys use stock::buy_qty_nodiv.  No XU conversion or fp64 division is left on
+    // the balance chain (stock_env.cuh); every trade is branch-free (a zero-quantity trade
+    // leaves balance and shares bit-identical).
     __syncthreads();  // every warp's act-row copy has read the staged actions
-    volatile float* my = stage + tid * kSLD;  // int32 bit patterns after this loop
+    volatile float* my = stage + tid * SA;  // int32 bit patterns after this loop
+    if (a.mt_f32) {
+      const float mtf = (float)a.max_trade;
+      const int32_t mti = (int32_t)a.max_trade;
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-      my[k] = __int_as_float((int32_t)trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade)));
+      for (int k = 0; k < K; ++k) my[k] = __int_as_float(stock::desired_qty_f32(my[k], mtf, mti));
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        my[k] = __int_as_float((int32_t)trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade)));
+    }
     const int done = a.done_seq[h];
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
       const int32_t di = __float_as_int(my[k]);
       const int32_t qi = (di < 0) ? -min(-di, sh[k]) : 0;
-      const double qv = (double)qi;
+      const double qv = stock::i2d_exact(qi);
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
       sh[k] += qi;
     }
-    const double cf = __dadd_rn(1.0, a.cost);
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
       const int32_t di = __float_as_int(my[k]);
-      const double d = (double)di;
+      const double d = stock::i2d_exact(di);
+      int32_t qb;
+      const double qb_v = stock::buy_qty_nodiv(d, di, bal, s.bp[k], qb);
+      const double qv = (di > 0) ? qb_v : 0.0;
+      const int32_t qi = (di > 0) ? qb : 0;
       const double price = s.p0[k];
-      const double pc = __dmul_rn(price, cf);
-      // stock::buy_qty: `d` itself when the exact residual d*pc - bal <= 0 (no conversion back)
-      const bool fast = __fma_rn(d, pc, -bal) <= 0.0;
-      const bool none = stock::cannot_afford_one(bal, pc);  // affordable == 0 without the division
-      const double qv = (di > 0 && !none) ? (fast ? d : stock::buy_qty_limited(d, bal, pc)) : 0.0;
-      const int32_t qi = (di > 0 && !none) ? (fast ? di : (int32_t)qv) : 0;
-      const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
+      const double cost = __dmul_rn(__dmul_rn(a.cost, qv), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
       sh[k] += qi;
     }
     double va = bal;
 #pragma unroll
-    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)sh[k], s.p1[k]));
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn(stock::i2d_exact(sh[k]), s.p1[k]));
     const double rw = __dsub_rn(va, vb);
     ret = __dadd_rn(ret, rw);
     // next step's value_before: the same shares at close[t+1] plus the same balance is exactly
@@ -390,11 +419,16 @@ void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s) {
   case KK: {                                                                                                 \
     static bool attr = false;                                                                                \
     if (!attr) {                                                                                             \
-      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                    (int)smem));                                                             \
+      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK, false>,                                      \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
+      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK, true>,                                       \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
       attr = true;                                                                                           \
     }                                                                                                        \
-    stock_rollout_tc_kernel<KK><<<grid, kM, smem, s>>>(a);                                                   \
+    if (a.trace)                                                                                             \
+      stock_rollout_tc_kernel<KK, true><<<grid, kM, smem, s>>>(a);                                           \
+    else                                                                                                     \
+      stock_rollout_tc_kernel<KK, false><<<grid, kM, smem, s>>>(a);                                          \
     break;                                                                                                   \
   }
   switch (a.K) {

@@ -16,6 +16,7 @@ struct TcRolloutArgs {
   const double* close_tk;  // [T][K]
   const float* feat;       // [T][5K]
   double cap, max_trade, cost;
+  int mt_f32;  // max_trade is an integer < 2^22: desired quantities in exact fp32 (stock::desired_qty_f32)
   int N, H;
   uint64_t seed;
   double* balance;

@@ -35,5 +35,71 @@ __device__ __forceinline__ double buy_qty(double desired, double balance, double
   return buy_qty_limited(desired, balance, pc);
 }
 
+// ---- conversion- and division-free pieces of the fused rollout's env step ----
+// The fp64 <-> int conversions (I2F.F64 / F2I.F64) and __ddiv_rn run on the
+// quarter-rate XU pipe and sit on the per-env dependency chain through the
+// balance; these restatements use only the fp32 / fp64 FMA pipes and integer
+// ops and are bit-identical to the reference expressions they replace.
+
+// (double)i for any int32, exact: the double 2^52 + 2^31 + i has low word i + 2^31.
+__device__ __forceinline__ double i2d_exact(int32_t i) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)((uint32_t)i ^ 0x80000000u)), 4503601774854144.0);
+}
+
+// desired = trunc(clamp(a, -1, 1) * max_trade) (stock_env.hpp:83-87) for an fp32 action and an
+// integer-valued max_trade < 2^22 (mt as a float and as mti, both exact).  In fp64 the product
+// of a 24-bit action and a <= 22-bit integer is exact, so the reference truncates the EXACT
+// product x.  RZ(x) (the fp32 product rounded toward zero) has the same truncation: no integer
+// lies strictly between x and RZ(x), every integer below 2^24 being a float.  The clamp of the
+// action to [-1, 1] is then the clamp of the integer to [-mti, mti] (RZ is monotone and mt is
+// exact); cvt.rzi maps NaN to 0 (the reference: a NaN desired is neither < 0 nor > 0, no
+// trade) and saturates infinities.
+__device__ __forceinline__ int32_t desired_qty_f32(float a, float mt, int32_t mti) {
+  const int32_t d = __float2int_rz(__fmul_rz(a, mt));
+  return min(max(d, -mti), mti);
+}
+
+// Per step and asset, shared by every env of the VecEnv (lock-step t): pc = price * (1 + c),
+// inv = RN(1 / pc), thr = pc * 2^-50.
+struct BuyPrice {
+  double pc, inv, thr;
+};
+
+__device__ __forceinline__ BuyPrice buy_price(double price, double cost_rate) {
+  BuyPrice b;
+  b.pc = __dmul_rn(price, __dadd_rn(1.0, cost_rate));
+  b.inv = __drcp_rn(b.pc);
+  b.thr = __dmul_rn(b.pc, 0x1p-50);
+  return b;
+}
+
+// min(desired, max(floor(RN(balance / pc)), 0)) (stock_env.hpp:91-97) without the division.
+// qa = RN(balance * inv) is within ~2^-52 relative of q = balance / pc; n = floor(qa) by the
+// 2^52-biased round-down add (exact for |qa| < 2^51).  n is floor(RN(q)) when
+//   balance - n*pc >= 0            (q >= n, so RN(q) >= n; exact sign of the FMA residual)
+//   (n+1)*pc - balance > thr*(n+1) (q is more than 2^-50 relative below n+1, so RN(q) < n+1),
+// which fails only when q is within a few ulp of an integer; that case (never seen in
+// practice) takes the reference's own division.  n < desired <= max_trade < 2^31 whenever it is
+// the result, so the int32 count is the low word of the biased sum.  Returns the quantity as a
+// double and sets qi to it as int32.
+__device__ __forceinline__ double buy_qty_nodiv(double desired, int32_t di, double balance, const BuyPrice& b,
+                                                int32_t& qi) {
+  const double qa = __dmul_rn(balance, b.inv);
+  const double t = __dadd_rd(qa, 0x1p52);
+  const double n = __dsub_rn(t, 0x1p52);
+  const double n1 = __dadd_rn(n, 1.0);
+  const bool ok = (__fma_rn(-n, b.pc, balance) >= 0.0) && (__fma_rn(n1, b.pc, -balance) > __dmul_rn(b.thr, n1));
+  double f = n;
+  int32_t fi = __double2loint(t);
+  if (!ok) {  // q within a few ulp of an integer: the reference's division decides
+    f = buy_qty_limited(desired, balance, b.pc);
+    fi = (int32_t)f;
+  }
+  const bool lim = f < desired;  // else the affordable count is >= desired: buy desired
+  const bool neg = f < 0.0;      // std::max(affordable, 0)
+  qi = lim ? (neg ? 0 : fi) : di;
+  return lim ? (neg ? 0.0 : f) : desired;
+}
+
 }  // namespace stock
 }  // namespace prb

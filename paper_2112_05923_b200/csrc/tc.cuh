@@ -139,12 +139,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // clock64 event trace (debug builds of a launch pass a buffer; null in production)
-template <int LEN>
+// (ON = false compiles every mark() away: the production instantiation carries no trace code)
+template <int LEN, bool ON = true>
 struct Tracer {
   unsigned long long* p = nullptr;
   int n = 0;
   __device__ __forceinline__ void mark() {
-    if (p && n < LEN) p[n++] = clock64();
+    if constexpr (ON) {
+      if (p && n < LEN) p[n++] = clock64();
+    }
   }
 };
 

@@ -76,3 +76,52 @@ extern "C" int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* hA, con
     ctx->sync();
   });
 }
+
+// ---- self-test of the fused rollout's conversion/division-free trade math (stock_env.cuh) ----
+#include "stock_env.cuh"
+
+namespace {
+
+__global__ void trade_math_selftest_kernel(const float* __restrict__ act, float mt, const double* __restrict__ bal,
+                                           const double* __restrict__ price, double cost, int n,
+                                           int32_t* __restrict__ desired, double* __restrict__ buy,
+                                           int32_t* __restrict__ buy_i) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t di = stock::desired_qty_f32(act[i], mt, (int32_t)mt);
+  desired[i] = di;
+  const stock::BuyPrice bp = stock::buy_price(price[i], cost);
+  int32_t qi;
+  const double d = stock::i2d_exact(di);
+  buy[i] = stock::buy_qty_nodiv(d, di, bal[i], bp, qi);
+  buy_i[i] = qi;
+}
+
+}  // namespace
+
+extern "C" int prb_debug_trade_math(prb_ctx ctx, size_t n, const float* act, double max_trade, const double* balance,
+                                    const double* price, double cost_rate, int32_t* desired, double* buy,
+                                    int32_t* buy_i) {
+  return guard([&] {
+    PRB_REQUIRE(ctx && act && balance && price && desired && buy && buy_i, PRB_ERR_USAGE,
+                "prb_debug_trade_math: NULL argument");
+    PRB_REQUIRE(max_trade == floor(max_trade) && max_trade >= 0.0 && max_trade < 4194304.0, PRB_ERR_CONFIG,
+                "prb_debug_trade_math: max_trade must be an integer < 2^22");
+    if (n == 0) return;
+    DevBuf<float> dA;
+    DevBuf<double> dB, dP, dBuy;
+    DevBuf<int32_t> dD, dBi;
+    dA.alloc(n); dB.alloc(n); dP.alloc(n); dBuy.alloc(n); dD.alloc(n); dBi.alloc(n);
+    cudaStream_t s = ctx->stream;
+    PRB_CUDA(cudaMemcpyAsync(dA.p, act, dA.bytes(), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dB.p, balance, dB.bytes(), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(dP.p, price, dP.bytes(), cudaMemcpyHostToDevice, s));
+    trade_math_selftest_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dA.p, (float)max_trade, dB.p, dP.p, cost_rate,
+                                                                          (int)n, dD.p, dBuy.p, dBi.p);
+    PRB_CHECK_LAUNCH();
+    PRB_CUDA(cudaMemcpyAsync(desired, dD.p, dD.bytes(), cudaMemcpyDeviceToHost, s));
+    PRB_CUDA(cudaMemcpyAsync(buy, dBuy.p, dBuy.bytes(), cudaMemcpyDeviceToHost, s));
+    PRB_CUDA(cudaMemcpyAsync(buy_i, dBi.p, dBi.bytes(), cudaMemcpyDeviceToHost, s));
+    ctx->sync();
+  });
+}
