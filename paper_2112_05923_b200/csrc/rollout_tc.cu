@@ -116,6 +116,41 @@ __device__ __forceinline__ void store_tile(float* __restrict__ dst, const float*
   for (int i = (n4 << 2) + threadIdx.x; i < nfl; i += kM) __stcs(dst + i, stage[i]);
 }
 
+// store_tile for the action tile, then each thread turns the float4 it copied into the desired
+// quantities (stock::desired_qty_f32) in place: conflict-free 16-byte shared accesses.
+__device__ __forceinline__ void store_tile_desired(float* __restrict__ dst, float* stage, int nfl, float mt,
+                                                   int32_t mti) {
+  const int n4 = nfl >> 2;
+  float4* s4 = reinterpret_cast<float4*>(stage);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int i = threadIdx.x; i < n4; i += kM) {
+    const float4 v = s4[i];
+    __stcs(d4 + i, v);
+    s4[i] = make_float4(__int_as_float(stock::desired_qty_f32(v.x, mt, mti)),
+                        __int_as_float(stock::desired_qty_f32(v.y, mt, mti)),
+                        __int_as_float(stock::desired_qty_f32(v.z, mt, mti)),
+                        __int_as_float(stock::desired_qty_f32(v.w, mt, mti)));
+  }
+  for (int i = (n4 << 2) + threadIdx.x; i < nfl; i += kM) {
+    const float v = stage[i];
+    __stcs(dst + i, v);
+    stage[i] = __int_as_float(stock::desired_qty_f32(v, mt, mti));
+  }
+}
+
+// Desired quantities k, k+1 (k even) of this thread's staged row, re-read from shared memory on
+// every use (volatile asm: the 30 values are not kept live next to the 30 share counts).  The
+// even stride 30 reads both with one 8-byte load, conflict-free per half-warp.
+template <int SA>
+__device__ __forceinline__ void desired_pair(const float* row, int k, int32_t& d0, int32_t& d1) {
+  if constexpr (SA % 2 == 0) {
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tc::smem_u32(row + k)) : "memory");
+  } else {
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d0) : "r"(tc::smem_u32(row + k)) : "memory");
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d1) : "r"(tc::smem_u32(row + k + 1)) : "memory");
+  }
+}
+
 // Warp-per-row copy of the staged [rows][kSLD] fp32 tile to a contiguous [rows][cols] span.
 __device__ __forceinline__ void store_rows(float* __restrict__ dst, const float* stage, int cols, int nrows,
                                            int sld = kSLD) {
@@ -320,45 +355,49 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     const float lp = s.lpc - 0.5f * zz;
     __syncthreads();
     tr.mark();
-    if (kTileAct && vec_ok)
+    // desired_k = trunc(clamp(a_k, -1, 1) * max_trade) (stock_env.hpp:83-87) ONCE per step, as
+    // int32 bit patterns written over the staged action tile: in the vectorised tile copy when it
+    // applies (each thread converts the float4 it has just stored), else row by row.
+    const bool tile_desired = kTileAct && vec_ok && a.mt_f32;
+    if (tile_desired)
+      store_tile_desired(a.b_act + ((size_t)h * a.N + e0) * A, stage, nloc * A, (float)a.max_trade,
+                         (int32_t)a.max_trade);
+    else if (kTileAct && vec_ok)
       store_tile(a.b_act + ((size_t)h * a.N + e0) * A, stage, nloc * A);
     else
       store_rows(a.b_act + ((size_t)h * a.N + e0) * A, stage, A, nloc, SA);
     tr.mark();
     // ---- env step (stock_env_step stock_env.hpp:55-103), this thread's env, fp64 ----
-    // desired_k = trunc(clamp(a_k, -1, 1) * max_trade) (stock_env.hpp:83-87) ONCE per step, as
-    // int32 bit patterns written over this thread's staged action row (the action rows were
-    // stored above; `my` is volatile so the 30 values are re-read from shared memory instead of
-    // being kept live next to the 30 share counts).  Sells run in integers except the cash
-    // arithmetic; buys use stock::buy_qty_nodiv.  No XU conversion or fp64 division is left on
-    // the balance chain (stock_env.cuh); every trade is branch-free (a zero-quantity trade
-    // leaves balance and shares bit-identical).
-    __syncthreads();  // every warp's act-row copy has read the staged actions
-    volatile float* my = stage + tid * SA;  // int32 bit patterns after this loop
-    if (a.mt_f32) {
-      const float mtf = (float)a.max_trade;
-      const int32_t mti = (int32_t)a.max_trade;
+    // The desired quantities are re-read from this thread's staged row in each loop (8-byte
+    // loads at the even stride 30: conflict-free per half-warp) instead of being kept live next
+    // to the 30 share counts.  Sells run in integers except the cash arithmetic; buys use
+    // stock::buy_qty_nodiv.  No XU conversion or fp64 division is left on the balance chain
+    // (stock_env.cuh); every trade is branch-free (a zero-quantity trade leaves balance and
+    // shares bit-identical).
+    __syncthreads();  // the act tile copy (and its in-place conversion) is complete
+    float* my = stage + tid * SA;
+    if (!tile_desired) {
+      if (a.mt_f32) {
+        const float mtf = (float)a.max_trade;
+        const int32_t mti = (int32_t)a.max_trade;
 #pragma unroll
-      for (int k = 0; k < K; ++k) my[k] = __int_as_float(stock::desired_qty_f32(my[k], mtf, mti));
-    } else {
+        for (int k = 0; k < K; ++k) my[k] = __int_as_float(stock::desired_qty_f32(my[k], mtf, mti));
+      } else {
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        my[k] = __int_as_float((int32_t)trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade)));
+        for (int k = 0; k < K; ++k)
+          my[k] = __int_as_float((int32_t)trunc(__dmul_rn(clamp_ref((double)my[k], -1.0, 1.0), a.max_trade)));
+      }
     }
     const int done = a.done_seq[h];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
-      const int32_t di = __float_as_int(my[k]);
+    auto sell = [&](int k, int32_t di) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
       const int32_t qi = (di < 0) ? -min(-di, sh[k]) : 0;
       const double qv = stock::i2d_exact(qi);
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
       sh[k] += qi;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
-      const int32_t di = __float_as_int(my[k]);
+    };
+    auto buy = [&](int k, int32_t di) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
       const double d = stock::i2d_exact(di);
       int32_t qb;
       const double qb_v = stock::buy_qty_nodiv(d, di, bal, s.bp[k], qb);
@@ -368,6 +407,20 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
       const double cost = __dmul_rn(__dmul_rn(a.cost, qv), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
       sh[k] += qi;
+    };
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      int32_t d0, d1;
+      desired_pair<SA>(my, k, d0, d1);
+      sell(k, d0);
+      if (k + 1 < K) sell(k + 1, d1);
+    }
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      int32_t d0, d1;
+      desired_pair<SA>(my, k, d0, d1);
+      buy(k, d0);
+      if (k + 1 < K) buy(k + 1, d1);
     }
     double va = bal;
 #pragma unroll
