@@ -81,16 +81,37 @@ __global__ void pm_pack_kernel(const float* __restrict__ P, PmPackOffsets o, uin
   *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(v);
 }
 
+// kPair: one CTA pair (cluster of 2 SMs) per 256 envs with cta_group::2 MMAs (M = 256).  Each
+// CTA keeps its own 128 rows of A (obs / hidden tiles) and streams HALF of every weight chunk
+// (the B columns n in [128·rank, 128·rank + 128), a contiguous half of the chunk's K-major
+// image): the per-SM weight bytes halve while the per-SM MMA work is unchanged, which is what
+// bounded the single-CTA kernel (profiles/mb/mb_l2smem.cu).  The leader (rank 0) issues every
+// MMA; commits are multicast to both CTAs' barriers; the peer's epilogue groups arrive on the
+// leader's barriers through DSMEM, and both CTAs' halves of a weight chunk are loaded by
+// .cta_group::2 tensor-map TMA that completes on the leader's `full` barrier.
+template <bool kPair>
+struct PmCfg {
+  static constexpr int kSlotB = kPair ? kSlot / 2 : kSlot;       // bytes per ring slot
+  static constexpr int kStagesT = kPair ? 2 * kStages : kStages;  // same ring bytes
+  static constexpr int kRows = kPair ? 2 * kM : kM;               // envs per (pair-)tile
+  static constexpr uint32_t kArr = kPair ? 8 : 4;                 // epilogue-warp arrivals per signal
+  // half-size copies complete no faster than whole ones (~350 clk each, one in flight per warp),
+  // so a pair CTA keeps twice as many in flight
+  static constexpr int kProd = kPair ? 2 * kProducers : kProducers;
+  static constexpr int kThr = 32 * (9 + kProd);
+};
+
+template <bool kPair>
 struct PmSmem {
-  alignas(1024) uint8_t ring[kStages][kSlot];     // weight ring (both nets, global op order)
+  alignas(1024) uint8_t ring[PmCfg<kPair>::kStagesT][PmCfg<kPair>::kSlotB];  // weight ring (global op order)
   alignas(1024) uint8_t h[2][kM * kHid * 2];      // bf16 A operands [128][256]: actor, critic
   alignas(1024) uint8_t x[kM * kX * 2];           // bf16 obs tile [128][16]
   float bias[2][3][kHid];                         // hidden-layer biases [net][layer]
   float b4a[2], b4c, sig[2], isig[2], lpc;
-  uint64_t full[kStages], empty[kStages];
+  uint64_t full[PmCfg<kPair>::kStagesT], empty[PmCfg<kPair>::kStagesT];
   uint64_t dfull[2];  // MMA -> group: layer result in TMEM
-  uint64_t ready[2];  // group -> MMA: operand written / accumulator free (4 warp arrivals)
-  uint64_t xready;    // actor group -> both MMA warps: obs tile written (4 warp arrivals)
+  uint64_t ready[2];  // group -> MMA: operand written / accumulator free (epilogue-warp arrivals)
+  uint64_t xready;    // actor group -> MMA: obs tile written
   uint64_t xfree;     // critic MMA -> actor group: the critic's L1 has consumed the obs tile
   uint64_t aepi1;     // actor group -> critic MMA: actor layer-1 epilogue done (phase offset)
   uint32_t tmem;
@@ -105,15 +126,34 @@ struct Tracer {
   }
 };
 
-__device__ __forceinline__ void group_signal(uint64_t* bar) {
+// one arrive per warp on the MMA issuer's barrier (the leader's, through DSMEM, in the peer)
+template <bool kPair>
+__device__ __forceinline__ void arrive_mma(uint64_t* bar, uint32_t rank) {
+  if (kPair && rank != 0)
+    tc::mbar_arrive_cluster(tc::mapa_shared(bar, 0));
+  else
+    tc::mbar_arrive(bar);
+}
+
+template <bool kPair>
+__device__ __forceinline__ void group_signal(uint64_t* bar, uint32_t rank) {
   tc::fence_proxy_async();  // this thread's operand stores -> async proxy
   tc::fence_before_sync();  // this thread's TMEM loads are complete
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
+  if ((threadIdx.x & 31) == 0) arrive_mma<kPair>(bar, rank);
 }
 
+template <bool kPair>
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t ph) {
+  if (kPair)
+    tc::mbar_wait_cluster(bar, ph);
+  else
+    tc::mbar_wait(bar, ph);
+}
+
+template <bool kPair>
 __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t& ph) {
-  tc::mbar_wait(bar, ph);
+  bar_wait<kPair>(bar, ph);
   ph ^= 1;
   tc::fence_after_sync();
 }
@@ -136,14 +176,20 @@ __device__ __forceinline__ void epi_hidden(uint32_t trow, const float* bias, uin
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) {
+template <bool kPair>
+__global__ void __launch_bounds__(PmCfg<kPair>::kThr, 1) pm_rollout_tc_kernel(const __grid_constant__ PmTcArgs a) {
+  using Cfg = PmCfg<kPair>;
+  constexpr int kSlotB = Cfg::kSlotB, kStagesT = Cfg::kStagesT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  PmSmem& s = *reinterpret_cast<PmSmem*>(smem_raw);
+  PmSmem<kPair>& s = *reinterpret_cast<PmSmem<kPair>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ntiles = (a.N + kM - 1) / kM;
+  const uint32_t rank = kPair ? tc::cluster_ctarank() : 0u;
+  const int unit = kPair ? (int)blockIdx.x / 2 : (int)blockIdx.x;     // pair (or CTA) index
+  const int nunits = kPair ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int ntiles = (a.N + Cfg::kRows - 1) / Cfg::kRows;
   const float* P = a.params;
 
-  for (int i = tid; i < 2 * 3 * kHid; i += kThreads) {
+  for (int i = tid; i < 2 * 3 * kHid; i += Cfg::kThr) {
     const int net = i / (3 * kHid), L = (i / kHid) % 3, n = i % kHid;
     const int w = net ? a.o.c_w[L] : a.o.a_w[L];
     const int in = (L == 0) ? a.o.S : kHid;
@@ -158,21 +204,27 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
   if (tid == 0) {
     s.b4c = P[a.o.c_w[3] + kHid];
     s.lpc = -kLogTwoPiF - P[a.o.log_std] - P[a.o.log_std + 1];
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kStagesT; ++i) {
       tc::mbar_init(&s.full[i], 1);
       tc::mbar_init(&s.empty[i], 1);
     }
     for (int n = 0; n < 2; ++n) {
       tc::mbar_init(&s.dfull[n], 1);
-      tc::mbar_init(&s.ready[n], 4);
+      tc::mbar_init(&s.ready[n], Cfg::kArr);
     }
-    tc::mbar_init(&s.xready, 4);
+    tc::mbar_init(&s.xready, Cfg::kArr);
     tc::mbar_init(&s.xfree, 1);
-    tc::mbar_init(&s.aepi1, 4);
+    tc::mbar_init(&s.aepi1, Cfg::kArr);
   }
-  if (warp == 8) tc::tmem_alloc(&s.tmem, kTmemCols);
+  if (warp == 8) {
+    if (kPair)
+      tc::tmem_alloc_pair(&s.tmem, kTmemCols);
+    else
+      tc::tmem_alloc(&s.tmem, kTmemCols);
+  }
   tc::fence_before_sync();
   __syncthreads();
+  if (kPair) tc::cluster_sync();  // both CTAs' barriers initialised before any DSMEM arrive
   tc::fence_after_sync();
   const uint32_t tbase = s.tmem;
 
@@ -181,52 +233,74 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
   // The critic runs about one epilogue behind the actor (C1 waits for the actor's
   // layer-1 epilogue), so this order is also the order in which the operands
   // become ready: one ring serves both nets without head-of-line blocking.
-  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int G = my_tiles * (a.H + 1);  // steps this CTA runs
+  const int my_tiles = (ntiles - unit + nunits - 1) / nunits;
+  const int G = my_tiles * (a.H + 1);  // steps this CTA (pair) runs
+  // every chunk of the global order, in order: f(it, net, chunk)
+  auto for_each_chunk = [&](auto&& f) {
+    uint32_t it = 0;
+    for (int g = 0; g <= G; ++g)
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        if ((g == G && k != 1) || (g == 0 && k == 1)) continue;
+        const int net = kOpNet[k], layer = kOpLayer[k], nq = op_nchunks(layer);
+#pragma unroll 1
+        for (int q = 0; q < nq; ++q, ++it) f(it, net, op_chunk(layer, q));
+      }
+  };
   if (warp >= 9) {  // ---------------- producers ----------------
     // Bulk copies issued by one warp complete roughly one at a time
-    // (profiles/mb/mb_l2smem.cu); chunk `it` goes to producer it % kProducers.
+    // (profiles/mb/mb_l2smem.cu); chunk `it` goes to producer it % kProd.
     const int pr = warp - 9;
     if (lane == 0) {
-      uint32_t it = 0;
-      for (int g = 0; g <= G; ++g)
-#pragma unroll 1
-        for (int k = 0; k < 8; ++k) {
-          if ((g == G && k != 1) || (g == 0 && k == 1)) continue;
-          const int net = kOpNet[k], layer = kOpLayer[k], nq = op_nchunks(layer);
-#pragma unroll 1
-          for (int q = 0; q < nq; ++q, ++it) {
-            if ((int)(it % kProducers) != pr) continue;
-            const uint32_t slot = it % kStages, use = it / kStages;
-            const int c = op_chunk(layer, q);
-            if (use) tc::mbar_wait(&s.empty[slot], (use - 1) & 1);
-            tc::mbar_arrive_expect_tx(&s.full[slot], chunk_bytes(c));
-            tc::bulk_g2s(s.ring[slot], a.pack + (size_t)net * kNetPack + (size_t)c * kSlot, chunk_bytes(c),
-                         &s.full[slot]);
-          }
+      for_each_chunk([&](uint32_t it, int net, int c) {
+        if ((int)(it % Cfg::kProd) != pr) return;
+        const uint32_t slot = it % kStagesT, use = it / kStagesT;
+        if (use) bar_wait<kPair>(&s.empty[slot], (use - 1) & 1);
+        if constexpr (kPair) {
+          // this CTA's half of chunk c: rows [off/256, +half/256) of the [.][128] bf16 view, 16-row boxes;
+          // both halves complete on the leader's full[slot], which expects the whole chunk
+          const uint32_t half = chunk_bytes(c) / 2;
+          const uint32_t off = (uint32_t)net * kNetPack + (uint32_t)c * kSlot + rank * half;
+          const uint32_t bar = tc::mapa_shared(&s.full[slot], 0);
+          if (rank == 0) tc::mbar_arrive_expect_tx(&s.full[slot], 2 * half);
+          for (uint32_t b = 0; b < half; b += 4096)
+            tc::tma_load_2d_pair(s.ring[slot] + b, &a.pack_map, 0, (int)((off + b) >> 8), bar);
+        } else {
+          tc::mbar_arrive_expect_tx(&s.full[slot], chunk_bytes(c));
+          tc::bulk_g2s(s.ring[slot], a.pack + (size_t)net * kNetPack + (size_t)c * kSlot, chunk_bytes(c),
+                       &s.full[slot]);
         }
+      });
     }
-  } else if (warp == 8) {  // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      constexpr uint32_t ID_256 = tc::idesc_bf16(kM, kHid), ID_16 = tc::idesc_bf16(kM, 16);
+  } else if (warp == 8) {  // ---------------- MMA issuer (leader) / relay (peer) ----------------
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t ID_256 = tc::idesc_bf16(Cfg::kRows, kHid), ID_16 = tc::idesc_bf16(Cfg::kRows, 16);
       const uint32_t x_addr = tc::smem_u32(s.x), ring0 = tc::smem_u32(s.ring[0]);
       uint32_t it = 0, rph[2] = {0, 0}, xph = 0, eph = 0;
       Tracer tr;
       if (a.trace && blockIdx.x == 0) tr.p = a.trace + 2 * kPmTraceLen;
       unsigned long long waited = 0;  // trace: clocks spent waiting for weight chunks
-      auto take = [&]() -> uint32_t {  // next weight chunk: wait until it has landed
-        const uint32_t slot = it % kStages;
-        if (tr.p) {
-          const unsigned long long t0 = clock64();
-          tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
-          waited += clock64() - t0;
-        } else {
-          tc::mbar_wait(&s.full[slot], (it / kStages) & 1);
-        }
-        return ring0 + slot * kSlot;
+      auto take = [&]() -> uint32_t {  // next weight chunk: wait until it (both halves) has landed
+        const uint32_t slot = it % kStagesT, ph = (it / kStagesT) & 1;
+        const unsigned long long t0 = tr.p ? clock64() : 0ull;
+        bar_wait<kPair>(&s.full[slot], ph);  // both halves (pair: the peer's TMA completes here too)
+        if (tr.p) waited += clock64() - t0;
+        return ring0 + slot * kSlotB;
       };
-      auto release = [&]() {  // the chunk's MMAs done -> slot reusable
-        tc::mma_commit(&s.empty[it % kStages]);
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
+        if (kPair)
+          tc::mma_bf16_pair(d, ad, bd, id, acc);
+        else
+          tc::mma_bf16(d, ad, bd, id, acc);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (kPair)
+          tc::mma_commit_pair(bar);
+        else
+          tc::mma_commit(bar);
+      };
+      auto release = [&]() {  // the chunk's MMAs done -> slot reusable (in both CTAs)
+        commit(&s.empty[it % kStagesT]);
         ++it;
       };
       for (int g = 0; g <= G; ++g)
@@ -235,13 +309,13 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
           if ((g == G && k != 1) || (g == 0 && k == 1)) continue;
           const int net = kOpNet[k], layer = kOpLayer[k];
           if (net == 0 && layer == 0) {
-            tc::mbar_wait(&s.xready, xph);  // obs tile written
+            bar_wait<kPair>(&s.xready, xph);  // obs tile written
             xph ^= 1;
           } else {
-            tc::mbar_wait(&s.ready[net], rph[net]);  // operand written / accumulator read
+            bar_wait<kPair>(&s.ready[net], rph[net]);  // operand written / accumulator read
             rph[net] ^= 1;
             if (net == 1 && layer == 0) {  // the actor's layer-1 epilogue is done (phase offset)
-              tc::mbar_wait(&s.aepi1, eph);
+              bar_wait<kPair>(&s.aepi1, eph);
               eph ^= 1;
             }
           }
@@ -249,30 +323,31 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
           tr.mark();
           const uint32_t d = tbase + (uint32_t)net * kHid;
           const uint32_t h_addr = tc::smem_u32(s.h[net]);
+          // B operands: [n][k] K-major; in pair mode each CTA's slot holds its n-half, same strides
           if (layer == 0) {  // [128 x 16] obs . [16 x 256]
             const uint32_t b = take();
-            tc::mma_bf16(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(b, 128, kX * 16), ID_256, 0);
+            mma(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(b, 128, kX * 16), ID_256, 0);
             release();
-            if (net == 1) tc::mma_commit(&s.xfree);
+            if (net == 1) commit(&s.xfree);
           } else if (layer < 3) {  // [128 x 256] h . [256 x 256], kCPL chunks of kKC/16 K-steps
 #pragma unroll 1
             for (int q = 0; q < kCPL; ++q) {
               const uint32_t b = take();
 #pragma unroll
               for (int j = 0; j < kKC / 16; ++j)
-                tc::mma_bf16(d, tc::smem_desc(h_addr + (q * (kKC / 16) + j) * 256, 128, kHid * 16),
-                             tc::smem_desc(b + j * 256, 128, kKC * 16), ID_256, (q | j) != 0);
+                mma(d, tc::smem_desc(h_addr + (q * (kKC / 16) + j) * 256, 128, kHid * 16),
+                    tc::smem_desc(b + j * 256, 128, kKC * 16), ID_256, (q | j) != 0);
               release();
             }
           } else {  // head: [128 x 256] h . [256 x 16]
             const uint32_t b = take();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              tc::mma_bf16(d, tc::smem_desc(h_addr + j * 256, 128, kHid * 16),
-                           tc::smem_desc(b + j * 256, 128, kHid * 16), ID_16, j != 0);
+              mma(d, tc::smem_desc(h_addr + j * 256, 128, kHid * 16), tc::smem_desc(b + j * 256, 128, kHid * 16),
+                  ID_16, j != 0);
             release();
           }
-          tc::mma_commit(&s.dfull[net]);
+          commit(&s.dfull[net]);
           tr.mark();
           if (tr.p && g < 8 && k == 7) a.trace[3 * kPmTraceLen + g] = waited;
         }
@@ -285,8 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
     Tracer tr;
     if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
     const size_t N = a.N;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const size_t e = (size_t)tile * kM + row;
+    for (int tile = unit; tile < ntiles; tile += nunits) {
+      const size_t e = (size_t)tile * Cfg::kRows + rank * kM + row;
       const bool live = e < N;
       double st[6];
       int32_t steps = 0, idx = 0;
@@ -303,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
 #pragma unroll
         for (int j = 0; j < 6; ++j) o[j] = (float)st[j];
         if (!first) {  // the critic's L1 of the previous step has consumed X
-          tc::mbar_wait(&s.xfree, fph);
+          bar_wait<kPair>(&s.xfree, fph);
           fph ^= 1;
         }
         first = false;
@@ -312,18 +387,18 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
               make_uint4(tc::pack_bf16(o[0], o[1]), tc::pack_bf16(o[2], o[3]), tc::pack_bf16(o[4], o[5]), 0u);
           *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(row, 8, kX)) = make_uint4(0u, 0u, 0u, 0u);
         }
-        group_signal(&s.xready);
+        group_signal<kPair>(&s.xready, rank);
         tr.mark();
 #pragma unroll 1
         for (int L = 0; L < 3; ++L) {
-          group_wait(&s.dfull[0], dph);
+          group_wait<kPair>(&s.dfull[0], dph);
           tr.mark();
           epi_hidden(trow, s.bias[0][L], s.h[0], row);
-          group_signal(&s.ready[0]);
-          if (L == 0 && (threadIdx.x & 31) == 0) tc::mbar_arrive(&s.aepi1);
+          group_signal<kPair>(&s.ready[0], rank);
+          if (L == 0 && (threadIdx.x & 31) == 0) arrive_mma<kPair>(&s.aepi1, rank);
           tr.mark();
         }
-        group_wait(&s.dfull[0], dph);
+        group_wait<kPair>(&s.dfull[0], dph);
         tr.mark();
         float mv[16];
         tc::tmem_ld16(trow, mv);
@@ -383,24 +458,24 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
     Tracer tr;
     if (a.trace && blockIdx.x == 0 && tid == kM) tr.p = a.trace + kPmTraceLen;
     const size_t N = a.N;
-    group_signal(&s.ready[1]);  // critic accumulator free
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const size_t e = (size_t)tile * kM + row;
+    group_signal<kPair>(&s.ready[1], rank);  // critic accumulator free
+    for (int tile = unit; tile < ntiles; tile += nunits) {
+      const size_t e = (size_t)tile * Cfg::kRows + rank * kM + row;
       const bool live = e < N;
       for (int h = 0; h <= a.H; ++h) {
 #pragma unroll 1
         for (int L = 0; L < 3; ++L) {
-          group_wait(&s.dfull[1], dph);
+          group_wait<kPair>(&s.dfull[1], dph);
           tr.mark();
           epi_hidden(trow, s.bias[1][L], s.h[1], row);
-          group_signal(&s.ready[1]);
+          group_signal<kPair>(&s.ready[1], rank);
           tr.mark();
         }
-        group_wait(&s.dfull[1], dph);
+        group_wait<kPair>(&s.dfull[1], dph);
         tr.mark();
         float vv[16];
         tc::tmem_ld16(trow, vv);
-        group_signal(&s.ready[1]);  // accumulator read: the next step's L1 may overwrite it
+        group_signal<kPair>(&s.ready[1], rank);  // accumulator read: the next step's L1 may overwrite it
         const float value = vv[0] + s.b4c;
         tr.mark();
         if (live) {
@@ -414,12 +489,18 @@ __global__ void __launch_bounds__(kThreads, 1) pm_rollout_tc_kernel(PmTcArgs a) 
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 8) tc::tmem_dealloc(tbase, kTmemCols);
+  if (kPair) tc::cluster_sync();  // the peer is done with TMEM and DSMEM before the pair deallocates
+  if (warp == 8) {
+    if (kPair)
+      tc::tmem_dealloc_pair(tbase, kTmemCols);
+    else
+      tc::tmem_dealloc(tbase, kTmemCols);
+  }
 }
 
 }  // namespace
 
-size_t pm_rollout_tc_smem() { return sizeof(PmSmem); }
+size_t pm_rollout_tc_smem() { return sizeof(PmSmem<true>) > sizeof(PmSmem<false>) ? sizeof(PmSmem<true>) : sizeof(PmSmem<false>); }
 
 void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, cudaStream_t s) {
   const int total = 2 * (4096 + 2 * 65536 + 4096);
@@ -427,16 +508,69 @@ void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, 
   PRB_CHECK_LAUNCH();
 }
 
-void launch_pm_rollout_tc(const PmTcArgs& a, int num_sms, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(PmSmem)));
-    attr = true;
+// The pack as a 2-D bf16 tensor [kPmPackBytes / 256 rows][128], boxes of [16 rows][128] = 4 KB
+// (every half chunk is a whole number of boxes).  cuTensorMapEncodeTiled through the runtime's
+// driver entry point (no -lcuda).
+void encode_pm_pack_map(CUtensorMap* map, const uint8_t* pack) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PRB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    PRB_REQUIRE(p && q == cudaDriverEntryPointSuccess, PRB_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<Fn>(p);
   }
-  const int ntiles = (a.N + kM - 1) / kM;
-  const int grid = ntiles < num_sms ? ntiles : num_sms;
-  pm_rollout_tc_kernel<<<grid, kThreads, sizeof(PmSmem), s>>>(a);
+  const cuuint64_t dims[2] = {128, kPmPackBytes / 256};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {128, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint8_t*>(pack), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PRB_REQUIRE(r == CUDA_SUCCESS, PRB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+// PRB_PM_PAIR=1 selects the CTA-pair kernel; the single-CTA kernel is the default because it is
+// faster: 1.37e9 vs 1.13e9 transitions/s at configs[2].  The pair halves the
+// per-SM weight bytes, but the layer time was not bound by them: each M=256 pair MMA takes as
+// long as an M=128 single one (same per-SM tensor throughput), the epilogues are bound by the
+// 16/clk/SM MUFU tanh rate, and every epilogue -> MMA hand-off now crosses SMs.
+void launch_pm_rollout_tc(const PmTcArgs& a, int num_sms, cudaStream_t s) {
+  static int pair = -1;
+  if (pair < 0) {
+    const char* e = getenv("PRB_PM_PAIR");
+    pair = (e && e[0] == '1') ? 1 : 0;
+    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(PmSmem<false>)));
+    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(PmSmem<true>)));
+  }
+  if (pair) {
+    PmTcArgs ap = a;
+    encode_pm_pack_map(&ap.pack_map, a.pack);
+    const int ntiles = (a.N + 2 * kM - 1) / (2 * kM);
+    const int npairs = ntiles < num_sms / 2 ? ntiles : num_sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * npairs);
+    cfg.blockDim = dim3(PmCfg<true>::kThr);
+    cfg.dynamicSmemBytes = sizeof(PmSmem<true>);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PRB_CUDA(cudaLaunchKernelEx(&cfg, pm_rollout_tc_kernel<true>, ap));
+  } else {
+    const int ntiles = (a.N + kM - 1) / kM;
+    const int grid = ntiles < num_sms ? ntiles : num_sms;
+    pm_rollout_tc_kernel<false><<<grid, PmCfg<false>::kThr, sizeof(PmSmem<false>), s>>>(a);
+  }
   PRB_CHECK_LAUNCH();
 }
 

@@ -1,5 +1,6 @@
 // rollout_pm_tc.h -- launch descriptor of the tcgen05 PointMass 3x256 rollout.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -17,6 +18,7 @@ struct PmPackOffsets {
 };
 
 struct PmTcArgs {
+  CUtensorMap pack_map; // the pack as a 2-D bf16 tensor [kPmPackBytes/256][128], box [16][128] (CTA-pair kernel)
   const uint8_t* pack;  // kPmPackBytes, from launch_pm_pack
   const float* params;
   PmPackOffsets o;

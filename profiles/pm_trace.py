@@ -20,3 +20,5 @@ for h in steps:
     print("  mma   :", " ".join(f"{x - t0:6d}" for x in m))
     if h < 8:
         print("  mma waited for chunks (cumulative):", t[3, h])
+        if t[3, 16 + h]:
+            print("  ... of which waiting for the peer CTA's half (cumulative):", t[3, 16 + h])

@@ -541,3 +541,17 @@ def _pm_log_std(agent):
     flat = agent.flatten_params()
     pa = 6 * 256 + 256 + 2 * (256 * 256 + 256) + 256 * 2 + 2
     return flat[pa:pa + 2]
+
+
+def test_collect_pointmass_cta_pair_kernel():
+    """The opt-in CTA-pair (cta_group::2) PointMass kernel (PRB_PM_PAIR=1, read once per
+    process) passes the same replay / tolerance checks as the default kernel."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PRB_PM_PAIR="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_pointmass_rollout"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
