@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libprb.so")
+LIB_PATH = os.environ.get("PRB_LIB_PATH") or os.path.join(_HERE, "libprb.so")  # override: A/B builds
 
 _lock = threading.Lock()
 _lib = None
