@@ -166,9 +166,11 @@ __device__ __forceinline__ void epi_hidden(uint32_t trow, const float* bias, uin
     tc::tmem_ld32(trow + c, v);
     uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      pk[i] = tc::pack_bf16(tc::tanh_fast(__uint_as_float(v[2 * i]) + bias[c + 2 * i]),
-                            tc::tanh_fast(__uint_as_float(v[2 * i + 1]) + bias[c + 2 * i + 1]));
+    for (int i = 0; i < 16; ++i) {
+      float z0 = __uint_as_float(v[2 * i]), z1 = __uint_as_float(v[2 * i + 1]);
+      tc::add2(z0, z1, bias[c + 2 * i], bias[c + 2 * i + 1]);
+      pk[i] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       *reinterpret_cast<uint4*>(hb + tc::kmajor_offset(row, c + 8 * q, kHid)) =

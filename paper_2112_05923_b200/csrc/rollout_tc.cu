@@ -74,9 +74,11 @@ __device__ __forceinline__ void epilogue64(uint32_t tlane, int col, const float*
     tc::tmem_ld16(tlane + col + c, v);
     uint32_t pk[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      pk[i] = tc::pack_bf16(tc::tanh_fast(v[2 * i] + add[col + c + 2 * i]),
-                            tc::tanh_fast(v[2 * i + 1] + add[col + c + 2 * i + 1]));
+    for (int i = 0; i < 8; ++i) {
+      float z0 = v[2 * i], z1 = v[2 * i + 1];
+      tc::add2(z0, z1, add[col + c + 2 * i], add[col + c + 2 * i + 1]);
+      pk[i] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
+    }
     *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c, 64)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c + 8, 64)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }

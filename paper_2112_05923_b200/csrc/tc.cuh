@@ -237,6 +237,13 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
+// (x0, x1) += (b0, b1) as one packed FADD2 (sm_100 add.rn.f32x2; same rounding as two FADDs)
+__device__ __forceinline__ void add2(float& x0, float& x1, float b0, float b1) {
+  asm("{.reg .b64 a, b; mov.b64 a, {%0,%1}; mov.b64 b, {%2,%3}; add.rn.f32x2 a, a, b; mov.b64 {%0,%1}, a;}"
+      : "+f"(x0), "+f"(x1)
+      : "f"(b0), "f"(b1));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
