@@ -311,8 +311,8 @@ PRB_API int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* A, const f
 /* Per element i, the device functions the tcgen05 stock rollout uses for
  * stock_env_step (stock_env.hpp:83-97): desired[i] = trunc(clamp(act[i],-1,1)
  * * max_trade) and buy[i] = buy_i[i] = min(desired, max(floor(balance /
- * (price * (1 + cost_rate))), 0)) (for desired > 0; the buy of desired <= 0 is
- * not defined by the reference and returns desired).  max_trade: integer < 2^22. */
+ * (price * (1 + cost_rate))), 0)) (for desired > 0; desired <= 0 is no buy in the
+ * reference and gives 0).  max_trade: integer < 2^22. */
 PRB_API int prb_debug_trade_math(prb_ctx ctx, size_t n, const float* act, double max_trade, const double* balance,
                                  const double* price, double cost_rate, int32_t* desired, double* buy,
                                  int32_t* buy_i);

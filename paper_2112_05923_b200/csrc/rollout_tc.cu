@@ -140,6 +140,16 @@ __device__ __forceinline__ void store_tile_desired(float* __restrict__ dst, floa
   }
 }
 
+// int32 -> double, exact either way: the XU conversion (1 issue slot, quarter-rate pipe) or the
+// biased DADD (3 issue slots on the FMA/ALU pipes); PRB_TC_I2D_EXACT selects the latter.
+__device__ __forceinline__ double to_f64(int32_t i) {
+#ifdef PRB_TC_I2D_EXACT
+  return stock::i2d_exact(i);
+#else
+  return (double)i;
+#endif
+}
+
 // Desired quantities k, k+1 (k even) of this thread's staged row, re-read from shared memory on
 // every use (volatile asm: the 30 values are not kept live next to the 30 share counts).  The
 // even stride 30 reads both with one 8-byte load, conflict-free per half-warp.
@@ -373,9 +383,8 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     // The desired quantities are re-read from this thread's staged row in each loop (8-byte
     // loads at the even stride 30: conflict-free per half-warp) instead of being kept live next
     // to the 30 share counts.  Sells run in integers except the cash arithmetic; buys use
-    // stock::buy_qty_nodiv.  No XU conversion or fp64 division is left on the balance chain
-    // (stock_env.cuh); every trade is branch-free (a zero-quantity trade leaves balance and
-    // shares bit-identical).
+    // stock::buy_qty_i32 (no fp64 division on the balance chain, stock_env.cuh); every trade is
+    // branch-free (a zero-quantity trade leaves balance and shares bit-identical).
     __syncthreads();  // the act tile copy (and its in-place conversion) is complete
     float* my = stage + tid * SA;
     if (!tile_desired) {
@@ -392,19 +401,16 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     }
     const int done = a.done_seq[h];
     auto sell = [&](int k, int32_t di) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
-      const int32_t qi = (di < 0) ? -min(-di, sh[k]) : 0;
-      const double qv = stock::i2d_exact(qi);
+      const int32_t qi = min(max(di, -sh[k]), 0);
+      const double qv = to_f64(qi);
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(qv)), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
       sh[k] += qi;
     };
     auto buy = [&](int k, int32_t di) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
-      const double d = stock::i2d_exact(di);
-      int32_t qb;
-      const double qb_v = stock::buy_qty_nodiv(d, di, bal, s.bp[k], qb);
-      const double qv = (di > 0) ? qb_v : 0.0;
-      const int32_t qi = (di > 0) ? qb : 0;
+      const int32_t qi = stock::buy_qty_i32(di, bal, s.bp[k]);
+      const double qv = to_f64(qi);
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, qv), price);
       bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, price), cost));
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     }
     double va = bal;
 #pragma unroll
-    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn(stock::i2d_exact(sh[k]), s.p1[k]));
+    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn(to_f64(sh[k]), s.p1[k]));
     const double rw = __dsub_rn(va, vb);
     ret = __dadd_rn(ret, rw);
     // next step's value_before: the same shares at close[t+1] plus the same balance is exactly

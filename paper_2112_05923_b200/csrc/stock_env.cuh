@@ -73,32 +73,24 @@ __device__ __forceinline__ BuyPrice buy_price(double price, double cost_rate) {
   return b;
 }
 
-// min(desired, max(floor(RN(balance / pc)), 0)) (stock_env.hpp:91-97) without the division.
-// qa = RN(balance * inv) is within ~2^-52 relative of q = balance / pc; n = floor(qa) by the
-// 2^52-biased round-down add (exact for |qa| < 2^51).  n is floor(RN(q)) when
-//   balance - n*pc >= 0            (q >= n, so RN(q) >= n; exact sign of the FMA residual)
-//   (n+1)*pc - balance > thr*(n+1) (q is more than 2^-50 relative below n+1, so RN(q) < n+1),
-// which fails only when q is within a few ulp of an integer; that case (never seen in
-// practice) takes the reference's own division.  n < desired <= max_trade < 2^31 whenever it is
-// the result, so the int32 count is the low word of the biased sum.  Returns the quantity as a
-// double and sets qi to it as int32.
-__device__ __forceinline__ double buy_qty_nodiv(double desired, int32_t di, double balance, const BuyPrice& b,
-                                                int32_t& qi) {
+// Buy quantity min(desired, max(floor(RN(balance / pc)), 0)) (stock_env.hpp:91-97) as int32,
+// without the division.  qa = RN(balance · inv) is within 2^-51·q of q = balance / pc (two
+// roundings), RN(q) within 2^-53·q.  For 0 < qa < 2^31 those are < 2^-19.7, so when the fraction
+// of qa is more than 2^-19 away from both integers, q and RN(q) lie strictly inside
+// (floor(qa), floor(qa) + 1) and floor(RN(q)) = floor(qa) = n.  n comes from the 2^52-biased
+// round-down add; its int32 value is the low word.  Any lane outside that certificate (quotient
+// within 2^-19 of an integer, balance <= 0, absurd cash) takes the reference's own division; the
+// warp-uniform vote keeps that path out of line.  Non-buys (desired <= 0) give 0.
+__device__ __forceinline__ int32_t buy_qty_i32(int32_t di, double balance, const BuyPrice& b) {
   const double qa = __dmul_rn(balance, b.inv);
   const double t = __dadd_rd(qa, 0x1p52);
-  const double n = __dsub_rn(t, 0x1p52);
-  const double n1 = __dadd_rn(n, 1.0);
-  const bool ok = (__fma_rn(-n, b.pc, balance) >= 0.0) && (__fma_rn(n1, b.pc, -balance) > __dmul_rn(b.thr, n1));
-  double f = n;
-  int32_t fi = __double2loint(t);
-  if (!ok) {  // q within a few ulp of an integer: the reference's division decides
-    f = buy_qty_limited(desired, balance, b.pc);
-    fi = (int32_t)f;
+  const double frac = __dsub_rn(qa, __dsub_rn(t, 0x1p52));
+  const bool ok = (fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-19) && (fabs(__dsub_rn(qa, 0x1p30)) < 0x1p30);
+  int32_t n = __double2loint(t);
+  if (__any_sync(0xffffffffu, !ok)) {
+    if (!ok) n = (int32_t)buy_qty_limited((double)di, balance, b.pc);
   }
-  const bool lim = f < desired;  // else the affordable count is >= desired: buy desired
-  const bool neg = f < 0.0;      // std::max(affordable, 0)
-  qi = lim ? (neg ? 0 : fi) : di;
-  return lim ? (neg ? 0.0 : f) : desired;
+  return max(min(n, di), 0);
 }
 
 }  // namespace stock

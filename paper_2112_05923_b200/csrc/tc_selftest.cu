@@ -86,15 +86,17 @@ __global__ void trade_math_selftest_kernel(const float* __restrict__ act, float 
                                            const double* __restrict__ price, double cost, int n,
                                            int32_t* __restrict__ desired, double* __restrict__ buy,
                                            int32_t* __restrict__ buy_i) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  // every lane runs the math (buy_qty_i32 votes across the warp); only in-range lanes store
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = i0 < n ? i0 : n - 1;
   const int32_t di = stock::desired_qty_f32(act[i], mt, (int32_t)mt);
-  desired[i] = di;
   const stock::BuyPrice bp = stock::buy_price(price[i], cost);
-  int32_t qi;
-  const double d = stock::i2d_exact(di);
-  buy[i] = stock::buy_qty_nodiv(d, di, bal[i], bp, qi);
-  buy_i[i] = qi;
+  const int32_t qi = stock::buy_qty_i32(di, bal[i], bp);
+  if (i0 < n) {
+    desired[i] = di;
+    buy[i] = (double)qi;
+    buy_i[i] = qi;
+  }
 }
 
 }  // namespace
