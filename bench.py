@@ -73,6 +73,13 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device, self.rows, self.proc, self.nvml, self.stop_evt = device, [], None, None, threading.Event()
+        self.window = None  # (t0, t1) wall times of the timed region; samples outside it are dropped
+
+    def begin(self):
+        self.t_begin = time.perf_counter()
+
+    def end(self):
+        self.window = (self.t_begin, time.perf_counter())
 
     def start(self):
         try:
@@ -87,7 +94,7 @@ class ClockSampler:
                     try:
                         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                         rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.rows.append((sm, mx, rs))
+                        self.rows.append((sm, mx, rs, time.perf_counter()))
                     except Exception:
                         pass
                     self.stop_evt.wait(0.002)
@@ -114,7 +121,8 @@ class ClockSampler:
             p = [x.strip() for x in line.split(",")]
             if len(p) >= 6 and p[0].replace(".", "").isdigit():
                 rs = {n for n, v in zip(names, p[2:6]) if v.lower().startswith("active")}
-                self.rows.append((float(p[0]), float(p[1]) if p[1].replace(".", "").isdigit() else None, rs))
+                self.rows.append((float(p[0]), float(p[1]) if p[1].replace(".", "").isdigit() else None, rs,
+                                  time.perf_counter()))
 
     def stop(self):
         self.stop_evt.set()
@@ -129,6 +137,8 @@ class ClockSampler:
         return self.summary()
 
     def summary(self):
+        if self.window is not None:  # the sampler runs from before the warm-up: keep the timed region only
+            self.rows = [r for r in self.rows if self.window[0] <= r[3] <= self.window[1]]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows]
@@ -255,18 +265,20 @@ def run_ours(args, d: Dist):
     agent = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=7 + d.rank)
     ro = pr.Rollout.for_env(env, H)
 
-    # ---- warm-up ----
+    # ---- warm-up (the clock sampler is already polling, so it is warm when the region starts) ----
+    clocks = ClockSampler(d.local)
+    clocks.start()
     for i in range(args.warmup):
         ro.collect(agent, env, seed=1000 + i)
     ctx.synchronize()
 
     # ---- timed region: K rollout collections, CUDA events on the launching stream ----
     lib.prb_ctx_profile(ctx.h, 1)  # per-kernel event pairs inside the region (kernel shares / roofline)
-    clocks = ClockSampler(d.local)
     d.barrier()
     ctx.synchronize()
-    clocks.start()
+    clocks.begin()
     dev_ms = time_region(lib, ctx, lambda: [ro.collect(agent, env, seed=2000 + i) for i in range(args.steps)])
+    clocks.end()
     clk = clocks.stop()
     prof = {}
     for name, kind in (("policy_fwd_sample", 0), ("env_stock_step", 1), ("stock_rollout_fused", 7)):
@@ -637,7 +649,7 @@ def pinned(nbytes: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--envs", type=int, default=65536)
