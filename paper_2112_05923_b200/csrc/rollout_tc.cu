@@ -47,8 +47,8 @@ struct TcSmem {
   alignas(128) uint8_t w3a[32 * 64 * 2];   // B [32][64]   (rows >= A zero)
   alignas(128) uint8_t w3c[16 * 64 * 2];   // B [16][64]   (row 0 = critic head)
   alignas(128) uint8_t x[kM * 64 * 2];     // A tile: [128][32] obs, [128][64] h, fp32 [128][31] staging
-  float c1[128];
-  float b2[128];
+  alignas(16) float c1[128];
+  alignas(16) float b2[128];
   float b3[32];
   float sig[32], isig[32];
   float b3c, lpc;
@@ -73,11 +73,15 @@ __device__ __forceinline__ void epilogue64(uint32_t tlane, int col, const float*
     float v[16];
     tc::tmem_ld16(tlane + col + c, v);
     uint32_t pk[8];
+    const float4* add4 = reinterpret_cast<const float4*>(add + col + c);  // 16-byte aligned (TcSmem)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float z0 = v[2 * i], z1 = v[2 * i + 1];
-      tc::add2(z0, z1, add[col + c + 2 * i], add[col + c + 2 * i + 1]);
-      pk[i] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
+    for (int j = 0; j < 4; ++j) {
+      const float4 b = add4[j];
+      float z0 = v[4 * j], z1 = v[4 * j + 1], z2 = v[4 * j + 2], z3 = v[4 * j + 3];
+      tc::add2(z0, z1, b.x, b.y);
+      tc::add2(z2, z3, b.z, b.w);
+      pk[2 * j] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
+      pk[2 * j + 1] = tc::pack_bf16(tc::tanh_fast(z2), tc::tanh_fast(z3));
     }
     *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c, 64)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c + 8, 64)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -151,15 +155,17 @@ __device__ __forceinline__ double to_f64(int32_t i) {
 }
 
 // Desired quantities k, k+1 (k even) of this thread's staged row, re-read from shared memory on
-// every use (volatile asm: the 30 values are not kept live next to the 30 share counts).  The
+// every use (volatile asm: the 30 values are not kept live next to the 30 share counts; no memory
+// clobber, so the shared price loads around it can still be merged -- volatile asm keeps its
+// order relative to the __syncthreads that publish the staged row).  The
 // even stride 30 reads both with one 8-byte load, conflict-free per half-warp.
 template <int SA>
 __device__ __forceinline__ void desired_pair(const float* row, int k, int32_t& d0, int32_t& d1) {
   if constexpr (SA % 2 == 0) {
-    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tc::smem_u32(row + k)) : "memory");
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(d0), "=r"(d1) : "r"(tc::smem_u32(row + k)));
   } else {
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d0) : "r"(tc::smem_u32(row + k)) : "memory");
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d1) : "r"(tc::smem_u32(row + k + 1)) : "memory");
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d0) : "r"(tc::smem_u32(row + k)));
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(d1) : "r"(tc::smem_u32(row + k + 1)));
   }
 }
 
