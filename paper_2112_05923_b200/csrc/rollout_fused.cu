@@ -444,6 +444,10 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
       ta.close_tk = f.close_tk; ta.feat = f.feat;
       ta.cap = f.cap; ta.max_trade = f.max_trade; ta.cost = f.cost;
       ta.mt_f32 = (f.max_trade == floor(f.max_trade) && f.max_trade >= 0.0 && f.max_trade < 4194304.0) ? 1 : 0;
+      {
+        const char* fr = getenv("PRB_TC_FORCE_REDO");  // tests: exercise the rare redo path every step
+        ta.force_redo = (fr && fr[0] == '1') ? 1 : 0;
+      }
       ta.N = f.N; ta.H = f.H; ta.seed = f.seed;
       ta.balance = f.balance; ta.shares = f.shares; ta.ep_return = f.ep_return; ta.obs_out = f.obs_out;
       ta.b_obs = f.b_obs; ta.b_act = f.b_act; ta.b_logp = f.b_logp; ta.b_val = f.b_val; ta.b_rew = f.b_rew;

@@ -406,6 +406,8 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
       }
     }
     const int done = a.done_seq[h];
+    const double bal_s = bal;  // for the rare redo below
+    bool bad = a.force_redo != 0;  // a buy quantity outside stock::buy_qty_i32_spec's certificate
     auto sell = [&](int k, int32_t di) {  // sells first (:88-90): q = -min(-d, shares), exact in int32
       const int32_t qi = min(max(di, -sh[k]), 0);
       const double qv = to_f64(qi);
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
       sh[k] += qi;
     };
     auto buy = [&](int k, int32_t di) {  // then buys, clipped to the affordable balance incl. cost (:91-97)
-      const int32_t qi = stock::buy_qty_i32(di, bal, s.bp[k]);
+      const int32_t qi = stock::buy_qty_i32_spec(di, bal, s.bp[k], bad);
       const double qv = to_f64(qi);
       const double price = s.p0[k];
       const double cost = __dmul_rn(__dmul_rn(a.cost, qv), price);
@@ -435,6 +437,35 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
       desired_pair<SA>(my, k, d0, d1);
       buy(k, d0);
       if (k + 1 < K) buy(k + 1, d1);
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      // Some lane's quotient was within 2^-19 of an integer (or its cash <= 0): redo this step's
+      // trades for the warp with the reference's division, from the shares at the start of the
+      // step (this row of the compact obs tile written above; exact as floats) and bal_s.
+      const float* orow = a.b_obs + ((size_t)h * a.N + row) * P1 + 1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) sh[k] = live ? (int32_t)orow[k] : 0;
+      bal = bal_s;
+      const double cf = __dadd_rn(1.0, a.cost);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t di = __float_as_int(my[k]);
+        if (di < 0) {
+          const int32_t q = -min(-di, sh[k]);
+          const double qv = (double)q;
+          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, s.p0[k]), __dmul_rn(__dmul_rn(a.cost, fabs(qv)), s.p0[k])));
+          sh[k] += q;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t di = __float_as_int(my[k]);
+        if (di > 0) {
+          const double qv = stock::buy_qty((double)di, bal, __dmul_rn(s.p0[k], cf));
+          bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(qv, s.p0[k]), __dmul_rn(__dmul_rn(a.cost, qv), s.p0[k])));
+          sh[k] += (int32_t)qv;
+        }
+      }
     }
     double va = bal;
 #pragma unroll

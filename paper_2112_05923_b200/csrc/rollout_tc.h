@@ -30,6 +30,7 @@ struct TcRolloutArgs {
   float* b_rew;
   uint8_t* b_done;
   float* b_boot;
+  int force_redo;   // PRB_TC_FORCE_REDO=1 (tests): every step takes the reference-division redo path
   unsigned long long* trace;  // optional clock64 phase trace of CTA 0 thread 0 (PRB_TC_TRACE), else null
 };
 constexpr int kTcTraceLen = 512;

@@ -93,5 +93,16 @@ __device__ __forceinline__ int32_t buy_qty_i32(int32_t di, double balance, const
   return max(min(n, di), 0);
 }
 
+// buy_qty_i32 without the vote: the certificate failure is accumulated in `bad` and the caller
+// redoes the whole trade sequence with the reference's division when any lane of the warp saw
+// one (rollout_tc.cu); the returned quantity is then discarded.
+__device__ __forceinline__ int32_t buy_qty_i32_spec(int32_t di, double balance, const BuyPrice& b, bool& bad) {
+  const double qa = __dmul_rn(balance, b.inv);
+  const double t = __dadd_rd(qa, 0x1p52);
+  const double frac = __dsub_rn(qa, __dsub_rn(t, 0x1p52));
+  bad |= !((fabs(__dsub_rn(frac, 0.5)) < 0.5 - 0x1p-19) && (fabs(__dsub_rn(qa, 0x1p30)) < 0x1p30));
+  return max(min((int32_t)__double2loint(t), di), 0);
+}
+
 }  // namespace stock
 }  // namespace prb

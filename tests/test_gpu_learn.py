@@ -555,3 +555,19 @@ def test_collect_pointmass_cta_pair_kernel():
                         os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_pointmass_rollout"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_collect_stock_tc_redo_path():
+    """The tcgen05 stock rollout's rare redo path (a buy quantity outside the division-free
+    certificate -> the warp redoes the step's trades with the reference's division) forced on
+    every step (PRB_TC_FORCE_REDO=1, read per collect): the env transitions still replay
+    bit-exactly on the oracle."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PRB_TC_FORCE_REDO="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_stock_rollout_replays_on_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
