@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     float vcrit[16];
     tc::tmem_ld16(tlane + 32, vcrit);
     const float value = vcrit[0] + s.b3c;
-    __syncthreads();  // every thread is past its L3c wait: X is free for fp32 staging
+    // no barrier needed before staging into X: L3c (X's last reader) is complete for every
+    // thread that has passed its own mbarrier wait, and the next MMA is behind publish_operand
     if (h == a.H) {  // bootstrap V(s_H) (pod.hpp:127-131) and the VecEnv's final states
       tc::fence_before_sync();
       if (live) a.b_boot[row] = value;
