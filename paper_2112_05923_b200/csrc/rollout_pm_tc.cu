@@ -173,7 +173,7 @@ __device__ __forceinline__ void epi_hidden(uint32_t trow, const float* bias, uin
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      *reinterpret_cast<uint4*>(hb + tc::kmajor_offset(row, c + 8 * q, kHid)) =
+      *reinterpret_cast<uint4*>(hb + tc::arow_offset(row, c + 8 * q)) =
           make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
   }
 }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(PmCfg<kPair>::kThr, 1) pm_rollout_tc_kernel(co
           // B operands: [n][k] K-major; in pair mode each CTA's slot holds its n-half, same strides
           if (layer == 0) {  // [128 x 16] obs . [16 x 256]
             const uint32_t b = take();
-            mma(d, tc::smem_desc(x_addr, 128, kX * 16), tc::smem_desc(b, 128, kX * 16), ID_256, 0);
+            mma(d, tc::smem_desc(x_addr, 2048, 128), tc::smem_desc(b, 128, kX * 16), ID_256, 0);
             release();
             if (net == 1) commit(&s.xfree);
           } else if (layer < 3) {  // [128 x 256] h . [256 x 256], kCPL chunks of kKC/16 K-steps
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(PmCfg<kPair>::kThr, 1) pm_rollout_tc_kernel(co
               const uint32_t b = take();
 #pragma unroll
               for (int j = 0; j < kKC / 16; ++j)
-                mma(d, tc::smem_desc(h_addr + (q * (kKC / 16) + j) * 256, 128, kHid * 16),
+                mma(d, tc::smem_desc(h_addr + (q * (kKC / 16) + j) * 4096, 2048, 128),
                     tc::smem_desc(b + j * 256, 128, kKC * 16), ID_256, (q | j) != 0);
               release();
             }
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(PmCfg<kPair>::kThr, 1) pm_rollout_tc_kernel(co
             const uint32_t b = take();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              mma(d, tc::smem_desc(h_addr + j * 256, 128, kHid * 16), tc::smem_desc(b + j * 256, 128, kHid * 16),
+              mma(d, tc::smem_desc(h_addr + j * 4096, 2048, 128), tc::smem_desc(b + j * 256, 128, kHid * 16),
                   ID_16, j != 0);
             release();
           }
@@ -385,9 +385,9 @@ __global__ void __launch_bounds__(PmCfg<kPair>::kThr, 1) pm_rollout_tc_kernel(co
         }
         first = false;
         {  // obs row -> X (bf16, cols 6..15 zero)
-          *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(row, 0, kX)) =
+          *reinterpret_cast<uint4*>(s.x + tc::arow_offset(row, 0)) =
               make_uint4(tc::pack_bf16(o[0], o[1]), tc::pack_bf16(o[2], o[3]), tc::pack_bf16(o[4], o[5]), 0u);
-          *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(row, 8, kX)) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(s.x + tc::arow_offset(row, 8)) = make_uint4(0u, 0u, 0u, 0u);
         }
         group_signal<kPair>(&s.xready, rank);
         tr.mark();

@@ -22,6 +22,15 @@ __host__ __device__ __forceinline__ uint32_t kmajor_offset(int r, int k, int K) 
   return (uint32_t)((r >> 3) * (K * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
 
+// byte offset of element (r, k) of a [128 rows][K] A operand in the "row-interleaved" K-major
+// layout: core matrix (row group g, k chunk c) at c*2048 + g*128, i.e. LBO = 2048 (k chunks),
+// SBO = 128 (row groups), MMA K-step j at base + j*4096.  A warp's 32 rows of one k chunk are then
+// 512 contiguous bytes, so row-per-thread 16-byte operand stores are bank-conflict free (with
+// kmajor_offset the 4 row groups of a warp are K*16 bytes apart: same banks, 2 extra wavefronts).
+__host__ __device__ __forceinline__ uint32_t arow_offset(int r, int k) {
+  return (uint32_t)((k >> 3) * 2048 + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
 // UMMA shared-memory matrix descriptor (SWIZZLE_NONE, version 1 for sm_100)
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
