@@ -319,6 +319,12 @@ def run_ours(args, d: Dist):
                 "traffic_source": "ncu dram bytes/transition, profiles/r1_s3_tc_r11_full.txt, x transitions per launch",
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json "
                                f"{'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
+    if dom == "stock_rollout_fused":
+        # neither the tensor nor the HBM roof binds this kernel (both < 20%): per-thread instruction
+        # issue does -- the fp64 portfolio chain + sampling + epilogues; ncu of the same kernel
+        roofline["limiter"] = ("instruction issue/latency: ~3.4K instructions per transition, ~50% issue-active "
+                               "at the 16 warps/SM that TMEM (128 cols/CTA) and registers allow "
+                               "(profiles/r1_s3_tc_r11_full.txt, DESIGN.md section 3)")
 
     # ---- env step alone (the VecEnv boundary) at configs[4] scale: 1M envs/GPU, > L2 ----
     env_step = env_leg(pr, lib, ctx, market, cfg, args.env_envs, hbm, d)
