@@ -53,15 +53,19 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t k0, uint32_t 
   return Philox4{c0, c1, c2, c3};
 }
 
-// Two unit normals from two 32-bit draws (Box-Muller, fp32).  u1 in (0,1].
+// Two unit normals from two 32-bit draws (Box-Muller, fp32).  The top 23 bits of each draw become
+// the mantissa of a float in [1, 2) (one LEA.HI each, no int->float conversion); u1 = 2 - that is
+// in (0, 1] (>= 2^-23, so the log never sees 0 or a denormal), and sin/cos take 2*pi*[1, 2), the
+// same angles as [0, 1).  SFU forms (MUFU.LG2 / SQRT / SIN / COS): sampling noise needs ~1e-6,
+// not correct rounding.
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-  const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
-  const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
-  // SFU forms (MUFU.LG2 / RSQ / SIN / COS): sampling noise needs ~1e-6, not correct rounding
-  const float m = -2.0f * __logf(u1);
-  const float r = (m > 0.0f) ? m * rsqrtf(m) : 0.0f;
+  const float u1 = 2.0f - __uint_as_float(0x3F800000u | (a >> 9));
+  const float x2 = __uint_as_float(0x3F800000u | (b >> 9));
+  float lg, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u1));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-1.3862943611198906f * lg));  // sqrt(-2 ln u1)
   float s, c;
-  __sincosf(6.2831853071795865f * u2, &s, &c);
+  __sincosf(6.2831853071795865f * x2, &s, &c);
   return make_float2(r * c, r * s);
 }
 

@@ -38,6 +38,7 @@ constexpr int kM = 128;     // envs per CTA == MMA M == TMEM lanes
 constexpr int kKX = 32;     // private obs width (1 + K <= 32)
 constexpr uint32_t kTmemCols = 128;
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
+constexpr uint32_t kXLo = 8192;  // byte offset of the low-half private obs tile inside X
 constexpr int kSLD = 31;    // fp32 staging row stride (odd: conflict-free both ways)
 
 struct TcSmem {
@@ -83,8 +84,8 @@ __device__ __forceinline__ void epilogue64(uint32_t tlane, int col, const float*
       pk[2 * j] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
       pk[2 * j + 1] = tc::pack_bf16(tc::tanh_fast(z2), tc::tanh_fast(z3));
     }
-    *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c, 64)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    *reinterpret_cast<uint4*>(x + tc::kmajor_offset(row, c + 8, 64)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    *reinterpret_cast<uint4*>(x + tc::arow_offset(row, c)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(x + tc::arow_offset(row, c + 8)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }
 }
 
@@ -95,15 +96,22 @@ __device__ __forceinline__ void publish_operand() {
   __syncthreads();
 }
 
-// thread 0: D[d_col..] (+)= X[128 x 16*ksteps] . B ; commit; everyone waits.
-__device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32_t x_addr, uint32_t x_sbo,
-                                          uint32_t b_addr, uint32_t b_sbo, int ksteps, uint32_t idesc,
-                                          uint64_t* mbar, uint32_t& phase) {
+// thread 0: D[d_col..] (+)= X[128 x 16*ksteps] . B ; commit; everyone waits.  X is in the
+// row-interleaved layout (tc::arow_offset: K-step j at +j*4096, LBO 2048, SBO 128); with
+// x_lo != 0 a second A tile at x_lo (the low bf16 halves of the same inputs) is accumulated
+// against the same B, so the product sees X_hi + X_lo (~16 significant bits) instead of bf16(X).
+__device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32_t x_addr, uint32_t b_addr,
+                                          uint32_t b_sbo, int ksteps, uint32_t idesc, uint64_t* mbar,
+                                          uint32_t& phase, uint32_t x_lo = 0) {
   if (threadIdx.x == 0) {
     tc::fence_after_sync();
     for (int j = 0; j < ksteps; ++j)
-      tc::mma_bf16(tbase + d_col, tc::smem_desc(x_addr + j * 256, 128, x_sbo), tc::smem_desc(b_addr + j * 256, 128, b_sbo),
-                   idesc, j > 0);
+      tc::mma_bf16(tbase + d_col, tc::smem_desc(x_addr + j * 4096, 2048, 128),
+                   tc::smem_desc(b_addr + j * 256, 128, b_sbo), idesc, j > 0);
+    if (x_lo)
+      for (int j = 0; j < ksteps; ++j)
+        tc::mma_bf16(tbase + d_col, tc::smem_desc(x_lo + j * 4096, 2048, 128),
+                     tc::smem_desc(b_addr + j * 256, 128, b_sbo), idesc, 1);
     tc::mma_commit(mbar);
   }
   tc::mbar_wait(mbar, phase);
@@ -273,40 +281,47 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     }
     // ---- X <- [balance/cap, shares] (stock_observation stock_env.hpp:115-121) ----
     const float x0 = (float)__ddiv_rn(bal, a.cap);
-    {
+    {  // hi / lo bf16 halves: raw share counts need more than bf16's 8 bits (integers < 2^16 exact)
       float xv[kKX];
       xv[0] = x0;
 #pragma unroll
       for (int k = 0; k < kKX - 1; ++k) xv[1 + k] = (k < K) ? (float)sh[k] : 0.f;
 #pragma unroll
-      for (int c = 0; c < kKX / 8; ++c)
-        *reinterpret_cast<uint4*>(s.x + tc::kmajor_offset(tid, 8 * c, kKX)) =
-            make_uint4(tc::pack_bf16(xv[8 * c], xv[8 * c + 1]), tc::pack_bf16(xv[8 * c + 2], xv[8 * c + 3]),
-                       tc::pack_bf16(xv[8 * c + 4], xv[8 * c + 5]), tc::pack_bf16(xv[8 * c + 6], xv[8 * c + 7]));
+      for (int c = 0; c < kKX / 8; ++c) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          hi[i] = tc::pack_bf16(xv[8 * c + 2 * i], xv[8 * c + 2 * i + 1]);
+          lo[i] = tc::pack_bf16(xv[8 * c + 2 * i] - __uint_as_float(hi[i] << 16),
+                                xv[8 * c + 2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
+        }
+        *reinterpret_cast<uint4*>(s.x + tc::arow_offset(tid, 8 * c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(s.x + kXLo + tc::arow_offset(tid, 8 * c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
     }
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 0, x_addr, kKX * 16, w1_addr, kKX * 16, kKX / 16, ID_L1, &s.mbar, phase);   // L1
+    mma_layer(tbase, 0, x_addr, w1_addr, kKX * 16, kKX / 16, ID_L1, &s.mbar, phase, x_addr + kXLo);  // L1
     tr.mark();
     epilogue64(tlane, 0, s.c1, s.x, tid);                                                          // actor h1
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 0, x_addr, 1024, w2a_addr, 1024, 4, ID_L2, &s.mbar, phase);                    // L2a
+    mma_layer(tbase, 0, x_addr, w2a_addr, 1024, 4, ID_L2, &s.mbar, phase);                   // L2a
     tr.mark();
     epilogue64(tlane, 64, s.c1, s.x, tid);                                                         // critic h1
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 64, x_addr, 1024, w2c_addr, 1024, 4, ID_L2, &s.mbar, phase);                   // L2c
+    mma_layer(tbase, 64, x_addr, w2c_addr, 1024, 4, ID_L2, &s.mbar, phase);                  // L2c
     tr.mark();
     epilogue64(tlane, 0, s.b2, s.x, tid);                                                          // actor h2
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 0, x_addr, 1024, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase);                   // L3a
+    mma_layer(tbase, 0, x_addr, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase);                  // L3a
     tr.mark();
     epilogue64(tlane, 64, s.b2, s.x, tid);                                                         // critic h2
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 32, x_addr, 1024, w3c_addr, 1024, 4, ID_L3C, &s.mbar, phase);                  // L3c
+    mma_layer(tbase, 32, x_addr, w3c_addr, 1024, 4, ID_L3C, &s.mbar, phase);                 // L3c
     tr.mark();
     float vcrit[16];
     tc::tmem_ld16(tlane + 32, vcrit);
@@ -361,8 +376,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
               if (d < A) {
                 const float m = mean[4 * qq + i] + s.b3[d];
                 const float act = m + s.sig[d] * e4[i];
-                const float z = (act - m) * s.isig[d];
-                zz += z * z;
+                zz += e4[i] * e4[i];  // z = (a - mu) / sigma is eps up to the rounding of a
                 stage[tid * SA + d] = act;
               }
             }

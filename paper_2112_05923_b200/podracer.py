@@ -12,6 +12,7 @@ Tensor2 layouts; device-resident variants take/return ``DeviceArray``.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -63,6 +64,8 @@ class Context:
             self.h = None
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             self.close()
         except Exception:
@@ -104,6 +107,8 @@ class DeviceArray:
             self.ptr = None
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             self.free()
         except Exception:
@@ -152,6 +157,8 @@ class MarketData:
         return cls(ctx, m["close"], compute_indicators(m["high"], m["low"], m["close"]))
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             if self.h:
                 self.ctx.lib.prb_market_destroy(self.h)
@@ -262,6 +269,8 @@ class VectorizedEnvironment:
         self.ctx.lib.prb_vecenv_step(self.h, d_actions, d_reward, d_done, d_term_obs, d_term_ret, d_term_len)
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             if self.h:
                 self.ctx.lib.prb_vecenv_destroy(self.h)
@@ -386,6 +395,8 @@ class Agent:
         return out.numpy()
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             if self.h:
                 self.ctx.lib.prb_agent_destroy(self.h)
@@ -490,6 +501,8 @@ class Rollout:
         return losses, g
 
     def __del__(self):
+        if sys.is_finalizing():  # interpreter teardown: arbitrary order (a context may already be gone)
+            return
         try:
             if self.h:
                 self.ctx.lib.prb_rollout_destroy(self.h)
