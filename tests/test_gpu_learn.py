@@ -118,7 +118,7 @@ def _oracle_gae(orc, r, v, d, boot, N, H, gamma, lam, normalize):
     return adv, ret
 
 
-@pytest.mark.parametrize("N,H", [(1, 1), (7, 33), (300, 256), (4096, 8)])
+@pytest.mark.parametrize("N,H", [(1, 1), (7, 33), (300, 256), (4096, 8), (256, 100), (128, 256), (1024, 17)])
 def test_gae_parity(pr, ctx, orc, N, H):
     rng = np.random.default_rng(N * 31 + H)
     n = N * H
