@@ -16,8 +16,11 @@
 // exactly the reference's Tensor2 layout; the device keeps fp32 / fp64 copies.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -390,6 +393,50 @@ inline std::vector<int> leaderboard_rank(Context& ctx, const std::vector<double>
   std::int32_t n = 0;
   check(prb_leaderboard_rank_host(ctx.get(), scores.data(), seqs.data(), scores.size(), capacity, order.data(), &n));
   return std::vector<int>(order.begin(), order.begin() + n);
+}
+
+// GeneratorConfig tournament.hpp:125-129
+struct GeneratorConfig {
+  std::size_t top_k = 3;
+  double mutation_sigma = 0.01;
+  double fresh_prob = 0.2;
+};
+
+struct PodLineage {  // the AgentArtifact::lineage fields generate_pod_init sets
+  std::int64_t parent_pod = -1;
+  std::uint64_t mutation_seed = 0;
+};
+
+// generate_pod_init tournament.hpp:136-162.  `board` is the leaderboard's entries in rank order
+// (their agents stay on the device); the fresh / parent decision consumes the caller's
+// mt19937_64 exactly as the reference does (same libstdc++ distributions, same draw order:
+// u01, pick, mutation seed), so a pod_train driver makes the same choices; the copy and the
+// mutation never leave HBM: prb_agent_copy, then prb_agent_mutate (params += N(0, sigma^2) from a
+// Philox stream keyed by the reference's mutation seed -- statistics-level parity, DESIGN.md §6 --
+// and optimizer t := 0 with m / v kept).
+inline std::unique_ptr<Agent> generate_pod_init(const std::vector<const Agent*>& board,
+                                                const std::vector<std::int64_t>& board_pod_ids,
+                                                const GeneratorConfig& cfg, std::mt19937_64& rng,
+                                                const std::function<std::unique_ptr<Agent>(std::uint64_t)>& fresh_init,
+                                                PodLineage* lineage = nullptr) {
+  if (cfg.top_k < 1) throw ConfigError("generator.top_k must be >= 1");
+  if (board_pod_ids.size() != board.size())
+    throw DimensionError("generate_pod_init: " + std::to_string(board.size()) + " entries, " +
+                         std::to_string(board_pod_ids.size()) + " pod ids");
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  if (board.empty() || u01(rng) < cfg.fresh_prob) {
+    auto fresh = fresh_init(rng());
+    if (lineage) *lineage = PodLineage{};
+    return fresh;
+  }
+  const std::size_t pool = std::min(cfg.top_k, board.size());
+  std::uniform_int_distribution<std::size_t> pick(0, pool - 1);
+  const std::size_t i = pick(rng);
+  auto child = board.at(i)->clone();
+  const std::uint64_t mseed = rng();
+  if (lineage) *lineage = PodLineage{board_pod_ids[i], mseed};
+  check(prb_agent_mutate(child->get(), mseed, cfg.mutation_sigma > 0.0 ? cfg.mutation_sigma : 0.0));
+  return child;
 }
 
 }  // namespace podracer_b200

@@ -140,6 +140,54 @@ int main() {
   const std::vector<int> order = pb::leaderboard_rank(ctx, {1.0, 3.0, 3.0, 2.0}, {0, 1, 2, 3}, 3);
   EXPECT(order.size() == 3 && order[0] == 1 && order[1] == 2 && order[2] == 3);
 
+  // generate_pod_init (tournament.hpp:136-162): the reference's draw order on the caller's rng,
+  // the parent copied and mutated on the device, t := 0 with m / v kept, fresh path when empty
+  {
+    pb::GeneratorConfig gc;
+    gc.top_k = 2;
+    gc.fresh_prob = 0.3;
+    gc.mutation_sigma = 0.05;
+    auto fresh = [&](std::uint64_t seed) { return pb::Agent::init(ctx, S, K, seed, 1e-3); };
+    std::vector<const pb::Agent*> board = {l0.first.get(), l1.first.get(), fused.get()};
+    const std::vector<std::int64_t> ids = {11, 22, 33};
+    int n_fresh = 0, n_child = 0;
+    for (std::uint64_t seed = 1; seed <= 12; ++seed) {
+      std::mt19937_64 rng(seed), replay(seed);
+      pb::PodLineage lin;
+      auto pod = pb::generate_pod_init(board, ids, gc, rng, fresh, &lin);
+      // replay the reference's draws (tournament.hpp:142-153) on an identical generator
+      std::uniform_real_distribution<double> u01(0.0, 1.0);
+      if (u01(replay) < gc.fresh_prob) {
+        const std::uint64_t fs = replay();
+        EXPECT(lin.parent_pod == -1);
+        EXPECT(pod->flatten_params() == pb::Agent::init(ctx, S, K, fs, 1e-3)->flatten_params());
+        ++n_fresh;
+      } else {
+        std::uniform_int_distribution<std::size_t> pick(0, 1);
+        const std::size_t i = pick(replay);
+        const std::uint64_t ms = replay();
+        EXPECT(lin.parent_pod == ids[i] && lin.mutation_seed == ms);
+        EXPECT(pod->optimizer_t() == 0);
+        const auto pp = board[i]->flatten_params(), cp = pod->flatten_params();
+        double s1 = 0.0, s2 = 0.0;
+        for (size_t j = 0; j < cp.size(); ++j) {
+          const double dlt = cp[j] - pp[j];
+          s1 += dlt;
+          s2 += dlt * dlt;
+        }
+        const double mean = s1 / cp.size(), sd = std::sqrt(s2 / cp.size() - mean * mean);
+        EXPECT(std::fabs(mean) < 5e-3 && std::fabs(sd - gc.mutation_sigma) < 5e-3);  // N(0, sigma^2) noise
+        ++n_child;
+      }
+      EXPECT(rng() == replay());  // the caller's generator advanced exactly like the reference's
+    }
+    EXPECT(n_fresh > 0 && n_child > 0);
+    std::mt19937_64 rng(5);
+    pb::PodLineage lin;
+    auto pod = pb::generate_pod_init({}, {}, gc, rng, fresh, &lin);  // empty board: fresh
+    EXPECT(lin.parent_pod == -1 && pod->param_count() == l0.first->param_count());
+  }
+
   if (failures) {
     std::fprintf(stderr, "%d failures\n", failures);
     return 1;
