@@ -12,8 +12,8 @@
 //                                      features enter as the per-step term c_t)
 //   X  <- tanh(D[0:64] + c_t)          actor h1      L2a: D[0:64]   = X . W2a
 //   X  <- tanh(D[64:128] + c_t)        critic h1     L2c: D[64:128] = X . W2c
-//   X  <- tanh(D[0:64] + b2)           actor h2      L3a: D[0:32]   = X . W3a
-//   X  <- tanh(D[64:128] + b2)         critic h2     L3c: D[32:48]  = X . W3c
+//   X  <- tanh(D[0:64] + b2)           actor h2      L3a: D[0:32]   = X . W3a (issued, not awaited)
+//   value = tanh(D[64:128] + b2) . w3c + b3c   critic head in fp32 registers while L3a runs
 //   Philox Gaussian sample + log-prob, stock_env_step in fp64 (thread-local,
 //   reference operation order), rollout rows staged through X and written
 //   warp-per-row (coalesced).
@@ -46,7 +46,7 @@ struct TcSmem {
   alignas(128) uint8_t w2a[64 * 64 * 2];   // B [64][64]
   alignas(128) uint8_t w2c[64 * 64 * 2];
   alignas(128) uint8_t w3a[32 * 64 * 2];   // B [32][64]   (rows >= A zero)
-  alignas(128) uint8_t w3c[16 * 64 * 2];   // B [16][64]   (row 0 = critic head)
+  alignas(16) float w3c[64];               // critic head weights (fp32, SIMT dot product)
   alignas(128) uint8_t x[kM * 64 * 2];     // A tile: [128][32] obs, [128][64] h, fp32 [128][31] staging
   alignas(16) float c1[128];
   alignas(16) float b2[128];
@@ -100,9 +100,15 @@ __device__ __forceinline__ void publish_operand() {
 // row-interleaved layout (tc::arow_offset: K-step j at +j*4096, LBO 2048, SBO 128); with
 // x_lo != 0 a second A tile at x_lo (the low bf16 halves of the same inputs) is accumulated
 // against the same B, so the product sees X_hi + X_lo (~16 significant bits) instead of bf16(X).
+__device__ __forceinline__ void mma_wait(uint64_t* mbar, uint32_t& phase) {
+  tc::mbar_wait(mbar, phase);
+  phase ^= 1;
+  tc::fence_after_sync();
+}
+
 __device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32_t x_addr, uint32_t b_addr,
                                           uint32_t b_sbo, int ksteps, uint32_t idesc, uint64_t* mbar,
-                                          uint32_t& phase, uint32_t x_lo = 0) {
+                                          uint32_t& phase, uint32_t x_lo = 0, bool wait = true) {
   if (threadIdx.x == 0) {
     tc::fence_after_sync();
     for (int j = 0; j < ksteps; ++j)
@@ -114,9 +120,7 @@ __device__ __forceinline__ void mma_layer(uint32_t tbase, uint32_t d_col, uint32
                      tc::smem_desc(b_addr + j * 256, 128, b_sbo), idesc, 1);
     tc::mma_commit(mbar);
   }
-  tc::mbar_wait(mbar, phase);
-  phase ^= 1;
-  tc::fence_after_sync();
+  if (wait) mma_wait(mbar, phase);
 }
 
 // Copy of a staged tile that is already the contiguous [rows][cols] image of its HBM span (this
@@ -220,10 +224,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     const int n = i / 64, k = i % 64;
     st_bf16(s.w3a, tc::kmajor_offset(n, k, 64), (n < A) ? P[a.a_w3 + k * A + n] : 0.f);
   }
-  for (int i = tid; i < 16 * 64; i += kM) {
-    const int n = i / 64, k = i % 64;
-    st_bf16(s.w3c, tc::kmajor_offset(n, k, 64), (n == 0) ? P[a.c_w3 + k] : 0.f);
-  }
+  if (tid < 64) s.w3c[tid] = P[a.c_w3 + tid];
   const float b1_mine = (tid < 64) ? P[a.a_w1 + a.S * 64 + tid] : P[a.c_w1 + a.S * 64 + tid - 64];
   s.b2[tid] = (tid < 64) ? P[a.a_w2 + 64 * 64 + tid] : P[a.c_w2 + 64 * 64 + tid - 64];
   if (tid < 32) {
@@ -253,9 +254,9 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
   const uint32_t x_addr = tc::smem_u32(s.x);
   const uint32_t w1_addr = tc::smem_u32(s.w1), w2a_addr = tc::smem_u32(s.w2a), w2c_addr = tc::smem_u32(s.w2c);
-  const uint32_t w3a_addr = tc::smem_u32(s.w3a), w3c_addr = tc::smem_u32(s.w3c);
+  const uint32_t w3a_addr = tc::smem_u32(s.w3a);
   constexpr uint32_t ID_L1 = tc::idesc_bf16(128, 128), ID_L2 = tc::idesc_bf16(128, 64);
-  constexpr uint32_t ID_L3A = tc::idesc_bf16(128, 32), ID_L3C = tc::idesc_bf16(128, 16);
+  constexpr uint32_t ID_L3A = tc::idesc_bf16(128, 32);
   uint32_t phase = 0;
   const size_t row = e0 + tid;
   tc::Tracer<kTcTraceLen, kTrace> tr;
@@ -316,17 +317,38 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     epilogue64(tlane, 0, s.b2, s.x, tid);                                                          // actor h2
     tr.mark();
     publish_operand();
-    mma_layer(tbase, 0, x_addr, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase);                  // L3a
+    mma_layer(tbase, 0, x_addr, w3a_addr, 1024, 4, ID_L3A, &s.mbar, phase, 0, false);  // L3a: issue only
     tr.mark();
-    epilogue64(tlane, 64, s.b2, s.x, tid);                                                         // critic h2
+    // critic head while L3a runs: value = tanh(D[64:128] + b2) . w3c + b3c in fp32 (the 64-wide dot
+    // product is cheaper on the FMA pipe than a round trip through X and a 5th MMA; L3a writes
+    // D[0:32] only)
+    float value;
+    {
+      float acc = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 16) {
+        float v[16];
+        tc::tmem_ld16(tlane + 64 + c, v);
+        const float4* b4 = reinterpret_cast<const float4*>(s.b2 + 64 + c);
+        const float4* w4 = reinterpret_cast<const float4*>(s.w3c + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 b = b4[j], w = w4[j];
+          float z0 = v[4 * j], z1 = v[4 * j + 1], z2 = v[4 * j + 2], z3 = v[4 * j + 3];
+          tc::add2(z0, z1, b.x, b.y);
+          tc::add2(z2, z3, b.z, b.w);
+          acc = fmaf(tc::tanh_fast(z0), w.x, acc);
+          acc = fmaf(tc::tanh_fast(z1), w.y, acc);
+          acc = fmaf(tc::tanh_fast(z2), w.z, acc);
+          acc = fmaf(tc::tanh_fast(z3), w.w, acc);
+        }
+      }
+      value = acc + s.b3c;
+    }
     tr.mark();
-    publish_operand();
-    mma_layer(tbase, 32, x_addr, w3c_addr, 1024, 4, ID_L3C, &s.mbar, phase);                 // L3c
+    mma_wait(&s.mbar, phase);  // L3a done: the actor head is in D[0:32]
     tr.mark();
-    float vcrit[16];
-    tc::tmem_ld16(tlane + 32, vcrit);
-    const float value = vcrit[0] + s.b3c;
-    // no barrier needed before staging into X: L3c (X's last reader) is complete for every
+    // no barrier needed before staging into X: L3a (X's last reader) is complete for every
     // thread that has passed its own mbarrier wait, and the next MMA is behind publish_operand
     if (h == a.H) {  // bootstrap V(s_H) (pod.hpp:127-131) and the VecEnv's final states
       tc::fence_before_sync();

@@ -7,7 +7,7 @@ import sys
 import numpy as np
 
 t = np.fromfile(sys.argv[1], dtype=np.uint64).astype(np.int64)
-names = ["X build", "L1 mma", "epi a1", "L2a mma", "epi c1", "L2c mma", "epi a2", "L3a mma", "epi c2", "L3c+value",
+names = ["X build", "L1 mma", "epi a1", "L2a mma", "epi c1", "L2c mma", "epi a2", "L3a issue", "critic head", "L3a wait",
          "obs rows", "sample", "act rows", "env step", "writes", "->next"]
 steps = [h for h in range(2, 30) if t[16 * h + 15] > 0][:6]
 acc = np.zeros(16)
