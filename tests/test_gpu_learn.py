@@ -579,3 +579,30 @@ def test_collect_stock_tc_redo_path():
                         os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_stock_rollout_replays_on_oracle"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("max_trade,cost,cap", [(37.5, 0.002, 1e6), (1000.0, 0.0, 2e4), (3.0, 0.01, 5e5)])
+def test_collect_stock_tc_config_variants(pr, ctx, orc, max_trade, cost, cap):
+    """The tcgen05 stock rollout under other StockConfigs, replayed bit-exactly on the oracle:
+    a non-integer max_trade_shares (the fp64 desired-quantity path instead of the exact fp32
+    one), a cash-starved portfolio with large trades and no cost (most buys cash-limited: the
+    division-free certificate on almost every buy), and tiny trades with a high cost rate."""
+    K, N, H, T = 30, 256, 40, 200
+    m = pr.synthetic_market(K, T, seed=2112)
+    ind = pr.compute_indicators(m["high"], m["low"], m["close"])
+    market = pr.MarketData(ctx, m["close"], ind)
+    cfg = pr.StockConfig(initial_capital=cap, max_trade_shares=max_trade, cost_rate=cost)
+    start, end = 10, 40
+    env = pr.VectorizedEnvironment.stock(ctx, market, cfg, start, end, N)
+    env.reset(1)
+    agent = pr.Agent.init(ctx, 1 + 6 * K, K, seed=7)
+    ro = pr.Rollout.for_env(env, H)
+    ro.set_mode(2)
+    ro.collect(agent, env, seed=5)
+    b = ro.download()
+    acts = b["actions"].reshape(N, H, K)
+    st, rw, dn, final = _replay_stock(orc, np.ascontiguousarray(m["close"]), np.ascontiguousarray(ind), cfg, start,
+                                      end, N, H, acts, K)
+    assert np.array_equal(b["states"], f32(st))
+    assert np.array_equal(b["rewards"], f32(rw)) and np.array_equal(b["dones"], dn)
+    assert np.array_equal(env.states(), f32(final))
