@@ -34,6 +34,7 @@
 #include "policy_internal.h"
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "tc.cuh"
 
 using namespace prb;
 
@@ -79,6 +80,11 @@ struct PpoArgs {
   int del_off[2][kMaxLayers];  // delta_l rows ([mb][dims[l+1]])
   int ls_off, loss_off;        // [mb][A] log_std terms, [mb][2] policy / value loss terms
   unsigned long long* trace;   // debug (PRB_PPO_TRACE): clock64 phase marks of CTA (0, net), else null
+  // persistent rows-of-8 update: [W;b] of both nets in the staged shared-memory layout (actor
+  // blocks, then the critic's at img_c), kept current by the Adam phase, so phase A stages a
+  // net with a few bulk async copies instead of ~5K per-thread cp.async (null: cp.async path)
+  float* wimg;
+  int img_c;
 };
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n).
@@ -120,6 +126,21 @@ __host__ __device__ inline size_t staged_floats(const MlpDesc& d, int r8 = 0) {
   for (int l = 0; l < d.nl; ++l)
     n += r8 ? (size_t)r8_block(d.dims[l], d.dims[l + 1]) : (size_t)d.dims[l] * (d.dims[l + 1] + 1);
   return (n + 3) & ~size_t(3);
+}
+
+// position of flat parameter p (a weight or bias of net d) in the net's staged r8 image, or -1
+__device__ __forceinline__ int r8_img_pos(const MlpDesc& d, int p) {
+  int base = 0;
+  for (int l = 0; l < d.nl; ++l) {
+    const int in = d.dims[l], out = d.dims[l + 1];
+    const int i = p - d.off[l];
+    if (i >= 0 && i < (in + 1) * out) {
+      const int k = i / out;
+      return base + k * r8_ld(out) + (i - k * out);
+    }
+    base += r8_block(in, out);
+  }
+  return -1;
 }
 
 constexpr int kR8Scratch = 8 * 8 * 64;  // rows-of-8 path: [warp][row][col] partial sums
@@ -392,7 +413,8 @@ __device__ __forceinline__ void store_rows_r8(float* __restrict__ g, int w, cons
   }
 }
 
-__device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
+__device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, int64_t step, float* smem,
+                                             uint64_t* mbar = nullptr, uint32_t* mphase = nullptr) {
   const MlpDesc& d = net ? a.critic : a.actor;
   unsigned long long* tr = (a.trace && bx == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
   int ntr = 0;
@@ -453,7 +475,24 @@ __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, 
       retv = a.ret[i];
     }
   }
-  stage_weights_r8(a, d, s.w);
+  if (mbar) {  // bulk async copies of the net's image (persistent update): 8 KB per lane of warp 0
+    if (warp == 0) {
+      const uint32_t bytes = (uint32_t)(staged_floats(d, 1) * sizeof(float));
+      const char* src = reinterpret_cast<const char*>(a.wimg + (net ? a.img_c : 0));
+      char* dst = reinterpret_cast<char*>(s.w);
+      if (lane == 0) {
+        tc::fence_proxy_async();  // this CTA's earlier generic reads of s.w before the async writes
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // image stores of the last Adam phase
+        tc::mbar_arrive_expect_tx(mbar, bytes);
+      }
+      __syncwarp();
+      constexpr uint32_t kChunk = 8192;
+      for (uint32_t o = (uint32_t)lane * kChunk; o < bytes; o += 32 * kChunk)
+        tc::bulk_g2s(dst + o, src + o, min(kChunk, bytes - o), mbar);
+    }
+  } else {
+    stage_weights_r8(a, d, s.w);
+  }
   mark();
   if (net == 0)
     for (int dd = threadIdx.x; dd < A; dd += blockDim.x) s.ls[dd] = a.params[a.log_std_off + dd];
@@ -469,7 +508,12 @@ __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, 
     }
   }
   mark();
-  stage_wait();
+  if (mbar) {
+    tc::mbar_wait(mbar, *mphase);
+    *mphase ^= 1u;
+  } else {
+    stage_wait();
+  }
   mark();
   __syncthreads();
   mark();
@@ -751,9 +795,10 @@ __device__ __forceinline__ void fwd_delta_block(const PpoArgs& a, int bx, int ne
 
 // MODE: 0 weights read from L2, 1 staged (fwd_delta_block), 2 rows-of-8 path (fwd_delta_r8)
 template <int MODE>
-__device__ __forceinline__ void fwd_delta_any(const PpoArgs& a, int bx, int net, int64_t step, float* smem) {
+__device__ __forceinline__ void fwd_delta_any(const PpoArgs& a, int bx, int net, int64_t step, float* smem,
+                                              uint64_t* mbar = nullptr, uint32_t* mphase = nullptr) {
   if (MODE == 2)
-    fwd_delta_r8(a, bx, net, step, smem);
+    fwd_delta_r8(a, bx, net, step, smem, mbar, mphase);
   else
     fwd_delta_block<MODE == 1>(a, bx, net, step, smem);
 }
@@ -1056,6 +1101,16 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int& 
   __syncthreads();
 }
 
+// parameter p's copy in the staged-weight image (persistent rows-of-8 update)
+__device__ __forceinline__ void img_store(const PpoArgs& a, int p, float v) {
+  int q = r8_img_pos(a.actor, p);
+  if (q < 0) {
+    q = r8_img_pos(a.critic, p);
+    if (q >= 0) q += a.img_c;
+  }
+  if (q >= 0) a.wimg[q] = v;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs a, GradArgs g, int64_t steps,
                                                                      unsigned int* bar, int32_t* flags,
@@ -1065,7 +1120,16 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
   __shared__ double s_lsum[2 * kMaxSplits];
   __shared__ int s_lcode;
   __shared__ double s_loss[3];
+  __shared__ __align__(8) uint64_t s_mbar;  // bulk staging of the weight image (MODE 2)
   const int tid = threadIdx.x;
+  const bool img = MODE == 2 && a.wimg;
+  uint64_t* mbar = img ? &s_mbar : nullptr;
+  uint32_t mphase = 0;
+  if (img) {
+    if (tid == 0) tc::mbar_init(&s_mbar, 1);
+    for (int p = blockIdx.x * 256 + tid; p < a.P; p += gridDim.x * 256) img_store(a, p, a.params[p]);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
   const unsigned int nb = gridDim.x;
   unsigned int bt = 0;  // barrier target
   const int nA = (a.mb + a.R - 1) / a.R;
@@ -1089,7 +1153,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
     if (mk) tr[0] = gtime();
     // ---- A: forward + head gradients + backward deltas, row-parallel ----
     for (int vb = blockIdx.x; vb < 2 * nA; vb += nb) {
-      fwd_delta_any<MODE>(a, vb % nA, vb / nA, st, smem);
+      fwd_delta_any<MODE>(a, vb % nA, vb / nA, st, smem, mbar, &mphase);
       __syncthreads();
     }
     if (mk) tr[1] = gtime();
@@ -1176,6 +1240,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       g.m[p0] = nm0;
       g.v[p0] = nv0;
       g.p_rw[p0] = np0;
+      if (img) img_store(a, p0, np0);
     }
     for (int p = p0 + nb * 256; p < g.P; p += nb * 256) {
       const float gi = g.grads[p];
@@ -1183,8 +1248,11 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       const float vi = b2 * g.v[p] + omb2 * gi * gi;
       g.m[p] = mi;
       g.v[p] = vi;
-      g.p_rw[p] -= g.lr * (mi * bc.x) / (sqrtf(vi * bc.y) + g.eps);
+      const float np = g.p_rw[p] - g.lr * (mi * bc.x) / (sqrtf(vi * bc.y) + g.eps);
+      g.p_rw[p] = np;
+      if (img) img_store(a, p, np);
     }
+    if (img) asm volatile("fence.proxy.async.global;" ::: "memory");  // image -> next step's bulk copies
     if (mk) tr[7] = gtime();
     grid_barrier(bar, bt, nb);
     if (mk) tr[8] = gtime();
@@ -1204,6 +1272,7 @@ struct PpoWorkspace {
   DevBuf<int32_t> bar;               // persistent update: grid barrier + non-finite flags
   DevBuf<float2> bias;               // persistent update: Adam bias corrections per step
   DevBuf<unsigned long long> ptrace; // PRB_PPO_TRACE of the persistent update: [grid][10]
+  DevBuf<float> wimg;                // persistent rows-of-8 update: staged-layout weight image
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -1419,6 +1488,13 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   }
   ws.bias.ensure((size_t)steps);
   float2* bias_tab = ws.bias.p;
+  if (p.r8 && p.stage && !getenv("PRB_PPO_CPASYNC")) {  // PRB_PPO_CPASYNC=1: per-thread cp.async staging (A/B)
+    pa.img_c = (int)staged_floats(p.actor, 1);
+    const size_t nimg = (size_t)pa.img_c + staged_floats(p.critic, 1);
+    ws.wimg.ensure(nimg);
+    PRB_CUDA(cudaMemsetAsync(ws.wimg.p, 0, nimg * sizeof(float), s));  // row padding
+    pa.wimg = ws.wimg.p;
+  }
   void* args[] = {&pa, &g, &steps, &bar, &flags, &bias_tab, &trace};
   const size_t smem = persistent_smem(p);
   launch_coop(p.r8 ? (const void*)ppo_persistent_kernel<2>
