@@ -366,14 +366,10 @@ __device__ __forceinline__ void r8_partials(const float* W, int ldw, const float
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const float4 x = *reinterpret_cast<const float4*>(s_in + r * ldi + i);
-      acc0[r] = fmaf(x.x, w0[0], acc0[r]);
-      acc0[r] = fmaf(x.y, w0[1], acc0[r]);
-      acc0[r] = fmaf(x.z, w0[2], acc0[r]);
-      acc0[r] = fmaf(x.w, w0[3], acc0[r]);
-      acc1[r] = fmaf(x.x, w1[0], acc1[r]);
-      acc1[r] = fmaf(x.y, w1[1], acc1[r]);
-      acc1[r] = fmaf(x.z, w1[2], acc1[r]);
-      acc1[r] = fmaf(x.w, w1[3], acc1[r]);
+      tc::fma2(acc0[r], acc1[r], x.x, w0[0], w1[0]);  // packed: the same per-column fmaf chain
+      tc::fma2(acc0[r], acc1[r], x.y, w0[1], w1[1]);
+      tc::fma2(acc0[r], acc1[r], x.z, w0[2], w1[2]);
+      tc::fma2(acc0[r], acc1[r], x.w, w0[3], w1[3]);
     }
   }
   if (w == 7)
@@ -382,9 +378,7 @@ __device__ __forceinline__ void r8_partials(const float* W, int ldw, const float
       const float wb = on1 ? (TRANS ? W[c1 * ldw + i] : W[i * ldw + c1]) : 0.0f;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const float x = s_in[r * ldi + i];
-        acc0[r] = fmaf(x, wa, acc0[r]);
-        acc1[r] = fmaf(x, wb, acc1[r]);
+        tc::fma2(acc0[r], acc1[r], s_in[r * ldi + i], wa, wb);
       }
     }
   float* sc = scratch + w * 512;
@@ -909,7 +903,7 @@ __device__ __forceinline__ void grad_block(const GradArgs& g, int vb, float* gsm
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ak[i], bj[j], acc[i][j]);
+            for (int j = 0; j < 4; j += 2) tc::fma2(acc[i][j], acc[i][j + 1], ak[i], bj[j], bj[j + 1]);
           if (with_bias) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) bsum[j] += bj[j];

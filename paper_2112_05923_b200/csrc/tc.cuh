@@ -253,6 +253,15 @@ __device__ __forceinline__ void add2(float& x0, float& x1, float b0, float b1) {
       : "f"(b0), "f"(b1));
 }
 
+// (d0, d1) = a * (b0, b1) + (d0, d1) as one packed FFMA2 with a scalar (broadcast) operand
+// (sm_100 fma.rn.f32x2; each half rounds exactly like fmaf)
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a, float b0, float b1) {
+  asm("{.reg .b64 x, y, z; mov.b64 x, {%2,%2}; mov.b64 y, {%3,%4}; mov.b64 z, {%0,%1}; fma.rn.f32x2 z, x, y, z; "
+      "mov.b64 {%0,%1}, z;}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a), "f"(b0), "f"(b1));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
