@@ -85,6 +85,7 @@ struct PpoArgs {
   // net with a few bulk async copies instead of ~5K per-thread cp.async (null: cp.async path)
   float* wimg;
   int img_c;
+  int nospec;  // 1: Adam stored after the gate barrier (PRB_PPO_NOSPEC, A/B), else speculatively before it
 };
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n).
@@ -970,6 +971,16 @@ __global__ void __launch_bounds__(256) ppo_grad_kernel(GradArgs g) {
 // and releases the others, which then apply Adam to their parameter range (skipped when
 // the gate failed, so a rejected step leaves params/m/v/t untouched, nn.hpp:169-171).
 // Launched cooperatively (every CTA resident), grid-stride over the parameters.
+// adam_step (nn.hpp:164-182) for one fp32 parameter with every rounding explicit: the device
+// compiler's FMA contraction choices can differ between kernels, and the persistent and the
+// per-kernel updates must agree bit for bit
+__device__ __forceinline__ void adam_param(float b1, float b2, float omb1, float omb2, float lr, float eps, float ibc1,
+                                           float ibc2, float g, float& m, float& v, float& w) {
+  m = __fmaf_rn(b1, m, __fmul_rn(omb1, g));
+  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
+  w = __fsub_rn(w, __fdiv_rn(__fmul_rn(lr, __fmul_rn(m, ibc1)), __fadd_rn(__fsqrt_rn(__fmul_rn(v, ibc2)), eps)));
+}
+
 __global__ void __launch_bounds__(256) ppo_sum_adam_kernel(GradArgs g) {
   if (g.status[0] != 0) return;
   const int tid = threadIdx.x;
@@ -1054,12 +1065,11 @@ __global__ void __launch_bounds__(256) ppo_sum_adam_kernel(GradArgs g) {
   const float ibc1 = sb[0], ibc2 = sb[1];
   const float b1 = (float)g.b1, b2 = (float)g.b2, omb1 = (float)(1.0 - g.b1), omb2 = (float)(1.0 - g.b2);
   for (int p = blockIdx.x * 256 + tid; p < g.P; p += gridDim.x * 256) {
-    const float gi = g.grads[p];
-    const float mi = b1 * g.m[p] + omb1 * gi;
-    const float vi = b2 * g.v[p] + omb2 * gi * gi;
+    float mi = g.m[p], vi = g.v[p], wi = g.p_rw[p];
+    adam_param(b1, b2, omb1, omb2, g.lr, g.eps, ibc1, ibc2, g.grads[p], mi, vi, wi);
     g.m[p] = mi;
     g.v[p] = vi;
-    g.p_rw[p] -= g.lr * (mi * ibc1) / (sqrtf(vi * ibc2) + g.eps);
+    g.p_rw[p] = wi;
   }
 }
 
@@ -1142,6 +1152,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
   // PRB_PPO_TRACE: globaltimer stamps of step 4 per CTA (phase ends and barrier exits)
   unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 16 : nullptr;
   const int p0 = blockIdx.x * 256 + tid;  // this thread's first parameter (its Adam update is kept in registers)
+  const bool spec = (int64_t)nb * 256 >= g.P && !a.nospec;  // every parameter has its own thread
   for (int64_t st = 0; st < steps; ++st) {
     const bool mk = tr && st == (steps > 4 ? 4 : 0);
     if (mk) tr[0] = gtime();
@@ -1159,6 +1170,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       __syncthreads();
     }
     if (mk) tr[3] = gtime();
+    for (int dd = tid; dd < g.A; dd += 256) s_ls[dd] = g.params[g.log_std_off + dd];  // before any Adam write
     grid_barrier(bar, bt, nb);
     if (mk) tr[4] = gtime();
     // ---- C1: split sums in split order (ppo_sum_adam_kernel's arithmetic), the loss half of
@@ -1175,7 +1187,6 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       s_lsum[tid - 32] = (double)g.partial[(size_t)(tid - 32) * g.Pext + g.P];
       s_lsum[kMaxSplits + tid - 32] = (double)g.partial[(size_t)(tid - 32) * g.Pext + g.P + 1];
     }
-    for (int dd = tid; dd < g.A; dd += 256) s_ls[dd] = g.params[g.log_std_off + dd];  // before any Adam write
     int bad = 0;
     for (int p = p0; p < g.P; p += nb * 256) {
       float v[kMaxSplits];
@@ -1188,9 +1199,10 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       if (p >= g.log_std_off && p < g.log_std_off + g.A) sum -= (float)g.ent;  // ppo.hpp:157
       bad |= !isfinite(sum);
       if (p == p0) {
-        nm0 = b1 * m0 + omb1 * sum;
-        nv0 = b2 * v0 + omb2 * sum * sum;
-        np0 = w0 - g.lr * (nm0 * bc.x) / (sqrtf(nv0 * bc.y) + g.eps);
+        nm0 = m0;
+        nv0 = v0;
+        np0 = w0;
+        adam_param(b1, b2, omb1, omb2, g.lr, g.eps, bc.x, bc.y, sum, nm0, nv0, np0);
       } else {
         g.grads[p] = sum;
       }
@@ -1209,6 +1221,15 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       s_loss[1] = vl;
       s_loss[2] = ent;
     }
+    // one parameter per thread: the Adam update is stored now and undone from the registers
+    // if the gate (known after the barrier) fails -- one grid barrier per step fewer
+    if (spec && p0 < g.P) {
+      g.m[p0] = nm0;
+      g.v[p0] = nv0;
+      g.p_rw[p0] = np0;
+      if (img) img_store(a, p0, np0);
+    }
+    if (spec && img) asm volatile("fence.proxy.async.global;" ::: "memory");
     if (mk) tr[5] = gtime();
     grid_barrier(bar, bt, nb);
     if (mk) tr[6] = gtime();
@@ -1229,7 +1250,19 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       *g.step += 1;
       flags[(st + 1) & 1] = 0;  // next step's flag: last read before the previous barrier
     }
-    if (code) break;  // identical decision in every CTA
+    if (code) {  // identical decision in every CTA
+      if (spec && p0 < g.P) {  // nn.hpp:169-171: a rejected step leaves params, m and v untouched
+        g.m[p0] = m0;
+        g.v[p0] = v0;
+        g.p_rw[p0] = w0;
+        if (img) img_store(a, p0, w0);
+      }
+      break;
+    }
+    if (spec) {
+      if (mk) tr[7] = tr[8] = gtime();
+      continue;
+    }
     if (p0 < g.P) {
       g.m[p0] = nm0;
       g.v[p0] = nv0;
@@ -1237,12 +1270,10 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
       if (img) img_store(a, p0, np0);
     }
     for (int p = p0 + nb * 256; p < g.P; p += nb * 256) {
-      const float gi = g.grads[p];
-      const float mi = b1 * g.m[p] + omb1 * gi;
-      const float vi = b2 * g.v[p] + omb2 * gi * gi;
+      float mi = g.m[p], vi = g.v[p], np = g.p_rw[p];
+      adam_param(b1, b2, omb1, omb2, g.lr, g.eps, bc.x, bc.y, g.grads[p], mi, vi, np);
       g.m[p] = mi;
       g.v[p] = vi;
-      const float np = g.p_rw[p] - g.lr * (mi * bc.x) / (sqrtf(vi * bc.y) + g.eps);
       g.p_rw[p] = np;
       if (img) img_store(a, p, np);
     }
@@ -1482,6 +1513,7 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   }
   ws.bias.ensure((size_t)steps);
   float2* bias_tab = ws.bias.p;
+  pa.nospec = getenv("PRB_PPO_NOSPEC") ? 1 : 0;
   if (p.r8 && p.stage && !getenv("PRB_PPO_CPASYNC")) {  // PRB_PPO_CPASYNC=1: per-thread cp.async staging (A/B)
     pa.img_c = (int)staged_floats(p.actor, 1);
     const size_t nimg = (size_t)pa.img_c + staged_floats(p.critic, 1);

@@ -1,8 +1,9 @@
-"""A/B of the persistent PPO update's weight staging at configs[0] (1,024 stock envs x 256,
-minibatch 1,024, 4 epochs = 1,024 Adam steps): bulk async copies of the staged-layout image
-(default) vs per-thread cp.async (PRB_PPO_CPASYNC=1). Device-timed with CUDA events; also
-checks both give bit-identical parameters.
-    python profiles/ppo_ab.py"""
+"""A/B of a persistent PPO update knob at configs[0] (1,024 stock envs x 256, minibatch 1,024,
+4 epochs = 1,024 Adam steps): the default build vs the same with VAR=1 -- PRB_PPO_CPASYNC
+(per-thread cp.async weight staging instead of bulk copies of the staged-layout image, the
+default VAR) or PRB_PPO_NOSPEC (Adam stored after the gate barrier instead of speculatively
+before it). Device-timed with CUDA events; also checks both give bit-identical parameters.
+    python profiles/ppo_ab.py [VAR]"""
 import os
 import sys
 
@@ -24,12 +25,13 @@ agent = pr.Agent.init(ctx, bench.S_DIM, bench.K_ASSETS, seed=7)
 ro = pr.Rollout.for_env(env, H)
 ro.collect(agent, env, seed=1)
 cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=4, buffer_size=N * H)
+VAR = sys.argv[1] if len(sys.argv) > 1 else "PRB_PPO_CPASYNC"
 outs = {}
-for name, flag in (("bulk", None), ("cp.async", "1")) * 4:
+for name, flag in (("default", None), (VAR, "1")) * 4:
     if flag:
-        os.environ["PRB_PPO_CPASYNC"] = flag
+        os.environ[VAR] = flag
     else:
-        os.environ.pop("PRB_PPO_CPASYNC", None)
+        os.environ.pop(VAR, None)
     out = pr.Agent.init(ctx, bench.S_DIM, bench.K_ASSETS, seed=7)
     pr.ppo_update(agent, ro, cfg, seed=2, out=out)  # warm
     ts = []
@@ -42,5 +44,5 @@ for name, flag in (("bulk", None), ("cp.async", "1")) * 4:
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     outs[name] = out.flatten_params()
-    print(f"{name:9s} update {np.median(ts):7.2f} ms = {np.median(ts) / 1024 * 1e3:6.2f} us/minibatch (min {min(ts):.2f})")
-print("bit-identical params:", np.array_equal(outs["bulk"], outs["cp.async"]))
+    print(f"{name:16s} update {np.median(ts):7.2f} ms = {np.median(ts) / 1024 * 1e3:6.2f} us/minibatch (min {min(ts):.2f})")
+print("bit-identical params:", np.array_equal(outs["default"], outs[VAR]))

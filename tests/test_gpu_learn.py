@@ -606,3 +606,39 @@ def test_collect_stock_tc_config_variants(pr, ctx, orc, max_trade, cost, cap):
     assert np.array_equal(b["states"], f32(st))
     assert np.array_equal(b["rewards"], f32(rw)) and np.array_equal(b["dones"], dn)
     assert np.array_equal(env.states(), f32(final))
+
+
+@pytest.mark.parametrize("hid", [(64, 64), (8, 8)])
+def test_ppo_update_gate_midway_rolls_back(pr, ctx, hid, monkeypatch):
+    """A non-finite loss at a LATER minibatch step (a NaN old log-prob placed in epoch 0's third
+    minibatch by an injected permutation): the persistent update stores each Adam step before
+    its gate is known and undoes it on failure, so the destination agent holds exactly the state
+    after the last accepted step -- params, m, v and t identical to the per-kernel path, whose
+    Adam kernel runs only after the gate (adam_step nn.hpp:169-171)."""
+    S, A, N, H, mb = 181, 30, 64, 64, 512
+    n = N * H
+    rng = np.random.default_rng(11)
+    agent = pr.Agent.init(ctx, S, A, seed=9, hidden=hid)
+    ro, buf = _upload_random_buffer(pr, ctx, rng, N, H, S, A)
+    bad_row = 1234
+    lp = buf["log_probs"].copy()
+    lp[bad_row] = np.nan
+    ro.upload(buf["states"], buf["actions"], lp, buf["rewards"], buf["dones"], buf["values"], buf["bootstrap"])
+    perm = np.concatenate([rng.permutation(n) for _ in range(2)]).astype(np.uint64)
+    k = int(np.where(perm[:n] == bad_row)[0][0])
+    perm[[k, 2 * mb + 5]] = perm[[2 * mb + 5, k]]  # the bad row lands in step 2
+    cfg = pr.PpoConfig(epochs_per_update=2, minibatch_size=mb, buffer_size=n)
+    outs = []
+    for graph in (False, True):
+        if graph:
+            monkeypatch.setenv("PRB_PPO_GRAPH", "1")
+        out = pr.Agent.init(ctx, S, A, seed=1, hidden=hid)
+        with pytest.raises(pr.NumericError):
+            pr.ppo_update(agent, ro, cfg, 3, perm=perm, out=out)
+        outs.append(out.get())
+    monkeypatch.delenv("PRB_PPO_GRAPH")
+    (p1, m1, v1, t1), (p2, m2, v2, t2) = outs
+    t0 = agent.get()[3]
+    assert t1 == t2 == t0 + 2
+    assert np.array_equal(p1, p2) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    assert not np.array_equal(p1, agent.flatten_params())  # two steps were applied
