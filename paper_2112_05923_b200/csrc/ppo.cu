@@ -436,6 +436,24 @@ __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, 
     for (int i = 0; i < l; ++i) p += r8_block(d.dims[i], d.dims[i + 1]);
     return p;
   };
+  if (mbar) {  // bulk async copies of the net's image (persistent update): 8 KB per lane of warp 0,
+    // issued before the gather (the proxy fence would otherwise wait for the gather's loads)
+    if (warp == 0) {
+      const uint32_t bytes = (uint32_t)(staged_floats(d, 1) * sizeof(float));
+      const char* src = reinterpret_cast<const char*>(a.wimg + (net ? a.img_c : 0));
+      char* dst = reinterpret_cast<char*>(s.w);
+      if (lane == 0) {
+        tc::fence_proxy_async();  // this CTA's earlier generic reads of s.w before the async writes
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // image stores of the last Adam phase
+        tc::mbar_arrive_expect_tx(mbar, bytes);
+      }
+      __syncwarp();
+      constexpr uint32_t kChunk = 8192;
+      for (uint32_t o = (uint32_t)lane * kChunk; o < bytes; o += 32 * kChunk)
+        tc::bulk_g2s(dst + o, src + o, min(kChunk, bytes - o), mbar);
+    }
+  }
+  mark();
   // ---- gather (gather_minibatch ppo.hpp:83-103): warp r gathers row r; its loads are issued
   // first, then the weight copies (asynchronous), then the gathered values are stored ----
   float xv[kGatherUnroll];
@@ -470,24 +488,7 @@ __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, 
       retv = a.ret[i];
     }
   }
-  if (mbar) {  // bulk async copies of the net's image (persistent update): 8 KB per lane of warp 0
-    if (warp == 0) {
-      const uint32_t bytes = (uint32_t)(staged_floats(d, 1) * sizeof(float));
-      const char* src = reinterpret_cast<const char*>(a.wimg + (net ? a.img_c : 0));
-      char* dst = reinterpret_cast<char*>(s.w);
-      if (lane == 0) {
-        tc::fence_proxy_async();  // this CTA's earlier generic reads of s.w before the async writes
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // image stores of the last Adam phase
-        tc::mbar_arrive_expect_tx(mbar, bytes);
-      }
-      __syncwarp();
-      constexpr uint32_t kChunk = 8192;
-      for (uint32_t o = (uint32_t)lane * kChunk; o < bytes; o += 32 * kChunk)
-        tc::bulk_g2s(dst + o, src + o, min(kChunk, bytes - o), mbar);
-    }
-  } else {
-    stage_weights_r8(a, d, s.w);
-  }
+  if (!mbar) stage_weights_r8(a, d, s.w);
   mark();
   if (net == 0)
     for (int dd = threadIdx.x; dd < A; dd += blockDim.x) s.ls[dd] = a.params[a.log_std_off + dd];

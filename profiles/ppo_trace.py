@@ -40,7 +40,7 @@ print(f"{len(t)} CTAs; times in us from the earliest step start (min / median / 
 for i, nm in enumerate(names):
     c = (t[:, i] - t0) / 1e3
     print(f"  {nm:22s} {c.min():8.2f} {np.median(c):8.2f} {c.max():8.2f}")
-mk_names = ["weights issued", "gather landed", "weights landed", "sync", "layer 0", "layer 1", "layer 2", "inputs stored", "head grads", "head stored",
+mk_names = ["weights issued", "gather issued", "gather landed", "weights landed", "sync", "layer 0", "layer 1", "layer 2", "inputs stored", "head grads", "head stored",
             "bwd 2->1", "stored", "bwd 1->0", "stored"]  # fwd_delta_r8's marks (3-layer nets)
 for net in (0, 1):
     mk = marks[net]
