@@ -86,6 +86,9 @@ struct PpoArgs {
   float* wimg;
   int img_c;
   int nospec;  // 1: Adam stored after the gate barrier (PRB_PPO_NOSPEC, A/B), else speculatively before it
+  // persistent update: [2][mb] (buffer index, shared-feature row) of a step's minibatch rows,
+  // resolved one step ahead by the CTAs that have no row block in phase A (null: mb_row inline)
+  uint2* rtab;
 };
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n).
@@ -409,7 +412,8 @@ __device__ __forceinline__ void store_rows_r8(float* __restrict__ g, int w, cons
 }
 
 __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, int64_t step, float* smem,
-                                             uint64_t* mbar = nullptr, uint32_t* mphase = nullptr) {
+                                             uint64_t* mbar = nullptr, uint32_t* mphase = nullptr,
+                                             const uint2* rows = nullptr) {
   const MlpDesc& d = net ? a.critic : a.actor;
   unsigned long long* tr = (a.trace && bx == 0 && threadIdx.x == 0) ? a.trace + 16 * net : nullptr;
   int ntr = 0;
@@ -460,9 +464,16 @@ __device__ __forceinline__ void fwd_delta_r8(const PpoArgs& a, int bx, int net, 
   float act = 0.f, lp0 = 0.f, advv = 0.f, retv = 0.f;
   const int r = warp;
   if (r < nrows) {
-    const uint32_t i = mb_row(a, step, (uint32_t)(q0 + r));
+    uint32_t i;
     const float* fr = nullptr;
-    if (a.obs_mode == 1) fr = a.feat + (size_t)a.row[i / a.N] * (a.S - a.Sp);
+    if (rows) {  // resolved during the previous step
+      const uint2 e = rows[q0 + r];
+      i = e.x;
+      if (a.obs_mode == 1) fr = a.feat + (size_t)e.y * (a.S - a.Sp);
+    } else {
+      i = mb_row(a, step, (uint32_t)(q0 + r));
+      if (a.obs_mode == 1) fr = a.feat + (size_t)a.row[i / a.N] * (a.S - a.Sp);
+    }
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u) {
       const int c = lane + 32 * u;
@@ -792,9 +803,10 @@ __device__ __forceinline__ void fwd_delta_block(const PpoArgs& a, int bx, int ne
 // MODE: 0 weights read from L2, 1 staged (fwd_delta_block), 2 rows-of-8 path (fwd_delta_r8)
 template <int MODE>
 __device__ __forceinline__ void fwd_delta_any(const PpoArgs& a, int bx, int net, int64_t step, float* smem,
-                                              uint64_t* mbar = nullptr, uint32_t* mphase = nullptr) {
+                                              uint64_t* mbar = nullptr, uint32_t* mphase = nullptr,
+                                              const uint2* rows = nullptr) {
   if (MODE == 2)
-    fwd_delta_r8(a, bx, net, step, smem, mbar, mphase);
+    fwd_delta_r8(a, bx, net, step, smem, mbar, mphase, rows);
   else
     fwd_delta_block<MODE == 1>(a, bx, net, step, smem);
 }
@@ -1154,12 +1166,22 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_persistent_kernel(PpoArgs 
   unsigned long long* tr = (trace && tid == 0) ? trace + (size_t)blockIdx.x * 16 : nullptr;
   const int p0 = blockIdx.x * 256 + tid;  // this thread's first parameter (its Adam update is kept in registers)
   const bool spec = (int64_t)nb * 256 >= g.P && !a.nospec;  // every parameter has its own thread
+  const bool pf = MODE == 2 && a.rtab && (int)nb > 2 * nA;   // CTAs without a row block exist
   for (int64_t st = 0; st < steps; ++st) {
     const bool mk = tr && st == (steps > 4 ? 4 : 0);
     if (mk) tr[0] = gtime();
-    // ---- A: forward + head gradients + backward deltas, row-parallel ----
+    // ---- A: forward + head gradients + backward deltas, row-parallel; the CTAs without a row
+    // block resolve the next step's minibatch rows (Feistel permutation + feature row) ----
+    if (pf && (int)blockIdx.x >= 2 * nA && st + 1 < steps) {
+      uint2* t = a.rtab + ((st + 1) & 1) * a.mb;
+      for (int q = ((int)blockIdx.x - 2 * nA) * 256 + tid; q < a.mb; q += ((int)nb - 2 * nA) * 256) {
+        const uint32_t i = mb_row(a, st + 1, (uint32_t)q);
+        t[q] = make_uint2(i, a.obs_mode == 1 ? (uint32_t)a.row[i / a.N] : 0u);
+      }
+    }
+    const uint2* rows = (pf && st > 0) ? a.rtab + (st & 1) * a.mb : nullptr;
     for (int vb = blockIdx.x; vb < 2 * nA; vb += nb) {
-      fwd_delta_any<MODE>(a, vb % nA, vb / nA, st, smem, mbar, &mphase);
+      fwd_delta_any<MODE>(a, vb % nA, vb / nA, st, smem, mbar, &mphase, rows);
       __syncthreads();
     }
     if (mk) tr[1] = gtime();
@@ -1299,6 +1321,7 @@ struct PpoWorkspace {
   DevBuf<float2> bias;               // persistent update: Adam bias corrections per step
   DevBuf<unsigned long long> ptrace; // PRB_PPO_TRACE of the persistent update: [grid][10]
   DevBuf<float> wimg;                // persistent rows-of-8 update: staged-layout weight image
+  DevBuf<uint2> rtab;                // ... and the next step's resolved minibatch rows
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -1521,6 +1544,10 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
     ws.wimg.ensure(nimg);
     PRB_CUDA(cudaMemsetAsync(ws.wimg.p, 0, nimg * sizeof(float), s));  // row padding
     pa.wimg = ws.wimg.p;
+  }
+  if (p.r8 && !getenv("PRB_PPO_NOTAB")) {  // PRB_PPO_NOTAB=1: rows resolved inline (A/B)
+    ws.rtab.ensure(2 * (size_t)p.mb);
+    pa.rtab = ws.rtab.p;
   }
   void* args[] = {&pa, &g, &steps, &bar, &flags, &bias_tab, &trace};
   const size_t smem = persistent_smem(p);
