@@ -1,3 +1,6 @@
+"""Bit-equality check of the persistent PPO update's A/B knobs against the per-kernel path
+(PRB_PPO_GRAPH=1) at a configs[0]-like shape: prints, per knob, how many params / m / v differ.
+    python profiles/dbg_eq.py"""
 import os, sys, numpy as np
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
 from paper_2112_05923_b200 import podracer as pr
