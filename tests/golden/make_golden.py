@@ -87,7 +87,8 @@ def main():
     c3, h3, l3 = synthetic_market_np(K3, T3, seed=5)
     ind3 = indicators(ref, h3, l3, c3)
     cfg3 = np.array([1e4, 100.0, 0.002]); start, end = 40, 52
-    seq = np.array([rng.uniform(-1.2, 1.2, size=(N3, K3)) for _ in range(30)])
+    # fp32-representable actions: the device VecEnv takes its actions as fp32
+    seq = np.array([rng.uniform(-1.2, 1.2, size=(N3, K3)).astype(np.float32).astype(np.float64) for _ in range(30)])
     S3 = 1 + 6 * K3
     h = ref.ref_stock_vec_create(ptr(c3), ptr(ind3), T3, K3, ptr(cfg3), start, end, N3)
     obs0 = np.zeros((N3, S3)); assert ref.ref_vec_reset(h, 9, ptr(obs0)) == 0

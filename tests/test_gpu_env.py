@@ -186,3 +186,33 @@ def test_pointmass_reset_deterministic(pr, ctx):
     assert np.array_equal(s1, s2)
     assert not np.array_equal(s1, e1.reset(100))  # test_envs.cpp:101-112
     assert np.all(np.abs(s1[:, [0, 1, 4, 5]]) <= 0.4) and np.all(s1[:, [2, 3]] == 0.0)
+
+
+def test_stock_vecenv_matches_reference_golden(pr, ctx):
+    """Device VecEnv against vectors the REFERENCE produced (tests/golden/ref_golden.npz via
+    oracle/_ref; env.hpp:167-249, stock_env.hpp:55-184): 30 steps, 6 envs, 12-step episodes
+    with auto-reset.  Dones, episode lengths and fp64 episode returns bit-exact; obs and rewards
+    are the fp32 rounding of the reference's fp64 values."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_golden.npz"))
+    start, end = (int(x) for x in g["vec_window"])
+    close, ind = np.ascontiguousarray(g["vec_close"]), np.ascontiguousarray(g["vec_ind"])
+    seq = g["vec_actions"]
+    N = seq.shape[1]
+    market = pr.MarketData(ctx, close, ind)
+    env = pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(*(float(x) for x in g["vec_cfg"])), start, end,
+                                         N)
+    obs = env.reset(9)
+    assert np.array_equal(obs, g["vec_obs0"].astype(np.float32))
+    f32 = lambda x: x.astype(np.float32).astype(np.float64)
+    for s, a in enumerate(seq):
+        res = env.step(np.ascontiguousarray(a))
+        assert np.array_equal(res.dones, g["vec_done"][s]), f"dones step {s}"
+        assert np.array_equal(res.next_states, f32(g["vec_next"][s])), f"obs step {s}"
+        assert np.array_equal(res.rewards, f32(g["vec_reward"][s])), f"reward step {s}"
+        for i in np.nonzero(g["vec_done"][s])[0]:
+            info = res.infos[i]
+            assert info.episode_end and info.episode_length == g["vec_term_len"][s][i]
+            assert info.episode_return == g["vec_term_ret"][s][i]
+            assert np.array_equal(info.terminal_state, f32(g["vec_term"][s][i]))
+    assert g["vec_done"].any()
