@@ -216,3 +216,14 @@ def test_stock_vecenv_matches_reference_golden(pr, ctx):
             assert info.episode_return == g["vec_term_ret"][s][i]
             assert np.array_equal(info.terminal_state, f32(g["vec_term"][s][i]))
     assert g["vec_done"].any()
+
+
+def test_leaderboard_rank_matches_reference_golden(pr, ctx):
+    """Device ranking (prb_leaderboard_rank_host) against the final boards the REFERENCE's
+    sequential leaderboard_update produced (tournament.hpp:104-119; ties keep the earlier arrival),
+    40 sequences of 30 candidates, capacity 1..6: indices bit-exact."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_golden.npz"))
+    for scores, cap, final in zip(g["lb_scores"], g["lb_cap"], g["lb_final"]):
+        order = pr.leaderboard_rank(ctx, scores, np.arange(scores.size, dtype=np.uint64), int(cap))
+        assert np.array_equal(order.astype(np.int64), final[final >= 0])
