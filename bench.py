@@ -49,6 +49,11 @@ S_DIM = 1 + 6 * K_ASSETS
 ENV_BYTES = 36 * K_ASSETS + 41  # action 4K + balance 16 + shares 8K + ep_return 16 + obs 4(1+6K) + reward 4 + done 1
 BUF_BYTES = 4 * (1 + K_ASSETS) + 4 * K_ASSETS + 4 * 3 + 1  # compact rollout row: obs 124 + act 120 + logp/val/rew 12 + done 1
 MLP_FLOPS = 2 * (181 * 64 + 64 * 64 + 64 * 30) + 2 * (181 * 64 + 64 * 64 + 64 * 1)  # 66,688
+# What stock_rollout_tc_kernel actually issues to the tensor cores per transition (rollout_tc.cu
+# header): layer 1 of both nets as ONE [32 private features x 128] MMA (the 150 shared features'
+# term is computed once per step for the whole VecEnv), layer 2 of each net [64 x 64], the actor
+# head [64 x 32]; the critic head is a 64-term fp32 dot product on the SIMT pipes.
+TC_EXEC_FLOPS = 2 * 32 * 128 + 2 * (2 * 64 * 64) + 2 * 64 * 32  # 28,672
 # dram__bytes_read.sum + dram__bytes_write.sum of stock_rollout_tc_kernel<30> from one `ncu --set full`
 # capture (profiles/r1_tc_r3_full.txt: 65,536 envs x 32 steps), per transition; scaled to the launch below.
 TC_DRAM_BYTES_PER_TRANSITION = 261  # ncu dram__bytes_read+write.sum per transition, profiles/r1_s3_tc_r13_full.txt (1,094 MB / 65,536 x 64)
@@ -189,57 +194,101 @@ def market_arrays():
     return m, ind
 
 
-def cpu_reference_rate(m, ind, seconds: float, envs_per_worker: int = 64, horizon: int = 32):
-    """The reference's own worker_collect (pod.hpp:408-433: one VecEnv per
-    thread, disjoint buffer segments) on this box's host cores, built from the
-    unmodified headers (oracle/_ref/libpodracer_ref_bench.so)."""
+def ref_inputs(ref):
+    """The reference arm's inputs built by the reference build itself (oracle/_ref shim): the
+    BASELINE.md §3 synthetic market, compute_indicators (market.hpp:373-392) and
+    artifact_init(S, A, seed=7) (artifact.hpp:91-105) -- libprb.so is never loaded on this arm."""
+    from oracle_bind import ptr, SZ
+    close, high, low = (np.zeros((K_ASSETS, T_ROWS)) for _ in range(3))
+    ref.ref_synthetic_market(MARKET_SEED, K_ASSETS, T_ROWS, ptr(close), ptr(high), ptr(low))
+    ind = np.zeros((4, K_ASSETS, T_ROWS))
+    assert ref.ref_compute_indicators(ptr(high), ptr(low), ptr(close), T_ROWS, K_ASSETS, ptr(ind)) == 0
+    hid = np.array([64, 64], dtype=np.uint64)
+    P = ref.ref_artifact_init(S_DIM, K_ASSETS, 7, 1e-3, ptr(hid, SZ), 2, None)
+    flat = np.zeros(P)
+    ref.ref_artifact_init(S_DIM, K_ASSETS, 7, 1e-3, ptr(hid, SZ), 2, ptr(flat))
+    return close, ind, flat, hid
+
+
+REF_ENVS, REF_HORIZON = 1024, 256  # configs[0]: the reference's own CPU-runnable pod shape
+
+
+def ref_collect_step(ref, inputs, seed: int):
+    """ONE whole worker_collect phase of the reference's pod_train (pod.hpp:408-433) on the host
+    cores: W = the largest power of two <= cores threads, each owning a VecEnv of 1,024 / W stock
+    envs, horizon 256 -- 262,144 transitions of the configs[1] per-transition work (same env, same
+    181-64-64-30 / 181-64-64-1 nets).  Returns (seconds, transitions, threads)."""
+    from oracle_bind import ptr, SZ
+    close, ind, flat, hid = inputs
+    cores = os.cpu_count() or 1
+    W = min(1 << (cores.bit_length() - 1), REF_ENVS)
+    dt = ref.ref_bench_collect(ptr(close), ptr(ind), T_ROWS, K_ASSETS, 0, T_ROWS - 1, W, REF_ENVS // W, REF_HORIZON,
+                               ptr(flat), ptr(hid, SZ), 2, seed)
+    return dt, W * (REF_ENVS // W) * REF_HORIZON, W
+
+
+def ref_sample_desc(W, reps, total_tr, total_s):
+    return (f"{reps} whole worker_collect phases (pod.hpp:408-433): {W} threads x {REF_ENVS // W} stock envs x "
+            f"horizon {REF_HORIZON} = {REF_ENVS * REF_HORIZON} transitions each ({total_tr} transitions, "
+            f"{total_s:.1f} s), 64x64 actor/critic, f64, unmodified reference headers -O3 -march=x86-64-v3")
+
+
+def cpu_reference_rate(seconds: float):
+    """cpu_baseline: whole configs[0]-sized reference collects (ref_collect_step) repeated for
+    about `seconds` on the host cores."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bind import REF_BENCH_SO, load_ref, ptr, SZ
+    from oracle_bind import REF_BENCH_SO, load_ref
     ref = load_ref(REF_BENCH_SO)
     if ref is None:
         return None
-    from paper_2112_05923_b200 import podracer as pr
-    cores = os.cpu_count() or 1
-    W = 1 << (cores.bit_length() - 1)  # largest power of two <= cores (BASELINE.md §3)
-    flat = pr.artifact_init(S_DIM, K_ASSETS, 7)
-    hid = np.array([64, 64], dtype=np.uint64)
-    close = np.ascontiguousarray(m["close"]); indc = np.ascontiguousarray(ind)
+    inputs = ref_inputs(ref)
     total_s, total_tr, reps = 0.0, 0, 0
     while total_s < seconds or reps < 1:
-        dt = ref.ref_bench_collect(ptr(close), ptr(indc), T_ROWS, K_ASSETS, 0, T_ROWS - 1, W, envs_per_worker,
-                                   horizon, ptr(flat), ptr(hid, SZ), 2, 2112 + reps)
+        dt, tr, W = ref_collect_step(ref, inputs, 2112 + reps)
         total_s += dt
-        total_tr += W * envs_per_worker * horizon
+        total_tr += tr
         reps += 1
     return {"value": total_tr / total_s, "unit": UNIT, "cores": W, "kind": "reference",
-            "sample": f"worker_collect x{reps}: {W} threads x {envs_per_worker} stock envs x horizon {horizon} "
-                      f"({total_tr} transitions, {total_s:.1f} s), 64x64 actor/critic, f64, -O3 -march=x86-64-v3"}
+            "sample": ref_sample_desc(W, reps, total_tr, total_s)}
 
 
 def run_reference(args, d: Dist):
+    """--impl reference: the reference's own CPU path (oracle/_ref/libpodracer_ref_bench.so, the
+    unmodified headers) on the host cores, rank 0 only.  A step is one whole worker_collect
+    phase of a configs[0]-sized pod (1,024 envs x 256); nothing is projected."""
     if d.rank != 0:
         return
-    m, ind = market_arrays()
-    # each step = one bounded sample of the configs[1] workload on the host cores
-    rates = []
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import REF_BENCH_SO, load_ref
+    ref = load_ref(REF_BENCH_SO)
+    if ref is None:
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"})
+        return
+    inputs = ref_inputs(ref)
+    times, trs = [], []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_rate(m, ind, seconds=2.0)  # ~2 s of host work per step
-        if r is None:
-            emit(({"impl": "reference", "unavailable": "oracle/_ref/libpodracer_ref_bench.so not built"}))
-            return
+        dt, tr, W = ref_collect_step(ref, inputs, 2112 + i)
         if i >= args.warmup:
-            rates.append(r)
-    value = float(np.mean([r["value"] for r in rates]))
-    cb = dict(rates[-1])
-    cb["value"] = value
+            times.append(dt)
+            trs.append(tr)
+    total_s, total_tr = float(sum(times)), int(sum(trs))
+    value = total_tr / total_s
+    cb = {"value": value, "unit": UNIT, "cores": W, "kind": "reference",
+          "sample": ref_sample_desc(W, len(times), total_tr, total_s)}
+    cfg = config_dict(args)
+    cfg.update({"workload": f"reference worker_collect, configs[0]-sized sample of the configs[1] workload: "
+                            f"stock-trading VecEnv {K_ASSETS} assets x {REF_ENVS} envs ({W} threads x "
+                            f"{REF_ENVS // W}), horizon {REF_HORIZON}, one whole collect per step",
+                "envs_per_gpu": None, "envs": REF_ENVS, "horizon": REF_HORIZON,
+                "parallelism": f"{W} host threads (rank 0 only)",
+                "l2": "host CPU path (no GPU)"})
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": args.envs * args.horizon / value * 1e3,  # one full configs[1] collect at the sampled rate
-           "ms_per_step_note": "projected: envs x horizon / sampled rate", "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": config_dict(args), "cpu_baseline": cb,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / len(times) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.md §3 market and artifact_init weights, built by the reference build)",
+           "config": cfg, "cpu_baseline": cb,
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    emit((out))
+    emit(out)
 
 
 def config_dict(args):
@@ -305,8 +354,13 @@ def run_ours(args, d: Dist):
             k = {"bound": "hbm", "unit": "GB/s", "achieved": N * ENV_BYTES / avg_s / 1e9, "peak": hbm,
                  "work_per_launch": f"{N} envs x {ENV_BYTES} B"}
         else:
-            k = {"bound": "tensor", "unit": "TFLOP/s", "achieved": N * H * MLP_FLOPS / avg_s / 1e12, "peak": bf16_sus,
-                 "work_per_launch": f"{N}x{H} transitions x {MLP_FLOPS} FLOP (actor+critic fwd)",
+            # one launch is a ~4 ms collect inside a ~80 ms region: the burst bf16 peak applies
+            k = {"bound": "tensor", "unit": "TFLOP/s", "achieved": N * H * MLP_FLOPS / avg_s / 1e12, "peak": bf16,
+                 "work_per_launch": f"{N}x{H} transitions x {MLP_FLOPS} FLOP (algorithmic actor+critic fwd)",
+                 "executed_tensor_tflops": N * H * TC_EXEC_FLOPS / avg_s / 1e12,
+                 "executed_tensor_flop_per_transition": TC_EXEC_FLOPS,
+                 "executed_note": "the kernel issues 28,672 tensor FLOP per transition: layer 1 over the 31 "
+                                  "private features (K=32), the 150 shared features' term once per step per VecEnv",
                  "hbm_gbs": N * H * BUF_BYTES / avg_s / 1e9, "hbm_frac": N * H * BUF_BYTES / avg_s / 1e9 / hbm,
                  "hbm_bytes_per_transition": BUF_BYTES}
         k.update({"ms_total": ms, "launches": n, "share": ms / region_ms, "frac": k["achieved"] / k["peak"]})
@@ -318,7 +372,7 @@ def run_ours(args, d: Dist):
                 "traffic": (N * H * TC_DRAM_BYTES_PER_TRANSITION if dom == "stock_rollout_fused" else None),
                 "traffic_source": "ncu dram bytes/transition, profiles/r1_s3_tc_r13_full.txt, x transitions per launch",
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json "
-                               f"{'bf16_tflops_sustained' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
+                               f"{'bf16_tflops (burst)' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
     if dom == "stock_rollout_fused":
         # neither the tensor nor the HBM roof binds this kernel (both < 20%): per-thread instruction
         # issue does -- the fp64 portfolio chain + sampling + epilogues; ncu of the same kernel
@@ -409,14 +463,14 @@ def run_ours(args, d: Dist):
     # ---- CPU baseline: the reference path on this box's host cores (rank 0, N=1 only) ----
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.skip_cpu:
-        cpu = cpu_reference_rate(m, ind, seconds=args.cpu_seconds)
+        cpu = cpu_reference_rate(seconds=args.cpu_seconds)
 
     # kernel launches in the timed region: fused collect = shared-layer kernel + fused kernel
     launches = int(prof["policy_fwd_sample"][1] + prof["env_stock_step"][1] + 2 * prof["stock_rollout_fused"][1])
     if d.rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32 (MLP, obs) + f64 (portfolio accounting)",
+               "scaling": "weak", "vs_baseline": None, "dtype": "bf16 tcgen05 MLP (fp32 accum) + fp64 accounting",
                "data": "synthetic (BASELINE.md §3 market, random-init artifact_init weights)",
                "config": config_dict(args), "roofline": roofline, "kernels": kernels, "env_step": env_step,
                "gae": gae, "adam": adam, "ppo_update": ppo, "other_configs": other, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -393,6 +394,78 @@ inline std::vector<int> leaderboard_rank(Context& ctx, const std::vector<double>
   std::int32_t n = 0;
   check(prb_leaderboard_rank_host(ctx.get(), scores.data(), seqs.data(), scores.size(), capacity, order.data(), &n));
   return std::vector<int>(order.begin(), order.begin() + n);
+}
+
+// ---- Leaderboard tournament.hpp:31-119 -----------------------------------------
+// Entries keep their agents on the device; refresh_stats runs prb_leaderboard_stats over the
+// entries' parameter blobs (fp64, the reference's summation order).
+struct PopulationStats {  // tournament.hpp:38-41
+  std::vector<double> mean;
+  std::vector<double> variance;
+};
+
+struct LeaderboardEntry {  // tournament.hpp:31-36
+  std::shared_ptr<const Agent> artifact;
+  double score = 0.0;
+  std::int64_t pod_id = -1;
+  std::uint64_t seq = 0;
+};
+
+class Leaderboard {
+ public:
+  explicit Leaderboard(std::size_t capacity = 10) : capacity_(capacity) {
+    if (capacity_ == 0) throw ConfigError("Leaderboard: capacity must be > 0");
+  }
+  std::size_t capacity() const { return capacity_; }
+  std::size_t size() const { return entries_.size(); }
+  bool empty() const { return entries_.empty(); }
+  const std::vector<LeaderboardEntry>& entries() const { return entries_; }
+  const LeaderboardEntry& at(std::size_t rank) const { return entries_.at(rank); }
+  const PopulationStats& stats() const { return stats_; }
+  double min_score() const { return entries_.back().score; }
+  double best_score() const { return entries_.front().score; }
+  std::uint64_t next_seq() { return seq_counter_++; }
+  std::vector<LeaderboardEntry>& mutable_entries() { return entries_; }
+  void refresh_stats() {  // tournament.hpp:66-87, on the device
+    stats_.mean.clear();
+    stats_.variance.clear();
+    if (entries_.empty()) return;
+    std::vector<prb_agent> hs;
+    for (const auto& e : entries_) hs.push_back(e.artifact->get());
+    const std::size_t P = entries_.front().artifact->param_count();
+    stats_.mean.assign(P, 0.0);
+    stats_.variance.assign(P, 0.0);
+    check(prb_leaderboard_stats_host(hs.data(), hs.size(), stats_.mean.data(), stats_.variance.data()));
+  }
+
+ private:
+  std::size_t capacity_;
+  std::vector<LeaderboardEntry> entries_;  // (score desc, seq asc)
+  PopulationStats stats_;
+  std::uint64_t seq_counter_ = 0;
+};
+
+struct LeaderboardUpdate {  // tournament.hpp:93-96
+  bool inserted = false;
+  bool has_rank = false;
+  std::size_t rank = 0;
+};
+
+// leaderboard_update tournament.hpp:104-119: non-finite -> NumericError; seq = arrival counter;
+// a full board rejects scores <= its minimum; insert after every entry scoring >= the candidate;
+// evict the tail; refresh the population stats.
+inline LeaderboardUpdate leaderboard_update(Leaderboard& board, LeaderboardEntry candidate) {
+  if (!(candidate.score == candidate.score) || candidate.score == HUGE_VAL || candidate.score == -HUGE_VAL)
+    throw NumericError("leaderboard_update: candidate score is not finite");
+  candidate.seq = board.next_seq();
+  auto& entries = board.mutable_entries();
+  if (entries.size() >= board.capacity() && candidate.score <= entries.back().score) return {};
+  std::size_t pos = 0;
+  while (pos < entries.size() && entries[pos].score >= candidate.score) ++pos;
+  entries.insert(entries.begin() + (std::ptrdiff_t)pos, std::move(candidate));
+  if (entries.size() > board.capacity()) entries.pop_back();
+  board.refresh_stats();
+  return LeaderboardUpdate{true, true, pos};
 }
 
 // GeneratorConfig tournament.hpp:125-129

@@ -242,7 +242,8 @@ typedef struct {
  * gradients, Adam).  GAE is (re)computed from r.  Permutations: if perm is
  * NULL they are generated on device from seed; else perm holds
  * epochs*buffer_size indices in the reference index space (e.g. the exact
- * std::shuffle sequence).  On error dst is unspecified and src untouched. */
+ * std::shuffle sequence).  On error dst is unspecified and src untouched;
+ * src == dst is allowed (the agent is restored on error). */
 PRB_API int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed,
                            const uint64_t* perm, prb_agent dst, prb_ppo_stats* stats);
 /* detail::ppo_loss_grads ppo.hpp:116-188 on one minibatch of rollout rows
@@ -283,6 +284,13 @@ PRB_API int prb_leaderboard_rank(prb_ctx ctx, const double* d_scores, const uint
                                  size_t capacity, int32_t* d_order, int32_t* d_count);
 PRB_API int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t* seqs, size_t n,
                                       size_t capacity, int32_t* order, int32_t* count);
+/* Leaderboard::refresh_stats tournament.hpp:66-87 (PopulationStats :38-41):
+ * per-coordinate mean and population variance (divide by n) of the flat
+ * parameters of the board's entries, entries[0..n) in board order, fp64 in
+ * the reference's summation order.  d_mean / d_variance: [P] fp64 device
+ * arrays on the entries' device.  n == 0 (empty board) writes nothing. */
+PRB_API int prb_leaderboard_stats(const prb_agent* entries, size_t n, double* d_mean, double* d_variance);
+PRB_API int prb_leaderboard_stats_host(const prb_agent* entries, size_t n, double* mean, double* variance);
 /* generate_pod_init's mutation (tournament.hpp:149-159): params += N(0, sigma^2)
  * from a Philox stream keyed by mutation_seed; optimiser t := 0, m/v kept. */
 PRB_API int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma);
@@ -301,6 +309,14 @@ PRB_API int prb_leaderboard_allgather_rank(prb_comm c, const double* d_scores, c
                                            int32_t* d_count);
 /* Broadcast an agent's params, m, v and t from `root` (elite broadcast). */
 PRB_API int prb_agent_broadcast(prb_comm c, prb_agent a, int root);
+
+/* ---- test-only switches (no reference analogue) -------------------------- */
+/* Process-wide; they select alternate device paths so tests can check them
+ * against the default path.  Production code never sets them. */
+#define PRB_OPT_PPO_PER_KERNEL 1 /* prb_ppo_update: per-kernel path (4 launches per minibatch) */
+#define PRB_OPT_TC_FORCE_REDO 2  /* stock tcgen05 rollout: exact-division redo of every step's trades */
+#define PRB_OPT_PM_CTA_PAIR 3    /* PointMass 3x256 rollout: the cta_group::2 CTA-pair kernel */
+PRB_API int prb_debug_set_option(int option, int value);
 
 /* ---- self-test of the tcgen05 building block (tests only) --------------- */
 /* D[128][N] = bf16(A[128][K]) . bf16(B[N][K])^T with fp32 accumulation in

@@ -748,6 +748,23 @@ ORC_API int orc_leaderboard_update(double* scores, uint64_t* seqs, int64_t* ids,
   return (int)pos;
 }
 
+/* Leaderboard::refresh_stats tournament.hpp:66-87: per-coordinate mean and    */
+/* population variance of the entries' flat params (entries[e] in board order).*/
+ORC_API void orc_population_stats(const double* const* entries, size_t n, size_t P, double* mean, double* var) {
+  if (n == 0) return; /* :69 */
+  for (size_t i = 0; i < P; ++i) mean[i] = var[i] = 0.0;
+  for (size_t e = 0; e < n; ++e) /* :73-76 */
+    for (size_t i = 0; i < P; ++i) mean[i] += entries[e][i];
+  const double inv = 1.0 / (double)n; /* :77-78 */
+  for (size_t i = 0; i < P; ++i) mean[i] *= inv;
+  for (size_t e = 0; e < n; ++e) /* :79-85 */
+    for (size_t i = 0; i < P; ++i) {
+      const double d = entries[e][i] - mean[i];
+      var[i] += d * d;
+    }
+  for (size_t i = 0; i < P; ++i) var[i] *= inv; /* :86 */
+}
+
 /* ------------------------------------------------------------------------- */
 /* Indicators: compute_indicators market.hpp:373-392 and helpers :285-366.    */
 /* out[(i*K + k)*T + t] for i in macd, rsi_14, cci_30, sma_20.                */

@@ -440,6 +440,32 @@ REF_API int ref_leaderboard_sequence(const double* scores, const int64_t* ids, s
   })
 }
 
+// ---- leaderboard_update + refresh_stats tournament.hpp:66-119 with real artifacts ----
+// Candidate i carries flat params cand[i*P .. i*P+P) of an S-hidden-A agent.  Inserts them in
+// order; writes the final board's pod ids (rank order) and the board's PopulationStats.
+REF_API int ref_leaderboard_stats(const double* cand, const double* scores, const int64_t* ids, size_t n,
+                                  size_t capacity, size_t S, size_t A, const size_t* hidden, int nh,
+                                  int64_t* out_ids, size_t* out_size, double* mean, double* variance) {
+  GUARD({
+    Leaderboard board(capacity);
+    size_t P = 0;
+    for (size_t i = 0; i < n; ++i) {
+      LeaderboardEntry e;
+      e.artifact = artifact_init(S, A, 0, 1e-3, dims_of(hidden, nh));
+      P = e.artifact.param_count();
+      e.artifact.unflatten_params(std::vector<double>(cand + i * P, cand + (i + 1) * P));
+      e.score = scores[i];
+      e.pod_id = ids[i];
+      leaderboard_update(board, e);
+    }
+    *out_size = board.size();
+    for (size_t r = 0; r < board.size(); ++r) out_ids[r] = board.at(r).pod_id;
+    const PopulationStats& st = board.stats();
+    std::copy(st.mean.begin(), st.mean.end(), mean);
+    std::copy(st.variance.begin(), st.variance.end(), variance);
+  })
+}
+
 // ppo_update ppo.hpp:249 timing on a synthetic buffer of n transitions (chunks of
 // `horizon`; states/actions/log-probs/values/rewards from mt19937_64(seed)),
 // `epochs` x (n / minibatch) sequential Adam steps.  Returns wall seconds.
@@ -474,6 +500,23 @@ REF_API double ref_bench_ppo(const double* flat, size_t S, size_t A, const size_
 }
 
 // ---- CPU baseline timing (bench.py --impl reference / cpu_baseline) --------
+// The bench's synthetic market (the reference ships no generator): mt19937_64(seed);
+// p0_k ~ U(10,200) for k = 0..K-1, then for t = 1..T-1, k = 0..K-1: p_k[t] = p_k[t-1] * exp(1e-3 N(0,1));
+// high = 1.001 p, low = 0.999 p.  Arrays [K][T].  Lets the reference arm build its inputs without
+// the product library.
+REF_API void ref_synthetic_market(uint64_t seed, int K, size_t T, double* close, double* high, double* low) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u0(10.0, 200.0);
+  std::normal_distribution<double> nrm(0.0, 1.0);
+  for (int k = 0; k < K; ++k) close[(size_t)k * T] = u0(rng);
+  for (size_t t = 1; t < T; ++t)
+    for (int k = 0; k < K; ++k) close[(size_t)k * T + t] = close[(size_t)k * T + t - 1] * std::exp(1e-3 * nrm(rng));
+  for (size_t i = 0; i < (size_t)K * T; ++i) {
+    high[i] = 1.001 * close[i];
+    low[i] = 0.999 * close[i];
+  }
+}
+
 // pod_train's collect phase (pod.hpp:408-433): `workers` threads, each owning
 // a VectorizedEnvironment of envs_per_worker stock envs, running worker_collect
 // for `horizon` steps into disjoint segments of one shared buffer.

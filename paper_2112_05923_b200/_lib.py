@@ -165,6 +165,9 @@ SIGNATURES = {
     "prb_leaderboard_rank": (I, [P, P, P, SZ, SZ, P, P]),
     "prb_leaderboard_rank_host": (I, [P, pD, pU64, SZ, SZ, pI32, pI32]),
     "prb_agent_mutate": (I, [P, U64, D]),
+    "prb_leaderboard_stats": (I, [C.POINTER(P), SZ, P, P]),
+    "prb_leaderboard_stats_host": (I, [C.POINTER(P), SZ, pD, pD]),
+    "prb_debug_set_option": (I, [I, I]),
     "prb_comm_unique_id": (I, [C.POINTER(C.c_uint8)]),
     "prb_comm_init": (I, [P, C.POINTER(C.c_uint8), I, I, C.POINTER(P)]),
     "prb_comm_destroy": (I, [P]),

@@ -146,13 +146,37 @@ __global__ void leaderboard_rank_kernel(const double* __restrict__ score, const 
     int rank = 0;
     for (int j = 0; j < n; ++j) {
       const double sj = score[j];
-      rank += (sj > si) || (sj == si && seq[j] < qi);
+      // (score desc, seq asc); duplicate (score, seq) keys fall back to the candidate index so
+      // every rank is taken exactly once
+      rank += (sj > si) || (sj == si && (seq[j] < qi || (seq[j] == qi && j < i)));
     }
     if (rank < capacity) order[rank] = i;
   }
   if (threadIdx.x == 0) {
     *count = min(n, capacity);
     status[0] = 0;
+  }
+}
+
+// Leaderboard::refresh_stats (tournament.hpp:66-87): per-coordinate mean and population variance
+// of the entries' flat parameters, in the reference's order -- sum over the entries in board
+// order, times 1/n, then the sum of squared deviations times 1/n -- in fp64 with explicit
+// round-to-nearest (the -ffp-contract=off reference build).  One thread per coordinate; every
+// entry's params are read twice (n x 4 B x 2, L2 serves the second pass for a board of <= 10).
+__global__ void population_stats_kernel(const float* const* __restrict__ entries, int n, size_t P,
+                                        double* __restrict__ mean, double* __restrict__ var) {
+  const double inv = 1.0 / (double)n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (size_t)gridDim.x * blockDim.x) {
+    double m = 0.0;
+    for (int e = 0; e < n; ++e) m = __dadd_rn(m, (double)entries[e][i]);
+    m = __dmul_rn(m, inv);
+    double v = 0.0;
+    for (int e = 0; e < n; ++e) {
+      const double d = __dsub_rn((double)entries[e][i], m);
+      v = __dadd_rn(v, __dmul_rn(d, d));
+    }
+    mean[i] = m;
+    var[i] = __dmul_rn(v, inv);
   }
 }
 
@@ -190,6 +214,7 @@ extern "C" {
 
 int prb_agent_create(prb_ctx ctx, size_t S, size_t A, const size_t* hidden, int nh, prb_agent* out) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_agent_create: NULL argument");
     PRB_REQUIRE(S > 0 && A > 0, PRB_ERR_USAGE, "mlp_init: need at least input and output dims");
     PRB_REQUIRE(nh >= 0 && nh <= 6, PRB_ERR_CONFIG, "prb_agent_create: 0..6 hidden layers supported");
@@ -224,6 +249,7 @@ int prb_agent_create(prb_ctx ctx, size_t S, size_t A, const size_t* hidden, int 
 
 int prb_agent_destroy(prb_agent a) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     if (a) cudaStreamSynchronize(a->ctx->stream);
     delete a;
   });
@@ -234,6 +260,7 @@ float* prb_agent_params_device(prb_agent a) { return a ? a->d_params.p : nullptr
 
 int prb_agent_set_host(prb_agent a, const double* flat, const double* m, const double* v, int64_t t, double lr) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && flat, PRB_ERR_USAGE, "prb_agent_set_host: NULL argument");
     std::vector<float> buf(a->P);
     cudaStream_t s = a->ctx->stream;
@@ -262,6 +289,7 @@ int prb_agent_set_host(prb_agent a, const double* flat, const double* m, const d
 
 int prb_agent_get_host(prb_agent a, double* flat, double* m, double* v, int64_t* t) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_get_host: NULL agent");
     std::vector<float> buf(a->P);
     cudaStream_t s = a->ctx->stream;
@@ -283,6 +311,7 @@ int prb_agent_get_host(prb_agent a, double* flat, double* m, double* v, int64_t*
 
 int prb_agent_copy(prb_agent dst, prb_agent src) {
   return guard([&] {
+    DeviceScope dev_(dst ? dst->ctx : nullptr);
     PRB_REQUIRE(dst && src, PRB_ERR_USAGE, "prb_agent_copy: NULL agent");
     PRB_REQUIRE(dst->P == src->P && dst->adims == src->adims && dst->cdims == src->cdims, PRB_ERR_USAGE,
                 "prb_agent_copy: incompatible shapes");
@@ -298,6 +327,7 @@ int prb_agent_copy(prb_agent dst, prb_agent src) {
 
 int prb_adam_step_host(prb_agent a, const double* grads) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && grads, PRB_ERR_USAGE, "prb_adam_step_host: NULL argument");
     for (size_t i = 0; i < a->P; ++i)  // nn.hpp:169-171: reject before touching state
       PRB_REQUIRE(std::isfinite(grads[i]), PRB_ERR_NUMERIC, "adam_step: non-finite gradient, step aborted");
@@ -312,6 +342,7 @@ int prb_adam_step_host(prb_agent a, const double* grads) {
 
 int prb_adam_step_device(prb_agent a, const float* d_grads) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_grads, PRB_ERR_USAGE, "prb_adam_step_device: NULL argument");
     cudaStream_t s = a->ctx->stream;
     prb_agent_finite_gate_and_adam(a, d_grads, s);
@@ -328,6 +359,7 @@ int prb_adam_step_device(prb_agent a, const float* d_grads) {
 
 int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out) {
   return guard([&] {
+    DeviceScope dev_(out ? out->ctx : nullptr);
     PRB_REQUIRE(n > 0 && agents, PRB_ERR_USAGE, "fuse_parameters: empty artifact list");  // pod.hpp:142
     PRB_REQUIRE(out, PRB_ERR_USAGE, "fuse_parameters: NULL output");
     for (size_t i = 0; i < n; ++i)
@@ -395,6 +427,7 @@ int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out) {
 int prb_leaderboard_rank(prb_ctx ctx, const double* d_scores, const uint64_t* d_seqs, size_t n, size_t capacity,
                          int32_t* d_order, int32_t* d_count) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx, PRB_ERR_USAGE, "prb_leaderboard_rank: NULL ctx");
     PRB_REQUIRE(capacity > 0, PRB_ERR_CONFIG, "Leaderboard: capacity must be > 0");  // tournament.hpp:47
     PRB_REQUIRE(n < (1u << 20), PRB_ERR_CONFIG, "prb_leaderboard_rank: too many candidates");
@@ -412,6 +445,7 @@ int prb_leaderboard_rank(prb_ctx ctx, const double* d_scores, const uint64_t* d_
 int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t* seqs, size_t n, size_t capacity,
                               int32_t* order, int32_t* count) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx, PRB_ERR_USAGE, "prb_leaderboard_rank_host: NULL ctx");
     DevBuf<double> ds;
     DevBuf<uint64_t> dq;
@@ -434,8 +468,51 @@ int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t*
   });
 }
 
+int prb_leaderboard_stats(const prb_agent* entries, size_t n, double* d_mean, double* d_variance) {
+  return guard([&] {
+    PRB_REQUIRE(entries && d_mean && d_variance, PRB_ERR_USAGE, "prb_leaderboard_stats: NULL argument");
+    if (n == 0) return;  // an empty board has empty stats (tournament.hpp:69)
+    for (size_t i = 0; i < n; ++i)
+      PRB_REQUIRE(entries[i] && entries[i]->P == entries[0]->P && entries[i]->ctx->device == entries[0]->ctx->device,
+                  PRB_ERR_USAGE, "prb_leaderboard_stats: entries have different shapes or devices");
+    PRB_REQUIRE(n < (1u << 20), PRB_ERR_CONFIG, "prb_leaderboard_stats: too many entries");
+    prb_ctx_s* ctx = entries[0]->ctx;
+    DeviceScope dev(ctx);
+    cudaStream_t s = ctx->stream;
+    for (size_t i = 1; i < n; ++i)
+      if (entries[i]->ctx->stream != s) entries[i]->ctx->sync();
+    std::vector<const float*> hp(n);
+    for (size_t i = 0; i < n; ++i) hp[i] = entries[i]->d_params.p;
+    DevBuf<const float*> dp;
+    dp.alloc(n);
+    PRB_CUDA(cudaMemcpyAsync(dp.p, hp.data(), n * sizeof(float*), cudaMemcpyHostToDevice, s));
+    const size_t P = entries[0]->P;
+    const int grid = (int)std::min<size_t>((P + 255) / 256, (size_t)ctx->num_sms * 8);
+    population_stats_kernel<<<grid, 256, 0, s>>>(dp.p, (int)n, P, d_mean, d_variance);
+    PRB_CHECK_LAUNCH();
+    ctx->sync();  // dp is released on return
+  });
+}
+
+int prb_leaderboard_stats_host(const prb_agent* entries, size_t n, double* mean, double* variance) {
+  return guard([&] {
+    PRB_REQUIRE(entries && mean && variance, PRB_ERR_USAGE, "prb_leaderboard_stats_host: NULL argument");
+    if (n == 0) return;
+    PRB_REQUIRE(entries[0], PRB_ERR_USAGE, "prb_leaderboard_stats_host: NULL entry");
+    DeviceScope dev(entries[0]->ctx);
+    const size_t P = entries[0]->P;
+    DevBuf<double> d;
+    d.alloc(2 * P);
+    int rc = prb_leaderboard_stats(entries, n, d.p, d.p + P);
+    if (rc) fail(rc, prb_last_error());
+    PRB_CUDA(cudaMemcpy(mean, d.p, P * sizeof(double), cudaMemcpyDeviceToHost));
+    PRB_CUDA(cudaMemcpy(variance, d.p + P, P * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
 int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_mutate: NULL agent");
     cudaStream_t s = a->ctx->stream;
     if (sigma > 0.0) {

@@ -1,7 +1,9 @@
 // api_core.cu -- context, memory, errors, seeds, market data and artifact
 // initialisation for the prb_* C ABI.  Host code; the market feature table
 // and price table it builds are the device-resident inputs of the env kernels.
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -17,6 +19,31 @@ static thread_local int g_last_code = 0;
 void set_last_error(int code, const std::string& msg) {
   g_last_code = code;
   g_last_error = msg;
+}
+
+void ensure_smem_attr(const void* kernel, size_t smem_bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;  // ((kernel, device), bytes)
+  int dev = 0;
+  PRB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first.first == kernel && e.first.second == dev && e.second >= smem_bytes) return;
+  PRB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  done.push_back({{kernel, dev}, smem_bytes});
+}
+
+static std::atomic<int> g_options[8];
+
+int debug_option(int option) { return (option > 0 && option < 8) ? g_options[option].load() : 0; }
+
+const char* debug_env(const char* name) {
+#ifdef PRB_DEBUG_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
 }
 
 uint64_t splitmix64(uint64_t x) { return splitmix64_d(x); }
@@ -69,6 +96,13 @@ extern "C" {
 const char* prb_last_error(void) { return g_last_error.c_str(); }
 int prb_version(void) { return 1; }
 
+int prb_debug_set_option(int option, int value) {
+  return guard([&] {
+    PRB_REQUIRE(option > 0 && option < 8, PRB_ERR_USAGE, "prb_debug_set_option: unknown option");
+    g_options[option].store(value);
+  });
+}
+
 uint64_t prb_splitmix64(uint64_t x) { return splitmix64(x); }
 
 uint64_t prb_derive_seed(uint64_t base, const uint64_t* tags, int n) {
@@ -94,6 +128,7 @@ int prb_ctx_create(int device, prb_ctx* out) {
 
 int prb_ctx_destroy(prb_ctx c) {
   return guard([&] {
+    DeviceScope dev_(c);
     if (!c) return;
     cudaStreamSynchronize(c->stream);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -107,6 +142,7 @@ int prb_ctx_synchronize(prb_ctx c) { return guard([&] { c->sync(); }); }
 
 int prb_ctx_profile(prb_ctx c, int enable) {
   return guard([&] {
+    DeviceScope dev_(c);
     PRB_REQUIRE(c, PRB_ERR_USAGE, "prb_ctx_profile: NULL ctx");
     c->sync();
     for (auto& e : c->ev_live) {
@@ -124,6 +160,7 @@ int prb_ctx_profile(prb_ctx c, int enable) {
 
 int prb_ctx_profile_read(prb_ctx c, int kind, double* total_ms, uint64_t* launches) {
   return guard([&] {
+    DeviceScope dev_(c);
     PRB_REQUIRE(c && kind >= 0 && kind < 16, PRB_ERR_USAGE, "prb_ctx_profile_read: bad argument");
     c->sync();
     for (auto& e : c->ev_live) {
@@ -143,6 +180,7 @@ void* prb_ctx_stream(prb_ctx c) { return c ? (void*)c->stream : nullptr; }
 
 int prb_device_alloc(prb_ctx c, size_t bytes, void** out) {
   return guard([&] {
+    DeviceScope dev_(c);
     PRB_CUDA(cudaSetDevice(c->device));
     PRB_CUDA(cudaMalloc(out, bytes ? bytes : 1));
   });
@@ -150,12 +188,14 @@ int prb_device_alloc(prb_ctx c, size_t bytes, void** out) {
 int prb_device_free(prb_ctx, void* p) { return guard([&] { PRB_CUDA(cudaFree(p)); }); }
 int prb_memcpy_h2d(prb_ctx c, void* d, const void* s, size_t n) {
   return guard([&] {
+    DeviceScope dev_(c);
     PRB_CUDA(cudaMemcpyAsync(d, s, n, cudaMemcpyHostToDevice, c->stream));
     c->sync();
   });
 }
 int prb_memcpy_d2h(prb_ctx c, void* d, const void* s, size_t n) {
   return guard([&] {
+    DeviceScope dev_(c);
     PRB_CUDA(cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
   });
@@ -276,6 +316,7 @@ int prb_compute_indicators(const double* high, const double* low, const double* 
 
 int prb_market_create(prb_ctx ctx, const double* close, const double* indicators, size_t T, int K, prb_market* out) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && out && close, PRB_ERR_USAGE, "prb_market_create: NULL argument");
     PRB_REQUIRE(K > 0 && T >= 2, PRB_ERR_DIMENSION, "prb_market_create: need K > 0 tickers and T >= 2 rows");
     PRB_CUDA(cudaSetDevice(ctx->device));

@@ -79,6 +79,7 @@ int prb_comm_unique_id(uint8_t id[128]) {
 
 int prb_comm_init(prb_ctx ctx, const uint8_t id[128], int nranks, int rank, prb_comm* out) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && id && out, PRB_ERR_USAGE, "prb_comm_init: NULL argument");
     PRB_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, PRB_ERR_CONFIG, "prb_comm_init: bad rank/nranks");
     PRB_CUDA(cudaSetDevice(ctx->device));
@@ -95,6 +96,7 @@ int prb_comm_init(prb_ctx ctx, const uint8_t id[128], int nranks, int rank, prb_
 
 int prb_comm_destroy(prb_comm c) {
   return guard([&] {
+    DeviceScope dev_(c ? c->ctx : nullptr);
     if (!c) return;
     if (c->comm) nccl().CommDestroy(c->comm);
     delete c;
@@ -108,6 +110,7 @@ int prb_leaderboard_allgather_rank(prb_comm c, const double* d_scores, const uin
                                    size_t n_local, size_t capacity, double* d_all_scores, uint64_t* d_all_seqs,
                                    int64_t* d_all_ids, int32_t* d_order, int32_t* d_count) {
   return guard([&] {
+    DeviceScope dev_(c ? c->ctx : nullptr);
     PRB_REQUIRE(c && d_scores && d_seqs && d_ids && d_all_scores && d_all_seqs && d_all_ids && d_order && d_count,
                 PRB_ERR_USAGE, "prb_leaderboard_allgather_rank: NULL argument");
     cudaStream_t s = c->ctx->stream;
@@ -125,6 +128,7 @@ int prb_leaderboard_allgather_rank(prb_comm c, const double* d_scores, const uin
 
 int prb_agent_broadcast(prb_comm c, prb_agent a, int root) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(c && a, PRB_ERR_USAGE, "prb_agent_broadcast: NULL argument");
     PRB_REQUIRE(root >= 0 && root < c->nranks, PRB_ERR_CONFIG, "prb_agent_broadcast: bad root");
     cudaStream_t s = c->ctx->stream;

@@ -57,189 +57,6 @@ struct StockStepArgs {
   int32_t* __restrict__ term_len;
 };
 
-// Coalesced write of a CTA's block of obs rows: row r = [priv[r][0..P), shared[0..S-P)].
-// The block is one contiguous span; when it is 16-byte aligned it is written
-// as float4 (4x fewer store instructions), tracking (row, col) incrementally.
-__device__ __forceinline__ void write_obs_rows(float* __restrict__ dst, int nrows, int S, int P,
-                                               const float* __restrict__ s_priv, int Pp,
-                                               const float* __restrict__ s_shared) {
-  const int total = nrows * S;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    const int total4 = total >> 2;
-    const int step = 4 * (int)blockDim.x;
-    int f = 4 * threadIdx.x;
-    int r = f / S, c = f - r * S;
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int q = threadIdx.x; q < total4; q += blockDim.x) {
-      float v[4];
-      int rr = r, cc = c;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        v[i] = (cc < P) ? s_priv[rr * Pp + cc] : s_shared[cc - P];
-        if (++cc == S) {
-          cc = 0;
-          ++rr;
-        }
-      }
-      d4[q] = make_float4(v[0], v[1], v[2], v[3]);
-      c += step;
-      while (c >= S) {
-        c -= S;
-        ++r;
-      }
-    }
-    for (int i = total4 * 4 + threadIdx.x; i < total; i += blockDim.x) {
-      const int rr = i / S, cc = i - rr * S;
-      dst[i] = (cc < P) ? s_priv[rr * Pp + cc] : s_shared[cc - P];
-    }
-    return;
-  }
-  int r = threadIdx.x / S, c = threadIdx.x - (threadIdx.x / S) * S;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    dst[i] = (c < P) ? s_priv[r * Pp + c] : s_shared[c - P];
-    c += blockDim.x;
-    while (c >= S) {
-      c -= S;
-      ++r;
-    }
-  }
-}
-
-// One VecEnv step of N stock envs (env.hpp:200-236 -> StockTradingEnv::step
-// stock_env.hpp:165-170 -> stock_env_step :55-103 -> stock_observation :115-131).
-template <int KMAX>
-__global__ void __launch_bounds__(kEnvBlock) stock_step_kernel(StockStepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K, Kp = K + 1, F = 5 * K;
-  double* s_p0 = reinterpret_cast<double*>(smem_raw);      // [K] close[t]
-  double* s_p1 = s_p0 + K;                                  // [K] close[t+1]
-  float* s_act = reinterpret_cast<float*>(s_p1 + K);        // [128][Kp]
-  int32_t* s_sh = reinterpret_cast<int32_t*>(s_act + kEnvBlock * Kp);  // [K][128]
-  float* s_priv = reinterpret_cast<float*>(s_sh + K * kEnvBlock);      // [128][Kp]
-  float* s_feat_obs = s_priv + kEnvBlock * Kp;                         // [5K]
-  float* s_feat_term = s_feat_obs + F;                                 // [5K]
-
-  const int tid = threadIdx.x;
-  const size_t e0 = (size_t)blockIdx.x * kEnvBlock;
-  const int nloc = min(kEnvBlock, a.N - (int)e0);
-
-  for (int k = tid; k < K; k += blockDim.x) {
-    s_p0[k] = a.close_tk[(size_t)a.t * K + k];
-    s_p1[k] = a.close_tk[(size_t)(a.t + 1) * K + k];
-  }
-  for (int j = tid; j < F; j += blockDim.x) {
-    s_feat_obs[j] = a.feat[(size_t)a.t_obs * F + j];
-    if (a.done) s_feat_term[j] = a.feat[(size_t)(a.t + 1) * F + j];
-  }
-  // Issue every global load of this CTA before consuming any (memory-level
-  // parallelism is what an HBM-bound step needs): the [nloc][K] action block
-  // as 16-byte vectors, the env's shares (SoA, coalesced), balance, return.
-  const int total = nloc * K;
-  const float* src = a.actions + e0 * K;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  const int total4 = vec_ok ? total / 4 : 0;
-  constexpr int kVec = (kEnvBlock * KMAX / 4 + kEnvBlock - 1) / kEnvBlock;  // float4 per thread (K <= KMAX)
-  float4 av[kVec];
-#pragma unroll
-  for (int j = 0; j < kVec; ++j) {
-    const int idx = tid + j * kEnvBlock;
-    if (idx < total4) av[j] = __ldg(reinterpret_cast<const float4*>(src) + idx);
-  }
-  int32_t shv[KMAX];
-  const bool live = tid < nloc;
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k)
-    if (k < K && live) shv[k] = __ldg(a.shares + (size_t)k * a.N + e0 + tid);
-  const double bal_in = live ? a.balance[e0 + tid] : 0.0;
-  const double ret_in = live ? a.ep_return[e0 + tid] : 0.0;
-#pragma unroll
-  for (int j = 0; j < kVec; ++j) {
-    const int idx = tid + j * kEnvBlock;
-    if (idx < total4) {
-      const float v4[4] = {av[j].x, av[j].y, av[j].z, av[j].w};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int f = idx * 4 + c, r = f / K;
-        s_act[r * Kp + (f - r * K)] = v4[c];
-      }
-    }
-  }
-  for (int f = total4 * 4 + tid; f < total; f += kEnvBlock) {  // tail / unaligned fallback
-    const int r = f / K;
-    s_act[r * Kp + (f - r * K)] = src[f];
-  }
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k)
-    if (k < K && live) s_sh[k * kEnvBlock + tid] = shv[k];
-  __syncthreads();
-
-  if (tid < nloc) {
-    const size_t e = e0 + tid;
-    double bal = bal_in;
-    // value_before (PortfolioState::account_value stock_env.hpp:27-31)
-    double vb = bal;
-    for (int k = 0; k < K; ++k) vb = __dadd_rn(vb, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p0[k]));
-    // desired = trunc(clamp(a) * max_trade_shares)  (:83-87; the VecEnv clip env.hpp:213-215 is idempotent)
-    const float* act = s_act + tid * Kp;
-    // sells first (:88-90)
-    for (int k = 0; k < K; ++k) {
-      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
-      if (d < 0.0) {
-        const int32_t held = s_sh[k * kEnvBlock + tid];
-        const double q = -min_ref(-d, (double)held);
-        const double price = s_p0[k];
-        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
-        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
-        s_sh[k * kEnvBlock + tid] = held + (int32_t)q;
-      }
-    }
-    // then buys, each clipped to the affordable balance incl. cost (:91-97)
-    const double cost_factor = __dadd_rn(1.0, a.cost);
-    for (int k = 0; k < K; ++k) {
-      const double d = trunc(__dmul_rn(clamp_ref((double)act[k], -1.0, 1.0), a.max_trade));
-      if (d > 0.0) {
-        const double price = s_p0[k];
-        const double q = stock::buy_qty(d, bal, __dmul_rn(price, cost_factor));
-        const double cost = __dmul_rn(__dmul_rn(a.cost, fabs(q)), price);
-        bal = __dsub_rn(bal, __dadd_rn(__dmul_rn(q, price), cost));
-        s_sh[k * kEnvBlock + tid] += (int32_t)q;
-      }
-    }
-    // t+1, reward = value_after - value_before (:99-100)
-    double va = bal;
-    for (int k = 0; k < K; ++k) va = __dadd_rn(va, __dmul_rn((double)s_sh[k * kEnvBlock + tid], s_p1[k]));
-    const double r = __dsub_rn(va, vb);
-    const double ret = __dadd_rn(ret_in, r);  // env.hpp:218
-    if (a.reward) a.reward[e] = (float)r;
-    if (a.done_out) a.done_out[e] = (uint8_t)a.done;
-    float* priv = s_priv + tid * Kp;
-    priv[0] = (float)__ddiv_rn(bal, a.cap);
-    for (int k = 0; k < K; ++k) priv[1 + k] = (float)s_sh[k * kEnvBlock + tid];
-    if (a.done) {  // env.hpp:221-229: report the terminal episode, auto-reset (stock_env.hpp:158-163)
-      if (a.term_ret) a.term_ret[e] = ret;
-      if (a.term_len) a.term_len[e] = a.ep_len;
-      a.balance[e] = a.cap;
-      a.ep_return[e] = 0.0;
-    } else {
-      a.balance[e] = bal;
-      a.ep_return[e] = ret;
-    }
-  }
-  __syncthreads();
-  const int S = a.S;
-  if (a.done) {
-    if (a.term_obs) write_obs_rows(a.term_obs + e0 * S, nloc, S, K + 1, s_priv, Kp, s_feat_term);
-    __syncthreads();
-    for (int i = tid; i < nloc * Kp; i += blockDim.x) s_priv[i] = ((i % Kp) == 0) ? (float)(a.cap / a.cap) : 0.0f;
-    if (tid < nloc)
-      for (int k = 0; k < K; ++k) s_sh[k * kEnvBlock + tid] = 0;
-    __syncthreads();
-  }
-  if (tid < nloc)
-    for (int k = 0; k < K; ++k) a.shares[(size_t)k * a.N + e0 + tid] = s_sh[k * kEnvBlock + tid];
-  write_obs_rows(a.obs + e0 * S, nloc, S, K + 1, s_priv, Kp, s_feat_obs);
-}
-
 // ---- v2: asynchronous staging (cp.async) and no private-obs copy -----------
 // Every load of the CTA is an LDGSTS issued up front (no registers held, all
 // bytes in flight at once); the obs writer reads the portfolio straight from
@@ -664,11 +481,6 @@ __global__ void pm_reset_kernel(int N, uint64_t seed, uint64_t tag, double* st, 
   }
 }
 
-size_t stock_smem_bytes(int K) {
-  const int Kp = K + 1;
-  return 2 * K * sizeof(double) + (size_t)kEnvBlock * Kp * sizeof(float) * 2 + (size_t)K * kEnvBlock * sizeof(int32_t) +
-         (size_t)10 * K * sizeof(float);
-}
 
 void check_env(prb_vecenv env) { PRB_REQUIRE(env, PRB_ERR_USAGE, "vecenv handle is NULL"); }
 
@@ -704,38 +516,19 @@ void prb_stock_step_launch(prb_vecenv env, const float* d_actions, float* d_rewa
   a.term_obs = d_term_obs;
   a.term_ret = d_term_ret;
   a.term_len = d_term_len;
-  static bool attr_set = false;
-  if (!attr_set) {
-    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PRB_CUDA(cudaFuncSetAttribute(stock_step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PRB_CUDA(cudaFuncSetAttribute(stock_step_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
-  const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
   {
     ProfScope prof(env->ctx, kProfEnvStock);
-    if (env->step_kernel == 2 && m->K <= 32 && (m->K & 1) == 0 && env->cfg.max_trade_shares < 16777216.0) {
+    if (m->K <= 32 && (m->K & 1) == 0 && env->cfg.max_trade_shares < 16777216.0) {
       // 256 envs per CTA: measured 72.2% of HBM peak at 1M envs vs 70.9% (128), 68.6% (64),
-      // 61.7% (512); PRB_ENV_EB=64|128 keeps the smaller tiles selectable for A/B runs
-      static const int eb = [] {
-        const char* v = getenv("PRB_ENV_EB");
-        return v ? atoi(v) : 256;
-      }();
-      const int gN = (int)((env->N + eb - 1) / eb);
-      if (eb == 64)
-        stock_step_v3_kernel<32, 64><<<gN, 64, stock_v3_smem_bytes(m->K, 64), env->ctx->stream>>>(a);
-      else if (eb == 128)
-        stock_step_v3_kernel<32, 128><<<gN, 128, stock_v3_smem_bytes(m->K, 128), env->ctx->stream>>>(a);
-      else
-        stock_step_v3_kernel<32, 256><<<gN, 256, stock_v3_smem_bytes(m->K, 256), env->ctx->stream>>>(a);
-    } else if (env->step_kernel == 2) {
-      stock_step_v2_kernel<<<grid, kEnvBlock, stock_v2_smem_bytes(m->K), env->ctx->stream>>>(a);
-    } else {
-      const size_t smem = stock_smem_bytes(m->K);
-      if (m->K <= 32)
-        stock_step_kernel<32><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
-      else
-        stock_step_kernel<64><<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
+      // 61.7% (512)
+      constexpr int kEb = 256;
+      const int gN = (int)((env->N + kEb - 1) / kEb);
+      stock_step_v3_kernel<32, kEb><<<gN, kEb, stock_v3_smem_bytes(m->K, kEb), env->ctx->stream>>>(a);
+    } else {  // odd K, K > 32 or share quantities beyond fp32's exact integers
+      const size_t smem = stock_v2_smem_bytes(m->K);
+      ensure_smem(stock_step_v2_kernel, smem);
+      const int grid = (int)((env->N + kEnvBlock - 1) / kEnvBlock);
+      stock_step_v2_kernel<<<grid, kEnvBlock, smem, env->ctx->stream>>>(a);
     }
   }
   PRB_CHECK_LAUNCH();
@@ -781,6 +574,7 @@ extern "C" {
 int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t start, size_t end, size_t N,
                             prb_vecenv* out) {
   return guard([&] {
+    DeviceScope dev_(m ? m->ctx : nullptr);
     PRB_REQUIRE(m && cfg && out, PRB_ERR_USAGE, "prb_vecenv_create_stock: NULL argument");
     PRB_REQUIRE(N > 0, PRB_ERR_CONFIG, "VectorizedEnvironment: num_envs must be > 0");           // env.hpp:170
     PRB_REQUIRE(!m->indicators.empty(), PRB_ERR_USAGE,
@@ -834,6 +628,7 @@ int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t st
 
 int prb_vecenv_create_pointmass(prb_ctx ctx, size_t N, prb_vecenv* out) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_vecenv_create_pointmass: NULL argument");
     PRB_REQUIRE(N > 0, PRB_ERR_CONFIG, "VectorizedEnvironment: num_envs must be > 0");
     PRB_REQUIRE(N < (size_t)1 << 31, PRB_ERR_CONFIG, "prb: num_envs must be < 2^31");
@@ -862,6 +657,7 @@ int prb_vecenv_create_pointmass(prb_ctx ctx, size_t N, prb_vecenv* out) {
 
 int prb_vecenv_destroy(prb_vecenv env) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     if (env) cudaStreamSynchronize(env->ctx->stream);
     delete env;
   });
@@ -869,6 +665,7 @@ int prb_vecenv_destroy(prb_vecenv env) {
 
 int prb_vecenv_spec(prb_vecenv env, prb_env_spec* out) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     out->state_dim = env->S;
     out->action_dim = env->A;
@@ -906,6 +703,7 @@ void prb_vecenv_reset_tagged(prb_vecenv env, uint64_t seed, uint64_t tag) {
 
 int prb_vecenv_reset(prb_vecenv env, uint64_t seed, float* d_obs) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     cudaStream_t s = env->ctx->stream;
     prb_vecenv_reset_tagged(env, seed, 1);
@@ -917,6 +715,7 @@ int prb_vecenv_reset(prb_vecenv env, uint64_t seed, float* d_obs) {
 int prb_vecenv_step(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_terminal_obs,
                     double* d_episode_return, int32_t* d_episode_length) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     PRB_REQUIRE(d_actions, PRB_ERR_USAGE, "vec_step: actions is NULL");
     prb_env_step_launch(env, d_actions, d_reward, d_done, d_terminal_obs, d_episode_return, d_episode_length);
@@ -931,6 +730,7 @@ int prb_vecenv_reset_host(prb_vecenv env, uint64_t seed, double* states) {
 
 int prb_vecenv_states_host(prb_vecenv env, double* states) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     const size_t n = env->N * env->S;
     float* h = static_cast<float*>(env->ctx->pinned_staging(n * sizeof(float)));
@@ -943,6 +743,7 @@ int prb_vecenv_states_host(prb_vecenv env, double* states) {
 int prb_vecenv_step_host(prb_vecenv env, const double* actions, double* next_states, double* rewards, uint8_t* dones,
                          double* terminal_states, double* episode_returns, uint64_t* episode_lengths) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     PRB_REQUIRE(actions, PRB_ERR_USAGE, "vec_step: actions is NULL");
     const size_t N = env->N, S = env->S, A = env->A;
@@ -998,6 +799,7 @@ int prb_vecenv_step_host(prb_vecenv env, const double* actions, double* next_sta
 
 int prb_vecenv_step_counts_host(prb_vecenv env, uint64_t* out) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     check_env(env);
     if (env->kind == PRB_KIND_STOCK) {
       for (size_t i = 0; i < env->N; ++i) out[i] = env->step_count;

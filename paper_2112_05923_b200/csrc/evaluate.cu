@@ -41,6 +41,7 @@ extern "C" {
 int prb_evaluate(prb_agent a, prb_vecenv env, uint64_t seed, int sample_actions, double* episodic_rewards,
                  double* mean, double* std_dev, uint64_t* eval_steps) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && env && episodic_rewards, PRB_ERR_USAGE, "evaluate: NULL argument");
     PRB_REQUIRE(env->N >= 1, PRB_ERR_USAGE, "evaluate: episodes must be >= 1");
     PRB_REQUIRE(a->S == env->S && a->A == env->A, PRB_ERR_DIMENSION, "evaluate: agent/env shapes disagree");

@@ -165,6 +165,7 @@ int prb_compute_gae(prb_ctx ctx, const float* d_rewards, const float* d_values, 
                     const float* d_bootstrap, size_t N, size_t H, double gamma, double lambda, float* d_adv,
                     float* d_ret) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && d_rewards && d_values && d_dones && d_bootstrap && d_adv && d_ret, PRB_ERR_USAGE,
                 "compute_gae: NULL argument");
     PRB_REQUIRE(N > 0 && H > 0, PRB_ERR_DIMENSION, "compute_gae: empty trajectory");  // ppo.hpp:54-57
@@ -174,6 +175,7 @@ int prb_compute_gae(prb_ctx ctx, const float* d_rewards, const float* d_values, 
 
 int prb_gae(prb_rollout r, double gamma, double lambda, int normalize) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r, PRB_ERR_USAGE, "buffer_advantages: NULL rollout");
     PRB_REQUIRE(r->full, PRB_ERR_USAGE,
                 "buffer_advantages: chunks cover 0 of " + std::to_string(r->N * r->H) + " transitions");
@@ -186,6 +188,7 @@ int prb_gae(prb_rollout r, double gamma, double lambda, int normalize) {
 
 int prb_gae_download(prb_rollout r, double* advantages, double* returns) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r && r->gae_valid, PRB_ERR_USAGE, "prb_gae_download: call prb_gae first");
     const size_t N = r->N, H = r->H, n = N * H;
     std::vector<float> a(n), t(n);
@@ -206,6 +209,7 @@ int prb_gae_download(prb_rollout r, double* advantages, double* returns) {
 
 int prb_rollout_set_advantages(prb_rollout r, const double* advantages, const double* returns) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r && advantages && returns, PRB_ERR_USAGE, "prb_rollout_set_advantages: NULL argument");
     const size_t N = r->N, H = r->H, n = N * H;
     std::vector<float> a(n), t(n);

@@ -165,11 +165,7 @@ void prb_policy_launch(const PolicyArgs& p, prb_ctx_s* ctx) {
   if (p.n == 0) return;
   const size_t smem = prb_policy_smem(p);
   PRB_REQUIRE(smem <= 220 * 1024, PRB_ERR_CONFIG, "policy: tile does not fit in shared memory");
-  static bool attr = false;
-  if (!attr) {
-    PRB_CUDA(cudaFuncSetAttribute(policy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
-  }
+  ensure_smem(policy_kernel, 220 * 1024);
   const size_t grid = (p.n + p.rows_per_cta - 1) / p.rows_per_cta;
   policy_kernel<<<(unsigned)grid, 256, smem, s>>>(p);
   PRB_CHECK_LAUNCH();
@@ -191,6 +187,7 @@ extern "C" {
 int prb_policy_sample(prb_agent a, const float* d_states, size_t n, uint64_t seed, uint64_t counter, float* d_actions,
                       float* d_log_probs, float* d_values, float* d_eps) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_states && d_actions && d_log_probs, PRB_ERR_USAGE, "policy_sample: NULL argument");
     PolicyArgs p = prb_policy_args(a, d_states, n);
     p.mode = kPolicySample;
@@ -208,6 +205,7 @@ int prb_policy_sample(prb_agent a, const float* d_states, size_t n, uint64_t see
 int prb_policy_sample_eps(prb_agent a, const float* d_states, size_t n, const float* d_eps, float* d_actions,
                           float* d_log_probs, float* d_values) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_states && d_eps && d_actions && d_log_probs, PRB_ERR_USAGE, "policy_sample: NULL argument");
     PolicyArgs p = prb_policy_args(a, d_states, n);
     p.mode = kPolicyEpsIn;
@@ -222,6 +220,7 @@ int prb_policy_sample_eps(prb_agent a, const float* d_states, size_t n, const fl
 
 int prb_policy_mean(prb_agent a, const float* d_states, size_t n, float* d_mean) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_states && d_mean, PRB_ERR_USAGE, "policy_mean: NULL argument");
     PolicyArgs p = prb_policy_args(a, d_states, n);
     p.mode = kPolicyMean;
@@ -234,6 +233,7 @@ int prb_policy_mean(prb_agent a, const float* d_states, size_t n, float* d_mean)
 
 int prb_policy_log_prob(prb_agent a, const float* d_states, const float* d_actions, size_t n, float* d_lp) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_states && d_actions && d_lp, PRB_ERR_USAGE, "gaussian_log_prob: NULL argument");
     PolicyArgs p = prb_policy_args(a, d_states, n);
     p.mode = kPolicyLogProb;
@@ -247,6 +247,7 @@ int prb_policy_log_prob(prb_agent a, const float* d_states, const float* d_actio
 
 int prb_critic_value(prb_agent a, const float* d_states, size_t n, float* d_values) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && d_states && d_values, PRB_ERR_USAGE, "critic: NULL argument");
     PolicyArgs p = prb_policy_args(a, d_states, n);
     p.mode = kPolicyValueOnly;

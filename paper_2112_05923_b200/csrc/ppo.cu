@@ -1368,11 +1368,11 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   // rows per CTA: as many CTAs as possible while every CTA keeps >= 8 rows
   p.R = 8;
   while (p.R < 64 && (size_t)(mb / (p.R * 2)) >= (size_t)a->ctx->num_sms) p.R *= 2;
-  if (const char* rv = getenv("PRB_PPO_R")) p.R = std::max(8, std::min(64, atoi(rv)));  // A/B knob
+  if (const char* rv = debug_env("PRB_PPO_R")) p.R = std::max(8, std::min(64, atoi(rv)));  // A/B knob
   p.stage = 1;
   p.r8 = 0;
   {  // rows-of-8 path: 8-row blocks, every layer output <= 64 wide, A <= 32
-    bool ok = (p.R == 8) && p.A <= 32 && !(getenv("PRB_PPO_R8") && atoi(getenv("PRB_PPO_R8")) == 0);
+    bool ok = (p.R == 8) && p.A <= 32 && !(debug_env("PRB_PPO_R8") && atoi(debug_env("PRB_PPO_R8")) == 0);
     for (int l = 0; l < p.actor.nl; ++l) ok = ok && p.actor.dims[l + 1] <= 64;
     for (int l = 0; l < p.critic.nl; ++l) ok = ok && p.critic.dims[l + 1] <= 64;
     if (ok) {
@@ -1422,7 +1422,7 @@ PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_
   PRB_CUDA(cudaMemcpyAsync(ws.tiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice,
                            a->ctx->stream));
   ws.tickets.ensure(2);  // [0] completed-CTA counter of ppo_sum, [1] gradient non-finite flag
-  if (getenv("PRB_PPO_TRACE")) {
+  if (debug_env("PRB_PPO_TRACE")) {
     ws.trace.alloc((size_t)ws.ntiles * ws.RS * 8 + 32);
     PRB_CUDA(cudaMemsetAsync(ws.trace.p, 0, ws.trace.bytes(), a->ctx->stream));
   }
@@ -1490,11 +1490,9 @@ void launch_step(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double ent, in
     ppo_fwd_delta_kernel<0><<<grid, kPpoThreads, smem, s>>>(pt);
   GradArgs g = make_grad_args(p, a, ws, ent, apply);
   ppo_grad_kernel<<<ws.ntiles * ws.RS, 256, 2 * kGChunk * kGLd * sizeof(float), s>>>(g);
-  static int occ = 0;
-  if (!occ) {
-    PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_sum_adam_kernel, 256, 0));
-    occ = std::max(occ, 1);
-  }
+  int occ = 0;
+  PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_sum_adam_kernel, 256, 0));
+  occ = std::max(occ, 1);
   const int sgrid = std::min((p.P + 255) / 256, a->ctx->num_sms * occ);
   // cooperative: every CTA resident (the CTAs wait for the last one's gate)
   void* args[] = {&g};
@@ -1507,7 +1505,7 @@ size_t persistent_smem(const PpoArgs& p) {
 
 // Grid of the persistent update (0: not launchable -> per-kernel path).
 int persistent_grid(const PpoArgs& p, prb_agent a, const PpoWorkspace& ws) {
-  if (p.A > 256 || getenv("PRB_PPO_GRAPH")) return 0;  // PRB_PPO_GRAPH: force the per-kernel path (A/B)
+  if (p.A > 256 || debug_option(PRB_OPT_PPO_PER_KERNEL)) return 0;  // tests: force the per-kernel path
   const size_t smem = persistent_smem(p);
   int occ = 0;
   const void* fn = p.r8 ? (const void*)ppo_persistent_kernel<2>
@@ -1529,7 +1527,7 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   unsigned int* bar = reinterpret_cast<unsigned int*>(ws.bar.p);
   int32_t* flags = ws.bar.p + 2;
   unsigned long long* trace = nullptr;
-  if (getenv("PRB_PPO_TRACE")) {  // [grid][10] phase stamps, then fwd_delta_block's 2 x 16 clock64 marks
+  if (debug_env("PRB_PPO_TRACE")) {  // [grid][10] phase stamps, then fwd_delta_block's 2 x 16 clock64 marks
     ws.ptrace.alloc((size_t)grid * 16 + 32);
     PRB_CUDA(cudaMemsetAsync(ws.ptrace.p, 0, ws.ptrace.bytes(), s));
     trace = ws.ptrace.p;
@@ -1537,15 +1535,15 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
   }
   ws.bias.ensure((size_t)steps);
   float2* bias_tab = ws.bias.p;
-  pa.nospec = getenv("PRB_PPO_NOSPEC") ? 1 : 0;
-  if (p.r8 && p.stage && !getenv("PRB_PPO_CPASYNC")) {  // PRB_PPO_CPASYNC=1: per-thread cp.async staging (A/B)
+  pa.nospec = debug_env("PRB_PPO_NOSPEC") ? 1 : 0;
+  if (p.r8 && p.stage && !debug_env("PRB_PPO_CPASYNC")) {  // PRB_PPO_CPASYNC=1: per-thread cp.async staging (A/B)
     pa.img_c = (int)staged_floats(p.actor, 1);
     const size_t nimg = (size_t)pa.img_c + staged_floats(p.critic, 1);
     ws.wimg.ensure(nimg);
     PRB_CUDA(cudaMemsetAsync(ws.wimg.p, 0, nimg * sizeof(float), s));  // row padding
     pa.wimg = ws.wimg.p;
   }
-  if (p.r8 && !getenv("PRB_PPO_NOTAB")) {  // PRB_PPO_NOTAB=1: rows resolved inline (A/B)
+  if (p.r8 && !debug_env("PRB_PPO_NOTAB")) {  // PRB_PPO_NOTAB=1: rows resolved inline (A/B)
     ws.rtab.ensure(2 * (size_t)p.mb);
     pa.rtab = ws.rtab.p;
   }
@@ -1576,18 +1574,12 @@ void check_status(prb_agent a) {
   }
 }
 
-void set_smem_attr() {
-  static bool done = false;
-  if (!done) {
-    const void* fns[] = {(const void*)ppo_fwd_delta_kernel<0>, (const void*)ppo_fwd_delta_kernel<1>,
-                         (const void*)ppo_fwd_delta_kernel<2>, (const void*)ppo_persistent_kernel<0>,
-                         (const void*)ppo_persistent_kernel<1>, (const void*)ppo_persistent_kernel<2>};
-    for (const void* f : fns)
-      PRB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-    PRB_CUDA(cudaFuncSetAttribute(ppo_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(2 * kGChunk * kGLd * sizeof(float))));
-    done = true;
-  }
+void set_smem_attr() {  // per device (ensure_smem_attr); the caller's DeviceScope made it current
+  const void* fns[] = {(const void*)ppo_fwd_delta_kernel<0>, (const void*)ppo_fwd_delta_kernel<1>,
+                       (const void*)ppo_fwd_delta_kernel<2>, (const void*)ppo_persistent_kernel<0>,
+                       (const void*)ppo_persistent_kernel<1>, (const void*)ppo_persistent_kernel<2>};
+  for (const void* f : fns) ensure_smem_attr(f, kSmemBudget);
+  ensure_smem_attr((const void*)ppo_grad_kernel, 2 * kGChunk * kGLd * sizeof(float));
 }
 
 std::vector<uint32_t> ref_rows_to_device(prb_rollout r, const uint64_t* rows, size_t count) {
@@ -1611,6 +1603,7 @@ extern "C" {
 int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, const uint64_t* perm,
                    prb_agent dst, prb_ppo_stats* stats) {
   return guard([&] {
+    DeviceScope dev_(src ? src->ctx : nullptr);
     PRB_REQUIRE(src && r && cfg && dst, PRB_ERR_USAGE, "ppo_update: NULL argument");
     // PpoConfig::validate ppo.hpp:29-37
     PRB_REQUIRE(cfg->gamma > 0.0 && cfg->gamma <= 1.0, PRB_ERR_CONFIG, "ppo.gamma must be in (0, 1]");
@@ -1628,10 +1621,23 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     PRB_REQUIRE(cfg->minibatch_size < (1u << 30), PRB_ERR_CONFIG, "ppo.minibatch_size too large");
     set_smem_attr();
     cudaStream_t s = dst->ctx->stream;
+    // ppo_update is pure w.r.t. its inputs (ppo.hpp:246-248): with src == dst the agent is
+    // snapshotted first and restored if the update fails, so a NumericError leaves it intact
+    DevBuf<float> snap;
+    int64_t snap_t = 0;
+    const double snap_lr = dst->lr;
     if (src != dst) {
       int rc = prb_agent_copy(dst, src);
       if (rc) fail(rc, prb_last_error());
+    } else {
+      snap.alloc(3 * dst->P);
+      PRB_CUDA(cudaMemcpyAsync(snap.p, dst->d_params.p, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      PRB_CUDA(cudaMemcpyAsync(snap.p + dst->P, dst->d_m.p, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      PRB_CUDA(cudaMemcpyAsync(snap.p + 2 * dst->P, dst->d_v.p, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      PRB_CUDA(cudaMemcpyAsync(&snap_t, dst->d_t.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      dst->ctx->sync();
     }
+    try {
     dst->lr = cfg->learning_rate;  // ppo.hpp:265
     PRB_CUDA(cudaMemsetAsync(dst->d_status.p, 0, 4 * sizeof(int32_t), s));
     prb_gae_launch(r->ctx, r->d_rew.p, r->d_val.p, r->d_done.p, r->d_boot.p, r->N, r->H, cfg->gamma, cfg->gae_lambda,
@@ -1677,7 +1683,7 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
       for (size_t i = 0; i < steps; ++i) launch_step(p, dst, ws, cfg->entropy_coef, 1, s);
     }
     PRB_CHECK_LAUNCH();
-    if (const char* tp = getenv("PRB_PPO_TRACE")) {  // debug: globaltimer marks of the last step's ppo_grad CTAs
+    if (const char* tp = debug_env("PRB_PPO_TRACE")) {  // debug: globaltimer marks of the last step's ppo_grad CTAs
       DevBuf<unsigned long long>& tb = ws.ptrace.p ? ws.ptrace : ws.trace;  // persistent: [grid][10] stamps
       std::vector<unsigned long long> h(tb.n);
       PRB_CUDA(cudaMemcpy(h.data(), tb.p, tb.bytes(), cudaMemcpyDeviceToHost));
@@ -1697,12 +1703,25 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
       stats->mean_value_loss = st[1] * inv;
       stats->mean_entropy = st[2] * inv;
     }
+    } catch (...) {
+      if (snap.p) {  // src == dst: put the input back
+        cudaStreamSynchronize(s);
+        cudaMemcpyAsync(dst->d_params.p, snap.p, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(dst->d_m.p, snap.p + dst->P, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(dst->d_v.p, snap.p + 2 * dst->P, dst->P * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(dst->d_t.p, &snap_t, sizeof(int64_t), cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);
+        dst->lr = snap_lr;
+      }
+      throw;
+    }
   });
 }
 
 int prb_ppo_loss_grads(prb_agent a, prb_rollout r, const uint64_t* rows, size_t n, const prb_ppo_config* cfg,
                        double* grads, double* losses) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(a && r && rows && cfg, PRB_ERR_USAGE, "ppo_loss_grads: NULL argument");
     PRB_REQUIRE(r->gae_valid, PRB_ERR_USAGE, "ppo_loss_grads: call prb_gae first");
     PRB_REQUIRE(n > 0 && n < (1u << 30), PRB_ERR_DIMENSION, "ppo_loss_grads: bad minibatch size");

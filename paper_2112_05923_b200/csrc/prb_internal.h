@@ -82,6 +82,23 @@ struct DevBuf {
   }
 };
 
+// Per-device opt-in to more than 48 KB of dynamic shared memory.  The
+// attribute belongs to the device context, so it is set once per (kernel,
+// device) -- a process driving several GPUs (one host thread per pod, the
+// reference's threading model) opts in on each of them;
+// thread-safe.  Call with the launching device current.
+void ensure_smem_attr(const void* kernel, size_t smem_bytes);
+template <typename K>
+inline void ensure_smem(K* kernel, size_t smem_bytes) {
+  ensure_smem_attr(reinterpret_cast<const void*>(kernel), smem_bytes);
+}
+
+// Test-only switches (prb_debug_set_option, PRB_OPT_* in prb.h); 0 unless a test set them.
+int debug_option(int option);
+// Developer tracing / A-B knobs: read from the environment only in a build with
+// -DPRB_DEBUG_KNOBS (make NVFLAGS_EXTRA=-DPRB_DEBUG_KNOBS); nullptr otherwise.
+const char* debug_env(const char* name);
+
 uint64_t splitmix64(uint64_t x);
 uint64_t derive_seed(uint64_t base, std::initializer_list<uint64_t> tags);
 
@@ -114,6 +131,26 @@ struct prb_ctx_s {
   double prof_ms[16] = {0};
   uint64_t prof_n[16] = {0};
   cudaEvent_t take_event();
+};
+
+// Makes the context's device current for the duration of an entry point and
+// restores the caller's device afterwards (every launching prb_* entry opens
+// one, so two contexts on two GPUs can be driven from one host thread).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const prb_ctx_s* c) {
+    if (!c) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device) {
+      PRB_CUDA(cudaSetDevice(c->device));
+      prev = cur;
+    }
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
 };
 
 // Kernel classes reported by prb_ctx_profile_read (index == PRB_PROF_* in prb.h).
@@ -164,7 +201,6 @@ struct prb_vecenv_s {
   prb_market_s* market = nullptr;
   prb_stock_config cfg{};
   size_t start = 0, end = 0;
-  int step_kernel = 2;     // 2: cp.async staging (default), 1: register staging (kept for A/B)
   size_t t = 0;            // uniform portfolio time index (stock_env.hpp:161)
   uint64_t step_count = 0; // uniform VecEnv step counter (env.hpp:217)
   prb::DevBuf<float> d_feat;       // [T][5K] shared obs features for this window

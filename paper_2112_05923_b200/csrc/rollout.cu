@@ -78,7 +78,7 @@ static void pm_tc_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t s
   t.b_rew = r->d_rew.p;
   t.b_done = r->d_done.p;
   t.b_boot = r->d_boot.p;
-  const char* trace_path = getenv("PRB_PM_TRACE");  // debug: clock64 phase trace of CTA 0
+  const char* trace_path = debug_env("PRB_PM_TRACE");  // debug: clock64 phase trace of CTA 0
   prb::DevBuf<unsigned long long> d_trace;
   if (trace_path) {
     d_trace.alloc(4 * kPmTraceLen);
@@ -105,6 +105,7 @@ extern "C" {
 
 int prb_rollout_create(prb_vecenv env, size_t horizon, prb_rollout* out) {
   return guard([&] {
+    DeviceScope dev_(env ? env->ctx : nullptr);
     PRB_REQUIRE(env && out, PRB_ERR_USAGE, "prb_rollout_create: NULL argument");
     PRB_REQUIRE(horizon > 0, PRB_ERR_CONFIG, "pod.rollout_horizon must be > 0");
     PRB_REQUIRE(env->N * horizon < ((size_t)1 << 32), PRB_ERR_CONFIG, "prb_rollout_create: N*H must be < 2^32");
@@ -130,6 +131,7 @@ int prb_rollout_create(prb_vecenv env, size_t horizon, prb_rollout* out) {
 
 int prb_rollout_create_raw(prb_ctx ctx, size_t N, size_t H, size_t S, size_t A, prb_rollout* out) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && out, PRB_ERR_USAGE, "prb_rollout_create_raw: NULL argument");
     PRB_REQUIRE(N > 0 && H > 0 && S > 0 && A > 0, PRB_ERR_CONFIG, "prb_rollout_create_raw: zero dimension");
     PRB_REQUIRE(N * H < ((size_t)1 << 32), PRB_ERR_CONFIG, "prb_rollout_create_raw: N*H must be < 2^32");
@@ -148,6 +150,7 @@ int prb_rollout_create_raw(prb_ctx ctx, size_t N, size_t H, size_t S, size_t A, 
 
 int prb_rollout_destroy(prb_rollout r) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     if (r) cudaStreamSynchronize(r->ctx->stream);
     delete r;
   });
@@ -155,6 +158,7 @@ int prb_rollout_destroy(prb_rollout r) {
 
 int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t seed) {
   return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
     PRB_REQUIRE(r && a && env, PRB_ERR_USAGE, "worker_collect: NULL argument");
     PRB_REQUIRE(env->N == r->N && env->S == r->S && env->A == r->A && a->S == env->S && a->A == env->A,
                 PRB_ERR_USAGE, "worker_collect: rollout/agent/env shapes disagree");
@@ -217,6 +221,7 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
 
 int prb_rollout_set_mode(prb_rollout r, int mode) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_set_mode: NULL rollout");
     PRB_REQUIRE(mode >= 0 && mode <= 2, PRB_ERR_CONFIG, "prb_rollout_set_mode: mode must be 0, 1 or 2");
     r->mode = mode;
@@ -226,6 +231,7 @@ int prb_rollout_set_mode(prb_rollout r, int mode) {
 int prb_rollout_device_fields(prb_rollout r, float** d_obs, float** d_actions, float** d_log_probs, float** d_rewards,
                               float** d_values, uint8_t** d_dones, float** d_bootstrap) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_device_fields: NULL rollout");
     if (d_obs) *d_obs = r->d_obs.p;
     if (d_actions) *d_actions = r->d_act.p;
@@ -240,6 +246,7 @@ int prb_rollout_device_fields(prb_rollout r, float** d_obs, float** d_actions, f
 int prb_rollout_download(prb_rollout r, double* states, double* actions, double* log_probs, double* rewards,
                          uint8_t* dones, double* values, double* bootstrap) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r, PRB_ERR_USAGE, "prb_rollout_download: NULL rollout");
     const size_t N = r->N, H = r->H, n = N * H, S = r->S, A = r->A, Sp = r->Sp;
     cudaStream_t s = r->ctx->stream;
@@ -289,6 +296,7 @@ int prb_rollout_download(prb_rollout r, double* states, double* actions, double*
 int prb_rollout_upload(prb_rollout r, const double* states, const double* actions, const double* log_probs,
                        const double* rewards, const uint8_t* dones, const double* values, const double* bootstrap) {
   return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
     PRB_REQUIRE(r && states && actions && log_probs && rewards && dones && values && bootstrap, PRB_ERR_USAGE,
                 "prb_rollout_upload: NULL argument");
     const size_t N = r->N, H = r->H, n = N * H, S = r->S, A = r->A;

@@ -433,7 +433,13 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
     f.b_rew = r->d_rew.p;
     f.b_done = r->d_done.p;
     f.b_boot = r->d_boot.p;
-    if (r->mode == 2 && stock_rollout_tc_supported(K) && env->cfg.max_trade_shares < 2147483648.0) {  // tcgen05 bf16 MLP (rollout_tc.cu)
+    // tcgen05 bf16 MLP (rollout_tc.cu).  Its rare exact-division redo rebuilds the step's start
+    // shares from the fp32 compact obs row, so every reachable share count must be an exact
+    // float: at most max_trade_shares bought per step for at most end - start steps of an
+    // episode (stock_env.hpp:91-97, :165-170) must stay below 2^24.
+    const bool shares_exact_f32 =
+        env->cfg.max_trade_shares * (double)(env->end - env->start + 1) < 16777216.0;
+    if (r->mode == 2 && stock_rollout_tc_supported(K) && shares_exact_f32) {
       TcRolloutArgs ta{};
       ta.params = f.params;
       ta.a_w1 = f.a_w1; ta.a_w2 = f.a_w2; ta.a_w3 = f.a_w3;
@@ -444,15 +450,12 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
       ta.close_tk = f.close_tk; ta.feat = f.feat;
       ta.cap = f.cap; ta.max_trade = f.max_trade; ta.cost = f.cost;
       ta.mt_f32 = (f.max_trade == floor(f.max_trade) && f.max_trade >= 0.0 && f.max_trade < 4194304.0) ? 1 : 0;
-      {
-        const char* fr = getenv("PRB_TC_FORCE_REDO");  // tests: exercise the rare redo path every step
-        ta.force_redo = (fr && fr[0] == '1') ? 1 : 0;
-      }
+      ta.force_redo = debug_option(PRB_OPT_TC_FORCE_REDO) ? 1 : 0;  // tests: the rare redo path every step
       ta.N = f.N; ta.H = f.H; ta.seed = f.seed;
       ta.balance = f.balance; ta.shares = f.shares; ta.ep_return = f.ep_return; ta.obs_out = f.obs_out;
       ta.b_obs = f.b_obs; ta.b_act = f.b_act; ta.b_logp = f.b_logp; ta.b_val = f.b_val; ta.b_rew = f.b_rew;
       ta.b_done = f.b_done; ta.b_boot = f.b_boot;
-      const char* trace_path = getenv("PRB_TC_TRACE");  // debug: clock64 phase trace of CTA 0
+      const char* trace_path = debug_env("PRB_TC_TRACE");  // debug: clock64 phase trace of CTA 0
       DevBuf<unsigned long long> d_trace;
       if (trace_path) {
         d_trace.alloc(kTcTraceLen);
@@ -470,12 +473,7 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
         }
       }
     } else {  // fp32 SIMT MLP
-      static bool attr = false;
-      if (!attr) {
-        PRB_CUDA(cudaFuncSetAttribute(stock_rollout_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(Smem)));
-        attr = true;
-      }
+      ensure_smem(stock_rollout_fused_kernel, sizeof(Smem));
       const unsigned grid = (unsigned)((N + kRows - 1) / kRows);
       stock_rollout_fused_kernel<<<grid, kThreads, sizeof(Smem), s>>>(f);
       PRB_CHECK_LAUNCH();

@@ -517,14 +517,13 @@ void encode_pm_pack_map(CUtensorMap* map, const uint8_t* pack) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static Fn fn = nullptr;
-  if (!fn) {
+  static const Fn fn = [] {  // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     PRB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
     PRB_REQUIRE(p && q == cudaDriverEntryPointSuccess, PRB_ERR_CUDA, "cuTensorMapEncodeTiled not available");
-    fn = reinterpret_cast<Fn>(p);
-  }
+    return reinterpret_cast<Fn>(p);
+  }();
   const cuuint64_t dims[2] = {128, kPmPackBytes / 256};
   const cuuint64_t strides[1] = {256};
   const cuuint32_t box[2] = {128, 16};
@@ -541,15 +540,9 @@ void encode_pm_pack_map(CUtensorMap* map, const uint8_t* pack) {
 // long as an M=128 single one (same per-SM tensor throughput), the epilogues are bound by the
 // 16/clk/SM MUFU tanh rate, and every epilogue -> MMA hand-off now crosses SMs.
 void launch_pm_rollout_tc(const PmTcArgs& a, int num_sms, cudaStream_t s) {
-  static int pair = -1;
-  if (pair < 0) {
-    const char* e = getenv("PRB_PM_PAIR");
-    pair = (e && e[0] == '1') ? 1 : 0;
-    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(PmSmem<false>)));
-    PRB_CUDA(cudaFuncSetAttribute(pm_rollout_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(PmSmem<true>)));
-  }
+  const bool pair = debug_option(PRB_OPT_PM_CTA_PAIR) != 0;  // tests: the opt-in CTA-pair kernel
+  ensure_smem(pm_rollout_tc_kernel<false>, sizeof(PmSmem<false>));
+  ensure_smem(pm_rollout_tc_kernel<true>, sizeof(PmSmem<true>));
   if (pair) {
     PmTcArgs ap = a;
     encode_pm_pack_map(&ap.pack_map, a.pack);

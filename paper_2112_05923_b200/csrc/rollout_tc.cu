@@ -478,7 +478,9 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
     if (__any_sync(0xffffffffu, bad)) {
       // Some lane's quotient was within 2^-19 of an integer (or its cash <= 0): redo this step's
       // trades for the warp with the reference's division, from the shares at the start of the
-      // step (this row of the compact obs tile written above; exact as floats) and bal_s.
+      // step (this row of the compact obs tile written above) and bal_s.  The floats are the
+      // exact share counts: the launcher routes here only when every reachable count is below
+      // 2^24 (rollout_fused.cu).
       const float* orow = a.b_obs + ((size_t)h * a.N + row) * P1 + 1;
 #pragma unroll
       for (int k = 0; k < K; ++k) sh[k] = live ? (int32_t)orow[k] : 0;
@@ -552,14 +554,8 @@ void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s) {
   const size_t smem = stock_rollout_tc_smem();
 #define PRB_TC_CASE(KK)                                                                                      \
   case KK: {                                                                                                 \
-    static bool attr = false;                                                                                \
-    if (!attr) {                                                                                             \
-      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK, false>,                                      \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
-      PRB_CUDA(cudaFuncSetAttribute(stock_rollout_tc_kernel<KK, true>,                                       \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
-      attr = true;                                                                                           \
-    }                                                                                                        \
+    ensure_smem(stock_rollout_tc_kernel<KK, false>, smem);                                                   \
+    ensure_smem(stock_rollout_tc_kernel<KK, true>, smem);                                                    \
     if (a.trace)                                                                                             \
       stock_rollout_tc_kernel<KK, true><<<grid, kM, smem, s>>>(a);                                           \
     else                                                                                                     \

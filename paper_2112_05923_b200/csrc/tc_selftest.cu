@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(128) tc_gemm_selftest_kernel(const float* __re
 
 extern "C" int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* hA, const float* hB, float* hD) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && hA && hB && hD, PRB_ERR_USAGE, "prb_debug_tc_gemm: NULL argument");
     PRB_REQUIRE(K % 16 == 0 && K <= 256 && N % 16 == 0 && N <= 256, PRB_ERR_CONFIG, "prb_debug_tc_gemm: bad shape");
     DevBuf<float> dA, dB, dD;
@@ -69,7 +70,7 @@ extern "C" int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* hA, con
     PRB_CUDA(cudaMemcpyAsync(dA.p, hA, dA.bytes(), cudaMemcpyHostToDevice, s));
     PRB_CUDA(cudaMemcpyAsync(dB.p, hB, dB.bytes(), cudaMemcpyHostToDevice, s));
     const size_t smem = (size_t)(128 + N) * K * 2;
-    PRB_CUDA(cudaFuncSetAttribute(tc_gemm_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    ensure_smem(tc_gemm_selftest_kernel, 200 * 1024);
     tc_gemm_selftest_kernel<<<1, 128, smem, s>>>(dA.p, dB.p, dD.p, K, N);
     PRB_CHECK_LAUNCH();
     PRB_CUDA(cudaMemcpyAsync(hD, dD.p, dD.bytes(), cudaMemcpyDeviceToHost, s));
@@ -105,6 +106,7 @@ extern "C" int prb_debug_trade_math(prb_ctx ctx, size_t n, const float* act, dou
                                     const double* price, double cost_rate, int32_t* desired, double* buy,
                                     int32_t* buy_i) {
   return guard([&] {
+    DeviceScope dev_(ctx);
     PRB_REQUIRE(ctx && act && balance && price && desired && buy && buy_i, PRB_ERR_USAGE,
                 "prb_debug_trade_math: NULL argument");
     PRB_REQUIRE(max_trade == floor(max_trade) && max_trade >= 0.0 && max_trade < 4194304.0, PRB_ERR_CONFIG,

@@ -567,3 +567,28 @@ def leaderboard_rank(ctx: Context, scores, seqs, capacity: int) -> np.ndarray:
     ctx.lib.prb_leaderboard_rank_host(ctx.h, _p(s, C.c_double), _p(q, C.c_uint64), s.size, capacity,
                                       _p(order, C.c_int32), C.byref(cnt))
     return order[:cnt.value]
+
+
+class PopulationStats:  # tournament.hpp:38-41
+    def __init__(self, mean: np.ndarray, variance: np.ndarray):
+        self.mean, self.variance = mean, variance
+
+
+def leaderboard_stats(entries: Sequence[Agent]) -> PopulationStats:
+    """Leaderboard::refresh_stats (tournament.hpp:66-87) over the board's entries in board order:
+    per-coordinate mean and population variance of the flat params, computed on the device."""
+    if not entries:
+        return PopulationStats(np.zeros(0), np.zeros(0))
+    P = entries[0].param_count
+    arr = (C.c_void_p * len(entries))(*[e.h for e in entries])
+    mean, var = np.zeros(P), np.zeros(P)
+    entries[0].ctx.lib.prb_leaderboard_stats_host(arr, len(entries), _p(mean, C.c_double), _p(var, C.c_double))
+    return PopulationStats(mean, var)
+
+
+def set_debug_option(option: int, value: int) -> None:
+    """Test-only switches (PRB_OPT_* in include/prb.h)."""
+    _lib.lib().prb_debug_set_option(option, value)
+
+
+OPT_PPO_PER_KERNEL, OPT_TC_FORCE_REDO, OPT_PM_CTA_PAIR = 1, 2, 3

@@ -5,6 +5,8 @@
   python profiles/drive.py env      [N]       # prb_vecenv_step on device buffers
   python profiles/drive.py ppo      [N] [H]   # a few PPO minibatch steps
   python profiles/drive.py pm       [N] [H]   # PointMass 3x256 tcgen05 rollout (configs[2])
+  python profiles/drive.py gae      [N] [H]   # buffer_advantages on a collected configs[1] buffer
+  python profiles/drive.py adam     [P]       # adam_step on a 10.5M-param agent (> L2)
 """
 import os
 import sys
@@ -67,6 +69,25 @@ def main():
         ro = pr.Rollout.for_env(env, H)
         for i in range(2):
             ro.collect(agent, env, seed=i)
+        ctx.synchronize()
+    elif what == "gae":
+        N = int(args[0]) if args else 65536
+        H = int(args[1]) if len(args) > 1 else 256
+        ctx, market, env = setup(N)
+        agent = pr.Agent.init(ctx, 181, 30, seed=7)
+        ro = pr.Rollout.for_env(env, H)
+        ro.collect(agent, env, seed=1)
+        for _ in range(3):
+            ctx.lib.prb_gae(ro.h, 0.99, 0.95, 1)
+        ctx.synchronize()
+    elif what == "adam":
+        import ctypes as C
+        ctx = pr.Context(0)
+        agent = pr.Agent.init(ctx, 4096, 2, seed=1, hidden=(1024, 1024))
+        g = pr.DeviceArray.from_numpy(ctx, np.random.default_rng(0).normal(size=agent.param_count).astype(np.float32)
+                                      * 1e-3)
+        for _ in range(3):
+            ctx.lib.prb_adam_step_device(agent.h, C.c_void_p(g.ptr))
         ctx.synchronize()
     print("ok", what)
 

@@ -188,6 +188,50 @@ int main() {
     EXPECT(lin.parent_pod == -1 && pod->param_count() == l0.first->param_count());
   }
 
+  // Leaderboard + leaderboard_update + refresh_stats (tournament.hpp:44-119): ties keep the earlier
+  // arrival, a full board rejects scores <= its minimum, stats = mean / population variance of the
+  // entries' params (on the device; checked here against a host restatement in the same order)
+  {
+    pb::Leaderboard lb(3);
+    const double sc[] = {1.0, 3.0, 3.0, 0.5, 2.0, 3.0};
+    std::vector<std::shared_ptr<const pb::Agent>> pods;
+    int inserted = 0;
+    for (int i = 0; i < 6; ++i) {
+      pods.push_back(std::shared_ptr<const pb::Agent>(pb::Agent::init(ctx, S, K, 40 + i, 1e-3).release()));
+      pb::LeaderboardEntry e;
+      e.artifact = pods.back();
+      e.score = sc[i];
+      e.pod_id = i;
+      inserted += pb::leaderboard_update(lb, e).inserted ? 1 : 0;
+    }
+    EXPECT(inserted == 5);  // 0.5 rejected once full (board {3,3,1} at that point)
+    EXPECT(lb.size() == 3 && lb.at(0).pod_id == 1 && lb.at(1).pod_id == 2 && lb.at(2).pod_id == 5);
+    const auto& st = lb.stats();
+    std::vector<std::vector<double>> fl;
+    for (const auto& e : lb.entries()) fl.push_back(e.artifact->flatten_params());
+    bool same = st.mean.size() == fl[0].size();
+    for (size_t j = 0; same && j < fl[0].size(); ++j) {
+      double m = 0.0;
+      for (const auto& f : fl) m += f[j];
+      m *= 1.0 / 3.0;
+      double v = 0.0;
+      for (const auto& f : fl) v += (f[j] - m) * (f[j] - m);
+      v *= 1.0 / 3.0;
+      same = same && m == st.mean[j] && v == st.variance[j];
+    }
+    EXPECT(same);
+    bool threw_nan = false;
+    try {
+      pb::LeaderboardEntry bad;
+      bad.artifact = pods[0];
+      bad.score = std::nan("");
+      pb::leaderboard_update(lb, bad);
+    } catch (const pb::NumericError&) {
+      threw_nan = true;
+    }
+    EXPECT(threw_nan);
+  }
+
   if (failures) {
     std::fprintf(stderr, "%d failures\n", failures);
     return 1;

@@ -101,6 +101,8 @@ def load_oracle():
     lib.orc_ppo_update.argtypes = [D, D, D, I64, SZ, C.c_int, SZ, C.c_int, D, D, D, D, U8, D, C.c_size_t, C.c_int,
                                    SZ, SZ, D, C.c_size_t, C.POINTER(PpoCfg), U64, D]
     lib.orc_fuse.argtypes = [C.POINTER(D), C.POINTER(D), C.POINTER(D), I64, C.c_size_t, C.c_size_t, D, D, D, I64]
+    lib.orc_population_stats.restype = None
+    lib.orc_population_stats.argtypes = [C.POINTER(D), C.c_size_t, C.c_size_t, D, D]
     lib.orc_leaderboard_update.restype = C.c_int
     lib.orc_leaderboard_update.argtypes = [D, U64, I64, SZ, C.c_size_t, U64, C.c_double, C.c_int64]
     lib.orc_compute_indicators.restype = C.c_int
@@ -154,8 +156,13 @@ def load_ref(path: str = REF_EXACT_SO):
     lib.ref_fuse.restype = C.c_int
     lib.ref_fuse.argtypes = [C.POINTER(D), C.POINTER(D), C.POINTER(D), I64, C.c_size_t, C.c_size_t, C.c_size_t,
                              SZ, C.c_int, D, D, D, I64]
+    lib.ref_leaderboard_stats.restype = C.c_int
+    lib.ref_leaderboard_stats.argtypes = [D, D, I64, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, SZ, C.c_int,
+                                          I64, SZ, D, D]
     lib.ref_leaderboard_sequence.restype = C.c_int
     lib.ref_leaderboard_sequence.argtypes = [D, I64, C.c_size_t, C.c_size_t, I64, D, SZ, I64]
+    lib.ref_synthetic_market.restype = None
+    lib.ref_synthetic_market.argtypes = [C.c_uint64, C.c_int, C.c_size_t, D, D, D]
     lib.ref_bench_ppo.restype = C.c_double
     lib.ref_bench_ppo.argtypes = [D, C.c_size_t, C.c_size_t, SZ, C.c_int, C.c_size_t, C.c_size_t, C.c_size_t,
                                   C.c_size_t, C.c_uint64]
@@ -200,3 +207,14 @@ def indicators(lib, high, low, close):
     rc = fn(ptr(high), ptr(low), ptr(close), T, K, ptr(out))
     assert rc == 0
     return out
+
+
+def population_stats(orc, entries):
+    """orc_population_stats over a list of flat f64 param vectors in board order."""
+    n = len(entries)
+    P = len(entries[0]) if n else 0
+    arrs = [np.ascontiguousarray(e, dtype=np.float64) for e in entries]
+    ptrs = (D * max(n, 1))(*[ptr(a) for a in arrs])
+    mean, var = np.zeros(P), np.zeros(P)
+    orc.orc_population_stats(ptrs, n, P, ptr(mean), ptr(var))
+    return mean, var

@@ -108,3 +108,19 @@ def test_leaderboard_golden(orc, g):  # tournament.hpp:44-119, ranking indices b
                                           C.byref(seq), float(s), i) for i, s in enumerate(scores)]
         assert np.array_equal(np.array(got), ranks)
         assert np.array_equal(bi[:size.value], final[final >= 0])
+
+
+GOLDEN_R2 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_golden_r2.npz")
+
+
+@pytest.fixture(scope="module")
+def g2():
+    return np.load(GOLDEN_R2)
+
+
+def test_population_stats_golden(orc, g2):  # Leaderboard::refresh_stats tournament.hpp:66-87
+    from oracle_bind import population_stats
+    for c, b, m, v in zip(g2["lbs_cand"], g2["lbs_board"], g2["lbs_mean"], g2["lbs_var"]):
+        entries = [c[i].astype(np.float64) for i in b if i >= 0]
+        om, ov = population_stats(orc, entries)
+        assert np.array_equal(om, m) and np.array_equal(ov, v)

@@ -227,3 +227,39 @@ def test_leaderboard_rank_matches_reference_golden(pr, ctx):
     for scores, cap, final in zip(g["lb_scores"], g["lb_cap"], g["lb_final"]):
         order = pr.leaderboard_rank(ctx, scores, np.arange(scores.size, dtype=np.uint64), int(cap))
         assert np.array_equal(order.astype(np.int64), final[final >= 0])
+
+
+def test_leaderboard_stats_matches_reference_golden(pr, ctx):
+    """Leaderboard::refresh_stats (tournament.hpp:66-87) on the device: the board the device
+    ranking selects from the candidates, then prb_leaderboard_stats over those agents' fp32
+    parameter blobs, against the PopulationStats the REFERENCE produced for the same sequence.
+    The params are fp32-representable and the device sums in the reference's order in fp64:
+    bit-exact."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_golden_r2.npz"))
+    S, A, *hid = (int(x) for x in g["lbs_shape"])
+    for c, s, cap, board, m, v in zip(g["lbs_cand"], g["lbs_scores"], g["lbs_cap"], g["lbs_board"], g["lbs_mean"],
+                                      g["lbs_var"]):
+        order = pr.leaderboard_rank(ctx, s, np.arange(s.size, dtype=np.uint64), int(cap))
+        assert np.array_equal(order.astype(np.int64), board[board >= 0])
+        agents = []
+        for i in order:
+            a = pr.Agent(ctx, S, A, hidden=hid)
+            a.set(c[i].astype(np.float64))
+            agents.append(a)
+        st = pr.leaderboard_stats(agents)
+        assert np.array_equal(st.mean, m) and np.array_equal(st.variance, v)
+
+
+def test_leaderboard_stats_stock_board_bit_exact_vs_oracle(pr, ctx, orc):
+    """Ten 64x64 stock agents (P = 33,661) on the device: mean / population variance equal the
+    oracle's restatement of refresh_stats over the same fp32 parameters bit for bit."""
+    from oracle_bind import population_stats
+    S, K = 181, 30
+    agents = [pr.Agent.init(ctx, S, K, seed=100 + i) for i in range(10)]
+    for i, a in enumerate(agents):
+        a.mutate(7 + i, 0.05)
+    st = pr.leaderboard_stats(agents)
+    om, ov = population_stats(orc, [a.flatten_params() for a in agents])
+    assert np.array_equal(st.mean, om) and np.array_equal(st.variance, ov)
+    assert pr.leaderboard_stats([]).mean.size == 0

@@ -337,7 +337,7 @@ def test_ppo_update_properties(pr, ctx):
 @pytest.mark.parametrize("S,A,hid,N,H,mb,epochs", [(181, 30, (64, 64), 64, 64, 1024, 2),
                                                     (6, 2, (256, 256, 256), 16, 32, 256, 1),
                                                     (11, 3, (8, 8), 9, 13, 37, 3)])
-def test_ppo_update_persistent_equals_per_kernel_path(pr, ctx, S, A, hid, N, H, mb, epochs, monkeypatch):
+def test_ppo_update_persistent_equals_per_kernel_path(pr, ctx, S, A, hid, N, H, mb, epochs):
     """The persistent cooperative update (one launch, grid barriers between phases) runs the
     per-kernel path's device functions in the same reduction orders: bit-identical results."""
     rng = np.random.default_rng(S + mb)
@@ -345,9 +345,11 @@ def test_ppo_update_persistent_equals_per_kernel_path(pr, ctx, S, A, hid, N, H, 
     ro, _ = _upload_random_buffer(pr, ctx, rng, N, H, S, A)
     cfg = pr.PpoConfig(epochs_per_update=epochs, minibatch_size=mb, buffer_size=N * H)
     a1, s1 = pr.ppo_update(agent, ro, cfg, 21)
-    monkeypatch.setenv("PRB_PPO_GRAPH", "1")
-    a2, s2 = pr.ppo_update(agent, ro, cfg, 21)
-    monkeypatch.delenv("PRB_PPO_GRAPH")
+    pr.set_debug_option(pr.OPT_PPO_PER_KERNEL, 1)
+    try:
+        a2, s2 = pr.ppo_update(agent, ro, cfg, 21)
+    finally:
+        pr.set_debug_option(pr.OPT_PPO_PER_KERNEL, 0)
     p1, m1, v1, t1 = a1.get()
     p2, m2, v2, t2 = a2.get()
     assert t1 == t2 == epochs * ((N * H) // mb) and s1.minibatches == s2.minibatches == t1
@@ -551,34 +553,35 @@ def _pm_log_std(agent):
     return flat[pa:pa + 2]
 
 
-def test_collect_pointmass_cta_pair_kernel():
-    """The opt-in CTA-pair (cta_group::2) PointMass kernel (PRB_PM_PAIR=1, read once per
-    process) passes the same replay / tolerance checks as the default kernel."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, PRB_PM_PAIR="1")
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_pointmass_rollout"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+@pytest.fixture
+def debug_option(pr):
+    """Sets a test-only switch (PRB_OPT_* in include/prb.h) for one test and clears it after."""
+    set_ = []
+
+    def _set(opt, val=1):
+        pr.set_debug_option(opt, val)
+        set_.append(opt)
+    yield _set
+    for o in set_:
+        pr.set_debug_option(o, 0)
 
 
-def test_collect_stock_tc_redo_path():
+@pytest.mark.parametrize("N,H", [(64, 250), (1000, 40), (40000, 6)])
+def test_collect_pointmass_cta_pair_kernel(pr, ctx, orc, debug_option, N, H):
+    """The opt-in CTA-pair (cta_group::2) PointMass kernel (PRB_OPT_PM_CTA_PAIR) passes the same
+    replay / tolerance checks as the default kernel."""
+    debug_option(pr.OPT_PM_CTA_PAIR)
+    test_collect_pointmass_rollout(pr, ctx, orc, 2, N, H)
+
+
+@pytest.mark.parametrize("K,N,H", [(30, 96, 48), (30, 300, 17), (3, 200, 40)])
+def test_collect_stock_tc_redo_path(pr, ctx, orc, debug_option, K, N, H):
     """The tcgen05 stock rollout's rare redo path (a buy quantity outside the division-free
     certificate -> the warp redoes the step's trades with the reference's division) forced on
-    every step (PRB_TC_FORCE_REDO=1, read per collect): the env transitions still replay
-    bit-exactly on the oracle."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, PRB_TC_FORCE_REDO="1")
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_learn.py"), "-k", "test_collect_stock_rollout_replays_on_oracle"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    every step (PRB_OPT_TC_FORCE_REDO): the env transitions still replay bit-exactly on the
+    oracle."""
+    debug_option(pr.OPT_TC_FORCE_REDO)
+    test_collect_stock_rollout_replays_on_oracle(pr, ctx, orc, 2, K, N, H)
 
 
 @pytest.mark.parametrize("max_trade,cost,cap", [(37.5, 0.002, 1e6), (1000.0, 0.0, 2e4), (3.0, 0.01, 5e5)])
@@ -609,7 +612,7 @@ def test_collect_stock_tc_config_variants(pr, ctx, orc, max_trade, cost, cap):
 
 
 @pytest.mark.parametrize("hid", [(64, 64), (8, 8)])
-def test_ppo_update_gate_midway_rolls_back(pr, ctx, hid, monkeypatch):
+def test_ppo_update_gate_midway_rolls_back(pr, ctx, hid, debug_option):
     """A non-finite loss at a LATER minibatch step (a NaN old log-prob placed in epoch 0's third
     minibatch by an injected permutation): the persistent update stores each Adam step before
     its gate is known and undoes it on failure, so the destination agent holds exactly the state
@@ -631,12 +634,11 @@ def test_ppo_update_gate_midway_rolls_back(pr, ctx, hid, monkeypatch):
     outs = []
     for graph in (False, True):
         if graph:
-            monkeypatch.setenv("PRB_PPO_GRAPH", "1")
+            debug_option(pr.OPT_PPO_PER_KERNEL)
         out = pr.Agent.init(ctx, S, A, seed=1, hidden=hid)
         with pytest.raises(pr.NumericError):
             pr.ppo_update(agent, ro, cfg, 3, perm=perm, out=out)
         outs.append(out.get())
-    monkeypatch.delenv("PRB_PPO_GRAPH")
     (p1, m1, v1, t1), (p2, m2, v2, t2) = outs
     t0 = agent.get()[3]
     assert t1 == t2 == t0 + 2

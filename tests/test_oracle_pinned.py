@@ -359,3 +359,23 @@ def test_leaderboard_matches_reference_with_ties(orc, ref):
         assert size.value == osz.value
         assert np.array_equal(bi[:size.value], oi[:osz.value])
         assert np.array_equal(np.array(ranks1), rk)
+
+
+def test_population_stats_bit_exact(orc, ref):
+    """Leaderboard::refresh_stats (tournament.hpp:66-87) after a leaderboard_update sequence of real
+    64x64 stock artifacts: the oracle's mean / population variance over the final board's entries
+    equals the reference's PopulationStats bit for bit."""
+    from oracle_bind import population_stats
+    rng = np.random.default_rng(5)
+    S, A, hid = 181, 30, np.array([64, 64], dtype=np.uint64)
+    P = 33661
+    n, cap = 14, 10
+    cand = rng.normal(scale=0.3, size=(n, P))
+    scores = rng.integers(0, 6, n).astype(np.float64)
+    ids = np.arange(n, dtype=np.int64)
+    oi = np.full(cap, -1, np.int64); osz = C.c_size_t(); mean = np.zeros(P); var = np.zeros(P)
+    assert ref.ref_leaderboard_stats(ptr(cand), ptr(scores), ptr(ids, I64), n, cap, S, A, ptr(hid, SZ), 2,
+                                     ptr(oi, I64), C.byref(osz), ptr(mean), ptr(var)) == 0
+    assert osz.value == cap
+    om, ov = population_stats(orc, [cand[i] for i in oi[:osz.value]])
+    assert np.array_equal(om, mean) and np.array_equal(ov, var)
