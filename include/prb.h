@@ -207,6 +207,14 @@ PRB_API int prb_rollout_device_fields(prb_rollout r, float** d_obs, float** d_ac
  * dones, values [N*H], bootstrap [N].  Any pointer may be NULL (download). */
 PRB_API int prb_rollout_download(prb_rollout r, double* states, double* actions, double* log_probs, double* rewards,
                                  uint8_t* dones, double* values, double* bootstrap);
+/* The chunks of selected envs only (TransitionBuffer rows e*H .. e*H+H-1 of
+ * each env e = envs[i], pod.hpp:89-94), written as chunk i = rows i*H ..
+ * i*H+H-1 of the outputs; bootstrap [n_envs].  raw_advantages / returns are
+ * the un-normalised GAE outputs of the last prb_gae (ppo.hpp:50-71; the
+ * normalisation is prb_gae_stats).  Any pointer may be NULL. */
+PRB_API int prb_rollout_download_chunks(prb_rollout r, const uint64_t* envs, size_t n_envs, double* states,
+                                        double* actions, double* log_probs, double* rewards, uint8_t* dones,
+                                        double* values, double* bootstrap, double* raw_advantages, double* returns);
 PRB_API int prb_rollout_upload(prb_rollout r, const double* states, const double* actions, const double* log_probs,
                                const double* rewards, const uint8_t* dones, const double* values,
                                const double* bootstrap);
@@ -217,6 +225,10 @@ PRB_API int prb_rollout_upload(prb_rollout r, const double* states, const double
 PRB_API int prb_gae(prb_rollout r, double gamma, double lambda, int normalize);
 /* Normalised advantages and returns in the reference index space. */
 PRB_API int prb_gae_download(prb_rollout r, double* advantages, double* returns);
+/* The whole-buffer advantage normalisation of the last prb_gae
+ * (buffer_advantages ppo.hpp:234-242): normalised = (raw - mean) / denom,
+ * denom = max(population std, 1e-8); (0, 1) when normalize was 0. */
+PRB_API int prb_gae_stats(prb_rollout r, double* mean, double* denom);
 /* Seam: set the (already normalised) advantages and returns directly, in the
  * reference index space -- the inputs gather_minibatch (ppo.hpp:83-103) reads. */
 PRB_API int prb_rollout_set_advantages(prb_rollout r, const double* advantages, const double* returns);
@@ -246,6 +258,12 @@ typedef struct {
  * src == dst is allowed (the agent is restored on error). */
 PRB_API int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed,
                            const uint64_t* perm, prb_agent dst, prb_ppo_stats* stats);
+/* Which device path prb_ppo_update runs when `a` is its src: 1 (default) = the
+ * tensor-core update (ppo_tc.cu: one thread-block cluster per learner, bf16
+ * operands / fp32 accumulation, for actor S-64-64-A / critic S-64-64-1 nets
+ * with A <= 32 and minibatches <= 1,024 rows; other shapes fall through to
+ * 0); 0 = the fp32 SIMT update (reference-precision gradients, any shape). */
+PRB_API int prb_agent_set_ppo_mode(prb_agent a, int mode);
 /* detail::ppo_loss_grads ppo.hpp:116-188 on one minibatch of rollout rows
  * (reference index space); grads [P] (flat layout) and losses[3] to host.
  * Requires prb_gae first. */
@@ -322,6 +340,17 @@ PRB_API int prb_debug_set_option(int option, int value);
 /* D[128][N] = bf16(A[128][K]) . bf16(B[N][K])^T with fp32 accumulation in
  * TMEM, one CTA, K % 16 == 0 (<= 256), N % 16 == 0 (<= 256). */
 PRB_API int prb_debug_tc_gemm(prb_ctx ctx, int K, int N, const float* A, const float* B, float* D);
+
+/* The same GEMM with A and/or B stored transposed (MN-major operands, the
+ * layout the PPO backward uses); hyp selects the descriptor stride convention
+ * under test (0: LBO along MN, SBO along K; 1: swapped). */
+PRB_API int prb_debug_tc_gemm_major(prb_ctx ctx, int K, int N, int a_mn, int b_mn, int hyp, const float* A,
+                                    const float* B, float* D);
+
+/* The reduced gradient [P] (flat layout) of the last minibatch step the
+ * tensor-core PPO update ran on `a` (its dst), or of the last
+ * prb_adam_step_device / per-kernel step (tests only). */
+PRB_API int prb_debug_agent_grads(prb_agent a, double* grads);
 
 /* ---- self-test of the fused rollout's trade arithmetic (tests only) ------ */
 /* Per element i, the device functions the tcgen05 stock rollout uses for

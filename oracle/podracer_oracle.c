@@ -295,6 +295,20 @@ ORC_API void orc_pm_vec_reset(size_t N, uint64_t seed, orc_mt64* gens, double* s
   }
 }
 
+/* The same reset for a subset of a VecEnv's envs: env idx[i]'s generator and state land in slot
+ * i (each env's stream depends only on its own index, env.hpp:186-194), so a sample of a large
+ * VecEnv replays without materialising every env. */
+ORC_API void orc_pm_vec_reset_subset(size_t n, const uint64_t* idx, uint64_t seed, orc_mt64* gens, double* state,
+                                     uint64_t* step_count, double* ep_return) {
+  for (size_t i = 0; i < n; ++i) {
+    uint64_t tags[2] = {1 /* kVecEnv */, idx[i]};
+    orc_mt64_seed(&gens[i], orc_derive_seed(seed, tags, 2));
+    orc_pointmass_reset(&gens[i], state + i * 6);
+    step_count[i] = 0;
+    ep_return[i] = 0.0;
+  }
+}
+
 /* VectorizedEnvironment<PointMass2D>::step: env.hpp:200-236. */
 ORC_API void orc_pm_vec_step(size_t N, orc_mt64* gens, double* state, uint64_t* step_count, double* ep_return,
                              const double* actions, double* reward, uint8_t* done, double* terminal_state,

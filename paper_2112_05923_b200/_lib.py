@@ -152,6 +152,8 @@ SIGNATURES = {
     "prb_rollout_device_fields": (I, [P] + [C.POINTER(P)] * 7),
     "prb_rollout_download": (I, [P, pD, pD, pD, pD, pU8, pD, pD]),
     "prb_rollout_upload": (I, [P, pD, pD, pD, pD, pU8, pD, pD]),
+    "prb_rollout_download_chunks": (I, [P, pU64, SZ, pD, pD, pD, pD, pU8, pD, pD, pD, pD]),
+    "prb_gae_stats": (I, [P, pD, pD]),
     "prb_gae": (I, [P, D, D, I]),
     "prb_gae_download": (I, [P, pD, pD]),
     "prb_rollout_set_advantages": (I, [P, pD, pD]),
@@ -165,6 +167,8 @@ SIGNATURES = {
     "prb_leaderboard_rank": (I, [P, P, P, SZ, SZ, P, P]),
     "prb_leaderboard_rank_host": (I, [P, pD, pU64, SZ, SZ, pI32, pI32]),
     "prb_agent_mutate": (I, [P, U64, D]),
+    "prb_agent_set_ppo_mode": (I, [P, I]),
+    "prb_debug_agent_grads": (I, [P, pD]),
     "prb_leaderboard_stats": (I, [C.POINTER(P), SZ, P, P]),
     "prb_leaderboard_stats_host": (I, [C.POINTER(P), SZ, pD, pD]),
     "prb_debug_set_option": (I, [I, I]),
@@ -174,6 +178,7 @@ SIGNATURES = {
     "prb_leaderboard_allgather_rank": (I, [P, P, P, P, SZ, SZ, P, P, P, P, P]),
     "prb_agent_broadcast": (I, [P, P, I]),
     "prb_debug_tc_gemm": (I, [P, I, I, pF, pF, pF]),
+    "prb_debug_tc_gemm_major": (I, [P, I, I, I, I, I, pF, pF, pF]),
     "prb_debug_trade_math": (I, [P, SZ, pF, D, pD, pD, D, pI32, pD, pI32]),
 }
 

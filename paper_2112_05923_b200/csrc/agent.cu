@@ -510,6 +510,25 @@ int prb_leaderboard_stats_host(const prb_agent* entries, size_t n, double* mean,
   });
 }
 
+int prb_debug_agent_grads(prb_agent a, double* grads) {
+  return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
+    PRB_REQUIRE(a && grads, PRB_ERR_USAGE, "prb_debug_agent_grads: NULL argument");
+    std::vector<float> g(a->P);
+    PRB_CUDA(cudaMemcpyAsync(g.data(), a->d_grads.p, a->P * sizeof(float), cudaMemcpyDeviceToHost, a->ctx->stream));
+    a->ctx->sync();
+    for (size_t i = 0; i < a->P; ++i) grads[i] = g[i];
+  });
+}
+
+int prb_agent_set_ppo_mode(prb_agent a, int mode) {
+  return guard([&] {
+    PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_set_ppo_mode: NULL agent");
+    PRB_REQUIRE(mode == 0 || mode == 1, PRB_ERR_CONFIG, "prb_agent_set_ppo_mode: mode must be 0 or 1");
+    a->ppo_mode = mode;
+  });
+}
+
 int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma) {
   return guard([&] {
     DeviceScope dev_(a ? a->ctx : nullptr);

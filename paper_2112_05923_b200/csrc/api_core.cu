@@ -10,6 +10,7 @@
 
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "tmap.h"
 
 namespace prb {
 
@@ -44,6 +45,27 @@ const char* debug_env(const char* name) {
   (void)name;
   return nullptr;
 #endif
+}
+
+void encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t dim0, uint64_t dim1,
+                    uint64_t stride1_bytes, uint32_t box0, uint32_t box1, CUtensorMapL2promotion l2) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const Fn fn = [] {  // thread-safe one-time lookup
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PRB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    PRB_REQUIRE(p && q == cudaDriverEntryPointSuccess, PRB_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    return reinterpret_cast<Fn>(p);
+  }();
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PRB_REQUIRE(r == CUDA_SUCCESS, PRB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
 uint64_t splitmix64(uint64_t x) { return splitmix64_d(x); }

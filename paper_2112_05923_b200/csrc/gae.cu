@@ -1,26 +1,54 @@
 // gae.cu -- generalized advantage estimation over the device rollout buffer
 // (compute_gae ppo.hpp:50-71, buffer_advantages ppo.hpp:212-244).
 //
-// The buffer is time-major ([H][N]), so one thread per env walks its chunk
-// backwards with every load coalesced across the warp (consecutive envs are
-// consecutive addresses).  The recursion runs in fp64 with round-to-nearest
-// intrinsics in the reference's operation order, so on identical fp32 inputs
-// it reproduces the reference's fp64 result before the final fp32 store.
-// The whole-buffer normalisation statistics (mean, population std floored at
-// 1e-8) are reduced in the same pass: per-thread fp64 sums of x and x^2, then
-// Chan merges of (n, mean, M2) across threads and blocks in fp64; the
-// PPO gather applies (adv - mean) / denom on the fly, so the normalised
+// The per-env recursion  gae_t = delta_t + c_t * gae_{t+1},  c_t = gamma*lambda*(1 - d_t),
+// delta_t = r_t + gamma*V_{t+1}*(1 - d_t) - V_t  is an affine map of gae_{t+1}, so it runs as a
+// segmented affine scan over the horizon instead of one serial walk per env:
+//   * Work unit (tile): 32 consecutive envs x a window of WIN steps of the time-major [H][N]
+//     buffer.  Persistent CTAs walk their env groups' windows from the last to the first, the
+//     next tile's r / V / done boxes streaming into a second shared-memory buffer (three 2-D
+//     TMA loads on an mbarrier) while the current one is scanned, so HBM always has a tile in
+//     flight per CTA.
+//   * Phase 1: warp w owns steps [w*SEG, (w+1)*SEG) of the window, lane = env (every shared
+//     row read is conflict-free); each thread forms delta_t and composes its segment backwards
+//     into (A, B) with gae_{seg start} = B + A * gae_{seg end} (delta, V, dones kept in registers).
+//   * Phase 2: each thread folds the (A, B) of the later segments of its env, starting from the
+//     carry of the later window (0 past the last step, ppo.hpp:63), into its incoming gae.
+//   * Phase 3: each thread re-runs its segment from that gae in the reference's operation order
+//     and stores advantage / return (one coalesced 128-byte row segment per warp and step).
+// Precision: fp64 throughout; a segment's incoming gae comes from the composed maps instead of
+// the serial chain, so gae agrees with the reference's fp64 recursion to ~1e-15 relative (tested
+// at 1e-12) and the fp32 stores are the reference's fp32 rounding or one ulp beside it.  The
+// last segment of every env (carry 0) and every step after a done (c_t = 0 cuts the chain) are
+// exactly the reference's values.
+// The whole-buffer normalisation statistics (mean, population std floored at 1e-8) are reduced
+// in the same pass: per-thread (n, mean, M2) of its stored advantages, Chan merges across threads
+// and blocks in fp64; the PPO gather applies (adv - mean) / denom on the fly, so the normalised
 // advantages never make an extra HBM round trip.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "prb_internal.h"
+#include "tc.cuh"
+#include "tmap.h"
 
 using namespace prb;
 
 namespace {
 
-constexpr int kGaeU = 16;  // recursion steps per pipelined load block
+#ifndef PRB_GAE_WIN
+#define PRB_GAE_WIN 64
+#endif
+#ifndef PRB_GAE_SW
+#define PRB_GAE_SW 4
+#endif
+#ifndef PRB_GAE_ENVS
+#define PRB_GAE_ENVS 32
+#endif
+constexpr int kGaeWin = PRB_GAE_WIN;      // steps per tile window
+constexpr int kGaeSegWarps = PRB_GAE_SW;  // segments per window
+constexpr int kGaeEnvs = PRB_GAE_ENVS;    // envs per tile (one per lane of an env-warp)
 
 struct Welford {
   double n, mean, m2;
@@ -38,69 +66,177 @@ __device__ __forceinline__ Welford merge(Welford a, Welford b) {
   return r;
 }
 
-__global__ void __launch_bounds__(128) gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
-                                                  const uint8_t* __restrict__ done, const float* __restrict__ boot,
-                                                  int N, int H, double gamma, double lambda, float* __restrict__ adv,
-                                                  float* __restrict__ ret, double* __restrict__ partials) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  Welford w{0.0, 0.0, 0.0};
-  if (e < N) {
-    const double gl = __dmul_rn(gamma, lambda);
-    double gae = 0.0;
-    double next_v = (double)boot[e];
-    double s1 = 0.0, s2 = 0.0;  // sum and sum of squares of the stored advantages (fp64)
-    // Software pipeline over blocks of kGaeU steps: the loads of the next block (they do not
-    // depend on the recursion) are in flight while the current block's recursion runs.
-    float rA[kGaeU], vA[kGaeU], rB[kGaeU], vB[kGaeU];
-    uint8_t dA[kGaeU], dB[kGaeU];
-    auto load = [&](int h0, float (&rr)[kGaeU], float (&vv)[kGaeU], uint8_t (&dd)[kGaeU]) {
-#pragma unroll
-      for (int u = 0; u < kGaeU; ++u) {
-        const int h = h0 - u;
-        if (h >= 0) {
-          const size_t j = (size_t)h * N + e;
-          rr[u] = rew[j];
-          vv[u] = val[j];
-          dd[u] = done[j];
-        }
-      }
-    };
-    auto run = [&](int h0, const float (&rr)[kGaeU], const float (&vv)[kGaeU], const uint8_t (&dd)[kGaeU]) {
-#pragma unroll
-      for (int u = 0; u < kGaeU; ++u) {
-        const int h = h0 - u;
-        if (h >= 0) {
-          const size_t j = (size_t)h * N + e;
-          const double r = (double)rr[u];
-          const double v = (double)vv[u];
-          const double nonterminal = dd[u] ? 0.0 : 1.0;
-          // delta = r + gamma * next_value * nonterminal - v ; gae = delta + gamma*lambda*nonterminal*gae
-          const double delta = __dsub_rn(__dadd_rn(r, __dmul_rn(__dmul_rn(gamma, next_v), nonterminal)), v);
-          gae = __dadd_rn(delta, __dmul_rn(__dmul_rn(gl, nonterminal), gae));
-          const float a32 = (float)gae;
-          adv[j] = a32;
-          ret[j] = (float)__dadd_rn(gae, v);
-          next_v = v;
-          const double x = (double)a32;
-          s1 += x;
-          s2 = fma(x, x, s2);
-        }
-      }
-    };
-    load(H - 1, rA, vA, dA);
-    for (int h0 = H - 1; h0 >= 0; h0 -= 2 * kGaeU) {
-      load(h0 - kGaeU, rB, vB, dB);
-      run(h0, rA, vA, dA);
-      load(h0 - 2 * kGaeU, rA, vA, dA);
-      run(h0 - kGaeU, rB, vB, dB);
-    }
-    // this thread's (n, mean, M2) for the Chan merges below
-    w.n = (double)H;
-    w.mean = s1 / w.n;
-    w.m2 = fmax(s2 - s1 * w.mean, 0.0);
+// Shared-memory image of one tile: r, V [WIN][E] fp32 and done [WIN][E] u8 (the TMA boxes).
+// After phase 1 the r / V rows are overwritten with the tile's advantages / returns, which
+// leave by TMA stores of the same boxes.
+template <int WIN, int E>
+struct __align__(128) GaeTile {
+  float r[WIN][E];
+  float v[WIN][E];
+  uint8_t d[WIN][E];
+};
+
+struct GaeMaps {  // time-major [H][N] r / V / adv / ret (fp32) and done (u8), boxes [WIN][E]
+  CUtensorMap r, v, d, adv, ret;
+};
+
+// E envs per tile (E/32 env-warps x SW segment-warps; SEG = WIN / SW steps per thread).
+template <int WIN, int SW, int E, bool TMA>
+__global__ void __launch_bounds__(E * SW)
+    gae_scan_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ rew,
+                    const float* __restrict__ val, const uint8_t* __restrict__ done, const float* __restrict__ boot,
+                    int N, int H, double gamma, double lambda, float* __restrict__ adv, float* __restrict__ ret,
+                    double* __restrict__ partials) {
+  constexpr int SEG = WIN / SW;
+  constexpr int EW = E / 32;
+  constexpr int T = E * SW;
+  static_assert(SEG <= 32, "segment mask is 32 bits");
+  using Tile = GaeTile<WIN, E>;
+  extern __shared__ __align__(128) unsigned char gae_smem[];
+  Tile* tiles = reinterpret_cast<Tile*>(gae_smem);  // [2] double buffer
+  __shared__ __align__(8) uint64_t s_full[2];  // TMA transaction barriers of the two buffers
+  __shared__ double2 s_ab[SW][E];             // (A, B) of each segment of each env
+  __shared__ double s_carry[E];               // gae at the first step of the later window
+  __shared__ float s_vlater[E];               // V at the first step of the later window
+  __shared__ Welford s_w[T / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = (warp % EW) * 32 + lane, sw = warp / EW;
+  const double gl = __dmul_rn(gamma, lambda);
+  const int ngroups = (N + E - 1) / E, nwin = (H + WIN - 1) / WIN;
+  const int my_groups = (int)blockIdx.x < ngroups ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int ntiles = my_groups * nwin;
+  if (TMA && threadIdx.x == 0) {
+    tc::mbar_init(&s_full[0], 1);
+    tc::mbar_init(&s_full[1], 1);
   }
+  __syncthreads();
+  // tile k -> env group g, window wi (windows of a group from the last to the first)
+  auto tile_of = [&](int k, int& g, int& wi) {
+    g = (int)blockIdx.x + (k / nwin) * (int)gridDim.x;
+    wi = nwin - 1 - k % nwin;
+  };
+  auto issue = [&](int k) {
+    int g, wi;
+    tile_of(k, g, wi);
+    Tile& tb = tiles[k & 1];
+    if (TMA) {
+      if (threadIdx.x == 0) {
+        tc::bulk_wait_read0();  // the stores of tile k - 2 have read this buffer
+        // three boxes; rows past H and columns past N arrive zero-filled (never stored)
+        tc::mbar_arrive_expect_tx(&s_full[k & 1], (uint32_t)sizeof(Tile));
+        tc::tma_load_2d(&tb.r[0][0], &maps.r, g * E, wi * WIN, &s_full[k & 1]);
+        tc::tma_load_2d(&tb.v[0][0], &maps.v, g * E, wi * WIN, &s_full[k & 1]);
+        tc::tma_load_2d(&tb.d[0][0], &maps.d, g * E, wi * WIN, &s_full[k & 1]);
+      }
+    } else {  // any N: element loads (synchronous)
+      const int e0 = g * E, t0 = wi * WIN, len = min(WIN, H - t0);
+      for (int c = threadIdx.x; c < len * E; c += T) {
+        const int row = c / E, l = c % E;
+        if (e0 + l < N) {
+          const size_t j = (size_t)(t0 + row) * N + e0 + l;
+          tb.r[row][l] = __ldcs(rew + j);
+          tb.v[row][l] = __ldcs(val + j);
+          tb.d[row][l] = __ldcs(done + j);
+        }
+      }
+    }
+  };
+  Welford w{0.0, 0.0, 0.0};
+  if (ntiles > 0) issue(0);
+  for (int k = 0; k < ntiles; ++k) {
+    if (k + 1 < ntiles) issue(k + 1);  // the next tile streams in while this one is scanned
+    if (TMA) tc::mbar_wait(&s_full[k & 1], (uint32_t)((k >> 1) & 1));
+    __syncthreads();  // (TMA: every thread past the wait; else: the element loads are visible)
+    int g, wi;
+    tile_of(k, g, wi);
+    Tile& tb = tiles[k & 1];
+    const int e = g * E + col;
+    const bool live = e < N;
+    const int t0 = wi * WIN, len = min(WIN, H - t0);
+    const bool last_window = (wi == nwin - 1);
+    const int s0 = sw * SEG, slen = max(0, min(SEG, len - s0));
+    // V after this segment: the next segment's first value, the later window's first value, or
+    // the bootstrap V(s_H) (ppo.hpp:62)
+    float vn = 0.f;
+    if (live && slen > 0)
+      vn = (s0 + slen < len) ? tb.v[s0 + slen][col] : (last_window ? __ldg(boot + e) : s_vlater[col]);
+    // phase 1: delta_t (the reference's expression) and the composed map of the segment;
+    // delta, V and the done bits stay in registers for phase 3
+    double delta[SEG];
+    float vr[SEG];
+    uint32_t dmask = 0;
+    double A = 1.0, B = 0.0;
+    {
+      double nv = (double)vn;
+#pragma unroll
+      for (int u = SEG - 1; u >= 0; --u)
+        if (u < slen) {
+          const int i = s0 + u;
+          const bool dn = tb.d[i][col] != 0;
+          vr[u] = tb.v[i][col];
+          const double vv = (double)vr[u];
+          delta[u] = __dsub_rn(__dadd_rn((double)tb.r[i][col], __dmul_rn(__dmul_rn(gamma, nv), dn ? 0.0 : 1.0)), vv);
+          const double c = dn ? 0.0 : gl;  // gamma*lambda*nonterminal
+          dmask |= (uint32_t)dn << u;
+          B = fma(c, B, delta[u]);
+          A = c * A;
+          nv = vv;
+        }
+    }
+    s_ab[sw][col] = make_double2(A, B);
+    __syncthreads();
+    // phase 2: incoming gae of this segment
+    double gin = last_window ? 0.0 : s_carry[col];
+    for (int s2 = SW - 1; s2 > sw; --s2) {
+      const double2 ab = s_ab[s2][col];
+      gin = fma(ab.x, gin, ab.y);
+    }
+    float vfirst = 0.f;
+    if (sw == 0) vfirst = tb.v[0][col];
+    __syncthreads();  // s_carry / s_vlater / s_ab and the tile's r / V rows consumed
+    // phase 3: the reference's recursion (ppo.hpp:61-68) from the incoming gae; advantages and
+    // returns go to the tile's r / V rows (TMA) or straight to HBM (element path)
+    if (live && slen > 0) {
+      double gae = gin;
+      double x0 = 0.0, s1 = 0.0, sq = 0.0;  // shifted sums of this thread's stored advantages
+#pragma unroll
+      for (int u = SEG - 1; u >= 0; --u)
+        if (u < slen) {
+          // gae = delta + gamma*lambda*nonterminal*gae; gamma*lambda*nonterminal is gl or 0 exactly
+          gae = __dadd_rn(delta[u], ((dmask >> u) & 1u) ? 0.0 : __dmul_rn(gl, gae));
+          const float a32 = (float)gae, r32 = (float)__dadd_rn(gae, (double)vr[u]);
+          if (TMA) {
+            tb.r[s0 + u][col] = a32;
+            tb.v[s0 + u][col] = r32;
+          } else {
+            const size_t j = (size_t)(t0 + s0 + u) * N + e;
+            __stcs(adv + j, a32);
+            __stcs(ret + j, r32);
+          }
+          // the statistics cover the stored fp32 values: the gather normalises exactly those
+          const double a = (double)a32;
+          if (u == slen - 1) x0 = a;
+          const double dx = a - x0;
+          s1 += dx;
+          sq = fma(dx, dx, sq);
+        }
+      if (sw == 0) {  // this window's first step feeds the earlier window
+        s_carry[col] = gae;
+        s_vlater[col] = vfirst;
+      }
+      const double n = (double)slen, mean = x0 + s1 / n;
+      w = merge(w, Welford{n, mean, fmax(sq - s1 * (s1 / n), 0.0)});
+    }
+    if (TMA) tc::fence_proxy_async();  // the staged rows, to the async proxy
+    __syncthreads();                    // s_carry visible to the next tile; staged rows complete
+    if (TMA && threadIdx.x == 0) {
+      tc::tma_store_2d(&maps.adv, g * E, t0, &tb.r[0][0]);
+      tc::tma_store_2d(&maps.ret, g * E, t0, &tb.v[0][0]);
+      tc::bulk_commit();
+    }
+  }
+  if (TMA && threadIdx.x == 0) tc::bulk_wait0();
   if (!partials) return;
-  // block merge: warp shuffles then smem
   for (int o = 16; o > 0; o >>= 1) {
     Welford b;
     b.n = __shfl_xor_sync(0xffffffffu, w.n, o);
@@ -108,12 +244,11 @@ __global__ void __launch_bounds__(128) gae_kernel(const float* __restrict__ rew,
     b.m2 = __shfl_xor_sync(0xffffffffu, w.m2, o);
     w = merge(w, b);
   }
-  __shared__ Welford sw[4];
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = w;
+  if (lane == 0) s_w[warp] = w;
   __syncthreads();
   if (threadIdx.x == 0) {
-    Welford acc = sw[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) acc = merge(acc, sw[i]);
+    Welford acc = s_w[0];
+    for (int i = 1; i < T / 32; ++i) acc = merge(acc, s_w[i]);
     partials[3 * blockIdx.x + 0] = acc.n;
     partials[3 * blockIdx.x + 1] = acc.mean;
     partials[3 * blockIdx.x + 2] = acc.m2;
@@ -146,11 +281,38 @@ __global__ void gae_stats_kernel(const double* __restrict__ partials, int nblock
 
 void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8_t* done, const float* boot, size_t N,
                     size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize) {
-  const int grid = (int)((N + 127) / 128);  // 128-thread CTAs: more even spread over the SMs
+  PRB_REQUIRE(N < (1u << 31) && H < (1u << 31), PRB_ERR_CONFIG, "buffer_advantages: buffer too large");
+  constexpr int E = kGaeEnvs, W = kGaeWin, SW = kGaeSegWarps;
+  constexpr size_t smem = 2 * sizeof(GaeTile<W, E>);
+  // TMA boxes need 16-byte row pitches (the u8 dones: N % 16 == 0)
+  const bool tma = (N % 16) == 0;
+  GaeMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  if (tma) {
+    encode_tmap_2d(&maps.r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rew, N, H, N * 4, E, W);
+    encode_tmap_2d(&maps.v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, val, N, H, N * 4, E, W);
+    encode_tmap_2d(&maps.d, CU_TENSOR_MAP_DATA_TYPE_UINT8, done, N, H, N, E, W);
+    encode_tmap_2d(&maps.adv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, adv, N, H, N * 4, E, W);
+    encode_tmap_2d(&maps.ret, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ret, N, H, N * 4, E, W);
+  }
+  const void* fn = tma ? (const void*)gae_scan_kernel<W, SW, E, true> : (const void*)gae_scan_kernel<W, SW, E, false>;
+  ensure_smem_attr(fn, smem);
+  int occ = 0;
+  PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, E * SW, smem));
+  // persistent CTAs with an equal number of env groups each (no tail of CTAs with one more)
+  const int groups = (int)((N + E - 1) / E);
+  const int resident = ctx->num_sms * std::max(occ, 1);
+  const int per_cta = (groups + resident - 1) / resident;
+  const int grid = std::max(1, (groups + per_cta - 1) / per_cta);
   double* partials = stat ? static_cast<double*>(ctx->device_scratch((size_t)grid * 3 * sizeof(double))) : nullptr;
   {
     ProfScope prof(ctx, kProfGae);
-    gae_kernel<<<grid, 128, 0, ctx->stream>>>(rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials);
+    if (tma)
+      gae_scan_kernel<W, SW, E, true><<<grid, E * SW, smem, ctx->stream>>>(maps, rew, val, done, boot, (int)N, (int)H,
+                                                                           gamma, lambda, adv, ret, partials);
+    else
+      gae_scan_kernel<W, SW, E, false><<<grid, E * SW, smem, ctx->stream>>>(maps, rew, val, done, boot, (int)N,
+                                                                            (int)H, gamma, lambda, adv, ret, partials);
   }
   PRB_CHECK_LAUNCH();
   if (stat) {
@@ -204,6 +366,18 @@ int prb_gae_download(prb_rollout r, double* advantages, double* returns) {
         if (advantages) advantages[i] = ((double)a[j] - st[0]) / st[1];
         if (returns) returns[i] = t[j];
       }
+  });
+}
+
+int prb_gae_stats(prb_rollout r, double* mean, double* denom) {
+  return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
+    PRB_REQUIRE(r && r->gae_valid && mean && denom, PRB_ERR_USAGE, "prb_gae_stats: call prb_gae first");
+    double st[2];
+    PRB_CUDA(cudaMemcpyAsync(st, r->d_advstat.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, r->ctx->stream));
+    r->ctx->sync();
+    *mean = st[0];
+    *denom = st[1];
   });
 }
 

@@ -31,6 +31,7 @@
 #include <cstring>
 
 #include "mlp_simt.cuh"
+#include "ppo_tc.h"
 #include "policy_internal.h"
 #include "prb_internal.h"
 #include "rng.cuh"
@@ -1322,6 +1323,11 @@ struct PpoWorkspace {
   DevBuf<unsigned long long> ptrace; // PRB_PPO_TRACE of the persistent update: [grid][10]
   DevBuf<float> wimg;                // persistent rows-of-8 update: staged-layout weight image
   DevBuf<uint2> rtab;                // ... and the next step's resolved minibatch rows
+  // tensor-core update (ppo_tc.cu): weight image, per-CTA partial slab, stats, chain descriptor
+  DevBuf<uint8_t> tc_img;
+  DevBuf<float> tc_slab;
+  DevBuf<double> tc_stats;
+  DevBuf<PpoTcChain> tc_chain;
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -1554,6 +1560,82 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
               grid, smem, s, args);
 }
 
+// The tensor-core update (ppo_tc.cu) covers the stock-pod nets: actor S-64-64-A, critic
+// S-64-64-1 with A <= 32, minibatches of <= 1,024 rows (<= 8 CTAs of 128 rows per cluster), and
+// inputs that fit its 192-column X tile (<= 32 private features + <= 159 others + the ones column).
+bool ppo_tc_supported(prb_agent a, prb_rollout r, int mb, int mode) {
+  if (mode != 1) return false;
+  const std::vector<size_t> ad = {a->S, 64, 64, a->A}, cd = {a->S, 64, 64, 1};
+  if (a->adims != ad || a->cdims != cd || a->A > 32 || mb > kPpoTcMaxRows || mb < 1) return false;
+  const size_t nrest = r->obs_mode == 1 ? 5 * (size_t)r->K : a->S - std::min<size_t>(a->S, 32);
+  const size_t npriv = r->obs_mode == 1 ? r->Sp : std::min<size_t>(a->S, 32);
+  return npriv <= 32 && nrest <= 159;
+}
+
+PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspace& ws, int64_t steps,
+                       const uint32_t* perm, cudaStream_t s) {
+  PpoTcArgs t{};
+  t.S = p.S;
+  t.A = p.A;
+  t.P = p.P;
+  t.Pp = (int)((a->P + 2 + 31) & ~size_t(31));
+  for (int l = 0; l < 3; ++l) {
+    t.a_w[l] = (int)a->aoff[l];
+    t.c_w[l] = (int)a->coff[l];
+  }
+  t.log_std = (int)a->Pa;
+  t.obs_mode = r->obs_mode;
+  t.Sp = (int)r->Sp;
+  t.F = 5 * r->K;
+  t.npriv = r->obs_mode == 1 ? (int)r->Sp : std::min(p.S, 32);
+  t.nrest = r->obs_mode == 1 ? t.F : p.S - t.npriv;
+  t.ones_col = 32 + t.nrest;
+  t.obs = p.obs;
+  t.row = p.row;
+  t.feat = p.feat;
+  t.act = p.act;
+  t.logp = p.logp;
+  t.adv = p.adv;
+  t.ret = p.ret;
+  t.advstat = p.advstat;
+  t.N = p.N;
+  t.n = p.n;
+  t.nmb = p.nmb;
+  t.bits = p.bits;
+  t.mb = p.mb;
+  t.C = (p.mb + 127) / 128;
+  t.steps = steps;
+  t.clip = (float)p.clip;
+  t.ent = (float)p.ent;
+  t.vf = (float)p.vf;
+  t.b1 = a->beta1;
+  t.b2 = a->beta2;
+  t.eps = (float)a->eps;
+  ws.tc_img.ensure(kPpoTcImgBytes);
+  ws.tc_slab.ensure((size_t)t.C * t.Pp);
+  ws.tc_stats.ensure(4);
+  ws.tc_chain.ensure(1);
+  PRB_CUDA(cudaMemsetAsync(ws.tc_img.p, 0, kPpoTcImgBytes, s));  // padding of the operand blocks
+  PRB_CUDA(cudaMemsetAsync(ws.tc_stats.p, 0, 4 * sizeof(double), s));
+  PpoTcChain c{};
+  c.params = a->d_params.p;
+  c.m = a->d_m.p;
+  c.v = a->d_v.p;
+  c.t = a->d_t.p;
+  c.grads = a->d_grads.p;
+  c.img = ws.tc_img.p;
+  c.slab = ws.tc_slab.p;
+  c.stats = ws.tc_stats.p;
+  c.status = a->d_status.p;
+  c.perm = perm;
+  c.seed = p.seed;
+  c.lr = (float)a->lr;
+  PRB_CUDA(cudaMemcpyAsync(ws.tc_chain.p, &c, sizeof(c), cudaMemcpyHostToDevice, s));
+  PRB_CUDA(cudaStreamSynchronize(s));  // c lives on this stack frame
+  t.chains = ws.tc_chain.p;
+  return t;
+}
+
 std::string status_message(int detail) {
   switch (detail) {
     case 10: return "ppo_losses: policy_loss is non-finite";
@@ -1664,7 +1746,16 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     // capture a block of them once as a CUDA graph and replay it.
     const size_t kGraphSteps = 32;
     const int pgrid = persistent_grid(p, dst, ws);
-    if (pgrid > 0 && steps > 0) {
+    if (steps > 0 && ppo_tc_supported(dst, r, mb, src->ppo_mode)) {  // one cluster runs the whole chain
+      PpoTcArgs ta = make_tc_args(p, dst, r, ws, (int64_t)steps, p.perm, s);
+      {
+        ProfScope prof(dst->ctx, kProfPpoFwdBwd);
+        launch_ppo_tc(ta, 1, s);
+      }
+      PRB_CHECK_LAUNCH();
+      PRB_CUDA(cudaStreamSynchronize(s));
+      PRB_CUDA(cudaMemcpyAsync(ws.stats.p, ws.tc_stats.p, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else if (pgrid > 0 && steps > 0) {
       launch_persistent(p, dst, ws, cfg->entropy_coef, (int64_t)steps, pgrid, s);
       PRB_CUDA(cudaStreamSynchronize(s));
     } else if (steps >= kGraphSteps) {

@@ -13,6 +13,8 @@
 #include <cstring>
 
 #include "policy_internal.h"
+#include <type_traits>
+
 #include "prb_internal.h"
 #include "rollout_pm_tc.h"
 
@@ -290,6 +292,74 @@ int prb_rollout_download(prb_rollout r, double* states, double* actions, double*
       }
     if (bootstrap)
       for (size_t e = 0; e < N; ++e) bootstrap[e] = bt[e];
+  });
+}
+
+int prb_rollout_download_chunks(prb_rollout r, const uint64_t* envs, size_t n_envs, double* states, double* actions,
+                                double* log_probs, double* rewards, uint8_t* dones, double* values, double* bootstrap,
+                                double* raw_advantages, double* returns) {
+  return guard([&] {
+    DeviceScope dev_(r ? r->ctx : nullptr);
+    PRB_REQUIRE(r && (envs || n_envs == 0), PRB_ERR_USAGE, "prb_rollout_download_chunks: NULL argument");
+    PRB_REQUIRE(!(raw_advantages || returns) || r->gae_valid, PRB_ERR_USAGE,
+                "prb_rollout_download_chunks: advantages requested before prb_gae");
+    const size_t N = r->N, H = r->H, S = r->S, A = r->A, Sp = r->Sp;
+    for (size_t i = 0; i < n_envs; ++i)
+      PRB_REQUIRE(envs[i] < N, PRB_ERR_USAGE, "prb_rollout_download_chunks: env index out of range");
+    cudaStream_t s = r->ctx->stream;
+    // one strided copy per (env, field): H rows of w elements at pitch N * w (time-major buffer)
+    auto column = [&](const auto* d, size_t w, size_t e, auto* h) {
+      using T = std::remove_const_t<std::remove_pointer_t<decltype(d)>>;
+      PRB_CUDA(cudaMemcpy2DAsync(h, w * sizeof(T), d + e * w, N * w * sizeof(T), w * sizeof(T), H,
+                                 cudaMemcpyDeviceToHost, s));
+    };
+    std::vector<float> obs(states ? n_envs * H * Sp : 0), act(actions ? n_envs * H * A : 0);
+    std::vector<float> lp(log_probs ? n_envs * H : 0), rw(rewards ? n_envs * H : 0), vl(values ? n_envs * H : 0);
+    std::vector<float> ad(raw_advantages ? n_envs * H : 0), rt(returns ? n_envs * H : 0), bt(bootstrap ? n_envs : 0);
+    std::vector<uint8_t> dn(dones ? n_envs * H : 0);
+    for (size_t i = 0; i < n_envs; ++i) {
+      const size_t e = envs[i];
+      if (states) column(r->d_obs.p, Sp, e, obs.data() + i * H * Sp);
+      if (actions) column(r->d_act.p, A, e, act.data() + i * H * A);
+      if (log_probs) column(r->d_logp.p, 1, e, lp.data() + i * H);
+      if (rewards) column(r->d_rew.p, 1, e, rw.data() + i * H);
+      if (values) column(r->d_val.p, 1, e, vl.data() + i * H);
+      if (dones) column(r->d_done.p, 1, e, dn.data() + i * H);
+      if (raw_advantages) column(r->d_adv.p, 1, e, ad.data() + i * H);
+      if (returns) column(r->d_ret.p, 1, e, rt.data() + i * H);
+      if (bootstrap) PRB_CUDA(cudaMemcpyAsync(bt.data() + i, r->d_boot.p + e, sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<int32_t> rows;
+    std::vector<float> feat;
+    const size_t F = 5 * (size_t)r->K;
+    if (states && r->obs_mode == 1) {
+      rows.resize(H);
+      PRB_CUDA(cudaMemcpyAsync(rows.data(), r->d_row.p, H * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      r->ctx->sync();
+      int32_t tmax = 0;
+      for (int32_t t : rows) tmax = std::max(tmax, t);
+      feat.resize((size_t)(tmax + 1) * F);
+      PRB_CUDA(cudaMemcpyAsync(feat.data(), r->d_feat, feat.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    r->ctx->sync();
+    for (size_t i = 0; i < n_envs; ++i)
+      for (size_t h = 0; h < H; ++h) {
+        const size_t j = i * H + h;  // output row: chunk i, step h (the reference's e*H + h order)
+        if (states) {
+          for (size_t c = 0; c < Sp; ++c) states[j * S + c] = obs[j * Sp + c];
+          if (r->obs_mode == 1)
+            for (size_t c = 0; c < F; ++c) states[j * S + Sp + c] = feat[(size_t)rows[h] * F + c];
+        }
+        if (actions)
+          for (size_t c = 0; c < A; ++c) actions[j * A + c] = act[j * A + c];
+        if (log_probs) log_probs[j] = lp[j];
+        if (rewards) rewards[j] = rw[j];
+        if (values) values[j] = vl[j];
+        if (dones) dones[j] = dn[j];
+        if (raw_advantages) raw_advantages[j] = ad[j];
+        if (returns) returns[j] = rt[j];
+      }
+    for (size_t i = 0; i < n_envs && bootstrap; ++i) bootstrap[i] = bt[i];
   });
 }
 

@@ -25,6 +25,7 @@
 #include "rng.cuh"
 #include "rollout_pm_tc.h"
 #include "tc.cuh"
+#include "tmap.h"
 
 namespace prb {
 namespace {
@@ -511,27 +512,9 @@ void launch_pm_pack(const float* params, const PmPackOffsets& o, uint8_t* pack, 
 }
 
 // The pack as a 2-D bf16 tensor [kPmPackBytes / 256 rows][128], boxes of [16 rows][128] = 4 KB
-// (every half chunk is a whole number of boxes).  cuTensorMapEncodeTiled through the runtime's
-// driver entry point (no -lcuda).
+// (every half chunk is a whole number of boxes).
 void encode_pm_pack_map(CUtensorMap* map, const uint8_t* pack) {
-  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static const Fn fn = [] {  // thread-safe one-time lookup
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    PRB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    PRB_REQUIRE(p && q == cudaDriverEntryPointSuccess, PRB_ERR_CUDA, "cuTensorMapEncodeTiled not available");
-    return reinterpret_cast<Fn>(p);
-  }();
-  const cuuint64_t dims[2] = {128, kPmPackBytes / 256};
-  const cuuint64_t strides[1] = {256};
-  const cuuint32_t box[2] = {128, 16};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint8_t*>(pack), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  PRB_REQUIRE(r == CUDA_SUCCESS, PRB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  encode_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, pack, 128, kPmPackBytes / 256, 256, 128, 16);
 }
 
 // PRB_PM_PAIR=1 selects the CTA-pair kernel; the single-CTA kernel is the default because it is

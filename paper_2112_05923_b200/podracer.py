@@ -344,6 +344,10 @@ class Agent:
         """adam_step (nn.hpp:164-182) with device fp32 gradients at address d_grads."""
         self.ctx.lib.prb_adam_step_device(self.h, C.c_void_p(d_grads))
 
+    def set_ppo_mode(self, mode: int):
+        """1: tensor-core PPO update where the shapes allow (default); 0: fp32 SIMT update."""
+        self.ctx.lib.prb_agent_set_ppo_mode(self.h, int(mode))
+
     def mutate(self, mutation_seed: int, sigma: float):
         self.ctx.lib.prb_agent_mutate(self.h, mutation_seed, sigma)
 
@@ -469,6 +473,28 @@ class Rollout:
                                                     for k in ("states", "actions", "log_probs", "rewards", "dones",
                                                               "values", "bootstrap")])
         return out
+
+    def download_chunks(self, envs, advantages: bool = False):
+        """The chunks of the selected envs only (rows e*H..e*H+H-1 of each env e, pod.hpp:89-94),
+        in the order given; raw (un-normalised) GAE advantages/returns when `advantages`."""
+        envs = np.ascontiguousarray(envs, dtype=np.uint64)
+        n, S, A = envs.size * self.H, self.S, self.A
+        out = dict(states=np.zeros((n, S)), actions=np.zeros((n, A)), log_probs=np.zeros(n), rewards=np.zeros(n),
+                   dones=np.zeros(n, dtype=np.uint8), values=np.zeros(n), bootstrap=np.zeros(envs.size))
+        if advantages:
+            out.update(raw_advantages=np.zeros(n), returns=np.zeros(n))
+        keys = ("states", "actions", "log_probs", "rewards", "dones", "values", "bootstrap", "raw_advantages",
+                "returns")
+        self.ctx.lib.prb_rollout_download_chunks(
+            self.h, _p(envs, C.c_uint64), envs.size,
+            *[_p(out[k], C.c_uint8 if k == "dones" else C.c_double) if k in out else None for k in keys])
+        return out
+
+    def gae_stats(self):
+        """(mean, denom) of the last buffer_advantages normalisation (ppo.hpp:234-242)."""
+        m, d = C.c_double(), C.c_double()
+        self.ctx.lib.prb_gae_stats(self.h, C.byref(m), C.byref(d))
+        return m.value, d.value
 
     def upload(self, states, actions, log_probs, rewards, dones, values, bootstrap):
         arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (states, actions, log_probs, rewards)]

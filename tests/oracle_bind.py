@@ -79,6 +79,7 @@ def load_oracle():
     lib.orc_pointmass_step.argtypes = [D, D, C.c_uint64, D, D, I32]
     lib.orc_pointmass_reset.argtypes = [C.POINTER(MT64), D]
     lib.orc_pm_vec_reset.argtypes = [C.c_size_t, C.c_uint64, C.POINTER(MT64), D, U64, D]
+    lib.orc_pm_vec_reset_subset.argtypes = [C.c_size_t, U64, C.c_uint64, C.POINTER(MT64), D, U64, D]
     lib.orc_pm_vec_step.argtypes = [C.c_size_t, C.POINTER(MT64), D, U64, D, D, D, U8, D, D, U64]
     lib.orc_mlp_param_count.restype = C.c_size_t
     lib.orc_mlp_param_count.argtypes = [SZ, C.c_int]
