@@ -228,10 +228,13 @@ int prb_agent_create(prb_ctx ctx, size_t S, size_t A, const size_t* hidden, int 
     a->A = A;
     a->hidden.assign(hidden, hidden + nh);
     layout(a);
-    a->d_params.alloc(a->P);
-    a->d_m.alloc(a->P);
-    a->d_v.alloc(a->P);
-    a->d_grads.alloc(a->P);
+    // rounded up to whole 16-byte blocks (zero padding): the tensor-core PPO update bulk-copies
+    // parameter slices whose ends are 16-byte aligned
+    const size_t Palloc = (a->P + 3) & ~size_t(3);
+    a->d_params.alloc(Palloc);
+    a->d_m.alloc(Palloc);
+    a->d_v.alloc(Palloc);
+    a->d_grads.alloc(Palloc);
     a->d_t.alloc(1);
     a->d_status.alloc(4);
     // on the agent's (non-blocking) stream, then waited: a legacy-stream cudaMemset would not be

@@ -1328,6 +1328,8 @@ struct PpoWorkspace {
   DevBuf<float> tc_slab;
   DevBuf<double> tc_stats;
   DevBuf<PpoTcChain> tc_chain;
+  DevBuf<int2> tc_pos;  // weight-image position of every parameter (for the net shape below)
+  std::vector<int> tc_pos_key;
 };
 
 PpoArgs make_args(prb_agent a, prb_rollout r, const prb_ppo_config* cfg, uint64_t seed, PpoWorkspace& ws, int mb) {
@@ -1562,14 +1564,14 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
 
 // The tensor-core update (ppo_tc.cu) covers the stock-pod nets: actor S-64-64-A, critic
 // S-64-64-1 with A <= 32, minibatches of <= 1,024 rows (<= 8 CTAs of 128 rows per cluster), and
-// inputs that fit its 192-column X tile (<= 32 private features + <= 159 others + the ones column).
+// inputs that fit its 192-column X tile (<= 32 private features + <= 156 others + the ones column).
 bool ppo_tc_supported(prb_agent a, prb_rollout r, int mb, int mode) {
   if (mode != 1) return false;
   const std::vector<size_t> ad = {a->S, 64, 64, a->A}, cd = {a->S, 64, 64, 1};
   if (a->adims != ad || a->cdims != cd || a->A > 32 || mb > kPpoTcMaxRows || mb < 1) return false;
   const size_t nrest = r->obs_mode == 1 ? 5 * (size_t)r->K : a->S - std::min<size_t>(a->S, 32);
   const size_t npriv = r->obs_mode == 1 ? r->Sp : std::min<size_t>(a->S, 32);
-  return npriv <= 32 && nrest <= 159;
+  return npriv <= 32 && nrest <= 156;  // X and the fp32 gather staging fit (ppo_tc.cu)
 }
 
 PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspace& ws, int64_t steps,
@@ -1617,6 +1619,15 @@ PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspac
   ws.tc_chain.ensure(1);
   PRB_CUDA(cudaMemsetAsync(ws.tc_img.p, 0, kPpoTcImgBytes, s));  // padding of the operand blocks
   PRB_CUDA(cudaMemsetAsync(ws.tc_stats.p, 0, 4 * sizeof(double), s));
+  {  // image positions depend only on the net layout: computed once per workspace and shape
+    const std::vector<int> key = {t.S, t.A, t.P, t.npriv, t.nrest, t.a_w[0], t.c_w[0]};
+    if (ws.tc_pos_key != key) {
+      ws.tc_pos.ensure((size_t)t.P);
+      ppo_tc_image_positions(t, ws.tc_pos.p, s);
+      ws.tc_pos_key = key;
+    }
+    t.imgpos = ws.tc_pos.p;
+  }
   PpoTcChain c{};
   c.params = a->d_params.p;
   c.m = a->d_m.p;
@@ -1748,15 +1759,33 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     const int pgrid = persistent_grid(p, dst, ws);
     if (steps > 0 && ppo_tc_supported(dst, r, mb, src->ppo_mode)) {  // one cluster runs the whole chain
       PpoTcArgs ta = make_tc_args(p, dst, r, ws, (int64_t)steps, p.perm, s);
+      const char* tpath = debug_env("PRB_PPO_TC_TRACE");  // debug: phase marks of one step
+      DevBuf<unsigned long long> tbuf;
+      if (tpath) {
+        tbuf.alloc(32);
+        PRB_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes(), s));
+        ta.trace = tbuf.p;
+      }
       {
         ProfScope prof(dst->ctx, kProfPpoFwdBwd);
         launch_ppo_tc(ta, 1, s);
       }
       PRB_CHECK_LAUNCH();
       PRB_CUDA(cudaStreamSynchronize(s));
+      if (tpath) {
+        unsigned long long h[32];
+        PRB_CUDA(cudaMemcpy(h, tbuf.p, sizeof(h), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(tpath, "w")) {
+          for (int i = 0; i < 32; ++i) fprintf(f, "%d %lld\n", i, h[i] ? (long long)(h[i] - h[0]) : -1LL);
+          fclose(f);
+        }
+      }
       PRB_CUDA(cudaMemcpyAsync(ws.stats.p, ws.tc_stats.p, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s));
     } else if (pgrid > 0 && steps > 0) {
-      launch_persistent(p, dst, ws, cfg->entropy_coef, (int64_t)steps, pgrid, s);
+      {
+        ProfScope prof(dst->ctx, kProfPpoFwdBwd);
+        launch_persistent(p, dst, ws, cfg->entropy_coef, (int64_t)steps, pgrid, s);
+      }
       PRB_CUDA(cudaStreamSynchronize(s));
     } else if (steps >= kGraphSteps) {
       cudaGraph_t graph;

@@ -58,6 +58,7 @@ constexpr int kThreads = 256;
 constexpr int kXC = 192;  // X columns
 constexpr int kHC = 128;  // H1 / H2 / d1 / d2 / d3 columns (actor 0-63 | critic 64-127)
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
+constexpr int kScr = 41;  // fp32 head-epilogue scratch row stride (odd: conflict-free both ways)
 
 // shared-memory map (bytes from the 1024-aligned dynamic base)
 constexpr uint32_t kOffXhi = 0;                        // X_hi   [128][192]            49152
@@ -65,6 +66,7 @@ constexpr uint32_t kOffRB = 49152;                     // X_lo [128][192] | BUF1
 constexpr uint32_t kOffBuf1 = kOffRB;                  // d3 / d1 [128][128]          32768
 constexpr uint32_t kOffBuf2 = kOffRB + 32768;          // d2 [128][128] (+ fp32 reduce scratch)
 constexpr uint32_t kOffRC = kOffRB + 65536;            // W1 image [128 out][192] | H1 [128][128]
+constexpr uint32_t kOffAct = kOffRC + 32768;           // actions [128][32] fp32 (after L1: W1 dead)
 constexpr uint32_t kOffH2 = kOffRC + 49152;            // H2 [128][128]               32768
 constexpr uint32_t kOffRE = kOffH2 + 32768;            // W2a, W2c [64][64], W3a [64][32], W3c [64][16]
 constexpr uint32_t kOffW2a = kOffRE, kOffW2c = kOffRE + 8192, kOffW3a = kOffRE + 16384, kOffW3c = kOffRE + 20480;
@@ -72,6 +74,8 @@ constexpr uint32_t kOffF32 = kOffRE + 22528;           // fp32 block (image tail
 constexpr uint32_t kOffRows = kOffF32 + 1040;          // per-row old_lp, adv, ret, dv [4][128] fp32
 constexpr uint32_t kOffRidx = kOffRows + 2048;         // per-row buffer index [128] u32
 constexpr uint32_t kSmemBytes = kOffRidx + 512;
+constexpr uint32_t kStageBytes = kOffRE;  // X_hi .. H2, dead during the reduction: slice staging
+constexpr uint32_t kOffGather = 98304;    // the next rows' fp32 staging [128][gs] (after X_hi / X_lo)
 // image (global) = W1 block | RE | fp32 block, the smem bytes [kOffRC, +49152) ++ [kOffRE, +23568)
 constexpr uint32_t kImgW1 = 49152, kImgRest = 22528 + 1040;
 static_assert(kImgW1 + kImgRest == (uint32_t)kPpoTcImgBytes, "image size");
@@ -101,6 +105,14 @@ __device__ __forceinline__ void mma_chain(uint32_t d_tmem, uint32_t a_addr, int 
     tc::mma_bf16(d_tmem, ad, bd, idesc, (accumulate || j > 0) ? 1u : 0u);
   }
 }
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
@@ -144,7 +156,7 @@ __device__ __forceinline__ void adam_param(float b1, float b2, float omb1, float
 
 // Where flat parameter p lives in the weight image: *bf16 = byte offset of its bf16 copy (or -1),
 // *f32 / *f32b = float indices into the fp32 block (or -1).
-__device__ __forceinline__ void img_pos(const PpoTcArgs& a, int p, int* bf16, int* f32, int* f32b) {
+__host__ __device__ inline void img_pos(const PpoTcArgs& a, int p, int* bf16, int* f32, int* f32b) {
   *bf16 = -1;
   *f32 = -1;
   *f32b = -1;
@@ -184,33 +196,49 @@ __device__ __forceinline__ void img_pos(const PpoTcArgs& a, int p, int* bf16, in
   if (p >= a.log_std && p < a.log_std + A) *f32 = kFls + (p - a.log_std);
 }
 
-__device__ __forceinline__ void img_store(const PpoTcArgs& a, uint8_t* img, int p, float w) {
-  int b, f, f2;
-  img_pos(a, p, &b, &f, &f2);
-  if (b >= 0) *reinterpret_cast<__nv_bfloat16*>(img + b) = __float2bfloat16_rn(w);
+__device__ __forceinline__ void img_store_at(uint8_t* img, int2 e, float w) {
+  if (e.x >= 0) *reinterpret_cast<__nv_bfloat16*>(img + e.x) = __float2bfloat16_rn(w);
   float* fb = reinterpret_cast<float*>(img + kImgW1 + 22528);
-  if (f >= 0) fb[f] = w;
-  if (f2 >= 0) fb[f2] = w;
+  const int f = e.y & 0xffff, f2 = (e.y >> 16) & 0xffff;
+  if (f != 0xffff) fb[f] = w;
+  if (f2 != 0xffff) fb[f2] = w;
+}
+
+__device__ __forceinline__ void img_store(const PpoTcArgs& a, uint8_t* img, int p, float w) {
+#ifdef PRB_TC_IMGPOS_ONTHEFLY
+  int2 e;
+  {
+    int b, f, f2;
+    img_pos(a, p, &b, &f, &f2);
+    e = make_int2(b, (f < 0 ? 0xffff : f) | ((f2 < 0 ? 0xffff : f2) << 16));
+  }
+#else
+  const int2 e = a.imgpos[p];
+#endif
+  if (e.x >= 0) *reinterpret_cast<__nv_bfloat16*>(img + e.x) = __float2bfloat16_rn(w);
+  float* fb = reinterpret_cast<float*>(img + kImgW1 + 22528);
+  const int f = e.y & 0xffff, f2 = (e.y >> 16) & 0xffff;
+  if (f != 0xffff) fb[f] = w;
+  if (f2 != 0xffff) fb[f2] = w;
 }
 
 // 16 consecutive accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem16(uint32_t taddr, float* v) { tc::tmem_ld16(taddr, v); }
 
-// a row's 64 columns [c0, c0+64) -> tanh(. + add[c]) -> bf16 into an R=128 core-form matrix at col cd
+// a row's 64 accumulator columns -> tanh(. + add[c]) -> bf16 into an R=128 core-form matrix at col cd
 __device__ __forceinline__ void epi_tanh64(uint32_t tl, const float* add, uint8_t* dst, int row, int cd) {
-#pragma unroll 1
-  for (int c = 0; c < 64; c += 16) {
-    float v[16];
-    tmem16(tl + c, v);
-    uint32_t pk[8];
+  float v[64];
+  tc::tmem_ld64(tl, v);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float z0 = v[2 * j], z1 = v[2 * j + 1];
+  for (int c = 0; c < 64; c += 8) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float z0 = v[c + 2 * j], z1 = v[c + 2 * j + 1];
       if (add) tc::add2(z0, z1, add[c + 2 * j], add[c + 2 * j + 1]);
       pk[j] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
     }
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    *reinterpret_cast<uint4*>(dst + core_off(row, cd + c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }
 }
 
@@ -219,21 +247,19 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 
 // delta = D[c] * (1 - h^2) with h the bf16 activations at `hsrc` (same row / columns)
 __device__ __forceinline__ void epi_delta64(uint32_t tl, const uint8_t* hsrc, uint8_t* dst, int row, int cd) {
-#pragma unroll 1
-  for (int c = 0; c < 64; c += 16) {
-    float v[16];
-    tmem16(tl + c, v);
-    const uint4 h0 = *reinterpret_cast<const uint4*>(hsrc + core_off(row, cd + c, 128));
-    const uint4 h1 = *reinterpret_cast<const uint4*>(hsrc + core_off(row, cd + c + 8, 128));
-    const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-    uint32_t pk[8];
+  float v[64];
+  tc::tmem_ld64(tl, v);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+  for (int c = 0; c < 64; c += 8) {
+    const uint4 h0 = *reinterpret_cast<const uint4*>(hsrc + core_off(row, cd + c, 128));
+    const uint32_t hw[4] = {h0.x, h0.y, h0.z, h0.w};
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
       const float a0 = bf_lo(hw[j]), a1 = bf_hi(hw[j]);
-      pk[j] = tc::pack_bf16(v[2 * j] * (1.f - a0 * a0), v[2 * j + 1] * (1.f - a1 * a1));
+      pk[j] = tc::pack_bf16(v[c + 2 * j] * (1.f - a0 * a0), v[c + 2 * j + 1] * (1.f - a1 * a1));
     }
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    *reinterpret_cast<uint4*>(dst + core_off(row, cd + c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }
 }
 
@@ -255,14 +281,25 @@ __device__ __forceinline__ void publish() {
   tc::fence_after_sync();
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t s_mma, s_img;
+  __shared__ __align__(8) uint64_t s_mma, s_mma2, s_img;
   __shared__ uint32_t s_tmem;
   __shared__ uint32_t s_flags[8];  // gate parts of the cluster's CTAs (written over DSMEM)
   __shared__ float s_red[2][40];   // head-epilogue column sums (two row halves)
   __shared__ float s_db3[33];      // column sums of d3 (actor 0..31, critic 32)
+  __shared__ float s_isig[32];     // 1 / sigma_d = exp(-log_std_d) of the step (0 past A)
+  __shared__ double s_lossc[2][8]; // the C CTAs' policy / value loss terms
+  __shared__ uint2 s_next[kRows];  // the next step's rows: (buffer index | ~0, shared-feature row)
   __shared__ double s_loss[3];
+  __shared__ int s_colk[kXC];
+  __shared__ __align__(8) uint64_t s_red_bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C;
   const uint32_t rank = tc::cluster_ctarank();
@@ -280,15 +317,24 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
   if (tid == 0) {
     tc::mbar_init(&s_mma, 1);
+    tc::mbar_init(&s_mma2, 1);
     tc::mbar_init(&s_img, 1);
+    tc::mbar_init(&s_red_bar, 1);
   }
   if (tid < 8) s_flags[tid] = 0;
+  if (tid < kXC) {  // X column -> W1 input row (the ones column -> the bias row S), -1 for padding
+    int k = -1;
+    if (tid < a.npriv) k = tid;
+    else if (tid >= 32 && tid < 32 + a.nrest) k = a.npriv + (tid - 32);
+    else if (tid == a.ones_col) k = a.S;
+    s_colk[tid] = k;
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = s_tmem;
   const uint32_t tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quarter
-  Pipe mma{&s_mma, 0}, imgp{&s_img, 0};
+  Pipe mma{&s_mma, 0}, mma2{&s_mma2, 0}, imgp{&s_img, 0};
 
   // parameter slice of this CTA (reduction / Adam / image entries)
   const int chunk = ((a.P + C - 1) / C + 3) & ~3;
@@ -301,57 +347,86 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   asm volatile("fence.proxy.async.global;" ::: "memory");
   cluster_arrive();
 
-  // gather (gather_minibatch ppo.hpp:83-103) of step st into X_hi / X_lo and the row scalars
-  auto gather = [&](int64_t st) {
-    const int q = tid & 127, hh = tid >> 7;
-    const int qg = (int)rank * kRows + q;
-    const bool valid = qg < a.mb;
-    uint32_t i = 0;
-    const float* prv = nullptr;
-    const float* rest = nullptr;
-    if (valid) {
-      i = mb_index(a, ch, st, (uint32_t)qg);
+  // gather (gather_minibatch ppo.hpp:83-103) of step st into X_hi / X_lo and the row scalars.
+  // Thread (row q, half hh) owns 96 of the 192 X columns; every load is issued before any
+  // conversion (one memory latency per gather, not one per column chunk).
+  // gather (gather_minibatch ppo.hpp:83-103) of step st, in two halves: gather_issue streams
+  // the rows' features (one warp per row: coalesced 4-byte cp.async, no registers held) and row
+  // scalars into an fp32 staging area [128][gs] laid out like the X columns; gather_convert
+  // (after cp.async.wait_all + a barrier) turns it into the bf16 hi / lo X tiles, one row per
+  // thread (conflict-free 16-byte stores).
+  float* gst = reinterpret_cast<float*>(smem + kOffGather);
+  const int gs = (32 + a.nrest + 3) | 1;  // odd row stride: row-per-thread reads are conflict-free
+  // the minibatch rows of step st resolved ahead of time (Feistel / injected permutation and the
+  // shared-feature row, whose dependent loads would otherwise serialise the gather): s_next[q]
+  auto resolve_rows = [&](int64_t st) {
+    if (tid < kRows) {
+      const int qg = (int)rank * kRows + tid;
+      uint2 e = make_uint2(0xffffffffu, 0u);
+      if (qg < a.mb) {
+        e.x = mb_index(a, ch, st, (uint32_t)qg);
+        if (a.obs_mode == 1) e.y = (uint32_t)a.row[e.x / a.N];
+      }
+      s_next[tid] = e;
+    }
+  };
+  auto gather_issue = [&]() {  // the rows in s_next (resolve_rows + a barrier before)
+    for (int q = warp; q < kRows; q += kThreads / 32) {
+      const uint2 e = s_next[q];
+      const bool valid = e.x != 0xffffffffu;
+      if (!valid) {
+        if (lane == 0) ridx[q] = 0xffffffffu;
+        continue;
+      }
+      const uint32_t i = e.x;
+      const float* prv;
+      const float* rest;
       if (a.obs_mode == 1) {
         prv = a.obs + (size_t)i * a.Sp;
-        rest = a.feat + (size_t)a.row[i / a.N] * a.F;
+        rest = a.feat + (size_t)e.y * a.F;
       } else {
         prv = a.obs + (size_t)i * a.S;
         rest = prv + a.npriv;
       }
-    }
-    if (hh == 0) {
-      ridx[q] = valid ? i : 0xffffffffu;
-      const double mean = a.advstat[0], denom = a.advstat[1];
-      rows_f[q] = valid ? a.logp[i] : 0.f;
-      rows_f[128 + q] = valid ? (float)(((double)a.adv[i] - mean) / denom) : 0.f;
-      rows_f[256 + q] = valid ? a.ret[i] : 0.f;
-    }
-#pragma unroll 1
-    for (int ck = hh * 12; ck < hh * 12 + 12; ++ck) {
-      float x[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = ck * 8 + j;
-        float v = 0.f;
-        if (valid) {
-          if (c < 32)
-            v = (c < a.npriv) ? __ldg(prv + c) : 0.f;
-          else if (c < 32 + a.nrest)
-            v = __ldg(rest + (c - 32));
-          else if (c == a.ones_col)
-            v = 1.f;
-        }
-        x[j] = v;
+      float* row = gst + q * gs;
+      for (int k = lane; k < a.npriv; k += 32) cp_async4(row + k, prv + k);
+      for (int k = lane; k < a.nrest; k += 32) cp_async4(row + 32 + k, rest + k);
+      if (lane == 0) {
+        ridx[q] = i;
+        cp_async4(row + gs - 3, a.logp + i);
+        cp_async4(row + gs - 2, a.adv + i);
+        cp_async4(row + gs - 1, a.ret + i);
       }
+    }
+  };
+  auto gather_convert = [&]() {
+    const int q = tid & 127, hh = tid >> 7;
+    const bool valid = ridx[q] != 0xffffffffu;
+    const float* row = gst + q * gs;
+#pragma unroll
+    for (int ck = 0; ck < 12; ++ck) {
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        hi[j] = tc::pack_bf16(x[2 * j], x[2 * j + 1]);
-        lo[j] = tc::pack_bf16(x[2 * j] - bf_lo(hi[j]), x[2 * j + 1] - bf_hi(hi[j]));
+        float x2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = (hh * 12 + ck) * 8 + 2 * j + u;
+          const bool use = valid && (c < a.npriv || (c >= 32 && c < 32 + a.nrest));
+          x2[u] = use ? row[c] : ((valid && c == a.ones_col) ? 1.f : 0.f);
+        }
+        hi[j] = tc::pack_bf16(x2[0], x2[1]);
+        lo[j] = tc::pack_bf16(x2[0] - bf_lo(hi[j]), x2[1] - bf_hi(hi[j]));
       }
-      const uint32_t off = core_off(q, ck * 8, 128);
+      const uint32_t off = core_off(q, (hh * 12 + ck) * 8, 128);
       *reinterpret_cast<uint4*>(smem + kOffXhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(smem + kOffRB + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    if (hh == 0) {
+      const double mean = a.advstat[0], denom = a.advstat[1];
+      rows_f[q] = valid ? row[gs - 3] : 0.f;
+      rows_f[128 + q] = valid ? (float)(((double)row[gs - 2] - mean) / denom) : 0.f;
+      rows_f[256 + q] = valid ? row[gs - 1] : 0.f;
     }
   };
   auto load_image = [&]() {
@@ -366,41 +441,100 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
   };
 
-  gather(0);
+  resolve_rows(0);
+  __syncthreads();
+  gather_issue();
+  cp_async_wait_all();
+  __syncthreads();
+  gather_convert();
   cluster_wait();  // the initial image is complete in global memory
   load_image();
 
   int fail_code = 0, fail_detail = 0;
+  // debug phase trace (PpoTcArgs::trace, PRB_DEBUG_KNOBS builds): globaltimer marks of step 8
+  unsigned long long* trp = (a.trace && rank == 0 && chain_id == 0 && tid == 0) ? a.trace : nullptr;
+  int64_t cur_step = -1;
+#define TCMARK(i)                                   \
+  do {                                              \
+    if (trp && cur_step == 8) trp[(i)] = gtimer(); \
+  } while (0)
+  uint32_t red_phase = 0;  // parity of s_red_bar (one completion per staged piece, across steps)
   for (int64_t st = 0; st < a.steps; ++st) {
+    cur_step = st;
+    TCMARK(0);
     imgp.wait();
+    if (tid < 32) s_isig[tid] = tid < a.A ? __expf(-f32[kFls + tid]) : 0.f;
     publish();  // X (gather) visible to the tensor core
-    // ---- L1: D[0,128) = X_hi . W1 + X_lo . W1 ----
+    TCMARK(1);
+    // ---- L1: D[0,64) = X_hi . W1a + X_lo . W1a, then D[64,128) for the critic (its own commit,
+    // so the actor epilogue overlaps the critic's MMAs) ----
     if (tid == 0) {
-      mma_chain(tbase + 0, sbase + kOffXhi, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 128, false);
-      mma_chain(tbase + 0, sbase + kOffRB, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 128, true);
+      mma_chain(tbase + 0, sbase + kOffXhi, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, false);
+      mma_chain(tbase + 0, sbase + kOffRB, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, true);
       tc::mma_commit(&s_mma);
+      mma_chain(tbase + 64, sbase + kOffXhi, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, false);
+      mma_chain(tbase + 64, sbase + kOffRB, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, true);
+      tc::mma_commit(&s_mma2);
     }
-    mma.wait();
-    // ---- H1 = tanh(D) -> RC (W1 is consumed); ones of nothing: b2 enters in the epilogue ----
-    epi_tanh64(tl + half * 64, nullptr, smem + kOffRC, lrow, half * 64);
+    if (st + 1 < a.steps) resolve_rows(st + 1);  // read by gather_issue at the end of this step
+    // ---- H1 = tanh(D) -> RC once both halves' MMAs are done reading W1 (b1 came with the ones
+    // column; b2 enters in the next epilogue); the rows' actions start streaming into RC's spare
+    // 16 KB (cp.async, consumed by the head epilogue) ----
+    {
+      mma.wait();
+      float hreg[64];
+      if (half == 0) tc::tmem_ld64(tl, hreg);
+      mma2.wait();
+      if (half == 1) tc::tmem_ld64(tl + 64, hreg);
+      TCMARK(2);
+      tc::fence_before_sync();
+      __syncthreads();  // W1 (in RC) is no longer read by the tensor core: H1 may overwrite it
+      {  // actions of this CTA's rows: [128][32] fp32, 8-byte copies (A even) or 4-byte
+        float* sact = reinterpret_cast<float*>(smem + kOffAct);
+        const bool even = (a.A & 1) == 0;
+        const int per = even ? a.A / 2 : a.A;
+        for (int e = tid; e < kRows * per; e += kThreads) {
+          const int r = e / per, k = e - r * per;
+          const uint32_t i = ridx[r];
+          if (i == 0xffffffffu) continue;
+          const float* src = a.act + (size_t)i * a.A;
+          if (even)
+            cp_async8(sact + r * 32 + 2 * k, src + 2 * k);
+          else
+            cp_async4(sact + r * 32 + k, src + k);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 64; c += 8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pk[j] = tc::pack_bf16(tc::tanh_fast(hreg[c + 2 * j]), tc::tanh_fast(hreg[c + 2 * j + 1]));
+        *reinterpret_cast<uint4*>(smem + kOffRC + core_off(lrow, half * 64 + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
     publish();
+    TCMARK(3);
     if (tid == 0) {  // L2 actor / critic (W2 read MN-major: K = its rows = inputs)
       mma_chain(tbase + 128, sbase + kOffRC, 128, 0, sbase + kOffW2a, 64, 1, 4, 64, false);
       mma_chain(tbase + 192, sbase + kOffRC + 16384, 128, 0, sbase + kOffW2c, 64, 1, 4, 64, false);
       tc::mma_commit(&s_mma);
     }
     mma.wait();
+    TCMARK(4);
     epi_tanh64(tl + 128 + half * 64, f32 + kFb2 + half * 64, smem + kOffH2, lrow, half * 64);
+    cp_async_wait_all();  // the action copies (visible to every thread after the barrier)
     publish();
+    TCMARK(5);
     if (tid == 0) {  // heads: actor N = 32, critic N = 16 (column 0 used)
       mma_chain(tbase + 256, sbase + kOffH2, 128, 0, sbase + kOffW3a, 64, 1, 4, 32, false);
       mma_chain(tbase + 288, sbase + kOffH2 + 16384, 128, 0, sbase + kOffW3c, 64, 1, 4, 16, false);
       tc::mma_commit(&s_mma);
     }
     mma.wait();
+    TCMARK(6);
     // ---- head gradients (detail::ppo_loss_grads ppo.hpp:126-167), one row per thread ----
     {
-      float* scr = reinterpret_cast<float*>(smem + kOffBuf2);  // [128][40] fp32: dlog_std terms, losses
+      float* scr = reinterpret_cast<float*>(smem + kOffBuf2);  // [128][kScr] fp32: dlog_std terms, losses
       const int r = lrow;
       const bool valid = ridx[r] != 0xffffffffu;
       const float inv_n = 1.f / (float)a.mb;
@@ -411,8 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
         tmem16(tl + 256 + 16, mu + 16);
         float pl = 0.f;
         float g[32];
+        const float* sact = reinterpret_cast<const float*>(smem + kOffAct) + r * 32;
         if (valid) {
-          const float* act = a.act + (size_t)ridx[r] * a.A;
           float lp = 0.f;
           float z[32];
 #pragma unroll
@@ -421,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
             if (d < a.A) {
               const float ls = f32[kFls + d];
               const float m = mu[d] + f32[kFb3a + d];
-              z[d] = (__ldg(act + d) - m) * __expf(-ls);
+              z[d] = (sact[d] - m) * s_isig[d];
               lp += -0.5f * kLogTwoPiF - ls - 0.5f * z[d] * z[d];
             }
           }
@@ -433,18 +567,17 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           const float dl = (s1 <= s2) ? -adv * ratio * inv_n : 0.f;  // ties flow (ppo.hpp:146)
 #pragma unroll
           for (int d = 0; d < 32; ++d) {
-            const float isig = (d < a.A) ? __expf(-f32[kFls + d]) : 0.f;
-            g[d] = dl * z[d] * isig;                        // dL/dmu
-            scr[r * 40 + d] = (d < a.A) ? dl * (z[d] * z[d] - 1.f) : 0.f;  // dL/dlog_std terms
+            g[d] = dl * z[d] * s_isig[d];                                  // dL/dmu
+            scr[r * kScr + d] = (d < a.A) ? dl * (z[d] * z[d] - 1.f) : 0.f;  // dL/dlog_std terms
           }
         } else {
 #pragma unroll
           for (int d = 0; d < 32; ++d) {
             g[d] = 0.f;
-            scr[r * 40 + d] = 0.f;
+            scr[r * kScr + d] = 0.f;
           }
         }
-        scr[r * 40 + 32] = pl;
+        scr[r * kScr + 32] = pl;
 #pragma unroll
         for (int c = 0; c < 32; c += 8) {
           uint32_t pk[4];
@@ -462,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           dv = a.vf * 2.f * err * inv_n;
         }
         rows_f[384 + r] = dv;
-        scr[r * 40 + 33] = vl;
+        scr[r * kScr + 33] = vl;
         // d3 columns [32, 128): dV in column 32, zeros
 #pragma unroll
         for (int c = 32; c < 128; c += 8) {
@@ -472,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       }
     }
     publish();
+    TCMARK(7);
     // ---- d2a = d3a . W3a^T (K-major W3a: N = its rows); dW3^T = d3^T . H2 (both MN-major) ----
     if (tid == 0) {
       mma_chain(tbase + 256, sbase + kOffBuf1, 128, 0, sbase + kOffW3a, 64, 0, 2, 64, false);
@@ -485,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       if (tid < 68) {
         const int c = tid % 34, hh = tid / 34;
         float s = 0.f;
-        for (int r = hh * 64; r < hh * 64 + 64; ++r) s += scr[r * 40 + c];
+        for (int r = hh * 64; r < hh * 64 + 64; ++r) s += scr[r * kScr + c];
         s_red[hh][c] = s;
       } else if (tid >= 128 && tid < 128 + 33) {
         const int c = tid - 128;
@@ -496,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       }
     }
     mma.wait();
+    TCMARK(8);
     __syncthreads();  // s_red complete; the scratch in BUF2 is dead
     // ---- d2 = (.) o (1 - H2^2): actor from TMEM, critic as dV x w3c ----
     if (half == 0) {
@@ -517,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       }
     }
     publish();
+    TCMARK(9);
     // ---- d1 pre-activations = d2 . W2^T (K-major W2: N = its rows); dW2^T = d2^T . H1 ----
     if (tid == 0) {
       mma_chain(tbase + 320, sbase + kOffBuf2, 128, 0, sbase + kOffW2a, 64, 0, 4, 64, false);
@@ -525,109 +661,239 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       tc::mma_commit(&s_mma);
     }
     mma.wait();
+    TCMARK(10);
     epi_delta64(tl + 320 + half * 64, smem + kOffRC, smem + kOffBuf1, lrow, half * 64);
     publish();
+    TCMARK(11);
     if (tid == 0) {  // dW1^T = d1^T . X_hi
       mma_chain(tbase + 256, sbase + kOffBuf1, 128, 1, sbase + kOffXhi, 128, 1, 8, 192, false);
       tc::mma_commit(&s_mma);
     }
+    // db2 = column sums of d2 (BUF2, bf16, as dW2 sees them) while dW1 runs -- BUF2 lies inside
+    // the flat staging below, so the sums are held in registers
+    float db2 = 0.f;
+    if (tid < 128)
+      for (int r = 0; r < 128; ++r)
+        db2 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(smem + kOffBuf2 + core_off(r, tid, 128)));
+    __syncthreads();  // BUF2 read completely before the flat staging below overwrites it
     // bias gradients of layers 2 and 3: column sums of d2 (BUF2) and d3 (in BUF1 until dW1's d1
     // overwrote it -- so d3's sums are taken from the per-row values below instead)
     mma.wait();
-    // ---- partials: TMEM -> this CTA's slab row in the flat parameter order ----
-    float* slab = ch.slab + (size_t)rank * a.Pp;
+    TCMARK(12);
+    // ---- partials: TMEM -> shared memory in the flat parameter order (the operand regions are
+    // dead), then ONE bulk store of the CTA's slab row ----
+    float* flat = reinterpret_cast<float*>(smem);  // [Pp] (dead X_hi / RB / RC / H2)
     {
       const int o = lrow;  // TMEM lane = output index (actor 0-63 | critic 64-127; d3: actor 0..A-1, critic 32)
-      // dW3^T [0,128): columns = H2 inputs (actor 0-63, critic 64-127)
-#pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
-        float v[16];
-        tmem16(tl + c0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int k = c0 + j;
-          if (k < 64 && o < a.A) slab[a.a_w[2] + k * a.A + o] = v[j];
-          if (k >= 64 && o == 32) slab[a.c_w[2] + (k - 64)] = v[j];
-        }
-      }
-      // dW2^T [128,256)
-#pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
-        float v[16];
-        tmem16(tl + 128 + c0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int k = c0 + j;
-          if (k < 64 && o < 64) slab[a.a_w[1] + k * 64 + o] = v[j];
-          if (k >= 64 && o >= 64) slab[a.c_w[1] + (k - 64) * 64 + (o - 64)] = v[j];
-        }
-      }
-      // dW1^T [256,448): columns = X columns
-      const int* w1 = (o < 64) ? a.a_w : a.c_w;
       const int oo = o & 63;
-#pragma unroll 1
-      for (int c0 = half * 96; c0 < half * 96 + 96; c0 += 16) {
-        float v[16];
-        tmem16(tl + 256 + c0, v);
+      // dW3^T [0,128): columns = H2 inputs (actor 0-63 | critic 64-127); half h reads its net's
+      // block (tcgen05.ld is warp-collective: every lane loads, the owners store)
+      {
+        const bool mine = half == 0 ? o < a.A : o == 32;
+        float* dst = half == 0 ? flat + a.a_w[2] + o : flat + a.c_w[2];
+        const int stride = half == 0 ? a.A : 1;
+        float v[64];
+        tc::tmem_ld64(tl + half * 64, v);
+        if (mine) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = c0 + j;
-          int k = -1;
-          if (c < a.npriv) k = c;
-          else if (c >= 32 && c < 32 + a.nrest) k = a.npriv + (c - 32);
-          else if (c == a.ones_col) k = a.S;  // the bias b1 follows W1 [S][64]
-          if (k >= 0) slab[w1[0] + k * 64 + oo] = v[j];
+          for (int j = 0; j < 64; ++j) dst[j * stride] = v[j];
+        }
+      }
+      // dW2^T [128,256): the net's block is lanes of that net x its own input columns
+      {
+        const bool mine = (half == 0) == (o < 64);
+        float* dst = (o < 64 ? flat + a.a_w[1] : flat + a.c_w[1]) + oo;
+        float v[64];
+        tc::tmem_ld64(tl + 128 + half * 64, v);
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) dst[j * 64] = v[j];
+        }
+      }
+      // dW1^T [256,448): columns = X columns -> W1 rows (s_colk), the ones column -> b1
+      {
+        float* dst = (o < 64 ? flat + a.a_w[0] : flat + a.c_w[0]) + oo;
+#pragma unroll 1
+        for (int c0 = half * 96; c0 < half * 96 + 96; c0 += 48) {
+          uint32_t r[64];
+          tc::tmem_ld16_nw(tl + 256 + c0, r);
+          tc::tmem_ld16_nw(tl + 256 + c0 + 16, r + 16);
+          tc::tmem_ld16_nw(tl + 256 + c0 + 32, r + 32);
+          tc::tmem_wait_ld64(r);
+#pragma unroll
+          for (int j = 0; j < 48; ++j) {
+            const int k = s_colk[c0 + j];
+            if (k >= 0) dst[k * 64] = __uint_as_float(r[j]);
+          }
         }
       }
     }
-    // db2 = column sums of d2 (BUF2, bf16, as dW2 sees them); db3, dlog_std, losses from above
+    TCMARK(18);
+    tc::fence_before_sync();
+    __syncthreads();  // every flat entry of the TMEM blocks written
     if (tid < 128) {
-      float sum = 0.f;
-      for (int r = 0; r < 128; ++r)
-        sum += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(smem + kOffBuf2 + core_off(r, tid, 128)));
       const int* w2 = (tid < 64) ? a.a_w : a.c_w;
-      slab[w2[1] + 64 * 64 + (tid & 63)] = sum;
+      flat[w2[1] + 64 * 64 + (tid & 63)] = db2;
     } else if (tid < 128 + 34) {
       const int c = tid - 128;
       const float sum = s_red[0][c] + s_red[1][c];
       if (c < a.A) {
-        slab[a.log_std + c] = sum;
-        slab[a.a_w[2] + 64 * a.A + c] = s_db3[c];
+        flat[a.log_std + c] = sum;
+        flat[a.a_w[2] + 64 * a.A + c] = s_db3[c];
       }
       if (c == 32) {
-        slab[a.P] = sum;  // policy loss terms
-        slab[a.c_w[2] + 64] = s_db3[32];
+        flat[a.P] = sum;  // policy loss terms
+        flat[a.c_w[2] + 64] = s_db3[32];
       }
-      if (c == 33) slab[a.P + 1] = sum;  // value loss terms
+      if (c == 33) flat[a.P + 1] = sum;  // value loss terms
     }
+    TCMARK(19);
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)(((a.P + 2 + 3) & ~3) * 4);
+      float* dst = ch.slab + (size_t)rank * a.Pp;
+      constexpr uint32_t kChunk = 32768;
+      for (uint32_t o = 0; o < bytes; o += kChunk) tc::bulk_s2g(reinterpret_cast<uint8_t*>(dst) + o,
+                                                                  reinterpret_cast<const uint8_t*>(flat) + o,
+                                                                  min(kChunk, bytes - o));
+      tc::bulk_commit();
+      TCMARK(20);
+      tc::bulk_wait0();  // complete; then async proxy -> generic proxy before the barrier's release
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    TCMARK(13);
     tc::fence_before_sync();
     cluster_arrive();  // release: this CTA's slab row
     cluster_wait();
-    // ---- reduce this CTA's parameter slice over the C slab rows (rank order), gate, Adam ----
+    TCMARK(14);
+    // ---- reduce this CTA's parameter slice over the C slab rows (rank order), Adam (speculative),
+    // gate.  The slice's C partial rows and its m / v / master weights are staged into shared
+    // memory by bulk copies (the MMA operand regions are dead by now): one L2 round trip.  Adam's
+    // results stay in the staging area and the bf16 image is written at once; one cluster barrier
+    // then both publishes the image and exchanges the gate, and only an accepted step's results
+    // are stored to the master weights / moments (nn.hpp:169-171: a rejected step changes nothing;
+    // the image is rebuilt from the master weights when the next update starts) ----
+    // staging: m, v, w [piece] first, then the C partial rows [piece] (the gather of the next step
+    // streams into kOffGather.. once the partial rows are consumed)
+    const int piece = min(chunk, ((int)(kStageBytes / 4) / (C + 3)) & ~3);
+    float* stw = reinterpret_cast<float*>(smem);  // m, v, w [piece] each
+    float* stg = stw + 3 * (size_t)piece;         // [C][piece] partials; row 0 := the reduced g
     int bad = 0;
-    for (int p = p_lo + tid; p < p_hi; p += kThreads) {
-      float g = 0.f;
-      for (int c = 0; c < C; ++c) g += __ldcg(ch.slab + (size_t)c * a.Pp + p);
-      if (p >= a.log_std && p < a.log_std + a.A) g -= a.ent;  // ppo.hpp:157
-      bad |= !isfinite(g);
-      ch.grads[p] = g;
+    const int npieces = (p_hi > p_lo) ? (p_hi - p_lo + piece - 1) / piece : 0;
+    auto stage = [&](int pc, bool slab_rows, bool state) {
+      if (tid == 0) {
+        const int q0 = p_lo + pc * piece, cnt = min(piece, p_hi - q0);
+        const uint32_t bytes = (uint32_t)(((cnt + 3) & ~3) * 4);
+        tc::fence_proxy_async();  // earlier generic accesses of the staging area
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // the peers' slab rows (acquired by the barrier)
+        tc::mbar_arrive_expect_tx(&s_red_bar, bytes * ((slab_rows ? C : 0) + (state ? 3 : 0)));
+        if (slab_rows)
+          for (int c = 0; c < C; ++c)
+            tc::bulk_g2s(stg + (size_t)c * piece, ch.slab + (size_t)c * a.Pp + q0, bytes, &s_red_bar);
+        if (state) {
+          tc::bulk_g2s(stw, ch.m + q0, bytes, &s_red_bar);
+          tc::bulk_g2s(stw + piece, ch.v + q0, bytes, &s_red_bar);
+          tc::bulk_g2s(stw + 2 * (size_t)piece, ch.params + q0, bytes, &s_red_bar);
+        }
+      }
+      tc::mbar_wait(&s_red_bar, red_phase);
+      red_phase ^= 1;
+    };
+    const float ibc1 = (float)(1.0 / (1.0 - pow(a.b1, (double)(t + 1))));
+    const float ibc2 = (float)(1.0 / (1.0 - pow(a.b2, (double)(t + 1))));
+    auto adam_piece = [&](int pc) {  // staging rows C..C+2 := the updated m, v, w; image entries
+      const int q0 = p_lo + pc * piece, cnt = min(piece, p_hi - q0);
+      constexpr int kB = 8;  // parameters per thread whose image positions are loaded together
+      for (int j0 = 0; j0 < cnt; j0 += kB * kThreads) {
+        int2 pos[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int j = j0 + b * kThreads + tid;
+          pos[b] = (j < cnt) ? __ldg(a.imgpos + q0 + j) : make_int2(-1, -1);
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int j = j0 + b * kThreads + tid;
+          if (j >= cnt) continue;
+          float* sm_ = stw + j;
+          float* sv_ = stw + piece + j;
+          float* sw_ = stw + 2 * (size_t)piece + j;
+          float m = *sm_, v = *sv_, w = *sw_;
+          adam_param(b1, b2, omb1, omb2, ch.lr, a.eps, ibc1, ibc2, stg[j], m, v, w);
+          *sm_ = m;
+          *sv_ = v;
+          *sw_ = w;
+          img_store_at(img, pos[b], w);
+        }
+      }
+    };
+    auto commit_piece = [&](int pc) {  // an accepted step: the staged results to the master copies
+      const int q0 = p_lo + pc * piece, cnt = min(piece, p_hi - q0);
+      for (int j = tid; j < cnt; j += kThreads) {
+        ch.m[q0 + j] = stw[j];
+        ch.v[q0 + j] = stw[piece + j];
+        ch.params[q0 + j] = stw[2 * (size_t)piece + j];
+      }
+    };
+    for (int pc = 0; pc < npieces; ++pc) {
+      stage(pc, true, npieces == 1);
+      TCMARK(21);
+      const int q0 = p_lo + pc * piece, cnt = min(piece, p_hi - q0);
+#pragma unroll 2
+      for (int j = tid; j < cnt; j += kThreads) {
+        float part[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) part[c] = (c < C) ? stg[(size_t)c * piece + j] : 0.f;
+        float g = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < C) g += part[c];  // rank order
+        const int p = q0 + j;
+        if (p >= a.log_std && p < a.log_std + a.A) g -= a.ent;  // ppo.hpp:157
+        bad |= !isfinite(g);
+        stg[j] = g;  // row 0 now holds the reduced gradient
+        ch.grads[p] = g;
+      }
+      if (npieces > 1) {  // Adam + commit need the gate first: the pieces are revisited below
+        __syncthreads();
+      } else {
+        __syncthreads();
+        TCMARK(22);
+        adam_piece(0);
+      }
+    }
+    if (tid >= 64 && tid < 64 + 2 * C) {  // the C CTAs' loss terms, one load each
+      const int c = (tid - 64) >> 1, which = (tid - 64) & 1;
+      s_lossc[which][c] = (double)__ldcg(ch.slab + (size_t)c * a.Pp + a.P + which);
     }
     bad = __syncthreads_or(bad);
+    TCMARK(15);
     if (tid == 0) {  // this CTA's gradient verdict to every CTA of the cluster (DSMEM)
       for (int c = 0; c < C; ++c) st_cluster_u32(tc::mapa_shared(&s_flags[rank], (uint32_t)c), (uint32_t)bad);
       // losses (every CTA sums them in the same order) -- the reference checks these first
       double pl = 0.0, vl = 0.0, en = 0.0;
       for (int c = 0; c < C; ++c) {
-        pl += (double)__ldcg(ch.slab + (size_t)c * a.Pp + a.P);
-        vl += (double)__ldcg(ch.slab + (size_t)c * a.Pp + a.P + 1);
+        pl += s_lossc[0][c];
+        vl += s_lossc[1][c];
       }
       for (int d = 0; d < a.A; ++d) en += 0.5 * (1.8378770664093454836 + 1.0) + (double)f32[kFls + d];  // nn.hpp:273-277
       s_loss[0] = pl;
       s_loss[1] = vl;
       s_loss[2] = en;
     }
+    TCMARK(23);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the image entries, to the next bulk copies
+    TCMARK(24);
+    const bool more = st + 1 < a.steps;
+    // the next rows' copies fly across the barrier when the staged m / v / w leave the gather
+    // area free (one piece, i.e. >= 5 CTAs per cluster at the stock pod's size)
+    const bool early = npieces == 1 && 3 * piece * 4 <= (int)kOffGather;
+    if (more && early) gather_issue();
+    TCMARK(25);
     cluster_arrive();
     cluster_wait();
+    TCMARK(16);
     {
       const double pl = s_loss[0], vl = s_loss[1], en = s_loss[2];
       int code = 0, detail = 0;
@@ -651,23 +917,32 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       }
     }
     ++t;
-    {
-      const float ibc1 = (float)(1.0 / (1.0 - pow(a.b1, (double)t)));
-      const float ibc2 = (float)(1.0 / (1.0 - pow(a.b2, (double)t)));
-      for (int p = p_lo + tid; p < p_hi; p += kThreads) {
-        float m = ch.m[p], v = ch.v[p], w = ch.params[p];
-        adam_param(b1, b2, omb1, omb2, ch.lr, a.eps, ibc1, ibc2, ch.grads[p], m, v, w);
-        ch.m[p] = m;
-        ch.v[p] = v;
-        ch.params[p] = w;
-        img_store(a, img, p, w);
+    if (npieces == 1) {
+      commit_piece(0);
+    } else {  // large slices (few CTAs): re-stage the gradient and state piece by piece
+      for (int pc = 0; pc < npieces; ++pc) {
+        const int q0 = p_lo + pc * piece, cnt = min(piece, p_hi - q0);
+        stage(pc, false, true);
+        for (int j = tid; j < cnt; j += kThreads) stg[j] = __ldcg(ch.grads + q0 + j);
+        __syncthreads();
+        adam_piece(pc);
+        __syncthreads();
+        commit_piece(pc);
+        __syncthreads();
       }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      cluster_arrive();  // these image entries were written after the gate
+      cluster_wait();
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    cluster_arrive();  // the slice's image entries
-    if (st + 1 < a.steps) gather(st + 1);  // overlaps the barrier
-    cluster_wait();
-    if (st + 1 < a.steps) load_image();
+    __syncthreads();  // the staging area is free: the next X tiles and the image may land
+    if (more) {
+      if (!early) gather_issue();
+      cp_async_wait_all();
+      __syncthreads();
+      gather_convert();
+      load_image();
+    }
+    TCMARK(17);
   }
   if (rank == 0 && tid == 0) {
     *ch.t = t;
@@ -685,6 +960,21 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
 }  // namespace
 
 size_t ppo_tc_smem_bytes() { return kSmemBytes; }
+
+namespace {
+__global__ void ppo_tc_pos_kernel(const PpoTcArgs a, int2* out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.P; p += gridDim.x * blockDim.x) {
+    int b, f, f2;
+    img_pos(a, p, &b, &f, &f2);
+    out[p] = make_int2(b, (f < 0 ? 0xffff : f) | ((f2 < 0 ? 0xffff : f2) << 16));
+  }
+}
+}  // namespace
+
+void ppo_tc_image_positions(const PpoTcArgs& a, int2* d_out, cudaStream_t s) {
+  ppo_tc_pos_kernel<<<(a.P + 255) / 256, 256, 0, s>>>(a, d_out);
+  PRB_CHECK_LAUNCH();
+}
 
 void launch_ppo_tc(const PpoTcArgs& a, int nchains, cudaStream_t s) {
   ensure_smem(ppo_tc_kernel, kSmemBytes);

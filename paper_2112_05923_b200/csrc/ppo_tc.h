@@ -46,12 +46,17 @@ struct PpoTcArgs {
   float clip, ent, vf;
   double b1, b2;
   float eps;
+  const int2* imgpos;  // [P] weight-image position of each flat parameter (ppo_tc_image_positions)
+  unsigned long long* trace;  // debug: [18] globaltimer phase marks of step 8 (null: off)
 };
 
 constexpr int kPpoTcImgBytes = 72720;
 constexpr int kPpoTcMaxRows = 1024;  // 8 CTAs x 128 rows
 
 size_t ppo_tc_smem_bytes();
+// Per flat parameter: .x = byte offset of its bf16 copy in the weight image (-1: none), .y = the
+// float indices of its fp32 copies in the image's fp32 block, (first | second << 16), 0xffff = none.
+void ppo_tc_image_positions(const PpoTcArgs& a, int2* d_out, cudaStream_t s);
 void launch_ppo_tc(const PpoTcArgs& a, int nchains, cudaStream_t s);
 
 }  // namespace prb

@@ -38,9 +38,14 @@ cfg = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=n, learni
 CLIP = float(sys.argv[2]) if len(sys.argv) > 2 else 0.2
 cfg1 = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=n, learning_rate=0.0, clip_eps=CLIP)
 out = pr.Agent(ctx, S, K)
-new, st = pr.ppo_update(agent, ro, cfg1, 3, perm=perm, out=out)
+try:
+    new, st = pr.ppo_update(agent, ro, cfg1, 3, perm=perm, out=out)
+except pr.NumericError as ex:
+    print("NumericError", ex, "accepted steps", out.get()[3])
+    st = None
 g = np.zeros(agent.param_count)
 ctx.lib.prb_debug_agent_grads(out.h, g.ctypes.data_as(C.POINTER(C.c_double)))
+print("non-finite grads:", int(np.sum(~np.isfinite(g))), "first idx", np.where(~np.isfinite(g))[0][:20])
 # the last step's rows are perm[(nmb-1)*mb : nmb*mb]
 nmb = n // mb
 rows = perm[(nmb - 1) * mb: nmb * mb]
