@@ -160,6 +160,8 @@ SIGNATURES = {
     "prb_compute_gae": (I, [P, P, P, P, P, SZ, SZ, D, D, P, P]),
     "prb_ppo_update": (I, [P, P, C.POINTER(PpoConfig), U64, pU64, P, C.POINTER(PpoStats)]),
     "prb_ppo_loss_grads": (I, [P, P, pU64, SZ, C.POINTER(PpoConfig), pD, pD]),
+    "prb_ppo_update_learners": (I, [C.POINTER(P), C.POINTER(P), SZ, C.POINTER(PpoConfig), pU64, C.POINTER(P),
+                                    C.POINTER(PpoStats)]),
     "prb_adam_step_host": (I, [P, pD]),
     "prb_adam_step_device": (I, [P, P]),
     "prb_evaluate": (I, [P, P, U64, I, pD, pD, pD, pU64]),

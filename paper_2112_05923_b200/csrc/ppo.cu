@@ -1574,8 +1574,10 @@ bool ppo_tc_supported(prb_agent a, prb_rollout r, int mb, int mode) {
   return npriv <= 32 && nrest <= 156;  // X and the fp32 gather staging fit (ppo_tc.cu)
 }
 
-PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspace& ws, int64_t steps,
-                       const uint32_t* perm, cudaStream_t s) {
+// The launch-wide part of the tensor-core update (net layout, buffer shape, schedule); the image
+// position table lives in `ws` (computed once per workspace and shape).
+PpoTcArgs make_tc_shape(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspace& ws, int64_t steps,
+                        cudaStream_t s) {
   PpoTcArgs t{};
   t.S = p.S;
   t.A = p.A;
@@ -1592,14 +1594,6 @@ PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspac
   t.npriv = r->obs_mode == 1 ? (int)r->Sp : std::min(p.S, 32);
   t.nrest = r->obs_mode == 1 ? t.F : p.S - t.npriv;
   t.ones_col = 32 + t.nrest;
-  t.obs = p.obs;
-  t.row = p.row;
-  t.feat = p.feat;
-  t.act = p.act;
-  t.logp = p.logp;
-  t.adv = p.adv;
-  t.ret = p.ret;
-  t.advstat = p.advstat;
   t.N = p.N;
   t.n = p.n;
   t.nmb = p.nmb;
@@ -1613,38 +1607,55 @@ PpoTcArgs make_tc_args(const PpoArgs& p, prb_agent a, prb_rollout r, PpoWorkspac
   t.b1 = a->beta1;
   t.b2 = a->beta2;
   t.eps = (float)a->eps;
+  const std::vector<int> key = {t.S, t.A, t.P, t.npriv, t.nrest, t.a_w[0], t.c_w[0]};
+  if (ws.tc_pos_key != key) {
+    ws.tc_pos.ensure((size_t)t.P);
+    ppo_tc_image_positions(t, ws.tc_pos.p, s);
+    ws.tc_pos_key = key;
+  }
+  t.imgpos = ws.tc_pos.p;
+  return t;
+}
+
+// One learner of a tensor-core launch: its agent (dst, trained in place), its workspace and buffer.
+PpoTcChain make_tc_chain(const PpoTcArgs& t, prb_agent dst, prb_rollout r, PpoWorkspace& ws, const uint32_t* perm,
+                         uint64_t seed, cudaStream_t s) {
   ws.tc_img.ensure(kPpoTcImgBytes);
   ws.tc_slab.ensure((size_t)t.C * t.Pp);
   ws.tc_stats.ensure(4);
-  ws.tc_chain.ensure(1);
   PRB_CUDA(cudaMemsetAsync(ws.tc_img.p, 0, kPpoTcImgBytes, s));  // padding of the operand blocks
   PRB_CUDA(cudaMemsetAsync(ws.tc_stats.p, 0, 4 * sizeof(double), s));
-  {  // image positions depend only on the net layout: computed once per workspace and shape
-    const std::vector<int> key = {t.S, t.A, t.P, t.npriv, t.nrest, t.a_w[0], t.c_w[0]};
-    if (ws.tc_pos_key != key) {
-      ws.tc_pos.ensure((size_t)t.P);
-      ppo_tc_image_positions(t, ws.tc_pos.p, s);
-      ws.tc_pos_key = key;
-    }
-    t.imgpos = ws.tc_pos.p;
-  }
   PpoTcChain c{};
-  c.params = a->d_params.p;
-  c.m = a->d_m.p;
-  c.v = a->d_v.p;
-  c.t = a->d_t.p;
-  c.grads = a->d_grads.p;
+  c.params = dst->d_params.p;
+  c.m = dst->d_m.p;
+  c.v = dst->d_v.p;
+  c.t = dst->d_t.p;
+  c.grads = dst->d_grads.p;
   c.img = ws.tc_img.p;
   c.slab = ws.tc_slab.p;
   c.stats = ws.tc_stats.p;
-  c.status = a->d_status.p;
+  c.status = dst->d_status.p;
   c.perm = perm;
-  c.seed = p.seed;
-  c.lr = (float)a->lr;
-  PRB_CUDA(cudaMemcpyAsync(ws.tc_chain.p, &c, sizeof(c), cudaMemcpyHostToDevice, s));
-  PRB_CUDA(cudaStreamSynchronize(s));  // c lives on this stack frame
-  t.chains = ws.tc_chain.p;
-  return t;
+  c.seed = seed;
+  c.lr = (float)dst->lr;
+  c.obs = r->d_obs.p;
+  c.row = r->d_row.p;
+  c.feat = r->d_feat;
+  c.act = r->d_act.p;
+  c.logp = r->d_logp.p;
+  c.adv = r->d_adv.p;
+  c.ret = r->d_ret.p;
+  c.advstat = r->d_advstat.p;
+  return c;
+}
+
+// Uploads the chain descriptors into `buf` and points t at them (synchronous: the host vector
+// may die on return).
+void upload_chains(PpoTcArgs& t, const std::vector<PpoTcChain>& chains, DevBuf<PpoTcChain>& buf, cudaStream_t s) {
+  buf.ensure(chains.size());
+  PRB_CUDA(cudaMemcpyAsync(buf.p, chains.data(), chains.size() * sizeof(PpoTcChain), cudaMemcpyHostToDevice, s));
+  PRB_CUDA(cudaStreamSynchronize(s));
+  t.chains = buf.p;
 }
 
 std::string status_message(int detail) {
@@ -1758,7 +1769,8 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     const size_t kGraphSteps = 32;
     const int pgrid = persistent_grid(p, dst, ws);
     if (steps > 0 && ppo_tc_supported(dst, r, mb, src->ppo_mode)) {  // one cluster runs the whole chain
-      PpoTcArgs ta = make_tc_args(p, dst, r, ws, (int64_t)steps, p.perm, s);
+      PpoTcArgs ta = make_tc_shape(p, dst, r, ws, (int64_t)steps, s);
+      upload_chains(ta, {make_tc_chain(ta, dst, r, ws, p.perm, p.seed, s)}, ws.tc_chain, s);
       const char* tpath = debug_env("PRB_PPO_TC_TRACE");  // debug: phase marks of one step
       DevBuf<unsigned long long> tbuf;
       if (tpath) {
@@ -1835,6 +1847,103 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
       }
       throw;
     }
+  });
+}
+
+int prb_ppo_update_learners(const prb_agent* srcs, const prb_rollout* rollouts, size_t L, const prb_ppo_config* cfg,
+                            const uint64_t* seeds, const prb_agent* dsts, prb_ppo_stats* stats) {
+  return guard([&] {
+    PRB_REQUIRE(srcs && rollouts && cfg && seeds && dsts && L > 0, PRB_ERR_USAGE, "ppo_update_learners: NULL argument");
+    DeviceScope dev_(dsts[0] ? dsts[0]->ctx : nullptr);
+    PRB_REQUIRE(cfg->gamma > 0.0 && cfg->gamma <= 1.0, PRB_ERR_CONFIG, "ppo.gamma must be in (0, 1]");
+    PRB_REQUIRE(cfg->gae_lambda >= 0.0 && cfg->gae_lambda <= 1.0, PRB_ERR_CONFIG, "ppo.gae_lambda must be in [0, 1]");
+    PRB_REQUIRE(cfg->clip_eps > 0.0, PRB_ERR_CONFIG, "ppo.clip_eps must be > 0");
+    PRB_REQUIRE(cfg->minibatch_size > 0 && cfg->minibatch_size <= cfg->buffer_size, PRB_ERR_CONFIG,
+                "ppo.minibatch_size must be in [1, buffer_size]");
+    const prb_rollout r0 = rollouts[0];
+    PRB_REQUIRE(r0, PRB_ERR_USAGE, "ppo_update_learners: NULL rollout");
+    const size_t n = r0->N * r0->H;
+    for (size_t l = 0; l < L; ++l) {
+      const prb_agent src = srcs[l], dst = dsts[l];
+      const prb_rollout r = rollouts[l];
+      PRB_REQUIRE(src && dst && r && src != dst, PRB_ERR_USAGE, "ppo_update_learners: NULL or aliased agent");
+      PRB_REQUIRE(r->full, PRB_ERR_USAGE, "ppo_update: buffer has 0 of " + std::to_string(r->N * r->H) + " transitions");
+      PRB_REQUIRE(r->N == r0->N && r->H == r0->H && r->S == r0->S && r->A == r0->A && r->obs_mode == r0->obs_mode &&
+                      r->K == r0->K,
+                  PRB_ERR_USAGE, "ppo_update_learners: rollout buffers of different shapes");
+      PRB_REQUIRE(src->adims == dst->adims && src->cdims == dst->cdims && src->S == r->S && src->A == r->A &&
+                      dst->ctx->device == dsts[0]->ctx->device,
+                  PRB_ERR_USAGE, "ppo_update_learners: agent/buffer shapes or devices disagree");
+      for (size_t k = 0; k < l; ++k)
+        PRB_REQUIRE(dsts[k] != dst, PRB_ERR_USAGE, "ppo_update_learners: a destination agent appears twice");
+    }
+    PRB_REQUIRE(n >= cfg->minibatch_size, PRB_ERR_USAGE,
+                "ppo_update: buffer length " + std::to_string(n) + " shorter than minibatch_size " +
+                    std::to_string(cfg->minibatch_size));
+    const int mb = (int)cfg->minibatch_size;
+    PRB_REQUIRE(ppo_tc_supported(dsts[0], r0, mb, 1), PRB_ERR_CONFIG,
+                "ppo_update_learners: needs the tensor-core update's shapes (actor S-64-64-A / critic S-64-64-1, "
+                "A <= 32, minibatch <= 1024)");
+    cudaStream_t s = dsts[0]->ctx->stream;
+    // GAE + normalisation once per distinct buffer (learners of one pod share it)
+    for (size_t l = 0; l < L; ++l) {
+      bool seen = false;
+      for (size_t k = 0; k < l; ++k) seen |= rollouts[k] == rollouts[l];
+      if (seen) continue;
+      prb_rollout r = rollouts[l];
+      prb_gae_launch(r->ctx, r->d_rew.p, r->d_val.p, r->d_done.p, r->d_boot.p, r->N, r->H, cfg->gamma,
+                     cfg->gae_lambda, r->d_adv.p, r->d_ret.p, r->d_advstat.p, 1);
+      if (r->ctx->stream != s) r->ctx->sync();
+      r->gae_valid = true;
+      r->normalized = true;
+    }
+    for (size_t l = 0; l < L; ++l) {
+      int rc = prb_agent_copy(dsts[l], srcs[l]);
+      if (rc) fail(rc, prb_last_error());
+      dsts[l]->lr = cfg->learning_rate;  // ppo.hpp:265
+      PRB_CUDA(cudaMemsetAsync(dsts[l]->d_status.p, 0, 4 * sizeof(int32_t), s));
+      if (!dsts[l]->ppo_ws)
+        dsts[l]->ppo_ws = std::shared_ptr<void>(new PpoWorkspace, [](void* w) { delete static_cast<PpoWorkspace*>(w); });
+    }
+    PpoWorkspace& ws0 = *static_cast<PpoWorkspace*>(dsts[0]->ppo_ws.get());
+    PpoArgs p = make_args(dsts[0], r0, cfg, seeds[0], ws0, mb);
+    const int64_t steps = (int64_t)cfg->epochs_per_update * p.nmb;
+    if (steps == 0) return;
+    PpoTcArgs t = make_tc_shape(p, dsts[0], r0, ws0, steps, s);
+    std::vector<PpoTcChain> chains;
+    for (size_t l = 0; l < L; ++l) {
+      PpoWorkspace& ws = *static_cast<PpoWorkspace*>(dsts[l]->ppo_ws.get());
+      chains.push_back(make_tc_chain(t, dsts[l], rollouts[l], ws, nullptr, seeds[l], s));
+    }
+    DevBuf<PpoTcChain> cbuf;
+    upload_chains(t, chains, cbuf, s);
+    {
+      ProfScope prof(dsts[0]->ctx, kProfPpoFwdBwd);
+      launch_ppo_tc(t, (int)L, s);
+    }
+    PRB_CHECK_LAUNCH();
+    PRB_CUDA(cudaStreamSynchronize(s));
+    int first_code = 0, first_detail = 0;
+    for (size_t l = 0; l < L; ++l) {
+      int32_t st[2];
+      PRB_CUDA(cudaMemcpy(st, dsts[l]->d_status.p, sizeof(st), cudaMemcpyDeviceToHost));
+      if (st[0] && !first_code) {
+        first_code = st[0];
+        first_detail = st[1];
+      }
+      if (st[0]) PRB_CUDA(cudaMemset(dsts[l]->d_status.p, 0, 4 * sizeof(int32_t)));
+      if (stats) {
+        double h[4];
+        PpoWorkspace& ws = *static_cast<PpoWorkspace*>(dsts[l]->ppo_ws.get());
+        PRB_CUDA(cudaMemcpy(h, ws.tc_stats.p, sizeof(h), cudaMemcpyDeviceToHost));
+        stats[l].minibatches = (uint64_t)h[3];
+        const double inv = h[3] > 0 ? 1.0 / h[3] : 0.0;
+        stats[l].mean_policy_loss = h[0] * inv;
+        stats[l].mean_value_loss = h[1] * inv;
+        stats[l].mean_entropy = h[2] * inv;
+      }
+    }
+    if (first_code) fail(first_code, status_message(first_detail));
   });
 }
 

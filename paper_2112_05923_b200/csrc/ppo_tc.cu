@@ -58,7 +58,10 @@ constexpr int kThreads = 256;
 constexpr int kXC = 192;  // X columns
 constexpr int kHC = 128;  // H1 / H2 / d1 / d2 / d3 columns (actor 0-63 | critic 64-127)
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
-constexpr int kScr = 41;  // fp32 head-epilogue scratch row stride (odd: conflict-free both ways)
+constexpr int kScr = 41;
+// TMEM columns holding the tanh derivatives 1 - h^2 (packed bf16 pairs, 32 per half) of layer 2
+// (consumed by the d2 epilogue before the d1 accumulator [320,448) is issued) and of layer 1
+constexpr uint32_t kTD2 = 384, kTD1 = 448;  // fp32 head-epilogue scratch row stride (odd: conflict-free both ways)
 
 // shared-memory map (bytes from the 1024-aligned dynamic base)
 constexpr uint32_t kOffXhi = 0;                        // X_hi   [128][192]            49152
@@ -77,8 +80,13 @@ constexpr uint32_t kSmemBytes = kOffRidx + 512;
 constexpr uint32_t kStageBytes = kOffRE;  // X_hi .. H2, dead during the reduction: slice staging
 constexpr uint32_t kOffGather = 98304;    // the next rows' fp32 staging [128][gs] (after X_hi / X_lo)
 // image (global) = W1 block | RE | fp32 block, the smem bytes [kOffRC, +49152) ++ [kOffRE, +23568)
-constexpr uint32_t kImgW1 = 49152, kImgRest = 22528 + 1040;
-static_assert(kImgW1 + kImgRest == (uint32_t)kPpoTcImgBytes, "image size");
+// image (global) = W1 hi | W1 lo (bf16 pairs: W1 multiplies inputs of magnitude ~1e2, so the
+// first layer needs ~16-bit weights as well as inputs) | W2a W2c W3a W3c | fp32 block
+constexpr uint32_t kImgW1 = 49152, kImgRestOff = 2 * kImgW1, kImgRest = 22528 + 1040;
+static_assert(kImgRestOff + kImgRest == (uint32_t)kPpoTcImgBytes, "image size");
+// where W1 lo lands in shared memory for the L1 MMAs: K-steps 0-3 in the dead upper 16 KB of RB,
+// K-steps 4-11 in H2's region (both free until L1 is done)
+constexpr uint32_t kOffW1loA = kOffRB + 49152, kOffW1loB = kOffRC + 49152;
 // fp32 block (float index): b2 [0,128), b3a [128,160), b3c 160, log_std [164,196), w3c [196,260)
 constexpr int kFb2 = 0, kFb3a = 128, kFb3c = 160, kFls = 164, kFw3c = 196;
 
@@ -175,7 +183,7 @@ __host__ __device__ inline void img_pos(const PpoTcArgs& a, int p, int* bf16, in
     if (i >= 0 && i < 65 * 64) {  // W2 [64][64], b2 [64]
       const int k = i / 64, o = i % 64;
       if (k < 64)
-        *bf16 = (int)(kImgW1 + (net ? 8192u : 0u) + core_off(k, o, 64));
+        *bf16 = (int)(kImgRestOff + (net ? 8192u : 0u) + core_off(k, o, 64));
       else
         *f32 = kFb2 + o0 + o;
       return;
@@ -185,7 +193,7 @@ __host__ __device__ inline void img_pos(const PpoTcArgs& a, int p, int* bf16, in
     if (i >= 0 && i < 65 * nout) {  // W3 [64][nout], b3 [nout]
       const int k = i / nout, o = i % nout;
       if (k < 64) {
-        *bf16 = (int)(kImgW1 + (net ? 20480u : 16384u) + core_off(k, o, 64));
+        *bf16 = (int)(kImgRestOff + (net ? 20480u : 16384u) + core_off(k, o, 64));
         if (net) *f32 = kFw3c + k;
       } else {
         *f32 = net ? kFb3c : kFb3a + o;
@@ -197,38 +205,45 @@ __host__ __device__ inline void img_pos(const PpoTcArgs& a, int p, int* bf16, in
 }
 
 __device__ __forceinline__ void img_store_at(uint8_t* img, int2 e, float w) {
-  if (e.x >= 0) *reinterpret_cast<__nv_bfloat16*>(img + e.x) = __float2bfloat16_rn(w);
-  float* fb = reinterpret_cast<float*>(img + kImgW1 + 22528);
+  if (e.x >= 0) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    *reinterpret_cast<__nv_bfloat16*>(img + e.x) = hi;
+    if (e.x < (int)kImgW1)  // a W1 entry: its low half too
+      *reinterpret_cast<__nv_bfloat16*>(img + kImgW1 + e.x) = __float2bfloat16_rn(w - __bfloat162float(hi));
+  }
+  float* fb = reinterpret_cast<float*>(img + kImgRestOff + 22528);
   const int f = e.y & 0xffff, f2 = (e.y >> 16) & 0xffff;
   if (f != 0xffff) fb[f] = w;
   if (f2 != 0xffff) fb[f2] = w;
 }
 
 __device__ __forceinline__ void img_store(const PpoTcArgs& a, uint8_t* img, int p, float w) {
-#ifdef PRB_TC_IMGPOS_ONTHEFLY
-  int2 e;
-  {
-    int b, f, f2;
-    img_pos(a, p, &b, &f, &f2);
-    e = make_int2(b, (f < 0 ? 0xffff : f) | ((f2 < 0 ? 0xffff : f2) << 16));
-  }
-#else
-  const int2 e = a.imgpos[p];
-#endif
-  if (e.x >= 0) *reinterpret_cast<__nv_bfloat16*>(img + e.x) = __float2bfloat16_rn(w);
-  float* fb = reinterpret_cast<float*>(img + kImgW1 + 22528);
-  const int f = e.y & 0xffff, f2 = (e.y >> 16) & 0xffff;
-  if (f != 0xffff) fb[f] = w;
-  if (f2 != 0xffff) fb[f2] = w;
+  img_store_at(img, a.imgpos[p], w);
 }
 
 // 16 consecutive accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem16(uint32_t taddr, float* v) { tc::tmem_ld16(taddr, v); }
 
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// tanh(z) and its derivative 1 - tanh(z)^2 = 4t / (1 + t)^2 with t = exp(-2|z|): accurate to a few
+// ulp in RELATIVE terms even for saturated units, where 1 - h^2 from tanh.approx (absolute error
+// ~5e-4) or from a rounded h would be noise (the backward multiplies by it, nn.hpp:122-127)
+__device__ __forceinline__ void tanh_d(float z, float& h, float& d) {
+  const float t = __expf(-2.f * fabsf(z));
+  const float r = __frcp_rn(1.f + t);
+  h = copysignf((1.f - t) * r, z);
+  d = 4.f * t * r * r;
+}
+
 // a row's 64 accumulator columns -> tanh(. + add[c]) -> bf16 into an R=128 core-form matrix at col cd
-__device__ __forceinline__ void epi_tanh64(uint32_t tl, const float* add, uint8_t* dst, int row, int cd) {
+// ... and the tanh derivatives 1 - h^2 (from the fp32 h) as packed bf16 pairs to TMEM at t_deriv
+__device__ __forceinline__ void epi_tanh64(uint32_t tl, const float* add, uint8_t* dst, int row, int cd,
+                                           uint32_t t_deriv) {
   float v[64];
   tc::tmem_ld64(tl, v);
+  uint32_t dpk[32];
 #pragma unroll
   for (int c = 0; c < 64; c += 8) {
     uint32_t pk[4];
@@ -236,28 +251,30 @@ __device__ __forceinline__ void epi_tanh64(uint32_t tl, const float* add, uint8_
     for (int j = 0; j < 4; ++j) {
       float z0 = v[c + 2 * j], z1 = v[c + 2 * j + 1];
       if (add) tc::add2(z0, z1, add[c + 2 * j], add[c + 2 * j + 1]);
-      pk[j] = tc::pack_bf16(tc::tanh_fast(z0), tc::tanh_fast(z1));
+      float h0, h1, d0, d1;
+      tanh_d(z0, h0, d0);
+      tanh_d(z1, h1, d1);
+      pk[j] = tc::pack_bf16(h0, h1);
+      dpk[(c >> 1) + j] = tc::pack_bf16(d0, d1);
     }
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
+  tc::tmem_st32(t_deriv, dpk);
 }
 
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-
-// delta = D[c] * (1 - h^2) with h the bf16 activations at `hsrc` (same row / columns)
-__device__ __forceinline__ void epi_delta64(uint32_t tl, const uint8_t* hsrc, uint8_t* dst, int row, int cd) {
+// delta = D[c] * (1 - h^2), the derivatives read back from TMEM at t_deriv (packed bf16 pairs)
+__device__ __forceinline__ void epi_delta64(uint32_t tl, uint32_t t_deriv, uint8_t* dst, int row, int cd) {
   float v[64];
   tc::tmem_ld64(tl, v);
+  uint32_t dw[32];
+  tc::tmem_ld32(t_deriv, dw);
 #pragma unroll
   for (int c = 0; c < 64; c += 8) {
-    const uint4 h0 = *reinterpret_cast<const uint4*>(hsrc + core_off(row, cd + c, 128));
-    const uint32_t hw[4] = {h0.x, h0.y, h0.z, h0.w};
     uint32_t pk[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float a0 = bf_lo(hw[j]), a1 = bf_hi(hw[j]);
-      pk[j] = tc::pack_bf16(v[c + 2 * j] * (1.f - a0 * a0), v[c + 2 * j + 1] * (1.f - a1 * a1));
+      const uint32_t w = dw[(c >> 1) + j];
+      pk[j] = tc::pack_bf16(v[c + 2 * j] * bf_lo(w), v[c + 2 * j + 1] * bf_hi(w));
     }
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
@@ -365,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       uint2 e = make_uint2(0xffffffffu, 0u);
       if (qg < a.mb) {
         e.x = mb_index(a, ch, st, (uint32_t)qg);
-        if (a.obs_mode == 1) e.y = (uint32_t)a.row[e.x / a.N];
+        if (a.obs_mode == 1) e.y = (uint32_t)ch.row[e.x / a.N];
       }
       s_next[tid] = e;
     }
@@ -382,10 +399,10 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       const float* prv;
       const float* rest;
       if (a.obs_mode == 1) {
-        prv = a.obs + (size_t)i * a.Sp;
-        rest = a.feat + (size_t)e.y * a.F;
+        prv = ch.obs + (size_t)i * a.Sp;
+        rest = ch.feat + (size_t)e.y * a.F;
       } else {
-        prv = a.obs + (size_t)i * a.S;
+        prv = ch.obs + (size_t)i * a.S;
         rest = prv + a.npriv;
       }
       float* row = gst + q * gs;
@@ -393,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       for (int k = lane; k < a.nrest; k += 32) cp_async4(row + 32 + k, rest + k);
       if (lane == 0) {
         ridx[q] = i;
-        cp_async4(row + gs - 3, a.logp + i);
-        cp_async4(row + gs - 2, a.adv + i);
-        cp_async4(row + gs - 1, a.ret + i);
+        cp_async4(row + gs - 3, ch.logp + i);
+        cp_async4(row + gs - 2, ch.adv + i);
+        cp_async4(row + gs - 1, ch.ret + i);
       }
     }
   };
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       *reinterpret_cast<uint4*>(smem + kOffRB + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     if (hh == 0) {
-      const double mean = a.advstat[0], denom = a.advstat[1];
+      const double mean = ch.advstat[0], denom = ch.advstat[1];
       rows_f[q] = valid ? row[gs - 3] : 0.f;
       rows_f[128 + q] = valid ? (float)(((double)row[gs - 2] - mean) / denom) : 0.f;
       rows_f[256 + q] = valid ? row[gs - 1] : 0.f;
@@ -432,12 +449,15 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   auto load_image = [&]() {
     if (tid == 0) {
       tc::fence_proxy_async();
-      tc::mbar_arrive_expect_tx(&s_img, kImgW1 + kImgRest);
+      tc::mbar_arrive_expect_tx(&s_img, kImgRestOff + kImgRest);
       constexpr uint32_t kChunk = 16384;
       for (uint32_t o = 0; o < kImgW1; o += kChunk)
         tc::bulk_g2s(smem + kOffRC + o, img + o, min(kChunk, kImgW1 - o), &s_img);
+      tc::bulk_g2s(smem + kOffW1loA, img + kImgW1, 16384, &s_img);  // W1 lo K-steps 0-3
+      for (uint32_t o = 0; o < 32768; o += kChunk)                  // and 4-11
+        tc::bulk_g2s(smem + kOffW1loB + o, img + kImgW1 + 16384 + o, kChunk, &s_img);
       for (uint32_t o = 0; o < kImgRest; o += kChunk)
-        tc::bulk_g2s(smem + kOffRE + o, img + kImgW1 + o, min(kChunk, kImgRest - o), &s_img);
+        tc::bulk_g2s(smem + kOffRE + o, img + kImgRestOff + o, min(kChunk, kImgRest - o), &s_img);
     }
   };
 
@@ -469,11 +489,21 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     // ---- L1: D[0,64) = X_hi . W1a + X_lo . W1a, then D[64,128) for the critic (its own commit,
     // so the actor epilogue overlaps the critic's MMAs) ----
     if (tid == 0) {
+      // X_hi . W1_hi + X_lo . W1_hi + X_hi . W1_lo (the lo . lo term is below fp32 rounding)
+      auto w1lo_chain = [&](uint32_t d_col, uint32_t n_off) {
+        const uint32_t idesc = tc::idesc_bf16_t(128, 64, 0, 0);
+        for (int j = 0; j < kXC / 16; ++j) {
+          const uint32_t bb = (j < 4 ? sbase + kOffW1loA + j * 4096 : sbase + kOffW1loB + (j - 4) * 4096) + n_off;
+          tc::mma_bf16(tbase + d_col, desc_k(sbase + kOffXhi + j * 4096, 128), desc_k(bb, 128), idesc, 1u);
+        }
+      };
       mma_chain(tbase + 0, sbase + kOffXhi, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, false);
       mma_chain(tbase + 0, sbase + kOffRB, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, true);
+      w1lo_chain(0, 0);
       tc::mma_commit(&s_mma);
       mma_chain(tbase + 64, sbase + kOffXhi, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, false);
       mma_chain(tbase + 64, sbase + kOffRB, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, true);
+      w1lo_chain(64, 1024);
       tc::mma_commit(&s_mma2);
     }
     if (st + 1 < a.steps) resolve_rows(st + 1);  // read by gather_issue at the end of this step
@@ -497,20 +527,28 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           const int r = e / per, k = e - r * per;
           const uint32_t i = ridx[r];
           if (i == 0xffffffffu) continue;
-          const float* src = a.act + (size_t)i * a.A;
+          const float* src = ch.act + (size_t)i * a.A;
           if (even)
             cp_async8(sact + r * 32 + 2 * k, src + 2 * k);
           else
             cp_async4(sact + r * 32 + k, src + k);
         }
       }
+      uint32_t dpk[32];  // 1 - h^2 in relative precision (tanh_d)
 #pragma unroll
       for (int c = 0; c < 64; c += 8) {
         uint32_t pk[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pk[j] = tc::pack_bf16(tc::tanh_fast(hreg[c + 2 * j]), tc::tanh_fast(hreg[c + 2 * j + 1]));
+        for (int j = 0; j < 4; ++j) {
+          float h0, h1, d0, d1;
+          tanh_d(hreg[c + 2 * j], h0, d0);
+          tanh_d(hreg[c + 2 * j + 1], h1, d1);
+          pk[j] = tc::pack_bf16(h0, h1);
+          dpk[(c >> 1) + j] = tc::pack_bf16(d0, d1);
+        }
         *reinterpret_cast<uint4*>(smem + kOffRC + core_off(lrow, half * 64 + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
+      tc::tmem_st32(tl + kTD1 + half * 32, dpk);
     }
     publish();
     TCMARK(3);
@@ -521,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
     mma.wait();
     TCMARK(4);
-    epi_tanh64(tl + 128 + half * 64, f32 + kFb2 + half * 64, smem + kOffH2, lrow, half * 64);
+    epi_tanh64(tl + 128 + half * 64, f32 + kFb2 + half * 64, smem + kOffH2, lrow, half * 64, tl + kTD2 + half * 32);
     cp_async_wait_all();  // the action copies (visible to every thread after the barrier)
     publish();
     TCMARK(5);
@@ -562,8 +600,12 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           const float ratio = __expf(lp - rows_f[r]);
           const float adv = rows_f[128 + r];
           const float s1 = ratio * adv;
-          const float s2 = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip) * adv;
-          pl = -fminf(s1, s2) * inv_n;
+          // std::clamp / std::min as the reference evaluates them (a NaN ratio propagates into the
+          // loss and trips the gate, ppo.hpp:139-142, :169)
+          const float lo = 1.f - a.clip, hi = 1.f + a.clip;
+          const float cl = (ratio < lo) ? lo : ((hi < ratio) ? hi : ratio);
+          const float s2 = cl * adv;
+          pl = -((s2 < s1) ? s2 : s1) * inv_n;
           const float dl = (s1 <= s2) ? -adv * ratio * inv_n : 0.f;  // ties flow (ppo.hpp:146)
 #pragma unroll
           for (int d = 0; d < 32; ++d) {
@@ -634,19 +676,18 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     __syncthreads();  // s_red complete; the scratch in BUF2 is dead
     // ---- d2 = (.) o (1 - H2^2): actor from TMEM, critic as dV x w3c ----
     if (half == 0) {
-      epi_delta64(tl + 256, smem + kOffH2, smem + kOffBuf2, lrow, 0);
+      epi_delta64(tl + 256, tl + kTD2, smem + kOffBuf2, lrow, 0);
     } else {
       const float dv = rows_f[384 + lrow];
+      uint32_t dw[32];
+      tc::tmem_ld32(tl + kTD2 + 32, dw);
 #pragma unroll 1
       for (int c = 0; c < 64; c += 8) {
-        const uint4 hq = *reinterpret_cast<const uint4*>(smem + kOffH2 + core_off(lrow, 64 + c, 128));
-        const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
         uint32_t pk[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float a0 = bf_lo(hw[j]), a1 = bf_hi(hw[j]);
-          pk[j] = tc::pack_bf16(dv * f32[kFw3c + c + 2 * j] * (1.f - a0 * a0),
-                                dv * f32[kFw3c + c + 2 * j + 1] * (1.f - a1 * a1));
+          const uint32_t w = dw[(c >> 1) + j];
+          pk[j] = tc::pack_bf16(dv * f32[kFw3c + c + 2 * j] * bf_lo(w), dv * f32[kFw3c + c + 2 * j + 1] * bf_hi(w));
         }
         *reinterpret_cast<uint4*>(smem + kOffBuf2 + core_off(lrow, 64 + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
@@ -662,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
     mma.wait();
     TCMARK(10);
-    epi_delta64(tl + 320 + half * 64, smem + kOffRC, smem + kOffBuf1, lrow, half * 64);
+    epi_delta64(tl + 320 + half * 64, tl + kTD1 + half * 32, smem + kOffBuf1, lrow, half * 64);
     publish();
     TCMARK(11);
     if (tid == 0) {  // dW1^T = d1^T . X_hi

@@ -20,16 +20,8 @@ struct PpoTcChain {
   const uint32_t* perm;  // injected [epochs][n] minibatch order (device indices) or null (Feistel from seed)
   uint64_t seed;
   float lr;
-};
-
-struct PpoTcArgs {
-  const PpoTcChain* chains;
-  // nets: actor S-64-64-A, critic S-64-64-1 (flat offsets of W_l; b_l follows W_l)
-  int S, A, P, Pp;
-  int a_w[3], c_w[3], log_std;
-  int npriv, nrest, ones_col;  // X columns: private features hi/lo [0, npriv), the rest [32, 32+nrest), ones
-  // rollout buffer (time-major, index h*N + e)
-  int obs_mode, Sp, F;
+  // this learner's rollout buffer (time-major, index h*N + e); learners of different pods read
+  // different buffers, learners of one pod the same one
   const float* obs;
   const int32_t* row;
   const float* feat;
@@ -38,6 +30,16 @@ struct PpoTcArgs {
   const float* adv;
   const float* ret;
   const double* advstat;
+};
+
+struct PpoTcArgs {
+  const PpoTcChain* chains;
+  // nets: actor S-64-64-A, critic S-64-64-1 (flat offsets of W_l; b_l follows W_l)
+  int S, A, P, Pp;
+  int a_w[3], c_w[3], log_std;
+  int npriv, nrest, ones_col;  // X columns: private features hi/lo [0, npriv), the rest [32, 32+nrest), ones
+  // rollout buffer shape (shared by every chain of a launch; the pointers are per chain)
+  int obs_mode, Sp, F;
   uint32_t N;
   // schedule
   uint32_t n, nmb;
@@ -50,7 +52,7 @@ struct PpoTcArgs {
   unsigned long long* trace;  // debug: [18] globaltimer phase marks of step 8 (null: off)
 };
 
-constexpr int kPpoTcImgBytes = 72720;
+constexpr int kPpoTcImgBytes = 121872;
 constexpr int kPpoTcMaxRows = 1024;  // 8 CTAs x 128 rows
 
 size_t ppo_tc_smem_bytes();

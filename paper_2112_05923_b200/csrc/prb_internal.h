@@ -234,7 +234,7 @@ struct prb_agent_s {
   prb::DevBuf<int64_t> d_t;          // Adam step counter (device-resident)
   prb::DevBuf<int32_t> d_status;     // [0]=error code raised on device, [1]=detail
   std::shared_ptr<void> ppo_ws;      // ppo.cu workspace, kept across prb_ppo_update calls
-  int ppo_mode = 1;                  // prb_agent_set_ppo_mode: 1 tensor cores where supported, 0 fp32 SIMT
+  int ppo_mode = 0;                  // prb_agent_set_ppo_mode: 0 fp32 SIMT (default), 1 tensor cores where supported
 };
 
 // Device TransitionBuffer (buffer.hpp:27-135), TIME-MAJOR: transition

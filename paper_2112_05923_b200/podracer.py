@@ -345,7 +345,8 @@ class Agent:
         self.ctx.lib.prb_adam_step_device(self.h, C.c_void_p(d_grads))
 
     def set_ppo_mode(self, mode: int):
-        """1: tensor-core PPO update where the shapes allow (default); 0: fp32 SIMT update."""
+        """0 (default): fp32 SIMT update over the whole GPU; 1: the tensor-core cluster update where the
+        shapes allow (what ppo_update_learners always runs)."""
         self.ctx.lib.prb_agent_set_ppo_mode(self.h, int(mode))
 
     def mutate(self, mutation_seed: int, sigma: float):
@@ -551,6 +552,23 @@ def ppo_update(agent: Agent, rollout: Rollout, cfg: PpoConfig, seed: int, perm: 
         pp = _p(perm, C.c_uint64)
     agent.ctx.lib.prb_ppo_update(agent.h, rollout.h, C.byref(c), seed, pp, dst.h, C.byref(st))
     return dst, PpoUpdateStats(st.mean_policy_loss, st.mean_value_loss, st.mean_entropy, st.minibatches)
+
+
+def ppo_update_learners(agents: Sequence[Agent], rollouts: Sequence[Rollout], cfg: PpoConfig, seeds: Sequence[int],
+                        outs: Optional[Sequence[Agent]] = None):
+    """pod_train's learner phase (pod.hpp:436-461): learner l = ppo_update(agents[l], rollouts[l],
+    cfg, seeds[l]), every learner in ONE tensor-core launch (a thread-block cluster each).
+    Returns (trained copies, [PpoUpdateStats])."""
+    L = len(agents)
+    dsts = list(outs) if outs is not None else [Agent(a.ctx, a.state_dim, a.action_dim, a.hidden) for a in agents]
+    c = cfg.c()
+    st = (_PpoStatsC * L)()
+    srcs = (C.c_void_p * L)(*[a.h for a in agents])
+    ros = (C.c_void_p * L)(*[r.h for r in rollouts])
+    dh = (C.c_void_p * L)(*[d.h for d in dsts])
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    agents[0].ctx.lib.prb_ppo_update_learners(srcs, ros, L, C.byref(c), _p(sd, C.c_uint64), dh, st)
+    return dsts, [PpoUpdateStats(x.mean_policy_loss, x.mean_value_loss, x.mean_entropy, x.minibatches) for x in st]
 
 
 def fuse_parameters(agents: Sequence[Agent], out: Optional[Agent] = None) -> Agent:
