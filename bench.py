@@ -410,7 +410,8 @@ def run_ours(args, d: Dist):
     if not args.skip_configs:
         other["configs[2]_pointmass"] = leg_pointmass(pr, lib, ctx, args.pm_envs, args.pm_horizon, d)
         other["configs[4]_stock_1M"] = leg_stock_large(pr, lib, ctx, market, cfg, args.c5_envs, H, d)
-    other["configs[3]_tournament"] = leg_tournament(pr, ctx, d, args.pods_per_gpu)
+    if not args.skip_configs:
+        other["configs[3]_tournament"] = leg_tournament(pr, ctx, market, cfg, d, args.pods_per_gpu)
     if not args.skip_configs:
         other["configs[0]_iteration"] = leg_c1_iteration(pr, lib, ctx, market, cfg, m, ind, d,
                                                          with_cpu=(d.rank == 0 and d.world == 1 and not args.skip_cpu))
@@ -514,8 +515,21 @@ def leg_c1_iteration(pr, lib, ctx, market, cfg, m, ind, d, with_cpu: bool):
         pr.ppo_update(agent, ro, pcfg, seed=200 + i, out=agent)
     iteration(0)
     ms = d.max(time_region(lib, ctx, lambda: [iteration(i) for i in (1, 2, 3)])) / 3
+    # the reference pod's own iteration shape: num_learners = 2 (config.hpp PodConfig) concurrent
+    # learners + fuse_parameters (pod.hpp:436-461) -- here both learners in one tensor-core launch
+    outs = [pr.Agent(ctx, S_DIM, K_ASSETS), pr.Agent(ctx, S_DIM, K_ASSETS)]
+
+    def pod_iteration(i):
+        ro.collect(agent, env, seed=300 + i)
+        pr.ppo_update_learners([agent, agent], [ro, ro], pcfg, [400 + i, 500 + i], outs=outs)
+        pr.fuse_parameters(outs, out=agent)
+    pod_iteration(0)
+    ms2 = d.max(time_region(lib, ctx, lambda: [pod_iteration(i) for i in (1, 2, 3)])) / 3
     out = {"workload": "configs[0]: 30 assets x 1,024 envs, horizon 256, 4 epochs x 256 minibatches of 1,024",
-           "gpu_ms_per_iteration": ms, "gpu_transitions_per_s": N1 * H1 / (ms / 1e3)}
+           "gpu_ms_per_iteration": ms, "gpu_transitions_per_s": N1 * H1 / (ms / 1e3),
+           "gpu_ms_per_iteration_2_learners": ms2,
+           "two_learners_note": "collect + 2 concurrent tensor-core learners + fuse (the reference pod's "
+                                "num_learners = 2); gpu_ms_per_iteration is collect + 1 fp32 SIMT learner"}
     if with_cpu:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         from oracle_bind import REF_BENCH_SO, load_ref, ptr, SZ
@@ -554,38 +568,64 @@ def leg_stock_large(pr, lib, ctx, market, cfg, n_envs, horizon, d):
             "rollout_gb_per_gpu": n_envs * horizon * BUF_BYTES / 1e9}
 
 
-def leg_tournament(pr, ctx, d, pods):
-    """configs[3]: per generation, NCCL all-gather of every rank's pods' (score, seq, id), identical
-    ranking on every rank, and top-3 elite weight broadcasts from their owner ranks."""
+def leg_tournament(pr, ctx, market, cfg, d, pods, learners=2, gens=2):
+    """configs[3]: one GPU's pod population, a REAL generation timed end to end: every pod's collect
+    in one grouped tcgen05 launch (configs[0]-sized pods: 1,024 stock envs x 256 steps), every pod's
+    `learners` PPO learners (4 epochs x 256 minibatches of 1,024) in one tensor-core launch (a
+    cluster per learner), per-pod fusion, evaluation (10 episodes of 40 steps), the NCCL all-gather
+    ranking over every rank's pods and the top-3 elite broadcasts + device mutations
+    (tournament.PodPopulation, tournament.hpp:395-506).  Host wall clock around each generation
+    (max over ranks); the learners alone are also timed against the fp32 SIMT update run serially."""
     from paper_2112_05923_b200 import tournament as tn
+    comm = None
     if d.world > 1:
         def share(b):
             obj = [b]
             d.dist.broadcast_object_list(obj, src=0)
             return obj[0]
-    else:
-        def share(b):
-            return b
-    comm = tn.Communicator(ctx, d.rank, d.world, share)
-    elite = pr.Agent.init(ctx, S_DIM, K_ASSETS, seed=5)
-    gens, times = 5, []
-    for g in range(gens + 2):
-        rng = np.random.default_rng(g * 131 + d.rank)
-        scores = rng.normal(size=pods)
-        ids = [tn.global_pod_id(d.rank, i, pods) for i in range(pods)]
-        seqs = [tn.arrival_seq(g, p, d.world * pods) for p in ids]
+        comm = tn.Communicator(ctx, d.rank, d.world, share)
+    N, H = 1024, 256
+    pcfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=4, buffer_size=N * H)
+    pop = tn.PodPopulation(ctx, market, cfg, pods=pods, envs_per_pod=N, horizon=H, learners=learners, ppo_cfg=pcfg,
+                           window=(0, T_ROWS - 1), eval_episodes=10, eval_window=(1900, 1940), capacity=10, top_k=3,
+                           seed=2112, rank=d.rank, world=d.world, comm=comm)
+    pop.generation()  # warm-up (workspaces, first-touch)
+    times = []
+    for _ in range(gens):
         d.barrier()
-        t0 = time.perf_counter()
-        board, _ = tn.allgather_rank(comm, scores, seqs, ids, 10)
-        for b in board[:3]:
-            tn.broadcast_agent(comm, elite, tn.owner_rank(b.pod_id, pods))
         ctx.synchronize()
-        if g >= 2:
-            times.append(d.max(time.perf_counter() - t0))
-    comm.close()
-    return {"pods_per_gpu": pods, "pods_total": pods * d.world, "ms_per_generation": 1e3 * float(np.median(times)),
-            "elite_bytes": 3 * 3 * elite.param_count * 4,
-            "what": "all-gather (score,seq,pod_id) + device ranking + 3 elite broadcasts (params,m,v,t); host-timed"}
+        t0 = time.perf_counter()
+        out = pop.generation()
+        ctx.synchronize()
+        times.append(d.max(time.perf_counter() - t0))
+    # the learner phase alone: concurrent clusters vs the SIMT update one learner after another
+    srcs = [a for a in pop.agents for _ in range(learners)]
+    ros = [r for r in pop.rollouts for _ in range(learners)]
+    outs = [o for lo in pop.learner_out for o in lo]
+    pr.ppo_update_learners(srcs, ros, pcfg, list(range(len(srcs))), outs=outs)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    pr.ppo_update_learners(srcs, ros, pcfg, list(range(len(srcs))), outs=outs)
+    ctx.synchronize()
+    learn_tc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for l in range(2):  # two serial SIMT learners, scaled to all of them
+        pr.ppo_update(srcs[l], ros[l], pcfg, l, out=outs[l])
+    ctx.synchronize()
+    learn_simt = (time.perf_counter() - t0) / 2 * len(srcs)
+    if comm is not None:
+        comm.close()
+    gen_s = float(np.median(times))
+    trans = pods * N * H
+    return {"pods_per_gpu": pods, "pods_total": pods * d.world, "learners_per_pod": learners,
+            "pod": f"{N} stock envs x {H} steps, 4 epochs x {N * H // 1024} minibatches of 1,024 per learner",
+            "ms_per_generation": 1e3 * gen_s,
+            "transitions_per_s": d.world * trans / gen_s,
+            "learner_phase_ms": 1e3 * learn_tc, "learner_phase_ms_simt_serial": 1e3 * learn_simt,
+            "learner_speedup_vs_simt_serial": learn_simt / learn_tc,
+            "board_top3": out["board"][:3], "fresh_inits": out["fresh"],
+            "what": "grouped collect + concurrent tcgen05 learners + fusion + evaluation + all-gather ranking + "
+                    "elite broadcast/mutation; host-timed per generation (max over ranks)"}
 
 
 GAE_BYTES = 4 + 4 + 1 + 4 + 4  # read reward, value, done; write advantage, return (stats fused in the pass)

@@ -149,6 +149,7 @@ SIGNATURES = {
     "prb_ctx_profile": (I, [P, I]),
     "prb_ctx_profile_read": (I, [P, I, pD, pU64]),
     "prb_rollout_set_mode": (I, [P, I]),
+    "prb_rollout_collect_pods": (I, [C.POINTER(P), C.POINTER(P), C.POINTER(P), SZ, pU64]),
     "prb_rollout_device_fields": (I, [P] + [C.POINTER(P)] * 7),
     "prb_rollout_download": (I, [P, pD, pD, pD, pD, pU8, pD, pD]),
     "prb_rollout_upload": (I, [P, pD, pD, pD, pD, pU8, pD, pD]),

@@ -255,6 +255,10 @@ struct prb_rollout_s {
   prb::DevBuf<float> d_boot;       // [N] bootstrap V(s_H)
   prb::DevBuf<uint8_t> d_pack;     // bf16 weight chunks of the PointMass 3x256 tcgen05 rollout
   prb::DevBuf<double> d_advstat;   // mean, denom of the advantages (ppo.hpp:234-242)
+  // grouped (multi-pod) tcgen05 collect: this rollout's step schedule and shared first-layer term
+  prb::DevBuf<float> d_sl;         // [H+1][128]
+  prb::DevBuf<int32_t> d_tseq;     // [H+1]
+  prb::DevBuf<uint8_t> d_dseq;     // [H]
   bool gae_valid = false;
   bool normalized = true;
   bool full = false;

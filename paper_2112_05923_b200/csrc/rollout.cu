@@ -40,6 +40,8 @@ void alloc_rollout(prb_rollout_s* r) {
 }  // namespace
 
 bool prb_fused_rollout_supported(prb_rollout r, prb_agent a, prb_vecenv env);
+void prb_tc_rollout_pods(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P,
+                         const uint64_t* seeds);
 
 // configs[2]: PointMass2D with the 3x256 actor/critic -> rollout_pm_tc.cu
 static bool pm_tc_supported(prb_rollout r, prb_agent a, prb_vecenv env) {
@@ -218,6 +220,36 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
     r->ctx->sync();  // rows[] lives on this stack frame
     r->full = true;
     r->gae_valid = false;
+  });
+}
+
+int prb_rollout_collect_pods(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P,
+                             const uint64_t* seeds) {
+  return guard([&] {
+    PRB_REQUIRE(rs && as && es && seeds && P > 0, PRB_ERR_USAGE, "worker_collect (pods): NULL argument");
+    for (size_t p = 0; p < P; ++p) {
+      PRB_REQUIRE(rs[p] && as[p] && es[p], PRB_ERR_USAGE, "worker_collect (pods): NULL argument");
+      PRB_REQUIRE(rs[p]->ctx->device == rs[0]->ctx->device && as[p]->ctx->device == rs[0]->ctx->device,
+                  PRB_ERR_USAGE, "worker_collect (pods): pods on different devices");
+      PRB_REQUIRE(es[p]->N == rs[p]->N && es[p]->S == rs[p]->S && es[p]->A == rs[p]->A && as[p]->S == es[p]->S &&
+                      as[p]->A == es[p]->A,
+                  PRB_ERR_USAGE, "worker_collect: rollout/agent/env shapes disagree");
+      for (size_t q = 0; q < p; ++q)
+        PRB_REQUIRE(rs[q] != rs[p] && es[q] != es[p], PRB_ERR_USAGE,
+                    "worker_collect (pods): a rollout or VecEnv appears twice");
+      if (es[p]->kind == PRB_KIND_STOCK && rs[p]->obs_mode != 1) {  // back to compact rows after an upload
+        rs[p]->obs_mode = 1;
+        rs[p]->K = es[p]->market->K;
+        rs[p]->Sp = 1 + (size_t)rs[p]->K;
+        rs[p]->d_obs.alloc(rs[p]->N * rs[p]->H * rs[p]->Sp);
+      }
+    }
+    DeviceScope dev_(rs[0]->ctx);
+    prb_tc_rollout_pods(rs, as, es, P, seeds);
+    for (size_t p = 0; p < P; ++p) {
+      rs[p]->full = true;
+      rs[p]->gae_valid = false;
+    }
   });
 }
 

@@ -482,3 +482,101 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
   env->t = t;
   env->step_count = sc;
 }
+
+// worker_collect of P pods' stock VecEnvs in ONE tcgen05 launch: each pod's
+// uniform t / done schedule and shared first-layer term are prepared as for a single collect (its
+// own buffers in the rollout), then pods x tiles CTAs run, each with its pod's weights, env state
+// and rollout buffer.  Every pod: the tcgen05 stock path (64x64 nets, K in {1,2,3,30}), the same
+// num_envs / horizon / K.
+void prb_tc_rollout_pods(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P,
+                         const uint64_t* seeds) {
+  prb_ctx_s* ctx = rs[0]->ctx;
+  cudaStream_t s = ctx->stream;
+  const size_t N = rs[0]->N, H = rs[0]->H;
+  const int K = es[0]->market->K;
+  std::vector<TcRolloutArgs> args(P);
+  for (size_t p = 0; p < P; ++p) {
+    prb_rollout r = rs[p];
+    prb_agent a = as[p];
+    prb_vecenv env = es[p];
+    prb_market_s* m = env->market;
+    PRB_REQUIRE(r->N == N && r->H == H && env->N == N && m->K == K && env->kind == PRB_KIND_STOCK &&
+                    prb_fused_rollout_supported(r, a, env) && stock_rollout_tc_supported(K) &&
+                    env->cfg.max_trade_shares * (double)(env->end - env->start + 1) < 16777216.0,
+                PRB_ERR_USAGE, "worker_collect (pods): every pod needs the tcgen05 stock rollout and equal shapes");
+    PRB_REQUIRE(env->was_reset, PRB_ERR_DIMENSION, "vec_step: sub-environments have no state (call reset first)");
+    // this pod's schedule (stock_env.hpp:99-101,168) and shared-layer term in its own buffers
+    std::vector<int32_t> tseq(H + 1);
+    std::vector<uint8_t> dseq(H);
+    size_t t = env->t, sc = env->step_count;
+    for (size_t h = 0; h < H; ++h) {
+      PRB_REQUIRE(t + 1 < m->T, PRB_ERR_USAGE, "stock_env_step: no next timestamp at t=" + std::to_string(t));
+      tseq[h] = (int32_t)t;
+      const size_t t1 = t + 1;
+      const bool done = (t1 + 1 >= m->T) || (t1 >= env->end);
+      dseq[h] = done ? 1 : 0;
+      t = done ? env->start : t1;
+      sc = done ? 0 : sc + 1;
+    }
+    tseq[H] = (int32_t)t;
+    env->t = t;
+    env->step_count = sc;
+    r->d_sl.ensure((H + 1) * 128);
+    r->d_tseq.ensure(H + 1);
+    r->d_dseq.ensure(H);
+    PRB_CUDA(cudaMemcpyAsync(r->d_tseq.p, tseq.data(), (H + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_dseq.p, dseq.data(), H, cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaMemcpyAsync(r->d_row.p, tseq.data(), H * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PRB_CUDA(cudaStreamSynchronize(s));  // tseq / dseq live on this stack frame
+    {
+      ProfScope prof(ctx, kProfRollout);
+      shared_layer1_kernel<<<(unsigned)(H + 1), 128, 0, s>>>(a->d_params.p, (int)a->aoff[0], (int)a->coff[0], 1 + K,
+                                                             5 * K, env->d_feat.p, r->d_tseq.p, r->d_sl.p);
+    }
+    PRB_CHECK_LAUNCH();
+    TcRolloutArgs& ta = args[p];
+    ta = TcRolloutArgs{};
+    ta.params = a->d_params.p;
+    ta.a_w1 = (int)a->aoff[0];
+    ta.a_w2 = (int)a->aoff[1];
+    ta.a_w3 = (int)a->aoff[2];
+    ta.c_w1 = (int)a->coff[0];
+    ta.c_w2 = (int)a->coff[1];
+    ta.c_w3 = (int)a->coff[2];
+    ta.log_std = (int)a->Pa;
+    ta.S = (int)env->S;
+    ta.K = K;
+    ta.shared_l1 = r->d_sl.p;
+    ta.t_seq = r->d_tseq.p;
+    ta.done_seq = r->d_dseq.p;
+    ta.close_tk = m->d_close_tk.p;
+    ta.feat = env->d_feat.p;
+    ta.cap = env->cfg.initial_capital;
+    ta.max_trade = env->cfg.max_trade_shares;
+    ta.cost = env->cfg.cost_rate;
+    ta.mt_f32 = (ta.max_trade == floor(ta.max_trade) && ta.max_trade >= 0.0 && ta.max_trade < 4194304.0) ? 1 : 0;
+    ta.N = (int)N;
+    ta.H = (int)H;
+    ta.seed = seeds[p];
+    ta.balance = env->d_balance.p;
+    ta.shares = env->d_shares.p;
+    ta.ep_return = env->d_ep_return.p;
+    ta.obs_out = env->d_obs.p;
+    ta.b_obs = r->d_obs.p;
+    ta.b_act = r->d_act.p;
+    ta.b_logp = r->d_logp.p;
+    ta.b_val = r->d_val.p;
+    ta.b_rew = r->d_rew.p;
+    ta.b_done = r->d_done.p;
+    ta.b_boot = r->d_boot.p;
+    r->d_feat = env->d_feat.p;
+  }
+  DevBuf<TcRolloutArgs> d_args;
+  d_args.alloc(P);
+  PRB_CUDA(cudaMemcpyAsync(d_args.p, args.data(), P * sizeof(TcRolloutArgs), cudaMemcpyHostToDevice, s));
+  {
+    ProfScope prof(ctx, kProfRollout);
+    launch_stock_rollout_tc_group(d_args.p, (int)P, (int)N, K, s);
+  }
+  PRB_CUDA(cudaStreamSynchronize(s));  // d_args is released on return
+}

@@ -189,8 +189,8 @@ __device__ __forceinline__ void store_rows(float* __restrict__ dst, const float*
     if (lane < cols) dst[(size_t)r * cols + lane] = stage[r * sld + lane];
 }
 
-template <int K, bool kTrace>
-__global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a) {
+template <int K, bool kTrace, typename Args>
+__device__ __forceinline__ void rollout_tile(const Args& a, const int tile) {
   static_assert(K >= 1 && K <= 30, "private obs row and staging must fit 31 columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& s = *reinterpret_cast<TcSmem*>(smem_raw);
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   constexpr bool kTileObs = (P1 == kSLD), kTileAct = (SA == A);
   const bool vec_ok = (a.N & 3) == 0;  // 16-byte aligned spans of both tiles
   const int tid = threadIdx.x, warp = tid >> 5;
-  const size_t e0 = (size_t)blockIdx.x * kM;
+  const size_t e0 = (size_t)tile * kM;
   const int nloc = min(kM, a.N - (int)e0);
   const bool live = tid < nloc;
   const float* P = a.params;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   uint32_t phase = 0;
   const size_t row = e0 + tid;
   tc::Tracer<kTcTraceLen, kTrace> tr;
-  if (a.trace && blockIdx.x == 0 && tid == 0) tr.p = a.trace;
+  if (a.trace && tile == 0 && tid == 0) tr.p = a.trace;
   // value_before of the first step (stock_env.hpp:68); later steps carry value_after
   double vb = bal;
   {
@@ -543,11 +543,42 @@ __global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a
   if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
+template <int K, bool kTrace>
+__global__ void __launch_bounds__(kM, 4) stock_rollout_tc_kernel(TcRolloutArgs a) {
+  rollout_tile<K, kTrace>(a, (int)blockIdx.x);
+}
+
+// P pods' collects in one launch: CTA b runs tile b % tiles of pod
+// b / tiles with that pod's weights, env state and buffer (a grouped GEMM over the pods)
+template <int K>
+__global__ void __launch_bounds__(kM, 4) stock_rollout_tc_group_kernel(const TcRolloutArgs* __restrict__ group,
+                                                                       int tiles) {
+  rollout_tile<K, false>(group[blockIdx.x / tiles], (int)(blockIdx.x % tiles));
+}
+
 }  // namespace
 
 size_t stock_rollout_tc_smem() { return sizeof(TcSmem); }
 
 bool stock_rollout_tc_supported(int K) { return K == 30 || K == 3 || K == 2 || K == 1; }
+
+void launch_stock_rollout_tc_group(const TcRolloutArgs* d_group, int pods, int N, int K, cudaStream_t s) {
+  const int tiles = (N + kM - 1) / kM;
+  const size_t smem = stock_rollout_tc_smem();
+  switch (K) {
+    case 30:
+      ensure_smem(stock_rollout_tc_group_kernel<30>, smem);
+      stock_rollout_tc_group_kernel<30><<<(unsigned)(pods * tiles), kM, smem, s>>>(d_group, tiles);
+      break;
+    case 3:
+      ensure_smem(stock_rollout_tc_group_kernel<3>, smem);
+      stock_rollout_tc_group_kernel<3><<<(unsigned)(pods * tiles), kM, smem, s>>>(d_group, tiles);
+      break;
+    default:
+      fail(PRB_ERR_CONFIG, "grouped tcgen05 rollout: no instantiation for K=" + std::to_string(K));
+  }
+  PRB_CHECK_LAUNCH();
+}
 
 void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.N + kM - 1) / kM);

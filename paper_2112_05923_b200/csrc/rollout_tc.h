@@ -38,5 +38,7 @@ constexpr int kTcTraceLen = 512;
 size_t stock_rollout_tc_smem();
 bool stock_rollout_tc_supported(int K);
 void launch_stock_rollout_tc(const TcRolloutArgs& a, cudaStream_t s);
+// pods x ceil(N / 128) CTAs; d_group[p] = pod p's arguments (same N, H, K for every pod)
+void launch_stock_rollout_tc_group(const TcRolloutArgs* d_group, int pods, int N, int K, cudaStream_t s);
 
 }  // namespace prb

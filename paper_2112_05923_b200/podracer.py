@@ -329,6 +329,11 @@ class Agent:
     def flatten_params(self) -> np.ndarray:
         return self.get()[0]
 
+    def copy_from(self, other: "Agent") -> "Agent":
+        """Deep copy of other's params / Adam state into this agent (on the device)."""
+        self.ctx.lib.prb_agent_copy(self.h, other.h)
+        return self
+
     def clone(self) -> "Agent":
         b = Agent(self.ctx, self.state_dim, self.action_dim, self.hidden)
         self.ctx.lib.prb_agent_copy(b.h, self.h)
@@ -552,6 +557,17 @@ def ppo_update(agent: Agent, rollout: Rollout, cfg: PpoConfig, seed: int, perm: 
         pp = _p(perm, C.c_uint64)
     agent.ctx.lib.prb_ppo_update(agent.h, rollout.h, C.byref(c), seed, pp, dst.h, C.byref(st))
     return dst, PpoUpdateStats(st.mean_policy_loss, st.mean_value_loss, st.mean_entropy, st.minibatches)
+
+
+def collect_pods(rollouts: Sequence["Rollout"], agents: Sequence[Agent], envs: Sequence["VectorizedEnvironment"],
+                 seeds: Sequence[int]) -> None:
+    """worker_collect (pod.hpp:95-132) of every pod in ONE tcgen05 launch (per-pod weights)."""
+    P = len(rollouts)
+    rs = (C.c_void_p * P)(*[r.h for r in rollouts])
+    ag = (C.c_void_p * P)(*[a.h for a in agents])
+    es = (C.c_void_p * P)(*[e.h for e in envs])
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    agents[0].ctx.lib.prb_rollout_collect_pods(rs, ag, es, P, _p(sd, C.c_uint64))
 
 
 def ppo_update_learners(agents: Sequence[Agent], rollouts: Sequence[Rollout], cfg: PpoConfig, seeds: Sequence[int],

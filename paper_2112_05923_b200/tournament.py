@@ -102,3 +102,112 @@ def allgather_rank(comm: Communicator, scores: Sequence[float], seqs: Sequence[i
 def broadcast_agent(comm: Communicator, agent, root: int):
     """Elite weights (params, Adam m/v, t) from their owner rank to every rank."""
     comm.lib.prb_agent_broadcast(comm.h, agent.h, root)
+
+
+class PodPopulation:
+    """One GPU's pod population (BASELINE configs[3]): the tournament of tournament.hpp:395-506 run
+    as synchronous generations, every pod's data on the device.
+
+    Per generation (``generation``):
+      1. worker_collect of every pod in ONE tcgen05 launch (prb_rollout_collect_pods: per-pod
+         weights, a grouped GEMM; pod.hpp:408-433);
+      2. every pod's ``learners`` PPO learners in ONE tensor-core launch, a thread-block cluster
+         per learner (prb_ppo_update_learners; pod.hpp:436-461), then fuse_parameters per pod
+         (pod.hpp:141-172) into the pod's agent;
+      3. evaluate each pod (prb_evaluate: ``eval_episodes`` episodes as one VecEnv, policy mean;
+         pod.hpp:43-83) -> its score;
+      4. the leaderboard: every rank's (score, seq, pod_id) all-gathered over NCCL and ranked
+         identically on every rank (prb_leaderboard_allgather_rank; tournament.hpp:104-119), or
+         ranked on the device alone with one rank;
+      5. the next generation's pod inits (generate_pod_init tournament.hpp:136-162): a pod is
+         fresh with probability ``fresh_prob`` (artifact_init), else a copy of one of the top_k
+         elites -- broadcast from its owner rank (prb_agent_broadcast) -- mutated on the device
+         (prb_agent_mutate, t := 0).  Decisions draw from a per-rank numpy generator; the weights
+         never leave HBM.
+    Scores, seqs and ids are the only host traffic.
+    """
+
+    def __init__(self, ctx, market, stock_cfg, pods: int, envs_per_pod: int, horizon: int, learners: int,
+                 ppo_cfg, window=(0, None), eval_episodes: int = 10, eval_window=None, capacity: int = 10,
+                 top_k: int = 3, fresh_prob: float = 0.2, sigma: float = 0.01, seed: int = 2112, rank: int = 0,
+                 world: int = 1, comm: "Communicator" = None, state_dim: int = 181, action_dim: int = 30):
+        from . import podracer as pr
+        self.pr, self.ctx, self.rank, self.world, self.comm = pr, ctx, rank, world, comm
+        self.P, self.L, self.cfg = pods, learners, ppo_cfg
+        self.capacity, self.top_k, self.fresh_prob, self.sigma = capacity, top_k, fresh_prob, sigma
+        self.S, self.A, self.seed = state_dim, action_dim, seed
+        T = market.T if hasattr(market, "T") else None
+        start, end = window
+        if end is None:
+            end = (T - 1) if T else 2047
+        ew = eval_window or (start, end)
+        self.envs = [pr.VectorizedEnvironment.stock(ctx, market, stock_cfg, start, end, envs_per_pod)
+                     for _ in range(pods)]
+        self.eval_envs = [pr.VectorizedEnvironment.stock(ctx, market, stock_cfg, ew[0], ew[1], eval_episodes)
+                          for _ in range(pods)]
+        for p, e in enumerate(self.envs):
+            e.reset(pr.derive_seed(seed, 1, self.global_id(p)))
+        self.rollouts = [pr.Rollout.for_env(e, horizon) for e in self.envs]
+        self.agents = [pr.Agent.init(ctx, state_dim, action_dim, seed=pr.derive_seed(seed, 5, self.global_id(p)))
+                       for p in range(pods)]
+        self.learner_out = [[pr.Agent(ctx, state_dim, action_dim) for _ in range(learners)] for _ in range(pods)]
+        self.elites = [pr.Agent(ctx, state_dim, action_dim) for _ in range(top_k)]
+        self.rng = np.random.default_rng(seed * 7919 + rank)
+        self.board: List[BoardEntry] = []
+        self.gen = 0
+        self.last_scores = None
+
+    def global_id(self, p: int) -> int:
+        return global_pod_id(self.rank, p, self.P)
+
+    def generation(self) -> dict:
+        pr = self.pr
+        g = self.gen
+        # 1. every pod's collect in one launch
+        pr.collect_pods(self.rollouts, self.agents, self.envs,
+                        [pr.derive_seed(self.seed, 2, self.global_id(p), g) for p in range(self.P)])
+        # 2. every pod's learners in one launch, then per-pod fusion
+        srcs = [a for a in self.agents for _ in range(self.L)]
+        ros = [r for r in self.rollouts for _ in range(self.L)]
+        outs = [o for lo in self.learner_out for o in lo]
+        seeds = [pr.derive_seed(self.seed, 3, self.global_id(p), l, g) for p in range(self.P) for l in range(self.L)]
+        _, stats = pr.ppo_update_learners(srcs, ros, self.cfg, seeds, outs=outs)
+        for p in range(self.P):
+            pr.fuse_parameters(self.learner_out[p], out=self.agents[p])
+        # 3. evaluation scores
+        scores = np.array([pr.evaluate(self.agents[p], self.eval_envs[p],
+                                       pr.derive_seed(self.seed, 4, self.global_id(p), g)).mean
+                           for p in range(self.P)])
+        # 4. leaderboard over every rank's pods (the previous board's entries compete again)
+        ids = [self.global_id(p) for p in range(self.P)]
+        seqs = [arrival_seq(g, pid, self.world * self.P) for pid in ids]
+        if self.comm is not None:
+            board, _ = allgather_rank(self.comm, scores, seqs, ids, self.capacity)
+        else:
+            order = pr.leaderboard_rank(self.ctx, scores, np.asarray(seqs, dtype=np.uint64), self.capacity)
+            board = [BoardEntry(float(scores[i]), int(seqs[i]), int(ids[i])) for i in order]
+        self.board = board
+        # 5. elites (top_k) on every rank, then the next generation's inits
+        k = min(self.top_k, len(board))
+        for j in range(k):
+            pid = board[j].pod_id
+            owner = owner_rank(pid, self.P)
+            if owner == self.rank:
+                self.elites[j].copy_from(self.agents[pid - self.rank * self.P])
+            if self.comm is not None:
+                broadcast_agent(self.comm, self.elites[j], owner)
+        fresh = 0
+        for p in range(self.P):
+            if k == 0 or self.rng.random() < self.fresh_prob:
+                flat = pr.artifact_init(self.S, self.A, int(self.rng.integers(0, 2**63)))
+                self.agents[p].set(flat)
+                fresh += 1
+            else:
+                self.agents[p].copy_from(self.elites[int(self.rng.integers(0, k))])
+                self.agents[p].mutate(int(self.rng.integers(0, 2**63)), self.sigma)
+        self.ctx.synchronize()
+        self.gen += 1
+        self.last_scores = scores
+        return {"generation": g, "scores": scores.tolist(), "board": [b.pod_id for b in board], "fresh": fresh,
+                "mean_policy_loss": float(np.mean([s.mean_policy_loss for s in stats])),
+                "minibatches_per_learner": stats[0].minibatches}

@@ -53,6 +53,31 @@ def main():
     assert np.array_equal(got, expect), rank
     if rank != root:
         assert not np.array_equal(flat_rank, got)
+    # a real pod population on every rank (configs[3] shape, small): grouped collect, concurrent
+    # learners, fusion, evaluation, NCCL all-gather ranking, elite broadcast + mutation
+    K = 30
+    m = pr.synthetic_market(K, 512, seed=2112)
+    ind = pr.compute_indicators(m["high"], m["low"], m["close"])
+    market = pr.MarketData(ctx, m["close"], ind)
+    cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=1, buffer_size=128 * 32)
+    pop = tn.PodPopulation(ctx, market, pr.StockConfig(), pods=4, envs_per_pod=128, horizon=32, learners=2,
+                           ppo_cfg=cfg, window=(0, 400), eval_episodes=4, eval_window=(300, 340), capacity=5,
+                           top_k=3, seed=5, rank=rank, world=world, comm=comm)
+    for _ in range(2):
+        out = pop.generation()
+        boards = [None] * world
+        dist.all_gather_object(boards, out["board"])
+        assert all(bb == boards[0] for bb in boards), boards
+        scores = [None] * world
+        dist.all_gather_object(scores, out["scores"])
+        flat = [s for part in scores for s in part]
+        seqs = [tn.arrival_seq(out["generation"], pid, world * 4) for pid in range(world * 4)]
+        assert out["board"] == tn.rank_candidates_host(flat, seqs, 5)
+    # the elites are identical on every rank after their broadcasts
+    e0 = pop.elites[0].flatten_params()
+    sums = [None] * world
+    dist.all_gather_object(sums, float(np.sum(e0)))
+    assert all(x == sums[0] for x in sums)
     comm.close()
     dist.barrier()
     if rank == 0:
