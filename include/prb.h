@@ -157,6 +157,12 @@ PRB_API int prb_agent_set_host(prb_agent a, const double* flat, const double* m,
 PRB_API int prb_agent_get_host(prb_agent a, double* flat, double* m, double* v, int64_t* t);
 PRB_API int prb_agent_copy(prb_agent dst, prb_agent src); /* AgentArtifact copy (deep) */
 PRB_API float* prb_agent_params_device(prb_agent a);       /* [P] fp32 flat blob */
+/* artifact_init artifact.hpp:91-105 ON THE DEVICE into agent a (its shapes):
+ * the reference's mt19937_64 streams and uniform_real_distribution draw order
+ * (nn.hpp:40-54), so the fp32 params are the reference's values rounded once;
+ * Adam state zero, learning rate lr.  The generator's fresh pods never touch
+ * the host (tournament.hpp:142-144). */
+PRB_API int prb_agent_init_device(prb_agent a, uint64_t seed, double lr);
 /* artifact_init artifact.hpp:91-105 (host, bit-exact with the reference). */
 PRB_API int prb_artifact_init(size_t state_dim, size_t action_dim, uint64_t seed, const size_t* hidden, int n_hidden,
                               double* flat_out, size_t* param_count);
@@ -335,6 +341,34 @@ PRB_API int prb_leaderboard_stats_host(const prb_agent* entries, size_t n, doubl
 /* generate_pod_init's mutation (tournament.hpp:149-159): params += N(0, sigma^2)
  * from a Philox stream keyed by mutation_seed; optimiser t := 0, m/v kept. */
 PRB_API int prb_agent_mutate(prb_agent a, uint64_t mutation_seed, double sigma);
+
+/* ---- checkpoints: PODRCKPT v1 (checkpoint.hpp:16-317) ---------------------
+ * The byte format of encode_checkpoint(artifact_to_tensors(a, meta)): magic,
+ * version 1, the named f64 tensor table (actor/critic layers, log_std, Adam
+ * m / v / scalars, lineage, algo_tag, optional meta), CRC-32 (IEEE).  Readers
+ * check the CRC first (CorruptionError), then magic (FormatError) and version
+ * (VersionError), as the reference does.  algo_tag NULL = "ppo"; meta (nullable)
+ * = (wall_seconds, env_steps, score).  With out == NULL *size receives the
+ * byte count.  Decoding into an agent of other shapes is a DimensionError. */
+PRB_API int prb_checkpoint_encode(prb_agent a, int64_t parent_pod, uint64_t mutation_seed, const char* algo_tag,
+                                  const double* meta, uint8_t* out, size_t capacity, size_t* size);
+PRB_API int prb_checkpoint_decode(prb_agent a, const uint8_t* bytes, size_t size, int64_t* parent_pod,
+                                  uint64_t* mutation_seed, char* algo_tag, size_t tag_capacity, double* meta,
+                                  int* has_meta);
+PRB_API int prb_checkpoint_save(prb_agent a, const char* path, int64_t parent_pod, uint64_t mutation_seed,
+                                const char* algo_tag, const double* meta);              /* checkpoint.hpp:305 */
+PRB_API int prb_checkpoint_load(prb_agent a, const char* path, int64_t* parent_pod, uint64_t* mutation_seed,
+                                char* algo_tag, size_t tag_capacity, double* meta, int* has_meta); /* :314 */
+/* The same over host arrays in the flat layout (no device): hyper = (beta1,
+ * beta2, eps, lr); the network is actor S-hidden-A / critic S-hidden-1. */
+PRB_API int prb_checkpoint_encode_host(size_t S, size_t A, const size_t* hidden, int nh, const double* flat,
+                                       const double* m, const double* v, int64_t t, const double* hyper,
+                                       int64_t parent_pod, uint64_t mutation_seed, const char* algo_tag,
+                                       const double* meta, uint8_t* out, size_t capacity, size_t* size);
+PRB_API int prb_checkpoint_decode_host(const uint8_t* bytes, size_t size, size_t S, size_t A, const size_t* hidden,
+                                       int nh, double* flat, double* m, double* v, int64_t* t, double* hyper,
+                                       int64_t* parent_pod, uint64_t* mutation_seed, char* algo_tag,
+                                       size_t tag_capacity, double* meta, int* has_meta);
 
 /* ---- NCCL over NVLink (tournament C4) --------------------- */
 typedef struct prb_comm_s* prb_comm;

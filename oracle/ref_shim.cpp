@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "podracer/checkpoint.hpp"
 #include "podracer/artifact.hpp"
 #include "podracer/buffer.hpp"
 #include "podracer/common.hpp"
@@ -464,6 +465,60 @@ REF_API int ref_leaderboard_stats(const double* cand, const double* scores, cons
     std::copy(st.mean.begin(), st.mean.end(), mean);
     std::copy(st.variance.begin(), st.variance.end(), variance);
   })
+}
+
+// ---- checkpoints (checkpoint.hpp): an artifact from flat params / Adam state -> the reference's
+// own encode_checkpoint(artifact_to_tensors(...)) bytes, and decode + artifact_from_tensors back.
+// Returns the byte count (out may be NULL to size), or (size_t)-1 on error.
+REF_API size_t ref_checkpoint_encode(const double* flat, const double* m, const double* v, int64_t t,
+                                     const double* hyper, size_t S, size_t A, const size_t* hidden, int nh,
+                                     int64_t parent, uint64_t mseed, const char* tag, const double* meta,
+                                     uint8_t* out) {
+  try {
+    AgentArtifact a = artifact_from(flat, m, v, t, S, A, hidden, nh, hyper[3]);
+    a.optimizer.beta1 = hyper[0];
+    a.optimizer.beta2 = hyper[1];
+    a.optimizer.eps = hyper[2];
+    a.lineage.parent_pod = parent;
+    a.lineage.mutation_seed = mseed;
+    a.algo_tag = tag;
+    CheckpointMeta cm;
+    if (meta) {
+      cm.wall_seconds = meta[0];
+      cm.env_steps = meta[1];
+      cm.score = meta[2];
+    }
+    const std::vector<std::uint8_t> b = encode_checkpoint(artifact_to_tensors(a, meta ? &cm : nullptr));
+    if (out) std::copy(b.begin(), b.end(), out);
+    return b.size();
+  } catch (...) {
+    return (size_t)-1;
+  }
+}
+
+// decode_checkpoint + artifact_from_tensors; returns 0, or the error class: 7 corruption, 4 format,
+// 8 version, 99 other.  flat/m/v sized by the caller (the artifact's param_count).
+REF_API int ref_checkpoint_decode(const uint8_t* bytes, size_t n, double* flat, double* m, double* v, int64_t* t,
+                                  int64_t* parent, uint64_t* mseed) {
+  try {
+    AgentArtifact a = artifact_from_tensors(decode_checkpoint(std::vector<std::uint8_t>(bytes, bytes + n)));
+    const std::vector<double> f = a.flatten_params();
+    std::copy(f.begin(), f.end(), flat);
+    std::copy(a.optimizer.m.begin(), a.optimizer.m.end(), m);
+    std::copy(a.optimizer.v.begin(), a.optimizer.v.end(), v);
+    *t = a.optimizer.t;
+    *parent = a.lineage.parent_pod;
+    *mseed = a.lineage.mutation_seed;
+    return 0;
+  } catch (const CorruptionError&) {
+    return 7;
+  } catch (const FormatError&) {
+    return 4;
+  } catch (const VersionError&) {
+    return 8;
+  } catch (...) {
+    return 99;
+  }
 }
 
 // ppo_update ppo.hpp:249 timing on a synthetic buffer of n transitions (chunks of

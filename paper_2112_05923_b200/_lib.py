@@ -171,10 +171,19 @@ SIGNATURES = {
     "prb_leaderboard_rank_host": (I, [P, pD, pU64, SZ, SZ, pI32, pI32]),
     "prb_agent_mutate": (I, [P, U64, D]),
     "prb_agent_set_ppo_mode": (I, [P, I]),
+    "prb_agent_init_device": (I, [P, U64, D]),
     "prb_debug_agent_grads": (I, [P, pD]),
     "prb_leaderboard_stats": (I, [C.POINTER(P), SZ, P, P]),
     "prb_leaderboard_stats_host": (I, [C.POINTER(P), SZ, pD, pD]),
     "prb_debug_set_option": (I, [I, I]),
+    "prb_checkpoint_encode": (I, [P, I64, U64, C.c_char_p, pD, pU8, SZ, C.POINTER(SZ)]),
+    "prb_checkpoint_decode": (I, [P, pU8, SZ, C.POINTER(I64), pU64, C.c_char_p, SZ, pD, C.POINTER(I)]),
+    "prb_checkpoint_save": (I, [P, C.c_char_p, I64, U64, C.c_char_p, pD]),
+    "prb_checkpoint_load": (I, [P, C.c_char_p, C.POINTER(I64), pU64, C.c_char_p, SZ, pD, C.POINTER(I)]),
+    "prb_checkpoint_encode_host": (I, [SZ, SZ, pSZ, I, pD, pD, pD, I64, pD, I64, U64, C.c_char_p, pD, pU8, SZ,
+                                       C.POINTER(SZ)]),
+    "prb_checkpoint_decode_host": (I, [pU8, SZ, SZ, SZ, pSZ, I, pD, pD, pD, C.POINTER(I64), pD, C.POINTER(I64), pU64,
+                                       C.c_char_p, SZ, pD, C.POINTER(I)]),
     "prb_comm_unique_id": (I, [C.POINTER(C.c_uint8)]),
     "prb_comm_init": (I, [P, C.POINTER(C.c_uint8), I, I, C.POINTER(P)]),
     "prb_comm_destroy": (I, [P]),

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "mlp_simt.cuh"
 #include "prb_internal.h"
 #include "rng.cuh"
 
@@ -177,6 +178,35 @@ __global__ void population_stats_kernel(const float* const* __restrict__ entries
     }
     mean[i] = m;
     var[i] = __dmul_rn(v, inv);
+  }
+}
+
+// artifact_init (artifact.hpp:91-105) on the device: policy_init's actor MLP from
+// mt19937_64(derive_seed(seed, kInit, 1)) and the critic from mt19937_64(derive_seed(seed, kInit,
+// 2)), each layer's weights drawn row-major from uniform_real_distribution(-1/sqrt(fan_in),
+// +1/sqrt(fan_in)) (nn.hpp:40-54) -- the reference's own generator and draw order, so the fp32
+// parameters are the reference's values rounded once.  Thread 0 draws the actor, thread 1 the
+// critic (two independent streams); biases and log_std are zero (the caller's memset).
+struct InitNet {
+  int nl;
+  int dims[kMaxLayers + 1];
+  int off[kMaxLayers];
+  uint64_t seed;
+};
+
+__global__ void artifact_init_kernel(float* __restrict__ params, InitNet actor, InitNet critic) {
+  __shared__ uint64_t mt[2][kMtN];
+  const int t = threadIdx.x;
+  if (t > 1) return;
+  const InitNet& n = t == 0 ? actor : critic;
+  uint64_t* st = mt[t];
+  mt64_seed(st, 1, n.seed);
+  int32_t idx = kMtN;
+  for (int l = 0; l < n.nl; ++l) {
+    const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)n.dims[l]));
+    const int cnt = n.dims[l] * n.dims[l + 1];
+    float* w = params + n.off[l];
+    for (int i = 0; i < cnt; ++i) w[i] = (float)mt64_uniform(st, 1, idx, -scale, scale);
   }
 }
 
@@ -468,6 +498,32 @@ int prb_leaderboard_rank_host(prb_ctx ctx, const double* scores, const uint64_t*
     ctx->sync();
     *count = h[capacity];
     for (int i = 0; i < *count; ++i) order[i] = h[i];
+  });
+}
+
+int prb_agent_init_device(prb_agent a, uint64_t seed, double lr) {
+  return guard([&] {
+    DeviceScope dev_(a ? a->ctx : nullptr);
+    PRB_REQUIRE(a, PRB_ERR_USAGE, "prb_agent_init_device: NULL agent");
+    cudaStream_t s = a->ctx->stream;
+    PRB_CUDA(cudaMemsetAsync(a->d_params.p, 0, a->d_params.bytes(), s));  // biases, log_std (0)
+    PRB_CUDA(cudaMemsetAsync(a->d_m.p, 0, a->d_m.bytes(), s));            // adam_init (nn.hpp:155-160)
+    PRB_CUDA(cudaMemsetAsync(a->d_v.p, 0, a->d_v.bytes(), s));
+    PRB_CUDA(cudaMemsetAsync(a->d_t.p, 0, sizeof(int64_t), s));
+    InitNet nets[2];
+    for (int k = 0; k < 2; ++k) {
+      const std::vector<size_t>& d = k == 0 ? a->adims : a->cdims;
+      const std::vector<size_t>& off = k == 0 ? a->aoff : a->coff;
+      PRB_REQUIRE(d.size() <= (size_t)kMaxLayers + 1, PRB_ERR_CONFIG, "prb_agent_init_device: too many layers");
+      nets[k].nl = (int)d.size() - 1;
+      for (size_t i = 0; i < d.size(); ++i) nets[k].dims[i] = (int)d[i];
+      for (size_t i = 0; i < off.size(); ++i) nets[k].off[i] = (int)off[i];
+      nets[k].seed = derive_seed(seed, {5 /*kInit*/, (uint64_t)(k + 1)});
+    }
+    artifact_init_kernel<<<1, 32, 0, s>>>(a->d_params.p, nets[0], nets[1]);
+    PRB_CHECK_LAUNCH();
+    a->lr = lr;
+    a->ctx->sync();
   });
 }
 

@@ -329,6 +329,11 @@ class Agent:
     def flatten_params(self) -> np.ndarray:
         return self.get()[0]
 
+    def init_device(self, seed: int, lr: float = 1e-3) -> "Agent":
+        """artifact_init (artifact.hpp:91-105) drawn on the device, bit-exact with the reference."""
+        self.ctx.lib.prb_agent_init_device(self.h, seed, lr)
+        return self
+
     def copy_from(self, other: "Agent") -> "Agent":
         """Deep copy of other's params / Adam state into this agent (on the device)."""
         self.ctx.lib.prb_agent_copy(self.h, other.h)
@@ -652,3 +657,49 @@ def set_debug_option(option: int, value: int) -> None:
 
 
 OPT_PPO_PER_KERNEL, OPT_TC_FORCE_REDO, OPT_PM_CTA_PAIR = 1, 2, 3
+
+
+@dataclass
+class CheckpointInfo:  # lineage, algo_tag and CheckpointMeta of a PODRCKPT file (checkpoint.hpp:200-205)
+    parent_pod: int = -1
+    mutation_seed: int = 0
+    algo_tag: str = "ppo"
+    meta: Optional[tuple] = None
+
+
+def checkpoint_encode(agent: Agent, info: CheckpointInfo = CheckpointInfo()) -> bytes:
+    """encode_checkpoint(artifact_to_tensors(agent)) -- PODRCKPT v1 bytes (checkpoint.hpp:122-245)."""
+    meta = np.ascontiguousarray(info.meta, dtype=np.float64) if info.meta is not None else None
+    size = C.c_size_t()
+    args = (agent.h, info.parent_pod, info.mutation_seed, info.algo_tag.encode(),
+            _p(meta, C.c_double) if meta is not None else None)
+    agent.ctx.lib.prb_checkpoint_encode(*args, None, 0, C.byref(size))
+    out = np.zeros(size.value, dtype=np.uint8)
+    agent.ctx.lib.prb_checkpoint_encode(*args, _p(out, C.c_uint8), out.size, C.byref(size))
+    return out.tobytes()
+
+
+def checkpoint_decode(agent: Agent, data: bytes) -> CheckpointInfo:
+    """decode_checkpoint + artifact_from_tensors into `agent` (checkpoint.hpp:145-303)."""
+    b = np.frombuffer(data, dtype=np.uint8).copy()
+    parent, seed, has = C.c_int64(), C.c_uint64(), C.c_int()
+    tag = C.create_string_buffer(256)
+    meta = np.zeros(3)
+    agent.ctx.lib.prb_checkpoint_decode(agent.h, _p(b, C.c_uint8), b.size, C.byref(parent), C.byref(seed), tag, 256,
+                                        _p(meta, C.c_double), C.byref(has))
+    return CheckpointInfo(parent.value, seed.value, tag.value.decode(), tuple(meta) if has.value else None)
+
+
+def save_checkpoint(agent: Agent, path: str, info: CheckpointInfo = CheckpointInfo()) -> None:
+    meta = np.ascontiguousarray(info.meta, dtype=np.float64) if info.meta is not None else None
+    agent.ctx.lib.prb_checkpoint_save(agent.h, path.encode(), info.parent_pod, info.mutation_seed,
+                                      info.algo_tag.encode(), _p(meta, C.c_double) if meta is not None else None)
+
+
+def load_checkpoint(agent: Agent, path: str) -> CheckpointInfo:
+    parent, seed, has = C.c_int64(), C.c_uint64(), C.c_int()
+    tag = C.create_string_buffer(256)
+    meta = np.zeros(3)
+    agent.ctx.lib.prb_checkpoint_load(agent.h, path.encode(), C.byref(parent), C.byref(seed), tag, 256,
+                                      _p(meta, C.c_double), C.byref(has))
+    return CheckpointInfo(parent.value, seed.value, tag.value.decode(), tuple(meta) if has.value else None)

@@ -199,8 +199,7 @@ class PodPopulation:
         fresh = 0
         for p in range(self.P):
             if k == 0 or self.rng.random() < self.fresh_prob:
-                flat = pr.artifact_init(self.S, self.A, int(self.rng.integers(0, 2**63)))
-                self.agents[p].set(flat)
+                self.agents[p].init_device(int(self.rng.integers(0, 2**63)))  # artifact_init on the device
                 fresh += 1
             else:
                 self.agents[p].copy_from(self.elites[int(self.rng.integers(0, k))])

@@ -7,6 +7,7 @@ file so ref_golden.npz stays byte-identical.
 Run from the repo root after build():  python tests/golden/make_golden_r2.py
 Reference calls used:
   leaderboard_update + Leaderboard::refresh_stats   tournament.hpp:66-119
+  encode_checkpoint(artifact_to_tensors(...))       checkpoint.hpp:122-245
 """
 import ctypes as C
 import os
@@ -16,7 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
-from oracle_bind import load_ref, ptr, I64, SZ  # noqa: E402
+from oracle_bind import load_ref, ptr, I64, SZ, U8  # noqa: E402
 
 LBS_SHAPE = (5, 2, (4,))  # S, A, hidden: P = 65
 
@@ -61,6 +62,24 @@ def main():
     out.update(lbs_cand=np.array(cands, np.float32), lbs_scores=np.array(scores), lbs_cap=np.array(caps),
                lbs_board=np.array(boards), lbs_mean=np.array(means), lbs_var=np.array(vars_),
                lbs_shape=np.array([S, A, *hidden], np.int64))
+
+    # PODRCKPT v1 bytes written by the reference (checkpoint.hpp: encode_checkpoint(artifact_to_tensors))
+    # for a small artifact with Adam state, lineage, a custom algo tag and meta; and without meta
+    S2, A2, hid2 = 4, 2, np.array([3], dtype=np.uint64)
+    P2 = param_count(S2, A2, (3,))
+    ck_flat = rng.normal(size=P2); ck_m = rng.normal(size=P2) * 1e-2; ck_v = rng.uniform(0, 1e-3, P2)
+    hyper = np.array([0.9, 0.999, 1e-8, 3e-4])
+    meta = np.array([12.5, 4096.0, -0.75])
+    blobs = []
+    for with_meta, tag, parent, mseed in ((True, b"ppo", 7, 2**63 + 12345), (False, b"ppo-b200", -1, 99)):
+        n = ref.ref_checkpoint_encode(ptr(ck_flat), ptr(ck_m), ptr(ck_v), 17, ptr(hyper), S2, A2, ptr(hid2, SZ), 1,
+                                      parent, mseed, tag, ptr(meta) if with_meta else None, None)
+        buf = np.zeros(n, np.uint8)
+        ref.ref_checkpoint_encode(ptr(ck_flat), ptr(ck_m), ptr(ck_v), 17, ptr(hyper), S2, A2, ptr(hid2, SZ), 1,
+                                  parent, mseed, tag, ptr(meta) if with_meta else None, ptr(buf, U8))
+        blobs.append(buf)
+    out.update(ck_flat=ck_flat, ck_m=ck_m, ck_v=ck_v, ck_hyper=hyper, ck_meta=meta, ck_bytes_meta=blobs[0],
+               ck_bytes_nometa=blobs[1], ck_shape=np.array([S2, A2, 3], np.int64))
 
     path = os.path.join(HERE, "ref_golden_r2.npz")
     np.savez_compressed(path, **out)

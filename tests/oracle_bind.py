@@ -162,6 +162,11 @@ def load_ref(path: str = REF_EXACT_SO):
                                           I64, SZ, D, D]
     lib.ref_leaderboard_sequence.restype = C.c_int
     lib.ref_leaderboard_sequence.argtypes = [D, I64, C.c_size_t, C.c_size_t, I64, D, SZ, I64]
+    lib.ref_checkpoint_encode.restype = C.c_size_t
+    lib.ref_checkpoint_encode.argtypes = [D, D, D, C.c_int64, D, C.c_size_t, C.c_size_t, SZ, C.c_int, C.c_int64,
+                                          C.c_uint64, C.c_char_p, D, U8]
+    lib.ref_checkpoint_decode.restype = C.c_int
+    lib.ref_checkpoint_decode.argtypes = [U8, C.c_size_t, D, D, D, I64, I64, U64]
     lib.ref_synthetic_market.restype = None
     lib.ref_synthetic_market.argtypes = [C.c_uint64, C.c_int, C.c_size_t, D, D, D]
     lib.ref_bench_ppo.restype = C.c_double
