@@ -16,14 +16,16 @@ the C oracle (oracle/podracer_oracle.c):
     within 1e-9 relative of an fp64 host reduction.
   * ppo_update (ppo.hpp:249-296) at 181-64-64-30 / 181-64-64-1, minibatch 1,024, buffer 65,536
     (a real collected buffer), one epoch = 64 Adam steps under the reference's own std::shuffle
-    permutation, against orc_ppo_update.
+    permutation, against orc_ppo_update, plus a teacher-forced 65th step from the device state.
 
 Tolerances for the bf16 tcgen05 rollout MLP, vs the oracle's f64 forward on the same fp32
 parameters and observations (bf16 operands with hi+lo pairs for the private obs, fp32
 accumulation, tanh.approx):  value |d| <= 5e-2 (1 + |v|),  actor mean |d| <= 5e-2 (1 + |mu|)
 (checked through the log-prob: the recorded log-prob is log pi(a | mu_device); the test
 recomputes it from the oracle mean with the recorded action and bounds the difference by that
-mean tolerance propagated, see _lp_bound).
+mean tolerance propagated, see _lp_bound). Measured on B200 (stock, configs[1]): value
+3.7e-2 (1 + |v|), log-prob 0.26 of the bound; PointMass 3x256 (configs[2]): 1.0e-3, 0.019 -- that
+test therefore uses 5e-3.
 """
 import ctypes as C
 
@@ -270,48 +272,113 @@ def test_pointmass_collect_configs2_sampled_replay(pr, ctx, orc):
     assert np.array_equal(fin, f32(st))
     rec = {}
     check_mlp_vs_oracle(orc, agent, 6, 2, (256, 256, 256), b["states"], b["actions"], b["log_probs"], b["values"],
-                        5e-2, rec)
+                        5e-3, rec)
     print("RECORD configs[2]", rec)
     del ro
 
 
+def orc_update(orc, p, m, v, t, buf, rows, N, H, epochs, mb, perms):
+    """orc_ppo_update (f64) in place on (p, m, v); returns (t, [policy, value, entropy, steps])."""
+    tt = C.c_int64(t); so = np.zeros(4)
+    sl = {k: np.ascontiguousarray(buf[k][rows]) for k in ("states", "actions", "log_probs", "rewards", "dones",
+                                                         "values")}
+    offs = np.arange(N, dtype=np.uint64) * H; lens = np.full(N, H, dtype=np.uint64)
+    oc = PpoCfg(0.99, 0.95, 0.2, 0.01, 0.5, epochs, mb, N * H, 1e-3)
+    assert orc.orc_ppo_update(ptr(p), ptr(m), ptr(v), C.byref(tt), ptr(dims(S, 64, 64, K), SZ), 3,
+                              ptr(dims(S, 64, 64, 1), SZ), 3, ptr(sl["states"]), ptr(sl["actions"]),
+                              ptr(sl["log_probs"]), ptr(sl["rewards"]), ptr(sl["dones"], U8), ptr(sl["values"]),
+                              N * H, S, ptr(offs, SZ), ptr(lens, SZ), ptr(np.ascontiguousarray(buf["bootstrap"][:N])),
+                              N, C.byref(oc), ptr(perms, U64), ptr(so)) == 0
+    return tt.value, so
+
+
 def test_ppo_update_headline_shape_vs_oracle(pr, ctx, orc, ref):
     """ppo_update at the headline net (181-64-64-30 / 181-64-64-1), minibatch 1,024, on a real
-    collected buffer of 65,536 transitions (256 envs x 256 steps), one epoch = 64 sequential Adam
-    steps under the reference's own std::shuffle permutation, against orc_ppo_update on the same
-    fp32-rounded inputs (f64 arithmetic).  Bound: |p_device - p_oracle| <= 2e-5 per Adam step."""
+    collected buffer of 65,536 transitions (256 envs x 256 steps, old log-probs = the oracle's f64
+    values, so the first ratio is exactly 1 as in the reference), one epoch = 64 sequential Adam
+    steps under the reference's own std::shuffle permutation, against orc_ppo_update (f64), for
+    both device paths (fp32 SIMT, mode 0; tensor cores, mode 1).
+
+    Part 1, 64 free-running steps. The stock observation is unnormalised (prices and holdings in
+    the thousands), so a W1 change of lr moves a pre-activation by O(1): within a few steps the
+    ratios leave [0.8, 1.2], the actor's gradient comes from whichever samples sit inside the clip
+    range, and the actor's trajectory is chaotic under rounding -- measured for the fp32 SIMT path,
+    the device and f64 actor updates end uncorrelated (|dp| ~ |update|) while the critic, whose
+    loss is smooth, stays within 3% and its Adam moments within 0.3%. Bounded: the critic's
+    parameters and moments, the mean value loss and entropy, the policy loss within 10%, the
+    actor's update norm within 25% of the oracle's.
+    Part 2, teacher-forced step 65 at the drifted state (ratios far from 1, the clip active): from
+    the device state after part 1, one more minibatch (envs 0-3, 1,024 transitions) on the device
+    and on the oracle from the SAME (params, m, v, t); the update vectors must agree to a small
+    fraction (measured: SIMT 7.4e-6, tensor cores 3.9e-3 relative) -- the per-step precision claim at the headline shape."""
     N, H = 256, 256
     n = N * H
     m, ind, market = stock_market(pr, ctx)
     env = pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(), 1500, 2047, N)
     env.reset(5)
     agent = pr.Agent.init(ctx, S, K, seed=7)
-    ro = pr.Rollout.for_env(env, H)
-    ro.collect(agent, env, seed=77)
-    buf = ro.download()
+    ro0 = pr.Rollout.for_env(env, H)
+    ro0.collect(agent, env, seed=77)
+    buf = ro0.download()
+    flat = agent.flatten_params()
+    actor, log_std, _ = split_flat(S, K, (64, 64), flat)
+    pa = actor.size + K  # actor + log_std | critic
+    mean = oracle_mlp(orc, actor, dims(S, 64, 64, K), buf["states"])
+    buf["log_probs"] = np.array([orc.orc_gaussian_row_log_prob(ptr(log_std), K, ptr(np.ascontiguousarray(mean[i])),
+                                                               ptr(np.ascontiguousarray(buf["actions"][i])))
+                                 for i in range(n)])
+    ro = pr.Rollout.raw(ctx, N, H, S, K)
+    ro.upload(buf["states"], buf["actions"], buf["log_probs"], buf["rewards"], buf["dones"], buf["values"],
+              buf["bootstrap"])
+    N1 = 4  # part 2 sub-buffer: envs 0..3 (rows are env-major in the download)
+    ro1 = pr.Rollout.raw(ctx, N1, H, S, K)
+    r1 = slice(0, N1 * H)
+    ro1.upload(*(np.ascontiguousarray(buf[k][r1]) for k in ("states", "actions", "log_probs", "rewards", "dones",
+                                                            "values")), np.ascontiguousarray(buf["bootstrap"][:N1]))
     epochs, mb, seed = 1, 1024, 4242
     perms = np.zeros(epochs * n, dtype=np.uint64)
     ref.ref_ppo_permutations(seed, n, epochs, ptr(perms, U64))
+    perm1 = np.zeros(mb, dtype=np.uint64)
+    ref.ref_ppo_permutations(seed + 1, mb, 1, ptr(perm1, U64))
     cfg = pr.PpoConfig(epochs_per_update=epochs, minibatch_size=mb, buffer_size=n)
-    new, stats = pr.ppo_update(agent, ro, cfg, seed, perm=perms)
-    flat = agent.flatten_params()
-    fo = flat.copy(); mo = np.zeros(flat.size); vo = np.zeros(flat.size); to = C.c_int64(0); so = np.zeros(4)
-    offs = np.arange(N, dtype=np.uint64) * H; lens = np.full(N, H, dtype=np.uint64)
-    oc = PpoCfg(0.99, 0.95, 0.2, 0.01, 0.5, epochs, mb, n, 1e-3)
-    assert orc.orc_ppo_update(ptr(fo), ptr(mo), ptr(vo), C.byref(to), ptr(dims(S, 64, 64, K), SZ), 3,
-                              ptr(dims(S, 64, 64, 1), SZ), 3, ptr(buf["states"]), ptr(buf["actions"]),
-                              ptr(buf["log_probs"]), ptr(buf["rewards"]), ptr(buf["dones"], U8), ptr(buf["values"]),
-                              n, S, ptr(offs, SZ), ptr(lens, SZ), ptr(buf["bootstrap"]), N, C.byref(oc),
-                              ptr(perms, U64), ptr(so)) == 0
-    p, mm, vv, t = new.get()
+    cfg1 = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=mb)
+    fo, mo, vo = flat.copy(), np.zeros(flat.size), np.zeros(flat.size)
+    to, so = orc_update(orc, fo, mo, vo, 0, buf, slice(0, n), N, H, epochs, mb, perms)
     steps = epochs * (n // mb)
-    dp = float(np.max(np.abs(p - fo)))
-    print(f"RECORD ppo_update headline: {steps} steps, max|dp| {dp:.3e} (bound {steps * 2e-5:.3e}), "
-          f"policy loss {stats.mean_policy_loss:.6g} vs {so[0]:.6g}, value loss {stats.mean_value_loss:.6g} vs "
-          f"{so[1]:.6g}")
-    assert t == to.value == steps and stats.minibatches == so[3] == steps
-    assert dp <= steps * 2e-5
-    assert abs(stats.mean_policy_loss - so[0]) <= 1e-4 * (1 + abs(so[0]))
-    assert abs(stats.mean_value_loss - so[1]) <= 1e-4 * (1 + abs(so[1]))
-    assert abs(stats.mean_entropy - so[2]) <= 1e-5 * (1 + abs(so[2]))
+    rl2 = lambda x, y: float(np.linalg.norm(x - y) / np.linalg.norm(y))
+    for mode, tol_critic, tol65 in ((0, 0.05, 1e-4), (1, 0.1, 0.02)):  # measured 0.029/7.4e-6, 0.050/3.9e-3
+        agent.set_ppo_mode(mode)
+        new, stats = pr.ppo_update(agent, ro, cfg, seed, perm=perms)
+        p, mm, vv, t = new.get()
+        r = dict(actor_rel=float(np.linalg.norm((p - fo)[:pa]) / np.linalg.norm((fo - flat)[:pa])),
+                 critic_rel=float(np.linalg.norm((p - fo)[pa:]) / np.linalg.norm((fo - flat)[pa:])),
+                 m_actor=rl2(mm[:pa], mo[:pa]), m_critic=rl2(mm[pa:], mo[pa:]),
+                 v_actor=rl2(vv[:pa], vo[:pa]), v_critic=rl2(vv[pa:], vo[pa:]),
+                 pl=(stats.mean_policy_loss, so[0]), vl=(stats.mean_value_loss, so[1]),
+                 ent=(stats.mean_entropy, so[2]))
+        assert t == to == steps and stats.minibatches == so[3] == steps
+        # part 2: one teacher-forced step from the device state
+        a2 = pr.Agent(ctx, S, K)
+        a2.set(p, mm, vv, t)
+        a2.set_ppo_mode(mode)
+        n2, st2 = pr.ppo_update(a2, ro1, cfg1, seed + 1, perm=perm1)
+        p2, m2, v2, t2 = n2.get()
+        fo2, mo2, vo2 = p.copy(), mm.copy(), vv.copy()
+        t2o, so2 = orc_update(orc, fo2, mo2, vo2, t, buf, r1, N1, H, 1, mb, perm1)
+        dd, do = p2 - p, fo2 - p
+        r["step65_max_over_lr"] = float(np.max(np.abs(dd - do)) / 1e-3)
+        r["step65_rel"] = rl2(dd, do)
+        r["step65_pl"] = (st2.mean_policy_loss, so2[0])
+        assert t2 == t2o == t + 1
+        r["actor_update_norm_ratio"] = float(np.linalg.norm((p - flat)[:pa]) / np.linalg.norm((fo - flat)[:pa]))
+        print(f"RECORD ppo_update headline mode {mode}: {r}")
+        assert r["m_critic"] <= 0.01 and r["v_critic"] <= 0.01 and r["critic_rel"] <= tol_critic
+        un = r["actor_update_norm_ratio"]
+        assert 0.8 <= un <= 1.25 and np.isfinite(p).all()
+        assert abs(stats.mean_policy_loss - so[0]) <= 0.1 * abs(so[0])
+        assert abs(stats.mean_value_loss - so[1]) <= 1e-5 * abs(so[1])
+        assert abs(stats.mean_entropy - so[2]) <= 1e-3 * abs(so[2])
+        assert r["step65_rel"] <= tol65
+        assert abs(st2.mean_policy_loss - so2[0]) <= 1e-3 * (1 + abs(so2[0]))
+    agent.set_ppo_mode(0)
     assert np.array_equal(agent.flatten_params(), flat)  # purity (ppo.hpp:246-248)
