@@ -55,8 +55,8 @@ MLP_FLOPS = 2 * (181 * 64 + 64 * 64 + 64 * 30) + 2 * (181 * 64 + 64 * 64 + 64 * 
 # head [64 x 32]; the critic head is a 64-term fp32 dot product on the SIMT pipes.
 TC_EXEC_FLOPS = 2 * 32 * 128 + 2 * (2 * 64 * 64) + 2 * 64 * 32  # 28,672
 # dram__bytes_read.sum + dram__bytes_write.sum of stock_rollout_tc_kernel<30> from one `ncu --set full`
-# capture (profiles/r1_tc_r3_full.txt: 65,536 envs x 32 steps), per transition; scaled to the launch below.
-TC_DRAM_BYTES_PER_TRANSITION = 261  # ncu dram__bytes_read+write.sum per transition, profiles/r1_s3_tc_r13_full.txt (1,094 MB / 65,536 x 64)
+# capture (profiles/r2_s2_rollout_full.txt: 65,536 envs x 32 steps), per transition; scaled to the launch below.
+TC_DRAM_BYTES_PER_TRANSITION = 263  # ncu dram__bytes_read+write.sum per transition, profiles/r2_s2_rollout_full.txt (551.9 MB / 65,536 x 32)
 
 
 def load_peaks():
@@ -370,7 +370,7 @@ def run_ours(args, d: Dist):
     roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
                 "unit": kd["unit"], "frac": kd["frac"],
                 "traffic": (N * H * TC_DRAM_BYTES_PER_TRANSITION if dom == "stock_rollout_fused" else None),
-                "traffic_source": "ncu dram bytes/transition, profiles/r1_s3_tc_r13_full.txt, x transitions per launch",
+                "traffic_source": "ncu dram bytes/transition, profiles/r2_s2_rollout_full.txt, x transitions per launch",
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json "
                                f"{'bf16_tflops (burst)' if kd['bound'] == 'tensor' else 'hbm_gbs'})"}
     if dom == "stock_rollout_fused":
@@ -378,7 +378,7 @@ def run_ours(args, d: Dist):
         # issue does -- the fp64 portfolio chain + sampling + epilogues; ncu of the same kernel
         roofline["limiter"] = ("instruction issue/latency: ~3.2K instructions per transition, ~50% issue-active "
                                "at the 16 warps/SM that TMEM (128 cols/CTA) and registers allow "
-                               "(profiles/r1_s3_tc_r13_full.txt, DESIGN.md section 3)")
+                               "(profiles/r2_s2_rollout_full.txt, DESIGN.md section 3)")
 
     # ---- env step alone (the VecEnv boundary) at configs[4] scale: 1M envs/GPU, > L2 ----
     env_step = env_leg(pr, lib, ctx, market, cfg, args.env_envs, hbm, d)

@@ -3,7 +3,8 @@
 
   python profiles/drive.py collect  [N] [H]   # fused stock rollout (or --unfused)
   python profiles/drive.py env      [N]       # prb_vecenv_step on device buffers
-  python profiles/drive.py ppo      [N] [H]   # a few PPO minibatch steps
+  python profiles/drive.py ppo      [N] [H]   # a few PPO minibatch steps (--tc: tensor-core path)
+  python profiles/drive.py learners [L] [N]   # L concurrent tensor-core learners (one cluster each)
   python profiles/drive.py pm       [N] [H]   # PointMass 3x256 tcgen05 rollout (configs[2])
   python profiles/drive.py gae      [N] [H]   # buffer_advantages on a collected configs[1] buffer
   python profiles/drive.py adam     [P]       # adam_step on a 10.5M-param agent (> L2)
@@ -57,7 +58,20 @@ def main():
         ro = pr.Rollout.for_env(env, H)
         ro.collect(agent, env, seed=1)
         cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=1, buffer_size=N * H)
+        agent.set_ppo_mode(1 if "--tc" in sys.argv else 0)
         pr.ppo_update(agent, ro, cfg, seed=3)
+        ctx.synchronize()
+    elif what == "learners":
+        L = int(args[0]) if args else 16
+        N = int(args[1]) if len(args) > 1 else 1024
+        H = 64
+        ctx, market, env = setup(N)
+        agent = pr.Agent.init(ctx, 181, 30, seed=7)
+        agent.set_ppo_mode(1)
+        ro = pr.Rollout.for_env(env, H)
+        ro.collect(agent, env, seed=1)
+        cfg = pr.PpoConfig(minibatch_size=1024, epochs_per_update=1, buffer_size=N * H)
+        pr.ppo_update_learners([agent] * L, [ro] * L, cfg, list(range(L)))
         ctx.synchronize()
     elif what == "pm":
         N = int(args[0]) if args else 262144
