@@ -232,7 +232,8 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 // ~5e-4) or from a rounded h would be noise (the backward multiplies by it, nn.hpp:122-127)
 __device__ __forceinline__ void tanh_d(float z, float& h, float& d) {
   const float t = __expf(-2.f * fabsf(z));
-  const float r = __frcp_rn(1.f + t);
+  float r;  // 1 / (1 + t), t in (0, 1]: the approximate reciprocal is within 1 ulp
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + t));
   h = copysignf((1.f - t) * r, z);
   d = 4.f * t * r * r;
 }
@@ -373,7 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   // (after cp.async.wait_all + a barrier) turns it into the bf16 hi / lo X tiles, one row per
   // thread (conflict-free 16-byte stores).
   float* gst = reinterpret_cast<float*>(smem + kOffGather);
-  const int gs = (32 + a.nrest + 3) | 1;  // odd row stride: row-per-thread reads are conflict-free
+  // 8-byte copies of the shared-feature rows when they are 8-byte aligned (the stock pod: F = 150)
+  const bool rest8 = a.obs_mode == 1 && (a.F % 2) == 0 && (a.nrest % 2) == 0 && a.nrest <= 150 &&
+                     (reinterpret_cast<uintptr_t>(ch.feat) & 7) == 0;
+  // row stride: odd (row-per-thread reads of gather_convert conflict-free); with 8-byte copies
+  // 2 mod 4 floats (column 32 stays 8-byte aligned) and gs / 2 odd (2-way conflicts at most)
+  const int gs = rest8 ? (32 + a.nrest + 6) / 4 * 4 + 2 : (32 + a.nrest + 3) | 1;
   // the minibatch rows of step st resolved ahead of time (Feistel / injected permutation and the
   // shared-feature row, whose dependent loads would otherwise serialise the gather): s_next[q]
   auto resolve_rows = [&](int64_t st) {
@@ -407,7 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       }
       float* row = gst + q * gs;
       for (int k = lane; k < a.npriv; k += 32) cp_async4(row + k, prv + k);
-      for (int k = lane; k < a.nrest; k += 32) cp_async4(row + 32 + k, rest + k);
+      if (rest8) {  // the shared-feature rows are 8-byte aligned: half the copies
+        for (int k = lane; 2 * k < a.nrest; k += 32) cp_async8(row + 32 + 2 * k, rest + 2 * k);
+      } else {
+        for (int k = lane; k < a.nrest; k += 32) cp_async4(row + 32 + k, rest + k);
+      }
       if (lane == 0) {
         ridx[q] = i;
         cp_async4(row + gs - 3, ch.logp + i);
@@ -980,7 +990,9 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       if (!early) gather_issue();
       cp_async_wait_all();
       __syncthreads();
+      TCMARK(26);
       gather_convert();
+      TCMARK(27);
       load_image();
     }
     TCMARK(17);
