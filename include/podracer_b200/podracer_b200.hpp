@@ -231,6 +231,11 @@ class Agent {
     a->set(flat, nullptr, nullptr, 0, lr);
     return a;
   }
+  // artifact_init on the device (same mt19937_64 draws, bit-exact; Adam state zeroed): the
+  // generator's fresh pods never touch the host (tournament.hpp:142-144)
+  void init_device(std::uint64_t seed, double lr) { check(prb_agent_init_device(h_, seed, lr)); }
+  // 0: fp32 SIMT update over the whole GPU (default); 1: tensor-core update, one cluster per learner
+  void set_ppo_mode(int mode) { check(prb_agent_set_ppo_mode(h_, mode)); }
   std::unique_ptr<Agent> clone() const {
     auto b = std::make_unique<Agent>(*ctx_, S_, A_, hidden_);
     check(prb_agent_copy(b->h_, h_));
@@ -335,6 +340,26 @@ inline void worker_collect(const Agent& a, VectorizedEnvironment& env, Transitio
   check(prb_rollout_collect(buf.get(), a.get(), env.get(), seed));
 }
 
+// worker_collect of every pod of a GPU in ONE launch (per-pod weights, buffers and seeds);
+// identical to P worker_collect calls
+inline void worker_collect_pods(const std::vector<const Agent*>& agents, const std::vector<VectorizedEnvironment*>& envs,
+                                const std::vector<TransitionBuffer*>& bufs, const std::vector<std::uint64_t>& seeds) {
+  const std::size_t P = agents.size();
+  if (envs.size() != P || bufs.size() != P || seeds.size() != P)
+    throw DimensionError("worker_collect_pods: " + std::to_string(P) + " agents, " + std::to_string(envs.size()) +
+                         " envs, " + std::to_string(bufs.size()) + " buffers, " + std::to_string(seeds.size()) +
+                         " seeds");
+  std::vector<prb_rollout> r(P);
+  std::vector<prb_agent> a(P);
+  std::vector<prb_vecenv> e(P);
+  for (std::size_t p = 0; p < P; ++p) {
+    r[p] = bufs[p]->get();
+    a[p] = agents[p]->get();
+    e[p] = envs[p]->get();
+  }
+  check(prb_rollout_collect_pods(r.data(), a.data(), e.data(), P, seeds.data()));
+}
+
 // buffer_advantages ppo.hpp:212-244 -> (advantages, returns), reference index space
 inline std::pair<std::vector<double>, std::vector<double>> buffer_advantages(TransitionBuffer& buf,
                                                                              const PpoConfig& cfg,
@@ -354,6 +379,55 @@ inline std::pair<std::unique_ptr<Agent>, PpoUpdateStats> ppo_update(const Agent&
   prb_ppo_stats st{};
   check(prb_ppo_update(a.get(), buf.get(), &c, seed, perm ? perm->data() : nullptr, out->get(), &st));
   return {std::move(out), PpoUpdateStats{st.mean_policy_loss, st.mean_value_loss, st.mean_entropy, st.minibatches}};
+}
+
+// The learner phase of pod_train (pod.hpp:436-461): learner l = ppo_update(*agents[l], *bufs[l],
+// cfg, seeds[l]); all learners in ONE tensor-core launch (a thread-block cluster each).
+inline std::pair<std::vector<std::unique_ptr<Agent>>, std::vector<PpoUpdateStats>> ppo_update_learners(
+    const std::vector<const Agent*>& agents, const std::vector<TransitionBuffer*>& bufs, const PpoConfig& cfg,
+    const std::vector<std::uint64_t>& seeds) {
+  const std::size_t L = agents.size();
+  if (bufs.size() != L || seeds.size() != L)
+    throw DimensionError("ppo_update_learners: " + std::to_string(L) + " agents, " + std::to_string(bufs.size()) +
+                         " buffers, " + std::to_string(seeds.size()) + " seeds");
+  std::vector<std::unique_ptr<Agent>> outs;
+  std::vector<prb_agent> src(L), dst(L);
+  std::vector<prb_rollout> r(L);
+  for (std::size_t l = 0; l < L; ++l) {
+    const Agent& a = *agents[l];
+    outs.push_back(std::make_unique<Agent>(a.context(), a.state_dim(), a.action_dim(), a.hidden()));
+    src[l] = a.get();
+    dst[l] = outs.back()->get();
+    r[l] = bufs[l]->get();
+  }
+  const prb_ppo_config c = cfg.c();
+  std::vector<prb_ppo_stats> st(L);
+  check(prb_ppo_update_learners(src.data(), r.data(), L, &c, seeds.data(), dst.data(), st.data()));
+  std::vector<PpoUpdateStats> stats;
+  for (const auto& x : st) stats.push_back(PpoUpdateStats{x.mean_policy_loss, x.mean_value_loss, x.mean_entropy,
+                                                          x.minibatches});
+  return {std::move(outs), std::move(stats)};
+}
+
+// save_checkpoint / load_checkpoint checkpoint.hpp:305-317 (PODRCKPT v1, the reference's bytes)
+inline void save_checkpoint(const Agent& a, const std::string& path, std::int64_t parent_pod = -1,
+                            std::uint64_t mutation_seed = 0, const std::string& algo_tag = "ppo") {
+  check(prb_checkpoint_save(a.get(), path.c_str(), parent_pod, mutation_seed, algo_tag.c_str(), nullptr));
+}
+struct CheckpointInfo {
+  std::int64_t parent_pod = -1;
+  std::uint64_t mutation_seed = 0;
+  std::string algo_tag;
+};
+inline CheckpointInfo load_checkpoint(Agent& a, const std::string& path) {
+  CheckpointInfo info;
+  char tag[256] = {0};
+  int has_meta = 0;
+  double meta[3];
+  check(prb_checkpoint_load(a.get(), path.c_str(), &info.parent_pod, &info.mutation_seed, tag, sizeof(tag), meta,
+                            &has_meta));
+  info.algo_tag = tag;
+  return info;
 }
 
 // EvaluationRecord pod.hpp:30-36 and evaluate pod.hpp:43-83: one episode per env of

@@ -232,6 +232,53 @@ int main() {
     EXPECT(threw_nan);
   }
 
+  // ---- pods on one GPU: grouped collect, concurrent learners, device init, checkpoints ----
+  {
+    const size_t NP = 128, H = 32;
+    std::vector<std::unique_ptr<pb::VectorizedEnvironment>> envs;
+    std::vector<std::unique_ptr<pb::TransitionBuffer>> bufs, solo;
+    std::vector<std::unique_ptr<pb::Agent>> agents;
+    for (int p = 0; p < 2; ++p) {
+      envs.push_back(pb::VectorizedEnvironment::stock(market, cfg, start, end, NP));
+      envs.back()->reset(50 + p);
+      bufs.push_back(std::make_unique<pb::TransitionBuffer>(*envs.back(), H));
+      agents.push_back(pb::Agent::init(ctx, S, K, 60 + p, 1e-3));
+    }
+    pb::worker_collect_pods({agents[0].get(), agents[1].get()}, {envs[0].get(), envs[1].get()},
+                            {bufs[0].get(), bufs[1].get()}, {70, 71});
+    for (int p = 0; p < 2; ++p) {  // the same pods collected one by one
+      auto e = pb::VectorizedEnvironment::stock(market, cfg, start, end, NP);
+      e->reset(50 + p);
+      solo.push_back(std::make_unique<pb::TransitionBuffer>(*e, H));
+      pb::worker_collect(*agents[p], *e, *solo.back(), 70 + p);
+      EXPECT(solo.back()->rewards() == bufs[p]->rewards());
+    }
+    pb::PpoConfig pc;
+    pc.epochs_per_update = 1;
+    pc.minibatch_size = 1024;
+    pc.buffer_size = NP * H;
+    for (auto& a : agents) a->set_ppo_mode(1);
+    auto [outs, stats] = pb::ppo_update_learners({agents[0].get(), agents[1].get()}, {bufs[0].get(), bufs[1].get()},
+                                                 pc, {80, 81});
+    EXPECT(outs.size() == 2 && stats.size() == 2);
+    for (int l = 0; l < 2; ++l) {  // each learner == its own ppo_update on the same path
+      auto [one, st] = pb::ppo_update(*agents[l], *bufs[l], pc, 80 + l);
+      EXPECT(one->flatten_params() == outs[l]->flatten_params());
+      EXPECT(st.minibatches == stats[l].minibatches && st.mean_policy_loss == stats[l].mean_policy_loss);
+      EXPECT(outs[l]->optimizer_t() == (int64_t)(NP * H / 1024));
+    }
+    pb::Agent fresh(ctx, S, K);
+    fresh.init_device(60, 1e-3);
+    EXPECT(fresh.flatten_params() == agents[0]->flatten_params());
+    const std::string path = "/tmp/podracer_b200_dropin.ckpt";
+    pb::save_checkpoint(*outs[1], path, 4, 99);
+    pb::Agent back(ctx, S, K);
+    const pb::CheckpointInfo info = pb::load_checkpoint(back, path);
+    EXPECT(info.parent_pod == 4 && info.mutation_seed == 99 && info.algo_tag == "ppo");
+    EXPECT(back.flatten_params() == outs[1]->flatten_params() && back.optimizer_t() == outs[1]->optimizer_t());
+    std::remove(path.c_str());
+  }
+
   if (failures) {
     std::fprintf(stderr, "%d failures\n", failures);
     return 1;
