@@ -100,6 +100,14 @@ void* prb_ctx_s::device_scratch(size_t bytes) {
   return scratch;
 }
 
+unsigned int* prb_ctx_s::last_cta_counter() {
+  if (!done_counter) {
+    PRB_CUDA(cudaMalloc(&done_counter, sizeof(unsigned int)));
+    PRB_CUDA(cudaMemsetAsync(done_counter, 0, sizeof(unsigned int), stream));
+  }
+  return done_counter;
+}
+
 void prb_ctx_s::sync() { PRB_CUDA(cudaStreamSynchronize(stream)); }
 
 cudaEvent_t prb_ctx_s::take_event() {
@@ -155,6 +163,7 @@ int prb_ctx_destroy(prb_ctx c) {
     cudaStreamSynchronize(c->stream);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->done_counter) cudaFree(c->done_counter);
     cudaStreamDestroy(c->stream);
     delete c;
   });

@@ -46,23 +46,38 @@ namespace {
 #ifndef PRB_GAE_ENVS
 #define PRB_GAE_ENVS 32
 #endif
+#ifndef PRB_GAE_STAGES
+#define PRB_GAE_STAGES 2
+#endif
 constexpr int kGaeWin = PRB_GAE_WIN;      // steps per tile window
 constexpr int kGaeSegWarps = PRB_GAE_SW;  // segments per window
 constexpr int kGaeEnvs = PRB_GAE_ENVS;    // envs per tile (one per lane of an env-warp)
+constexpr int kGaeStages = PRB_GAE_STAGES;  // tile buffers (tiles in flight + the one scanned)
 
 struct Welford {
   double n, mean, m2;
 };
 
+// 1 / x for the merge weights: the approximate reciprocal refined by two Newton steps (~1 ulp;
+// the merges' weights need ~1e-15, not a correctly rounded division on the reduction's tail)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
+// Chan et al.'s pairwise merge of (n, mean, M2) records
 __device__ __forceinline__ Welford merge(Welford a, Welford b) {
   if (b.n == 0.0) return a;
   if (a.n == 0.0) return b;
   const double n = a.n + b.n;
+  const double fb = b.n * rcp_nr(n);  // b's weight
   const double d = b.mean - a.mean;
   Welford r;
   r.n = n;
-  r.mean = a.mean + d * (b.n / n);
-  r.m2 = a.m2 + b.m2 + d * d * (a.n * b.n / n);
+  r.mean = fma(d, fb, a.mean);
+  r.m2 = a.m2 + b.m2 + d * d * (a.n * fb);
   return r;
 }
 
@@ -81,20 +96,21 @@ struct GaeMaps {  // time-major [H][N] r / V / adv / ret (fp32) and done (u8), b
 };
 
 // E envs per tile (E/32 env-warps x SW segment-warps; SEG = WIN / SW steps per thread).
-template <int WIN, int SW, int E, bool TMA>
+template <int WIN, int SW, int E, bool TMA, int ST = kGaeStages>
 __global__ void __launch_bounds__(E * SW)
     gae_scan_kernel(const __grid_constant__ GaeMaps maps, const float* __restrict__ rew,
                     const float* __restrict__ val, const uint8_t* __restrict__ done, const float* __restrict__ boot,
                     int N, int H, double gamma, double lambda, float* __restrict__ adv, float* __restrict__ ret,
-                    double* __restrict__ partials) {
+                    double* __restrict__ partials, unsigned int* __restrict__ counter, int normalize,
+                    double* __restrict__ stat) {
   constexpr int SEG = WIN / SW;
   constexpr int EW = E / 32;
   constexpr int T = E * SW;
   static_assert(SEG <= 32, "segment mask is 32 bits");
   using Tile = GaeTile<WIN, E>;
   extern __shared__ __align__(128) unsigned char gae_smem[];
-  Tile* tiles = reinterpret_cast<Tile*>(gae_smem);  // [2] double buffer
-  __shared__ __align__(8) uint64_t s_full[2];  // TMA transaction barriers of the two buffers
+  Tile* tiles = reinterpret_cast<Tile*>(gae_smem);  // [ST] ring of tile buffers
+  __shared__ __align__(8) uint64_t s_full[ST];  // TMA transaction barriers of the buffers
   __shared__ double2 s_ab[SW][E];             // (A, B) of each segment of each env
   __shared__ double s_carry[E];               // gae at the first step of the later window
   __shared__ float s_vlater[E];               // V at the first step of the later window
@@ -105,10 +121,8 @@ __global__ void __launch_bounds__(E * SW)
   const int ngroups = (N + E - 1) / E, nwin = (H + WIN - 1) / WIN;
   const int my_groups = (int)blockIdx.x < ngroups ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int ntiles = my_groups * nwin;
-  if (TMA && threadIdx.x == 0) {
-    tc::mbar_init(&s_full[0], 1);
-    tc::mbar_init(&s_full[1], 1);
-  }
+  if (TMA && threadIdx.x == 0)
+    for (int b = 0; b < ST; ++b) tc::mbar_init(&s_full[b], 1);
   __syncthreads();
   // tile k -> env group g, window wi (windows of a group from the last to the first)
   auto tile_of = [&](int k, int& g, int& wi) {
@@ -118,15 +132,16 @@ __global__ void __launch_bounds__(E * SW)
   auto issue = [&](int k) {
     int g, wi;
     tile_of(k, g, wi);
-    Tile& tb = tiles[k & 1];
+    Tile& tb = tiles[k % ST];
     if (TMA) {
       if (threadIdx.x == 0) {
-        tc::bulk_wait_read0();  // the stores of tile k - 2 have read this buffer
+        tc::bulk_wait_read0();  // the stores of tile k - ST have read this buffer
         // three boxes; rows past H and columns past N arrive zero-filled (never stored)
-        tc::mbar_arrive_expect_tx(&s_full[k & 1], (uint32_t)sizeof(Tile));
-        tc::tma_load_2d(&tb.r[0][0], &maps.r, g * E, wi * WIN, &s_full[k & 1]);
-        tc::tma_load_2d(&tb.v[0][0], &maps.v, g * E, wi * WIN, &s_full[k & 1]);
-        tc::tma_load_2d(&tb.d[0][0], &maps.d, g * E, wi * WIN, &s_full[k & 1]);
+        uint64_t* bar = &s_full[k % ST];
+        tc::mbar_arrive_expect_tx(bar, (uint32_t)sizeof(Tile));
+        tc::tma_load_2d(&tb.r[0][0], &maps.r, g * E, wi * WIN, bar);
+        tc::tma_load_2d(&tb.v[0][0], &maps.v, g * E, wi * WIN, bar);
+        tc::tma_load_2d(&tb.d[0][0], &maps.d, g * E, wi * WIN, bar);
       }
     } else {  // any N: element loads (synchronous)
       const int e0 = g * E, t0 = wi * WIN, len = min(WIN, H - t0);
@@ -141,15 +156,18 @@ __global__ void __launch_bounds__(E * SW)
       }
     }
   };
-  Welford w{0.0, 0.0, 0.0};
-  if (ntiles > 0) issue(0);
+  // this thread's stored advantages as sums shifted by the first one it stored (no division
+  // per tile; one Welford record at the end)
+  double sn = 0.0, sx0 = 0.0, ss1 = 0.0, ssq = 0.0;
+  constexpr int kAhead = TMA ? ST - 1 : 1;  // tiles in flight while one is scanned
+  for (int k = 0; k < kAhead && k < ntiles; ++k) issue(k);
   for (int k = 0; k < ntiles; ++k) {
-    if (k + 1 < ntiles) issue(k + 1);  // the next tile streams in while this one is scanned
-    if (TMA) tc::mbar_wait(&s_full[k & 1], (uint32_t)((k >> 1) & 1));
+    if (k + kAhead < ntiles) issue(k + kAhead);  // later tiles stream in while this one is scanned
+    if (TMA) tc::mbar_wait(&s_full[k % ST], (uint32_t)((k / ST) & 1));
     __syncthreads();  // (TMA: every thread past the wait; else: the element loads are visible)
     int g, wi;
     tile_of(k, g, wi);
-    Tile& tb = tiles[k & 1];
+    Tile& tb = tiles[k % ST];
     const int e = g * E + col;
     const bool live = e < N;
     const int t0 = wi * WIN, len = min(WIN, H - t0);
@@ -198,7 +216,6 @@ __global__ void __launch_bounds__(E * SW)
     // returns go to the tile's r / V rows (TMA) or straight to HBM (element path)
     if (live && slen > 0) {
       double gae = gin;
-      double x0 = 0.0, s1 = 0.0, sq = 0.0;  // shifted sums of this thread's stored advantages
 #pragma unroll
       for (int u = SEG - 1; u >= 0; --u)
         if (u < slen) {
@@ -215,17 +232,16 @@ __global__ void __launch_bounds__(E * SW)
           }
           // the statistics cover the stored fp32 values: the gather normalises exactly those
           const double a = (double)a32;
-          if (u == slen - 1) x0 = a;
-          const double dx = a - x0;
-          s1 += dx;
-          sq = fma(dx, dx, sq);
+          if (sn == 0.0 && u == slen - 1) sx0 = a;
+          const double dx = a - sx0;
+          ss1 += dx;
+          ssq = fma(dx, dx, ssq);
         }
+      sn += (double)slen;
       if (sw == 0) {  // this window's first step feeds the earlier window
         s_carry[col] = gae;
         s_vlater[col] = vfirst;
       }
-      const double n = (double)slen, mean = x0 + s1 / n;
-      w = merge(w, Welford{n, mean, fmax(sq - s1 * (s1 / n), 0.0)});
     }
     if (TMA) tc::fence_proxy_async();  // the staged rows, to the async proxy
     __syncthreads();                    // s_carry visible to the next tile; staged rows complete
@@ -237,6 +253,8 @@ __global__ void __launch_bounds__(E * SW)
   }
   if (TMA && threadIdx.x == 0) tc::bulk_wait0();
   if (!partials) return;
+  Welford w{0.0, 0.0, 0.0};
+  if (sn > 0.0) w = Welford{sn, sx0 + ss1 / sn, fmax(ssq - ss1 * (ss1 / sn), 0.0)};
   for (int o = 16; o > 0; o >>= 1) {
     Welford b;
     b.n = __shfl_xor_sync(0xffffffffu, w.n, o);
@@ -246,34 +264,45 @@ __global__ void __launch_bounds__(E * SW)
   }
   if (lane == 0) s_w[warp] = w;
   __syncthreads();
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
     Welford acc = s_w[0];
     for (int i = 1; i < T / 32; ++i) acc = merge(acc, s_w[i]);
     partials[3 * blockIdx.x + 0] = acc.n;
     partials[3 * blockIdx.x + 1] = acc.mean;
     partials[3 * blockIdx.x + 2] = acc.m2;
+    __threadfence();  // this CTA's record before its arrival
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
-}
-
-__global__ void gae_stats_kernel(const double* __restrict__ partials, int nblocks, int normalize,
-                                 double* __restrict__ stat) {
-  __shared__ Welford sw[256];
-  Welford w{0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
-    w = merge(w, Welford{partials[3 * b], partials[3 * b + 1], partials[3 * b + 2]});
-  sw[threadIdx.x] = w;
+  __syncthreads();
+  if (!s_last) return;
+  // the last CTA to finish merges every CTA's record (no second launch): per-thread strided
+  // merges, then a tree over the warps
+  __threadfence();
+  Welford acc{0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += T)
+    acc = merge(acc, Welford{__ldcg(partials + 3 * b), __ldcg(partials + 3 * b + 1), __ldcg(partials + 3 * b + 2)});
+  for (int o = 16; o > 0; o >>= 1) {
+    Welford b;
+    b.n = __shfl_xor_sync(0xffffffffu, acc.n, o);
+    b.mean = __shfl_xor_sync(0xffffffffu, acc.mean, o);
+    b.m2 = __shfl_xor_sync(0xffffffffu, acc.m2, o);
+    acc = merge(acc, b);
+  }
+  __syncthreads();
+  if (lane == 0) s_w[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    Welford acc = sw[0];
-    for (int i = 1; i < (int)blockDim.x; ++i) acc = merge(acc, sw[i]);
-    if (normalize && acc.n > 0.0) {
-      const double var = acc.m2 / acc.n;
-      stat[0] = acc.mean;
-      stat[1] = fmax(sqrt(var), 1e-8);  // ppo.hpp:240
+    Welford all = s_w[0];
+    for (int i = 1; i < T / 32; ++i) all = merge(all, s_w[i]);
+    if (normalize && all.n > 0.0) {
+      stat[0] = all.mean;
+      stat[1] = fmax(sqrt(all.m2 / all.n), 1e-8);  // ppo.hpp:240
     } else {
       stat[0] = 0.0;
       stat[1] = 1.0;
     }
+    *counter = 0u;  // ready for the next launch (stream-ordered)
   }
 }
 
@@ -283,7 +312,8 @@ void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8
                     size_t H, double gamma, double lambda, float* adv, float* ret, double* stat, int normalize) {
   PRB_REQUIRE(N < (1u << 31) && H < (1u << 31), PRB_ERR_CONFIG, "buffer_advantages: buffer too large");
   constexpr int E = kGaeEnvs, W = kGaeWin, SW = kGaeSegWarps;
-  constexpr size_t smem = 2 * sizeof(GaeTile<W, E>);
+  const bool tma0 = (N % 16) == 0;
+  const size_t smem = (tma0 ? kGaeStages : 2) * sizeof(GaeTile<W, E>);
   // TMA boxes need 16-byte row pitches (the u8 dones: N % 16 == 0)
   const bool tma = (N % 16) == 0;
   GaeMaps maps;
@@ -295,7 +325,8 @@ void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8
     encode_tmap_2d(&maps.adv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, adv, N, H, N * 4, E, W);
     encode_tmap_2d(&maps.ret, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ret, N, H, N * 4, E, W);
   }
-  const void* fn = tma ? (const void*)gae_scan_kernel<W, SW, E, true> : (const void*)gae_scan_kernel<W, SW, E, false>;
+  const void* fn =
+      tma ? (const void*)gae_scan_kernel<W, SW, E, true> : (const void*)gae_scan_kernel<W, SW, E, false, 2>;
   ensure_smem_attr(fn, smem);
   int occ = 0;
   PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, E * SW, smem));
@@ -305,20 +336,17 @@ void prb_gae_launch(prb_ctx ctx, const float* rew, const float* val, const uint8
   const int per_cta = (groups + resident - 1) / resident;
   const int grid = std::max(1, (groups + per_cta - 1) / per_cta);
   double* partials = stat ? static_cast<double*>(ctx->device_scratch((size_t)grid * 3 * sizeof(double))) : nullptr;
+  unsigned int* counter = stat ? ctx->last_cta_counter() : nullptr;
   {
     ProfScope prof(ctx, kProfGae);
     if (tma)
-      gae_scan_kernel<W, SW, E, true><<<grid, E * SW, smem, ctx->stream>>>(maps, rew, val, done, boot, (int)N, (int)H,
-                                                                           gamma, lambda, adv, ret, partials);
+      gae_scan_kernel<W, SW, E, true><<<grid, E * SW, smem, ctx->stream>>>(
+          maps, rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials, counter, normalize, stat);
     else
-      gae_scan_kernel<W, SW, E, false><<<grid, E * SW, smem, ctx->stream>>>(maps, rew, val, done, boot, (int)N,
-                                                                            (int)H, gamma, lambda, adv, ret, partials);
+      gae_scan_kernel<W, SW, E, false, 2><<<grid, E * SW, smem, ctx->stream>>>(
+          maps, rew, val, done, boot, (int)N, (int)H, gamma, lambda, adv, ret, partials, counter, normalize, stat);
   }
   PRB_CHECK_LAUNCH();
-  if (stat) {
-    gae_stats_kernel<<<1, 256, 0, ctx->stream>>>(partials, grid, normalize, stat);
-    PRB_CHECK_LAUNCH();
-  }
 }
 
 extern "C" {

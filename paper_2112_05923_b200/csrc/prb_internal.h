@@ -117,6 +117,8 @@ struct prb_ctx_s {
   size_t pinned_bytes = 0;
   void* scratch = nullptr;  // device scratch, grown on demand
   size_t scratch_bytes = 0;
+  unsigned int* done_counter = nullptr;  // zero between launches (last-CTA reductions reset it)
+  unsigned int* last_cta_counter();
   void* pinned_staging(size_t bytes);
   void* device_scratch(size_t bytes);
   void sync();

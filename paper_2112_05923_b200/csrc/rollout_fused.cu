@@ -458,13 +458,14 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
       const char* trace_path = debug_env("PRB_TC_TRACE");  // debug: clock64 phase trace of CTA 0
       DevBuf<unsigned long long> d_trace;
       if (trace_path) {
-        d_trace.alloc(kTcTraceLen);
+        // [kTcTraceLen] clock64 marks of CTA 0, then per CTA (smid, start, end) globaltimer stamps
+        d_trace.alloc(kTcTraceLen + 3 * (size_t)((N + 127) / 128));
         PRB_CUDA(cudaMemsetAsync(d_trace.p, 0, d_trace.bytes(), s));
         ta.trace = d_trace.p;
       }
       launch_stock_rollout_tc(ta, s);
       if (trace_path) {
-        std::vector<unsigned long long> hbuf(kTcTraceLen);
+        std::vector<unsigned long long> hbuf(d_trace.n);
         PRB_CUDA(cudaMemcpyAsync(hbuf.data(), d_trace.p, d_trace.bytes(), cudaMemcpyDeviceToHost, s));
         PRB_CUDA(cudaStreamSynchronize(s));
         if (FILE* f = fopen(trace_path, "wb")) {
