@@ -1327,6 +1327,7 @@ struct PpoWorkspace {
   DevBuf<uint8_t> tc_img;
   DevBuf<float> tc_slab;
   DevBuf<double> tc_stats;
+  DevBuf<uint32_t> tc_sync;
   DevBuf<PpoTcChain> tc_chain;
   DevBuf<int2> tc_pos;  // weight-image position of every parameter (for the net shape below)
   std::vector<int> tc_pos_key;
@@ -1625,7 +1626,10 @@ PpoTcChain make_tc_chain(const PpoTcArgs& t, prb_agent dst, prb_rollout r, PpoWo
   ws.tc_stats.ensure(4);
   PRB_CUDA(cudaMemsetAsync(ws.tc_img.p, 0, kPpoTcImgBytes, s));  // padding of the operand blocks
   PRB_CUDA(cudaMemsetAsync(ws.tc_stats.p, 0, 4 * sizeof(double), s));
+  ws.tc_sync.ensure(16);
+  PRB_CUDA(cudaMemsetAsync(ws.tc_sync.p, 0, 16 * sizeof(uint32_t), s));
   PpoTcChain c{};
+  c.sync = ws.tc_sync.p;
   c.params = dst->d_params.p;
   c.m = dst->d_m.p;
   c.v = dst->d_v.p;
@@ -1917,12 +1921,27 @@ int prb_ppo_update_learners(const prb_agent* srcs, const prb_rollout* rollouts, 
     }
     DevBuf<PpoTcChain> cbuf;
     upload_chains(t, chains, cbuf, s);
+    const char* tpath = debug_env("PRB_PPO_TC_TRACE");  // debug: phase marks of chain 0, step 8
+    DevBuf<unsigned long long> tbuf;
+    if (tpath) {
+      tbuf.alloc(32);
+      PRB_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes(), s));
+      t.trace = tbuf.p;
+    }
     {
       ProfScope prof(dsts[0]->ctx, kProfPpoFwdBwd);
       launch_ppo_tc(t, (int)L, s);
     }
     PRB_CHECK_LAUNCH();
     PRB_CUDA(cudaStreamSynchronize(s));
+    if (tpath) {
+      unsigned long long h[32];
+      PRB_CUDA(cudaMemcpy(h, tbuf.p, sizeof(h), cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen(tpath, "w")) {
+        for (int i = 0; i < 32; ++i) fprintf(f, "%d %lld\n", i, h[i] ? (long long)(h[i] - h[0]) : -1LL);
+        fclose(f);
+      }
+    }
     int first_code = 0, first_detail = 0;
     for (size_t l = 0; l < L; ++l) {
       int32_t st[2];

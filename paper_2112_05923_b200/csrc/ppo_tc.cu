@@ -1,11 +1,12 @@
-// ppo_tc.cu -- ppo_update (ppo.hpp:249-296) on the 5th-gen tensor cores, one thread-block
-// cluster per learner.
+// ppo_tc.cu -- ppo_update (ppo.hpp:249-296) on the 5th-gen tensor cores, a group of C
+// co-resident CTAs per learner.
 //
 // A learner's update is a chain of minibatch steps (gather_minibatch ppo.hpp:83-103 ->
 // detail::ppo_loss_grads :116-188 -> adam_step nn.hpp:164-182).  Here the C = ceil(mb / 128)
-// CTAs of one cluster run the whole chain (every epoch, every minibatch) in one launch, without
-// grid-wide barriers, so several learners (pod.hpp:436-461) run at once,
-// one cluster each.  Per step, CTA c of the cluster owns minibatch rows [128c, 128c + 128):
+// CTAs of one learner run the whole chain (every epoch, every minibatch) in one launch, with
+// barriers among those C CTAs only (ChainBar), so several learners (pod.hpp:436-461, SURVEY.md
+// §7 step 6) run at once, C CTAs each.  Per step, CTA c of a learner owns minibatch rows
+// [128c, 128c + 128):
 //
 //   gather    X = [private features hi | rest | 1] per row as bf16 hi + lo pairs  [128 x 192]
 //   L1        D = X_hi . W1 + X_lo . W1        (actor | critic: N = 128; b1 via the ones column)
@@ -18,11 +19,11 @@
 //   weight gradients, batch as the contraction dimension (both operands MN-major):
 //             dW3^T = d3^T . H2,  dW2^T = d2^T . H1,  dW1^T = d1^T . X_hi   (fp32 in TMEM)
 //   partials  TMEM -> this CTA's slab row (flat parameter order) + log_std / loss terms
-//   cluster barrier; CTA c sums the C slab rows of its 1/C parameter slice in rank order,
+//   learner barrier; CTA c sums the C slab rows of its 1/C parameter slice in rank order,
 //   evaluates its part of the finiteness gate (losses first, then gradients, the reference's
-//   order), exchanges the gate over DSMEM; if every part passed, Adam on its slice (fp32 master
+//   order), publishes its gate part; if every part passed, Adam on its slice (fp32 master
 //   weights, adam_param's explicit roundings) and the slice's entries of the bf16 weight image;
-//   cluster barrier; every CTA bulk-copies the image (72 KB) for the next step.
+//   learner barrier; every CTA bulk-copies the image (122 KB) for the next step.
 //
 // Every matrix lives in shared memory once, in the "row-fast core form" of tc.cuh (8x8 bf16 core
 // matrices, 8-row groups 128 B apart, 8-column chunks R*16 B apart), which is the K-major operand
@@ -36,6 +37,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "ppo_tc.h"
@@ -122,11 +124,30 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
-}
+// Barrier of a learner's C CTAs (co-resident by the cooperative launch): a monotonic arrival
+// counter in global memory, released by thread 0 after a CTA barrier (cumulative: the CTA's
+// writes before it), acquired by thread 0's spin, then a CTA barrier.  A thread-block cluster
+// would give a hardware barrier and DSMEM, but only 15 clusters of 8 fit on a B200 at once
+// (its GPC layout), so 16 learners -- configs[3]'s 8 pods x 2 -- would run in two waves.
+struct ChainBar {
+  uint32_t* ctr;
+  uint32_t target;
+  int C;
+  __device__ __forceinline__ void arrive() {
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    target += (uint32_t)C;
+  }
+  __device__ __forceinline__ void wait() {
+    if (threadIdx.x == 0) {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while ((int32_t)(v - target) < 0);
+    }
+    __syncthreads();
+  }
+};
 
 // Keyed balanced-Feistel bijection on [0, 2^bits), cycle-walked into [0, n) -- the same
 // permutation the SIMT update draws (ppo.cu), so both paths see the same minibatches.
@@ -309,7 +330,6 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t s_mma, s_mma2, s_img;
   __shared__ uint32_t s_tmem;
-  __shared__ uint32_t s_flags[8];  // gate parts of the cluster's CTAs (written over DSMEM)
   __shared__ float s_red[2][40];   // head-epilogue column sums (two row halves)
   __shared__ float s_db3[33];      // column sums of d3 (actor 0..31, critic 32)
   __shared__ float s_isig[32];     // 1 / sigma_d = exp(-log_std_d) of the step (0 past A)
@@ -320,10 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   __shared__ __align__(8) uint64_t s_red_bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C;
-  const uint32_t rank = tc::cluster_ctarank();
-  uint32_t chain_id;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(chain_id));
+  const uint32_t rank = blockIdx.x % (uint32_t)C, chain_id = blockIdx.x / (uint32_t)C;
   const PpoTcChain ch = a.chains[chain_id];
+  ChainBar cbar{ch.sync, 0u, C};
   const uint32_t sbase = tc::smem_u32(smem);
   uint8_t* img = ch.img;
   float* f32 = reinterpret_cast<float*>(smem + kOffF32);
@@ -339,7 +358,6 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     tc::mbar_init(&s_img, 1);
     tc::mbar_init(&s_red_bar, 1);
   }
-  if (tid < 8) s_flags[tid] = 0;
   if (tid < kXC) {  // X column -> W1 input row (the ones column -> the bias row S), -1 for padding
     int k = -1;
     if (tid < a.npriv) k = tid;
@@ -363,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   // ---- prologue: this slice's entries of the weight image from the master weights ----
   for (int p = p_lo + tid; p < p_hi; p += kThreads) img_store(a, img, p, ch.params[p]);
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  cluster_arrive();
+  cbar.arrive();
 
   // gather (gather_minibatch ppo.hpp:83-103) of step st into X_hi / X_lo and the row scalars.
   // Thread (row q, half hh) owns 96 of the 192 X columns; every load is issued before any
@@ -477,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   cp_async_wait_all();
   __syncthreads();
   gather_convert();
-  cluster_wait();  // the initial image is complete in global memory
+  cbar.wait();  // the initial image is complete in global memory
   load_image();
 
   int fail_code = 0, fail_detail = 0;
@@ -815,13 +833,13 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
     TCMARK(13);
     tc::fence_before_sync();
-    cluster_arrive();  // release: this CTA's slab row
-    cluster_wait();
+    cbar.arrive();  // release: this CTA's slab row
+    cbar.wait();
     TCMARK(14);
     // ---- reduce this CTA's parameter slice over the C slab rows (rank order), Adam (speculative),
     // gate.  The slice's C partial rows and its m / v / master weights are staged into shared
     // memory by bulk copies (the MMA operand regions are dead by now): one L2 round trip.  Adam's
-    // results stay in the staging area and the bf16 image is written at once; one cluster barrier
+    // results stay in the staging area and the bf16 image is written at once; one learner barrier
     // then both publishes the image and exchanges the gate, and only an accepted step's results
     // are stored to the master weights / moments (nn.hpp:169-171: a rejected step changes nothing;
     // the image is rebuilt from the master weights when the next update starts) ----
@@ -920,8 +938,8 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
     bad = __syncthreads_or(bad);
     TCMARK(15);
-    if (tid == 0) {  // this CTA's gradient verdict to every CTA of the cluster (DSMEM)
-      for (int c = 0; c < C; ++c) st_cluster_u32(tc::mapa_shared(&s_flags[rank], (uint32_t)c), (uint32_t)bad);
+    if (tid == 0) {  // this CTA's gradient verdict, read by every CTA of the learner after the barrier
+      *reinterpret_cast<volatile uint32_t*>(ch.sync + 8 + rank) = (uint32_t)bad;
       // losses (every CTA sums them in the same order) -- the reference checks these first
       double pl = 0.0, vl = 0.0, en = 0.0;
       for (int c = 0; c < C; ++c) {
@@ -938,12 +956,12 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     TCMARK(24);
     const bool more = st + 1 < a.steps;
     // the next rows' copies fly across the barrier when the staged m / v / w leave the gather
-    // area free (one piece, i.e. >= 5 CTAs per cluster at the stock pod's size)
+    // area free (one piece, i.e. >= 5 CTAs per learner at the stock pod's size)
     const bool early = npieces == 1 && 3 * piece * 4 <= (int)kOffGather;
     if (more && early) gather_issue();
     TCMARK(25);
-    cluster_arrive();
-    cluster_wait();
+    cbar.arrive();
+    cbar.wait();
     TCMARK(16);
     {
       const double pl = s_loss[0], vl = s_loss[1], en = s_loss[2];
@@ -953,7 +971,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       else if (!isfinite(en)) { code = PRB_ERR_NUMERIC; detail = 12; }
       else {
         for (int c = 0; c < C; ++c)
-          if (s_flags[c]) { code = PRB_ERR_NUMERIC; detail = 0; }
+          if (__ldcg(ch.sync + 8 + c)) { code = PRB_ERR_NUMERIC; detail = 0; }
       }
       if (code) {  // nn.hpp:169-171: nothing is updated; the update ends at the last accepted step
         fail_code = code;
@@ -982,8 +1000,8 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
         __syncthreads();
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      cluster_arrive();  // these image entries were written after the gate
-      cluster_wait();
+      cbar.arrive();  // these image entries were written after the gate
+      cbar.wait();
     }
     __syncthreads();  // the staging area is free: the next X tiles and the image may land
     if (more) {
@@ -1037,13 +1055,22 @@ void launch_ppo_tc(const PpoTcArgs& a, int nchains, cudaStream_t s) {
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)a.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA of a learner co-resident (its barrier)
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  PRB_CUDA(cudaLaunchKernelEx(&cfg, ppo_tc_kernel, a));
+  int dev = 0, sms = 0, occ = 0;
+  PRB_CUDA(cudaGetDevice(&dev));
+  PRB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ppo_tc_kernel, kThreads, kSmemBytes));
+  const int per_wave = std::max(1, sms * std::max(occ, 1) / a.C);  // learners resident at once
+  for (int c0 = 0; c0 < nchains; c0 += per_wave) {  // more learners than fit: waves
+    PpoTcArgs w = a;
+    w.chains = a.chains + c0;
+    const int n = std::min(per_wave, nchains - c0);
+    cfg.gridDim = dim3((unsigned)(a.C * n));
+    PRB_CUDA(cudaLaunchKernelEx(&cfg, ppo_tc_kernel, w));
+  }
 }
 
 }  // namespace prb

@@ -1,4 +1,4 @@
-// ppo_tc.h -- the tensor-core PPO update (ppo_tc.cu): one thread-block cluster per learner.
+// ppo_tc.h -- the tensor-core PPO update (ppo_tc.cu): a group of C co-resident CTAs per learner.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -17,6 +17,7 @@ struct PpoTcChain {
   float* slab;      // [C][Pp] per-CTA partial gradients + loss terms
   double* stats;    // [4] sums of policy loss, value loss, entropy, accepted steps
   int32_t* status;  // [2] error code, detail
+  uint32_t* sync;   // [16] zeroed before the launch: [0] barrier arrivals, [8 + c] CTA c's gate part
   const uint32_t* perm;  // injected [epochs][n] minibatch order (device indices) or null (Feistel from seed)
   uint64_t seed;
   float lr;
