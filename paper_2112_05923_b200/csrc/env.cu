@@ -613,7 +613,7 @@ int prb_vecenv_create_stock(prb_market m, const prb_stock_config* cfg, size_t st
       for (int i = 0; i < 4; ++i)
         for (int k = 0; k < K; ++k) feat[t * F + K + (size_t)i * K + k] = (float)m->indicators[((size_t)i * K + k) * T + t];
     }
-    env->d_feat.alloc(feat.size());
+    env->d_feat.alloc(feat.size() + 16);  // + padding: whole-row 16-byte bulk copies (ppo_tc.cu gather)
     PRB_CUDA(cudaMemcpyAsync(env->d_feat.p, feat.data(), feat.size() * sizeof(float), cudaMemcpyHostToDevice,
                              env->ctx->stream));
     env->d_balance.alloc(N);

@@ -80,12 +80,14 @@ constexpr uint32_t kOffRows = kOffF32 + 1040;          // per-row old_lp, adv, r
 constexpr uint32_t kOffRidx = kOffRows + 2048;         // per-row buffer index [128] u32
 constexpr uint32_t kSmemBytes = kOffRidx + 512;
 constexpr uint32_t kStageBytes = kOffRE;  // X_hi .. H2, dead during the reduction: slice staging
-constexpr uint32_t kOffGather = 98304;    // the next rows' fp32 staging [128][gs] (after X_hi / X_lo)
+constexpr uint32_t kOffGather = 98304;    // the next rows' fp32 staging [128][784 B] (after X_hi / X_lo;
+                                          // its last 2 KB overlap W2a, reloaded with the image)
 // image (global) = W1 block | RE | fp32 block, the smem bytes [kOffRC, +49152) ++ [kOffRE, +23568)
 // image (global) = W1 hi | W1 lo (bf16 pairs: W1 multiplies inputs of magnitude ~1e2, so the
 // first layer needs ~16-bit weights as well as inputs) | W2a W2c W3a W3c | fp32 block
 constexpr uint32_t kImgW1 = 49152, kImgRestOff = 2 * kImgW1, kImgRest = 22528 + 1040;
 static_assert(kImgRestOff + kImgRest == (uint32_t)kPpoTcImgBytes, "image size");
+static_assert(kOffGather + 128 * 784 + 64 <= kOffF32, "gather staging must end before the fp32 block");
 // where W1 lo lands in shared memory for the L1 MMAs: K-steps 0-3 in the dead upper 16 KB of RB,
 // K-steps 4-11 in H2's region (both free until L1 is done)
 constexpr uint32_t kOffW1loA = kOffRB + 49152, kOffW1loB = kOffRC + 49152;
@@ -338,6 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   __shared__ double s_loss[3];
   __shared__ int s_colk[kXC];
   __shared__ __align__(8) uint64_t s_red_bar;
+  __shared__ __align__(8) uint64_t s_gat;  // the gather's bulk row copies (128 arrivals per phase)
+  __shared__ uint32_t s_gsh[kRows];         // per staged row: private base | rest base << 8 (floats)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C;
   const uint32_t rank = blockIdx.x % (uint32_t)C, chain_id = blockIdx.x / (uint32_t)C;
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     tc::mbar_init(&s_mma2, 1);
     tc::mbar_init(&s_img, 1);
     tc::mbar_init(&s_red_bar, 1);
+    tc::mbar_init(&s_gat, kRows);
   }
   if (tid < kXC) {  // X column -> W1 input row (the ones column -> the bias row S), -1 for padding
     int k = -1;
@@ -383,21 +388,18 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   asm volatile("fence.proxy.async.global;" ::: "memory");
   cbar.arrive();
 
-  // gather (gather_minibatch ppo.hpp:83-103) of step st into X_hi / X_lo and the row scalars.
-  // Thread (row q, half hh) owns 96 of the 192 X columns; every load is issued before any
-  // conversion (one memory latency per gather, not one per column chunk).
-  // gather (gather_minibatch ppo.hpp:83-103) of step st, in two halves: gather_issue streams
-  // the rows' features (one warp per row: coalesced 4-byte cp.async, no registers held) and row
-  // scalars into an fp32 staging area [128][gs] laid out like the X columns; gather_convert
-  // (after cp.async.wait_all + a barrier) turns it into the bf16 hi / lo X tiles, one row per
-  // thread (conflict-free 16-byte stores).
+  // gather (gather_minibatch ppo.hpp:83-103) of step st, in two halves.  gather_issue: thread q
+  // (< 128) copies row q's features with 1-D bulk copies (the TMA engine: one instruction per row
+  // segment instead of one 4-byte cp.async per element) from the 16-byte-aligned address at or
+  // below the row's start, so the row lands in its 784-byte staging slot at a shift of 0-3 floats
+  // (kept in s_gsh; the allocations are padded for the overhang); the row scalars go by 4-byte
+  // cp.async straight to rows_f.  gather_convert (after the mbarrier, cp.async and a CTA
+  // barrier): one row half per thread, branch-free selects -> the bf16 hi / lo X tiles.
+  // Slot: obs_mode 1 = the private obs row at [0, 36) floats, the shared-feature row from 36;
+  // obs_mode 0 = the whole obs row (private | rest contiguous).
+  constexpr int kSlot = 196;  // floats (784 B, 16-byte multiple; 196 = 4 mod 32)
   float* gst = reinterpret_cast<float*>(smem + kOffGather);
-  // 8-byte copies of the shared-feature rows when they are 8-byte aligned (the stock pod: F = 150)
-  const bool rest8 = a.obs_mode == 1 && (a.F % 2) == 0 && (a.nrest % 2) == 0 && a.nrest <= 150 &&
-                     (reinterpret_cast<uintptr_t>(ch.feat) & 7) == 0;
-  // row stride: odd (row-per-thread reads of gather_convert conflict-free); with 8-byte copies
-  // 2 mod 4 floats (column 32 stays 8-byte aligned) and gs / 2 odd (2-way conflicts at most)
-  const int gs = rest8 ? (32 + a.nrest + 6) / 4 * 4 + 2 : (32 + a.nrest + 3) | 1;
+  uint32_t gat_phase = 0;
   // the minibatch rows of step st resolved ahead of time (Feistel / injected permutation and the
   // shared-feature row, whose dependent loads would otherwise serialise the gather): s_next[q]
   auto resolve_rows = [&](int64_t st) {
@@ -412,42 +414,53 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
   };
   auto gather_issue = [&]() {  // the rows in s_next (resolve_rows + a barrier before)
-    for (int q = warp; q < kRows; q += kThreads / 32) {
+    if (tid < kRows) {
+      const int q = tid;
       const uint2 e = s_next[q];
-      const bool valid = e.x != 0xffffffffu;
-      if (!valid) {
-        if (lane == 0) ridx[q] = 0xffffffffu;
-        continue;
-      }
-      const uint32_t i = e.x;
-      const float* prv;
-      const float* rest;
-      if (a.obs_mode == 1) {
-        prv = ch.obs + (size_t)i * a.Sp;
-        rest = ch.feat + (size_t)e.y * a.F;
-      } else {
-        prv = ch.obs + (size_t)i * a.S;
-        rest = prv + a.npriv;
-      }
-      float* row = gst + q * gs;
-      for (int k = lane; k < a.npriv; k += 32) cp_async4(row + k, prv + k);
-      if (rest8) {  // the shared-feature rows are 8-byte aligned: half the copies
-        for (int k = lane; 2 * k < a.nrest; k += 32) cp_async8(row + 32 + 2 * k, rest + 2 * k);
-      } else {
-        for (int k = lane; k < a.nrest; k += 32) cp_async4(row + 32 + k, rest + k);
-      }
-      if (lane == 0) {
+      float* slot = gst + q * kSlot;
+      if (e.x != 0xffffffffu) {
+        const uint32_t i = e.x;
+        const int nobs = a.obs_mode == 1 ? a.Sp : a.S;  // floats of the obs row
+        const uintptr_t po = reinterpret_cast<uintptr_t>(ch.obs + (size_t)i * nobs);
+        const uintptr_t po0 = po & ~(uintptr_t)15;
+        const int sh1 = (int)(po - po0) >> 2;
+        const uint32_t b1 = (uint32_t)((4 * (nobs + sh1) + 15) & ~15);
+        int sh2 = 0;
+        uint32_t b2 = 0;
+        uintptr_t pf0 = 0;
+        if (a.obs_mode == 1) {
+          const uintptr_t pf = reinterpret_cast<uintptr_t>(ch.feat + (size_t)e.y * a.F);
+          pf0 = pf & ~(uintptr_t)15;
+          sh2 = (int)(pf - pf0) >> 2;
+          b2 = (uint32_t)((4 * (a.F + sh2) + 15) & ~15);
+        }
+        tc::mbar_arrive_expect_tx(&s_gat, b1 + b2);
+        tc::bulk_g2s(slot, reinterpret_cast<const void*>(po0), b1, &s_gat);
+        if (b2) tc::bulk_g2s(slot + 36, reinterpret_cast<const void*>(pf0), b2, &s_gat);
         ridx[q] = i;
-        cp_async4(row + gs - 3, ch.logp + i);
-        cp_async4(row + gs - 2, ch.adv + i);
-        cp_async4(row + gs - 1, ch.ret + i);
+        s_gsh[q] = (uint32_t)sh1 | ((uint32_t)(a.obs_mode == 1 ? 4 + sh2 : sh1) << 8);
+        cp_async4(rows_f + q, ch.logp + i);
+        cp_async4(rows_f + 128 + q, ch.adv + i);
+        cp_async4(rows_f + 256 + q, ch.ret + i);
+      } else {
+        tc::mbar_arrive(&s_gat);
+        ridx[q] = 0xffffffffu;
+        s_gsh[q] = 0;
       }
     }
+  };
+  auto gather_wait = [&]() {  // the bulk rows and the scalar copies of gather_issue, then a barrier
+    tc::mbar_wait(&s_gat, gat_phase);
+    gat_phase ^= 1;
+    cp_async_wait_all();
+    __syncthreads();
   };
   auto gather_convert = [&]() {
     const int q = tid & 127, hh = tid >> 7;
     const bool valid = ridx[q] != 0xffffffffu;
-    const float* row = gst + q * gs;
+    const float* slot = gst + q * kSlot;
+    const int pb = (int)(s_gsh[q] & 0xff), rb = (int)(s_gsh[q] >> 8);  // private / rest bases
+    const int npriv = a.npriv, rend = 32 + a.nrest, onec = a.ones_col;
 #pragma unroll
     for (int ck = 0; ck < 12; ++ck) {
       uint32_t hi[4], lo[4];
@@ -456,22 +469,26 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
         float x2[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int c = (hh * 12 + ck) * 8 + 2 * j + u;
-          const bool use = valid && (c < a.npriv || (c >= 32 && c < 32 + a.nrest));
-          x2[u] = use ? row[c] : ((valid && c == a.ones_col) ? 1.f : 0.f);
+          const int c = hh * 96 + ck * 8 + 2 * j + u;
+          const bool priv = c < 32;
+          const int idx = (priv ? pb : rb) + c;  // rest column c sits at rb + c (see gather_issue)
+          const bool use = priv ? (c < npriv) : (c < rend);
+          const float v = slot[idx];  // always a shared-memory address (overhang lands in RE)
+          const float d = (c == onec) ? 1.f : 0.f;
+          x2[u] = valid ? (use ? v : d) : 0.f;
         }
         hi[j] = tc::pack_bf16(x2[0], x2[1]);
         lo[j] = tc::pack_bf16(x2[0] - bf_lo(hi[j]), x2[1] - bf_hi(hi[j]));
       }
-      const uint32_t off = core_off(q, (hh * 12 + ck) * 8, 128);
+      const uint32_t off = core_off(q, hh * 96 + ck * 8, 128);
       *reinterpret_cast<uint4*>(smem + kOffXhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(smem + kOffRB + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     if (hh == 0) {
       const double mean = ch.advstat[0], denom = ch.advstat[1];
-      rows_f[q] = valid ? row[gs - 3] : 0.f;
-      rows_f[128 + q] = valid ? (float)(((double)row[gs - 2] - mean) / denom) : 0.f;
-      rows_f[256 + q] = valid ? row[gs - 1] : 0.f;
+      rows_f[q] = valid ? rows_f[q] : 0.f;
+      rows_f[128 + q] = valid ? (float)(((double)rows_f[128 + q] - mean) / denom) : 0.f;
+      rows_f[256 + q] = valid ? rows_f[256 + q] : 0.f;
     }
   };
   auto load_image = [&]() {
@@ -492,8 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   resolve_rows(0);
   __syncthreads();
   gather_issue();
-  cp_async_wait_all();
-  __syncthreads();
+  gather_wait();
   gather_convert();
   cbar.wait();  // the initial image is complete in global memory
   load_image();
@@ -1006,8 +1022,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     __syncthreads();  // the staging area is free: the next X tiles and the image may land
     if (more) {
       if (!early) gather_issue();
-      cp_async_wait_all();
-      __syncthreads();
+      gather_wait();
       TCMARK(26);
       gather_convert();
       TCMARK(27);

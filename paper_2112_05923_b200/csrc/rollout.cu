@@ -24,7 +24,7 @@ namespace {
 
 void alloc_rollout(prb_rollout_s* r) {
   const size_t cap = r->N * r->H;
-  r->d_obs.alloc(cap * r->Sp);
+  r->d_obs.alloc(cap * r->Sp + 16);  // + padding: 16-byte bulk row copies (ppo_tc.cu)
   r->d_row.alloc(r->H);
   r->d_act.alloc(cap * r->A);
   r->d_logp.alloc(cap);
@@ -173,7 +173,7 @@ int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint64_t see
         r->obs_mode = 1;
         r->K = env->market->K;
         r->Sp = 1 + (size_t)r->K;
-        r->d_obs.alloc(r->N * r->H * r->Sp);
+        r->d_obs.alloc(r->N * r->H * r->Sp + 16);
       }
       r->d_feat = env->d_feat.p;
     }
@@ -241,7 +241,7 @@ int prb_rollout_collect_pods(const prb_rollout* rs, const prb_agent* as, const p
         rs[p]->obs_mode = 1;
         rs[p]->K = es[p]->market->K;
         rs[p]->Sp = 1 + (size_t)rs[p]->K;
-        rs[p]->d_obs.alloc(rs[p]->N * rs[p]->H * rs[p]->Sp);
+        rs[p]->d_obs.alloc(rs[p]->N * rs[p]->H * rs[p]->Sp + 16);
       }
     }
     DeviceScope dev_(rs[0]->ctx);
@@ -405,7 +405,7 @@ int prb_rollout_upload(prb_rollout r, const double* states, const double* action
     if (r->obs_mode != 0) {
       r->obs_mode = 0;
       r->Sp = S;
-      r->d_obs.alloc(n * S);
+      r->d_obs.alloc(n * S + 16);
     }
     std::vector<float> obs(n * S), act(n * A), lp(n), rw(n), vl(n), bt(N);
     std::vector<uint8_t> dn(n);
