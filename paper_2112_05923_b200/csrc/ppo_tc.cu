@@ -262,47 +262,50 @@ __device__ __forceinline__ void tanh_d(float z, float& h, float& d) {
 }
 
 // a row's 64 accumulator columns -> tanh(. + add[c]) -> bf16 into an R=128 core-form matrix at col cd
-// ... and the tanh derivatives 1 - h^2 (from the fp32 h) as packed bf16 pairs to TMEM at t_deriv
+// ... and the tanh derivatives 1 - h^2 (from the fp32 h) as packed bf16 pairs to TMEM at t_deriv.
+// Four 16-column chunks in a rolled loop: the kernel is large, and fully unrolled epilogues
+// stalled on instruction fetch (ncu no_instruction at the tanh lines).
 __device__ __forceinline__ void epi_tanh64(uint32_t tl, const float* add, uint8_t* dst, int row, int cd,
                                            uint32_t t_deriv) {
-  float v[64];
-  tc::tmem_ld64(tl, v);
-  uint32_t dpk[32];
+#pragma unroll 1
+  for (int c = 0; c < 64; c += 16) {
+    float v[16];
+    tc::tmem_ld16(tl + c, v);
+    uint32_t pk[8], dpk[8];
 #pragma unroll
-  for (int c = 0; c < 64; c += 8) {
-    uint32_t pk[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float z0 = v[c + 2 * j], z1 = v[c + 2 * j + 1];
+    for (int j = 0; j < 8; ++j) {
+      float z0 = v[2 * j], z1 = v[2 * j + 1];
       if (add) tc::add2(z0, z1, add[c + 2 * j], add[c + 2 * j + 1]);
       float h0, h1, d0, d1;
       tanh_d(z0, h0, d0);
       tanh_d(z1, h1, d1);
       pk[j] = tc::pack_bf16(h0, h1);
-      dpk[(c >> 1) + j] = tc::pack_bf16(d0, d1);
+      dpk[j] = tc::pack_bf16(d0, d1);
     }
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(dst + core_off(row, cd + c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    tc::tmem_st8(t_deriv + (c >> 1), dpk);
   }
-  tc::tmem_st32(t_deriv, dpk);
 }
 
 // delta = D[c] * (1 - h^2), the derivatives read back from TMEM at t_deriv (packed bf16 pairs)
 __device__ __forceinline__ void epi_delta64(uint32_t tl, uint32_t t_deriv, uint8_t* dst, int row, int cd) {
-  float v[64];
-  tc::tmem_ld64(tl, v);
-  uint32_t dw[32];
-  tc::tmem_ld32(t_deriv, dw);
+#pragma unroll 1
+  for (int c = 0; c < 64; c += 16) {
+    float v[16];
+    tc::tmem_ld16(tl + c, v);
+    uint32_t dw[8];
+    tc::tmem_ld8(t_deriv + (c >> 1), dw);
+    uint32_t pk[8];
 #pragma unroll
-  for (int c = 0; c < 64; c += 8) {
-    uint32_t pk[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t w = dw[(c >> 1) + j];
-      pk[j] = tc::pack_bf16(v[c + 2 * j] * bf_lo(w), v[c + 2 * j + 1] * bf_hi(w));
-    }
+    for (int j = 0; j < 8; ++j) pk[j] = tc::pack_bf16(v[2 * j] * bf_lo(dw[j]), v[2 * j + 1] * bf_hi(dw[j]));
     *reinterpret_cast<uint4*>(dst + core_off(row, cd + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(dst + core_off(row, cd + c + 8, 128)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }
 }
+
+// column swizzle of the staged action rows (even: 8-byte pairs stay adjacent and aligned)
+__device__ __forceinline__ int act_swz(int r) { return (r & 15) << 1; }
 
 struct Pipe {
   uint64_t* mbar;
@@ -554,46 +557,27 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     // ---- H1 = tanh(D) -> RC once both halves' MMAs are done reading W1 (b1 came with the ones
     // column; b2 enters in the next epilogue); the rows' actions start streaming into RC's spare
     // 16 KB (cp.async, consumed by the head epilogue) ----
-    {
-      mma.wait();
-      float hreg[64];
-      if (half == 0) tc::tmem_ld64(tl, hreg);
-      mma2.wait();
-      if (half == 1) tc::tmem_ld64(tl + 64, hreg);
-      TCMARK(2);
-      tc::fence_before_sync();
-      __syncthreads();  // W1 (in RC) is no longer read by the tensor core: H1 may overwrite it
-      {  // actions of this CTA's rows: [128][32] fp32, 8-byte copies (A even) or 4-byte
-        float* sact = reinterpret_cast<float*>(smem + kOffAct);
-        const bool even = (a.A & 1) == 0;
-        const int per = even ? a.A / 2 : a.A;
-        for (int e = tid; e < kRows * per; e += kThreads) {
-          const int r = e / per, k = e - r * per;
-          const uint32_t i = ridx[r];
-          if (i == 0xffffffffu) continue;
-          const float* src = ch.act + (size_t)i * a.A;
-          if (even)
-            cp_async8(sact + r * 32 + 2 * k, src + 2 * k);
-          else
-            cp_async4(sact + r * 32 + k, src + k);
+    mma.wait();
+    mma2.wait();
+    TCMARK(2);
+    tc::fence_before_sync();
+    __syncthreads();  // W1 (in RC) is no longer read by the tensor core: H1 may overwrite it
+    {  // actions of this CTA's rows: [128][32] fp32, element d of row r at column
+       // d ^ act_swz(r) (the row-per-thread reads of the head epilogue would otherwise all hit
+       // one bank); 8-byte copies (A even: pairs stay adjacent) or 4-byte; two threads per row
+      float* sact = reinterpret_cast<float*>(smem + kOffAct);
+      const int r = tid >> 1, sw = act_swz(r);
+      const uint32_t i = ridx[r];
+      if (i != 0xffffffffu) {
+        const float* src = ch.act + (size_t)i * a.A;
+        if ((a.A & 1) == 0) {
+          for (int k = 2 * (tid & 1); k < a.A; k += 4) cp_async8(sact + r * 32 + (k ^ sw), src + k);
+        } else {
+          for (int k = tid & 1; k < a.A; k += 2) cp_async4(sact + r * 32 + (k ^ sw), src + k);
         }
       }
-      uint32_t dpk[32];  // 1 - h^2 in relative precision (tanh_d)
-#pragma unroll
-      for (int c = 0; c < 64; c += 8) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float h0, h1, d0, d1;
-          tanh_d(hreg[c + 2 * j], h0, d0);
-          tanh_d(hreg[c + 2 * j + 1], h1, d1);
-          pk[j] = tc::pack_bf16(h0, h1);
-          dpk[(c >> 1) + j] = tc::pack_bf16(d0, d1);
-        }
-        *reinterpret_cast<uint4*>(smem + kOffRC + core_off(lrow, half * 64 + c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      }
-      tc::tmem_st32(tl + kTD1 + half * 32, dpk);
     }
+    epi_tanh64(tl + half * 64, nullptr, smem + kOffRC, lrow, half * 64, tl + kTD1 + half * 32);
     publish();
     TCMARK(3);
     if (tid == 0) {  // L2 actor / critic (W2 read MN-major: K = its rows = inputs)
@@ -621,26 +605,31 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       const bool valid = ridx[r] != 0xffffffffu;
       const float inv_n = 1.f / (float)a.mb;
       uint8_t* d3 = smem + kOffBuf1;
-      if (half == 0) {  // actor: mean, log-prob, ratio, clipped surrogate
-        float mu[32];
-        tmem16(tl + 256, mu);
-        tmem16(tl + 256 + 16, mu + 16);
-        float pl = 0.f;
-        float g[32];
+      if (half == 0) {  // actor: mean, log-prob, ratio, clipped surrogate (rolled 8-dim chunks;
+                        // z is staged in this row's scratch, then replaced by the dlog_std terms)
         const float* sact = reinterpret_cast<const float*>(smem + kOffAct) + r * 32;
-        if (valid) {
-          float lp = 0.f;
-          float z[32];
+        const int asw = act_swz(r);
+        float* zr = scr + r * kScr;
+        float lp = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 32; c += 8) {
+          uint32_t mw[8];
+          tc::tmem_ld8(tl + 256 + c, mw);
 #pragma unroll
-          for (int d = 0; d < 32; ++d) {
-            z[d] = 0.f;
-            if (d < a.A) {
+          for (int j = 0; j < 8; ++j) {
+            const int d = c + j;
+            float z = 0.f;
+            if (valid && d < a.A) {
               const float ls = f32[kFls + d];
-              const float m = mu[d] + f32[kFb3a + d];
-              z[d] = (sact[d] - m) * s_isig[d];
-              lp += -0.5f * kLogTwoPiF - ls - 0.5f * z[d] * z[d];
+              const float m = __uint_as_float(mw[j]) + f32[kFb3a + d];
+              z = (sact[d ^ asw] - m) * s_isig[d];
+              lp += -0.5f * kLogTwoPiF - ls - 0.5f * z * z;
             }
+            zr[d] = z;
           }
+        }
+        float pl = 0.f, dl = 0.f;
+        if (valid) {
           const float ratio = __expf(lp - rows_f[r]);
           const float adv = rows_f[128 + r];
           const float s1 = ratio * adv;
@@ -650,27 +639,26 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           const float cl = (ratio < lo) ? lo : ((hi < ratio) ? hi : ratio);
           const float s2 = cl * adv;
           pl = -((s2 < s1) ? s2 : s1) * inv_n;
-          const float dl = (s1 <= s2) ? -adv * ratio * inv_n : 0.f;  // ties flow (ppo.hpp:146)
-#pragma unroll
-          for (int d = 0; d < 32; ++d) {
-            g[d] = dl * z[d] * s_isig[d];                                  // dL/dmu
-            scr[r * kScr + d] = (d < a.A) ? dl * (z[d] * z[d] - 1.f) : 0.f;  // dL/dlog_std terms
-          }
-        } else {
-#pragma unroll
-          for (int d = 0; d < 32; ++d) {
-            g[d] = 0.f;
-            scr[r * kScr + d] = 0.f;
-          }
+          dl = (s1 <= s2) ? -adv * ratio * inv_n : 0.f;  // ties flow (ppo.hpp:146)
         }
-        scr[r * kScr + 32] = pl;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < 32; c += 8) {
           uint32_t pk[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) pk[j] = tc::pack_bf16(g[c + 2 * j], g[c + 2 * j + 1]);
+          for (int j = 0; j < 8; j += 2) {
+            float g2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int d = c + j + u;
+              const float z = zr[d];
+              g2[u] = valid ? dl * z * s_isig[d] : 0.f;                      // dL/dmu
+              zr[d] = (valid && d < a.A) ? dl * (z * z - 1.f) : 0.f;       // dL/dlog_std terms
+            }
+            pk[j >> 1] = tc::pack_bf16(g2[0], g2[1]);
+          }
           *reinterpret_cast<uint4*>(d3 + core_off(r, c, 128)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
+        zr[32] = pl;
       } else {  // critic: value error, dV
         float vv[16];
         tmem16(tl + 288, vv);
@@ -777,22 +765,28 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
         const bool mine = half == 0 ? o < a.A : o == 32;
         float* dst = half == 0 ? flat + a.a_w[2] + o : flat + a.c_w[2];
         const int stride = half == 0 ? a.A : 1;
-        float v[64];
-        tc::tmem_ld64(tl + half * 64, v);
-        if (mine) {
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 16) {
+          float v[16];
+          tc::tmem_ld16(tl + half * 64 + c, v);
+          if (mine) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) dst[j * stride] = v[j];
+            for (int j = 0; j < 16; ++j) dst[(c + j) * stride] = v[j];
+          }
         }
       }
       // dW2^T [128,256): the net's block is lanes of that net x its own input columns
       {
         const bool mine = (half == 0) == (o < 64);
         float* dst = (o < 64 ? flat + a.a_w[1] : flat + a.c_w[1]) + oo;
-        float v[64];
-        tc::tmem_ld64(tl + 128 + half * 64, v);
-        if (mine) {
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 16) {
+          float v[16];
+          tc::tmem_ld16(tl + 128 + half * 64 + c, v);
+          if (mine) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) dst[j * 64] = v[j];
+            for (int j = 0; j < 16; ++j) dst[(c + j) * 64] = v[j];
+          }
         }
       }
       // dW1^T [256,448): columns = X columns -> W1 rows (s_colk), the ones column -> b1
