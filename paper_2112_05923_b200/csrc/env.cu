@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
 // the obs writer.  ~170 B of shared memory per env -> ~2x the resident warps
 // of v2, which is what keeps HBM busy while other CTAs run the fp64 chain.
 template <int KMAX, int EB>
-__global__ void __launch_bounds__(EB, 1024 / EB) stock_step_v3_kernel(StockStepArgs a) {
+#ifndef PRB_ENV_TPS
+#define PRB_ENV_TPS 1024  // resident threads per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB) stock_step_v3_kernel(StockStepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, F = 5 * K, Kp = K + 1;  // K even -> odd stride
   double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
