@@ -333,7 +333,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t s_mma, s_mma2, s_img;
+  __shared__ __align__(8) uint64_t s_mma, s_img;
   __shared__ uint32_t s_tmem;
   __shared__ float s_red[2][40];   // head-epilogue column sums (two row halves)
   __shared__ float s_db3[33];      // column sums of d3 (actor 0..31, critic 32)
@@ -361,7 +361,6 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
   if (tid == 0) {
     tc::mbar_init(&s_mma, 1);
-    tc::mbar_init(&s_mma2, 1);
     tc::mbar_init(&s_img, 1);
     tc::mbar_init(&s_red_bar, 1);
     tc::mbar_init(&s_gat, kRows);
@@ -378,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
   tc::fence_after_sync();
   const uint32_t tbase = s_tmem;
   const uint32_t tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quarter
-  Pipe mma{&s_mma, 0}, mma2{&s_mma2, 0}, imgp{&s_img, 0};
+  Pipe mma{&s_mma, 0}, imgp{&s_img, 0};
 
   // parameter slice of this CTA (reduction / Adam / image entries)
   const int chunk = ((a.P + C - 1) / C + 3) & ~3;
@@ -533,32 +532,23 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     if (tid < 32) s_isig[tid] = tid < a.A ? __expf(-f32[kFls + tid]) : 0.f;
     publish();  // X (gather) visible to the tensor core
     TCMARK(1);
-    // ---- L1: D[0,64) = X_hi . W1a + X_lo . W1a, then D[64,128) for the critic (its own commit,
-    // so the actor epilogue overlaps the critic's MMAs) ----
+    // ---- L1: D[0,128) = [actor | critic] in N = 128 MMAs (the W1 image holds both nets' output
+    // rows): X_hi . W1_hi + X_lo . W1_hi + X_hi . W1_lo (the lo . lo term is below fp32 rounding) ----
     if (tid == 0) {
-      // X_hi . W1_hi + X_lo . W1_hi + X_hi . W1_lo (the lo . lo term is below fp32 rounding)
-      auto w1lo_chain = [&](uint32_t d_col, uint32_t n_off) {
-        const uint32_t idesc = tc::idesc_bf16_t(128, 64, 0, 0);
-        for (int j = 0; j < kXC / 16; ++j) {
-          const uint32_t bb = (j < 4 ? sbase + kOffW1loA + j * 4096 : sbase + kOffW1loB + (j - 4) * 4096) + n_off;
-          tc::mma_bf16(tbase + d_col, desc_k(sbase + kOffXhi + j * 4096, 128), desc_k(bb, 128), idesc, 1u);
-        }
-      };
-      mma_chain(tbase + 0, sbase + kOffXhi, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, false);
-      mma_chain(tbase + 0, sbase + kOffRB, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 64, true);
-      w1lo_chain(0, 0);
+      const uint32_t idesc = tc::idesc_bf16_t(128, 128, 0, 0);
+      mma_chain(tbase + 0, sbase + kOffXhi, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 128, false);
+      mma_chain(tbase + 0, sbase + kOffRB, 128, 0, sbase + kOffRC, 128, 0, kXC / 16, 128, true);
+      for (int j = 0; j < kXC / 16; ++j) {
+        const uint32_t bb = j < 4 ? sbase + kOffW1loA + j * 4096 : sbase + kOffW1loB + (j - 4) * 4096;
+        tc::mma_bf16(tbase, desc_k(sbase + kOffXhi + j * 4096, 128), desc_k(bb, 128), idesc, 1u);
+      }
       tc::mma_commit(&s_mma);
-      mma_chain(tbase + 64, sbase + kOffXhi, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, false);
-      mma_chain(tbase + 64, sbase + kOffRB, 128, 0, sbase + kOffRC + 1024, 128, 0, kXC / 16, 64, true);
-      w1lo_chain(64, 1024);
-      tc::mma_commit(&s_mma2);
     }
     if (st + 1 < a.steps) resolve_rows(st + 1);  // read by gather_issue at the end of this step
     // ---- H1 = tanh(D) -> RC once both halves' MMAs are done reading W1 (b1 came with the ones
     // column; b2 enters in the next epilogue); the rows' actions start streaming into RC's spare
     // 16 KB (cp.async, consumed by the head epilogue) ----
     mma.wait();
-    mma2.wait();
     TCMARK(2);
     tc::fence_before_sync();
     __syncthreads();  // W1 (in RC) is no longer read by the tensor core: H1 may overwrite it
