@@ -198,3 +198,76 @@ def test_tc_gate_midway_keeps_last_accepted_step(pr, ctx, orc):
     assert out.get()[3] == 2
     assert np.all(np.isfinite(out.flatten_params()))
     agent.set_ppo_mode(0)
+
+
+def _blocks_for(S_, A):
+    out, off = [], 0
+    for net, n_out in (("a", A), ("c", 1)):
+        d = [S_, 64, 64, n_out]
+        for l in range(3):
+            i, o = d[l], d[l + 1]
+            out += [(f"{net}.W{l + 1}", off, off + i * o), (f"{net}.b{l + 1}", off + i * o, off + i * o + o)]
+            off += i * o + o
+        if net == "a":
+            out.append(("log_std", off, off + A))
+            off += A
+    return out
+
+
+@pytest.mark.parametrize("K_,mb,compact", [(3, 1024, False), (3, 700, True), (30, 700, True), (30, 1024, True),
+                                           (2, 128, True)])
+def test_tc_gradient_blocks_shapes(pr, ctx, orc, K_, mb, compact):
+    """The tensor-core update's reduced gradient at other shapes: odd action counts (4-byte action
+    copies), a partial last CTA (mb = 700: rows 640-699 live, 700-767 invalid), a single-CTA
+    learner (mb = 128), and both buffer forms -- full rows (raw upload: obs_mode 0, rows at every
+    4-byte shift of the 16-byte bulk-copy window) and the collected compact rows + shared-feature
+    table (obs_mode 1).  Compact buffers keep the rollout's own old log-probs (the oracle gets the
+    same values); full-row buffers use the oracle's.  Tolerance TOL_BLOCK per block."""
+    S_ = 1 + 6 * K_
+    N, H = 16, 64
+    n = N * H
+    m = pr.synthetic_market(K_, 2048, 2112)
+    ind = pr.compute_indicators(m["high"], m["low"], m["close"])
+    market = pr.MarketData(ctx, m["close"], ind)
+    env = pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(), 1500, 2047, N)
+    env.reset(5)
+    agent = pr.Agent.init(ctx, S_, K_, seed=9)
+    agent.set_ppo_mode(1)
+    ro = pr.Rollout.for_env(env, H)
+    ro.collect(agent, env, seed=31)
+    b = ro.download()
+    flat = agent.flatten_params()
+    if not compact:
+        pa = sum((i + 1) * o for i, o in zip([S_, 64, 64], [64, 64, K_]))
+        mean = np.zeros((n, K_))
+        orc.orc_mlp_forward(ptr(np.ascontiguousarray(flat[:pa])), ptr(dims(S_, 64, 64, K_), SZ), 3,
+                            ptr(np.ascontiguousarray(b["states"])), n, ptr(mean), None)
+        ls = np.ascontiguousarray(flat[pa:pa + K_])
+        b["log_probs"] = np.array([orc.orc_gaussian_row_log_prob(ptr(ls), K_, ptr(np.ascontiguousarray(mean[i])),
+                                                                 ptr(np.ascontiguousarray(b["actions"][i])))
+                                   for i in range(n)])
+        ro = pr.Rollout.raw(ctx, N, H, S_, K_)
+        ro.upload(b["states"], b["actions"], b["log_probs"], b["rewards"], b["dones"], b["values"], b["bootstrap"])
+    perm = np.random.default_rng(4).permutation(n).astype(np.uint64)
+    cfg = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=n - n % mb, learning_rate=0.0)
+    out = pr.Agent(ctx, S_, K_)
+    pr.ppo_update(agent, ro, cfg, 1, perm=perm, out=out)
+    g = np.zeros(agent.param_count)
+    ctx.lib.prb_debug_agent_grads(out.h, g.ctypes.data_as(C.POINTER(C.c_double)))
+    # the gradient the device left is its LAST step's: minibatch n // mb - 1 of the permutation
+    steps = (n - n % mb) // mb
+    adv, ret = ro.buffer_advantages(cfg, normalize=True)
+    idx = perm[(steps - 1) * mb:steps * mb].astype(np.int64)
+    og, ol = np.zeros(flat.size), np.zeros(3)
+    oc = PpoCfg(0.99, 0.95, 0.2, 0.01, 0.5, 1, mb, n - n % mb, 0.0)
+    assert orc.orc_ppo_loss_grads(ptr(flat), ptr(dims(S_, 64, 64, K_), SZ), 3, ptr(dims(S_, 64, 64, 1), SZ), 3,
+                                  ptr(np.ascontiguousarray(b["states"][idx])),
+                                  ptr(np.ascontiguousarray(b["actions"][idx])),
+                                  ptr(np.ascontiguousarray(b["log_probs"][idx])), ptr(np.ascontiguousarray(adv[idx])),
+                                  ptr(np.ascontiguousarray(ret[idx])), mb, C.byref(oc), ptr(og), ptr(ol)) == 0
+    errs = {}
+    for name, lo, hi in _blocks_for(S_, K_):
+        ref = og[lo:hi]
+        errs[name] = float(np.linalg.norm(g[lo:hi] - ref) / max(np.linalg.norm(ref), 1e-30))
+    print(f"RECORD tc gradient rel L2 per block K={K_} mb={mb} compact={compact}:", errs)
+    assert max(errs.values()) <= TOL_BLOCK, errs
