@@ -194,19 +194,56 @@ struct InitNet {
   uint64_t seed;
 };
 
-__global__ void artifact_init_kernel(float* __restrict__ params, InitNet actor, InitNet critic) {
-  __shared__ uint64_t mt[2][kMtN];
+// mlp_init (nn.hpp:40-54) for both nets, CTA k = net k, the reference's mt19937_64 stream
+// (derive_seed(seed, kInit, k + 1)) generated 312 words at a time in parallel: the twist of a
+// block is three data-parallel phases (words [0,156) read only old words; [156,311) read the
+// new words 156 below them; word 311 reads new words 0 and 155 -- the serial loop's
+// dependencies exactly), then thread i tempers word i and turns draw 312 b + i into its weight
+// (uniform_real_distribution(-1/sqrt(fan_in), +) over generate_canonical<double, 53>: one
+// 64-bit draw per weight).  Bit-identical to the serial stream; ~40x faster than one thread
+// per net, which a generation's fresh pods used to wait ~2.3 ms for.
+__global__ void __launch_bounds__(320) artifact_init_kernel(float* __restrict__ params, InitNet actor, InitNet critic) {
+  __shared__ uint64_t mt[kMtN];
+  const InitNet& n = blockIdx.x == 0 ? actor : critic;
   const int t = threadIdx.x;
-  if (t > 1) return;
-  const InitNet& n = t == 0 ? actor : critic;
-  uint64_t* st = mt[t];
-  mt64_seed(st, 1, n.seed);
-  int32_t idx = kMtN;
-  for (int l = 0; l < n.nl; ++l) {
-    const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)n.dims[l]));
-    const int cnt = n.dims[l] * n.dims[l + 1];
-    float* w = params + n.off[l];
-    for (int i = 0; i < cnt; ++i) w[i] = (float)mt64_uniform(st, 1, idx, -scale, scale);
+  if (t == 0) mt64_seed(mt, 1, n.seed);
+  int total = 0;
+  for (int l = 0; l < n.nl; ++l) total += n.dims[l] * n.dims[l + 1];
+  __syncthreads();
+  constexpr uint64_t kUp = 0xFFFFFFFF80000000ULL, kLo = 0x7FFFFFFFULL, kMag = 0xB5026F5AA96619E9ULL;
+  auto twist_word = [&](uint64_t cur, uint64_t nxt, uint64_t far) {
+    const uint64_t y = (cur & kUp) | (nxt & kLo);
+    return far ^ (y >> 1) ^ ((y & 1ULL) ? kMag : 0ULL);
+  };
+  for (int k0 = 0; k0 < total; k0 += kMtN) {
+    uint64_t v = 0;
+    if (t < 156) v = twist_word(mt[t], mt[t + 1], mt[t + 156]);
+    __syncthreads();
+    if (t < 156) mt[t] = v;
+    __syncthreads();
+    if (t >= 156 && t < kMtN - 1) v = twist_word(mt[t], mt[t + 1], mt[t - 156]);
+    __syncthreads();
+    if (t >= 156 && t < kMtN - 1) mt[t] = v;
+    if (t == 0) mt[kMtN - 1] = twist_word(mt[kMtN - 1], mt[0], mt[155]);
+    __syncthreads();
+    const int k = k0 + t;
+    if (t < kMtN && k < total) {
+      uint64_t x = mt[t];
+      x ^= (x >> 29) & 0x5555555555555555ULL;
+      x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+      x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+      x ^= (x >> 43);
+      int l = 0, start = 0;
+      while (k - start >= n.dims[l] * n.dims[l + 1]) {
+        start += n.dims[l] * n.dims[l + 1];
+        ++l;
+      }
+      const double scale = __ddiv_rn(1.0, __dsqrt_rn((double)n.dims[l]));
+      double u = __dmul_rn(__ull2double_rn(x), 5.421010862427522170037264e-20);  // 2^-64
+      if (u >= 1.0) u = 0.99999999999999988898;  // nextafter(1, 0)
+      params[n.off[l] + (k - start)] = (float)__dadd_rn(__dmul_rn(u, __dsub_rn(scale, -scale)), -scale);
+    }
+    __syncthreads();  // the next twist overwrites the words just tempered
   }
 }
 
@@ -520,7 +557,7 @@ int prb_agent_init_device(prb_agent a, uint64_t seed, double lr) {
       for (size_t i = 0; i < off.size(); ++i) nets[k].off[i] = (int)off[i];
       nets[k].seed = derive_seed(seed, {5 /*kInit*/, (uint64_t)(k + 1)});
     }
-    artifact_init_kernel<<<1, 32, 0, s>>>(a->d_params.p, nets[0], nets[1]);
+    artifact_init_kernel<<<2, 320, 0, s>>>(a->d_params.p, nets[0], nets[1]);
     PRB_CHECK_LAUNCH();
     a->lr = lr;
     a->ctx->sync();
