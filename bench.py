@@ -571,8 +571,8 @@ def leg_stock_large(pr, lib, ctx, market, cfg, n_envs, horizon, d):
 def leg_tournament(pr, ctx, market, cfg, d, pods, learners=2, gens=2):
     """configs[3]: one GPU's pod population, a REAL generation timed end to end: every pod's collect
     in one grouped tcgen05 launch (configs[0]-sized pods: 1,024 stock envs x 256 steps), every pod's
-    `learners` PPO learners (4 epochs x 256 minibatches of 1,024) in one tensor-core launch (a
-    cluster per learner), per-pod fusion, evaluation (10 episodes of 40 steps), the NCCL all-gather
+    `learners` PPO learners (4 epochs x 256 minibatches of 1,024) in one tensor-core launch (8
+    co-resident CTAs per learner), per-pod fusion, evaluation (10 episodes of 40 steps), the NCCL all-gather
     ranking over every rank's pods and the top-3 elite broadcasts + device mutations
     (tournament.PodPopulation, tournament.hpp:395-506).  Host wall clock around each generation
     (max over ranks); the learners alone are also timed against the fp32 SIMT update run serially."""

@@ -450,6 +450,36 @@ inline EvaluationRecord evaluate(const Agent& actor, VectorizedEnvironment& env,
   return rec;
 }
 
+// evaluate for every pod of a GPU in one pass (record p == evaluate(*agents[p], *envs[p], seeds[p]))
+inline std::vector<EvaluationRecord> evaluate_pods(const std::vector<const Agent*>& agents,
+                                                   const std::vector<VectorizedEnvironment*>& envs,
+                                                   const std::vector<std::uint64_t>& seeds, bool sample_actions = false) {
+  const std::size_t P = agents.size();
+  if (envs.size() != P || seeds.size() != P)
+    throw DimensionError("evaluate_pods: " + std::to_string(P) + " agents, " + std::to_string(envs.size()) +
+                         " envs, " + std::to_string(seeds.size()) + " seeds");
+  if (P == 0) return {};
+  const std::size_t n = envs[0]->num_envs();
+  std::vector<prb_agent> a(P);
+  std::vector<prb_vecenv> e(P);
+  for (std::size_t p = 0; p < P; ++p) {
+    a[p] = agents[p]->get();
+    e[p] = envs[p]->get();
+  }
+  std::vector<double> r(P * n), m(P), sd(P);
+  std::vector<std::uint64_t> st(P);
+  check(prb_evaluate_pods(a.data(), e.data(), P, seeds.data(), sample_actions ? 1 : 0, r.data(), m.data(), sd.data(),
+                          st.data()));
+  std::vector<EvaluationRecord> out(P);
+  for (std::size_t p = 0; p < P; ++p) {
+    out[p].episodic_rewards.assign(r.begin() + p * n, r.begin() + (p + 1) * n);
+    out[p].mean = m[p];
+    out[p].std_dev = sd[p];
+    out[p].eval_steps = st[p];
+  }
+  return out;
+}
+
 // fuse_parameters pod.hpp:141-172
 inline std::unique_ptr<Agent> fuse_parameters(const std::vector<const Agent*>& agents) {
   if (agents.empty()) throw UsageError("fuse_parameters: empty artifact list");

@@ -318,6 +318,13 @@ PRB_API int prb_adam_step_device(prb_agent a, const float* d_grads);
  * bound. */
 PRB_API int prb_evaluate(prb_agent a, prb_vecenv env, uint64_t seed, int sample_actions, double* episodic_rewards,
                          double* mean, double* std_dev, uint64_t* eval_steps);
+/* prb_evaluate for the P pods of a GPU in one pass (one policy launch per step for every pod):
+ * pod p's results equal prb_evaluate(agents[p], envs[p], seeds[p], sample_actions, ...) exactly.
+ * Every eval VecEnv: the same num_envs, action dim, episode bound and context.  episodic_rewards
+ * [P][num_envs]; means, std_devs, eval_steps [P] (nullable).                       pod.hpp:43-83 */
+PRB_API int prb_evaluate_pods(const prb_agent* agents, const prb_vecenv* envs, size_t P, const uint64_t* seeds,
+                              int sample_actions, double* episodic_rewards, double* means, double* std_devs,
+                              uint64_t* eval_steps);
 
 /* ---- learner fusion (pod.hpp:141-172) ----------------------------------- */
 PRB_API int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out);

@@ -166,6 +166,7 @@ SIGNATURES = {
     "prb_adam_step_host": (I, [P, pD]),
     "prb_adam_step_device": (I, [P, P]),
     "prb_evaluate": (I, [P, P, U64, I, pD, pD, pD, pU64]),
+    "prb_evaluate_pods": (I, [C.POINTER(P), C.POINTER(P), SZ, pU64, I, pD, pD, pD, pU64]),
     "prb_fuse_parameters": (I, [C.POINTER(P), SZ, P]),
     "prb_leaderboard_rank": (I, [P, P, P, SZ, SZ, P, P]),
     "prb_leaderboard_rank_host": (I, [P, pD, pU64, SZ, SZ, pI32, pI32]),

@@ -81,12 +81,14 @@ __device__ __forceinline__ void linear_tile(const float* __restrict__ W, int ldw
   int TJ = 32;
   while (TJ < out && TJ < (int)blockDim.x) TJ <<= 1;
   const int G = blockDim.x / TJ;
-  // rows per thread per pass: enough groups x RB to cover the tile in one pass when possible
-  if (nrows >= 8 * G)
+  // rows per thread per pass: the smallest RB whose G x RB rows cover the tile in ONE pass (each
+  // pass re-walks the weights: for a few rows the walk's load latency is the whole cost), else 8.
+  // A row's sum is the same fmaf chain over k whatever RB is.
+  if (nrows > 4 * G)
     linear_tile_rb<TANH, 8>(W, ldw, b, in, out, s_in, ldi, s_out, ldo, nrows, TJ);
-  else if (nrows >= 4 * G)
+  else if (nrows > 2 * G)
     linear_tile_rb<TANH, 4>(W, ldw, b, in, out, s_in, ldi, s_out, ldo, nrows, TJ);
-  else if (nrows >= 2 * G)
+  else if (nrows > G)
     linear_tile_rb<TANH, 2>(W, ldw, b, in, out, s_in, ldi, s_out, ldo, nrows, TJ);
   else
     linear_tile_rb<TANH, 1>(W, ldw, b, in, out, s_in, ldi, s_out, ldo, nrows, TJ);

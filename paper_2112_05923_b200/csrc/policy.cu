@@ -21,7 +21,7 @@ namespace {
 
 constexpr float kLogTwoPiF = 1.8378770664093454836f;
 
-__global__ void __launch_bounds__(256) policy_kernel(PolicyArgs p) {
+__device__ __forceinline__ void policy_body(const PolicyArgs& p, size_t tile) {
   extern __shared__ __align__(16) float smem[];
   const int R = p.rows_per_cta;
   const int S = p.actor.dims[0];
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) policy_kernel(PolicyArgs p) {
   float* s_mean = buf1 + R * p.ldw;  // [R][ldA]  (actor head kept for sampling)
   const int A = p.A;
   const int ldA = round4(A);
-  const size_t row0 = (size_t)blockIdx.x * R;
+  const size_t row0 = tile * R;
   const int nrows = (p.n - row0 < (size_t)R) ? (int)(p.n - row0) : R;
 
   // ---- load the state tile (rows are contiguous in memory) ----
@@ -129,7 +129,28 @@ __global__ void __launch_bounds__(256) policy_kernel(PolicyArgs p) {
   }
 }
 
+__global__ void __launch_bounds__(256) policy_kernel(PolicyArgs p) { policy_body(p, blockIdx.x); }
+
+// one launch for several agents (blockIdx.y = agent): the evaluation of every pod of a GPU steps
+// all pods' policies at once; counter (the Philox step) is the launch's, for every agent
+__global__ void __launch_bounds__(256) policy_group_kernel(const PolicyArgs* __restrict__ group, uint64_t counter) {
+  PolicyArgs p = group[blockIdx.y];
+  p.counter = counter;
+  if ((size_t)blockIdx.x * p.rows_per_cta < p.n) policy_body(p, blockIdx.x);
+}
+
 }  // namespace
+
+void prb_policy_launch_group(const PolicyArgs* d_group, int P, size_t n_max, size_t smem, uint64_t counter,
+                             prb_ctx_s* ctx) {
+  ProfScope prof(ctx, kProfPolicy);
+  if (P == 0 || n_max == 0) return;
+  PRB_REQUIRE(smem <= 220 * 1024, PRB_ERR_CONFIG, "policy: tile does not fit in shared memory");
+  ensure_smem(policy_group_kernel, 220 * 1024);
+  const unsigned gx = (unsigned)((n_max + 31) / 32);
+  policy_group_kernel<<<dim3(gx, (unsigned)P), 256, smem, ctx->stream>>>(d_group, counter);
+  PRB_CHECK_LAUNCH();
+}
 
 PolicyArgs prb_policy_args(prb_agent a, const float* d_states, size_t n) {
   PolicyArgs p{};

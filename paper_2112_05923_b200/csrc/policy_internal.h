@@ -42,6 +42,10 @@ struct PolicyArgs {
 PolicyArgs prb_policy_args(prb_agent a, const float* d_states, size_t n);
 size_t prb_policy_smem(const PolicyArgs& p);
 void prb_policy_launch(const PolicyArgs& p, prb_ctx_s* ctx);
+// P agents' policies in one launch (d_group: P PolicyArgs in device memory, rows_per_cta 32 each;
+// n_max = the largest n; counter overrides every entry's Philox counter)
+void prb_policy_launch_group(const PolicyArgs* d_group, int P, size_t n_max, size_t smem, uint64_t counter,
+                             prb_ctx_s* ctx);
 void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
                          double* d_term_ret, int32_t* d_term_len);
 void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s);

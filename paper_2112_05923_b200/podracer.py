@@ -623,6 +623,25 @@ def evaluate(agent: Agent, env: "VectorizedEnvironment", seed: int, sample_actio
     return EvaluationRecord(r, m.value, sd.value, st.value)
 
 
+def evaluate_pods(agents: Sequence[Agent], envs: Sequence["VectorizedEnvironment"], seeds: Sequence[int],
+                  sample_actions: bool = False) -> List[EvaluationRecord]:
+    """evaluate (pod.hpp:43-83) for every pod of a GPU in one pass: record p equals
+    evaluate(agents[p], envs[p], seeds[p]) exactly (one policy launch per step for all pods)."""
+    P = len(agents)
+    if P == 0:
+        return []
+    n = envs[0].num_envs()
+    r = np.zeros((P, n), dtype=np.float64)
+    m, sd, st = np.zeros(P), np.zeros(P), np.zeros(P, dtype=np.uint64)
+    ah = (C.c_void_p * P)(*[a.h.value if hasattr(a.h, "value") else a.h for a in agents])
+    eh = (C.c_void_p * P)(*[e.h.value if hasattr(e.h, "value") else e.h for e in envs])
+    sd_ = np.ascontiguousarray(seeds, dtype=np.uint64)
+    agents[0].ctx.lib.prb_evaluate_pods(ah, eh, P, _p(sd_, C.c_uint64), 1 if sample_actions else 0,
+                                        _p(r, C.c_double), _p(m, C.c_double), _p(sd, C.c_double),
+                                        _p(st, C.c_uint64))
+    return [EvaluationRecord(r[p], float(m[p]), float(sd[p]), int(st[p])) for p in range(P)]
+
+
 def leaderboard_rank(ctx: Context, scores, seqs, capacity: int) -> np.ndarray:
     """Board order after inserting (score, seq) candidates (tournament.hpp:104-119)."""
     s = np.ascontiguousarray(scores, dtype=np.float64)

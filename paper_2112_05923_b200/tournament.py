@@ -175,9 +175,9 @@ class PodPopulation:
         for p in range(self.P):
             pr.fuse_parameters(self.learner_out[p], out=self.agents[p])
         # 3. evaluation scores
-        scores = np.array([pr.evaluate(self.agents[p], self.eval_envs[p],
-                                       pr.derive_seed(self.seed, 4, self.global_id(p), g)).mean
-                           for p in range(self.P)])
+        recs = pr.evaluate_pods(self.agents, self.eval_envs,
+                                [pr.derive_seed(self.seed, 4, self.global_id(p), g) for p in range(self.P)])
+        scores = np.array([rec.mean for rec in recs])
         # 4. leaderboard over every rank's pods (the previous board's entries compete again)
         ids = [self.global_id(p) for p in range(self.P)]
         seqs = [arrival_seq(g, pid, self.world * self.P) for pid in ids]

@@ -267,6 +267,16 @@ int main() {
       EXPECT(st.minibatches == stats[l].minibatches && st.mean_policy_loss == stats[l].mean_policy_loss);
       EXPECT(outs[l]->optimizer_t() == (int64_t)(NP * H / 1024));
     }
+    {  // grouped evaluation == per-pod evaluation
+      std::vector<std::unique_ptr<pb::VectorizedEnvironment>> ev;
+      for (int p = 0; p < 2; ++p) ev.push_back(pb::VectorizedEnvironment::stock(market, cfg, start, end, 4));
+      const auto recs = pb::evaluate_pods({outs[0].get(), outs[1].get()}, {ev[0].get(), ev[1].get()}, {5, 6});
+      for (int p = 0; p < 2; ++p) {
+        auto e1 = pb::VectorizedEnvironment::stock(market, cfg, start, end, 4);
+        const pb::EvaluationRecord one = pb::evaluate(*outs[p], *e1, 5 + p);
+        EXPECT(one.episodic_rewards == recs[p].episodic_rewards && one.mean == recs[p].mean);
+      }
+    }
     pb::Agent fresh(ctx, S, K);
     fresh.init_device(60, 1e-3);
     EXPECT(fresh.flatten_params() == agents[0]->flatten_params());

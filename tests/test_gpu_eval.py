@@ -108,3 +108,24 @@ def test_evaluate_errors(pr, ctx):
         pr.evaluate(wrong, env, 1)
     rec = pr.evaluate(agent, env, 1, sample_actions=True)  # Philox-sampled actions: statistics only
     assert np.all(np.isfinite(rec.episodic_rewards)) and 4 <= rec.eval_steps <= 800
+
+
+@pytest.mark.parametrize("kind,sample", [("stock", False), ("pointmass", True), ("pointmass", False)])
+def test_evaluate_pods_equals_per_pod_evaluate(pr, ctx, kind, sample):
+    """prb_evaluate_pods (one policy launch per step for every pod) gives each pod exactly the
+    record prb_evaluate gives it alone: episode totals, lengths, mean, std."""
+    P, E = 3, 10
+    if kind == "stock":
+        market = pr.MarketData.synthetic(ctx)
+        mk = lambda: pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(), 1900, 1940, E)  # noqa: E731
+        agents = [pr.Agent.init(ctx, 181, 30, seed=20 + p) for p in range(P)]
+    else:
+        mk = lambda: pr.VectorizedEnvironment.pointmass(ctx, E)  # noqa: E731
+        agents = [pr.Agent.init(ctx, 6, 2, seed=20 + p) for p in range(P)]
+    seeds = [100 + 7 * p for p in range(P)]
+    grouped = pr.evaluate_pods(agents, [mk() for _ in range(P)], seeds, sample_actions=sample)
+    for p in range(P):
+        one = pr.evaluate(agents[p], mk(), seeds[p], sample_actions=sample)
+        assert np.array_equal(grouped[p].episodic_rewards, one.episodic_rewards), p
+        assert grouped[p].mean == one.mean and grouped[p].std_dev == one.std_dev
+        assert grouped[p].eval_steps == one.eval_steps
