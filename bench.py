@@ -608,6 +608,9 @@ def leg_tournament(pr, ctx, market, cfg, d, pods, learners=2, gens=2):
     pr.ppo_update_learners(srcs, ros, pcfg, list(range(len(srcs))), outs=outs)
     ctx.synchronize()
     learn_tc = time.perf_counter() - t0
+    for l in range(2):  # warm: the SIMT update's workspace on these destinations (ppo_mode 0: SIMT)
+        pr.ppo_update(srcs[l], ros[l], pcfg, l, out=outs[l])
+    ctx.synchronize()
     t0 = time.perf_counter()
     for l in range(2):  # two serial SIMT learners, scaled to all of them
         pr.ppo_update(srcs[l], ros[l], pcfg, l, out=outs[l])
