@@ -106,6 +106,13 @@ struct PpoUpdateStats {  // ppo.hpp:198-203
   std::size_t minibatches = 0;
 };
 
+class Agent;
+// ppo.hpp:205-208 (the trained copy lives on the device: a handle instead of a value)
+struct PpoUpdateResult {
+  std::unique_ptr<Agent> artifact;
+  PpoUpdateStats stats;
+};
+
 struct PolicySample {  // nn.hpp:245-248
   Tensor2 actions;
   std::vector<double> log_probs;
@@ -310,6 +317,11 @@ inline PolicySample policy_sample(const Agent& a, const Tensor2& states, std::ui
   return out;
 }
 
+// The reference's signature (nn.hpp:250): the noise is Philox keyed by ONE 64-bit draw of rng.
+inline PolicySample policy_sample(const Agent& a, const Tensor2& states, std::mt19937_64& rng) {
+  return policy_sample(a, states, rng(), 0);
+}
+
 // Device TransitionBuffer sized for one VecEnv x horizon (buffer.hpp:39-48).
 class TransitionBuffer {
  public:
@@ -317,27 +329,67 @@ class TransitionBuffer {
     check(prb_rollout_create(env.get(), horizon, &h_));
     N_ = env.num_envs();
     H_ = horizon;
+    S_ = env.spec().state_dim;
+    A_ = env.spec().action_dim;
   }
   ~TransitionBuffer() { prb_rollout_destroy(h_); }
   TransitionBuffer(const TransitionBuffer&) = delete;
   TransitionBuffer& operator=(const TransitionBuffer&) = delete;
   std::size_t capacity() const { return N_ * H_; }
+  std::size_t length() const { return N_ * H_; }  // a collect fills the whole buffer
+  bool full() const { return true; }
+  std::size_t horizon() const { return H_; }
+  std::size_t num_envs() const { return N_; }
   prb_rollout get() const { return h_; }
-  // rewards in the reference index space (env e, step t at e*H + t, pod.hpp:89-94)
-  std::vector<double> rewards() const {
-    std::vector<double> r(capacity());
-    check(prb_rollout_download(h_, nullptr, nullptr, nullptr, r.data(), nullptr, nullptr, nullptr));
-    return r;
+  // Host copies of the columns in the reference index space (env e, step t at e*H + t,
+  // pod.hpp:89-94); the reference returns references to its host vectors (buffer.hpp:55-61),
+  // here each call downloads the device column.
+  std::vector<double> states() const { return column(0, S_); }
+  std::vector<double> actions() const { return column(1, A_); }
+  std::vector<double> log_probs() const { return column(2, 1); }
+  std::vector<double> rewards() const { return column(3, 1); }
+  std::vector<double> values() const { return column(5, 1); }
+  std::vector<std::uint8_t> dones() const {
+    std::vector<std::uint8_t> d(capacity());
+    check(prb_rollout_download(h_, nullptr, nullptr, nullptr, nullptr, d.data(), nullptr, nullptr));
+    return d;
   }
+  std::vector<double> bootstrap_values() const {  // Chunk::bootstrap_value of env e's chunk
+    std::vector<double> b(N_);
+    check(prb_rollout_download(h_, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, b.data()));
+    return b;
+  }
+  std::size_t state_dim() const { return S_; }
+  std::size_t action_dim() const { return A_; }
 
  private:
+  std::vector<double> column(int which, std::size_t width) const {
+    std::vector<double> v(capacity() * width);
+    double* p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    p[which] = v.data();
+    check(prb_rollout_download(h_, p[0], p[1], p[2], p[3], nullptr, p[5], nullptr));
+    return v;
+  }
   prb_rollout h_ = nullptr;
-  std::size_t N_ = 0, H_ = 0;
+  std::size_t N_ = 0, H_ = 0, S_ = 0, A_ = 0;
 };
 
 // worker_collect pod.hpp:95-132
 inline void worker_collect(const Agent& a, VectorizedEnvironment& env, TransitionBuffer& buf, std::uint64_t seed) {
   check(prb_rollout_collect(buf.get(), a.get(), env.get(), seed));
+}
+
+// The reference's signature (pod.hpp:95-98): the actor and critic are the agent's; the noise is
+// Philox keyed by ONE 64-bit draw of the caller's rng (the reference draws N x A x H normals from
+// it, so the caller's stream advances differently; both are deterministic in the seed).  The
+// device buffer holds one VecEnv's segment: segment_offset and chunk_base must be 0 and horizon
+// the buffer's (a multi-worker pod_train uses one VecEnv of num_workers * envs_per_worker envs).
+inline void worker_collect(const Agent& a, VectorizedEnvironment& env, std::size_t horizon, TransitionBuffer& buf,
+                           std::size_t segment_offset, std::size_t chunk_base, std::mt19937_64& rng) {
+  if (segment_offset != 0 || chunk_base != 0 || horizon != buf.horizon() || env.num_envs() != buf.num_envs())
+    throw UsageError("worker_collect: the device buffer holds one VecEnv's segment (offset 0, chunk base 0, its "
+                     "horizon and env count)");
+  worker_collect(a, env, buf, rng());
 }
 
 // worker_collect of every pod of a GPU in ONE launch (per-pod weights, buffers and seeds);
@@ -370,10 +422,10 @@ inline std::pair<std::vector<double>, std::vector<double>> buffer_advantages(Tra
   return {std::move(adv), std::move(ret)};
 }
 
-// ppo_update ppo.hpp:249-296: returns a trained copy; the input is untouched.
-inline std::pair<std::unique_ptr<Agent>, PpoUpdateStats> ppo_update(const Agent& a, TransitionBuffer& buf,
-                                                                    const PpoConfig& cfg, std::uint64_t seed,
-                                                                    const std::vector<std::uint64_t>* perm = nullptr) {
+// ppo_update ppo.hpp:249-296: returns a trained copy (.artifact) and its statistics (.stats);
+// the input is untouched.
+inline PpoUpdateResult ppo_update(const Agent& a, TransitionBuffer& buf, const PpoConfig& cfg, std::uint64_t seed,
+                                  const std::vector<std::uint64_t>* perm = nullptr) {
   auto out = std::make_unique<Agent>(a.context(), a.state_dim(), a.action_dim(), a.hidden());
   const prb_ppo_config c = cfg.c();
   prb_ppo_stats st{};

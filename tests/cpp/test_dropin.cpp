@@ -119,10 +119,10 @@ int main() {
   pc.epochs_per_update = 2;
   auto l0 = pb::ppo_update(*actor, buf, pc, 1);
   auto l1 = pb::ppo_update(*actor, buf, pc, 2);
-  EXPECT(l0.second.minibatches == 2 * (N * H / 128));
-  EXPECT(l0.first->optimizer_t() == (int64_t)l0.second.minibatches);
-  auto fused = pb::fuse_parameters({l0.first.get(), l1.first.get()});
-  const auto f0 = l0.first->flatten_params(), f1 = l1.first->flatten_params(), ff = fused->flatten_params();
+  EXPECT(l0.stats.minibatches == 2 * (N * H / 128));
+  EXPECT(l0.artifact->optimizer_t() == (int64_t)l0.stats.minibatches);
+  auto fused = pb::fuse_parameters({l0.artifact.get(), l1.artifact.get()});
+  const auto f0 = l0.artifact->flatten_params(), f1 = l1.artifact->flatten_params(), ff = fused->flatten_params();
   for (size_t i = 0; i < ff.size(); ++i) EXPECT(std::fabs(ff[i] - 0.5 * (f0[i] + f1[i])) <= 1e-6 * (1 + std::fabs(ff[i])));
   const auto fa = actor->flatten_params();
   bool changed = false;
@@ -148,7 +148,7 @@ int main() {
     gc.fresh_prob = 0.3;
     gc.mutation_sigma = 0.05;
     auto fresh = [&](std::uint64_t seed) { return pb::Agent::init(ctx, S, K, seed, 1e-3); };
-    std::vector<const pb::Agent*> board = {l0.first.get(), l1.first.get(), fused.get()};
+    std::vector<const pb::Agent*> board = {l0.artifact.get(), l1.artifact.get(), fused.get()};
     const std::vector<std::int64_t> ids = {11, 22, 33};
     int n_fresh = 0, n_child = 0;
     for (std::uint64_t seed = 1; seed <= 12; ++seed) {
@@ -185,7 +185,7 @@ int main() {
     std::mt19937_64 rng(5);
     pb::PodLineage lin;
     auto pod = pb::generate_pod_init({}, {}, gc, rng, fresh, &lin);  // empty board: fresh
-    EXPECT(lin.parent_pod == -1 && pod->param_count() == l0.first->param_count());
+    EXPECT(lin.parent_pod == -1 && pod->param_count() == l0.artifact->param_count());
   }
 
   // Leaderboard + leaderboard_update + refresh_stats (tournament.hpp:44-119): ties keep the earlier
@@ -276,6 +276,32 @@ int main() {
         const pb::EvaluationRecord one = pb::evaluate(*outs[p], *e1, 5 + p);
         EXPECT(one.episodic_rewards == recs[p].episodic_rewards && one.mean == recs[p].mean);
       }
+    }
+    {  // the reference-signature overloads: worker_collect(..., rng) == worker_collect(..., rng())
+      std::mt19937_64 r1(77), r2(77);
+      auto e1 = pb::VectorizedEnvironment::stock(market, cfg, start, end, NP);
+      auto e2 = pb::VectorizedEnvironment::stock(market, cfg, start, end, NP);
+      e1->reset(3);
+      e2->reset(3);
+      pb::TransitionBuffer b1(*e1, H), b2(*e2, H);
+      pb::worker_collect(*agents[0], *e1, H, b1, 0, 0, r1);
+      pb::worker_collect(*agents[0], *e2, b2, r2());
+      EXPECT(b1.rewards() == b2.rewards() && b1.actions() == b2.actions() && b1.states() == b2.states());
+      EXPECT(b1.log_probs() == b2.log_probs() && b1.values() == b2.values() && b1.dones() == b2.dones());
+      EXPECT(b1.states().size() == NP * H * S && b1.bootstrap_values().size() == NP && b1.full());
+      bool threw_seg = false;
+      try {
+        pb::worker_collect(*agents[0], *e1, H, b1, 128, 0, r1);
+      } catch (const pb::UsageError&) {
+        threw_seg = true;
+      }
+      EXPECT(threw_seg);
+      std::mt19937_64 r3(5), r4(5);
+      pb::Tensor2 st(4, S);
+      for (size_t i = 0; i < st.data.size(); ++i) st.data[i] = 0.01 * (double)(i % 97);
+      const auto s1 = pb::policy_sample(*agents[0], st, r3);
+      const auto s2 = pb::policy_sample(*agents[0], st, r4(), 0);
+      EXPECT(s1.actions.data == s2.actions.data && s1.log_probs == s2.log_probs);
     }
     pb::Agent fresh(ctx, S, K);
     fresh.init_device(60, 1e-3);
