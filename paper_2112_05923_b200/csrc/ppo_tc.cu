@@ -743,9 +743,10 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     // overwrote it -- so d3's sums are taken from the per-row values below instead)
     mma.wait();
     TCMARK(12);
-    // ---- partials: TMEM -> shared memory in the flat parameter order (the operand regions are
-    // dead), then ONE bulk store of the CTA's slab row ----
-    float* flat = reinterpret_cast<float*>(smem);  // [Pp] (dead X_hi / RB / RC / H2)
+    // ---- partials: TMEM -> this CTA's slab row in global memory, in the flat parameter order,
+    // straight from registers (a warp's 32 lanes = 32 consecutive outputs: coalesced 128-byte
+    // stores; no shared-memory staging and no bulk store to wait for) ----
+    float* flat = ch.slab + (size_t)rank * a.Pp;
     {
       const int o = lrow;  // TMEM lane = output index (actor 0-63 | critic 64-127; d3: actor 0..A-1, critic 32)
       const int oo = o & 63;
@@ -799,7 +800,6 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
     }
     TCMARK(18);
     tc::fence_before_sync();
-    __syncthreads();  // every flat entry of the TMEM blocks written
     if (tid < 128) {
       const int* w2 = (tid < 64) ? a.a_w : a.c_w;
       flat[w2[1] + 64 * 64 + (tid & 63)] = db2;
@@ -817,20 +817,9 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       if (c == 33) flat[a.P + 1] = sum;  // value loss terms
     }
     TCMARK(19);
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(((a.P + 2 + 3) & ~3) * 4);
-      float* dst = ch.slab + (size_t)rank * a.Pp;
-      constexpr uint32_t kChunk = 32768;
-      for (uint32_t o = 0; o < bytes; o += kChunk) tc::bulk_s2g(reinterpret_cast<uint8_t*>(dst) + o,
-                                                                  reinterpret_cast<const uint8_t*>(flat) + o,
-                                                                  min(kChunk, bytes - o));
-      tc::bulk_commit();
-      TCMARK(20);
-      tc::bulk_wait0();  // complete; then async proxy -> generic proxy before the barrier's release
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
+    // generic-proxy stores -> the peers' bulk (async-proxy) reads after the barrier
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    TCMARK(20);
     TCMARK(13);
     tc::fence_before_sync();
     cbar.arrive();  // release: this CTA's slab row
