@@ -732,24 +732,14 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
       mma_chain(tbase + 256, sbase + kOffBuf1, 128, 1, sbase + kOffXhi, 128, 1, 8, 192, false);
       tc::mma_commit(&s_mma);
     }
-    // db2 = column sums of d2 (BUF2, bf16, as dW2 sees them) while dW1 runs -- BUF2 lies inside
-    // the flat staging below, so the sums are held in registers
-    float db2 = 0.f;
-    if (tid < 128)
-      for (int r = 0; r < 128; ++r)
-        db2 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(smem + kOffBuf2 + core_off(r, tid, 128)));
-    __syncthreads();  // BUF2 read completely before the flat staging below overwrites it
-    // bias gradients of layers 2 and 3: column sums of d2 (BUF2) and d3 (in BUF1 until dW1's d1
-    // overwrote it -- so d3's sums are taken from the per-row values below instead)
-    mma.wait();
-    TCMARK(12);
     // ---- partials: TMEM -> this CTA's slab row in global memory, in the flat parameter order,
     // straight from registers (a warp's 32 lanes = 32 consecutive outputs: coalesced 128-byte
-    // stores; no shared-memory staging and no bulk store to wait for) ----
+    // stores; no shared-memory staging and no bulk store to wait for).  dW3^T and dW2^T are
+    // complete: they leave while the dW1 MMA runs ----
     float* flat = ch.slab + (size_t)rank * a.Pp;
+    const int o = lrow;  // TMEM lane = output index (actor 0-63 | critic 64-127; d3: actor 0..A-1, critic 32)
+    const int oo = o & 63;
     {
-      const int o = lrow;  // TMEM lane = output index (actor 0-63 | critic 64-127; d3: actor 0..A-1, critic 32)
-      const int oo = o & 63;
       // dW3^T [0,128): columns = H2 inputs (actor 0-63 | critic 64-127); half h reads its net's
       // block (tcgen05.ld is warp-collective: every lane loads, the owners store)
       {
@@ -780,6 +770,17 @@ __global__ void __launch_bounds__(kThreads, 1) ppo_tc_kernel(const PpoTcArgs a) 
           }
         }
       }
+    }
+    // db2 = column sums of d2 (BUF2, bf16, as dW2 sees them) while dW1 runs
+    float db2 = 0.f;
+    if (tid < 128)
+      for (int r = 0; r < 128; ++r)
+        db2 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(smem + kOffBuf2 + core_off(r, tid, 128)));
+    // bias gradients of layers 2 and 3: column sums of d2 (BUF2) and d3 (in BUF1 until dW1's d1
+    // overwrote it -- so d3's sums are taken from the per-row values below instead)
+    mma.wait();
+    TCMARK(12);
+    {
       // dW1^T [256,448): columns = X columns -> W1 rows (s_colk), the ones column -> b1
       {
         float* dst = (o < 64 ? flat + a.a_w[0] : flat + a.c_w[0]) + oo;
