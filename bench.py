@@ -598,7 +598,7 @@ def leg_tournament(pr, ctx, market, cfg, d, pods, learners=2, gens=2):
         out = pop.generation()
         ctx.synchronize()
         times.append(d.max(time.perf_counter() - t0))
-    # the learner phase alone: concurrent clusters vs the SIMT update one learner after another
+    # the learner phase alone: concurrent tensor-core learners vs the SIMT update one after another
     srcs = [a for a in pop.agents for _ in range(learners)]
     ros = [r for r in pop.rollouts for _ in range(learners)]
     outs = [o for lo in pop.learner_out for o in lo]

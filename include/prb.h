@@ -275,16 +275,16 @@ PRB_API int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* c
 /* Which device path prb_ppo_update runs when `a` is its src: 0 (default) = the
  * fp32 SIMT update over the whole GPU (reference-precision gradients, any
  * shape; the lowest latency for ONE learner); 1 = the tensor-core update
- * (ppo_tc.cu: one thread-block cluster of 8 SMs per learner, bf16 operands /
+ * (ppo_tc.cu: 8 co-resident CTAs per learner, bf16 operands /
  * fp32 accumulation, for actor S-64-64-A / critic S-64-64-1 nets with A <= 32
  * and minibatches <= 1,024 rows; other shapes fall back to 0) -- the path
  * prb_ppo_update_learners always takes, where many learners share the GPU. */
 PRB_API int prb_agent_set_ppo_mode(prb_agent a, int mode);
 /* pod_train's learner phase (pod.hpp:436-461): L learners, learner l running
  * ppo_update(srcs[l], rollouts[l], cfg, seeds[l]) into dsts[l] -- all of them in
- * ONE launch of the tensor-core update (one thread-block cluster of
- * ceil(minibatch / 128) CTAs per learner, ppo_tc.cu), so the learners of every
- * pod on the GPU train concurrently.  Learners of one pod pass the same rollout
+ * ONE cooperative launch of the tensor-core update (ceil(minibatch / 128)
+ * co-resident CTAs per learner, ppo_tc.cu; 18 learners of 8 CTAs per wave on a
+ * B200), so the learners of every pod on the GPU train concurrently.  Learners of one pod pass the same rollout
  * (its GAE runs once); every rollout must have the same shape, every agent the
  * shapes prb_agent_set_ppo_mode lists (else ConfigError).  Permutations are
  * drawn on the device from seeds[l].  stats (nullable) receives L entries.

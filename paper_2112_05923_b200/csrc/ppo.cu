@@ -1564,7 +1564,7 @@ void launch_persistent(const PpoArgs& p, prb_agent a, PpoWorkspace& ws, double e
 }
 
 // The tensor-core update (ppo_tc.cu) covers the stock-pod nets: actor S-64-64-A, critic
-// S-64-64-1 with A <= 32, minibatches of <= 1,024 rows (<= 8 CTAs of 128 rows per cluster), and
+// S-64-64-1 with A <= 32, minibatches of <= 1,024 rows (<= 8 CTAs of 128 rows per learner), and
 // inputs that fit its 192-column X tile (<= 32 private features + <= 156 others + the ones column).
 bool ppo_tc_supported(prb_agent a, prb_rollout r, int mb, int mode) {
   if (mode != 1) return false;
@@ -1772,7 +1772,7 @@ int prb_ppo_update(prb_agent src, prb_rollout r, const prb_ppo_config* cfg, uint
     // capture a block of them once as a CUDA graph and replay it.
     const size_t kGraphSteps = 32;
     const int pgrid = persistent_grid(p, dst, ws);
-    if (steps > 0 && ppo_tc_supported(dst, r, mb, src->ppo_mode)) {  // one cluster runs the whole chain
+    if (steps > 0 && ppo_tc_supported(dst, r, mb, src->ppo_mode)) {  // one learner's CTAs run the whole chain
       PpoTcArgs ta = make_tc_shape(p, dst, r, ws, (int64_t)steps, s);
       upload_chains(ta, {make_tc_chain(ta, dst, r, ws, p.perm, p.seed, s)}, ws.tc_chain, s);
       const char* tpath = debug_env("PRB_PPO_TC_TRACE");  // debug: phase marks of one step

@@ -355,7 +355,7 @@ class Agent:
         self.ctx.lib.prb_adam_step_device(self.h, C.c_void_p(d_grads))
 
     def set_ppo_mode(self, mode: int):
-        """0 (default): fp32 SIMT update over the whole GPU; 1: the tensor-core cluster update where the
+        """0 (default): fp32 SIMT update over the whole GPU; 1: the tensor-core update (8 co-resident CTAs per learner) where the
         shapes allow (what ppo_update_learners always runs)."""
         self.ctx.lib.prb_agent_set_ppo_mode(self.h, int(mode))
 
@@ -578,7 +578,7 @@ def collect_pods(rollouts: Sequence["Rollout"], agents: Sequence[Agent], envs: S
 def ppo_update_learners(agents: Sequence[Agent], rollouts: Sequence[Rollout], cfg: PpoConfig, seeds: Sequence[int],
                         outs: Optional[Sequence[Agent]] = None):
     """pod_train's learner phase (pod.hpp:436-461): learner l = ppo_update(agents[l], rollouts[l],
-    cfg, seeds[l]), every learner in ONE tensor-core launch (a thread-block cluster each).
+    cfg, seeds[l]), every learner in ONE tensor-core launch (8 co-resident CTAs each).
     Returns (trained copies, [PpoUpdateStats])."""
     L = len(agents)
     dsts = list(outs) if outs is not None else [Agent(a.ctx, a.state_dim, a.action_dim, a.hidden) for a in agents]

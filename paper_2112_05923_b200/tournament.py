@@ -111,11 +111,11 @@ class PodPopulation:
     Per generation (``generation``):
       1. worker_collect of every pod in ONE tcgen05 launch (prb_rollout_collect_pods: per-pod
          weights, a grouped GEMM; pod.hpp:408-433);
-      2. every pod's ``learners`` PPO learners in ONE tensor-core launch, a thread-block cluster
+      2. every pod's ``learners`` PPO learners in ONE tensor-core launch, 8 co-resident CTAs
          per learner (prb_ppo_update_learners; pod.hpp:436-461), then fuse_parameters per pod
          (pod.hpp:141-172) into the pod's agent;
-      3. evaluate each pod (prb_evaluate: ``eval_episodes`` episodes as one VecEnv, policy mean;
-         pod.hpp:43-83) -> its score;
+      3. evaluate every pod in one pass (prb_evaluate_pods: ``eval_episodes`` episodes per pod as
+         one VecEnv, policy mean; pod.hpp:43-83) -> its score;
       4. the leaderboard: every rank's (score, seq, pod_id) all-gathered over NCCL and ranked
          identically on every rank (prb_leaderboard_allgather_rank; tournament.hpp:104-119), or
          ranked on the device alone with one rank;
