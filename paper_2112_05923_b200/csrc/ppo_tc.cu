@@ -9,7 +9,8 @@
 // [128c, 128c + 128):
 //
 //   gather    X = [private features hi | rest | 1] per row as bf16 hi + lo pairs  [128 x 192]
-//   L1        D = X_hi . W1 + X_lo . W1        (actor | critic: N = 128; b1 via the ones column)
+//   L1        D = X_hi . W1_hi + X_lo . W1_hi + X_hi . W1_lo   (actor | critic in N = 128 MMAs;
+//             b1 via the ones column; W1 as bf16 hi + lo pairs too)
 //   L2        H1 = tanh(D);  D = H1_a . W2a,  D = H1_c . W2c        (+ b2 in the epilogue)
 //   heads     H2 = tanh(D);  D = H2_a . W3a (N = 32),  D = H2_c . W3c (N = 16)
 //   head grads (per row, fp32: log-prob, ratio, clipped surrogate with the tie rule of
@@ -37,7 +38,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <cstdio>
 #include <cstring>
 
 #include "ppo_tc.h"
