@@ -129,3 +129,17 @@ def test_evaluate_pods_equals_per_pod_evaluate(pr, ctx, kind, sample):
         assert np.array_equal(grouped[p].episodic_rewards, one.episodic_rewards), p
         assert grouped[p].mean == one.mean and grouped[p].std_dev == one.std_dev
         assert grouped[p].eval_steps == one.eval_steps
+
+
+def test_evaluate_pods_errors(pr, ctx):
+    """prb_evaluate_pods rejects pods whose eval VecEnvs differ in shape (UsageError) and agents that
+    do not match their envs (DimensionError); P = 0 is a no-op."""
+    a = pr.Agent.init(ctx, 6, 2, seed=1)
+    e10, e12 = pr.VectorizedEnvironment.pointmass(ctx, 10), pr.VectorizedEnvironment.pointmass(ctx, 12)
+    with pytest.raises(pr.UsageError):
+        pr.evaluate_pods([a, a], [e10, e12], [1, 2])
+    market = pr.MarketData.synthetic(ctx)
+    stock = pr.VectorizedEnvironment.stock(ctx, market, pr.StockConfig(), 1900, 1940, 10)
+    with pytest.raises((pr.DimensionError, pr.UsageError)):
+        pr.evaluate_pods([a], [stock], [1])
+    assert pr.evaluate_pods([], [], []) == []

@@ -178,6 +178,26 @@ def test_learners_equal_individual_updates(pr, ctx, orc):
         pr.ppo_update_learners([a0], [r0], cfg, [1], outs=[a0])  # src aliased as dst
 
 
+def test_learners_beyond_one_wave(pr, ctx, orc):
+    """More learners than fit on the GPU at once (8 CTAs each, 18 per wave on a B200): 20 learners
+    of a 1,024-row minibatch run in two cooperative launches and each still equals its own
+    tensor-core ppo_update exactly."""
+    N, H, mb = 32, 64, 1024
+    n = N * H
+    a0 = pr.Agent.init(ctx, S, K, seed=17)
+    r0, _ = real_buffer(pr, ctx, orc, N, H, a0, seed=3, oracle_lp=False)
+    cfg = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=n)
+    L = 20
+    outs, stats = pr.ppo_update_learners([a0] * L, [r0] * L, cfg, list(range(100, 100 + L)))
+    a0.set_ppo_mode(1)
+    for l in (0, 17, 18, 19):  # both waves, and the wave boundary
+        solo, st = pr.ppo_update(a0, r0, cfg, 100 + l)
+        assert np.array_equal(outs[l].get()[0], solo.get()[0]), l
+        assert stats[l].mean_policy_loss == st.mean_policy_loss and stats[l].minibatches == st.minibatches == n // mb
+    a0.set_ppo_mode(0)
+    assert len({outs[l].flatten_params().tobytes() for l in range(L)}) == L  # distinct seeds, distinct results
+
+
 def test_tc_gate_midway_keeps_last_accepted_step(pr, ctx, orc):
     """A NaN old log-prob in the third minibatch: NumericError, and the destination holds exactly the
     state after two accepted steps -- the same as a clean 2-step update (nn.hpp:169-171)."""
