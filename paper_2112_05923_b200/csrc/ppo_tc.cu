@@ -177,12 +177,17 @@ __device__ __forceinline__ uint32_t mb_index(const PpoTcArgs& a, const PpoTcChai
   return feistel(pos, a.n, a.bits, derive_seed2(ch.seed, 0x50504fULL /*"PPO"*/, epoch));
 }
 
-// adam_step (nn.hpp:164-182) for one fp32 parameter, every rounding explicit (as ppo.cu)
+// adam_step (nn.hpp:164-182) for one fp32 parameter.  The reference runs it in fp64; this path
+// (bf16 operands, fp32 master weights) is held to a tolerance, not to the SIMT path's bits, so the
+// square root and the division are the hardware approximations (~2 ulp) rather than the IEEE
+// sequences: 16 parameters per thread per step, on the step's critical path.
 __device__ __forceinline__ void adam_param(float b1, float b2, float omb1, float omb2, float lr, float eps, float ibc1,
                                            float ibc2, float g, float& m, float& v, float& w) {
   m = __fmaf_rn(b1, m, __fmul_rn(omb1, g));
   v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
-  w = __fsub_rn(w, __fdiv_rn(__fmul_rn(lr, __fmul_rn(m, ibc1)), __fadd_rn(__fsqrt_rn(__fmul_rn(v, ibc2)), eps)));
+  float sq;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(v * ibc2));
+  w = w - __fdividef(lr * (m * ibc1), sq + eps);
 }
 
 // Where flat parameter p lives in the weight image: *bf16 = byte offset of its bf16 copy (or -1),
