@@ -269,11 +269,11 @@ __global__ void __launch_bounds__(kEnvBlock) stock_step_v2_kernel(StockStepArgs 
 // else and consumed from registers; the share table stays in shared memory for
 // the obs writer.  ~170 B of shared memory per env -> ~2x the resident warps
 // of v2, which is what keeps HBM busy while other CTAs run the fp64 chain.
-template <int KMAX, int EB>
 #ifndef PRB_ENV_TPS
 #define PRB_ENV_TPS 1024  // resident threads per SM the register budget is sized for
 #endif
-__global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB) stock_step_v3_kernel(StockStepArgs a) {
+template <int KMAX, int EB>
+__device__ __forceinline__ void stock_step_v3_body(const StockStepArgs& a, size_t tile) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, F = 5 * K, Kp = K + 1;  // K even -> odd stride
   double* s_p0 = reinterpret_cast<double*>(smem_raw);          // [K]
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB) stock_step_v3_kernel(Sto
   float* s_feat_obs = s_x0 + EB;                            // [5K]
   float* s_feat_term = s_feat_obs + F;                             // [5K]
   const int tid = threadIdx.x;
-  const size_t e0 = (size_t)blockIdx.x * EB;
+  const size_t e0 = tile * EB;
   const int nloc = min(EB, a.N - (int)e0);
   const bool live = tid < nloc;
   const size_t e = e0 + tid;
@@ -383,6 +383,24 @@ __global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB) stock_step_v3_kernel(Sto
     __syncthreads();
   }
   write_obs_tab(a.obs + e0 * S, nloc, S, table, K, Kp, s_feat_obs);
+}
+
+template <int KMAX, int EB>
+__global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB) stock_step_v3_kernel(StockStepArgs a) {
+  stock_step_v3_body<KMAX, EB>(a, blockIdx.x);
+}
+
+// several lock-step VecEnvs of one market (the evaluation VecEnvs of a GPU's pods) in one launch:
+// blockIdx.y = env; the per-step scalars are the launch's, the pointers per env
+template <int KMAX, int EB>
+__global__ void __launch_bounds__(EB, PRB_ENV_TPS / EB)
+    stock_step_v3_group_kernel(const StockStepArgs* __restrict__ group, int t, int t_obs, int done, int ep_len) {
+  StockStepArgs a = group[blockIdx.y];
+  a.t = t;
+  a.t_obs = t_obs;
+  a.done = done;
+  a.ep_len = ep_len;
+  if ((size_t)blockIdx.x * EB < (size_t)a.N) stock_step_v3_body<KMAX, EB>(a, blockIdx.x);
 }
 
 size_t stock_v3_smem_bytes(int K, int eb = kEnvBlock) {
@@ -561,6 +579,71 @@ void prb_pm_step_launch(prb_vecenv env, const float* d_actions, float* d_reward,
     pm_step_kernel<<<grid, 256, 0, env->ctx->stream>>>(a);
   }
   PRB_CHECK_LAUNCH();
+}
+
+size_t prb_env_group_args_bytes(int P) { return (size_t)P * sizeof(StockStepArgs); }
+
+bool prb_env_step_group(const prb_vecenv* envs, int P, const float* d_act, size_t act_stride, float* d_rew,
+                        uint8_t* d_done, double* d_tret, int32_t* d_tlen, size_t n_stride, void* d_args, bool upload) {
+  if (P < 1) return false;
+  const prb_vecenv_s* e0 = envs[0];
+  if (e0->kind != PRB_KIND_STOCK || !e0->was_reset) return false;
+  prb_market_s* m = e0->market;
+  if (!(m->K <= 32 && (m->K & 1) == 0 && e0->cfg.max_trade_shares < 16777216.0)) return false;
+  for (int p = 1; p < P; ++p) {  // lock-step copies of one VecEnv shape, market, window and clock
+    const prb_vecenv_s* e = envs[p];
+    if (e->kind != PRB_KIND_STOCK || !e->was_reset || e->market != m || e->N != e0->N || e->start != e0->start ||
+        e->end != e0->end || e->t != e0->t || e->step_count != e0->step_count || e->ctx != e0->ctx ||
+        e->cfg.initial_capital != e0->cfg.initial_capital || e->cfg.max_trade_shares != e0->cfg.max_trade_shares ||
+        e->cfg.cost_rate != e0->cfg.cost_rate)
+      return false;
+  }
+  PRB_REQUIRE(e0->t + 1 < m->T, PRB_ERR_USAGE, "stock_env_step: no next timestamp at t=" + std::to_string(e0->t));
+  StockStepArgs* g = static_cast<StockStepArgs*>(d_args);
+  if (upload) {
+    std::vector<StockStepArgs> h(P);
+    for (int p = 0; p < P; ++p) {
+      prb_vecenv_s* env = envs[p];
+      StockStepArgs& a = h[p];
+      a = StockStepArgs{};
+      a.N = (int)env->N;
+      a.K = m->K;
+      a.S = (int)env->S;
+      a.close_tk = m->d_close_tk.p;
+      a.feat = env->d_feat.p;
+      a.cap = env->cfg.initial_capital;
+      a.max_trade = env->cfg.max_trade_shares;
+      a.cost = env->cfg.cost_rate;
+      a.actions = d_act + (size_t)p * act_stride;
+      a.balance = env->d_balance.p;
+      a.shares = env->d_shares.p;
+      a.ep_return = env->d_ep_return.p;
+      a.obs = env->d_obs.p;
+      a.reward = d_rew + (size_t)p * n_stride;
+      a.done_out = d_done + (size_t)p * n_stride;
+      a.term_obs = nullptr;
+      a.term_ret = d_tret + (size_t)p * n_stride;
+      a.term_len = d_tlen + (size_t)p * n_stride;
+    }
+    PRB_CUDA(cudaMemcpyAsync(g, h.data(), (size_t)P * sizeof(StockStepArgs), cudaMemcpyHostToDevice,
+                             e0->ctx->stream));
+    PRB_CUDA(cudaStreamSynchronize(e0->ctx->stream));  // h lives on this stack frame
+  }
+  const size_t t1 = e0->t + 1;
+  const bool done = (t1 + 1 >= m->T) || (t1 >= e0->end);  // stock_env.hpp:101,168
+  constexpr int kEb = 256;
+  const int gN = (int)((e0->N + kEb - 1) / kEb);
+  {
+    ProfScope prof(e0->ctx, kProfEnvStock);
+    stock_step_v3_group_kernel<32, kEb><<<dim3(gN, P), kEb, stock_v3_smem_bytes(m->K, kEb), e0->ctx->stream>>>(
+        g, (int)e0->t, done ? (int)e0->start : (int)t1, done ? 1 : 0, (int)(e0->step_count + 1));
+  }
+  PRB_CHECK_LAUNCH();
+  for (int p = 0; p < P; ++p) {
+    envs[p]->t = done ? envs[p]->start : t1;
+    envs[p]->step_count = done ? 0 : envs[p]->step_count + 1;
+  }
+  return true;
 }
 
 void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,

@@ -140,7 +140,8 @@ int prb_evaluate_pods(const prb_agent* agents, const prb_vecenv* envs, size_t P,
     const size_t PN = P * N;
     const size_t o_rew = up(PN * A * 4), o_lp = o_rew + up(PN * 4), o_done = o_lp + up(PN * 4),
                  o_tret = o_done + up(PN), o_tlen = o_tret + up(PN * 8), o_fret = o_tlen + up(PN * 4),
-                 o_flen = o_fret + up(PN * 8), o_args = o_flen + up(PN * 4), total = o_args + up(P * sizeof(PolicyArgs));
+                 o_flen = o_fret + up(PN * 8), o_args = o_flen + up(PN * 4), o_env = o_args + up(P * sizeof(PolicyArgs)),
+                 total = o_env + up(prb_env_group_args_bytes((int)P));
     uint8_t* base = static_cast<uint8_t*>(ctx->device_scratch(total));
     float* act = reinterpret_cast<float*>(base);
     float* rew = reinterpret_cast<float*>(base + o_rew);
@@ -151,6 +152,7 @@ int prb_evaluate_pods(const prb_agent* agents, const prb_vecenv* envs, size_t P,
     double* first_ret = reinterpret_cast<double*>(base + o_fret);
     int32_t* first_len = reinterpret_cast<int32_t*>(base + o_flen);
     PolicyArgs* d_args = reinterpret_cast<PolicyArgs*>(base + o_args);
+    void* d_env_args = base + o_env;
     PRB_CUDA(cudaMemsetAsync(first_len, 0, PN * sizeof(int32_t), s));
     std::vector<PolicyArgs> args(P);
     for (size_t p = 0; p < P; ++p) {
@@ -170,11 +172,15 @@ int prb_evaluate_pods(const prb_agent* agents, const prb_vecenv* envs, size_t P,
     }
     PRB_CUDA(cudaMemcpyAsync(d_args, args.data(), P * sizeof(PolicyArgs), cudaMemcpyHostToDevice, s));
     const size_t smem = prb_policy_smem(args[0]);
+    bool grouped = true;  // the pods' stock eval VecEnvs step in one launch when they are lock-step
     for (size_t step = 0; step < T; ++step) {
       prb_policy_launch_group(d_args, (int)P, N, smem, step, ctx);
-      for (size_t p = 0; p < P; ++p)
-        prb_env_step_launch(envs[p], act + p * N * A, rew + p * N, done + p * N, nullptr, tret + p * N,
-                            tlen + p * N);
+      if (grouped)
+        grouped = prb_env_step_group(envs, (int)P, act, N * A, rew, done, tret, tlen, N, d_env_args, step == 0);
+      if (!grouped)
+        for (size_t p = 0; p < P; ++p)
+          prb_env_step_launch(envs[p], act + p * N * A, rew + p * N, done + p * N, nullptr, tret + p * N,
+                              tlen + p * N);
       capture_first_done<<<(unsigned)((PN + 255) / 256), 256, 0, s>>>(PN, done, tret, tlen, first_ret, first_len);
       PRB_CHECK_LAUNCH();
     }

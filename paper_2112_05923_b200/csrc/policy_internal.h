@@ -48,5 +48,12 @@ void prb_policy_launch_group(const PolicyArgs* d_group, int P, size_t n_max, siz
                              prb_ctx_s* ctx);
 void prb_env_step_launch(prb_vecenv env, const float* d_actions, float* d_reward, uint8_t* d_done, float* d_term_obs,
                          double* d_term_ret, int32_t* d_term_len);
+// One launch stepping P lock-step stock VecEnvs of one market and window (the evaluation VecEnvs of
+// a GPU's pods): env p's actions at d_act + p * act_stride, its outputs at + p * n_stride.  The
+// argument block (d_args, prb_env_group_args_bytes(P)) is uploaded when `upload`.  Returns false,
+// doing nothing, when the envs are not such a group (the caller steps them one by one).
+size_t prb_env_group_args_bytes(int P);
+bool prb_env_step_group(const prb_vecenv* envs, int P, const float* d_act, size_t act_stride, float* d_rew,
+                        uint8_t* d_done, double* d_tret, int32_t* d_tlen, size_t n_stride, void* d_args, bool upload);
 void prb_adam_launch(prb_agent a, const float* d_grads, const int32_t* gate, cudaStream_t s);
 void prb_agent_finite_gate_and_adam(prb_agent a, const float* d_grads, cudaStream_t s);
