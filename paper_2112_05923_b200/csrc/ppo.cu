@@ -1112,8 +1112,11 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int& 
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
     unsigned int v;
+    unsigned long long t0 = 0;
+    int polls = 0;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+      if ((++polls & 1023) == 0) barrier_watchdog(t0);
     } while ((int)(v - target) < 0);
   }
   __syncthreads();

@@ -143,8 +143,11 @@ struct ChainBar {
   __device__ __forceinline__ void wait() {
     if (threadIdx.x == 0) {
       uint32_t v;
+      unsigned long long t0 = 0;
+      int polls = 0;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if ((++polls & 1023) == 0) barrier_watchdog(t0);
       } while ((int32_t)(v - target) < 0);
     }
     __syncthreads();

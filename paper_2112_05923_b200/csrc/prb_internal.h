@@ -108,6 +108,18 @@ uint64_t derive_seed(uint64_t base, std::initializer_list<uint64_t> tags);
 // Handle structs (opaque in prb.h).
 // ---------------------------------------------------------------------------
 
+// Spin-barrier watchdog (device): a barrier still waiting 20 s after its first check aborts the
+// kernel (a CUDA error on the host) instead of hanging the GPU.  Called every 1,024 polls.
+__device__ __forceinline__ void barrier_watchdog(unsigned long long& t0) {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  if (t0 == 0) {
+    t0 = g;
+  } else if (g - t0 > 20000000000ULL) {
+    asm volatile("trap;");
+  }
+}
+
 struct prb_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
