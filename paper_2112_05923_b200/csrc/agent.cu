@@ -113,12 +113,26 @@ __global__ void finite_check_kernel(const float* __restrict__ g, size_t n, int32
   }
 }
 
-__global__ void fuse_kernel(const float* const* __restrict__ src, size_t L, size_t n, float* __restrict__ dst,
-                            float inv) {
+// params, m and v of L agents (src: L param pointers, then L m, then L v) -> their means, one
+// pass; element i of every output is written after every input's element i is read, so an
+// output may alias an input.  Block 0 also sets t = max of the L counters (pod.hpp:149-171).
+__global__ void fuse_kernel(const float* const* __restrict__ src, const int64_t* const* __restrict__ ts, size_t L,
+                            size_t n, float* dst_p, float* dst_m, float* dst_v, int64_t* dst_t, float inv) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    float s = 0.0f;
-    for (size_t a = 0; a < L; ++a) s += src[a][i];
-    dst[i] = s * inv;
+    float sp = 0.0f, sm = 0.0f, sv = 0.0f;
+    for (size_t a = 0; a < L; ++a) {
+      sp += src[a][i];
+      sm += src[L + a][i];
+      sv += src[2 * L + a][i];
+    }
+    dst_p[i] = sp * inv;
+    dst_m[i] = sm * inv;
+    dst_v[i] = sv * inv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // every counter read before the (possibly aliased) write
+    int64_t t = 0;
+    for (size_t a = 0; a < L; ++a) t = max(t, *ts[a]);
+    *dst_t = t;
   }
 }
 
@@ -448,47 +462,23 @@ int prb_fuse_parameters(const prb_agent* agents, size_t n, prb_agent out) {
       }
       return;
     }
-    // mean of params, m, v; t = max (pod.hpp:149-171)
-    std::vector<const float*> hp(n), hm(n), hv(n);
+    // mean of params, m, v; t = max (pod.hpp:149-171) -- one kernel, no host round trips
+    std::vector<const void*> all(4 * n);
     for (size_t i = 0; i < n; ++i) {
-      hp[i] = agents[i]->d_params.p;
-      hm[i] = agents[i]->d_m.p;
-      hv[i] = agents[i]->d_v.p;
+      all[i] = agents[i]->d_params.p;
+      all[n + i] = agents[i]->d_m.p;
+      all[2 * n + i] = agents[i]->d_v.p;
+      all[3 * n + i] = agents[i]->d_t.p;
     }
-    const float** dptr = static_cast<const float**>(ctx->device_scratch(3 * n * sizeof(float*)));
-    std::vector<const float*> all;
-    all.insert(all.end(), hp.begin(), hp.end());
-    all.insert(all.end(), hm.begin(), hm.end());
-    all.insert(all.end(), hv.begin(), hv.end());
-    PRB_CUDA(cudaMemcpyAsync(dptr, all.data(), all.size() * sizeof(float*), cudaMemcpyHostToDevice, s));
+    const void** dptr = static_cast<const void**>(ctx->device_scratch(4 * n * sizeof(void*)));
+    PRB_CUDA(cudaMemcpyAsync(dptr, all.data(), all.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
     const float inv = (float)(1.0 / (double)n);
     const size_t P = out->P;
     const int grid = (int)std::min<size_t>((P + 255) / 256, 1184);
-    // Aliasing is safe only when out is not an input; stage through grads when it is.
-    bool alias = false;
-    for (size_t i = 0; i < n; ++i) alias |= (agents[i] == out);
-    float* dst_p = alias ? out->d_grads.p : out->d_params.p;
-    fuse_kernel<<<grid, 256, 0, s>>>(dptr, n, P, dst_p, inv);
-    if (alias) {
-      PRB_CUDA(cudaStreamSynchronize(s));
-      PRB_CUDA(cudaMemcpyAsync(out->d_params.p, dst_p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      fuse_kernel<<<grid, 256, 0, s>>>(dptr + n, n, P, out->d_grads.p, inv);
-      PRB_CUDA(cudaMemcpyAsync(out->d_m.p, out->d_grads.p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      fuse_kernel<<<grid, 256, 0, s>>>(dptr + 2 * n, n, P, out->d_grads.p, inv);
-      PRB_CUDA(cudaMemcpyAsync(out->d_v.p, out->d_grads.p, P * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    } else {
-      fuse_kernel<<<grid, 256, 0, s>>>(dptr + n, n, P, out->d_m.p, inv);
-      fuse_kernel<<<grid, 256, 0, s>>>(dptr + 2 * n, n, P, out->d_v.p, inv);
-    }
+    fuse_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float* const*>(dptr),
+                                     reinterpret_cast<const int64_t* const*>(dptr + 3 * n), n, P, out->d_params.p,
+                                     out->d_m.p, out->d_v.p, out->d_t.p, inv);
     PRB_CHECK_LAUNCH();
-    int64_t tmax = 0;
-    for (size_t i = 0; i < n; ++i) {
-      int64_t ti = 0;
-      PRB_CUDA(cudaMemcpyAsync(&ti, agents[i]->d_t.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      ctx->sync();
-      tmax = std::max(tmax, ti);
-    }
-    PRB_CUDA(cudaMemcpyAsync(out->d_t.p, &tmax, sizeof(int64_t), cudaMemcpyHostToDevice, s));
     out->lr = agents[0]->lr;
     ctx->sync();
   });

@@ -404,6 +404,9 @@ def test_fuse_parity(pr, ctx, orc):
     assert all(np.array_equal(x, y) for x, y in zip(single.get()[:3], agents[0].get()[:3]))
     with pytest.raises(pr.UsageError):
         pr.fuse_parameters([agents[0], pr.Agent(ctx, S, A, (5,))])
+    # the output may be one of the inputs (the elementwise mean reads every input before writing)
+    aliased = pr.fuse_parameters(agents, out=agents[1])
+    assert all(np.array_equal(x, y) for x, y in zip(aliased.get()[:3], got[:3])) and aliased.get()[3] == 9
 
 
 def test_leaderboard_rank_matches_sequential_insertion(pr, ctx, orc):
