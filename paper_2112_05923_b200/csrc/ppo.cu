@@ -1945,19 +1945,29 @@ int prb_ppo_update_learners(const prb_agent* srcs, const prb_rollout* rollouts, 
         fclose(f);
       }
     }
+    // every learner's status and statistics in one batch of copies, one synchronisation
+    struct Rec {
+      double h[4];
+      int32_t st[2];
+      int32_t pad[2];
+    };
+    Rec* rec = static_cast<Rec*>(dsts[0]->ctx->pinned_staging(L * sizeof(Rec)));
+    for (size_t l = 0; l < L; ++l) {
+      PpoWorkspace& ws = *static_cast<PpoWorkspace*>(dsts[l]->ppo_ws.get());
+      PRB_CUDA(cudaMemcpyAsync(rec[l].st, dsts[l]->d_status.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      if (stats) PRB_CUDA(cudaMemcpyAsync(rec[l].h, ws.tc_stats.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    PRB_CUDA(cudaStreamSynchronize(s));
     int first_code = 0, first_detail = 0;
     for (size_t l = 0; l < L; ++l) {
-      int32_t st[2];
-      PRB_CUDA(cudaMemcpy(st, dsts[l]->d_status.p, sizeof(st), cudaMemcpyDeviceToHost));
+      const int32_t* st = rec[l].st;
       if (st[0] && !first_code) {
         first_code = st[0];
         first_detail = st[1];
       }
-      if (st[0]) PRB_CUDA(cudaMemset(dsts[l]->d_status.p, 0, 4 * sizeof(int32_t)));
+      if (st[0]) PRB_CUDA(cudaMemsetAsync(dsts[l]->d_status.p, 0, 4 * sizeof(int32_t), s));
       if (stats) {
-        double h[4];
-        PpoWorkspace& ws = *static_cast<PpoWorkspace*>(dsts[l]->ppo_ws.get());
-        PRB_CUDA(cudaMemcpy(h, ws.tc_stats.p, sizeof(h), cudaMemcpyDeviceToHost));
+        const double* h = rec[l].h;
         stats[l].minibatches = (uint64_t)h[3];
         const double inv = h[3] > 0 ? 1.0 / h[3] : 0.0;
         stats[l].mean_policy_loss = h[0] * inv;
@@ -1965,6 +1975,7 @@ int prb_ppo_update_learners(const prb_agent* srcs, const prb_rollout* rollouts, 
         stats[l].mean_entropy = h[2] * inv;
       }
     }
+    PRB_CUDA(cudaStreamSynchronize(s));
     if (first_code) fail(first_code, status_message(first_detail));
   });
 }
