@@ -34,6 +34,15 @@ __global__ void capture_first_done(size_t N, const uint8_t* __restrict__ done, c
   }
 }
 
+// A few evaluation rows per CTA: stage the actor's weights in shared memory when they fit (the
+// 64x64 stock actor: 70 KB), so the forward does not walk them from L2 (same arithmetic).
+void stage_actor(PolicyArgs& p, prb_agent a) {
+  if (p.actor.off[0] != 0) return;
+  PolicyArgs q = p;
+  q.stage_actor_floats = (int)a->Pa;
+  if (prb_policy_smem(q) <= 200 * 1024) p.stage_actor_floats = (int)a->Pa;
+}
+
 }  // namespace
 
 extern "C" {
@@ -71,6 +80,7 @@ int prb_evaluate(prb_agent a, prb_vecenv env, uint64_t seed, int sample_actions,
     // loop is bounded; the first-done capture makes later steps inert
     for (size_t step = 0; step < env->max_episode_steps; ++step) {
       PolicyArgs p = prb_policy_args(a, env->d_obs.p, N);
+      stage_actor(p, a);
       if (sample_actions) {  // nn.hpp:250-265 with Philox noise (the reference draws mt19937_64 normals)
         p.mode = kPolicySample;
         p.seed = noise_seed;
@@ -159,6 +169,7 @@ int prb_evaluate_pods(const prb_agent* agents, const prb_vecenv* envs, size_t P,
       prb_vecenv_reset_tagged(envs[p], seeds[p], kTagEpisode);
       PolicyArgs& a = args[p];
       a = prb_policy_args(agents[p], envs[p]->d_obs.p, N);
+      stage_actor(a, agents[p]);
       if (sample_actions) {
         a.mode = kPolicySample;
         a.seed = derive_seed(seeds[p], {kTagEpisode});

@@ -14,6 +14,7 @@
 #include "policy_internal.h"
 #include "prb_internal.h"
 #include "rng.cuh"
+#include "tc.cuh"
 
 using namespace prb;
 
@@ -34,6 +35,17 @@ __device__ __forceinline__ void policy_body(const PolicyArgs& p, size_t tile) {
   const int ldA = round4(A);
   const size_t row0 = tile * R;
   const int nrows = (p.n - row0 < (size_t)R) ? (int)(p.n - row0) : R;
+  // optional staged actor weights, after the activation tiles (16-byte aligned)
+  float* s_w = s_mean + ((R * ldA + 3) & ~3);
+  __shared__ __align__(8) uint64_t s_wbar;
+  const bool stage = p.stage_actor_floats > 0 && p.mode != kPolicyValueOnly;
+  if (stage && threadIdx.x == 0) {
+    tc::mbar_init(&s_wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)(((size_t)p.stage_actor_floats * 4 + 15) & ~(size_t)15);
+    tc::mbar_arrive_expect_tx(&s_wbar, bytes);
+    tc::bulk_g2s(s_w, p.params, bytes, &s_wbar);
+  }
 
   // ---- load the state tile (rows are contiguous in memory) ----
   {
@@ -64,7 +76,19 @@ __device__ __forceinline__ void policy_body(const PolicyArgs& p, size_t tile) {
       acts[l] = (l + 1 == p.actor.nl) ? s_mean : ((l & 1) ? buf1 : buf0);
       lds[l] = (l + 1 == p.actor.nl) ? ldA : p.ldw;
     }
-    mlp_forward_tile(p.params, p.actor, s_x, ldx, acts, lds, nrows);
+    if (stage) {
+      __syncthreads();  // the barrier's initialisation before anyone waits on it
+      tc::mbar_wait(&s_wbar, 0);
+      LayerPtrs lp;
+      for (int l = 0; l < p.actor.nl; ++l) {
+        lp.W[l] = s_w + p.actor.off[l];
+        lp.B[l] = lp.W[l] + (size_t)p.actor.dims[l] * p.actor.dims[l + 1];
+        lp.ldw[l] = p.actor.dims[l + 1];
+      }
+      mlp_forward_tile_p(p.actor, lp, s_x, ldx, acts, lds, nrows);
+    } else {
+      mlp_forward_tile(p.params, p.actor, s_x, ldx, acts, lds, nrows);
+    }
   }
   // ---- critic (value head) ----
   if (p.values) {
@@ -177,7 +201,9 @@ size_t prb_policy_smem(const PolicyArgs& p) {
   const int R = p.rows_per_cta;
   const int ldx = (p.actor.dims[0] + 3) & ~3;
   const int ldA = (p.A + 3) & ~3;
-  return (size_t)R * (ldx + 2 * p.ldw + ldA) * sizeof(float);
+  const size_t tiles = (size_t)R * (ldx + 2 * p.ldw) + (((size_t)R * ldA + 3) & ~(size_t)3);
+  return (tiles + (p.stage_actor_floats > 0 ? (((size_t)p.stage_actor_floats + 3) & ~(size_t)3) : 0)) *
+         sizeof(float);
 }
 
 void prb_policy_launch(const PolicyArgs& p, prb_ctx_s* ctx) {

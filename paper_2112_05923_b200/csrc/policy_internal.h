@@ -37,6 +37,10 @@ struct PolicyArgs {
   float* obs_store;  // optional: first store_cols of every state row
   int store_cols;
   int32_t* status;
+  // > 0: the actor MLP block (this many floats at the start of params) is bulk-copied into shared
+  // memory first and the forward reads it there (a few rows per CTA: the weight walk from L2 is
+  // otherwise the whole cost); 0: weights read from global memory
+  int stage_actor_floats;
 };
 
 PolicyArgs prb_policy_args(prb_agent a, const float* d_states, size_t n);
