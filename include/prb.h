@@ -285,8 +285,9 @@ PRB_API int prb_agent_set_ppo_mode(prb_agent a, int mode);
  * ONE cooperative launch of the tensor-core update (ceil(minibatch / 128)
  * co-resident CTAs per learner, ppo_tc.cu; 18 learners of 8 CTAs per wave on a
  * B200), so the learners of every pod on the GPU train concurrently.  Learners of one pod pass the same rollout
- * (its GAE runs once); every rollout must have the same shape, every agent the
- * shapes prb_agent_set_ppo_mode lists (else ConfigError).  Permutations are
+ * (its GAE runs once); every rollout must have the same shape.  Agents of other
+ * shapes than prb_agent_set_ppo_mode lists run their updates one after another on
+ * the SIMT path (same results as prb_ppo_update each).  Permutations are
  * drawn on the device from seeds[l].  stats (nullable) receives L entries.
  * NumericError if a learner's gate failed (its dst holds its last accepted
  * step; the other learners finish their updates). */

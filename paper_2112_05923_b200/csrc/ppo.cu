@@ -1888,9 +1888,22 @@ int prb_ppo_update_learners(const prb_agent* srcs, const prb_rollout* rollouts, 
                 "ppo_update: buffer length " + std::to_string(n) + " shorter than minibatch_size " +
                     std::to_string(cfg->minibatch_size));
     const int mb = (int)cfg->minibatch_size;
-    PRB_REQUIRE(ppo_tc_supported(dsts[0], r0, mb, 1), PRB_ERR_CONFIG,
-                "ppo_update_learners: needs the tensor-core update's shapes (actor S-64-64-A / critic S-64-64-1, "
-                "A <= 32, minibatch <= 1024)");
+    if (!ppo_tc_supported(dsts[0], r0, mb, 1)) {
+      // other shapes (e.g. PointMass 3x256): each learner's own update on the whole-GPU SIMT path,
+      // one after another; a learner whose gate fails keeps its last accepted step and the
+      // others still run (the first failure is reported)
+      int first = 0;
+      std::string msg;
+      for (size_t l = 0; l < L; ++l) {
+        const int rc = prb_ppo_update(srcs[l], rollouts[l], cfg, seeds[l], nullptr, dsts[l], stats ? &stats[l] : nullptr);
+        if (rc && !first) {
+          first = rc;
+          msg = prb_last_error();
+        }
+      }
+      if (first) fail(first, msg);
+      return;
+    }
     cudaStream_t s = dsts[0]->ctx->stream;
     // GAE + normalisation once per distinct buffer (learners of one pod share it)
     for (size_t l = 0; l < L; ++l) {

@@ -578,7 +578,8 @@ def collect_pods(rollouts: Sequence["Rollout"], agents: Sequence[Agent], envs: S
 def ppo_update_learners(agents: Sequence[Agent], rollouts: Sequence[Rollout], cfg: PpoConfig, seeds: Sequence[int],
                         outs: Optional[Sequence[Agent]] = None):
     """pod_train's learner phase (pod.hpp:436-461): learner l = ppo_update(agents[l], rollouts[l],
-    cfg, seeds[l]), every learner in ONE tensor-core launch (8 co-resident CTAs each).
+    cfg, seeds[l]), every learner in ONE tensor-core launch (8 co-resident CTAs each); nets the
+    tensor-core update does not support run one after another on the SIMT path.
     Returns (trained copies, [PpoUpdateStats])."""
     L = len(agents)
     dsts = list(outs) if outs is not None else [Agent(a.ctx, a.state_dim, a.action_dim, a.hidden) for a in agents]

@@ -198,6 +198,24 @@ def test_learners_beyond_one_wave(pr, ctx, orc):
     assert len({outs[l].flatten_params().tobytes() for l in range(L)}) == L  # distinct seeds, distinct results
 
 
+def test_learners_other_shapes_run_serially(pr, ctx):
+    """ppo_update_learners with nets the tensor-core update does not take (PointMass 3x256): each
+    learner runs its own SIMT update, results identical to ppo_update one by one."""
+    N, H, mb = 64, 32, 256
+    env = pr.VectorizedEnvironment.pointmass(ctx, N)
+    env.reset(2)
+    a0 = pr.Agent.init(ctx, 6, 2, seed=3, hidden=(256, 256, 256))
+    ro = pr.Rollout.for_env(env, H)
+    ro.collect(a0, env, seed=4)
+    cfg = pr.PpoConfig(epochs_per_update=1, minibatch_size=mb, buffer_size=N * H)
+    outs, stats = pr.ppo_update_learners([a0, a0], [ro, ro], cfg, [7, 8])
+    for l, sd in enumerate((7, 8)):
+        solo, st = pr.ppo_update(a0, ro, cfg, sd)
+        assert np.array_equal(outs[l].get()[0], solo.get()[0]), l
+        assert stats[l].minibatches == st.minibatches == (N * H) // mb
+    assert not np.array_equal(outs[0].get()[0], outs[1].get()[0])
+
+
 def test_tc_gate_midway_keeps_last_accepted_step(pr, ctx, orc):
     """A NaN old log-prob in the third minibatch: NumericError, and the destination holds exactly the
     state after two accepted steps -- the same as a clean 2-step update (nn.hpp:169-171)."""
