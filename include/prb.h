@@ -200,9 +200,10 @@ PRB_API int prb_rollout_collect(prb_rollout r, prb_agent a, prb_vecenv env, uint
 /* worker_collect of P pods at once (all pods of a GPU in
  * ONE launch, per-pod weights as a grouped GEMM): rollout p = worker_collect(
  * agents[p], envs[p]) with noise seed seeds[p], exactly what P separate
- * prb_rollout_collect calls in mode 2 compute.  Every pod: a stock VecEnv on
- * the tcgen05 path (64x64 nets), the same num_envs, horizon and asset count;
- * rollouts and VecEnvs distinct. */
+ * prb_rollout_collect calls in mode 2 compute, when every pod is a stock VecEnv
+ * on the tcgen05 path (64x64 nets) with the same num_envs, horizon and asset
+ * count; other pods (e.g. PointMass) are collected one by one.  Rollouts and
+ * VecEnvs distinct. */
 PRB_API int prb_rollout_collect_pods(const prb_rollout* rollouts, const prb_agent* agents, const prb_vecenv* envs,
                                      size_t P, const uint64_t* seeds);
 /* Collection mode.  When the shapes allow it (stock env, 64x64 nets):

@@ -42,6 +42,7 @@ void alloc_rollout(prb_rollout_s* r) {
 bool prb_fused_rollout_supported(prb_rollout r, prb_agent a, prb_vecenv env);
 void prb_tc_rollout_pods(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P,
                          const uint64_t* seeds);
+bool prb_tc_rollout_pods_supported(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P);
 
 // configs[2]: PointMass2D with the 3x256 actor/critic -> rollout_pm_tc.cu
 static bool pm_tc_supported(prb_rollout r, prb_agent a, prb_vecenv env) {
@@ -245,6 +246,13 @@ int prb_rollout_collect_pods(const prb_rollout* rs, const prb_agent* as, const p
       }
     }
     DeviceScope dev_(rs[0]->ctx);
+    if (!prb_tc_rollout_pods_supported(rs, as, es, P)) {  // other envs / nets: one collect per pod
+      for (size_t p = 0; p < P; ++p) {
+        const int rc = prb_rollout_collect(rs[p], as[p], es[p], seeds[p]);
+        if (rc) fail(rc, prb_last_error());
+      }
+      return;
+    }
     prb_tc_rollout_pods(rs, as, es, P, seeds);
     for (size_t p = 0; p < P; ++p) {
       rs[p]->full = true;

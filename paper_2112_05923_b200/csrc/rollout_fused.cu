@@ -489,6 +489,22 @@ void prb_fused_rollout_launch(prb_rollout r, prb_agent a, prb_vecenv env, uint64
 // own buffers in the rollout), then pods x tiles CTAs run, each with its pod's weights, env state
 // and rollout buffer.  Every pod: the tcgen05 stock path (64x64 nets, K in {1,2,3,30}), the same
 // num_envs / horizon / K.
+// whether P pods can be collected by ONE grouped tcgen05 launch (prb_tc_rollout_pods)
+bool prb_tc_rollout_pods_supported(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P) {
+  const size_t N = rs[0]->N, H = rs[0]->H;
+  if (es[0]->kind != PRB_KIND_STOCK) return false;
+  const int K = es[0]->market->K;
+  for (size_t p = 0; p < P; ++p) {
+    prb_rollout r = rs[p];
+    prb_vecenv env = es[p];
+    if (env->kind != PRB_KIND_STOCK || r->N != N || r->H != H || env->N != N || env->market->K != K ||
+        !prb_fused_rollout_supported(r, as[p], env) || !stock_rollout_tc_supported(K) ||
+        !(env->cfg.max_trade_shares * (double)(env->end - env->start + 1) < 16777216.0))
+      return false;
+  }
+  return true;
+}
+
 void prb_tc_rollout_pods(const prb_rollout* rs, const prb_agent* as, const prb_vecenv* es, size_t P,
                          const uint64_t* seeds) {
   prb_ctx_s* ctx = rs[0]->ctx;

@@ -566,7 +566,8 @@ def ppo_update(agent: Agent, rollout: Rollout, cfg: PpoConfig, seed: int, perm: 
 
 def collect_pods(rollouts: Sequence["Rollout"], agents: Sequence[Agent], envs: Sequence["VectorizedEnvironment"],
                  seeds: Sequence[int]) -> None:
-    """worker_collect (pod.hpp:95-132) of every pod in ONE tcgen05 launch (per-pod weights)."""
+    """worker_collect (pod.hpp:95-132) of every pod in ONE tcgen05 launch (per-pod weights) when all
+    pods are stock VecEnvs of the tcgen05 shapes; other pods are collected one by one."""
     P = len(rollouts)
     rs = (C.c_void_p * P)(*[r.h for r in rollouts])
     ag = (C.c_void_p * P)(*[a.h for a in agents])

@@ -75,3 +75,21 @@ def test_pod_population_generation(pr, ctx, market):
         seqs = [tn.arrival_seq(g["generation"], p, P) for p in range(P)]
         assert g["board"] == tn.rank_candidates_host(s, seqs, 3)
     assert all(np.all(np.isfinite(a.flatten_params())) for a in pop.agents)
+
+
+def test_collect_pods_other_envs_fall_back(pr, ctx):
+    """prb_rollout_collect_pods with pods the grouped stock kernel does not take (PointMass): each
+    pod is collected on its own path, identical to prb_rollout_collect."""
+    agents = [pr.Agent.init(ctx, 6, 2, seed=30 + p, hidden=(64, 64)) for p in range(2)]
+    envs_a = [pr.VectorizedEnvironment.pointmass(ctx, 64) for _ in range(2)]
+    envs_b = [pr.VectorizedEnvironment.pointmass(ctx, 64) for _ in range(2)]
+    for p in range(2):
+        envs_a[p].reset(40 + p)
+        envs_b[p].reset(40 + p)
+    ro_a = [pr.Rollout.for_env(e, 16) for e in envs_a]
+    ro_b = [pr.Rollout.for_env(e, 16) for e in envs_b]
+    pr.collect_pods(ro_a, agents, envs_a, [50, 51])
+    for p in range(2):
+        ro_b[p].collect(agents[p], envs_b[p], seed=50 + p)
+        da, db = ro_a[p].download(), ro_b[p].download()
+        assert all(np.array_equal(da[k], db[k]) for k in ("states", "actions", "rewards", "dones"))
